@@ -1,0 +1,196 @@
+/*
+ * squint.h -- C ABI of libsquint, the B200 (sm_100a) hot path of Squint's visual SAC
+ * (arXiv 2602.21203).  Citations: P:n = PAPER.md line n, S:n = SPEC.md line n,
+ * Qn = reading n of SURVEY.md §8(c) (restated in DESIGN.md §3).
+ *
+ * Conventions for every entry point:
+ *  - Pointers are DEVICE pointers unless the comment says "host".
+ *  - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy default
+ *    stream).  No call synchronises, allocates or frees device memory: the caller
+ *    (PyTorch in the Python binding) owns all memory, including `workspace`.
+ *  - Calls on one stream serialise.  The library keeps no global state
+ *    except a thread-local error string and an optional per-thread graph cache.
+ *  - Errors are returned as squint_status; squint_last_error() gives the message.
+ *    Host-checkable conditions are checked before any launch (nothing is launched when
+ *    a check fails).  Device-side preconditions (index ranges, distinct slots) are
+ *    documented and are NOT checked (checking would need a synchronisation).
+ *  - Floating-point tensors are row-major fp32; images are u8 CHW planar (Q2).
+ */
+#ifndef SQUINT_H
+#define SQUINT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SQUINT_API __attribute__((visibility("default")))
+#else
+#define SQUINT_API
+#endif
+
+typedef struct CUstream_st* squint_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  SQUINT_OK = 0,
+  SQUINT_EINVAL = 1,       /* invalid argument value */
+  SQUINT_ESHAPE = 2,       /* inconsistent shapes */
+  SQUINT_ECUDA = 3,        /* a CUDA launch / runtime call failed */
+  SQUINT_ENCCL = 4,        /* an NCCL call failed */
+  SQUINT_EUNSUPPORTED = 5  /* shape/precision combination not built */
+} squint_status;
+
+enum { SQUINT_FP32 = 0, /* fp32 SIMT path (parity mode)                        */
+       SQUINT_BF16 = 1  /* bf16 operands, fp32 accumulate, fp32 master weights */ };
+
+/* Parameter groups.  CRITIC = encoder psi + critic projection + twin heads (the encoder
+ * is trained only by the critic loss); ACTOR = actor projection + MLP
+ * (P:157); ALPHA = log alpha; TARGET = EMA copy of the critic tensors except psi (Q28). */
+enum { SQUINT_GROUP_CRITIC = 0, SQUINT_GROUP_ACTOR = 1, SQUINT_GROUP_ALPHA = 2,
+       SQUINT_GROUP_TARGET = 3 };
+
+typedef struct {
+  char name[48];   /* e.g. "critic.q1.l2.w" */
+  int group;       /* SQUINT_GROUP_* */
+  int64_t offset;  /* in floats, into the group's flat buffer (128-byte aligned) */
+  int64_t numel;
+  int ndim;
+  int shape[4];    /* row-major; linear W is [out, in], conv W is [out, in, 3, 3] */
+} squint_tensor_desc;
+
+/* Problem shape, host struct.  Architecture per Q7-Q12:
+ * conv3x3/s2 -> ReLU -> conv3x3/s1 -> ReLU -> flatten (25*conv_ch) -> two projections
+ * Linear->latent->LN->tanh; actor MLP [z,s]->H->LN->ReLU->H->LN->ReLU->2A; twin critic
+ * heads [z,s,a]->H->LN->ReLU->H->LN->ReLU->n_atoms. */
+typedef struct {
+  int img_c, img_h, img_w;      /* 3, 16, 16 stored resolution          */
+  int pad;                      /* random-shift pad, 2 (Q5)                      */
+  int conv_ch;                  /* 32 | 64                                       */
+  int latent;                   /* 50                                            */
+  int proprio_dim, action_dim;  /* 12, 6                                         */
+  int critic_hidden, actor_hidden; /* 256 | 512, 256                             */
+  int n_atoms;                  /* 51 | 101                              */
+  float v_min, v_max;           /* atom support, v_min < v_max           */
+  int batch;                    /* per-rank batch B                              */
+  int precision;                /* SQUINT_FP32 | SQUINT_BF16                     */
+} squint_dims;
+
+typedef struct {
+  float gamma;          /* discount, 0 <= gamma <= 1                     */
+  float tau;            /* Polyak rate, 0 <= tau <= 1 (rho = 1 - tau) */
+  float lr_critic, lr_actor, lr_alpha;
+  float beta1, beta2, adam_eps;   /* Adam (Q26)                          */
+  float target_entropy; /* H_t, -A (Q15)                                  */
+  float ln_eps;         /* 1e-5 (Q9)                                      */
+  float log_std_min, log_std_max; /* -5, 2 (Q13)                          */
+} squint_hparams;
+
+/* Replay ring, structure of arrays, caller-owned. */
+typedef struct {
+  const uint8_t* obs;           /* [capacity, C, H, W] u8 */
+  const uint8_t* next_obs;      /* [capacity, C, H, W] u8 */
+  const float* proprio;         /* [capacity, P] */
+  const float* next_proprio;    /* [capacity, P] */
+  const float* action;          /* [capacity, A] in [-1, 1] */
+  const float* reward;          /* [capacity] */
+  const uint8_t* done;          /* [capacity], 1 = terminal (Q22) */
+  int64_t capacity, size;       /* sampled indices must be < size (not checked) */
+} squint_replay;
+
+/* Learner state: flat fp32 buffers laid out by squint_param_layout (caller-owned). */
+typedef struct {
+  float* critic;         /* group CRITIC params (master fp32)          */
+  float* critic_target;  /* group TARGET params                         */
+  float* actor;          /* group ACTOR params                          */
+  float* log_alpha;      /* [1]                                         */
+  float* m_critic; float* v_critic;   /* Adam moments, same layout */
+  float* m_actor;  float* v_actor;
+  float* m_alpha;  float* v_alpha;    /* [1] each */
+  int64_t* step;         /* [3] Adam step counters: critic, actor, alpha */
+} squint_state;
+
+/* ---- host-side layout queries (no GPU needed) ------------------------------------ */
+SQUINT_API const char* squint_last_error(void);
+SQUINT_API const char* squint_version(void);
+
+/* Fills `out[0..max_out)` (host, may be NULL) with every tensor of every group, sets
+ * *n_tensors, and group_sizes[4] (floats, padded) for CRITIC, ACTOR, ALPHA, TARGET.
+ * Errors: EINVAL on invalid dims (batch <= 0 ...). */
+SQUINT_API squint_status squint_param_layout(const squint_dims* dims, squint_tensor_desc* out, int max_out,
+                                  int* n_tensors, int64_t group_sizes[4]);
+
+/* Device workspace bytes needed by squint_update for `dims` (utd does not change it). */
+SQUINT_API squint_status squint_workspace_bytes(const squint_dims* dims, int utd, size_t* bytes);
+
+/* Offset/bytes of a named workspace region (debug/test access to intermediates):
+ * 0 = critic gradient (CRITIC layout), 1 = actor gradient (ACTOR layout),
+ * 2 = target distribution m [B, n_atoms], 3 = h [B, 25C], 4 = log pi (current) [B],
+ * 5 = log pi' (next) [B], 6 = actions a~ [B, A], 7 = scalars [16]. */
+SQUINT_API squint_status squint_workspace_region(const squint_dims* dims, int region, size_t* offset, size_t* bytes);
+
+/* Workspace bytes needed by squint_act for n frames. */
+SQUINT_API squint_status squint_act_workspace_bytes(const squint_dims* dims, int64_t n, size_t* bytes);
+
+/* ---- multi-GPU (data parallel) ------------------------------------ */
+/* Writes a 128-byte NCCL unique id to `id_out` (host).  Call on rank 0, broadcast the
+ * bytes with torch.distributed, then every rank calls squint_comm_init. */
+SQUINT_API squint_status squint_comm_unique_id(void* id_out);
+SQUINT_API squint_status squint_comm_init(void** comm, const void* id /* host, 128 B */, int rank, int nranks);
+SQUINT_API squint_status squint_comm_destroy(void* comm);
+
+/* ---- a1: resolution squint + insert (Q1, Q4) ------------
+ * frames u8 [n, c, h, w]; ring u8 [capacity, c, h/factor, w/factor];
+ * ring[slots[f]][ch][i][j] = round_half_even(sum_{a,b<factor} frames[f][ch][factor*i+a][factor*j+b] / factor^2).
+ * Preconditions (device, unchecked): 0 <= slots[f] < capacity, slots distinct.
+ * Errors: ESHAPE if h or w is not divisible by factor; EINVAL if n < 0,
+ * factor < 1, capacity < 1, or (w % 16) != 0 when factor == 8 (vector path).
+ * n == 0 is a no-op. */
+SQUINT_API squint_status squint_insert(const uint8_t* frames, int64_t n, int c, int h, int w, int factor,
+                            const int64_t* slots, uint8_t* ring, int64_t capacity,
+                            squint_stream_t stream);
+
+/* ---- a16: batched rollout inference (Algorithm 1 L4-5) -------------------
+ * frames u8 [n, img_c, frame_h, frame_w] with frame_h = img_h * f, frame_w = img_w * f
+ * (f >= 1; f = 1 means already squinted); proprio [n, P]; eps [n, A] N(0,1) noise or
+ * NULL for the mean action tanh(mu) (log pi then evaluated at eps = 0).
+ * Outputs action_out [n, A], logp_out [n] (may be NULL).  If `ring`/`slots` are non-NULL
+ * the squinted frames are also written to ring[slots[i]] (fused insert, Q4).
+ * actor_params / critic_params are the ACTOR / CRITIC flat buffers (the encoder psi is
+ * read from the head of CRITIC).  workspace >= squint_act_workspace_bytes.
+ * n == 0 is a no-op. */
+SQUINT_API squint_status squint_act(const squint_dims* dims, const squint_hparams* hp, const float* actor_params,
+                         const float* critic_params, const uint8_t* frames, int64_t n, int frame_h,
+                         int frame_w, const float* proprio, const float* eps, float* action_out,
+                         float* logp_out, uint8_t* ring, const int64_t* slots, int64_t ring_capacity,
+                         void* workspace, squint_stream_t stream);
+
+/* ---- a2-a15: `utd` sequential SAC updates (Algorithm 1 L8-24; Q17-Q30) -------------
+ * idx [utd, B] int64 in [0, replay->size) (device, unchecked);
+ * shifts [utd, B, 4] u8 = (dx, dy) for obs then (dx', dy') for next_obs, each in
+ * [0, 2*pad] (Q5); eps [utd, 2, B, A] fp32 N(0,1): [:,0] next-state sample (target),
+ * [:,1] current-state sample (alpha and actor losses) (Q18, Q32).
+ * state is read and updated in place.  metrics [utd, 8] (device) receives, per update,
+ * {L_Q, L_pi, L_alpha, alpha+, mean Q, entropy (-mean log pi), |grad critic|_2, nonfinite}.
+ * A non-finite loss sets metrics[j][7] = 1 and the update continues.
+ * comm: NULL for one GPU, else a handle from squint_comm_init; then B is the per-rank
+ * batch, losses are scaled by 1/(B*nranks) and gradients/metric sums are SUM
+ * all-reduced over ranks (Q33).
+ * Errors: EINVAL (utd < 1, batch < 1, gamma/tau outside [0,1], size < 1, bad support),
+ * ESHAPE (dims inconsistent), EUNSUPPORTED (shape/precision not built). */
+SQUINT_API squint_status squint_update(const squint_dims* dims, const squint_hparams* hp, const squint_replay* replay,
+                            const int64_t* idx, const uint8_t* shifts, const float* eps, int utd,
+                            const squint_state* state, float* metrics, void* workspace, size_t workspace_bytes,
+                            void* comm, squint_stream_t stream);
+
+/* ---- a14: standalone Polyak: target[i] = (1 - tau) target[i] + tau online[i].
+ * Errors: EINVAL if n < 0 or tau outside [0, 1]. */
+SQUINT_API squint_status squint_soft_update(float* target, const float* online, int64_t n, float tau,
+                                 squint_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SQUINT_H */

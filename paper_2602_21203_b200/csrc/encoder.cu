@@ -1,0 +1,388 @@
+// encoder.cu -- image kernels of the update and of rollout inference (fp32 SIMT).
+//
+//  a1  squint: integer 8x8 block sums of u8 frames (16-byte vector loads, byte sums with
+//      dp4a), round-half-to-even divide (Q1), scatter into the replay ring.
+//  a3-a5  replay gather + random shift (replicate pad, Q5) + conv 3x3/s2 + ReLU + conv 3x3/s1
+//      + ReLU (Q7), for obs and next_obs in one launch (both encoded with psi).
+//  a10 encoder backward: conv2 dX (masked by ReLU'), conv2/conv1 weight gradients as
+//      fixed-order per-chunk partials + a fixed-order reduction (bitwise reproducible).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "encoder.cuh"
+
+namespace sq {
+
+namespace {
+
+SQ_DEV uint32_t rhe_div(uint32_t s, uint32_t n) {
+  uint32_t q = s / n, r = s - q * n;
+  if (2 * r > n || (2 * r == n && (q & 1u))) ++q;
+  return q;
+}
+
+// Byte sums of a 16-byte vector: bytes 0-7 and 8-15.
+SQ_DEV void sum16(const uint4 v, uint32_t& lo, uint32_t& hi) {
+  lo = __dp4a(v.x, 0x01010101u, __dp4a(v.y, 0x01010101u, lo));
+  hi = __dp4a(v.z, 0x01010101u, __dp4a(v.w, 0x01010101u, hi));
+}
+
+// ---- a1 standalone insert ---------------------------------------------------------
+// factor 8, frame width a multiple of 16: one thread = 2 output pixels (one 16-byte
+// column chunk over 8 rows).
+__global__ void __launch_bounds__(256) k_insert_f8(const uint8_t* __restrict__ frames, int64_t n, int c, int h,
+                                                   int w, const int64_t* __restrict__ slots,
+                                                   uint8_t* __restrict__ ring) {
+  const int ho = h / 8, wo = w / 8, chunks = w / 16;
+  const int64_t items = n * c * ho * chunks;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int ch = (int)(it % chunks);
+    int64_t t = it / chunks;
+    const int oy = (int)(t % ho);
+    t /= ho;
+    const int cc = (int)(t % c);
+    const int64_t f = t / c;
+    const uint8_t* src = frames + ((f * c + cc) * (int64_t)h + oy * 8) * w + ch * 16;
+    uint4 v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = __ldcs(reinterpret_cast<const uint4*>(src + (int64_t)r * w));
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) sum16(v[r], lo, hi);
+    const uint32_t q0 = (lo + 31u + ((lo >> 6) & 1u)) >> 6;  // RHE(lo / 64)
+    const uint32_t q1 = (hi + 31u + ((hi >> 6) & 1u)) >> 6;
+    uint8_t* dst = ring + (slots[f] * c + cc) * (int64_t)(ho * wo) + oy * wo + ch * 2;
+    *reinterpret_cast<uint16_t*>(dst) = (uint16_t)(q0 | (q1 << 8));
+  }
+}
+
+// generic factor: one thread per output pixel
+__global__ void k_insert_generic(const uint8_t* __restrict__ frames, int64_t n, int c, int h, int w, int f,
+                                 const int64_t* __restrict__ slots, uint8_t* __restrict__ ring) {
+  const int ho = h / f, wo = w / f;
+  const int64_t items = n * c * ho * wo;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int ox = (int)(it % wo);
+    int64_t t = it / wo;
+    const int oy = (int)(t % ho);
+    t /= ho;
+    const int cc = (int)(t % c);
+    const int64_t fr = t / c;
+    const uint8_t* src = frames + ((fr * c + cc) * (int64_t)h + oy * f) * w + ox * f;
+    uint32_t s = 0;
+    for (int a = 0; a < f; ++a)
+      for (int b = 0; b < f; ++b) s += src[(int64_t)a * w + b];
+    ring[(slots[fr] * c + cc) * (int64_t)(ho * wo) + oy * wo + ox] = (uint8_t)rhe_div(s, (uint32_t)(f * f));
+  }
+}
+
+// ---- a3-a5 / a16 encoder forward ----------------------------------------------------
+__global__ void __launch_bounds__(256) k_enc_fwd(const __grid_constant__ EncFwdArgs a, int ipb) {
+  extern __shared__ float sm[];
+  const int C = a.C, ci = a.c_in, H = a.H, H1 = (H - 3) / 2 + 1, P1 = H1 * H1, H2 = H1 - 2, P2 = H2 * H2;
+  const int HH = H * H;
+  float* w1t = sm;                        // [9*ci][C+1]
+  float* w2t = w1t + 9 * ci * (C + 1);    // [9*C][C+1]
+  float* xs = w2t + 9 * C * (C + 1);      // [ipb][ci][HH]
+  float* y1s = xs + ipb * ci * HH;        // [ipb][C][P1]
+  const int tid = threadIdx.x;
+  const int src_i = blockIdx.y;
+  const int b0 = blockIdx.x * ipb;
+
+  for (int e = tid; e < C * 9 * ci; e += 256) {  // global [o][c][kk] -> [c*9+kk][o]
+    const int o = e / (9 * ci), r = e % (9 * ci);
+    w1t[r * (C + 1) + o] = a.w1[e];
+  }
+  for (int e = tid; e < C * 9 * C; e += 256) {
+    const int o = e / (9 * C), r = e % (9 * C);
+    w2t[r * (C + 1) + o] = a.w2[e];
+  }
+  const float inv255 = 1.0f / 255.0f;
+  if (a.mode == 0) {
+    const uint8_t* src = a.src[src_i];
+    for (int e = tid; e < ipb * ci * HH; e += 256) {
+      const int i = e / (ci * HH), r = e % (ci * HH), cc = r / HH, p = r % HH, y = p / H, x = p % H;
+      const int b = b0 + i;
+      float v = 0.f;
+      if (b < a.B) {
+        const int64_t row = a.idx[b];
+        const int dx = a.shifts[b * 4 + 2 * src_i], dy = a.shifts[b * 4 + 2 * src_i + 1];
+        const int sy = min(max(y + dy - a.pad, 0), H - 1), sx = min(max(x + dx - a.pad, 0), H - 1);
+        const uint8_t u = src[row * (ci * HH) + cc * HH + sy * H + sx];
+        if (src_i == 0 && a.img0) a.img0[(int64_t)b * ci * HH + r] = u;
+        v = (float)u * inv255;
+      }
+      xs[e] = v;
+    }
+  } else {
+    // squint: factor-f block sums of raw frames, RHE; optional ring write.
+    const int f = a.factor, W = H * f;
+    const uint8_t* frames = a.src[0];
+    if (f == 8 && (W % 16) == 0) {
+      const int chunks = W / 16;  // 2 output pixels per chunk
+      for (int e = tid; e < ipb * ci * H * chunks; e += 256) {
+        const int ch = e % chunks, t1 = e / chunks, oy = t1 % H, t2 = t1 / H, cc = t2 % ci, i = t2 / ci;
+        const int b = b0 + i;
+        uint32_t lo = 0, hi = 0;
+        if (b < a.B) {
+          const uint8_t* src = frames + (((int64_t)b * ci + cc) * W + oy * 8) * W + ch * 16;
+          uint4 v[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) v[r] = __ldcs(reinterpret_cast<const uint4*>(src + (int64_t)r * W));
+#pragma unroll
+          for (int r = 0; r < 8; ++r) sum16(v[r], lo, hi);
+        }
+        const uint32_t q0 = (lo + 31u + ((lo >> 6) & 1u)) >> 6, q1 = (hi + 31u + ((hi >> 6) & 1u)) >> 6;
+        xs[(i * ci + cc) * HH + oy * H + 2 * ch] = (float)q0 * inv255;
+        xs[(i * ci + cc) * HH + oy * H + 2 * ch + 1] = (float)q1 * inv255;
+        if (b < a.B && a.ring)
+          *reinterpret_cast<uint16_t*>(a.ring + (a.slots[b] * ci + cc) * (int64_t)HH + oy * H + 2 * ch) =
+              (uint16_t)(q0 | (q1 << 8));
+      }
+    } else {
+      for (int e = tid; e < ipb * ci * HH; e += 256) {
+        const int i = e / (ci * HH), r = e % (ci * HH), cc = r / HH, p = r % HH, oy = p / H, ox = p % H;
+        const int b = b0 + i;
+        uint32_t q = 0;
+        if (b < a.B) {
+          const uint8_t* src = frames + (((int64_t)b * ci + cc) * W + oy * f) * W + ox * f;
+          uint32_t s = 0;
+          for (int u = 0; u < f; ++u)
+            for (int v = 0; v < f; ++v) s += src[(int64_t)u * W + v];
+          q = rhe_div(s, (uint32_t)(f * f));
+          if (a.ring) a.ring[(a.slots[b] * ci + cc) * (int64_t)HH + p] = (uint8_t)q;
+        }
+        xs[e] = (float)q * inv255;
+      }
+    }
+  }
+  __syncthreads();
+
+  // conv1: 3x3 stride 2 valid + ReLU.  thread: o = tid % C, positions strided by 256 / C.
+  const int o = tid % C, grp = tid / C, ngrp = 256 / C;
+  for (int p = grp; p < ipb * P1; p += ngrp) {
+    const int i = p / P1, pix = p % P1, y = pix / H1, x = pix % H1;
+    float acc = a.b1[o];
+    for (int cc = 0; cc < ci; ++cc) {
+      const float* xi = xs + (i * ci + cc) * HH + (2 * y) * H + 2 * x;
+#pragma unroll
+      for (int ki = 0; ki < 3; ++ki)
+#pragma unroll
+        for (int kj = 0; kj < 3; ++kj) acc = fmaf(w1t[(cc * 9 + ki * 3 + kj) * (C + 1) + o], xi[ki * H + kj], acc);
+    }
+    const float v = fmaxf(acc, 0.f);
+    y1s[(i * C + o) * P1 + pix] = v;
+    const int b = b0 + i;
+    if (src_i == 0 && a.y1 && b < a.B) a.y1[((int64_t)b * C + o) * P1 + pix] = v;
+  }
+  __syncthreads();
+  // conv2: 3x3 stride 1 valid + ReLU -> h[b][o*P2 + pix] (CHW flatten)
+  float* hout = a.h[src_i];
+  for (int p = grp; p < ipb * P2; p += ngrp) {
+    const int i = p / P2, pix = p % P2, y = pix / H2, x = pix % H2;
+    const int b = b0 + i;
+    float acc = a.b2[o];
+    for (int cc = 0; cc < C; ++cc) {
+      const float* yi = y1s + (i * C + cc) * P1 + y * H1 + x;
+#pragma unroll
+      for (int ki = 0; ki < 3; ++ki)
+#pragma unroll
+        for (int kj = 0; kj < 3; ++kj) acc = fmaf(w2t[(cc * 9 + ki * 3 + kj) * (C + 1) + o], yi[ki * H1 + kj], acc);
+    }
+    if (b < a.B) hout[(int64_t)b * C * P2 + o * P2 + pix] = fmaxf(acc, 0.f);
+  }
+}
+
+// ---- a10 encoder backward -----------------------------------------------------------
+// dA1[b][c][pix] = ReLU'(y1) * sum_{o,ki,kj} dA2[b][o][y-ki][x-kj] W2[o][c][ki][kj]
+__global__ void __launch_bounds__(256) k_enc_bwd_dx(const __grid_constant__ EncBwdArgs a, int ipb) {
+  extern __shared__ float sm[];
+  const int C = a.C, H = a.H, H1 = (H - 3) / 2 + 1, P1 = H1 * H1, H2 = H1 - 2, P2 = H2 * H2;
+  float* w2s = sm;               // [o][c][9]
+  float* ds = w2s + C * C * 9;   // [ipb][C][P2]
+  const int tid = threadIdx.x, b0 = blockIdx.x * ipb;
+  for (int e = tid; e < C * C * 9; e += 256) w2s[e] = a.w2[e];
+  for (int e = tid; e < ipb * C * P2; e += 256) {
+    const int i = e / (C * P2), b = b0 + i;
+    ds[e] = (b < a.B) ? a.dA2[(int64_t)b * C * P2 + e % (C * P2)] : 0.f;
+  }
+  __syncthreads();
+  const int c = tid % C, grp = tid / C, ngrp = 256 / C;
+  for (int p = grp; p < ipb * P1; p += ngrp) {
+    const int i = p / P1, pix = p % P1, y = pix / H1, x = pix % H1, b = b0 + i;
+    if (b >= a.B) continue;
+    float acc = 0.f;
+    for (int o = 0; o < C; ++o) {
+      const float* wo = w2s + (o * C + c) * 9;
+      const float* d = ds + (i * C + o) * P2;
+#pragma unroll
+      for (int ki = 0; ki < 3; ++ki) {
+        const int yy = y - ki;
+        if (yy < 0 || yy >= H2) continue;
+#pragma unroll
+        for (int kj = 0; kj < 3; ++kj) {
+          const int xx = x - kj;
+          if (xx < 0 || xx >= H2) continue;
+          acc = fmaf(d[yy * H2 + xx], wo[ki * 3 + kj], acc);
+        }
+      }
+    }
+    const int64_t gi = ((int64_t)b * C + c) * P1 + pix;
+    a.dA1[gi] = a.y1[gi] > 0.f ? acc : 0.f;
+  }
+}
+
+// Partial weight gradient of a 3x3 conv over a chunk of images:
+//   dW[o][c][ki][kj] = sum_b sum_pix D[b][o][pix] X[b][c][s*y+ki][s*x+kj],  db[o] = sum D.
+// grid = (nchunk, O / OB); each thread owns up to 40 weights (fixed summation order).
+template <bool kU8>
+__global__ void __launch_bounds__(256) k_conv_dw(const float* __restrict__ D, const void* __restrict__ Xv, int B,
+                                                 int O, int Cin, int Hin, int Hout, int stride, int OB,
+                                                 int nchunk, float* __restrict__ part) {
+  extern __shared__ float sm[];
+  const int Pout = Hout * Hout, HH = Hin * Hin;
+  float* Ds = sm;               // [OB][Pout]
+  float* Xs = Ds + OB * Pout;   // [Cin][HH]
+  const int tid = threadIdx.x;
+  const int chunk = blockIdx.x, o0 = blockIdx.y * OB;
+  const int per = (B + nchunk - 1) / nchunk, bb0 = chunk * per, bb1 = min(B, bb0 + per);
+  const int nw = OB * Cin * 9;
+  constexpr int R = 40;
+  float acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = 0.f;
+  float sb = 0.f;
+  for (int b = bb0; b < bb1; ++b) {
+    for (int e = tid; e < OB * Pout; e += 256) Ds[e] = D[((int64_t)b * O + o0) * Pout + e];
+    for (int e = tid; e < Cin * HH; e += 256) {
+      if (kU8)
+        Xs[e] = (float)(reinterpret_cast<const uint8_t*>(Xv)[(int64_t)b * Cin * HH + e]) * (1.0f / 255.0f);
+      else
+        Xs[e] = reinterpret_cast<const float*>(Xv)[(int64_t)b * Cin * HH + e];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int w = tid + 256 * r;
+      if (w >= nw) break;
+      const int ol = w / (Cin * 9), c = (w / 9) % Cin, kk = w % 9, ki = kk / 3, kj = kk % 3;
+      const float* d = Ds + ol * Pout;
+      const float* x = Xs + c * HH + ki * Hin + kj;
+      float s = 0.f;
+      for (int y = 0; y < Hout; ++y)
+        for (int xx = 0; xx < Hout; ++xx) s = fmaf(d[y * Hout + xx], x[stride * y * Hin + stride * xx], s);
+      acc[r] += s;
+    }
+    if (tid < OB) {
+      float s = 0.f;
+      for (int p = 0; p < Pout; ++p) s += Ds[tid * Pout + p];
+      sb += s;
+    }
+    __syncthreads();
+  }
+  const int stride_part = O * Cin * 9 + O;
+  float* pp = part + (int64_t)chunk * stride_part;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int w = tid + 256 * r;
+    if (w >= nw) break;
+    pp[o0 * Cin * 9 + w] = acc[r];
+  }
+  if (tid < OB) pp[O * Cin * 9 + o0 + tid] = sb;
+}
+
+// out_w[i] = sum_chunk part[chunk][i] (i < nw), out_b[i] likewise for biases.
+__global__ void k_reduce_part(const float* __restrict__ part, int nchunk, int nw, int nb, float* __restrict__ out_w,
+                              float* __restrict__ out_b) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int stride = nw + nb;
+  if (i >= stride) return;
+  float s = 0.f;
+  for (int c = 0; c < nchunk; ++c) s += part[(int64_t)c * stride + i];
+  if (i < nw)
+    out_w[i] = s;
+  else
+    out_b[i - nw] = s;
+}
+
+int fwd_ipb(int C) { return C <= 32 ? 4 : 2; }
+size_t fwd_smem(int C, int ci, int H, int ipb) {
+  const int H1 = (H - 3) / 2 + 1;
+  return sizeof(float) * (size_t)(9 * ci * (C + 1) + 9 * C * (C + 1) + ipb * ci * H * H + ipb * C * H1 * H1);
+}
+int bwd_ipb(int C) { return C <= 32 ? 8 : 4; }
+int ob_of(int O, int Cin) {  // output-channel block so a thread owns <= 40 weights
+  int ob = O;
+  while (ob > 1 && (ob * Cin * 9 + 255) / 256 > 40) ob /= 2;
+  return ob;
+}
+
+}  // namespace
+
+int enc_bwd_nchunk(int B) { return B < 128 ? B : 128; }
+size_t enc_bwd_partial_floats(int C, int c_in, int nchunk) {
+  return (size_t)nchunk * (C * C * 9 + C) + (size_t)nchunk * (C * c_in * 9 + C);
+}
+
+int launch_enc_fwd(const EncFwdArgs& a, cudaStream_t s) {
+  if (a.B == 0) return 0;
+  const int ipb = fwd_ipb(a.C);
+  const size_t smem = fwd_smem(a.C, a.c_in, a.H, ipb);
+  cudaFuncSetAttribute(k_enc_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((a.B + ipb - 1) / ipb, a.nsrc);
+  k_enc_fwd<<<grid, 256, smem, s>>>(a, ipb);
+  return (int)cudaGetLastError();
+}
+
+int launch_enc_bwd(const EncBwdArgs& a, cudaStream_t s) {
+  const int C = a.C, H1 = (a.H - 3) / 2 + 1, P1 = H1 * H1, H2 = H1 - 2, P2 = H2 * H2;
+  {
+    const int ipb = bwd_ipb(C);
+    const size_t smem = sizeof(float) * (size_t)(C * C * 9 + ipb * C * P2);
+    cudaFuncSetAttribute(k_enc_bwd_dx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_enc_bwd_dx<<<(a.B + ipb - 1) / ipb, 256, smem, s>>>(a, ipb);
+  }
+  float* part2 = a.part;
+  float* part1 = a.part + (size_t)a.nchunk * (C * C * 9 + C);
+  {
+    const int ob = ob_of(C, C);
+    const size_t smem = sizeof(float) * (size_t)(ob * P2 + C * P1);
+    cudaFuncSetAttribute(k_conv_dw<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_conv_dw<false><<<dim3(a.nchunk, C / ob), 256, smem, s>>>(a.dA2, a.y1, a.B, C, C, H1, H2, 1, ob, a.nchunk,
+                                                                 part2);
+  }
+  {
+    const int ob = ob_of(C, a.c_in);
+    const size_t smem = sizeof(float) * (size_t)(ob * P1 + a.c_in * a.H * a.H);
+    cudaFuncSetAttribute(k_conv_dw<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_conv_dw<true><<<dim3(a.nchunk, C / ob), 256, smem, s>>>(a.dA1, a.img, a.B, C, a.c_in, a.H, H1, 2, ob,
+                                                               a.nchunk, part1);
+  }
+  {
+    const int n2 = C * C * 9 + C, n1 = C * a.c_in * 9 + C;
+    k_reduce_part<<<(n2 + 255) / 256, 256, 0, s>>>(part2, a.nchunk, C * C * 9, C, a.gw2, a.gb2);
+    k_reduce_part<<<(n1 + 255) / 256, 256, 0, s>>>(part1, a.nchunk, C * a.c_in * 9, C, a.gw1, a.gb1);
+  }
+  return (int)cudaGetLastError();
+}
+
+int launch_insert(const uint8_t* frames, int64_t n, int c, int h, int w, int factor, const int64_t* slots,
+                  uint8_t* ring, cudaStream_t s) {
+  if (n == 0) return 0;
+  if (factor == 8 && (w % 16) == 0) {
+    const int64_t items = n * c * (h / 8) * (w / 16);
+    int64_t blocks = (items + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_insert_f8<<<(unsigned)blocks, 256, 0, s>>>(frames, n, c, h, w, slots, ring);
+  } else {
+    const int64_t items = n * c * (h / factor) * (w / factor);
+    int64_t blocks = (items + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_insert_generic<<<(unsigned)blocks, 256, 0, s>>>(frames, n, c, h, w, factor, slots, ring);
+  }
+  return (int)cudaGetLastError();
+}
+
+}  // namespace sq

@@ -1,0 +1,48 @@
+// encoder.cuh -- launch interfaces for the image kernels: squint insert (a1), replay
+// gather + random shift + conv encoder forward (a3-a5), encoder backward (a10), and the
+// fused squint + encoder of rollout inference (a16).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sq {
+
+struct EncFwdArgs {
+  // source mode 0: replay gather + shift (update); mode 1: raw frames + squint (act)
+  int mode;
+  const uint8_t* src[2];   // mode 0: ring obs / next_obs [cap, c, H, W]; mode 1: frames [n, c, fH, fW]
+  const int64_t* idx;      // mode 0: [B]
+  const uint8_t* shifts;   // mode 0: [B, 4]
+  int factor;              // mode 1: squint factor (frame = H * factor)
+  uint8_t* ring;           // mode 1, optional: write squinted frames to ring[slots[i]]
+  const int64_t* slots;
+  int B;                   // images per source
+  int nsrc;                // mode 0: 2 (obs, next_obs); mode 1: 1
+  const float* w1; const float* b1; const float* w2; const float* b2;
+  float* h[2];             // [B, F] outputs per source
+  float* y1;               // [B, C, P1] conv1 activations of source 0 (NULL: not stored)
+  uint8_t* img0;           // [B, c, H, W] shifted images of source 0 (NULL: not stored)
+  int C, c_in, H, pad;
+};
+
+struct EncBwdArgs {
+  int B, C, c_in, H;
+  const float* dA2;        // [B, F]  dL/d(conv2 pre-activation)
+  const float* y1;         // [B, C, P1]
+  const uint8_t* img;      // [B, c, H, W]
+  const float* w2;         // conv2 weights [C, C, 3, 3]
+  float* dA1;              // [B, C, P1] workspace
+  float* part;             // partial weight grads [nchunk][C*C*9 + C + C*c*9 + C]
+  int nchunk;
+  float* gw1; float* gb1; float* gw2; float* gb2;  // final grads (CRITIC layout)
+};
+
+int launch_enc_fwd(const EncFwdArgs& a, cudaStream_t s);
+int launch_enc_bwd(const EncBwdArgs& a, cudaStream_t s);
+size_t enc_bwd_partial_floats(int C, int c_in, int nchunk);
+int enc_bwd_nchunk(int B);
+
+int launch_insert(const uint8_t* frames, int64_t n, int c, int h, int w, int factor, const int64_t* slots,
+                  uint8_t* ring, cudaStream_t s);
+
+}  // namespace sq

@@ -1,0 +1,37 @@
+// heads.cuh -- row kernels of the distributional critic (a9, a10, a12).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sq {
+
+struct TargetCEArgs {
+  int B, N;
+  float v_min, v_max, gamma, scale;
+  const float* tlogits;    // [2][B][N] target heads (theta_bar) on (z', s', a')
+  const float* logits;     // [2][B][N] online heads on (z, s, a)
+  const int64_t* idx;      // [B] replay rows
+  const float* reward;     // ring [cap]
+  const uint8_t* done;     // ring [cap]
+  const float* logp_next;  // [B]
+  const float* log_alpha;  // [1] (alpha_0 = exp, read before the alpha step)
+  float* m;                // [B][N]
+  float* dlogits;          // [2][B][N]
+  float* row_loss;         // [B]
+};
+
+struct ActorQArgs {
+  int B, N;
+  float v_min, v_max, scale;
+  const float* logits;     // [2][B][N] critic theta+ on (z+, s, a~)
+  const float* logp;       // [B]
+  const float* alpha1;     // [1] alpha after its step
+  float* dlogits;          // [2][B][N]
+  float* row_q;            // [B]
+  float* row_lpi;          // [B]
+};
+
+int launch_target_ce(const TargetCEArgs& a, cudaStream_t s);
+int launch_actor_q(const ActorQArgs& a, cudaStream_t s);
+
+}  // namespace sq

@@ -1,0 +1,215 @@
+// optim.cu -- temperature step (Algorithm 1 L17 with the sign of Q17), fused Adam (Q26),
+// Polyak (Algorithm 1 L24, Q28) and the per-update metrics row.  All reductions are fixed
+// order so results are bitwise reproducible and identical across data-parallel replicas.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "optim.cuh"
+
+namespace sq {
+
+namespace {
+
+__global__ void __launch_bounds__(256) k_row_sums(const float* __restrict__ logp, const float* __restrict__ row_loss,
+                                                  int B, float* __restrict__ extras) {
+  __shared__ float red[32];
+  float a = 0.f, b = 0.f;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) {
+    a += logp[i];
+    b += row_loss[i];
+  }
+  a = block_sum(a, red);
+  b = block_sum(b, red);
+  if (threadIdx.x == 0) {
+    extras[X_SUM_LOGP] = a;
+    extras[X_SUM_LQ] = b;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_scalars(const __grid_constant__ ScalarsArgs a) {
+  __shared__ float red[32];
+  float sl = 0.f, sq = 0.f;
+  if (a.compute_sums) {
+    for (int i = threadIdx.x; i < a.B; i += blockDim.x) {
+      sl += a.logp[i];
+      sq += a.row_loss[i];
+    }
+    sl = block_sum(sl, red);
+    sq = block_sum(sq, red);
+  }
+  if (threadIdx.x != 0) return;
+  if (a.compute_sums) {
+    a.extras[X_SUM_LOGP] = sl;
+    a.extras[X_SUM_LQ] = sq;
+  } else {
+    sl = a.extras[X_SUM_LOGP];
+    sq = a.extras[X_SUM_LQ];
+  }
+  const float mean_logp = sl * a.inv_btotal;
+  const float la = a.log_alpha[0];
+  const float alpha0 = expf(la);
+  const float loss = -alpha0 * (mean_logp + a.target_entropy);
+  const float g = loss;  // d/dlog_alpha of -exp(log_alpha) (...)
+  const int64_t t = ++a.step[2];
+  const float m = a.beta1 * a.m_alpha[0] + (1.f - a.beta1) * g;
+  const float v = a.beta2 * a.v_alpha[0] + (1.f - a.beta2) * g * g;
+  const float c1 = (float)(1.0 / (1.0 - pow((double)a.beta1, (double)t)));
+  const float c2 = (float)(1.0 / (1.0 - pow((double)a.beta2, (double)t)));
+  const float la1 = la - a.lr_alpha * (m * c1) / (sqrtf(v * c2) + a.adam_eps);
+  a.m_alpha[0] = m;
+  a.v_alpha[0] = v;
+  a.log_alpha[0] = la1;
+  const float alpha1 = expf(la1);
+  a.scal[S_ALPHA1] = alpha1;
+  a.scal[S_ALPHA1_SCALE] = alpha1 * a.loss_scale;
+  a.scal[S_MEAN_LOGP] = mean_logp;
+  a.scal[S_LALPHA] = loss;
+  a.scal[S_LQ] = sq;
+  const int64_t tc = ++a.step[0], ta = ++a.step[1];
+  a.scal[S_C1_CRITIC] = (float)(1.0 / (1.0 - pow((double)a.beta1, (double)tc)));
+  a.scal[S_C2_CRITIC] = (float)(1.0 / (1.0 - pow((double)a.beta2, (double)tc)));
+  a.scal[S_C1_ACTOR] = (float)(1.0 / (1.0 - pow((double)a.beta1, (double)ta)));
+  a.scal[S_C2_ACTOR] = (float)(1.0 / (1.0 - pow((double)a.beta2, (double)ta)));
+}
+
+__global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, const float4* __restrict__ g,
+                                              float4* __restrict__ m, float4* __restrict__ v, int64_t n4, float lr,
+                                              float b1, float b2, float eps, const float* __restrict__ c1p,
+                                              const float* __restrict__ c2p, float* __restrict__ part) {
+  __shared__ float red[32];
+  const float c1 = c1p[0], c2 = c2p[0];
+  float ss = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 gg = g[i], mm = m[i], vv = v[i], pp = p[i];
+    float* gf = reinterpret_cast<float*>(&gg);
+    float* mf = reinterpret_cast<float*>(&mm);
+    float* vf = reinterpret_cast<float*>(&vv);
+    float* pf = reinterpret_cast<float*>(&pp);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      ss = fmaf(gf[k], gf[k], ss);
+      mf[k] = b1 * mf[k] + (1.f - b1) * gf[k];
+      vf[k] = b2 * vf[k] + (1.f - b2) * gf[k] * gf[k];
+      pf[k] = pf[k] - lr * (mf[k] * c1) / (sqrtf(vf[k] * c2) + eps);
+    }
+    m[i] = mm;
+    v[i] = vv;
+    p[i] = pp;
+  }
+  if (part) {
+    ss = block_sum(ss, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = ss;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_polyak(float* __restrict__ t, const float* __restrict__ o, int64_t n,
+                                                float tau) {
+  const float keep = 1.f - tau;
+  const bool vec = ((reinterpret_cast<uintptr_t>(t) | reinterpret_cast<uintptr_t>(o)) & 15) == 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (vec) {
+    const int64_t n4 = n / 4;
+    float4* t4 = reinterpret_cast<float4*>(t);
+    const float4* o4 = reinterpret_cast<const float4*>(o);
+    for (int64_t i = i0; i < n4; i += stride) {
+      float4 a = t4[i];
+      const float4 b = o4[i];
+      a.x = keep * a.x + tau * b.x;
+      a.y = keep * a.y + tau * b.y;
+      a.z = keep * a.z + tau * b.z;
+      a.w = keep * a.w + tau * b.w;
+      t4[i] = a;
+    }
+    for (int64_t i = n4 * 4 + i0; i < n; i += stride) t[i] = keep * t[i] + tau * o[i];
+  } else {
+    for (int64_t i = i0; i < n; i += stride) t[i] = keep * t[i] + tau * o[i];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_lpi_sums(const float* __restrict__ row_lpi, const float* __restrict__ row_q,
+                                                  int B, float* __restrict__ out2) {
+  __shared__ float red[32];
+  float a = 0.f, b = 0.f;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) {
+    a += row_lpi[i];
+    b += row_q[i];
+  }
+  a = block_sum(a, red);
+  b = block_sum(b, red);
+  if (threadIdx.x == 0) {
+    out2[0] = a;
+    out2[1] = b;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_metrics(const __grid_constant__ MetricsArgs a) {
+  __shared__ float red[32];
+  float lpi = 0.f, q = 0.f, gs = 0.f;
+  if (a.reduce_local) {
+    for (int i = threadIdx.x; i < a.B; i += blockDim.x) {
+      lpi += a.row_lpi[i];
+      q += a.row_q[i];
+    }
+    lpi = block_sum(lpi, red);
+    q = block_sum(q, red);
+  } else {
+    lpi = a.extras2[0];
+    q = a.extras2[1];
+  }
+  for (int i = threadIdx.x; i < kAdamBlocks; i += blockDim.x) gs += a.sumsq_part[i];
+  gs = block_sum(gs, red);
+  if (threadIdx.x == 0) {
+    const float LQ = a.scal[S_LQ], La = a.scal[S_LALPHA];
+    float* o = a.out;
+    o[0] = LQ;
+    o[1] = lpi;
+    o[2] = La;
+    o[3] = a.scal[S_ALPHA1];
+    o[4] = q * a.inv_btotal;
+    o[5] = -a.scal[S_MEAN_LOGP];
+    o[6] = sqrtf(gs);
+    o[7] = (isfinite(LQ) && isfinite(lpi) && isfinite(La)) ? 0.f : 1.f;
+  }
+}
+
+}  // namespace
+
+int launch_row_sums(const float* logp, const float* row_loss, int B, float* extras, cudaStream_t s) {
+  k_row_sums<<<1, 256, 0, s>>>(logp, row_loss, B, extras);
+  return (int)cudaGetLastError();
+}
+
+int launch_scalars(const ScalarsArgs& a, cudaStream_t s) {
+  k_scalars<<<1, 256, 0, s>>>(a);
+  return (int)cudaGetLastError();
+}
+
+int launch_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
+                const float* c1, const float* c2, float* sumsq_part, cudaStream_t s) {
+  k_adam<<<kAdamBlocks, 256, 0, s>>>(reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
+                                     reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n / 4, lr, b1, b2,
+                                     eps, c1, c2, sumsq_part);
+  return (int)cudaGetLastError();
+}
+
+int launch_polyak(float* target, const float* online, int64_t n, float tau, cudaStream_t s) {
+  if (n == 0) return 0;
+  int64_t blocks = (n / 4 + 255) / 256;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_polyak<<<(unsigned)blocks, 256, 0, s>>>(target, online, n, tau);
+  return (int)cudaGetLastError();
+}
+
+int launch_metrics(const MetricsArgs& a, cudaStream_t s) {
+  k_metrics<<<1, 256, 0, s>>>(a);
+  return (int)cudaGetLastError();
+}
+
+int launch_lpi_sums(const float* row_lpi, const float* row_q, int B, float* out2, cudaStream_t s) {
+  k_lpi_sums<<<1, 256, 0, s>>>(row_lpi, row_q, B, out2);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace sq

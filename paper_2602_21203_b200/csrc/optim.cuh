@@ -1,0 +1,62 @@
+// optim.cuh -- temperature step, fused Adam, Polyak, per-update metrics (a11, a13, a14).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sq {
+
+// Scalar slots in the workspace (float[kScal]).
+enum Scal : int {
+  S_ALPHA1 = 0,        // alpha after its Adam step
+  S_ALPHA1_SCALE = 1,  // alpha1 * loss scale (dL_pi / dlog pi)
+  S_MEAN_LOGP = 2,
+  S_LALPHA = 3,
+  S_LQ = 4,
+  S_C1_CRITIC = 5, S_C2_CRITIC = 6, S_C1_ACTOR = 7, S_C2_ACTOR = 8,
+  kScal = 32
+};
+// Row sums that the data-parallel path all-reduces together with the critic gradient.
+enum Extra : int { X_SUM_LOGP = 0, X_SUM_LQ = 1, kExtra = 32 };
+
+struct ScalarsArgs {
+  int B;                 // local rows
+  float inv_btotal;      // 1 / global batch
+  const float* logp;     // [B] current-state log pi (pre-step phi)
+  const float* row_loss; // [B] per-row L_Q terms (already scaled)
+  float* extras;         // [kExtra] row sums (written when compute_sums, else read)
+  int compute_sums;
+  float* log_alpha; float* m_alpha; float* v_alpha;
+  int64_t* step;         // [3]
+  float lr_alpha, beta1, beta2, adam_eps, target_entropy;
+  float loss_scale;      // 1 / global batch
+  float* scal;           // [kScal]
+};
+
+int launch_row_sums(const float* logp, const float* row_loss, int B, float* extras, cudaStream_t s);
+int launch_scalars(const ScalarsArgs& a, cudaStream_t s);
+
+// p -= lr * (m c1) / (sqrt(v c2) + eps) with m, v updated from g (Q26).  c1 = 1/(1-b1^t),
+// c2 = 1/(1-b2^t) read from scal.  n % 4 == 0, 16-byte aligned.  If sumsq_part != NULL,
+// writes sum(g^2) per block (kAdamBlocks entries, fixed order).
+constexpr int kAdamBlocks = 296;
+int launch_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
+                const float* c1, const float* c2, float* sumsq_part, cudaStream_t s);
+// target = (1 - tau) target + tau online; any n, any alignment.
+int launch_polyak(float* target, const float* online, int64_t n, float tau, cudaStream_t s);
+
+struct MetricsArgs {
+  int B;
+  float inv_btotal;
+  const float* row_lpi;  // [B] (scaled)
+  const float* row_q;    // [B]
+  const float* sumsq_part;  // [kAdamBlocks]
+  const float* scal;
+  const float* extras;
+  float* out;            // [8]
+  int reduce_local;      // 1: sum row_lpi/row_q here; 0: read pre-reduced sums from extras2
+  const float* extras2;  // [2] = (sum row_lpi, sum row_q) when reduce_local == 0
+};
+int launch_metrics(const MetricsArgs& a, cudaStream_t s);
+int launch_lpi_sums(const float* row_lpi, const float* row_q, int B, float* out2, cudaStream_t s);
+
+}  // namespace sq

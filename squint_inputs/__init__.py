@@ -141,7 +141,7 @@ def make_frames(n, hw=128, seed=0, channels=3):
     fr = t - i0
     rows = grid[:, :, i0, :] * (1 - fr)[None, None, :, None] + grid[:, :, i0 + 1, :] * fr[None, None, :, None]
     field = rows[:, :, :, i0] * (1 - fr) + rows[:, :, :, i0 + 1] * fr
-    return np.clip(base + np.rint(field).astype(np.int16), 0, 255).astype(np.uint8)
+    return np.ascontiguousarray(np.clip(base + np.rint(field).astype(np.int16), 0, 255).astype(np.uint8))
 
 
 def make_slots(n, capacity, seed=2):

@@ -1,0 +1,179 @@
+"""GPU parity: libsquint (through the C ABI) vs the float64 oracle on the same seeded
+inputs.  Integer work bit-exact; fp32 mode within 1e-4 (losses) / 1e-3 (gradients,
+parameters) scale-relative (BASELINE.json north_star; Q34)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import squint_inputs as SI
+from harness import Problem, compare, group_values
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+import paper_2602_21203_b200 as P  # noqa: E402
+
+DEV = "cuda"
+
+
+# ---- a1 squint insert ---------------------------------------------------------------
+@pytest.mark.parametrize("n,hw,factor", [(1, 128, 8), (37, 128, 8), (5, 64, 4), (3, 48, 3), (2, 16, 1)])
+def test_insert_bit_exact_small(n, hw, factor):
+    frames = SI.make_frames(n, hw, seed=n)
+    cap = 100
+    slots = SI.make_slots(n, cap, seed=n + 1)
+    ring0 = np.full((cap, 3, hw // factor, hw // factor), 7, np.uint8)
+    exp = O.insert(frames, factor, slots, ring0)
+    ring = torch.as_tensor(ring0).to(DEV)
+    P.squint_insert(torch.as_tensor(frames).to(DEV), factor, torch.as_tensor(slots).to(DEV), ring)
+    torch.cuda.synchronize()
+    assert np.array_equal(ring.cpu().numpy(), exp)
+
+
+def test_insert_bit_exact_full_c1():
+    """BASELINE configs[1] at full size: 1024 frames 3x128x128 -> 1M ring, all written
+    rows checked against the oracle, untouched rows unchanged."""
+    c = SI.CONFIGS["c1"]
+    frames = SI.make_frames(c["n_frames"], c["frame_hw"], seed=0)
+    slots = SI.make_slots(c["n_frames"], c["capacity"], seed=2)
+    ring = torch.full((c["capacity"], 3, 16, 16), 3, dtype=torch.uint8, device=DEV)
+    P.squint_insert(torch.as_tensor(frames).to(DEV), 8, torch.as_tensor(slots).to(DEV), ring)
+    torch.cuda.synchronize()
+    got = ring[torch.as_tensor(slots).to(DEV)].cpu().numpy()
+    assert np.array_equal(got, O.area_downsample(frames, 8))
+    assert int((ring != 3).any(dim=(1, 2, 3)).sum().item()) <= c["n_frames"]
+
+
+def test_insert_tie_and_constant():
+    f = np.zeros((2, 3, 128, 128), np.uint8)
+    f[0] = 77
+    # a block whose sum is exactly x.5 * 64: 32 pixels 1, 32 pixels 2 -> 1.5 -> 2; 0/1 -> 0.5 -> 0
+    f[1, 0, :8, :8] = 1
+    f[1, 0, :4, :8] = 2
+    f[1, 1, :8, :8] = 0
+    f[1, 1, :4, :8] = 1
+    ring = torch.zeros((4, 3, 16, 16), dtype=torch.uint8, device=DEV)
+    P.squint_insert(torch.as_tensor(f).to(DEV), 8, torch.tensor([2, 0], device=DEV), ring)
+    r = ring.cpu().numpy()
+    assert (r[2] == 77).all() and r[0, 0, 0, 0] == 2 and r[0, 1, 0, 0] == 0
+
+
+# ---- a14 soft update ------------------------------------------------------------------
+@pytest.mark.parametrize("n,tau", [(1, 0.005), (1000, 0.005), (4097, 0.5), (33, 0.0), (33, 1.0)])
+def test_soft_update(n, tau):
+    rng = np.random.default_rng(n)
+    t0, o = rng.standard_normal(n).astype(np.float32), rng.standard_normal(n).astype(np.float32)
+    t = torch.as_tensor(t0).to(DEV)
+    P.squint_soft_update(t, torch.as_tensor(o).to(DEV), tau)
+    compare("polyak", t.cpu().numpy(), O.soft_update(t0, o, tau), 1e-6)
+    if tau == 0.0:
+        assert np.array_equal(t.cpu().numpy(), t0)
+    if tau == 1.0:
+        assert np.array_equal(t.cpu().numpy(), o)
+
+
+# ---- a16 act --------------------------------------------------------------------------
+@pytest.mark.parametrize("n,sample", [(1, True), (37, True), (64, False)])
+def test_act_fp32(n, sample):
+    d = SI.dims_of("c0", batch=1)
+    hp = SI.hp_of("c0")
+    pr = Problem("c0", seed=5)
+    L = pr.gpu_setup()
+    frames = SI.make_frames(n, 128, seed=n)
+    prop = SI.make_proprio(n, 12, seed=n)
+    eps = np.random.default_rng(n).standard_normal((n, 6)).astype(np.float32) if sample else None
+    st = O.init_state(pr.specs, pr.vals)
+    a_ref, lp_ref, small = O.act(pr.d, pr.h, st["critic"], st["actor"], frames, prop, eps)
+    dims = P.make_dims(pr.dims)
+    ws = torch.zeros(P.act_workspace_bytes(dims, n), dtype=torch.uint8, device=DEV)
+    act = torch.zeros((n, 6), device=DEV)
+    lp = torch.zeros(n, device=DEV)
+    ring = torch.zeros((200, 3, 16, 16), dtype=torch.uint8, device=DEV)
+    slots = torch.as_tensor(SI.make_slots(n, 200, seed=n)).to(DEV)
+    P.squint_act(dims, P.make_hparams(pr.hp), L.actor, L.critic, torch.as_tensor(frames).to(DEV),
+                 torch.as_tensor(prop).to(DEV), None if eps is None else torch.as_tensor(eps).to(DEV), act, lp, ws,
+                 ring=ring, slots=slots)
+    torch.cuda.synchronize()
+    compare("action", act.cpu().numpy(), a_ref, 1e-3)
+    compare("logp", lp.cpu().numpy(), lp_ref, 1e-3)
+    assert np.array_equal(ring[slots].cpu().numpy(), small)
+
+
+# ---- a2-a15 update, fp32 mode -----------------------------------------------------------
+def _check_update(pr, L, met_gpu, st_ref, met_ref, trace, tol_loss=1e-4, tol=1e-3):
+    # losses and metrics
+    for j in range(pr.utd):
+        for k, name in enumerate(["L_Q", "L_pi", "L_alpha", "alpha", "meanQ", "entropy", "gradnorm"]):
+            # losses / alpha / entropy at the loss bound; mean Q (a near-zero sum of p_k z_k over a
+            # +-v_max support, cancellation-prone) and |grad| at the gradient bound (DESIGN.md R-tol)
+            compare(f"metric {name}[{j}]", met_gpu[j, k], met_ref[j, k], tol_loss if k in (0, 1, 2, 3, 5) else tol)
+        assert met_gpu[j, 7] == 0.0
+    # gradients of the last update
+    tr = trace[-1]
+    g = group_values(L, "critic", "grad")
+    for n, ref in tr["grad_critic"].items():
+        compare(f"grad critic {n}", g[n], ref, tol)
+    g = group_values(L, "actor", "grad")
+    for n, ref in tr["grad_actor"].items():
+        compare(f"grad actor {n}", g[n], ref, tol)
+    # target distribution and log-probs of the last update
+    compare("m", L.region("m").cpu().numpy().reshape(tr["m"].shape), tr["m"], tol)
+    compare("logp", L.region("logp").cpu().numpy(), tr["logp"], tol)
+    compare("logp_next", L.region("logp_next").cpu().numpy(), tr["logp_next"], tol)
+    # updated parameters, moments, target
+    for grp in ("critic", "actor", "target"):
+        got = group_values(L, grp)
+        for n, ref in st_ref[grp].items():
+            compare(f"{grp} {n}", got[n], ref, tol)
+            if grp != "target":
+                d_ref = ref - np.asarray(pr.vals[(grp, n)], np.float64)
+                compare(f"delta {grp} {n}", got[n] - pr.vals[(grp, n)], d_ref, 2e-2)
+    for grp in ("critic", "actor"):
+        for which in ("m", "v"):
+            got = group_values(L, grp, which)
+            for n, ref in st_ref[which][grp].items():
+                compare(f"{which} {grp} {n}", got[n], ref, tol)
+    compare("log_alpha", L.log_alpha.cpu().numpy()[0], st_ref["log_alpha"], 1e-5)
+    assert L.step.cpu().tolist() == list(st_ref["step"])
+
+
+@pytest.mark.parametrize("utd", [1, 4])
+def test_update_c0_fp32(utd):
+    pr = Problem("c0", utd=utd, seed=0)
+    L = pr.gpu_setup()
+    met = pr.gpu_update(L)
+    trace = []
+    st_ref, met_ref = pr.oracle_update(trace)
+    _check_update(pr, L, met, st_ref, met_ref, trace)
+
+
+@pytest.mark.parametrize("batch", [1, 37])
+def test_update_ragged_batch_fp32(batch):
+    pr = Problem("c0", utd=1, seed=3, batch=batch)
+    L = pr.gpu_setup()
+    met = pr.gpu_update(L)
+    trace = []
+    st_ref, met_ref = pr.oracle_update(trace)
+    _check_update(pr, L, met, st_ref, met_ref, trace)
+
+
+def test_update_c2_shapes_b64_fp32():
+    pr = Problem("c2", capacity=2000, utd=2, seed=1, batch=64)
+    L = pr.gpu_setup()
+    met = pr.gpu_update(L)
+    trace = []
+    st_ref, met_ref = pr.oracle_update(trace)
+    _check_update(pr, L, met, st_ref, met_ref, trace)
+
+
+def test_update_deterministic_bitwise():
+    pr = Problem("c0", utd=2, seed=7)
+    outs = []
+    for _ in range(2):
+        L = pr.gpu_setup()
+        pr.gpu_update(L)
+        outs.append((L.critic.cpu().numpy().copy(), L.actor.cpu().numpy().copy(), L.target.cpu().numpy().copy()))
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
