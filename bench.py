@@ -1,0 +1,451 @@
+"""bench.py -- Squint hot path on B200: SAC gradient updates/s (BASELINE.json metric).
+
+One step = one Algorithm-1 iteration at BASELINE configs[2]:
+  squint_act   on N_env = 1024 rendered 3x128x128 frames (squint + encoder + actor + sample,
+               with the squinted obs written into the 1M replay ring: a16 + a1),
+  squint_insert of the 1024 next frames into the ring's next_obs (a1),
+  squint_update with UTD 4 at batch 512 (a2-a15), 101 atoms on [-20, 20].
+value = updates/s summed over ranks (weak scaling: every rank owns a 512-sample shard of
+the 512*N global batch; gradients are NCCL all-reduced).  Inputs live in HBM before the
+timed region; the replay ring (1.66 GB per rank) and three rotating 100 MB frame pools
+exceed the 126 MB L2.  Launch: python bench.py [--gpus N --steps K --warmup W]
+(torchrun for N > 1).  --impl reference times the CPU oracle instead (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import squint_inputs as SI  # noqa: E402
+
+N_ENV = 1024
+UTD = 4
+CFG = "c2"
+METRIC = "SAC gradient updates/sec (batch 512, 1/2/4/8 B200) + % HBM/tensor roofline"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+# ---------------------------------------------------------------------------------------
+# CPU oracle sample (cpu_baseline leg and --impl reference)
+# ---------------------------------------------------------------------------------------
+def oracle_sample(seed=0, n_frames=N_ENV // UTD):
+    """One update's share of a step on the CPU oracle: act + insert on n_frames frames and
+    one c2 update (B = 512) on rows gathered from a seeded replay sample."""
+    import oracle as O
+    d = SI.dims_of(CFG)
+    hp = SI.hp_of(CFG)
+    D, H = O.Dims(**d), O.HParams(**hp)
+    specs = O.param_specs(D)
+    vals = SI.make_params(specs, seed=1)
+    st = O.init_state(specs, vals)
+    B = d["batch"]
+    R = SI.make_replay(4 * B, d, seed=seed)  # rows the sample draws from (same distribution as the ring)
+    idx = SI.make_indices(1, B, 4 * B, seed=2 + seed)
+    sh = SI.make_shifts(1, B, d["pad"], seed=2 + seed)
+    eps = SI.make_eps(1, B, d["action_dim"], seed=3 + seed)
+    frames = SI.make_frames(n_frames, 128, seed=seed)
+    nxt = SI.make_frames(n_frames, 128, seed=seed + 100)
+    prop = SI.make_proprio(n_frames, d["proprio_dim"], seed=seed)
+    ae = np.random.default_rng(seed).standard_normal((n_frames, d["action_dim"])).astype(np.float32)
+    t0 = time.perf_counter()
+    O.act(D, H, st["critic"], st["actor"], frames, prop, ae)
+    O.area_downsample(nxt, 8)
+    O.update(D, H, R, idx, sh, eps, st)
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    for w in range(args.warmup):
+        oracle_sample(seed=w)
+    ts = [oracle_sample(seed=100 + k) for k in range(args.steps)]
+    tot = sum(ts)
+    value = args.steps / tot  # one update per sample
+    cores = blas_threads()
+    sample = f"per step: oracle act+insert on {N_ENV // UTD} frames + 1 update at B=512 (c2 shapes), float64 NumPy"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c2 update share of an Algorithm-1 step (CPU oracle)", "global_batch": 512,
+                       "utd": 1, "n_env_frames": N_ENV // UTD},
+            "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in out.strip().splitlines():
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------
+# algorithmic work per phase (per update unless noted) for the roofline line
+# ---------------------------------------------------------------------------------------
+def phase_work(d, n_env):
+    B, C, L, P, A = d["batch"], d["conv_ch"], d["latent"], d["proprio_dim"], d["action_dim"]
+    Hc, Ha, N = d["critic_hidden"], d["actor_hidden"], d["n_atoms"]
+    P1, P2 = 49, 25
+    F = C * P2
+    nq, npi = L + P + A, L + P
+    conv = P1 * C * 27 + P2 * C * 9 * C                      # MACs per image
+    mlp_q = nq * Hc + Hc * Hc + Hc * N
+    mlp_a = npi * Ha + Ha * Ha + Ha * 2 * A
+    fl = {
+        "enc_fwd": 2 * 2 * B * conv,
+        "proj_fwd": 2 * 4 * B * L * F,
+        "actor_fwd": 2 * 2 * B * mlp_a,
+        "heads_fwd": 2 * 4 * B * mlp_q,
+        "critic_bwd": 2 * (2 * B * (N * Hc + Hc * Hc) + B * 2 * Hc * L + B * L * F),
+        "critic_dw": 2 * (2 * B * mlp_q + B * L * F),
+        "enc_bwd": 2 * B * (P2 * C * 9 * C * 2 + P1 * C * 27),
+        "actor_loss": 2 * (B * L * F + 2 * B * mlp_q),
+        "actor_bwd": 2 * (2 * B * (N * Hc + Hc * Hc + Hc * A) + B * (2 * A * Ha + Ha * Ha + Ha * L)),
+        "actor_dw": 2 * (B * mlp_a + B * L * F),
+        "act_encode": 2 * n_env * conv,
+        "act_mlp": 2 * n_env * (L * F + mlp_a),
+    }
+    by = {"insert": n_env * 3 * 128 * 128 + n_env * 768,
+          "act_encode": n_env * 3 * 128 * 128 + n_env * 768 + n_env * F * 4}
+    return fl, by
+
+
+# ---------------------------------------------------------------------------------------
+# the GPU arm
+# ---------------------------------------------------------------------------------------
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_21203_b200 as P
+    from paper_2602_21203_b200 import squint as S
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    precision = {"fp32": P.FP32, "bf16": P.BF16}[args.precision]
+    d = SI.dims_of(CFG)
+    hp = SI.hp_of(CFG)
+    B, A = d["batch"], d["action_dim"]
+    cap = SI.CONFIGS[CFG]["capacity"]
+    K, W = args.steps, args.warmup
+
+    L = P.Learner(d, hp, precision=precision, device=dev, utd=UTD)
+    layout3 = [(S.GROUP_NAMES[g], n, s) for g, n, off, s in L.layout]
+    L.load_values(SI.make_params(SI.specs_from_layout(layout3), seed=1))
+    if world > 1:
+        uid = bytearray(128)
+        if rank == 0:
+            uid = bytearray(S.comm_unique_id())
+        t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, 0)
+        L.comm = S.comm_init(bytes(t.cpu().tolist()), rank, world)
+
+    # replay ring (replica per rank, data seed 0): device-side seeded fill, same distributions as c0
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    R = {
+        "obs": torch.randint(0, 256, (cap, 3, 16, 16), generator=g, device=dev, dtype=torch.uint8),
+        "next_obs": torch.randint(0, 256, (cap, 3, 16, 16), generator=g, device=dev, dtype=torch.uint8),
+        "proprio": torch.randn((cap, d["proprio_dim"]), generator=g, device=dev),
+        "next_proprio": torch.randn((cap, d["proprio_dim"]), generator=g, device=dev),
+        "action": torch.rand((cap, A), generator=g, device=dev) * 2 - 1,
+        "reward": torch.rand((cap,), generator=g, device=dev),
+        "done": (torch.rand((cap,), generator=g, device=dev) < 0.01).to(torch.uint8),
+    }
+    replay = P.replay_from_tensors(R)
+    # per-step inputs for all K + W steps, resident in HBM
+    T = K + W
+    gi = torch.Generator(device=dev)
+    gi.manual_seed(2 + 1000 * rank)
+    idx_all = torch.randint(0, cap, (T, UTD, B), generator=gi, device=dev, dtype=torch.int64)
+    sh_all = torch.randint(0, 2 * d["pad"] + 1, (T, UTD, B, 4), generator=gi, device=dev, dtype=torch.uint8)
+    eps_all = torch.randn((T, UTD, 2, B, A), generator=gi, device=dev)
+    aeps_all = torch.randn((T, N_ENV, A), generator=gi, device=dev)
+    prop_all = torch.randn((T, N_ENV, d["proprio_dim"]), generator=gi, device=dev)
+    slots_all = torch.stack([(torch.arange(N_ENV, device=dev) + k * N_ENV) % cap for k in range(T)])
+    # three rotating frame pools (act frames + next frames), 3 x 100 MB > L2
+    NPOOL = 3
+    pools = []
+    for p in range(NPOOL):
+        fr = torch.as_tensor(SI.make_frames(N_ENV, 128, seed=10 + p)).to(dev)
+        nx = torch.as_tensor(SI.make_frames(N_ENV, 128, seed=20 + p)).to(dev)
+        pools.append((fr, nx))
+    # static per-step buffers that the graphs read
+    idx_s, sh_s, eps_s = idx_all[0].clone(), sh_all[0].clone(), eps_all[0].clone()
+    aeps_s, prop_s, slots_s = aeps_all[0].clone(), prop_all[0].clone(), slots_all[0].clone()
+    metrics = torch.zeros((UTD, 8), device=dev)
+    act_out = torch.zeros((N_ENV, A), device=dev)
+    logp_out = torch.zeros((N_ENV,), device=dev)
+    act_ws = torch.zeros(P.act_workspace_bytes(L.dims, N_ENV), dtype=torch.uint8, device=dev)
+    obs_ring = R["obs"]
+    next_ring = R["next_obs"]
+
+    def step(pool, stream=None):
+        fr, nx = pools[pool]
+        P.squint_act(L.dims, L.hp, L.actor, L.critic, fr, prop_s, aeps_s, act_out, logp_out, act_ws,
+                     ring=obs_ring, slots=slots_s, stream=stream)
+        P.squint_insert(nx, 8, slots_s, next_ring, stream=stream)
+        L.update(replay, idx_s, sh_s, eps_s, metrics, stream=stream)
+
+    def load_inputs(k):
+        idx_s.copy_(idx_all[k], non_blocking=True)
+        sh_s.copy_(sh_all[k], non_blocking=True)
+        eps_s.copy_(eps_all[k], non_blocking=True)
+        aeps_s.copy_(aeps_all[k], non_blocking=True)
+        prop_s.copy_(prop_all[k], non_blocking=True)
+        slots_s.copy_(slots_all[k], non_blocking=True)
+
+    # eager warm step: counts launches, checks errors
+    c0 = S.launch_count()
+    load_inputs(0)
+    step(0)
+    torch.cuda.synchronize()
+    launches_per_step = S.launch_count() - c0
+
+    timers = [S.PhaseTimer(UTD) for _ in range(NPOOL)]
+    graphs = []
+    use_graph = not args.no_graph
+    if use_graph:
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            step(0)  # warm on the capture stream
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        for p in range(NPOOL):
+            gph = torch.cuda.CUDAGraph()
+            timers[p].enable()
+            with torch.cuda.graph(gph):
+                step(p)
+            S.PhaseTimer.disable()
+            graphs.append(gph)
+        torch.cuda.synchronize()
+
+    def run_one(k):
+        load_inputs(k)
+        if use_graph:
+            graphs[k % NPOOL].replay()
+        else:
+            timers[k % NPOOL].enable()
+            step(k % NPOOL)
+            S.PhaseTimer.disable()
+
+    for w in range(W):
+        run_one(w)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    st.record()
+    for k in range(W, W + K):
+        run_one(k)
+    en.record()
+    torch.cuda.synchronize()
+    ms = st.elapsed_time(en)
+    clocks = clk.stop()
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    met = metrics.cpu().numpy()
+    if not np.isfinite(met).all() or met[:, 7].any():
+        print(f"rank {rank}: non-finite metrics {met}", file=sys.stderr)
+        sys.exit(3)
+
+    # phase times (average over the pools' last replays)
+    ph = {}
+    for t in timers:
+        for k, v in t.times_ms().items():
+            ph.setdefault(k, []).append(v)
+    ph = {k: sum(v) / len(v) for k, v in ph.items()}
+
+    # e2e: same step through the C ABI from pinned host buffers (H2D inputs, D2H results)
+    e2e = None
+    if not args.no_e2e:
+        h_fr = [pools[p][0].cpu().pin_memory() for p in range(NPOOL)]
+        h_nx = [pools[p][1].cpu().pin_memory() for p in range(NPOOL)]
+        h_in = [t.cpu().pin_memory() for t in (idx_all, sh_all, eps_all, aeps_all, prop_all, slots_all)]
+        h_out = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (act_out, logp_out, metrics)]
+        dfr, dnx = pools[0][0].clone(), pools[0][1].clone()
+        stage = [idx_s, sh_s, eps_s, aeps_s, prop_s, slots_s]
+
+        def e2e_step(k):
+            dfr.copy_(h_fr[k % NPOOL], non_blocking=True)
+            dnx.copy_(h_nx[k % NPOOL], non_blocking=True)
+            for dst, src in zip(stage, h_in):
+                dst.copy_(src[k], non_blocking=True)
+            P.squint_act(L.dims, L.hp, L.actor, L.critic, dfr, prop_s, aeps_s, act_out, logp_out, act_ws,
+                         ring=obs_ring, slots=slots_s)
+            P.squint_insert(dnx, 8, slots_s, next_ring)
+            L.update(replay, idx_s, sh_s, eps_s, metrics)
+            for dst, src in zip(h_out, (act_out, logp_out, metrics)):
+                dst.copy_(src, non_blocking=True)
+
+        for w in range(W):
+            e2e_step(w)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for k in range(W, W + K):
+            e2e_step(k)
+        b.record()
+        torch.cuda.synchronize()
+        ems = a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        h2d = (pools[0][0].numel() + pools[0][1].numel() + sum(x[0].numel() * x.element_size() for x in h_in))
+        d2h = sum(x.numel() * x.element_size() for x in h_out)
+        e2e = {"value": world * UTD * K / (ems / 1e3), "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / K}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # roofline on the dominant phase
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    fl, by = phase_work(d, N_ENV)
+    step_ms = ms / K
+    dom = max(ph, key=ph.get) if ph else None
+    roof = None
+    if dom:
+        reps = UTD if dom not in ("insert", "act_encode", "act_mlp") else 1
+        t_launch = ph[dom] / reps / 1e3  # seconds per launch of the phase
+        if dom in by and dom not in fl:
+            ach = by[dom] / t_launch / 1e9
+            peak = peaks.get("hbm_gbs", 6650.0)
+            roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s"}
+        elif precision == P.BF16:
+            ach = fl[dom] / t_launch / 1e12
+            peak = peaks.get("bf16_tflops_sustained", 1400.0)
+            roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s"}
+        else:
+            ach = fl[dom] / t_launch / 1e12
+            peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12  # fp32 FFMA, DESIGN.md §6
+            roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["traffic"] = None
+        roof["kernel"] = dom
+        roof["share_of_step"] = ph[dom] / step_ms if step_ms > 0 else None
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        ts = [oracle_sample(seed=s) for s in range(args.cpu_samples)]
+        cpu = {"value": len(ts) / sum(ts), "unit": "updates/s", "cores": blas_threads(), "kind": "oracle",
+               "sample": f"{len(ts)} x (oracle act+insert on {N_ENV // UTD} frames + 1 update at B=512), "
+                         f"{sum(ts):.1f} s float64 NumPy"}
+    line = {"metric": METRIC, "value": world * UTD * K / (ms / 1e3), "unit": "updates/s", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": {P.FP32: "f32", P.BF16: "bf16"}[precision], "data": "synthetic",
+            "config": {"workload": "c2: Algorithm-1 step = act(1024 envs, 128x128) + insert(1024) + 4 updates at "
+                                   "B=512 per rank, 101 atoms, 1M ring", "global_batch": B * world, "utd": UTD,
+                       "n_env": N_ENV, "parallelism": f"dp{world}", "l2": "ring 1.66 GB + 3 rotating 100 MB frame pools > L2",
+                       "graph": use_graph},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": int(launches_per_step * K), "phases_ms_per_step": ph}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="squint", choices=["squint", "reference"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-samples", type=int, default=3)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

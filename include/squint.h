@@ -190,6 +190,16 @@ SQUINT_API squint_status squint_update(const squint_dims* dims, const squint_hpa
 SQUINT_API squint_status squint_soft_update(float* target, const float* online, int64_t n, float tau,
                                  squint_stream_t stream);
 
+/* ---- instrumentation (bench.py) --------------------------------------------------------
+ * Number of kernels libsquint has launched in this process (host counter). */
+SQUINT_API long squint_launch_count(void);
+/* When `events` (host array of n_phases * reps * 2 cudaEvent_t) is non-NULL, phase k of
+ * update j (rep j; act/insert use rep 0) records events[(k*reps+j)*2] before and
+ * events[(k*reps+j)*2+1] after its kernels on the launch stream.  NULL disables.
+ * Phase names: squint_phase_name(k) (16 phases). */
+SQUINT_API squint_status squint_set_phase_events(void** events, int n_phases, int reps);
+SQUINT_API const char* squint_phase_name(int k);
+
 #ifdef __cplusplus
 }
 #endif

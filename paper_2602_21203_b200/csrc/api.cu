@@ -5,10 +5,12 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <optional>
 #include <string>
 
 #include "../../include/squint.h"
 #include "comm.hpp"
+#include "common.cuh"
 #include "dense.cuh"
 #include "encoder.cuh"
 #include "heads.cuh"
@@ -223,7 +225,7 @@ static int run_dense(DenseBatch& b, cudaStream_t s) {
 // ---- one update, fp32 path -------------------------------------------------------------
 static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const int64_t* idx, const uint8_t* sh,
                                     const float* eps, const squint_state& st, float* metrics, Comm* comm,
-                                    float inv_btotal) {
+                                    float inv_btotal, int rep) {
   const squint_dims& d = c.d;
   const squint_hparams& hp = c.hp;
   const Layout& L = c.L;
@@ -248,6 +250,7 @@ static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const 
 
   // a3-a5: gather + shift + encoder for obs and next_obs
   {
+    PhaseScope ps(3, rep, s);
     EncFwdArgs e;
     memset(&e, 0, sizeof(e));
     e.mode = 0;
@@ -273,6 +276,7 @@ static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const 
   }
   // a6: four projections
   {
+    PhaseScope ps(4, rep, s);
     DenseBatch b;
     b.nprob = 4;
     b.p[0] = fwd_prob(B, cproj, Lt, F, {seg(c.F(w.h), F, F)}, EPI_LN_TANH, c.F(w.pq.z), c.F(w.pq.xh), c.F(w.pq.rs), le);
@@ -283,6 +287,7 @@ static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const 
   }
   // a7: actor MLP on next obs (target sample) and on current obs (alpha / actor losses)
   {
+    PhaseScope ps(5, rep, s);
     DenseBatch b;
     b.nprob = 2;
     b.p[0] = fwd_prob(B, am.l1, Ha, npi, {seg(c.F(w.ppn.z), Lt, Lt), seg(R.next_proprio, P, P, idx)}, EPI_LN_RELU,
@@ -310,6 +315,7 @@ static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const 
   }
   // a8: target heads on (z', s', a') and online heads on (z, s, a)
   {
+    PhaseScope ps(6, rep, s);
     DenseBatch b;
     b.nprob = 4;
     for (int i = 0; i < 2; ++i) {
@@ -338,6 +344,7 @@ static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const 
   }
   // a9-a10: target distribution, projection, CE and dL/dlogits
   {
+    PhaseScope ps(7, rep, s);
     TargetCEArgs t;
     t.B = B;
     t.N = N;
@@ -360,6 +367,7 @@ static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const 
   // a10: critic backward (heads -> projection -> encoder)
   float* gc = c.F(w.grad_critic);
   {
+    PhaseScope ps(8, rep, s);
     DenseBatch b;
     b.nprob = 2;
     for (int i = 0; i < 2; ++i) {
@@ -398,6 +406,7 @@ static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const 
     SQ_CK(run_dense(b, s));
   }
   {
+    PhaseScope ps(9, rep, s);
     DwBatch b;
     b.nprob = 7;
     int k = 0;
@@ -423,6 +432,7 @@ static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const 
     SQ_CK(launch_dw_f32(b, s));
   }
   {
+    PhaseScope ps(10, rep, s);
     EncBwdArgs e;
     e.B = B;
     e.C = C;
@@ -448,8 +458,9 @@ static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const 
     SQ_CK(launch_row_sums(c.F(w.logp_cur), c.F(w.row_loss), B, extras, s));
     if (comm_allreduce_sum(comm, gc, L.gsize[gC] + kExtra, s) != 0) return fail(SQUINT_ENCCL, comm_error());
   }
-  // a11: temperature step; Adam step counters and bias corrections
+  // a11: temperature step; Adam step counters and bias corrections; a13 Adam (critic)
   {
+    PhaseScope ps(11, rep, s);
     ScalarsArgs a;
     a.B = B;
     a.inv_btotal = inv_btotal;
@@ -469,12 +480,14 @@ static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const 
     a.loss_scale = inv_btotal;
     a.scal = scal;
     SQ_CK(launch_scalars(a, s));
+    // a13: Adam on the critic group (psi, projection, heads)
+    SQ_CK(launch_adam(st.critic, gc, st.m_critic, st.v_critic, L.gsize[gC], hp.lr_critic, hp.beta1, hp.beta2,
+                      hp.adam_eps, scal + S_C1_CRITIC, scal + S_C2_CRITIC, c.F(w.adam_part), s));
   }
-  // a13: Adam on the critic group (psi, projection, heads)
-  SQ_CK(launch_adam(st.critic, gc, st.m_critic, st.v_critic, L.gsize[gC], hp.lr_critic, hp.beta1, hp.beta2,
-                    hp.adam_eps, scal + S_C1_CRITIC, scal + S_C2_CRITIC, c.F(w.adam_part), s));
   // a12: actor loss against theta+ on sg(h)
   {
+    std::optional<PhaseScope> ps;
+    ps.emplace(12, rep, s);
     const MlpV cq1[2] = {mlpv(crit, L, gC, "critic.q1"), mlpv(crit, L, gC, "critic.q2")};  // same buffer, now theta+
     DenseBatch b;
     b.nprob = 1;
@@ -508,6 +521,8 @@ static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const 
     q.row_lpi = c.F(w.row_lpi);
     SQ_CK(launch_actor_q(q, s));
     // dL/da~ through theta+ heads
+    ps.reset();
+    ps.emplace(13, rep, s);
     for (int i = 0; i < 2; ++i) {
       b.p[i] = bwd_prob(B, Hc, {seg(c.F(w.dlogits) + (size_t)i * B * N, N, N)}, {BSeg{cq1[i].l3.w, Hc, N, 0}},
                         EPI_BWD_LN_RELU, c.F(w.dA2[i]), Hc);
@@ -565,6 +580,7 @@ static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const 
   }
   float* ga = c.F(w.grad_actor);
   {
+    PhaseScope ps(14, rep, s);
     DwBatch b;
     b.nprob = 4;
     LinG g3 = ling(ga, L, gA, "actor.l3", false, ""), g2 = ling(ga, L, gA, "actor.l2", true, "actor.ln2"),
@@ -581,6 +597,7 @@ static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const 
     SQ_CK(launch_dw_f32(b, s));
   }
   float* lpis = c.F(w.lpi_sums);
+  PhaseScope ps15(15, rep, s);
   if (comm) {
     float* ax = ga + L.gsize[gA];
     SQ_CK(launch_lpi_sums(c.F(w.row_lpi), c.F(w.row_q), B, ax, s));
@@ -711,6 +728,7 @@ squint_status squint_insert(const uint8_t* frames, int64_t n, int c, int h, int 
     return fail(SQUINT_EINVAL, "frames must be 16-byte aligned");
   if (factor == 8 && (w % 16) == 0 && ((h / 8) * (w / 8) % 2))
     return fail(SQUINT_EINVAL, "odd output row length not supported by the vector path");
+  PhaseScope ps(0, 0, (cudaStream_t)stream);
   SQ_CK(launch_insert(frames, n, c, h, w, factor, slots, ring, (cudaStream_t)stream));
   return SQUINT_OK;
 }
@@ -757,6 +775,8 @@ squint_status squint_act(const squint_dims* dims, const squint_hparams* hp, cons
   float* h2 = reinterpret_cast<float*>(ws + WP.take(n * Ha * fl));
   float* out = reinterpret_cast<float*>(ws + WP.take(n * 2 * A * fl));
   const int gC = SQUINT_GROUP_CRITIC, gA = SQUINT_GROUP_ACTOR;
+  std::optional<PhaseScope> ps;
+  ps.emplace(1, 0, s);
   {
     EncFwdArgs a;
     memset(&a, 0, sizeof(a));
@@ -781,6 +801,8 @@ squint_status squint_act(const squint_dims* dims, const squint_hparams* hp, cons
   const LinV ap = projv(actor_params, L, gA, "actor");
   const MlpV am = mlpv(actor_params, L, gA, "actor");
   const int M = (int)n;
+  ps.reset();
+  ps.emplace(2, 0, s);
   DenseBatch b;
   b.nprob = 1;
   b.p[0] = fwd_prob(M, ap, Lt, F, {seg(h, F, F)}, EPI_LN_TANH, z, nullptr, nullptr, hp->ln_eps);
@@ -837,7 +859,7 @@ squint_status squint_update(const squint_dims* dims, const squint_hparams* hp, c
       st = update_one_bf16(*dims, *hp, L, reinterpret_cast<char*>(workspace) + w.bf16, *replay, ij, sj, ej, *state, mj,
                            cm, inv_btotal, (cudaStream_t)stream, &g_err);
     else
-      st = update_one_f32(c, *replay, ij, sj, ej, *state, mj, cm, inv_btotal);
+      st = update_one_f32(c, *replay, ij, sj, ej, *state, mj, cm, inv_btotal, j);
     if (st != SQUINT_OK) return st;
   }
   return SQUINT_OK;

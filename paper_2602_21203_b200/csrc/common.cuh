@@ -42,3 +42,17 @@ SQ_DEV float block_sum(float v, float* red) {
 SQ_DEV bool is_finite(float x) { return isfinite(x); }
 
 }  // namespace sq
+
+namespace sq {
+// Host-side count of kernel launches issued by libsquint (bench "gpu_launches" claim).
+void note_launch();
+long launch_count();
+// Optional phase instrumentation (squint_set_phase_events): records cudaEvent pairs
+// around named phases of squint_update / squint_act / squint_insert on the launch stream.
+struct PhaseScope {
+  PhaseScope(int phase, int rep, cudaStream_t s);
+  ~PhaseScope();
+  int idx;
+  cudaStream_t s;
+};
+}  // namespace sq

@@ -176,18 +176,18 @@ __global__ void __launch_bounds__(256) k_metrics(const __grid_constant__ Metrics
 }  // namespace
 
 int launch_row_sums(const float* logp, const float* row_loss, int B, float* extras, cudaStream_t s) {
-  k_row_sums<<<1, 256, 0, s>>>(logp, row_loss, B, extras);
+  note_launch(); k_row_sums<<<1, 256, 0, s>>>(logp, row_loss, B, extras);
   return (int)cudaGetLastError();
 }
 
 int launch_scalars(const ScalarsArgs& a, cudaStream_t s) {
-  k_scalars<<<1, 256, 0, s>>>(a);
+  note_launch(); k_scalars<<<1, 256, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 
 int launch_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
                 const float* c1, const float* c2, float* sumsq_part, cudaStream_t s) {
-  k_adam<<<kAdamBlocks, 256, 0, s>>>(reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
+  note_launch(); k_adam<<<kAdamBlocks, 256, 0, s>>>(reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
                                      reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n / 4, lr, b1, b2,
                                      eps, c1, c2, sumsq_part);
   return (int)cudaGetLastError();
@@ -198,17 +198,17 @@ int launch_polyak(float* target, const float* online, int64_t n, float tau, cuda
   int64_t blocks = (n / 4 + 255) / 256;
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_polyak<<<(unsigned)blocks, 256, 0, s>>>(target, online, n, tau);
+  note_launch(); k_polyak<<<(unsigned)blocks, 256, 0, s>>>(target, online, n, tau);
   return (int)cudaGetLastError();
 }
 
 int launch_metrics(const MetricsArgs& a, cudaStream_t s) {
-  k_metrics<<<1, 256, 0, s>>>(a);
+  note_launch(); k_metrics<<<1, 256, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 
 int launch_lpi_sums(const float* row_lpi, const float* row_q, int B, float* out2, cudaStream_t s) {
-  k_lpi_sums<<<1, 256, 0, s>>>(row_lpi, row_q, B, out2);
+  note_launch(); k_lpi_sums<<<1, 256, 0, s>>>(row_lpi, row_q, B, out2);
   return (int)cudaGetLastError();
 }
 

@@ -75,6 +75,9 @@ def _load():
         "squint_update": (st, [C.POINTER(Dims), C.POINTER(HParams), C.POINTER(Replay), vp, vp, vp, i32,
                                C.POINTER(State), vp, vp, sz, vp, vp]),
         "squint_soft_update": (st, [vp, vp, i64, f32, vp]),
+        "squint_launch_count": (C.c_long, []),
+        "squint_set_phase_events": (st, [C.POINTER(vp), i32, i32]),
+        "squint_phase_name": (C.c_char_p, [i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -86,7 +89,52 @@ def _load():
 LIB = _load()
 EXPORTED = ["squint_last_error", "squint_version", "squint_param_layout", "squint_workspace_bytes",
             "squint_workspace_region", "squint_act_workspace_bytes", "squint_comm_unique_id", "squint_comm_init",
-            "squint_comm_destroy", "squint_insert", "squint_act", "squint_update", "squint_soft_update"]
+            "squint_comm_destroy", "squint_insert", "squint_act", "squint_update", "squint_soft_update",
+            "squint_launch_count", "squint_set_phase_events", "squint_phase_name"]
+N_PHASES = 16
+
+
+def launch_count() -> int:
+    return int(LIB.squint_launch_count())
+
+
+def phase_name(k: int) -> str:
+    return LIB.squint_phase_name(k).decode()
+
+
+class PhaseTimer:
+    """CUDA-event instrumentation of libsquint's phases (squint_set_phase_events)."""
+
+    def __init__(self, reps):
+        self.reps = reps
+        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(N_PHASES * reps * 2)]
+        for e in self.events:  # torch creates the cudaEvent lazily, on first record
+            e.record()
+        torch.cuda.synchronize()
+        self._arr = (C.c_void_p * len(self.events))(*[e.cuda_event for e in self.events])
+
+    def enable(self):
+        _check(LIB.squint_set_phase_events(self._arr, N_PHASES, self.reps))
+
+    @staticmethod
+    def disable():
+        _check(LIB.squint_set_phase_events(None, 0, 0))
+
+    def times_ms(self):
+        """{phase name: summed ms over reps} for phases that recorded."""
+        out = {}
+        for k in range(N_PHASES):
+            tot, hit = 0.0, False
+            for r in range(self.reps):
+                a, b = self.events[(k * self.reps + r) * 2], self.events[(k * self.reps + r) * 2 + 1]
+                try:
+                    tot += a.elapsed_time(b)
+                    hit = True
+                except RuntimeError:
+                    pass
+            if hit:
+                out[phase_name(k)] = tot
+        return out
 
 
 def _check(status):

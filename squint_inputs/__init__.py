@@ -119,6 +119,29 @@ def make_params(specs, seed=1, perturb=False):
     return vals
 
 
+def specs_from_layout(layout):
+    """(group, name, shape, kind, fan_in) from (group_name, name, shape) triples, by naming
+    convention: *.w weights (fan_in = prod(shape[1:])), *.b biases of the matching *.w,
+    *.ln*.g / *.ln*.b LayerNorm gain / bias, log_alpha."""
+    shapes = {(g, n): s for g, n, s in layout}
+    out = []
+    for g, n, s in layout:
+        if n == "log_alpha":
+            out.append((g, n, s, "zero", 0))
+        elif ".ln" in n and n.endswith(".g"):
+            out.append((g, n, s, "g", 0))
+        elif ".ln" in n and n.endswith(".b"):
+            out.append((g, n, s, "beta", 0))
+        elif n.endswith(".w"):
+            out.append((g, n, s, "w", int(np.prod(s[1:]))))
+        elif n.endswith(".b"):
+            ws = shapes[(g, n[:-2] + ".w")]
+            out.append((g, n, s, "b", int(np.prod(ws[1:]))))
+        else:
+            raise ValueError(n)
+    return out
+
+
 def make_adam_prewarm(specs, seed=4, step=10):
     """Pre-warmed Adam moments (Q27): m ~ N(0, 1e-3^2), v ~ U(1e-6, 1e-5), step 10."""
     g = _rng(seed)
