@@ -16,7 +16,7 @@
 #include "heads.cuh"
 #include "layout.hpp"
 #include "optim.cuh"
-#include "update_bf16.cuh"
+#include "dense_tc.cuh"
 
 namespace sq {
 
@@ -51,7 +51,6 @@ struct WsLay {
   size_t dA2[2], dN2[2], dA1[2], dN1[2], dAp, dNp, dAh, dA1enc, enc_part;
   size_t dO, adA2, adN2, adA1, adN1, adAp, adNp;
   size_t grad_critic, grad_actor, adam_part, scal, lpi_sums;
-  size_t bf16;  // bf16 path scratch
   size_t total;
 };
 
@@ -120,7 +119,6 @@ static WsLay plan_ws(const squint_dims& d, const Layout& L) {
   w.adam_part = P.take(kAdamBlocks * f);
   w.scal = P.take(kScal * f);
   w.lpi_sums = P.take(2 * f);
-  w.bf16 = P.take(d.precision == SQUINT_BF16 ? bf16_ws_bytes(d) : 0);
   w.total = P.top + 256;
   return w;
 }
@@ -217,13 +215,23 @@ struct Ctx {
   float* F(size_t off) const { return reinterpret_cast<float*>(ws + off); }
 };
 
+// Precision of the call in flight (set by the entry points; calls on one thread serialise).
+static thread_local int g_prec = SQUINT_FP32;
+
+// Dense layers: fp32 SIMT (parity mode) or bf16 tcgen05 tensor cores.
 static int run_dense(DenseBatch& b, cudaStream_t s) {
+  if (g_prec == SQUINT_BF16) return launch_dense_bf16(b, s);
   const int tn = plan_dense(b);
   return launch_dense_f32(b, tn, s);
 }
+static int run_dw(DwBatch& b, cudaStream_t s) {
+  if (g_prec == SQUINT_BF16) return launch_dw_bf16(b, s);
+  plan_dw(b);
+  return launch_dw_f32(b, s);
+}
 
-// ---- one update, fp32 path -------------------------------------------------------------
-static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const int64_t* idx, const uint8_t* sh,
+// ---- one update ---------------------------------------------------------------------------
+static squint_status update_one(const Ctx& c, const squint_replay& R, const int64_t* idx, const uint8_t* sh,
                                     const float* eps, const squint_state& st, float* metrics, Comm* comm,
                                     float inv_btotal, int rep) {
   const squint_dims& d = c.d;
@@ -428,8 +436,7 @@ static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const 
     LinG gp = ling(gc, L, gC, "critic.proj", true, "critic.proj.ln");
     b.p[k++] = DwProb{B, Lt, F, c.F(w.dAp), 1, {seg(c.F(w.h), F, F)}, gp.w, gp.b, c.F(w.dNp), c.F(w.pq.xh), gp.g,
                       gp.beta, 0, 0};
-    plan_dw(b);
-    SQ_CK(launch_dw_f32(b, s));
+    SQ_CK(run_dw(b, s));
   }
   {
     PhaseScope ps(10, rep, s);
@@ -593,8 +600,7 @@ static squint_status update_one_f32(const Ctx& c, const squint_replay& R, const 
                     c.F(w.adN1), c.F(w.ac.xh1), g1.g, g1.beta, 0, 0};
     b.p[3] = DwProb{B, Lt, F, c.F(w.adAp), 1, {seg(c.F(w.h), F, F)}, gp.w, gp.b, c.F(w.adNp), c.F(w.pp.xh), gp.g,
                     gp.beta, 0, 0};
-    plan_dw(b);
-    SQ_CK(launch_dw_f32(b, s));
+    SQ_CK(run_dw(b, s));
   }
   float* lpis = c.F(w.lpi_sums);
   PhaseScope ps15(15, rep, s);
@@ -764,6 +770,7 @@ squint_status squint_act(const squint_dims* dims, const squint_hparams* hp, cons
     return fail(SQUINT_EINVAL, "frames must be 16-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
   const squint_dims& d = *dims;
+  g_prec = d.precision;
   Layout L = make_layout(d);
   const int F = flat_dim(d), Lt = d.latent, Ha = d.actor_hidden, A = d.action_dim, P = d.proprio_dim;
   const size_t fl = sizeof(float);
@@ -854,12 +861,8 @@ squint_status squint_update(const squint_dims* dims, const squint_hparams* hp, c
     const uint8_t* sj = shifts + j * B * 4;
     const float* ej = eps + j * 2 * B * A;
     float* mj = metrics + j * 8;
-    squint_status st;
-    if (dims->precision == SQUINT_BF16)
-      st = update_one_bf16(*dims, *hp, L, reinterpret_cast<char*>(workspace) + w.bf16, *replay, ij, sj, ej, *state, mj,
-                           cm, inv_btotal, (cudaStream_t)stream, &g_err);
-    else
-      st = update_one_f32(c, *replay, ij, sj, ej, *state, mj, cm, inv_btotal, j);
+    g_prec = dims->precision;
+    squint_status st = update_one(c, *replay, ij, sj, ej, *state, mj, cm, inv_btotal, j);
     if (st != SQUINT_OK) return st;
   }
   return SQUINT_OK;

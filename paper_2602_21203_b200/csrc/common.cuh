@@ -41,6 +41,15 @@ SQ_DEV float block_sum(float v, float* red) {
 
 SQ_DEV bool is_finite(float x) { return isfinite(x); }
 
+// 1 - tanh(u)^2 without cancellation: sech^2 u = 4 t / (1 + t)^2, t = exp(-2|u|).
+// (1 - a*a with a = tanhf(u) loses ~all digits once |u| > 4; log pi's squash term and the
+// entropy shift of the C51 target depend on it.)
+SQ_DEV float sech2f(float u) {
+  const float t = expf(-2.f * fabsf(u));
+  const float d = 1.f + t;
+  return 4.f * t / (d * d);
+}
+
 }  // namespace sq
 
 namespace sq {

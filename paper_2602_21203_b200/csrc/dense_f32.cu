@@ -246,9 +246,9 @@ __global__ void __launch_bounds__(256) k_dense_f32(const __grid_constant__ Dense
         const float log_std = P.lo + 0.5f * (P.hi - P.lo) * (tl + 1.f);
         const float sd = expf(log_std);
         const float e = P.eps ? P.eps[(int64_t)r * A + d] : 0.f;
-        const float a = tanhf(fmaf(sd, e, mu));
-        P.act[(int64_t)r * A + d] = a;
-        lp += -0.5f * e * e - log_std - 0.5f * kLog2Pi - logf(1.f - a * a + kSquashEps);
+        const float u = fmaf(sd, e, mu);
+        P.act[(int64_t)r * A + d] = tanhf(u);
+        lp += -0.5f * e * e - log_std - 0.5f * kLog2Pi - logf(sech2f(u) + kSquashEps);
       }
       if (P.logp) P.logp[r] = lp;
     }
@@ -271,12 +271,13 @@ __global__ void __launch_bounds__(256) k_dense_f32(const __grid_constant__ Dense
         const float log_std = P.lo + 0.5f * (P.hi - P.lo) * (tl + 1.f);
         const float sd = expf(log_std);
         const float e = P.eps[(int64_t)r * A + d];
-        const float a = tanhf(fmaf(sd, e, mu));
-        const float om = 1.f - a * a;
+        const float u = fmaf(sd, e, mu);
+        const float a = tanhf(u);
+        const float om = sech2f(u);
         const float du = acc[i][j] * om + dlp * (2.f * a * om / (om + kSquashEps));
         const float dls = du * sd * e - dlp;
         P.out[(int64_t)r * P.ldo + d] = du;
-        P.out[(int64_t)r * P.ldo + A + d] = dls * 0.5f * (P.hi - P.lo) * (1.f - tl * tl);
+        P.out[(int64_t)r * P.ldo + A + d] = dls * 0.5f * (P.hi - P.lo) * sech2f(l);
       }
     }
     return;

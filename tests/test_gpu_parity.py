@@ -102,7 +102,7 @@ def test_act_fp32(n, sample):
 
 
 # ---- a2-a15 update, fp32 mode -----------------------------------------------------------
-def _check_update(pr, L, met_gpu, st_ref, met_ref, trace, tol_loss=1e-4, tol=1e-3):
+def _check_update(pr, L, met_gpu, st_ref, met_ref, trace, tol_loss=1e-4, tol=1e-3, check_delta=True):
     # losses and metrics
     for j in range(pr.utd):
         for k, name in enumerate(["L_Q", "L_pi", "L_alpha", "alpha", "meanQ", "entropy", "gradnorm"]):
@@ -127,7 +127,9 @@ def _check_update(pr, L, met_gpu, st_ref, met_ref, trace, tol_loss=1e-4, tol=1e-
         got = group_values(L, grp)
         for n, ref in st_ref[grp].items():
             compare(f"{grp} {n}", got[n], ref, tol)
-            if grp != "target":
+            if grp != "target" and check_delta:
+                # Delta p / lr (Q27): the pre-warmed Adam step itself, fp32 mode only -- with bf16
+                # operands m_hat / sqrt(v_hat) amplifies gradient rounding where v is tiny.
                 d_ref = ref - np.asarray(pr.vals[(grp, n)], np.float64)
                 compare(f"delta {grp} {n}", got[n] - pr.vals[(grp, n)], d_ref, 2e-2)
     for grp in ("critic", "actor"):
@@ -177,3 +179,42 @@ def test_update_deterministic_bitwise():
         outs.append((L.critic.cpu().numpy().copy(), L.actor.cpu().numpy().copy(), L.target.cpu().numpy().copy()))
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
+
+
+# ---- bf16 tensor-core mode (tcgen05), 2e-2 (BASELINE.json north_star) ------------------
+@pytest.mark.parametrize("n", [37, 256])
+def test_act_bf16(n):
+    pr = Problem("c0", seed=5)
+    L = pr.gpu_setup(precision=P.BF16)
+    frames = SI.make_frames(n, 128, seed=n)
+    prop = SI.make_proprio(n, 12, seed=n)
+    eps = np.random.default_rng(n).standard_normal((n, 6)).astype(np.float32)
+    st = O.init_state(pr.specs, pr.vals)
+    a_ref, lp_ref, _ = O.act(pr.d, pr.h, st["critic"], st["actor"], frames, prop, eps)
+    dims = P.make_dims(pr.dims, P.BF16)
+    ws = torch.zeros(P.act_workspace_bytes(dims, n), dtype=torch.uint8, device=DEV)
+    act = torch.zeros((n, 6), device=DEV)
+    lp = torch.zeros(n, device=DEV)
+    P.squint_act(dims, P.make_hparams(pr.hp), L.actor, L.critic, torch.as_tensor(frames).to(DEV),
+                 torch.as_tensor(prop).to(DEV), torch.as_tensor(eps).to(DEV), act, lp, ws)
+    torch.cuda.synchronize()
+    compare("action bf16", act.cpu().numpy(), a_ref, 2e-2)
+    compare("logp bf16", lp.cpu().numpy(), lp_ref, 2e-2)
+
+
+def _bf16_case(cfg, seed, utd=1, capacity=None, **over):
+    pr = Problem(cfg, capacity=capacity, utd=utd, seed=seed, **over)
+    L = pr.gpu_setup(precision=P.BF16)
+    met = pr.gpu_update(L)
+    trace = []
+    st_ref, met_ref = pr.oracle_update(trace)
+    _check_update(pr, L, met, st_ref, met_ref, trace, tol_loss=2e-2, tol=2e-2, check_delta=False)
+
+
+def test_update_c2_full_batch_utd2_bf16():
+    _bf16_case("c2", seed=3, utd=2, capacity=4096)
+
+
+def test_update_c2_full_batch_bf16():
+    """BASELINE configs[2] shapes at the full batch 512 (101 atoms), as bench.py runs them."""
+    _bf16_case("c2", seed=2, capacity=4096)
