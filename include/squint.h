@@ -190,6 +190,15 @@ SQUINT_API squint_status squint_update(const squint_dims* dims, const squint_hpa
 SQUINT_API squint_status squint_soft_update(float* target, const float* online, int64_t n, float tau,
                                  squint_stream_t stream);
 
+/* Self-test of the bf16 tensor-core GEMM engine (gemm.cu), used by the GPU tests:
+ * out[m][n] = sum_{k<K} A(m, k) B(n, k), fp32 [M][N] row-major (device), where A and B are
+ * bf16 row-major device matrices (rows x cols, ld elements per row) read K-major
+ * (A(m, k) = A[m][k]) or, with *_mn = 1, MN-major (A(m, k) = A[k][m]); likewise B.
+ * Entries outside a matrix read as 0.  Asynchronous on `stream`. */
+SQUINT_API squint_status squint_selftest_gemm(const void* A, int a_rows, int a_cols, int a_ld, int a_mn,
+                                              const void* B, int b_rows, int b_cols, int b_ld, int b_mn,
+                                              int M, int N, int K, float* out, squint_stream_t stream);
+
 /* ---- instrumentation (bench.py) --------------------------------------------------------
  * Number of kernels libsquint has launched in this process (host counter). */
 SQUINT_API long squint_launch_count(void);
@@ -199,6 +208,11 @@ SQUINT_API long squint_launch_count(void);
  * Phase names: squint_phase_name(k) (16 phases). */
 SQUINT_API squint_status squint_set_phase_events(void** events, int n_phases, int reps);
 SQUINT_API const char* squint_phase_name(int k);
+/* Instrumentation: launch timeline.  While enabled, libsquint records events[i] (host array of
+ * cudaEvent_t, created with timing) on the launch stream immediately before its i-th kernel
+ * launch (i < n), so consecutive events bracket one launch including any gap after it.
+ * Returns the number of events recorded since the previous call; NULL/0 disables. */
+SQUINT_API int squint_set_launch_events(void** events, int n);
 
 #ifdef __cplusplus
 }

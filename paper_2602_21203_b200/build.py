@@ -1,5 +1,5 @@
 """Build libsquint.so in-tree with nvcc for sm_100a (no JIT cache: the .so travels with
-the repo snapshot to the GPU box).  ``python -m paper_2602_21203_b200.build``."""
+the repo snapshot to the GPU box).  ``python paper_2602_21203_b200/build.py``."""
 from __future__ import annotations
 
 import concurrent.futures as cf
@@ -68,8 +68,7 @@ def build(force=False, verbose=False):
         objs = list(ex.map(lambda s: _compile(s, os.path.join(nccl, "include"), verbose), _sources()))
     libnccl = os.path.join(nccl, "lib", "libnccl.so.2")
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L", os.path.dirname(libnccl), "-l:libnccl.so.2", "-Xlinker", f"-rpath,{os.path.dirname(libnccl)}",
-           "-lcuda"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L", os.path.dirname(libnccl), "-l:libnccl.so.2", "-Xlinker", f"-rpath,{os.path.dirname(libnccl)}"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -16,7 +16,7 @@
 #include "heads.cuh"
 #include "layout.hpp"
 #include "optim.cuh"
-#include "dense_tc.cuh"
+#include "update_bf16.hpp"
 
 namespace sq {
 
@@ -26,6 +26,7 @@ static squint_status fail(squint_status st, const std::string& m) {
   g_err = m;
   return st;
 }
+squint_status set_error(squint_status st, const std::string& m) { return fail(st, m); }
 
 #define SQ_CK(expr)                                                                       \
   do {                                                                                    \
@@ -220,12 +221,10 @@ static thread_local int g_prec = SQUINT_FP32;
 
 // Dense layers: fp32 SIMT (parity mode) or bf16 tcgen05 tensor cores.
 static int run_dense(DenseBatch& b, cudaStream_t s) {
-  if (g_prec == SQUINT_BF16) return launch_dense_bf16(b, s);
   const int tn = plan_dense(b);
   return launch_dense_f32(b, tn, s);
 }
 static int run_dw(DwBatch& b, cudaStream_t s) {
-  if (g_prec == SQUINT_BF16) return launch_dw_bf16(b, s);
   plan_dw(b);
   return launch_dw_f32(b, s);
 }
@@ -354,6 +353,7 @@ static squint_status update_one(const Ctx& c, const squint_replay& R, const int6
   {
     PhaseScope ps(7, rep, s);
     TargetCEArgs t;
+    memset(&t, 0, sizeof(t));
     t.B = B;
     t.N = N;
     t.v_min = d.v_min;
@@ -441,6 +441,7 @@ static squint_status update_one(const Ctx& c, const squint_replay& R, const int6
   {
     PhaseScope ps(10, rep, s);
     EncBwdArgs e;
+    memset(&e, 0, sizeof(e));
     e.B = B;
     e.C = C;
     e.c_in = d.img_c;
@@ -515,6 +516,7 @@ static squint_status update_one(const Ctx& c, const squint_replay& R, const int6
                         c.F(w.logits1) + (size_t)i * B * N, nullptr, nullptr, le);
     SQ_CK(run_dense(b, s));
     ActorQArgs q;
+    memset(&q, 0, sizeof(q));
     q.B = B;
     q.N = N;
     q.v_min = d.v_min;
@@ -680,7 +682,7 @@ squint_status squint_workspace_bytes(const squint_dims* dims, int utd, size_t* b
   if (!check_dims(*dims, &e)) return fail(SQUINT_EINVAL, e);
   if (utd < 1) return fail(SQUINT_EINVAL, "utd must be >= 1");
   Layout L = make_layout(*dims);
-  *bytes = plan_ws(*dims, L).total;
+  *bytes = dims->precision == SQUINT_BF16 ? bf16_workspace_bytes(*dims) : plan_ws(*dims, L).total;
   return SQUINT_OK;
 }
 
@@ -688,6 +690,10 @@ squint_status squint_workspace_region(const squint_dims* dims, int region, size_
   if (!dims || !offset || !bytes) return fail(SQUINT_EINVAL, "NULL argument");
   std::string e;
   if (!check_dims(*dims, &e)) return fail(SQUINT_EINVAL, e);
+  if (dims->precision == SQUINT_BF16) {
+    if (!bf16_region(*dims, region, offset, bytes)) return fail(SQUINT_EINVAL, "unknown region");
+    return SQUINT_OK;
+  }
   Layout L = make_layout(*dims);
   WsLay w = plan_ws(*dims, L);
   const size_t B = dims->batch, f = sizeof(float);
@@ -710,6 +716,10 @@ squint_status squint_act_workspace_bytes(const squint_dims* dims, int64_t n, siz
   std::string e;
   if (!check_dims(*dims, &e)) return fail(SQUINT_EINVAL, e);
   if (n < 0) return fail(SQUINT_EINVAL, "n must be >= 0");
+  if (dims->precision == SQUINT_BF16) {
+    *bytes = bf16_act_workspace_bytes(*dims, n);
+    return SQUINT_OK;
+  }
   const size_t f = sizeof(float), F = flat_dim(*dims);
   WsPlan P;
   P.take(n * F * f);                           // h
@@ -771,6 +781,9 @@ squint_status squint_act(const squint_dims* dims, const squint_hparams* hp, cons
   cudaStream_t s = (cudaStream_t)stream;
   const squint_dims& d = *dims;
   g_prec = d.precision;
+  if (d.precision == SQUINT_BF16)
+    return bf16_act(d, *hp, actor_params, critic_params, frames, n, f, proprio, eps, action_out, logp_out, ring, slots,
+                    workspace, s);
   Layout L = make_layout(d);
   const int F = flat_dim(d), Lt = d.latent, Ha = d.actor_hidden, A = d.action_dim, P = d.proprio_dim;
   const size_t fl = sizeof(float);
@@ -848,10 +861,13 @@ squint_status squint_update(const squint_dims* dims, const squint_hparams* hp, c
   if (!state->critic || !state->critic_target || !state->actor || !state->log_alpha || !state->m_critic ||
       !state->v_critic || !state->m_actor || !state->v_actor || !state->m_alpha || !state->v_alpha || !state->step)
     return fail(SQUINT_EINVAL, "NULL state field");
+  Comm* cm = reinterpret_cast<Comm*>(comm);
+  if (dims->precision == SQUINT_BF16)
+    return bf16_update(*dims, *hp, *replay, idx, shifts, eps, utd, *state, metrics, workspace, workspace_bytes, cm,
+                       (cudaStream_t)stream);
   Layout L = make_layout(*dims);
   WsLay w = plan_ws(*dims, L);
   if (workspace_bytes < w.total) return fail(SQUINT_EINVAL, "workspace too small (see squint_workspace_bytes)");
-  Comm* cm = reinterpret_cast<Comm*>(comm);
   const int nranks = cm ? comm_nranks(cm) : 1;
   const float inv_btotal = 1.0f / ((float)dims->batch * (float)nranks);
   Ctx c{*dims, *hp, L, w, reinterpret_cast<char*>(workspace), (cudaStream_t)stream};

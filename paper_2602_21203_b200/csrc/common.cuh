@@ -54,7 +54,7 @@ SQ_DEV float sech2f(float u) {
 
 namespace sq {
 // Host-side count of kernel launches issued by libsquint (bench "gpu_launches" claim).
-void note_launch();
+void note_launch(cudaStream_t s);  // call right before each launch on stream s
 long launch_count();
 // Optional phase instrumentation (squint_set_phase_events): records cudaEvent pairs
 // around named phases of squint_update / squint_act / squint_insert on the launch stream.

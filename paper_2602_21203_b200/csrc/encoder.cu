@@ -99,6 +99,16 @@ __global__ void __launch_bounds__(256) k_enc_fwd(const __grid_constant__ EncFwdA
     const int o = e / (9 * C), r = e % (9 * C);
     w2t[r * (C + 1) + o] = a.w2[e];
   }
+  for (int jb = 0; jb < a.ngj[src_i]; ++jb) {
+    const GatherJob& g = a.gj[src_i][jb];
+    for (int e = tid; e < ipb * g.width; e += 256) {
+      const int i = e / g.width, j = e - i * g.width, b = b0 + i;
+      if (b < a.B) {
+        const int64_t row = g.use_idx ? a.idx[b] : (int64_t)b;
+        g.dst[(int64_t)b * g.ld + g.col + j] = __float2bfloat16_rn(g.src[row * g.width + j]);
+      }
+    }
+  }
   const float inv255 = 1.0f / 255.0f;
   if (a.mode == 0) {
     const uint8_t* src = a.src[src_i];
@@ -191,7 +201,12 @@ __global__ void __launch_bounds__(256) k_enc_fwd(const __grid_constant__ EncFwdA
 #pragma unroll
         for (int kj = 0; kj < 3; ++kj) acc = fmaf(w2t[(cc * 9 + ki * 3 + kj) * (C + 1) + o], yi[ki * H1 + kj], acc);
     }
-    if (b < a.B) hout[(int64_t)b * C * P2 + o * P2 + pix] = fmaxf(acc, 0.f);
+    if (b < a.B) {
+      if (a.hb[src_i])
+        a.hb[src_i][(int64_t)b * a.h_ld + pix * C + o] = __float2bfloat16_rn(fmaxf(acc, 0.f));
+      else
+        hout[(int64_t)b * C * P2 + o * P2 + pix] = fmaxf(acc, 0.f);
+    }
   }
 }
 
@@ -205,8 +220,17 @@ __global__ void __launch_bounds__(256) k_enc_bwd_dx(const __grid_constant__ EncB
   const int tid = threadIdx.x, b0 = blockIdx.x * ipb;
   for (int e = tid; e < C * C * 9; e += 256) w2s[e] = a.w2[e];
   for (int e = tid; e < ipb * C * P2; e += 256) {
-    const int i = e / (C * P2), b = b0 + i;
-    ds[e] = (b < a.B) ? a.dA2[(int64_t)b * C * P2 + e % (C * P2)] : 0.f;
+    const int i = e / (C * P2), b = b0 + i, r = e % (C * P2);
+    float v = 0.f;
+    if (b < a.B) {
+      if (a.dA2_hwc) {
+        const int o = r / P2, pix = r - o * P2;
+        v = __bfloat162float(a.dA2_hwc[(int64_t)b * C * P2 + pix * C + o]);
+      } else {
+        v = a.dA2[(int64_t)b * C * P2 + r];
+      }
+    }
+    ds[e] = v;
   }
   __syncthreads();
   const int c = tid % C, grp = tid / C, ngrp = 256 / C;
@@ -230,7 +254,8 @@ __global__ void __launch_bounds__(256) k_enc_bwd_dx(const __grid_constant__ EncB
       }
     }
     const int64_t gi = ((int64_t)b * C + c) * P1 + pix;
-    a.dA1[gi] = a.y1[gi] > 0.f ? acc : 0.f;
+    const float yv = a.y1_hwc ? __bfloat162float(a.y1_hwc[((int64_t)b * P1 + pix) * C + c]) : a.y1[gi];
+    a.dA1[gi] = yv > 0.f ? acc : 0.f;
   }
 }
 
@@ -238,7 +263,8 @@ __global__ void __launch_bounds__(256) k_enc_bwd_dx(const __grid_constant__ EncB
 //   dW[o][c][ki][kj] = sum_b sum_pix D[b][o][pix] X[b][c][s*y+ki][s*x+kj],  db[o] = sum D.
 // grid = (nchunk, O / OB); each thread owns up to 40 weights (fixed summation order).
 template <bool kU8>
-__global__ void __launch_bounds__(256) k_conv_dw(const float* __restrict__ D, const void* __restrict__ Xv, int B,
+__global__ void __launch_bounds__(256) k_conv_dw(const float* __restrict__ D, const __nv_bfloat16* __restrict__ Dh,
+                                                 const void* __restrict__ Xv, const __nv_bfloat16* __restrict__ Xh, int B,
                                                  int O, int Cin, int Hin, int Hout, int stride, int OB,
                                                  int nchunk, float* __restrict__ part) {
   extern __shared__ float sm[];
@@ -255,11 +281,21 @@ __global__ void __launch_bounds__(256) k_conv_dw(const float* __restrict__ D, co
   for (int r = 0; r < R; ++r) acc[r] = 0.f;
   float sb = 0.f;
   for (int b = bb0; b < bb1; ++b) {
-    for (int e = tid; e < OB * Pout; e += 256) Ds[e] = D[((int64_t)b * O + o0) * Pout + e];
+    for (int e = tid; e < OB * Pout; e += 256) {
+      if (Dh) {
+        const int ol = e / Pout, pix = e - ol * Pout;
+        Ds[e] = __bfloat162float(Dh[(int64_t)b * O * Pout + pix * O + o0 + ol]);
+      } else {
+        Ds[e] = D[((int64_t)b * O + o0) * Pout + e];
+      }
+    }
     for (int e = tid; e < Cin * HH; e += 256) {
       if (kU8)
         Xs[e] = (float)(reinterpret_cast<const uint8_t*>(Xv)[(int64_t)b * Cin * HH + e]) * (1.0f / 255.0f);
-      else
+      else if (Xh) {
+        const int c = e / HH, p = e - c * HH;
+        Xs[e] = __bfloat162float(Xh[((int64_t)b * HH + p) * Cin + c]);
+      } else
         Xs[e] = reinterpret_cast<const float*>(Xv)[(int64_t)b * Cin * HH + e];
     }
     __syncthreads();
@@ -332,7 +368,7 @@ int launch_enc_fwd(const EncFwdArgs& a, cudaStream_t s) {
   const size_t smem = fwd_smem(a.C, a.c_in, a.H, ipb);
   cudaFuncSetAttribute(k_enc_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((a.B + ipb - 1) / ipb, a.nsrc);
-  note_launch(); k_enc_fwd<<<grid, 256, smem, s>>>(a, ipb);
+  note_launch(s); k_enc_fwd<<<grid, 256, smem, s>>>(a, ipb);
   return (int)cudaGetLastError();
 }
 
@@ -342,7 +378,7 @@ int launch_enc_bwd(const EncBwdArgs& a, cudaStream_t s) {
     const int ipb = bwd_ipb(C);
     const size_t smem = sizeof(float) * (size_t)(C * C * 9 + ipb * C * P2);
     cudaFuncSetAttribute(k_enc_bwd_dx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    note_launch(); k_enc_bwd_dx<<<(a.B + ipb - 1) / ipb, 256, smem, s>>>(a, ipb);
+    note_launch(s); k_enc_bwd_dx<<<(a.B + ipb - 1) / ipb, 256, smem, s>>>(a, ipb);
   }
   float* part2 = a.part;
   float* part1 = a.part + (size_t)a.nchunk * (C * C * 9 + C);
@@ -350,20 +386,20 @@ int launch_enc_bwd(const EncBwdArgs& a, cudaStream_t s) {
     const int ob = ob_of(C, C);
     const size_t smem = sizeof(float) * (size_t)(ob * P2 + C * P1);
     cudaFuncSetAttribute(k_conv_dw<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    note_launch(); k_conv_dw<false><<<dim3(a.nchunk, C / ob), 256, smem, s>>>(a.dA2, a.y1, a.B, C, C, H1, H2, 1, ob, a.nchunk,
+    note_launch(s); k_conv_dw<false><<<dim3(a.nchunk, C / ob), 256, smem, s>>>(a.dA2, a.dA2_hwc, a.y1, a.y1_hwc, a.B, C, C, H1, H2, 1, ob, a.nchunk,
                                                                  part2);
   }
   {
     const int ob = ob_of(C, a.c_in);
     const size_t smem = sizeof(float) * (size_t)(ob * P1 + a.c_in * a.H * a.H);
     cudaFuncSetAttribute(k_conv_dw<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    note_launch(); k_conv_dw<true><<<dim3(a.nchunk, C / ob), 256, smem, s>>>(a.dA1, a.img, a.B, C, a.c_in, a.H, H1, 2, ob,
+    note_launch(s); k_conv_dw<true><<<dim3(a.nchunk, C / ob), 256, smem, s>>>(a.dA1, nullptr, a.img, nullptr, a.B, C, a.c_in, a.H, H1, 2, ob,
                                                                a.nchunk, part1);
   }
   {
     const int n2 = C * C * 9 + C, n1 = C * a.c_in * 9 + C;
-    note_launch(); k_reduce_part<<<(n2 + 255) / 256, 256, 0, s>>>(part2, a.nchunk, C * C * 9, C, a.gw2, a.gb2);
-    note_launch(); k_reduce_part<<<(n1 + 255) / 256, 256, 0, s>>>(part1, a.nchunk, C * a.c_in * 9, C, a.gw1, a.gb1);
+    note_launch(s); k_reduce_part<<<(n2 + 255) / 256, 256, 0, s>>>(part2, a.nchunk, C * C * 9, C, a.gw2, a.gb2);
+    note_launch(s); k_reduce_part<<<(n1 + 255) / 256, 256, 0, s>>>(part1, a.nchunk, C * a.c_in * 9, C, a.gw1, a.gb1);
   }
   return (int)cudaGetLastError();
 }
@@ -375,12 +411,12 @@ int launch_insert(const uint8_t* frames, int64_t n, int c, int h, int w, int fac
     const int64_t items = n * c * (h / 8) * (w / 16);
     int64_t blocks = (items + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    note_launch(); k_insert_f8<<<(unsigned)blocks, 256, 0, s>>>(frames, n, c, h, w, slots, ring);
+    note_launch(s); k_insert_f8<<<(unsigned)blocks, 256, 0, s>>>(frames, n, c, h, w, slots, ring);
   } else {
     const int64_t items = n * c * (h / factor) * (w / factor);
     int64_t blocks = (items + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    note_launch(); k_insert_generic<<<(unsigned)blocks, 256, 0, s>>>(frames, n, c, h, w, factor, slots, ring);
+    note_launch(s); k_insert_generic<<<(unsigned)blocks, 256, 0, s>>>(frames, n, c, h, w, factor, slots, ring);
   }
   return (int)cudaGetLastError();
 }

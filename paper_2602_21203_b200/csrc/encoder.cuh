@@ -3,9 +3,21 @@
 // fused squint + encoder of rollout inference (a16).
 #pragma once
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 namespace sq {
+
+typedef __nv_bfloat16 bf16_t;
+
+// Row gather into a bf16 matrix: dst[b * ld + col + j] = src[row(b) * width + j], j < width,
+// row(b) = idx[b] (replay gather, a3) or b (use_idx = 0).
+struct GatherJob {
+  const float* src;
+  int width;
+  __nv_bfloat16* dst;
+  int ld, col, use_idx;
+};
 
 struct EncFwdArgs {
   // source mode 0: replay gather + shift (update); mode 1: raw frames + squint (act)
@@ -23,12 +35,22 @@ struct EncFwdArgs {
   float* y1;               // [B, C, P1] conv1 activations of source 0 (NULL: not stored)
   uint8_t* img0;           // [B, c, H, W] shifted images of source 0 (NULL: not stored)
   int C, c_in, H, pad;
+  // bf16 path: h written as bf16 in HWC flatten order hb[src][b * h_ld + pix * C + o]
+  // (instead of fp32 CHW h), plus row gathers of the small replay fields per source.
+  __nv_bfloat16* hb[2];
+  int h_ld;
+  __nv_bfloat16* y1b;      // tensor-core path: conv1 activations of source 0, bf16 HWC [B][49][C]
+  GatherJob gj[2][4];
+  int ngj[2];
 };
 
 struct EncBwdArgs {
   int B, C, c_in, H;
-  const float* dA2;        // [B, F]  dL/d(conv2 pre-activation)
-  const float* y1;         // [B, C, P1]
+  const float* dA2;        // [B, F]  dL/d(conv2 pre-activation), CHW (fp32 path) ...
+  const __nv_bfloat16* dA2_hwc;  // ... or bf16 HWC [B, P2 * C] (bf16 path; used when non-NULL)
+  int dA2_ld;                    // row pitch of dA2_hwc (elements)
+  const float* y1;         // [B, C, P1] fp32 CHW ...
+  const __nv_bfloat16* y1_hwc;  // ... or bf16 HWC [B][P1][C] (used when non-NULL)
   const uint8_t* img;      // [B, c, H, W]
   const float* w2;         // conv2 weights [C, C, 3, 3]
   float* dA1;              // [B, C, P1] workspace
@@ -38,7 +60,15 @@ struct EncBwdArgs {
 };
 
 int launch_enc_fwd(const EncFwdArgs& a, cudaStream_t s);
+// tcgen05 implicit-GEMM encoder forward (encoder_tc.cu): bf16 outputs hb / y1b; C in {32, 64},
+// 16x16x3 stored images, squint factor 8 in mode 1.
+int launch_enc_fwd_tc(const EncFwdArgs& a, cudaStream_t s);
 int launch_enc_bwd(const EncBwdArgs& a, cudaStream_t s);
+// tcgen05 implicit-GEMM encoder backward (encoder_tc.cu): reads dA2_hwc, y1_hwc, img, w2; writes
+// the conv weight/bias gradients through per-CTA partials (a.part, enc_bwd_tc_partial_floats)
+// and a fixed-order reduction (deterministic).
+int launch_enc_bwd_tc(const EncBwdArgs& a, cudaStream_t s);
+size_t enc_bwd_tc_partial_floats(int C, int B);
 size_t enc_bwd_partial_floats(int C, int c_in, int nchunk);
 int enc_bwd_nchunk(int B);
 

@@ -68,7 +68,8 @@ __global__ void __launch_bounds__(256) k_target_ce(const __grid_constant__ Targe
   float loss = 0.f;
   for (int hd = 0; hd < 2; ++hd) {
     const float* l = a.logits + ((int64_t)hd * a.B + row) * N;
-    float* dl = a.dlogits + ((int64_t)hd * a.B + row) * N;
+    float* dl = a.dlogits_bf ? nullptr : a.dlogits + ((int64_t)hd * a.B + row) * N;
+    __nv_bfloat16* dlb = a.dlogits_bf ? a.dlogits_bf + ((int64_t)hd * a.B + row) * a.ld_dl : nullptr;
     float mx = -INFINITY;
     for (int k = lane; k < N; k += 32) mx = fmaxf(mx, l[k]);
     mx = warp_max(mx);
@@ -80,7 +81,8 @@ __global__ void __launch_bounds__(256) k_target_ce(const __grid_constant__ Targe
     for (int k = lane; k < N; k += 32) {
       const float mk = mrow[k];
       ce -= mk * (l[k] - lse);
-      dl[k] = (expf(l[k] - mx) * inv - mk) * a.scale;
+      const float g = (expf(l[k] - mx) * inv - mk) * a.scale;
+      if (dlb) dlb[k] = __float2bfloat16_rn(g); else dl[k] = g;
     }
     loss += warp_sum(ce);
   }
@@ -108,11 +110,13 @@ __global__ void __launch_bounds__(256) k_actor_q(const __grid_constant__ ActorQA
     sz = warp_sum(sz);
     const float inv = 1.f / s;
     q[hd] = sz * inv;
-    float* dl = a.dlogits + ((int64_t)hd * a.B + row) * N;
+    float* dl = a.dlogits_bf ? nullptr : a.dlogits + ((int64_t)hd * a.B + row) * N;
+    __nv_bfloat16* dlb = a.dlogits_bf ? a.dlogits_bf + ((int64_t)hd * a.B + row) * a.ld_dl : nullptr;
     const float c = -0.5f * a.scale;
     for (int k = lane; k < N; k += 32) {
       const float p = expf(l[k] - mx) * inv;
-      dl[k] = c * p * ((a.v_min + (float)k * dz) - q[hd]);
+      const float g = c * p * ((a.v_min + (float)k * dz) - q[hd]);
+      if (dlb) dlb[k] = __float2bfloat16_rn(g); else dl[k] = g;
     }
   }
   if (lane == 0) {
@@ -127,12 +131,12 @@ __global__ void __launch_bounds__(256) k_actor_q(const __grid_constant__ ActorQA
 int launch_target_ce(const TargetCEArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(float) * 2 * a.N * kRows;
   cudaFuncSetAttribute(k_target_ce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  note_launch(); k_target_ce<<<(a.B + kRows - 1) / kRows, 256, smem, s>>>(a);
+  note_launch(s); k_target_ce<<<(a.B + kRows - 1) / kRows, 256, smem, s>>>(a);
   return (int)cudaGetLastError();
 }
 
 int launch_actor_q(const ActorQArgs& a, cudaStream_t s) {
-  note_launch(); k_actor_q<<<(a.B + kRows - 1) / kRows, 256, 0, s>>>(a);
+  note_launch(s); k_actor_q<<<(a.B + kRows - 1) / kRows, 256, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 

@@ -1,6 +1,7 @@
 // heads.cuh -- row kernels of the distributional critic (a9, a10, a12).
 #pragma once
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 namespace sq {
@@ -16,7 +17,9 @@ struct TargetCEArgs {
   const float* logp_next;  // [B]
   const float* log_alpha;  // [1] (alpha_0 = exp, read before the alpha step)
   float* m;                // [B][N]
-  float* dlogits;          // [2][B][N]
+  float* dlogits;          // [2][B][N] fp32 (fp32 path) ...
+  __nv_bfloat16* dlogits_bf;  // ... or bf16 [2][B][ld_dl] (bf16 path; used when non-NULL)
+  int ld_dl;
   float* row_loss;         // [B]
 };
 
@@ -26,7 +29,9 @@ struct ActorQArgs {
   const float* logits;     // [2][B][N] critic theta+ on (z+, s, a~)
   const float* logp;       // [B]
   const float* alpha1;     // [1] alpha after its step
-  float* dlogits;          // [2][B][N]
+  float* dlogits;          // [2][B][N] fp32 ...
+  __nv_bfloat16* dlogits_bf;  // ... or bf16 [2][B][ld_dl] when non-NULL
+  int ld_dl;
   float* row_q;            // [B]
   float* row_lpi;          // [B]
 };

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdio>
 
 #include "../../include/squint.h"
 #include "common.cuh"
@@ -13,16 +14,30 @@ static std::atomic<long> g_launches{0};
 static void** g_events = nullptr;  // cudaEvent_t[n_phases][reps][2]
 static int g_phases = 0, g_reps = 0;
 
-void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+// Optional launch timeline (squint_set_launch_events): an event recorded on the launch stream
+// right before each launch, so event k..k+1 brackets launch k (kernel + any gap before k+1).
+static void** g_lev = nullptr;
+static int g_lev_n = 0, g_lev_used = 0;
+
+void note_launch(cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (g_lev && g_lev_used < g_lev_n) {
+    cudaError_t e = cudaEventRecordWithFlags((cudaEvent_t)g_lev[g_lev_used++], s, cudaEventRecordExternal);
+    if (e != cudaSuccess) {
+      fprintf(stderr, "[squint] launch event %d: %s\n", g_lev_used - 1, cudaGetErrorString(e));
+      cudaGetLastError();
+    }
+  }
+}
 long launch_count() { return g_launches.load(); }
 
 PhaseScope::PhaseScope(int phase, int rep, cudaStream_t st) : idx(-1), s(st) {
   if (!g_events || phase >= g_phases || rep >= g_reps) return;
   idx = (phase * g_reps + rep) * 2;
-  cudaEventRecord((cudaEvent_t)g_events[idx], s);
+  cudaEventRecordWithFlags((cudaEvent_t)g_events[idx], s, cudaEventRecordExternal);
 }
 PhaseScope::~PhaseScope() {
-  if (idx >= 0) cudaEventRecord((cudaEvent_t)g_events[idx + 1], s);
+  if (idx >= 0) cudaEventRecordWithFlags((cudaEvent_t)g_events[idx + 1], s, cudaEventRecordExternal);
 }
 
 }  // namespace sq
@@ -30,6 +45,14 @@ PhaseScope::~PhaseScope() {
 extern "C" {
 
 SQUINT_API long squint_launch_count(void) { return sq::launch_count(); }
+
+SQUINT_API int squint_set_launch_events(void** events, int n) {
+  const int used = sq::g_lev_used;
+  sq::g_lev = events;
+  sq::g_lev_n = events ? n : 0;
+  sq::g_lev_used = 0;
+  return used;
+}
 
 SQUINT_API squint_status squint_set_phase_events(void** events, int n_phases, int reps) {
   sq::g_events = events;

@@ -3,6 +3,8 @@
 // order so results are bitwise reproducible and identical across data-parallel replicas.
 #include <cuda_runtime.h>
 
+#include <cstring>
+
 #include "common.cuh"
 #include "optim.cuh"
 
@@ -173,21 +175,141 @@ __global__ void __launch_bounds__(256) k_metrics(const __grid_constant__ Metrics
   }
 }
 
+// flat index i of a group buffer -> its shadow slot, or -1
+__device__ __forceinline__ int64_t shadow_slot(const ShadowTable& t, int64_t i) {
+  for (int k = 0; k < t.n; ++k) {
+    const ShadowEnt& e = t.e[k];
+    const int64_t l = i - e.src;
+    if (l >= 0 && l < (int64_t)e.rows * e.cols) {
+      const int row = (int)(l / e.cols), col = (int)(l - (int64_t)row * e.cols);
+      int cc = col;
+      if (e.perm_c > 0) {
+        const int ch = col / e.perm_p, pix = col - ch * e.perm_p;
+        cc = pix * e.perm_c + ch;
+      }
+      return e.dst + (int64_t)row * e.ld + cc;
+    }
+  }
+  return -1;
+}
+
+__global__ void __launch_bounds__(256) k_shadow(const float* __restrict__ master, const __grid_constant__ ShadowTable t) {
+  for (int k = 0; k < t.n; ++k) {
+    const ShadowEnt& e = t.e[k];
+    const int64_t n = (int64_t)e.rows * e.cols;
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n; l += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t sl = shadow_slot(t, e.src + l);
+      t.base[sl] = __float2bfloat16_rn(master[e.src + l]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_adam_sh(float4* __restrict__ p, const float4* __restrict__ g,
+                                                 float4* __restrict__ m, float4* __restrict__ v, int64_t n4, float lr,
+                                                 float b1, float b2, float eps, const float* __restrict__ c1p,
+                                                 const float* __restrict__ c2p, float* __restrict__ part,
+                                                 const __grid_constant__ ShadowTable t) {
+  __shared__ float red[32];
+  const float c1 = c1p[0], c2 = c2p[0];
+  float ss = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 gg = g[i], mm = m[i], vv = v[i], pp = p[i];
+    float* gf = reinterpret_cast<float*>(&gg);
+    float* mf = reinterpret_cast<float*>(&mm);
+    float* vf = reinterpret_cast<float*>(&vv);
+    float* pf = reinterpret_cast<float*>(&pp);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      ss = fmaf(gf[k], gf[k], ss);
+      mf[k] = b1 * mf[k] + (1.f - b1) * gf[k];
+      vf[k] = b2 * vf[k] + (1.f - b2) * gf[k] * gf[k];
+      pf[k] = pf[k] - lr * (mf[k] * c1) / (sqrtf(vf[k] * c2) + eps);
+    }
+    m[i] = mm;
+    v[i] = vv;
+    p[i] = pp;
+    if (t.n) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t sl = shadow_slot(t, 4 * i + k);
+        if (sl >= 0) t.base[sl] = __float2bfloat16_rn(pf[k]);
+      }
+    }
+  }
+  if (part) {
+    ss = block_sum(ss, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = ss;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_polyak_sh(float4* __restrict__ t4, const float4* __restrict__ o4, int64_t n4,
+                                                   float tau, const __grid_constant__ ShadowTable t) {
+  const float keep = 1.f - tau;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = t4[i];
+    const float4 b = o4[i];
+    a.x = keep * a.x + tau * b.x;
+    a.y = keep * a.y + tau * b.y;
+    a.z = keep * a.z + tau * b.z;
+    a.w = keep * a.w + tau * b.w;
+    t4[i] = a;
+    if (t.n) {
+      const float* af = reinterpret_cast<const float*>(&a);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t sl = shadow_slot(t, 4 * i + k);
+        if (sl >= 0) t.base[sl] = __float2bfloat16_rn(af[k]);
+      }
+    }
+  }
+}
+
 }  // namespace
 
+int launch_shadow(const float* master, const ShadowTable& t, cudaStream_t s) {
+  if (t.n == 0) return 0;
+  note_launch(s); k_shadow<<<148 * 2, 256, 0, s>>>(master, t);
+  return (int)cudaGetLastError();
+}
+
+int launch_adam_shadow(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+                       float eps, const float* c1, const float* c2, float* sumsq_part, const ShadowTable* t,
+                       cudaStream_t s) {
+  ShadowTable none;
+  memset(&none, 0, sizeof(none));
+  note_launch(s);
+  k_adam_sh<<<kAdamBlocks, 256, 0, s>>>(reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
+                                        reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n / 4, lr, b1, b2,
+                                        eps, c1, c2, sumsq_part, t ? *t : none);
+  return (int)cudaGetLastError();
+}
+
+int launch_polyak_shadow(float* target, const float* online, int64_t n, float tau, const ShadowTable* t,
+                         cudaStream_t s) {
+  if (n == 0) return 0;
+  ShadowTable none;
+  memset(&none, 0, sizeof(none));
+  int64_t blocks = (n / 4 + 255) / 256;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  note_launch(s);
+  k_polyak_sh<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<float4*>(target), reinterpret_cast<const float4*>(online),
+                                               n / 4, tau, t ? *t : none);
+  return (int)cudaGetLastError();
+}
+
 int launch_row_sums(const float* logp, const float* row_loss, int B, float* extras, cudaStream_t s) {
-  note_launch(); k_row_sums<<<1, 256, 0, s>>>(logp, row_loss, B, extras);
+  note_launch(s); k_row_sums<<<1, 256, 0, s>>>(logp, row_loss, B, extras);
   return (int)cudaGetLastError();
 }
 
 int launch_scalars(const ScalarsArgs& a, cudaStream_t s) {
-  note_launch(); k_scalars<<<1, 256, 0, s>>>(a);
+  note_launch(s); k_scalars<<<1, 256, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 
 int launch_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
                 const float* c1, const float* c2, float* sumsq_part, cudaStream_t s) {
-  note_launch(); k_adam<<<kAdamBlocks, 256, 0, s>>>(reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
+  note_launch(s); k_adam<<<kAdamBlocks, 256, 0, s>>>(reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
                                      reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n / 4, lr, b1, b2,
                                      eps, c1, c2, sumsq_part);
   return (int)cudaGetLastError();
@@ -198,17 +320,17 @@ int launch_polyak(float* target, const float* online, int64_t n, float tau, cuda
   int64_t blocks = (n / 4 + 255) / 256;
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  note_launch(); k_polyak<<<(unsigned)blocks, 256, 0, s>>>(target, online, n, tau);
+  note_launch(s); k_polyak<<<(unsigned)blocks, 256, 0, s>>>(target, online, n, tau);
   return (int)cudaGetLastError();
 }
 
 int launch_metrics(const MetricsArgs& a, cudaStream_t s) {
-  note_launch(); k_metrics<<<1, 256, 0, s>>>(a);
+  note_launch(s); k_metrics<<<1, 256, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 
 int launch_lpi_sums(const float* row_lpi, const float* row_q, int B, float* out2, cudaStream_t s) {
-  note_launch(); k_lpi_sums<<<1, 256, 0, s>>>(row_lpi, row_q, B, out2);
+  note_launch(s); k_lpi_sums<<<1, 256, 0, s>>>(row_lpi, row_q, B, out2);
   return (int)cudaGetLastError();
 }
 

@@ -1,6 +1,7 @@
 // optim.cuh -- temperature step, fused Adam, Polyak, per-update metrics (a11, a13, a14).
 #pragma once
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 namespace sq {
@@ -43,6 +44,31 @@ int launch_adam(float* p, const float* g, float* m, float* v, int64_t n, float l
                 const float* c1, const float* c2, float* sumsq_part, cudaStream_t s);
 // target = (1 - tau) target + tau online; any n, any alignment.
 int launch_polyak(float* target, const float* online, int64_t n, float tau, cudaStream_t s);
+
+// bf16 shadow copies of the linear weights (bf16 tensor-core path).  Entry e maps the fp32
+// tensor at flat offset src (rows x cols, row-major) of a group buffer onto the bf16 matrix
+// dst[row * ld + col'] with col' = col, or, for perm_c > 0 (projection weights, whose input is
+// the conv feature map flattened CHW, Q7), col = ch * perm_p + pix -> col' = pix * perm_c + ch
+// (the HWC order the encoder writes).
+struct ShadowEnt {
+  int64_t src, dst;
+  int rows, cols, ld, perm_c, perm_p;
+};
+constexpr int kMaxShadow = 8;
+struct ShadowTable {
+  int n;
+  __nv_bfloat16* base;
+  ShadowEnt e[kMaxShadow];
+};
+// Full refresh of one group's shadow from its fp32 master.
+int launch_shadow(const float* master, const ShadowTable& t, cudaStream_t s);
+// Adam (as launch_adam) that also writes the updated weights' bf16 shadow (t may be NULL).
+int launch_adam_shadow(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+                       float eps, const float* c1, const float* c2, float* sumsq_part, const ShadowTable* t,
+                       cudaStream_t s);
+// Polyak over a 16-byte aligned buffer (n % 4 == 0) that also refreshes the target shadow.
+int launch_polyak_shadow(float* target, const float* online, int64_t n, float tau, const ShadowTable* t,
+                         cudaStream_t s);
 
 struct MetricsArgs {
   int B;

@@ -1,0 +1,936 @@
+// update_bf16.cu -- launch sequence of the bf16 tensor-core path (SQUINT_BF16) for
+// squint_update (Algorithm 1 L9-24) and squint_act (L4-5).
+//
+// Data flow.  Every GEMM operand is a bf16 row-major matrix read by TMA (gemm.cu):
+//  * linear weights: bf16 "shadow" copies of the fp32 master parameters, refreshed from the
+//    master at the start of each call (k_shadow) and rewritten by every Adam / Polyak step
+//    (a13, a14), so the tensor cores never read a stale weight;
+//  * activations: each layer's epilogue writes its bf16 output straight into the next
+//    GEMM's operand matrix.  Layer inputs that are concatenations (critic [z, s, a], Q11;
+//    actor [z, s], Q12) are single matrices whose column blocks are filled by their
+//    producers: the projection epilogue (z), the encoder kernel's replay row gathers (s, a;
+//    a3), the tanh-Gaussian epilogue (a~, a~').
+// The conv feature map h is stored HWC (pix * C + ch); the projection weights' shadow is
+// column-permuted to match, and their gradient is written back in the master's CHW order.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <optional>
+#include <string>
+
+#include "../../include/squint.h"
+#include "comm.hpp"
+#include "common.cuh"
+#include "encoder.cuh"
+#include "gemm.cuh"
+#include "heads.cuh"
+#include "layout.hpp"
+#include "optim.cuh"
+#include "update_bf16.hpp"
+
+namespace sq {
+
+namespace {
+
+inline int ld8(int x) { return (x + 7) & ~7; }
+inline int mtiles(int m) { return (m + 127) / 128; }
+
+struct BM {  // bf16 matrix inside the workspace
+  size_t off;
+  int rows, cols, ld;
+};
+
+struct ShadowPlan {
+  ShadowTable t;  // base filled at call time
+  size_t off;     // bytes into the workspace
+  size_t elems;
+};
+
+struct BfLay {
+  BM Xh, Xhn, Xq, Xt, Xq1, Xan, Xac;
+  BM H1an, H2an, H1ac, H2ac;
+  BM tqH1[2], tqH2[2], qH1[2], qH2[2], q1H1[2], q1H2[2];
+  BM XH1ac, XH2ac, XHpq, XHpp, XHpq1, qXH1[2], qXH2[2], q1XH1[2], q1XH2[2];  // bf16 LN caches x_hat
+  BM dlog, dlog1;  // [2B][N] (head i = rows i*B ...)
+  BM dA2c[2], dA1c[2], dA2a[2], dA1a[2], dAp, dh, dO, adA2, adA1, adAp;
+  size_t R1ac, R2ac, Rpq, Rpp, Rpq1, qR1[2], qR2[2], q1R1[2], q1R2[2];
+  size_t tlogits, logits, logits1, m, tgo_ac, a_cur, logp_cur, logp_next, row_loss, row_q, row_lpi;
+  size_t part_q2[2], part_q1[2], part_pq, part_a2, part_a1, part_pp;
+  size_t grad_critic, grad_actor, adam_part, scal, lpi_sums;
+  size_t y1b, img0, dA1enc, enc_part;
+  ShadowPlan sh[3];  // critic, target, actor
+  size_t total;
+};
+
+const char* kHeads[2] = {"critic.q1", "critic.q2"};
+
+ShadowPlan shadow_plan(WsPlan& P, const squint_dims& d, const Layout& L, int grp) {
+  ShadowPlan s;
+  memset(&s, 0, sizeof(s));
+  const int C = d.conv_ch, P2 = conv2_out(d) * conv2_out(d);
+  size_t e = 0;
+  auto add = [&](const std::string& name, int perm) {
+    for (const auto& t : L.t) {
+      if (t.group != grp || t.name != name) continue;
+      ShadowEnt& x = s.t.e[s.t.n++];
+      x.src = t.off;
+      x.rows = t.shape[0];
+      x.cols = t.shape[1];
+      x.ld = ld8(x.cols);
+      x.dst = (int64_t)e;
+      x.perm_c = perm ? C : 0;
+      x.perm_p = perm ? P2 : 0;
+      e += (((size_t)x.rows * x.ld) + 63) & ~size_t(63);
+    }
+  };
+  if (grp == SQUINT_GROUP_ACTOR) {
+    add("actor.proj.w", 1);
+    add("actor.l1.w", 0);
+    add("actor.l2.w", 0);
+    add("actor.l3.w", 0);
+  } else {
+    add("critic.proj.w", 1);
+    for (int i = 0; i < 2; ++i)
+      for (const char* l : {".l1.w", ".l2.w", ".l3.w"}) add(std::string(kHeads[i]) + l, 0);
+  }
+  s.elems = e;
+  s.off = P.take(e * 2);
+  return s;
+}
+
+BfLay plan_bf(const squint_dims& d, const Layout& L) {
+  WsPlan P;
+  BfLay w;
+  const int B = d.batch, F = flat_dim(d), Lt = d.latent, Hc = d.critic_hidden, Ha = d.actor_hidden, N = d.n_atoms,
+            A = d.action_dim, C = d.conv_ch, P1 = conv1_out(d) * conv1_out(d);
+  const int nq = Lt + d.proprio_dim + A, npi = Lt + d.proprio_dim;
+  const size_t f = sizeof(float);
+  auto bm = [&](int rows, int cols) {
+    BM m{0, rows, cols, ld8(cols)};
+    m.off = P.take((size_t)rows * m.ld * 2);
+    return m;
+  };
+  auto fl = [&](size_t n) { return P.take(n * f); };
+  w.Xh = bm(B, F);
+  w.Xhn = bm(B, F);
+  w.Xq = bm(B, nq);
+  w.Xt = bm(B, nq);
+  w.Xq1 = bm(B, nq);
+  w.Xan = bm(B, npi);
+  w.Xac = bm(B, npi);
+  w.H1an = bm(B, Ha);
+  w.H2an = bm(B, Ha);
+  w.H1ac = bm(B, Ha);
+  w.H2ac = bm(B, Ha);
+  w.XH1ac = bm(B, Ha);
+  w.XH2ac = bm(B, Ha);
+  w.XHpq = bm(B, Lt);
+  w.XHpp = bm(B, Lt);
+  w.XHpq1 = bm(B, Lt);
+  for (int i = 0; i < 2; ++i) {
+    w.tqH1[i] = bm(B, Hc);
+    w.tqH2[i] = bm(B, Hc);
+    w.qH1[i] = bm(B, Hc);
+    w.qH2[i] = bm(B, Hc);
+    w.qXH1[i] = bm(B, Hc);
+    w.qXH2[i] = bm(B, Hc);
+    w.q1H1[i] = bm(B, Hc);
+    w.q1H2[i] = bm(B, Hc);
+    w.q1XH1[i] = bm(B, Hc);
+    w.q1XH2[i] = bm(B, Hc);
+    w.dA2c[i] = bm(B, Hc);
+    w.dA1c[i] = bm(B, Hc);
+    w.dA2a[i] = bm(B, Hc);
+    w.dA1a[i] = bm(B, Hc);
+  }
+  w.dlog = bm(2 * B, N);
+  w.dlog1 = bm(2 * B, N);
+  w.dAp = bm(B, Lt);
+  w.dh = bm(B, F);
+  w.dO = bm(B, 2 * A);
+  w.adA2 = bm(B, Ha);
+  w.adA1 = bm(B, Ha);
+  w.adAp = bm(B, Lt);
+  w.R1ac = fl(B);
+  w.R2ac = fl(B);
+  w.Rpq = fl(B);
+  w.Rpp = fl(B);
+  w.Rpq1 = fl(B);
+  for (int i = 0; i < 2; ++i) {
+    w.qR1[i] = fl(B);
+    w.qR2[i] = fl(B);
+    w.q1R1[i] = fl(B);
+    w.q1R2[i] = fl(B);
+  }
+  w.tlogits = fl(2 * (size_t)B * N);
+  w.logits = fl(2 * (size_t)B * N);
+  w.logits1 = fl(2 * (size_t)B * N);
+  w.m = fl((size_t)B * N);
+  w.tgo_ac = fl((size_t)B * 2 * A);
+  w.a_cur = fl((size_t)B * A);
+  w.logp_cur = fl(B);
+  w.logp_next = fl(B);
+  w.row_loss = fl(B);
+  w.row_q = fl(B);
+  w.row_lpi = fl(B);
+  const size_t mt = mtiles(B);
+  for (int i = 0; i < 2; ++i) {
+    w.part_q2[i] = fl(mt * 3 * Hc);
+    w.part_q1[i] = fl(mt * 3 * Hc);
+  }
+  w.part_pq = fl(mt * 3 * Lt);
+  w.part_a2 = fl(mt * 3 * Ha);
+  w.part_a1 = fl(mt * 3 * Ha);
+  w.part_pp = fl(mt * 3 * Lt);
+  w.grad_critic = fl(L.gsize[SQUINT_GROUP_CRITIC] + kExtra);
+  w.grad_actor = fl(L.gsize[SQUINT_GROUP_ACTOR] + kExtra);
+  w.adam_part = fl(kAdamBlocks);
+  w.scal = fl(kScal);
+  w.lpi_sums = fl(2);
+  w.y1b = P.take((size_t)B * P1 * C * 2);
+  w.img0 = P.take((size_t)B * d.img_c * d.img_h * d.img_w);
+  w.dA1enc = 0;
+  w.enc_part = fl(enc_bwd_tc_partial_floats(C, B));
+  w.sh[0] = shadow_plan(P, d, L, SQUINT_GROUP_CRITIC);
+  w.sh[1] = shadow_plan(P, d, L, SQUINT_GROUP_TARGET);
+  w.sh[2] = shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
+  w.total = P.top + 256;
+  return w;
+}
+
+struct Ctx {
+  const squint_dims& d;
+  const Layout& L;
+  char* ws;
+  cudaStream_t s;
+  Mat mat(const BM& m) const { return Mat{ws + m.off, m.rows, m.cols, m.ld}; }
+  bf16* bp(const BM& m) const { return reinterpret_cast<bf16*>(ws + m.off); }
+  float* F(size_t off) const { return reinterpret_cast<float*>(ws + off); }
+  // head i of a [2B][N] matrix
+  Mat half(const BM& m, int i) const {
+    return Mat{ws + m.off + (size_t)i * (m.rows / 2) * m.ld * 2, m.rows / 2, m.cols, m.ld};
+  }
+  bf16* halfp(const BM& m, int i) const {
+    return reinterpret_cast<bf16*>(ws + m.off + (size_t)i * (m.rows / 2) * m.ld * 2);
+  }
+};
+
+// One linear layer: bf16 shadow weight + fp32 bias / LN affine (from the master buffer).
+struct Lin {
+  Mat w;
+  const float *b, *g, *beta;
+};
+Lin lin(const Ctx& c, const ShadowPlan& sp, const float* master, int grp, const std::string& p,
+        const std::string& lnp) {
+  Lin l;
+  memset(&l, 0, sizeof(l));
+  const int64_t woff = c.L.off(grp, p + ".w");
+  for (int k = 0; k < sp.t.n; ++k)
+    if (sp.t.e[k].src == woff) {
+      const ShadowEnt& e = sp.t.e[k];
+      l.w = Mat{c.ws + sp.off + (size_t)e.dst * 2, e.rows, e.cols, e.ld};
+    }
+  l.b = master + c.L.off(grp, p + ".b");
+  if (!lnp.empty()) {
+    l.g = master + c.L.off(grp, lnp + ".g");
+    l.beta = master + c.L.off(grp, lnp + ".b");
+  }
+  return l;
+}
+struct Mlp {
+  Lin l1, l2, l3;
+};
+Mlp mlp(const Ctx& c, const ShadowPlan& sp, const float* master, int grp, const std::string& p) {
+  return Mlp{lin(c, sp, master, grp, p + ".l1", p + ".ln1"), lin(c, sp, master, grp, p + ".l2", p + ".ln2"),
+             lin(c, sp, master, grp, p + ".l3", "")};
+}
+Lin proj(const Ctx& c, const ShadowPlan& sp, const float* master, int grp, const std::string& p) {
+  return lin(c, sp, master, grp, p + ".proj", p + ".proj.ln");
+}
+// gradient views
+struct LinG {
+  float *w, *b, *g, *beta;
+};
+LinG ling(const Layout& L, float* base, int grp, const std::string& p, const std::string& lnp) {
+  LinG v;
+  v.w = base + L.off(grp, p + ".w");
+  v.b = base + L.off(grp, p + ".b");
+  v.g = lnp.empty() ? nullptr : base + L.off(grp, lnp + ".g");
+  v.beta = lnp.empty() ? nullptr : base + L.off(grp, lnp + ".b");
+  return v;
+}
+
+// ---- problem helpers ---------------------------------------------------------------------
+// y = epi(X W^T + b): X [M][K] K-major, W [N][K] K-major.
+GProb& fwd(GemmBuilder& gb, const Mat& X, const Lin& W, int epi, bf16* out, int ldo, float ln_eps) {
+  GProb& p = gb.add(X.rows, W.w.rows, epi);
+  gb.seg(p, X, 0, 0, W.w, 0, 0, W.w.cols);
+  p.bias = W.b;
+  p.g = W.g;
+  p.beta = W.beta;
+  p.out = out;
+  p.ldo = ldo;
+  p.ln_eps = ln_eps;
+  return p;
+}
+// dX[m][j] = sum_n D[m][n] W[n][col0 + j], j < ncols: D K-major, W MN-major.
+// The MN-major box start must be 16-byte aligned: an unaligned col0 is aligned down and the
+// slack is skipped in the epilogue (acc_col0; only the tanh-Gaussian backward uses it).
+GProb& dx(GemmBuilder& gb, const Mat& D, const Mat& W, int col0, int ncols, int epi) {
+  const int al = col0 & ~7;
+  GProb& p = gb.add(D.rows, ncols + (col0 - al), epi);
+  gb.seg(p, D, 0, 0, W, 1, 0, W.rows);
+  p.b_n = al;
+  p.acc_col0 = col0 - al;
+  return p;
+}
+// dW[n][k] = sum_m D[m][n] X[m][k]: both operands MN-major (the batch is the reduction).
+GProb& dw(GemmBuilder& gb, const Mat& D, const Mat& X, const LinG& G, int nin) {
+  GProb& p = gb.add(D.cols, nin, GE_DW);
+  gb.seg(p, D, 1, 0, X, 1, 0, D.rows);
+  p.outf = G.w;
+  p.ldf = nin;
+  p.db = G.b;
+  p.dg = G.g;
+  p.dbeta = G.beta;
+  return p;
+}
+void bwd_ln(GProb& p, const Lin& W, bf16* xh, int ldx, float* rstd, bf16* out, int ldo, float* part) {
+  p.g = W.g;
+  p.beta = W.beta;
+  p.xh = xh;
+  p.ldx = ldx;
+  p.rstd = rstd;
+  p.out = out;
+  p.ldo = ldo;
+  p.part = part;
+}
+
+#define BF_CK(expr)                                                                                     \
+  do {                                                                                                  \
+    int _e = (int)(expr);                                                                               \
+    if (_e != 0)                                                                                        \
+      return set_error(SQUINT_ECUDA, std::string("bf16 path: ") + #expr + " failed (" +               \
+                                         (_e > 0 ? cudaGetErrorString((cudaError_t)_e) : "plan/map error") + ")"); \
+  } while (0)
+
+ShadowTable table_at(const Ctx& c, const ShadowPlan& sp) {
+  ShadowTable t = sp.t;
+  t.base = reinterpret_cast<bf16*>(c.ws + sp.off);
+  return t;
+}
+
+squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp, const squint_replay& R,
+                         const int64_t* idx, const uint8_t* sh, const float* eps, const squint_state& st,
+                         float* metrics, Comm* comm, float inv_btotal, int rep) {
+  const squint_dims& d = c.d;
+  const Layout& L = c.L;
+  cudaStream_t s = c.s;
+  const int B = d.batch, F = flat_dim(d), Lt = d.latent, Hc = d.critic_hidden, Ha = d.actor_hidden, N = d.n_atoms,
+            A = d.action_dim, P = d.proprio_dim, C = d.conv_ch;
+  const int nq = Lt + P + A, npi = Lt + P;
+  const int P2 = conv2_out(d) * conv2_out(d);
+  const float* eps_next = eps;
+  const float* eps_cur = eps + (size_t)B * A;
+  const float le = hp.ln_eps;
+  const int gC = SQUINT_GROUP_CRITIC, gA = SQUINT_GROUP_ACTOR, gT = SQUINT_GROUP_TARGET;
+  const float* crit = st.critic;
+  const float* tgt = st.critic_target;
+  const float* act = st.actor;
+  const Lin cproj = proj(c, w.sh[0], crit, gC, "critic"), tproj = proj(c, w.sh[1], tgt, gT, "critic"),
+            aproj = proj(c, w.sh[2], act, gA, "actor");
+  const Mlp cq[2] = {mlp(c, w.sh[0], crit, gC, kHeads[0]), mlp(c, w.sh[0], crit, gC, kHeads[1])};
+  const Mlp tq[2] = {mlp(c, w.sh[1], tgt, gT, kHeads[0]), mlp(c, w.sh[1], tgt, gT, kHeads[1])};
+  const Mlp am = mlp(c, w.sh[2], act, gA, "actor");
+  const int mt = mtiles(B);
+
+  // a3-a5: gather + shift + encoder (obs, next_obs); replay rows of s, a, s' into the layer
+  // input matrices
+  {
+    PhaseScope ps(3, rep, s);
+    EncFwdArgs e;
+    memset(&e, 0, sizeof(e));
+    e.mode = 0;
+    e.src[0] = R.obs;
+    e.src[1] = R.next_obs;
+    e.idx = idx;
+    e.shifts = sh;
+    e.B = B;
+    e.nsrc = 2;
+    e.w1 = crit + L.off(gC, "enc.conv1.w");
+    e.b1 = crit + L.off(gC, "enc.conv1.b");
+    e.w2 = crit + L.off(gC, "enc.conv2.w");
+    e.b2 = crit + L.off(gC, "enc.conv2.b");
+    e.hb[0] = c.bp(w.Xh);
+    e.hb[1] = c.bp(w.Xhn);
+    e.h_ld = w.Xh.ld;
+    e.y1b = reinterpret_cast<bf16*>(c.ws + w.y1b);
+    e.img0 = reinterpret_cast<uint8_t*>(c.ws + w.img0);
+    e.C = C;
+    e.c_in = d.img_c;
+    e.H = d.img_h;
+    e.pad = d.pad;
+    e.gj[0][0] = GatherJob{R.proprio, P, c.bp(w.Xq), w.Xq.ld, Lt, 1};
+    e.gj[0][1] = GatherJob{R.action, A, c.bp(w.Xq), w.Xq.ld, Lt + P, 1};
+    e.gj[0][2] = GatherJob{R.proprio, P, c.bp(w.Xac), w.Xac.ld, Lt, 1};
+    e.gj[0][3] = GatherJob{R.proprio, P, c.bp(w.Xq1), w.Xq1.ld, Lt, 1};
+    e.ngj[0] = 4;
+    e.gj[1][0] = GatherJob{R.next_proprio, P, c.bp(w.Xt), w.Xt.ld, Lt, 1};
+    e.gj[1][1] = GatherJob{R.next_proprio, P, c.bp(w.Xan), w.Xan.ld, Lt, 1};
+    e.ngj[1] = 2;
+    BF_CK(launch_enc_fwd_tc(e, s));
+  }
+  // a6: projections Linear -> LN -> tanh (Q8): critic(h), target(h'), actor(h'), actor(h)
+  {
+    PhaseScope ps(4, rep, s);
+    GemmBuilder gb;
+    GProb* p = &fwd(gb, c.mat(w.Xh), cproj, GE_LN_TANH, c.bp(w.Xq), w.Xq.ld, le);
+    p->xh = c.bp(w.XHpq), p->ldx = w.XHpq.ld, p->rstd = c.F(w.Rpq);
+    fwd(gb, c.mat(w.Xhn), tproj, GE_LN_TANH, c.bp(w.Xt), w.Xt.ld, le);
+    fwd(gb, c.mat(w.Xhn), aproj, GE_LN_TANH, c.bp(w.Xan), w.Xan.ld, le);
+    p = &fwd(gb, c.mat(w.Xh), aproj, GE_LN_TANH, c.bp(w.Xac), w.Xac.ld, le);
+    p->xh = c.bp(w.XHpp), p->ldx = w.XHpp.ld, p->rstd = c.F(w.Rpp);
+    BF_CK(gemm_launch(gb, s));
+  }
+  // a7: actor MLP on s' (target sample) and on s (alpha / actor losses)
+  {
+    PhaseScope ps(5, rep, s);
+    {
+      GemmBuilder gb;
+      fwd(gb, c.mat(w.Xan), am.l1, GE_LN_RELU, c.bp(w.H1an), w.H1an.ld, le);
+      GProb& p = fwd(gb, c.mat(w.Xac), am.l1, GE_LN_RELU, c.bp(w.H1ac), w.H1ac.ld, le);
+      p.xh = c.bp(w.XH1ac), p.ldx = w.XH1ac.ld, p.rstd = c.F(w.R1ac);
+      BF_CK(gemm_launch(gb, s));
+    }
+    {
+      GemmBuilder gb;
+      fwd(gb, c.mat(w.H1an), am.l2, GE_LN_RELU, c.bp(w.H2an), w.H2an.ld, le);
+      GProb& p = fwd(gb, c.mat(w.H1ac), am.l2, GE_LN_RELU, c.bp(w.H2ac), w.H2ac.ld, le);
+      p.xh = c.bp(w.XH2ac), p.ldx = w.XH2ac.ld, p.rstd = c.F(w.R2ac);
+      BF_CK(gemm_launch(gb, s));
+    }
+    {
+      GemmBuilder gb;
+      GProb& pn = fwd(gb, c.mat(w.H2an), am.l3, GE_TG_FWD, nullptr, 0, le);
+      pn.eps = eps_next;
+      pn.act_bf = c.bp(w.Xt) + Lt + P;
+      pn.ld_act_bf = w.Xt.ld;
+      pn.logp = c.F(w.logp_next);
+      pn.lo = hp.log_std_min;
+      pn.hi = hp.log_std_max;
+      GProb& pc = fwd(gb, c.mat(w.H2ac), am.l3, GE_TG_FWD, nullptr, 0, le);
+      pc.eps = eps_cur;
+      pc.act = c.F(w.a_cur);
+      pc.act_bf = c.bp(w.Xq1) + Lt + P;
+      pc.ld_act_bf = w.Xq1.ld;
+      pc.logp = c.F(w.logp_cur);
+      pc.tgo = c.F(w.tgo_ac);
+      pc.lo = hp.log_std_min;
+      pc.hi = hp.log_std_max;
+      BF_CK(gemm_launch(gb, s));
+    }
+  }
+  // a8: target heads on (z', s', a~') and online heads on (z, s, a)
+  {
+    PhaseScope ps(6, rep, s);
+    {
+      GemmBuilder gb;
+      for (int i = 0; i < 2; ++i) fwd(gb, c.mat(w.Xt), tq[i].l1, GE_LN_RELU, c.bp(w.tqH1[i]), w.tqH1[i].ld, le);
+      for (int i = 0; i < 2; ++i) {
+        GProb& p = fwd(gb, c.mat(w.Xq), cq[i].l1, GE_LN_RELU, c.bp(w.qH1[i]), w.qH1[i].ld, le);
+        p.xh = c.bp(w.qXH1[i]), p.ldx = w.qXH1[i].ld, p.rstd = c.F(w.qR1[i]);
+      }
+      BF_CK(gemm_launch(gb, s));
+    }
+    {
+      GemmBuilder gb;
+      for (int i = 0; i < 2; ++i)
+        fwd(gb, c.mat(w.tqH1[i]), tq[i].l2, GE_LN_RELU, c.bp(w.tqH2[i]), w.tqH2[i].ld, le);
+      for (int i = 0; i < 2; ++i) {
+        GProb& p = fwd(gb, c.mat(w.qH1[i]), cq[i].l2, GE_LN_RELU, c.bp(w.qH2[i]), w.qH2[i].ld, le);
+        p.xh = c.bp(w.qXH2[i]), p.ldx = w.qXH2[i].ld, p.rstd = c.F(w.qR2[i]);
+      }
+      BF_CK(gemm_launch(gb, s));
+    }
+    {
+      GemmBuilder gb;
+      for (int i = 0; i < 2; ++i) {
+        GProb& p = fwd(gb, c.mat(w.tqH2[i]), tq[i].l3, GE_BIAS_F32, nullptr, 0, le);
+        p.outf = c.F(w.tlogits) + (size_t)i * B * N;
+        p.ldf = N;
+      }
+      for (int i = 0; i < 2; ++i) {
+        GProb& p = fwd(gb, c.mat(w.qH2[i]), cq[i].l3, GE_BIAS_F32, nullptr, 0, le);
+        p.outf = c.F(w.logits) + (size_t)i * B * N;
+        p.ldf = N;
+      }
+      BF_CK(gemm_launch(gb, s));
+    }
+  }
+  // a9-a10: target distribution, categorical projection, CE, dL/dlogits
+  {
+    PhaseScope ps(7, rep, s);
+    TargetCEArgs t;
+    memset(&t, 0, sizeof(t));
+    t.B = B;
+    t.N = N;
+    t.v_min = d.v_min;
+    t.v_max = d.v_max;
+    t.gamma = hp.gamma;
+    t.scale = inv_btotal;
+    t.tlogits = c.F(w.tlogits);
+    t.logits = c.F(w.logits);
+    t.idx = idx;
+    t.reward = R.reward;
+    t.done = R.done;
+    t.logp_next = c.F(w.logp_next);
+    t.log_alpha = st.log_alpha;
+    t.m = c.F(w.m);
+    t.dlogits_bf = c.bp(w.dlog);
+    t.ld_dl = w.dlog.ld;
+    t.row_loss = c.F(w.row_loss);
+    BF_CK(launch_target_ce(t, s));
+  }
+  // a10: critic backward: heads -> critic projection -> ReLU'(conv2)
+  float* gc = c.F(w.grad_critic);
+  {
+    PhaseScope ps(8, rep, s);
+    {
+      GemmBuilder gb;
+      for (int i = 0; i < 2; ++i) {
+        GProb& p = dx(gb, c.half(w.dlog, i), cq[i].l3.w, 0, Hc, GE_BWD_LN_RELU);
+        bwd_ln(p, cq[i].l2, c.bp(w.qXH2[i]), w.qXH2[i].ld, c.F(w.qR2[i]), c.bp(w.dA2c[i]), w.dA2c[i].ld,
+               c.F(w.part_q2[i]));
+      }
+      BF_CK(gemm_launch(gb, s));
+    }
+    {
+      GemmBuilder gb;
+      for (int i = 0; i < 2; ++i) {
+        GProb& p = dx(gb, c.mat(w.dA2c[i]), cq[i].l2.w, 0, Hc, GE_BWD_LN_RELU);
+        bwd_ln(p, cq[i].l1, c.bp(w.qXH1[i]), w.qXH1[i].ld, c.F(w.qR1[i]), c.bp(w.dA1c[i]), w.dA1c[i].ld,
+               c.F(w.part_q1[i]));
+      }
+      BF_CK(gemm_launch(gb, s));
+    }
+    {
+      // dz = sum_i dA1_i W1_i[:, :L] (K-concatenation of the two heads) -> tanh + LN of the projection
+      GemmBuilder gb;
+      GProb& p = dx(gb, c.mat(w.dA1c[0]), cq[0].l1.w, 0, Lt, GE_BWD_LN_TANH);
+      gb.seg(p, c.mat(w.dA1c[1]), 0, 0, cq[1].l1.w, 1, 0, Hc);
+      bwd_ln(p, cproj, c.bp(w.XHpq), w.XHpq.ld, c.F(w.Rpq), c.bp(w.dAp), w.dAp.ld, c.F(w.part_pq));
+      BF_CK(gemm_launch(gb, s));
+    }
+    {
+      // dh = dAp Wp, masked by ReLU'(conv2) (h > 0), HWC
+      GemmBuilder gb;
+      GProb& p = dx(gb, c.mat(w.dAp), cproj.w, 0, F, GE_RELU_MASK);
+      p.y = c.bp(w.Xh);
+      p.ldy = w.Xh.ld;
+      p.out = c.bp(w.dh);
+      p.ldo = w.dh.ld;
+      BF_CK(gemm_launch(gb, s));
+    }
+  }
+  {
+    PhaseScope ps(9, rep, s);
+    GemmBuilder gb;
+    for (int i = 0; i < 2; ++i) {
+      const std::string hp_ = kHeads[i];
+      GProb& p3 = dw(gb, c.half(w.dlog, i), c.mat(w.qH2[i]), ling(L, gc, gC, hp_ + ".l3", ""), Hc);
+      p3.colsum = c.halfp(w.dlog, i);
+      p3.ld_colsum = w.dlog.ld;
+      p3.colsum_rows = B;
+      GProb& p2 = dw(gb, c.mat(w.dA2c[i]), c.mat(w.qH1[i]), ling(L, gc, gC, hp_ + ".l2", hp_ + ".ln2"), Hc);
+      p2.part_in = c.F(w.part_q2[i]);
+      p2.part_tiles = mt;
+      GProb& p1 = dw(gb, c.mat(w.dA1c[i]), c.mat(w.Xq), ling(L, gc, gC, hp_ + ".l1", hp_ + ".ln1"), nq);
+      p1.part_in = c.F(w.part_q1[i]);
+      p1.part_tiles = mt;
+    }
+    GProb& pp = dw(gb, c.mat(w.dAp), c.mat(w.Xh), ling(L, gc, gC, "critic.proj", "critic.proj.ln"), F);
+    pp.part_in = c.F(w.part_pq);
+    pp.part_tiles = mt;
+    pp.perm_c = C;
+    pp.perm_p = P2;
+    BF_CK(gemm_launch(gb, s));
+  }
+  {
+    PhaseScope ps(10, rep, s);
+    EncBwdArgs e;
+    memset(&e, 0, sizeof(e));
+    e.B = B;
+    e.C = C;
+    e.c_in = d.img_c;
+    e.H = d.img_h;
+    e.dA2_hwc = c.bp(w.dh);
+    e.dA2_ld = w.dh.ld;
+    e.y1_hwc = reinterpret_cast<const bf16*>(c.ws + w.y1b);
+    e.img = reinterpret_cast<const uint8_t*>(c.ws + w.img0);
+    e.w2 = crit + L.off(gC, "enc.conv2.w");
+    e.part = c.F(w.enc_part);
+    e.gw1 = gc + L.off(gC, "enc.conv1.w");
+    e.gb1 = gc + L.off(gC, "enc.conv1.b");
+    e.gw2 = gc + L.off(gC, "enc.conv2.w");
+    e.gb2 = gc + L.off(gC, "enc.conv2.b");
+    BF_CK(launch_enc_bwd_tc(e, s));
+  }
+  float* extras = gc + L.gsize[gC];
+  float* scal = c.F(w.scal);
+  if (comm) {
+    BF_CK(launch_row_sums(c.F(w.logp_cur), c.F(w.row_loss), B, extras, s));
+    if (comm_allreduce_sum(comm, gc, L.gsize[gC] + kExtra, s) != 0) return set_error(SQUINT_ENCCL, comm_error());
+  }
+  const ShadowTable shC = table_at(c, w.sh[0]), shT = table_at(c, w.sh[1]), shA = table_at(c, w.sh[2]);
+  // a11 temperature step + Adam bias corrections; a13 Adam on the critic group (+ shadow)
+  {
+    PhaseScope ps(11, rep, s);
+    ScalarsArgs a;
+    memset(&a, 0, sizeof(a));
+    a.B = B;
+    a.inv_btotal = inv_btotal;
+    a.logp = c.F(w.logp_cur);
+    a.row_loss = c.F(w.row_loss);
+    a.extras = extras;
+    a.compute_sums = comm ? 0 : 1;
+    a.log_alpha = st.log_alpha;
+    a.m_alpha = st.m_alpha;
+    a.v_alpha = st.v_alpha;
+    a.step = st.step;
+    a.lr_alpha = hp.lr_alpha;
+    a.beta1 = hp.beta1;
+    a.beta2 = hp.beta2;
+    a.adam_eps = hp.adam_eps;
+    a.target_entropy = hp.target_entropy;
+    a.loss_scale = inv_btotal;
+    a.scal = scal;
+    BF_CK(launch_scalars(a, s));
+    BF_CK(launch_adam_shadow(st.critic, gc, st.m_critic, st.v_critic, L.gsize[gC], hp.lr_critic, hp.beta1, hp.beta2,
+                             hp.adam_eps, scal + S_C1_CRITIC, scal + S_C2_CRITIC, c.F(w.adam_part), &shC, s));
+  }
+  // a12: actor loss against theta+ on sg(h) (Q19)
+  {
+    PhaseScope ps(12, rep, s);
+    const Lin cproj1 = proj(c, w.sh[0], crit, gC, "critic");  // same buffers, now theta+
+    const Mlp cq1[2] = {mlp(c, w.sh[0], crit, gC, kHeads[0]), mlp(c, w.sh[0], crit, gC, kHeads[1])};
+    {
+      GemmBuilder gb;
+      GProb& p = fwd(gb, c.mat(w.Xh), cproj1, GE_LN_TANH, c.bp(w.Xq1), w.Xq1.ld, le);
+      p.xh = c.bp(w.XHpq1), p.ldx = w.XHpq1.ld, p.rstd = c.F(w.Rpq1);
+      BF_CK(gemm_launch(gb, s));
+    }
+    {
+      GemmBuilder gb;
+      for (int i = 0; i < 2; ++i) {
+        GProb& p = fwd(gb, c.mat(w.Xq1), cq1[i].l1, GE_LN_RELU, c.bp(w.q1H1[i]), w.q1H1[i].ld, le);
+        p.xh = c.bp(w.q1XH1[i]), p.ldx = w.q1XH1[i].ld, p.rstd = c.F(w.q1R1[i]);
+      }
+      BF_CK(gemm_launch(gb, s));
+    }
+    {
+      GemmBuilder gb;
+      for (int i = 0; i < 2; ++i) {
+        GProb& p = fwd(gb, c.mat(w.q1H1[i]), cq1[i].l2, GE_LN_RELU, c.bp(w.q1H2[i]), w.q1H2[i].ld, le);
+        p.xh = c.bp(w.q1XH2[i]), p.ldx = w.q1XH2[i].ld, p.rstd = c.F(w.q1R2[i]);
+      }
+      BF_CK(gemm_launch(gb, s));
+    }
+    {
+      GemmBuilder gb;
+      for (int i = 0; i < 2; ++i) {
+        GProb& p = fwd(gb, c.mat(w.q1H2[i]), cq1[i].l3, GE_BIAS_F32, nullptr, 0, le);
+        p.outf = c.F(w.logits1) + (size_t)i * B * N;
+        p.ldf = N;
+      }
+      BF_CK(gemm_launch(gb, s));
+    }
+    ActorQArgs q;
+    memset(&q, 0, sizeof(q));
+    q.B = B;
+    q.N = N;
+    q.v_min = d.v_min;
+    q.v_max = d.v_max;
+    q.scale = inv_btotal;
+    q.logits = c.F(w.logits1);
+    q.logp = c.F(w.logp_cur);
+    q.alpha1 = scal + S_ALPHA1;
+    q.dlogits_bf = c.bp(w.dlog1);
+    q.ld_dl = w.dlog1.ld;
+    q.row_q = c.F(w.row_q);
+    q.row_lpi = c.F(w.row_lpi);
+    BF_CK(launch_actor_q(q, s));
+  }
+  {
+    PhaseScope ps(13, rep, s);
+    const Lin cproj1 = proj(c, w.sh[0], crit, gC, "critic");
+    const Mlp cq1[2] = {mlp(c, w.sh[0], crit, gC, kHeads[0]), mlp(c, w.sh[0], crit, gC, kHeads[1])};
+    (void)cproj1;
+    {
+      GemmBuilder gb;
+      for (int i = 0; i < 2; ++i) {
+        GProb& p = dx(gb, c.half(w.dlog1, i), cq1[i].l3.w, 0, Hc, GE_BWD_LN_RELU);
+        bwd_ln(p, cq1[i].l2, c.bp(w.q1XH2[i]), w.q1XH2[i].ld, c.F(w.q1R2[i]), c.bp(w.dA2a[i]), w.dA2a[i].ld,
+               nullptr);
+      }
+      BF_CK(gemm_launch(gb, s));
+    }
+    {
+      GemmBuilder gb;
+      for (int i = 0; i < 2; ++i) {
+        GProb& p = dx(gb, c.mat(w.dA2a[i]), cq1[i].l2.w, 0, Hc, GE_BWD_LN_RELU);
+        bwd_ln(p, cq1[i].l1, c.bp(w.q1XH1[i]), w.q1XH1[i].ld, c.F(w.q1R1[i]), c.bp(w.dA1a[i]), w.dA1a[i].ld,
+               nullptr);
+      }
+      BF_CK(gemm_launch(gb, s));
+    }
+    {
+      // dL/da~ = sum_i dA1_i W1_i[:, L+P : L+P+A] -> tanh-Gaussian backward (+ the log pi path)
+      GemmBuilder gb;
+      GProb& p = dx(gb, c.mat(w.dA1a[0]), cq1[0].l1.w, Lt + P, A, GE_TG_BWD);
+      gb.seg(p, c.mat(w.dA1a[1]), 0, 0, cq1[1].l1.w, 1, 0, Hc);
+      p.tgo = c.F(w.tgo_ac);
+      p.eps = eps_cur;
+      p.dlogp_scale = scal + S_ALPHA1_SCALE;
+      p.lo = hp.log_std_min;
+      p.hi = hp.log_std_max;
+      p.out = c.bp(w.dO);
+      p.ldo = w.dO.ld;
+      BF_CK(gemm_launch(gb, s));
+    }
+    {
+      GemmBuilder gb;
+      GProb& p = dx(gb, c.mat(w.dO), am.l3.w, 0, Ha, GE_BWD_LN_RELU);
+      bwd_ln(p, am.l2, c.bp(w.XH2ac), w.XH2ac.ld, c.F(w.R2ac), c.bp(w.adA2), w.adA2.ld, c.F(w.part_a2));
+      BF_CK(gemm_launch(gb, s));
+    }
+    {
+      GemmBuilder gb;
+      GProb& p = dx(gb, c.mat(w.adA2), am.l2.w, 0, Ha, GE_BWD_LN_RELU);
+      bwd_ln(p, am.l1, c.bp(w.XH1ac), w.XH1ac.ld, c.F(w.R1ac), c.bp(w.adA1), w.adA1.ld, c.F(w.part_a1));
+      BF_CK(gemm_launch(gb, s));
+    }
+    {
+      GemmBuilder gb;
+      GProb& p = dx(gb, c.mat(w.adA1), am.l1.w, 0, Lt, GE_BWD_LN_TANH);
+      bwd_ln(p, aproj, c.bp(w.XHpp), w.XHpp.ld, c.F(w.Rpp), c.bp(w.adAp), w.adAp.ld, c.F(w.part_pp));
+      BF_CK(gemm_launch(gb, s));
+    }
+  }
+  float* ga = c.F(w.grad_actor);
+  {
+    PhaseScope ps(14, rep, s);
+    GemmBuilder gb;
+    GProb& p3 = dw(gb, c.mat(w.dO), c.mat(w.H2ac), ling(L, ga, gA, "actor.l3", ""), Ha);
+    p3.colsum = c.bp(w.dO);
+    p3.ld_colsum = w.dO.ld;
+    p3.colsum_rows = B;
+    GProb& p2 = dw(gb, c.mat(w.adA2), c.mat(w.H1ac), ling(L, ga, gA, "actor.l2", "actor.ln2"), Ha);
+    p2.part_in = c.F(w.part_a2);
+    p2.part_tiles = mt;
+    GProb& p1 = dw(gb, c.mat(w.adA1), c.mat(w.Xac), ling(L, ga, gA, "actor.l1", "actor.ln1"), npi);
+    p1.part_in = c.F(w.part_a1);
+    p1.part_tiles = mt;
+    GProb& pp = dw(gb, c.mat(w.adAp), c.mat(w.Xh), ling(L, ga, gA, "actor.proj", "actor.proj.ln"), F);
+    pp.part_in = c.F(w.part_pp);
+    pp.part_tiles = mt;
+    pp.perm_c = C;
+    pp.perm_p = P2;
+    BF_CK(gemm_launch(gb, s));
+  }
+  float* lpis = c.F(w.lpi_sums);
+  PhaseScope ps15(15, rep, s);
+  if (comm) {
+    float* ax = ga + L.gsize[gA];
+    BF_CK(launch_lpi_sums(c.F(w.row_lpi), c.F(w.row_q), B, ax, s));
+    if (comm_allreduce_sum(comm, ga, L.gsize[gA] + kExtra, s) != 0) return set_error(SQUINT_ENCCL, comm_error());
+    lpis = ax;
+  }
+  BF_CK(launch_adam_shadow(st.actor, ga, st.m_actor, st.v_actor, L.gsize[gA], hp.lr_actor, hp.beta1, hp.beta2,
+                           hp.adam_eps, scal + S_C1_ACTOR, scal + S_C2_ACTOR, nullptr, &shA, s));
+  // a14: Polyak over every critic tensor except the encoder (+ target shadow)
+  BF_CK(launch_polyak_shadow(st.critic_target, st.critic + L.enc_end, L.gsize[gT], hp.tau, &shT, s));
+  {
+    MetricsArgs m;
+    memset(&m, 0, sizeof(m));
+    m.B = B;
+    m.inv_btotal = inv_btotal;
+    m.row_lpi = c.F(w.row_lpi);
+    m.row_q = c.F(w.row_q);
+    m.sumsq_part = c.F(w.adam_part);
+    m.scal = scal;
+    m.extras = extras;
+    m.out = metrics;
+    m.reduce_local = comm ? 0 : 1;
+    m.extras2 = lpis;
+    BF_CK(launch_metrics(m, s));
+  }
+  return SQUINT_OK;
+}
+
+}  // namespace
+
+size_t bf16_workspace_bytes(const squint_dims& d) {
+  Layout L = make_layout(d);
+  return plan_bf(d, L).total;
+}
+
+bool bf16_region(const squint_dims& d, int region, size_t* offset, size_t* bytes) {
+  Layout L = make_layout(d);
+  BfLay w = plan_bf(d, L);
+  const size_t B = d.batch, f = sizeof(float);
+  switch (region) {
+    case 0: *offset = w.grad_critic; *bytes = L.gsize[0] * f; break;
+    case 1: *offset = w.grad_actor; *bytes = L.gsize[1] * f; break;
+    case 2: *offset = w.m; *bytes = B * d.n_atoms * f; break;
+    case 3: *offset = w.Xh.off; *bytes = (size_t)w.Xh.rows * w.Xh.ld * 2; break;
+    case 4: *offset = w.logp_cur; *bytes = B * f; break;
+    case 5: *offset = w.logp_next; *bytes = B * f; break;
+    case 6: *offset = w.a_cur; *bytes = B * d.action_dim * f; break;
+    case 7: *offset = w.scal; *bytes = kScal * f; break;
+    default: return false;
+  }
+  return true;
+}
+
+squint_status bf16_check(const squint_dims& d) {
+  if (d.action_dim > 16) return set_error(SQUINT_EUNSUPPORTED, "bf16 path: action_dim > 16 not built");
+  if (d.critic_hidden > 512 || d.actor_hidden > 512 || d.n_atoms > 256 || d.latent > 256)
+    return set_error(SQUINT_EUNSUPPORTED, "bf16 path: layer width not built");
+  return SQUINT_OK;
+}
+
+squint_status bf16_update(const squint_dims& d, const squint_hparams& hp, const squint_replay& R,
+                          const int64_t* idx, const uint8_t* shifts, const float* eps, int utd,
+                          const squint_state& st, float* metrics, void* workspace, size_t workspace_bytes, Comm* comm,
+                          cudaStream_t s) {
+  squint_status chk = bf16_check(d);
+  if (chk != SQUINT_OK) return chk;
+  Layout L = make_layout(d);
+  BfLay w = plan_bf(d, L);
+  if (workspace_bytes < w.total) return set_error(SQUINT_EINVAL, "workspace too small (see squint_workspace_bytes)");
+  Ctx c{d, L, reinterpret_cast<char*>(workspace), s};
+  const int nranks = comm ? comm_nranks(comm) : 1;
+  const float inv_btotal = 1.0f / ((float)d.batch * (float)nranks);
+  // bf16 shadows of the current master weights
+  BF_CK(launch_shadow(st.critic, table_at(c, w.sh[0]), s));
+  BF_CK(launch_shadow(st.critic_target, table_at(c, w.sh[1]), s));
+  BF_CK(launch_shadow(st.actor, table_at(c, w.sh[2]), s));
+  const size_t B = d.batch, A = d.action_dim;
+  for (int j = 0; j < utd; ++j) {
+    squint_status r = update_one(c, w, hp, R, idx + j * B, shifts + j * B * 4, eps + j * 2 * B * A, st, metrics + j * 8,
+                                 comm, inv_btotal, j);
+    if (r != SQUINT_OK) return r;
+  }
+  return SQUINT_OK;
+}
+
+size_t bf16_act_workspace_bytes(const squint_dims& d, int64_t n) {
+  Layout L = make_layout(d);
+  WsPlan P;
+  const int F = flat_dim(d), npi = d.latent + d.proprio_dim, Ha = d.actor_hidden;
+  P.take((size_t)n * ld8(F) * 2);
+  P.take((size_t)n * ld8(npi) * 2);
+  P.take((size_t)n * ld8(Ha) * 2);
+  P.take((size_t)n * ld8(Ha) * 2);
+  shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
+  return P.top + 256;
+}
+
+squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const float* actor_params,
+                       const float* critic_params, const uint8_t* frames, int64_t n, int factor, const float* proprio,
+                       const float* eps, float* action_out, float* logp_out, uint8_t* ring, const int64_t* slots,
+                       void* workspace, cudaStream_t s) {
+  squint_status chk = bf16_check(d);
+  if (chk != SQUINT_OK) return chk;
+  Layout L = make_layout(d);
+  WsPlan P;
+  const int F = flat_dim(d), Lt = d.latent, npi = Lt + d.proprio_dim, Ha = d.actor_hidden, M = (int)n;
+  char* ws = reinterpret_cast<char*>(workspace);
+  BM Xh{P.take((size_t)n * ld8(F) * 2), M, F, ld8(F)};
+  BM Xa{P.take((size_t)n * ld8(npi) * 2), M, npi, ld8(npi)};
+  BM H1{P.take((size_t)n * ld8(Ha) * 2), M, Ha, ld8(Ha)};
+  BM H2{P.take((size_t)n * ld8(Ha) * 2), M, Ha, ld8(Ha)};
+  ShadowPlan sp = shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
+  Ctx c{d, L, ws, s};
+  const int gC = SQUINT_GROUP_CRITIC, gA = SQUINT_GROUP_ACTOR;
+  std::optional<PhaseScope> ps;
+  ps.emplace(1, 0, s);
+  BF_CK(launch_shadow(actor_params, table_at(c, sp), s));
+  {
+    EncFwdArgs a;
+    memset(&a, 0, sizeof(a));
+    a.mode = 1;
+    a.src[0] = frames;
+    a.factor = factor;
+    a.ring = ring;
+    a.slots = slots;
+    a.B = M;
+    a.nsrc = 1;
+    a.w1 = critic_params + L.off(gC, "enc.conv1.w");
+    a.b1 = critic_params + L.off(gC, "enc.conv1.b");
+    a.w2 = critic_params + L.off(gC, "enc.conv2.w");
+    a.b2 = critic_params + L.off(gC, "enc.conv2.b");
+    a.hb[0] = c.bp(Xh);
+    a.h_ld = Xh.ld;
+    a.C = d.conv_ch;
+    a.c_in = d.img_c;
+    a.H = d.img_h;
+    a.pad = d.pad;
+    a.gj[0][0] = GatherJob{proprio, d.proprio_dim, c.bp(Xa), Xa.ld, Lt, 0};
+    a.ngj[0] = 1;
+    BF_CK(launch_enc_fwd_tc(a, s));
+  }
+  ps.reset();
+  ps.emplace(2, 0, s);
+  const Lin ap = proj(c, sp, actor_params, gA, "actor");
+  const Mlp am = mlp(c, sp, actor_params, gA, "actor");
+  {
+    GemmBuilder gb;
+    fwd(gb, c.mat(Xh), ap, GE_LN_TANH, c.bp(Xa), Xa.ld, hp.ln_eps);
+    BF_CK(gemm_launch(gb, s));
+  }
+  {
+    GemmBuilder gb;
+    fwd(gb, c.mat(Xa), am.l1, GE_LN_RELU, c.bp(H1), H1.ld, hp.ln_eps);
+    BF_CK(gemm_launch(gb, s));
+  }
+  {
+    GemmBuilder gb;
+    fwd(gb, c.mat(H1), am.l2, GE_LN_RELU, c.bp(H2), H2.ld, hp.ln_eps);
+    BF_CK(gemm_launch(gb, s));
+  }
+  {
+    GemmBuilder gb;
+    GProb& p = fwd(gb, c.mat(H2), am.l3, GE_TG_FWD, nullptr, 0, hp.ln_eps);
+    p.eps = eps;
+    p.act = action_out;
+    p.logp = logp_out;
+    p.lo = hp.log_std_min;
+    p.hi = hp.log_std_max;
+    BF_CK(gemm_launch(gb, s));
+  }
+  return SQUINT_OK;
+}
+
+}  // namespace sq
+
+extern "C" squint_status squint_selftest_gemm(const void* A, int a_rows, int a_cols, int a_ld, int a_mn, const void* B,
+                                              int b_rows, int b_cols, int b_ld, int b_mn, int M, int N, int K,
+                                              float* out, squint_stream_t stream) {
+  using namespace sq;
+  if (!A || !B || !out || M < 1 || N < 1 || K < 1) return set_error(SQUINT_EINVAL, "selftest_gemm: bad argument");
+  GemmBuilder gb;
+  GProb& p = gb.add(M, N, GE_DW);
+  gb.seg(p, Mat{A, a_rows, a_cols, a_ld}, a_mn, 0, Mat{B, b_rows, b_cols, b_ld}, b_mn, 0, K);
+  p.outf = out;
+  p.ldf = N;
+  const int e = gemm_launch(gb, (cudaStream_t)stream);
+  if (e)
+    return set_error(SQUINT_ECUDA, std::string("selftest_gemm: ") +
+                                       (e > 0 ? cudaGetErrorString((cudaError_t)e) : "plan/map error"));
+  return SQUINT_OK;
+}
+
+extern "C" SQUINT_API int squint_debug_gemm_times(unsigned long long* host, int max_entries) {
+  return sq::gemm_debug_times(host, max_entries);
+}

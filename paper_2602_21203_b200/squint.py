@@ -55,7 +55,7 @@ class TensorDesc(C.Structure):
 
 def _load():
     if not os.path.exists(_LIB_PATH):
-        raise ImportError(f"{_LIB_PATH} is missing: build it with `python -m paper_2602_21203_b200.build` "
+        raise ImportError(f"{_LIB_PATH} is missing: build it with `python paper_2602_21203_b200/build.py` "
                           "(there is no CPU fallback)")
     lib = C.CDLL(_LIB_PATH)
     st, vp, i64, i32, f32, sz = C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_float, C.c_size_t
@@ -75,9 +75,11 @@ def _load():
         "squint_update": (st, [C.POINTER(Dims), C.POINTER(HParams), C.POINTER(Replay), vp, vp, vp, i32,
                                C.POINTER(State), vp, vp, sz, vp, vp]),
         "squint_soft_update": (st, [vp, vp, i64, f32, vp]),
+        "squint_selftest_gemm": (st, [vp, i32, i32, i32, i32, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp]),
         "squint_launch_count": (C.c_long, []),
         "squint_set_phase_events": (st, [C.POINTER(vp), i32, i32]),
         "squint_phase_name": (C.c_char_p, [i32]),
+        "squint_set_launch_events": (i32, [C.POINTER(vp), i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -90,7 +92,8 @@ LIB = _load()
 EXPORTED = ["squint_last_error", "squint_version", "squint_param_layout", "squint_workspace_bytes",
             "squint_workspace_region", "squint_act_workspace_bytes", "squint_comm_unique_id", "squint_comm_init",
             "squint_comm_destroy", "squint_insert", "squint_act", "squint_update", "squint_soft_update",
-            "squint_launch_count", "squint_set_phase_events", "squint_phase_name"]
+            "squint_launch_count", "squint_set_phase_events", "squint_phase_name", "squint_selftest_gemm",
+            "squint_set_launch_events"]
 N_PHASES = 16
 
 
@@ -205,6 +208,15 @@ def squint_insert(frames: torch.Tensor, factor: int, slots: torch.Tensor, ring: 
 def squint_soft_update(target: torch.Tensor, online: torch.Tensor, tau: float, stream=None):
     assert target.numel() == online.numel()
     _check(LIB.squint_soft_update(_ptr(target), _ptr(online), target.numel(), tau, _stream(stream)))
+
+
+def selftest_gemm(A: torch.Tensor, a_cols: int, a_mn: int, B: torch.Tensor, b_cols: int, b_mn: int, M: int, N: int,
+                  K: int, out: torch.Tensor, stream=None):
+    """out[m][n] = sum_k A(m, k) B(n, k) on the bf16 tcgen05 GEMM engine (see squint.h).  A, B are
+    contiguous row-major storage whose first a_cols / b_cols columns are the matrix."""
+    assert A.dtype == torch.bfloat16 and B.dtype == torch.bfloat16 and out.dtype == torch.float32
+    _check(LIB.squint_selftest_gemm(_ptr(A), A.shape[0], a_cols, A.shape[1], a_mn, _ptr(B), B.shape[0], b_cols,
+                                    B.shape[1], b_mn, M, N, K, _ptr(out), _stream(stream)))
 
 
 def squint_act(dims: Dims, hp: HParams, actor: torch.Tensor, critic: torch.Tensor, frames: torch.Tensor,

@@ -218,3 +218,29 @@ def test_update_c2_full_batch_utd2_bf16():
 def test_update_c2_full_batch_bf16():
     """BASELINE configs[2] shapes at the full batch 512 (101 atoms), as bench.py runs them."""
     _bf16_case("c2", seed=2, capacity=4096)
+
+
+# ---- bf16 GEMM engine (TMA + tcgen05) self-test: both operand majors, ragged tails -------
+def _padded(x):
+    """contiguous storage with a 16-byte multiple row pitch; returns (storage, logical cols)"""
+    r, c = x.shape
+    ld = (c + 7) // 8 * 8
+    st = torch.full((r, ld), float("nan"), dtype=x.dtype)
+    st[:, :c] = x
+    return st.to(DEV), c
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (200, 101, 68), (512, 256, 256), (50, 800, 512), (37, 520, 130),
+                                   (512, 6, 256), (512, 12, 256), (256, 62, 512)])
+def test_gemm_engine(a_mn, b_mn, M, N, K):
+    g = torch.Generator().manual_seed(M * 7 + N * 3 + K)
+    a = torch.randn((M, K), generator=g).to(torch.bfloat16)
+    b = torch.randn((N, K), generator=g).to(torch.bfloat16)
+    ref = a.double() @ b.double().T
+    A, ac = _padded(a.T.contiguous() if a_mn else a)
+    B, bc = _padded(b.T.contiguous() if b_mn else b)
+    out = torch.full((M, N), float("nan"), device=DEV)
+    P.squint.selftest_gemm(A, ac, a_mn, B, bc, b_mn, M, N, K, out)
+    torch.cuda.synchronize()
+    compare("gemm", out.cpu().numpy(), ref.numpy(), 1e-5)
