@@ -567,14 +567,23 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ 
   if (warp == 0) tc::tmem_dealloc(tmem, ncols);
 }
 
+// out[i] = sum over CTA partials, fixed order: 4 threads per output each sum a quarter of the
+// partials, then the four quarter sums are added in order.
 __global__ void __launch_bounds__(256) k_reduce_enc(const float* __restrict__ part, int nchunk, int C,
                                                     float* __restrict__ gw2, float* __restrict__ gb2,
                                                     float* __restrict__ gw1, float* __restrict__ gb1) {
+  __shared__ float red[4][64];
   const int stride = bwd_stride(C);
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= stride) return;
+  const int i = blockIdx.x * 64 + (threadIdx.x & 63), sl = threadIdx.x >> 6;
+  const int c0 = (nchunk * sl) / 4, c1 = (nchunk * (sl + 1)) / 4;
   float s = 0.f;
-  for (int c = 0; c < nchunk; ++c) s += part[(int64_t)c * stride + i];
+  if (i < stride)
+    for (int c = c0; c < c1; ++c) s += __ldg(part + (int64_t)c * stride + i);
+  red[sl][threadIdx.x & 63] = s;
+  __syncthreads();
+  if (sl != 0 || i >= stride) return;
+  const int t = threadIdx.x;
+  s = ((red[0][t] + red[1][t]) + red[2][t]) + red[3][t];
   const int n2 = C * C * 9;
   if (i < n2) gw2[i] = s;
   else if (i < n2 + C) gb2[i - n2] = s;
@@ -615,7 +624,7 @@ int launch_enc_bwd_tc(const EncBwdArgs& a, cudaStream_t s) {
   k_enc_bwd_tc<<<grid, kThr, smem, s>>>(a);
   const int stride = bwd_stride(a.C);
   note_launch(s);
-  k_reduce_enc<<<(stride + 255) / 256, 256, 0, s>>>(a.part, grid, a.C, a.gw2, a.gb2, a.gw1, a.gb1);
+  k_reduce_enc<<<(stride + 63) / 64, 256, 0, s>>>(a.part, grid, a.C, a.gw2, a.gb2, a.gw1, a.gb1);
   return (int)cudaGetLastError();
 }
 

@@ -33,7 +33,8 @@ constexpr int kMaxStages = 8;
 constexpr int kABytes = 16384;  // 128 x 64 bf16
 constexpr float kLog2Pi = 1.8378770664093453f;
 constexpr float kSquashEps = 1e-6f;
-constexpr int kEpiBytes = 8 * 4 * 4096 + 4 * 3 * 512 * 4;  // per-warp box slots + LN-bwd column partials
+constexpr int kColaccOff = 4 * 4 * 4096;                  // after the 4 warp pairs' box rings
+constexpr int kEpiBytes = kColaccOff + 4 * 3 * 512 * 4;    // + LN-bwd column partials [4][3][512]
 
 int g_pdl = 1;
 
@@ -146,11 +147,12 @@ __device__ __forceinline__ void box_get(const uint8_t* slot, int c, float (&v)[3
     }
   }
 }
-// all lanes have written the box: make it visible to the TMA unit and store it
-__device__ __forceinline__ void box_store(uint8_t* slot, const void* map, int col, int row) {
+// both warps of pair q have written their halves of the box: make it visible to the TMA unit
+// and store it from the pair's first warp
+__device__ __forceinline__ void pair_store(uint8_t* slot, const void* map, int col, int row, int q, int hh) {
   tc::fence_async_smem();
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0) {
+  tc::named_bar(1 + q, 64);
+  if (hh == 0 && (threadIdx.x & 31) == 0) {
     tc::tma_store_2d(map, slot, col, row);
     tc::bulk_commit();
   }
@@ -186,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   __shared__ uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], done_bar, ld_bar[8];
   __shared__ uint32_t tmem_slot;
   __shared__ float red[2][2][128];
+  __shared__ float cl_red[2][128];  // this CTA's per-row partials, read by the cluster peers
   __shared__ __align__(16) float s_bias[512], s_g[512], s_beta[512];  // per-column epilogue params
 
   const int tile = blockIdx.x;
@@ -317,8 +320,39 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   const int N = P.N;
   const int nch = (nreal + 31) / 32;       // 32-column chunks of the tile
   const int ngrp = (nreal + 63) / 64;      // 64-column groups (TMA boxes); warp hh owns groups hh, hh+2, ...
-  uint8_t* slots = smem + warp * 4 * kSlotBytes;
+  uint8_t* pslots = smem + q * 4 * kSlotBytes;  // the warp pair's ring of 4 boxes
   float v[32], a[32];
+  // per-row totals over the whole LayerNorm row: the two column halves of this CTA (smem), then
+  // the CTAs of the cluster (distributed shared memory, summed in rank order: every CTA gets the
+  // same bits)
+  auto row_total = [&](float part, int k) -> float {
+    red[k][hh][rl] = part;
+    __syncthreads();
+    float t = red[k][0][rl] + red[k][1][rl];
+    if (b.cs > 1) {
+      if (hh == 0) cl_red[k][rl] = t;
+      tc::cluster_sync();
+      t = 0.f;
+      for (int rk = 0; rk < b.cs; ++rk) t += tc::dsmem_ld(&cl_red[k][rl], (uint32_t)rk);
+    }
+    return t;
+  };
+  auto row_total2 = [&](float p1, float p2, float& t1, float& t2) {
+    red[0][hh][rl] = p1;
+    red[1][hh][rl] = p2;
+    __syncthreads();
+    t1 = red[0][0][rl] + red[0][1][rl];
+    t2 = red[1][0][rl] + red[1][1][rl];
+    if (b.cs > 1) {
+      if (hh == 0) cl_red[0][rl] = t1, cl_red[1][rl] = t2;
+      tc::cluster_sync();
+      t1 = t2 = 0.f;
+      for (int rk = 0; rk < b.cs; ++rk) {
+        t1 += tc::dsmem_ld(&cl_red[0][rl], (uint32_t)rk);
+        t2 += tc::dsmem_ld(&cl_red[1][rl], (uint32_t)rk);
+      }
+    }
+  };
 
   if constexpr (EPI == GE_BIAS_F32 || EPI == GE_DW) {
     for (int ch = hh; ch < nch; ch += 2) {
@@ -367,178 +401,152 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
       }
     }
   } else if constexpr (EPI == GE_RELU_MASK) {
-    // mask source boxes by TMA, masked gradient written in place, stored by TMA
-    int k = 0;
-    for (int g = hh; g < ngrp; g += 2, ++k) {
-      uint8_t* sl = slots + (k & 3) * kSlotBytes;
-      if (k >= 4 && lane == 0) tc::bulk_wait_read<3>();
-      __syncwarp();
-      if (lane == 0) {
-        tc::mbar_expect_tx(&ld_bar[warp], kSlotBytes);
-        tc::tma_load_2d(sl, &b.maps[P.ymap], n0 + g * 64, row0, &ld_bar[warp]);
+    // mask-source boxes by TMA (loaded once per warp pair), masked gradient written in place,
+    // stored by TMA; warp hh of pair q owns the 32-column half hh of each 64-column box
+    for (int g = 0; g < ngrp; ++g) {
+      uint8_t* sl = pslots + (g & 3) * kSlotBytes;
+      if (g >= 4) {
+        if (hh == 0 && lane == 0) tc::bulk_wait_read<3>();
+        tc::named_bar(1 + q, 64);
       }
-      tc::mbar_wait(&ld_bar[warp], k & 1);
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int ch = 2 * g + c;
-        if (ch < nch) {
-          tc::tmem_ld32(trow + ch * 32, v);
-          box_get(sl, c, a);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = a[j] > 0.f ? v[j] : 0.f;
-          box_put(sl, c, v);
-        }
+      if (hh == 0 && lane == 0) {
+        tc::mbar_expect_tx(&ld_bar[q], kSlotBytes);
+        tc::tma_load_2d(sl, &b.maps[P.ymap], n0 + g * 64, row0, &ld_bar[q]);
       }
-      box_store(sl, &b.maps[P.omap], n0 + g * 64, row0);
+      tc::mbar_wait(&ld_bar[q], g & 1);
+      const int ch = 2 * g + hh;
+      if (ch < nch) {
+        tc::tmem_ld32(trow + ch * 32, v);
+        box_get(sl, hh, a);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = a[j] > 0.f ? v[j] : 0.f;
+        box_put(sl, hh, v);
+      }
+      pair_store(sl, &b.maps[P.omap], n0 + g * 64, row0, q, hh);
     }
   } else if constexpr (EPI == GE_LN_RELU || EPI == GE_LN_TANH) {
     float s1 = 0.f;
-    for (int g = hh; g < ngrp; g += 2)
+    for (int ch = hh; ch < nch; ch += 2) {
+      tc::tmem_ld32(trow + ch * 32, v);
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int ch = 2 * g + c;
-        if (ch < nch) {
-          tc::tmem_ld32(trow + ch * 32, v);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int cc = ch * 32 + j;
-            if (cc < N) s1 += v[j] + s_bias[cc];
-          }
-        }
+      for (int j = 0; j < 32; ++j) {
+        const int cc = ch * 32 + j;
+        if (cc < nreal) s1 += v[j] + s_bias[cc];
       }
-    red[0][hh][rl] = s1;
-    __syncthreads();
-    const float mean = (red[0][0][rl] + red[0][1][rl]) / (float)N;
+    }
+    const float mean = row_total(s1, 0) / (float)N;
     float s2 = 0.f;
-    for (int g = hh; g < ngrp; g += 2)
+    for (int ch = hh; ch < nch; ch += 2) {
+      tc::tmem_ld32(trow + ch * 32, v);
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int ch = 2 * g + c;
-        if (ch < nch) {
-          tc::tmem_ld32(trow + ch * 32, v);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int cc = ch * 32 + j;
-            const float dd = v[j] + s_bias[cc] - mean;
-            if (cc < N) s2 += dd * dd;
-          }
-        }
+      for (int j = 0; j < 32; ++j) {
+        const int cc = ch * 32 + j;
+        const float dd = v[j] + s_bias[cc] - mean;
+        if (cc < nreal) s2 += dd * dd;
       }
-    red[1][hh][rl] = s2;
-    __syncthreads();
-    const float rs = rsqrtf((red[1][0][rl] + red[1][1][rl]) / (float)N + P.ln_eps);
-    if (rv && hh == 0 && P.rstd) P.rstd[r] = rs;
+    }
+    const float rs = rsqrtf(row_total(s2, 1) / (float)N + P.ln_eps);
+    if (rv && hh == 0 && n0 == 0 && P.rstd) P.rstd[r] = rs;
     const bool tma_out = (N & 7) == 0;
-    int k = 0;
-    for (int g = hh; g < ngrp; g += 2, ++k) {
-      uint8_t* sy = slots + ((2 * k) & 3) * kSlotBytes;
-      uint8_t* sx = slots + ((2 * k + 1) & 3) * kSlotBytes;
-      if (k >= 2 && lane == 0) tc::bulk_wait_read<2>();  // slots of group k-2 read by the TMA unit
-      __syncwarp();
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int ch = 2 * g + c;
-        if (ch < nch) {
-          tc::tmem_ld32(trow + ch * 32, v);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int cc = ch * 32 + j;
-            const float x = (v[j] + s_bias[cc] - mean) * rs;
-            const float n = fmaf(x, s_g[cc], s_beta[cc]);
-            a[j] = x;
-            v[j] = (EPI == GE_LN_RELU) ? fmaxf(n, 0.f) : tanhf(n);
-          }
-          // TMA stores are masked at 16-byte granularity: an output block whose last column is
-          // not 8-aligned (the projection's z inside [z | s | a]) is stored directly instead.
-          if (tma_out) box_put(sy, c, v);
-          else if (rv) row_st_bf16(P.out + (int64_t)r * P.ldo + ch * 32, min(32, N - ch * 32), v);
-          if (P.xh) box_put(sx, c, a);
-        }
+    for (int g = 0; g < ngrp; ++g) {
+      uint8_t* sy = pslots + ((2 * g) & 3) * kSlotBytes;
+      uint8_t* sx = pslots + ((2 * g + 1) & 3) * kSlotBytes;
+      if (g >= 2) {  // the pair's slots of group g-2 must have been read by the TMA unit
+        if (hh == 0 && lane == 0) tc::bulk_wait_read<2>();
+        tc::named_bar(1 + q, 64);
       }
-      if (tma_out) box_store(sy, &b.maps[P.omap], g * 64, row0);
-      if (P.xh) box_store(sx, &b.maps[P.xmap], g * 64, row0);
+      const int ch = 2 * g + hh;
+      if (ch < nch) {
+        tc::tmem_ld32(trow + ch * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int cc = ch * 32 + j;
+          const float x = (v[j] + s_bias[cc] - mean) * rs;
+          const float n = fmaf(x, s_g[cc], s_beta[cc]);
+          a[j] = x;
+          v[j] = (EPI == GE_LN_RELU) ? fmaxf(n, 0.f) : tanh_fast(n);
+        }
+        // TMA stores are masked at 16-byte granularity: an output block whose last column is
+        // not 8-aligned (the projection's z inside [z | s | a]) is stored directly instead.
+        if (tma_out) box_put(sy, hh, v);
+        else if (rv) row_st_bf16(P.out + (int64_t)r * P.ldo + n0 + ch * 32, min(32, nreal - ch * 32), v);
+        if (P.xh) box_put(sx, hh, a);
+      }
+      if (tma_out) pair_store(sy, &b.maps[P.omap], n0 + g * 64, row0, q, hh);
+      if (P.xh) pair_store(sx, &b.maps[P.xmap], n0 + g * 64, row0, q, hh);
     }
   } else if constexpr (EPI == GE_BWD_LN_RELU || EPI == GE_BWD_LN_TANH) {
-    float* colacc = reinterpret_cast<float*>(smem + 8 * 4 * kSlotBytes);  // [4][3][512]
-    // this warp's x_hat boxes (<= 4 groups) by TMA, one transaction barrier
-    const int ngw = ngrp > hh ? (ngrp - hh + 1) / 2 : 0;
-    if (lane == 0 && ngw > 0) {
-      tc::mbar_expect_tx(&ld_bar[warp], ngw * kSlotBytes);
-      for (int k = 0; k < ngw; ++k)
-        tc::tma_load_2d(slots + k * kSlotBytes, &b.maps[P.xmap], (hh + 2 * k) * 64, row0, &ld_bar[warp]);
+    float* colacc = reinterpret_cast<float*>(smem + kColaccOff);  // [4][3][512]
+    // the pair's x_hat boxes (<= 4) by TMA on one transaction barrier
+    if (hh == 0 && lane == 0) {
+      tc::mbar_expect_tx(&ld_bar[q], ngrp * kSlotBytes);
+      for (int g = 0; g < ngrp; ++g)
+        tc::tma_load_2d(pslots + g * kSlotBytes, &b.maps[P.xmap], n0 + g * 64, row0, &ld_bar[q]);
     }
-    if (ngw > 0) tc::mbar_wait(&ld_bar[warp], 0);
+    tc::mbar_wait(&ld_bar[q], 0);
     float s1 = 0.f, s2 = 0.f;
-    int k = 0;
-    for (int g = hh; g < ngrp; g += 2, ++k) {
+    for (int g = 0; g < ngrp; ++g) {
+      const int ch = 2 * g + hh;
+      if (ch < nch) {
+        const int c0 = ch * 32, ncv = min(32, nreal - c0);
+        tc::tmem_ld32(trow + ch * 32, v);
+        box_get(pslots + g * kSlotBytes, hh, a);
+        float pg[32], pb[32];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int ch = 2 * g + c;
-        if (ch < nch) {
-          const int c0 = ch * 32, ncv = min(32, N - c0);
-          tc::tmem_ld32(trow + ch * 32, v);
-          box_get(slots + k * kSlotBytes, c, a);
-          float pg[32], pb[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int cc = c0 + j;
-            const bool ok = rv && (j < ncv);
-            const float x = ok ? a[j] : 0.f;
-            const float n = fmaf(x, s_g[cc], s_beta[cc]);
-            const float dn = ok ? ((EPI == GE_BWD_LN_RELU) ? (n > 0.f ? v[j] : 0.f) : v[j] * sech2f(n)) : 0.f;
-            const float dxh = dn * s_g[cc];
-            s1 += dxh;
-            s2 += dxh * x;
-            pg[j] = dn * x;
-            pb[j] = dn;
-          }
-          const float cg = colsum32(pg);
-          const float cb = colsum32(pb);
-          colacc[(q * 3 + 1) * 512 + c0 + lane] = cg;
-          colacc[(q * 3 + 2) * 512 + c0 + lane] = cb;
+        for (int j = 0; j < 32; ++j) {
+          const int cc = c0 + j;
+          const bool ok = rv && (j < ncv);
+          const float x = ok ? a[j] : 0.f;
+          const float n = fmaf(x, s_g[cc], s_beta[cc]);
+          const float dn = ok ? ((EPI == GE_BWD_LN_RELU) ? (n > 0.f ? v[j] : 0.f) : v[j] * sech2_fast(n)) : 0.f;
+          const float dxh = dn * s_g[cc];
+          s1 += dxh;
+          s2 += dxh * x;
+          pg[j] = dn * x;
+          pb[j] = dn;
         }
+        const float cg = colsum32(pg);
+        const float cb = colsum32(pb);
+        colacc[(q * 3 + 1) * 512 + c0 + lane] = cg;
+        colacc[(q * 3 + 2) * 512 + c0 + lane] = cb;
       }
     }
-    red[0][hh][rl] = s1;
-    red[1][hh][rl] = s2;
-    __syncthreads();
-    const float m1 = (red[0][0][rl] + red[0][1][rl]) / (float)N, m2 = (red[1][0][rl] + red[1][1][rl]) / (float)N;
+    float m1, m2;
+    row_total2(s1, s2, m1, m2);
+    m1 /= (float)N;
+    m2 /= (float)N;
     const float rs = rv ? P.rstd[r] : 0.f;
-    k = 0;
-    for (int g = hh; g < ngrp; g += 2, ++k) {
-      uint8_t* sl = slots + k * kSlotBytes;
+    for (int g = 0; g < ngrp; ++g) {
+      uint8_t* sl = pslots + g * kSlotBytes;
+      const int ch = 2 * g + hh;
+      if (ch < nch) {
+        const int c0 = ch * 32, ncv = min(32, nreal - c0);
+        tc::tmem_ld32(trow + ch * 32, v);
+        box_get(sl, hh, a);
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int ch = 2 * g + c;
-        if (ch < nch) {
-          const int c0 = ch * 32, ncv = min(32, N - c0);
-          tc::tmem_ld32(trow + ch * 32, v);
-          box_get(sl, c, a);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int cc = c0 + j;
-            const bool ok = rv && (j < ncv);
-            const float x = ok ? a[j] : 0.f;
-            const float n = fmaf(x, s_g[cc], s_beta[cc]);
-            const float dn = ok ? ((EPI == GE_BWD_LN_RELU) ? (n > 0.f ? v[j] : 0.f) : v[j] * sech2f(n)) : 0.f;
-            v[j] = ok ? rs * (dn * s_g[cc] - m1 - x * m2) : 0.f;
-            a[j] = v[j];
-          }
-          box_put(sl, c, v);
-          const float cx = colsum32(a);
-          colacc[(q * 3 + 0) * 512 + c0 + lane] = cx;
+        for (int j = 0; j < 32; ++j) {
+          const int cc = c0 + j;
+          const bool ok = rv && (j < ncv);
+          const float x = ok ? a[j] : 0.f;
+          const float n = fmaf(x, s_g[cc], s_beta[cc]);
+          const float dn = ok ? ((EPI == GE_BWD_LN_RELU) ? (n > 0.f ? v[j] : 0.f) : v[j] * sech2_fast(n)) : 0.f;
+          v[j] = ok ? rs * (dn * s_g[cc] - m1 - x * m2) : 0.f;
+          a[j] = v[j];
         }
+        box_put(sl, hh, v);
+        const float cx = colsum32(a);
+        colacc[(q * 3 + 0) * 512 + c0 + lane] = cx;
       }
-      box_store(sl, &b.maps[P.omap], g * 64, row0);
+      pair_store(sl, &b.maps[P.omap], n0 + g * 64, row0, q, hh);
     }
     __syncthreads();
     if (P.part) {
-      for (int e = tid; e < 3 * N; e += kThreads) {
-        const int kk = e / N, c = e - kk * N;
+      for (int e = tid; e < 3 * nreal; e += kThreads) {
+        const int kk = e / nreal, c = e - kk * nreal;
         float s = 0.f;
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) s += colacc[(qq * 3 + kk) * 512 + c];
-        P.part[((int64_t)mt * 3 + kk) * N + c] = s;
+        P.part[((int64_t)mt * 3 + kk) * N + n0 + c] = s;
       }
     }
   } else if constexpr (EPI == GE_TG_FWD) {
@@ -606,6 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   if (lane == 0) tc::bulk_wait_all();  // TMA stores have finished reading this CTA's smem
   tc::fence_before_sync();
   __syncthreads();
+  if (b.cs > 1) tc::cluster_sync();  // peers are done reading cl_red
   stamp(4);
   if (warp == 0) tc::tmem_dealloc(tmem, ncols);
 }
@@ -646,6 +655,7 @@ static unsigned long long* g_dbg_dev = nullptr;
 static int g_dbg_tiles = 0;
 int gemm_debug_times(unsigned long long* host, int max_entries) {
   if (!g_dbg_dev) return 0;
+  cudaDeviceSynchronize();
   const int n = g_dbg_tiles * 8 < max_entries ? g_dbg_tiles * 8 : max_entries;
   cudaMemcpy(host, g_dbg_dev, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   return n;
@@ -686,7 +696,21 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   GBatch& b = gb.b;
   if (gb.err) return -1;
   if (b.nprob == 0) return 0;
-  // plan tiles
+  // plan tiles.  LayerNorm epilogues need whole rows: with N >= 128 the row is split over a
+  // cluster of cs CTAs of 64-column multiples (more SMs share the epilogue work).
+  const int epi0 = b.p[0].epi;
+  const bool ln_launch = epi0 == GE_LN_RELU || epi0 == GE_LN_TANH || epi0 == GE_BWD_LN_RELU || epi0 == GE_BWD_LN_TANH;
+  b.cs = 1;
+  if (ln_launch) {
+    int cs = 8;
+    for (int i = 0; i < b.nprob; ++i) {
+      const int n = b.p[i].N;
+      const int c = n >= 256 && n % 256 == 0 ? 4 : (n >= 128 && n % 128 == 0 ? 2 : 1);
+      cs = c < cs ? c : cs;
+    }
+    static const bool no_cluster = getenv("SQUINT_NO_CLUSTER") != nullptr;
+    b.cs = no_cluster ? 1 : cs;
+  }
   int t = 0, bmax = 0;
   for (int i = 0; i < b.nprob; ++i) {
     GProb& p = b.p[i];
@@ -698,7 +722,7 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     const int n16 = (p.N + 15) & ~15;
     if (row_complete(p.epi)) {
       if (n16 > 512) return -1;
-      p.bn = n16;
+      p.bn = b.cs > 1 ? p.N / b.cs : n16;
     } else if (p.epi == GE_DW) {
       p.bn = n16 >= 256 ? 64 : (n16 > 128 ? 128 : n16);
     } else {
@@ -716,7 +740,15 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   b.stage_bytes = kABytes + bmax;
   int S = (200 * 1024) / b.stage_bytes;
   S = S > kMaxStages ? kMaxStages : S;
-  if (S < 2) return -1;
+  int maxkb = 0;  // no more stages than K blocks
+  for (int i = 0; i < b.nprob; ++i) {
+    int k = 0;
+    for (int j = 0; j < b.p[i].nseg; ++j) k += b.p[i].seg[j].nkb;
+    maxkb = k > maxkb ? k : maxkb;
+  }
+  S = S > maxkb ? maxkb : S;
+  S = S < 2 ? 2 : S;
+  if ((size_t)S * b.stage_bytes > 200 * 1024) return -1;
   b.nstages = S;
   // tensor maps
   b.nmaps = 0;
@@ -768,12 +800,24 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   }
   b.dbg = nullptr;
   {
+    // SQUINT_GEMM_DBG=k: only launch k records; SQUINT_GEMM_DBG=all: every launch gets its own
+    // 64-tile slot (launch i at slot i % 256), for whole-update kernel-span timelines.
     static const char* dbg_env = getenv("SQUINT_GEMM_DBG");
     static int launch_no = 0;
-    if (dbg_env && launch_no++ == atoi(dbg_env)) {
-      if (!g_dbg_dev) cudaMalloc(&g_dbg_dev, 4096 * 8 * sizeof(unsigned long long));
-      g_dbg_tiles = b.ntiles < 4096 ? b.ntiles : 4096;
-      b.dbg = g_dbg_dev;
+    if (dbg_env) {
+      const int me = launch_no++;
+      const bool all = dbg_env[0] == 'a';
+      if (!g_dbg_dev) {
+        cudaMalloc(&g_dbg_dev, 256 * 64 * 8 * sizeof(unsigned long long));
+        cudaMemset(g_dbg_dev, 0, 256 * 64 * 8 * sizeof(unsigned long long));
+      }
+      if (all) {
+        b.dbg = g_dbg_dev + (size_t)(me % 256) * 64 * 8;
+        g_dbg_tiles = 256 * 64;
+      } else if (me == atoi(dbg_env)) {
+        g_dbg_tiles = b.ntiles < 4096 ? b.ntiles : 4096;
+        b.dbg = g_dbg_dev;
+      }
     }
   }
   cudaLaunchConfig_t cfg;
@@ -782,12 +826,23 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
   static const bool no_pdl = getenv("SQUINT_NO_PDL") != nullptr;
-  cfg.numAttrs = (g_pdl && !no_pdl) ? 1 : 0;
+  if (g_pdl && !no_pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (b.cs > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = b.cs;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
   note_launch(s);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, b);
   static const bool dbg = getenv("SQUINT_DEBUG_SYNC") != nullptr;

@@ -95,6 +95,7 @@ struct GBatch {
   GProb p[kGemmMaxProb];
   int nprob, ntiles, nmaps;
   int stage_bytes, nstages;
+  int cs;  // cluster size: LayerNorm rows split over cs CTAs (statistics exchanged through DSMEM)
   unsigned long long* dbg;  // optional per-CTA phase timestamps (globaltimer ns) [tile][8]
 };
 

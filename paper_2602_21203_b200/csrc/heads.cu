@@ -55,10 +55,21 @@ __global__ void __launch_bounds__(256) k_target_ce(const __grid_constant__ Targe
   }
   __syncwarp();
   float* mrow = a.m + (int64_t)row * N;
+  // b_j is non-decreasing in j (g_j is increasing in z_j and clipping preserves order), so the
+  // atoms j with |b_j - k| < 1 form a contiguous range: binary search its start, then add the
+  // same terms in the same (ascending j) order as the full sum.
   for (int k = lane; k < N; k += 32) {
+    const float kf = (float)k;
+    int lo = 0, hi = N;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (bj[mid] - kf > -1.f) hi = mid;
+      else lo = mid + 1;
+    }
     float acc = 0.f;
-    for (int j = 0; j < N; ++j) {
-      const float wgt = 1.f - fabsf(bj[j] - (float)k);
+    for (int j = lo; j < N; ++j) {
+      const float wgt = 1.f - fabsf(bj[j] - kf);
+      if (bj[j] - kf >= 1.f) break;
       if (wgt > 0.f) acc = fmaf(pb[j], wgt, acc);
     }
     mrow[k] = acc;

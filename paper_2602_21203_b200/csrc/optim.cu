@@ -28,6 +28,10 @@ __global__ void __launch_bounds__(256) k_row_sums(const float* __restrict__ logp
   }
 }
 
+// Adam bias correction 1 / (1 - beta^t) = -1 / expm1(t ln(beta)), ln(beta) = log1p(beta - 1)
+// (beta - 1 exact): float, no cancellation
+__device__ __forceinline__ float bias_corr(float beta, int64_t t) { return -1.f / expm1f((float)t * log1pf(beta - 1.f)); }
+
 __global__ void __launch_bounds__(256) k_scalars(const __grid_constant__ ScalarsArgs a) {
   __shared__ float red[32];
   float sl = 0.f, sq = 0.f;
@@ -55,8 +59,8 @@ __global__ void __launch_bounds__(256) k_scalars(const __grid_constant__ Scalars
   const int64_t t = ++a.step[2];
   const float m = a.beta1 * a.m_alpha[0] + (1.f - a.beta1) * g;
   const float v = a.beta2 * a.v_alpha[0] + (1.f - a.beta2) * g * g;
-  const float c1 = (float)(1.0 / (1.0 - pow((double)a.beta1, (double)t)));
-  const float c2 = (float)(1.0 / (1.0 - pow((double)a.beta2, (double)t)));
+  const float c1 = bias_corr(a.beta1, t);
+  const float c2 = bias_corr(a.beta2, t);
   const float la1 = la - a.lr_alpha * (m * c1) / (sqrtf(v * c2) + a.adam_eps);
   a.m_alpha[0] = m;
   a.v_alpha[0] = v;
@@ -68,10 +72,10 @@ __global__ void __launch_bounds__(256) k_scalars(const __grid_constant__ Scalars
   a.scal[S_LALPHA] = loss;
   a.scal[S_LQ] = sq;
   const int64_t tc = ++a.step[0], ta = ++a.step[1];
-  a.scal[S_C1_CRITIC] = (float)(1.0 / (1.0 - pow((double)a.beta1, (double)tc)));
-  a.scal[S_C2_CRITIC] = (float)(1.0 / (1.0 - pow((double)a.beta2, (double)tc)));
-  a.scal[S_C1_ACTOR] = (float)(1.0 / (1.0 - pow((double)a.beta1, (double)ta)));
-  a.scal[S_C2_ACTOR] = (float)(1.0 / (1.0 - pow((double)a.beta2, (double)ta)));
+  a.scal[S_C1_CRITIC] = bias_corr(a.beta1, tc);
+  a.scal[S_C2_CRITIC] = bias_corr(a.beta2, tc);
+  a.scal[S_C1_ACTOR] = bias_corr(a.beta1, ta);
+  a.scal[S_C2_ACTOR] = bias_corr(a.beta2, ta);
 }
 
 __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, const float4* __restrict__ g,
@@ -175,19 +179,20 @@ __global__ void __launch_bounds__(256) k_metrics(const __grid_constant__ Metrics
   }
 }
 
-// flat index i of a group buffer -> its shadow slot, or -1
-__device__ __forceinline__ int64_t shadow_slot(const ShadowTable& t, int64_t i) {
+// flat index i of a group buffer -> its shadow slot, or -1 (32-bit index math: every group
+// buffer is < 2^31 floats)
+__device__ __forceinline__ int shadow_slot(const ShadowTable& t, int i) {
   for (int k = 0; k < t.n; ++k) {
     const ShadowEnt& e = t.e[k];
-    const int64_t l = i - e.src;
-    if (l >= 0 && l < (int64_t)e.rows * e.cols) {
-      const int row = (int)(l / e.cols), col = (int)(l - (int64_t)row * e.cols);
+    const int l = i - (int)e.src;
+    if (l >= 0 && l < e.rows * e.cols) {
+      const int row = l / e.cols, col = l - row * e.cols;
       int cc = col;
       if (e.perm_c > 0) {
         const int ch = col / e.perm_p, pix = col - ch * e.perm_p;
         cc = pix * e.perm_c + ch;
       }
-      return e.dst + (int64_t)row * e.ld + cc;
+      return (int)e.dst + row * e.ld + cc;
     }
   }
   return -1;
@@ -196,10 +201,15 @@ __device__ __forceinline__ int64_t shadow_slot(const ShadowTable& t, int64_t i) 
 __global__ void __launch_bounds__(256) k_shadow(const float* __restrict__ master, const __grid_constant__ ShadowTable t) {
   for (int k = 0; k < t.n; ++k) {
     const ShadowEnt& e = t.e[k];
-    const int64_t n = (int64_t)e.rows * e.cols;
-    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n; l += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t sl = shadow_slot(t, e.src + l);
-      t.base[sl] = __float2bfloat16_rn(master[e.src + l]);
+    const int n = e.rows * e.cols;
+    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < n; l += gridDim.x * blockDim.x) {
+      const int row = l / e.cols, col = l - row * e.cols;
+      int cc = col;
+      if (e.perm_c > 0) {
+        const int ch = col / e.perm_p, pix = col - ch * e.perm_p;
+        cc = pix * e.perm_c + ch;
+      }
+      t.base[(int)e.dst + row * e.ld + cc] = __float2bfloat16_rn(master[e.src + l]);
     }
   }
 }
@@ -231,7 +241,7 @@ __global__ void __launch_bounds__(256) k_adam_sh(float4* __restrict__ p, const f
     if (t.n) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int64_t sl = shadow_slot(t, 4 * i + k);
+        const int sl = shadow_slot(t, (int)(4 * i + k));
         if (sl >= 0) t.base[sl] = __float2bfloat16_rn(pf[k]);
       }
     }
@@ -257,7 +267,7 @@ __global__ void __launch_bounds__(256) k_polyak_sh(float4* __restrict__ t4, cons
       const float* af = reinterpret_cast<const float*>(&a);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int64_t sl = shadow_slot(t, 4 * i + k);
+        const int sl = shadow_slot(t, (int)(4 * i + k));
         if (sl >= 0) t.base[sl] = __float2bfloat16_rn(af[k]);
       }
     }
