@@ -269,7 +269,6 @@ def run_gpu(args):
     torch.cuda.synchronize()
     launches_per_step = S.launch_count() - c0
 
-    timers = [S.PhaseTimer(UTD) for _ in range(NPOOL)]
     graphs = []
     use_graph = not args.no_graph
     if use_graph:
@@ -281,10 +280,8 @@ def run_gpu(args):
         torch.cuda.synchronize()
         for p in range(NPOOL):
             gph = torch.cuda.CUDAGraph()
-            timers[p].enable()
             with torch.cuda.graph(gph):
                 step(p)
-            S.PhaseTimer.disable()
             graphs.append(gph)
         torch.cuda.synchronize()
 
@@ -293,9 +290,7 @@ def run_gpu(args):
         if use_graph:
             graphs[k % NPOOL].replay()
         else:
-            timers[k % NPOOL].enable()
             step(k % NPOOL)
-            S.PhaseTimer.disable()
 
     for w in range(W):
         run_one(w)
@@ -326,12 +321,33 @@ def run_gpu(args):
         print(f"rank {rank}: non-finite metrics {met}", file=sys.stderr)
         sys.exit(3)
 
-    # phase times (average over the pools' last replays)
-    ph = {}
-    for t in timers:
-        for k, v in t.times_ms().items():
-            ph.setdefault(k, []).append(v)
-    ph = {k: sum(v) / len(v) for k, v in ph.items()}
+    # per-kernel device time inside the step: a second capture of the same step with a CUDA event
+    # before every libsquint launch (libsquint's launch timeline), replayed after the timed region.
+    # Events between kernels add small gaps and stop programmatic-launch overlap, so these
+    # durations are slightly pessimistic; shares are taken against their own sum.
+    kern = {}
+    if use_graph and not args.no_timeline:
+        tl = S.LaunchTimeline(4096)
+        s2 = torch.cuda.Stream(device=dev)
+        s2.wait_stream(torch.cuda.current_stream())
+        gtl = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s2):
+            tl.start()
+        with torch.cuda.graph(gtl, stream=s2):
+            step(0, stream=s2)
+            tl.stop(s2)
+        torch.cuda.synchronize()
+        R = 10
+        for r in range(R):
+            load_inputs(W + (r % K))
+            gtl.replay()
+            torch.cuda.synchronize()
+            for name, fl, by, us in tl.durations():
+                e = kern.setdefault(name, {"us": 0.0, "n": 0, "flops": 0.0, "bytes": 0.0})
+                e["us"] += us / R
+                e["n"] += 1.0 / R
+                e["flops"] += fl / R
+                e["bytes"] += by / R
 
     # e2e: same step through the C ABI from pinned host buffers (H2D inputs, D2H results)
     e2e = None
@@ -381,32 +397,33 @@ def run_gpu(args):
             dist.destroy_process_group()
         return
 
-    # roofline on the dominant phase
+    # roofline of the dominant kernel (largest device time per step in the timeline)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    fl, by = phase_work(d, N_ENV)
+    traffic_tab = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))) if os.path.exists(
+        os.path.join(ROOT, "profiles", "traffic.json")) else {}
     step_ms = ms / K
-    dom = max(ph, key=ph.get) if ph else None
     roof = None
-    if dom:
-        reps = UTD if dom not in ("insert", "act_encode", "act_mlp") else 1
-        t_launch = ph[dom] / reps / 1e3  # seconds per launch of the phase
-        if dom in by and dom not in fl:
-            ach = by[dom] / t_launch / 1e9
-            peak = peaks.get("hbm_gbs", 6650.0)
-            roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s"}
-        elif precision == P.BF16:
-            ach = fl[dom] / t_launch / 1e12
-            peak = peaks.get("bf16_tflops_sustained", 1400.0)
-            roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s"}
+    if kern:
+        tot_us = sum(e["us"] for e in kern.values())
+        dom = max(kern, key=lambda k: kern[k]["us"])
+        e = kern[dom]
+        t_launch = e["us"] / e["n"] * 1e-6  # seconds per launch
+        if e["flops"] > 0:
+            peak = peaks.get("bf16_tflops_sustained", 1400.0)  # kernel timed inside a long step
+            roof = {"bound": "tensor", "achieved": e["flops"] / e["n"] / t_launch / 1e12, "peak": peak,
+                    "unit": "TFLOP/s", "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (of measured)"}
         else:
-            ach = fl[dom] / t_launch / 1e12
-            peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12  # fp32 FFMA, DESIGN.md §6
-            roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s"}
+            peak = peaks.get("hbm_gbs", 6650.0)
+            roof = {"bound": "hbm", "achieved": e["bytes"] / e["n"] / t_launch / 1e9, "peak": peak, "unit": "GB/s",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
         roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["traffic"] = None
+        roof["traffic"] = traffic_tab.get(dom)
         roof["kernel"] = dom
-        roof["share_of_step"] = ph[dom] / step_ms if step_ms > 0 else None
+        roof["launches_per_step"] = round(e["n"], 2)
+        roof["us_per_launch"] = e["us"] / e["n"]
+        roof["share_of_step"] = e["us"] / tot_us if tot_us > 0 else None
+    kernels_us = {k: round(v["us"], 2) for k, v in sorted(kern.items(), key=lambda kv: -kv[1]["us"])}
     cpu = None
     if world == 1 and not args.no_cpu:
         ts = [oracle_sample(seed=s) for s in range(args.cpu_samples)]
@@ -421,7 +438,7 @@ def run_gpu(args):
                        "n_env": N_ENV, "parallelism": f"dp{world}", "l2": "ring 1.66 GB + 3 rotating 100 MB frame pools > L2",
                        "graph": use_graph},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-            "gpu_launches": int(launches_per_step * K), "phases_ms_per_step": ph}
+            "gpu_launches": int(launches_per_step * K), "kernels_us_per_step": kernels_us}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -438,6 +455,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=3)
+    ap.add_argument("--no-timeline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps

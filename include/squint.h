@@ -213,6 +213,12 @@ SQUINT_API const char* squint_phase_name(int k);
  * launch (i < n), so consecutive events bracket one launch including any gap after it.
  * Returns the number of events recorded since the previous call; NULL/0 disables. */
 SQUINT_API int squint_set_launch_events(void** events, int n);
+/* Records the next timeline event on `stream` without a launch (closes the last interval). */
+SQUINT_API squint_status squint_record_launch_event(squint_stream_t stream);
+/* Kernel name (static string) and algorithmic work of timeline launch i: FLOPs and bytes by the
+ * problem definition (2*M*N*K summed over a grouped GEMM's problems; bytes an HBM/L2-bound
+ * kernel must move), 0 when not tracked.  Host-only. */
+SQUINT_API squint_status squint_launch_info(int i, const char** name, double* flops, double* bytes);
 
 #ifdef __cplusplus
 }

@@ -66,7 +66,9 @@ SQ_DEV float tanh_fast(float u) {
 
 namespace sq {
 // Host-side count of kernel launches issued by libsquint (bench "gpu_launches" claim).
-void note_launch(cudaStream_t s);  // call right before each launch on stream s
+// Call right before each launch on stream s: kernel name and its algorithmic work (FLOPs and
+// DRAM/L2 bytes by the problem definition, 0 when not tracked) for the bench's roofline.
+void note_launch(cudaStream_t s, const char* name, double flops, double bytes);
 long launch_count();
 // Optional phase instrumentation (squint_set_phase_events): records cudaEvent pairs
 // around named phases of squint_update / squint_act / squint_insert on the launch stream.

@@ -402,7 +402,7 @@ static int launch_tn(const DenseBatch& b, cudaStream_t s) {
     cudaFuncSetAttribute(k_dense_f32<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  note_launch(s); k_dense_f32<TN><<<b.ntiles, 256, smem, s>>>(b);
+  note_launch(s, "k_dense_f32", 0, 0); k_dense_f32<TN><<<b.ntiles, 256, smem, s>>>(b);
   return (int)cudaGetLastError();
 }
 
@@ -418,7 +418,7 @@ int launch_dense_f32(const DenseBatch& b, int tn, cudaStream_t s) {
 
 int launch_dw_f32(const DwBatch& b, cudaStream_t s) {
   if (b.ntiles == 0) return 0;
-  note_launch(s); k_dw_f32<<<b.ntiles, 256, 0, s>>>(b);
+  note_launch(s, "k_dw_f32", 0, 0); k_dw_f32<<<b.ntiles, 256, 0, s>>>(b);
   return (int)cudaGetLastError();
 }
 

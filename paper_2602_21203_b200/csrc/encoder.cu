@@ -368,7 +368,7 @@ int launch_enc_fwd(const EncFwdArgs& a, cudaStream_t s) {
   const size_t smem = fwd_smem(a.C, a.c_in, a.H, ipb);
   cudaFuncSetAttribute(k_enc_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((a.B + ipb - 1) / ipb, a.nsrc);
-  note_launch(s); k_enc_fwd<<<grid, 256, smem, s>>>(a, ipb);
+  note_launch(s, "k_enc_fwd", 0, 0); k_enc_fwd<<<grid, 256, smem, s>>>(a, ipb);
   return (int)cudaGetLastError();
 }
 
@@ -378,7 +378,7 @@ int launch_enc_bwd(const EncBwdArgs& a, cudaStream_t s) {
     const int ipb = bwd_ipb(C);
     const size_t smem = sizeof(float) * (size_t)(C * C * 9 + ipb * C * P2);
     cudaFuncSetAttribute(k_enc_bwd_dx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    note_launch(s); k_enc_bwd_dx<<<(a.B + ipb - 1) / ipb, 256, smem, s>>>(a, ipb);
+    note_launch(s, "k_enc_bwd_dx", 0, 0); k_enc_bwd_dx<<<(a.B + ipb - 1) / ipb, 256, smem, s>>>(a, ipb);
   }
   float* part2 = a.part;
   float* part1 = a.part + (size_t)a.nchunk * (C * C * 9 + C);
@@ -386,20 +386,20 @@ int launch_enc_bwd(const EncBwdArgs& a, cudaStream_t s) {
     const int ob = ob_of(C, C);
     const size_t smem = sizeof(float) * (size_t)(ob * P2 + C * P1);
     cudaFuncSetAttribute(k_conv_dw<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    note_launch(s); k_conv_dw<false><<<dim3(a.nchunk, C / ob), 256, smem, s>>>(a.dA2, a.dA2_hwc, a.y1, a.y1_hwc, a.B, C, C, H1, H2, 1, ob, a.nchunk,
+    note_launch(s, "k_conv_dw", 0, 0); k_conv_dw<false><<<dim3(a.nchunk, C / ob), 256, smem, s>>>(a.dA2, a.dA2_hwc, a.y1, a.y1_hwc, a.B, C, C, H1, H2, 1, ob, a.nchunk,
                                                                  part2);
   }
   {
     const int ob = ob_of(C, a.c_in);
     const size_t smem = sizeof(float) * (size_t)(ob * P1 + a.c_in * a.H * a.H);
     cudaFuncSetAttribute(k_conv_dw<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    note_launch(s); k_conv_dw<true><<<dim3(a.nchunk, C / ob), 256, smem, s>>>(a.dA1, nullptr, a.img, nullptr, a.B, C, a.c_in, a.H, H1, 2, ob,
+    note_launch(s, "k_conv_dw", 0, 0); k_conv_dw<true><<<dim3(a.nchunk, C / ob), 256, smem, s>>>(a.dA1, nullptr, a.img, nullptr, a.B, C, a.c_in, a.H, H1, 2, ob,
                                                                a.nchunk, part1);
   }
   {
     const int n2 = C * C * 9 + C, n1 = C * a.c_in * 9 + C;
-    note_launch(s); k_reduce_part<<<(n2 + 255) / 256, 256, 0, s>>>(part2, a.nchunk, C * C * 9, C, a.gw2, a.gb2);
-    note_launch(s); k_reduce_part<<<(n1 + 255) / 256, 256, 0, s>>>(part1, a.nchunk, C * a.c_in * 9, C, a.gw1, a.gb1);
+    note_launch(s, "k_reduce_part", 0, 0); k_reduce_part<<<(n2 + 255) / 256, 256, 0, s>>>(part2, a.nchunk, C * C * 9, C, a.gw2, a.gb2);
+    note_launch(s, "k_reduce_part", 0, 0); k_reduce_part<<<(n1 + 255) / 256, 256, 0, s>>>(part1, a.nchunk, C * a.c_in * 9, C, a.gw1, a.gb1);
   }
   return (int)cudaGetLastError();
 }
@@ -411,12 +411,12 @@ int launch_insert(const uint8_t* frames, int64_t n, int c, int h, int w, int fac
     const int64_t items = n * c * (h / 8) * (w / 16);
     int64_t blocks = (items + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    note_launch(s); k_insert_f8<<<(unsigned)blocks, 256, 0, s>>>(frames, n, c, h, w, slots, ring);
+    note_launch(s, "k_insert_f8", 0, (double)n * c * h * w + (double)n * c * (h / 8) * (w / 8)); k_insert_f8<<<(unsigned)blocks, 256, 0, s>>>(frames, n, c, h, w, slots, ring);
   } else {
     const int64_t items = n * c * (h / factor) * (w / factor);
     int64_t blocks = (items + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    note_launch(s); k_insert_generic<<<(unsigned)blocks, 256, 0, s>>>(frames, n, c, h, w, factor, slots, ring);
+    note_launch(s, "k_insert_generic", 0, (double)n * c * h * w + (double)n * c * (h / factor) * (w / factor)); k_insert_generic<<<(unsigned)blocks, 256, 0, s>>>(frames, n, c, h, w, factor, slots, ring);
   }
   return (int)cudaGetLastError();
 }

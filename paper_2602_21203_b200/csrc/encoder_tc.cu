@@ -602,7 +602,12 @@ int launch_enc_fwd_tc(const EncFwdArgs& a, cudaStream_t s) {
   cudaFuncSetAttribute(k_enc_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int total = ((a.B + kG - 1) / kG) * a.nsrc;
   const int grid = total < 148 ? total : 148;
-  note_launch(s);
+  {
+    const double img = (double)a.B * a.nsrc, C = a.C;
+    const double flops = 2.0 * img * (49.0 * C * 27.0 + 25.0 * 9.0 * C * C);
+    const double bytes = a.mode == 1 ? img * (3.0 * 128 * 128 + 2.0 * 25 * C) : img * (768.0 + 2.0 * 25 * C);
+    note_launch(s, "k_enc_fwd_tc", flops, bytes);
+  }
   k_enc_fwd_tc<<<grid, kThr, smem, s>>>(a);
   return (int)cudaGetLastError();
 }
@@ -620,10 +625,13 @@ int launch_enc_bwd_tc(const EncBwdArgs& a, cudaStream_t s) {
   cudaFuncSetAttribute(k_enc_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int ngroups = (a.B + kG - 1) / kG;
   const int grid = ngroups < 148 ? ngroups : 148;
-  note_launch(s);
+  {
+    const double C = a.C;
+    note_launch(s, "k_enc_bwd_tc", 2.0 * a.B * (2.0 * 25.0 * 9.0 * C * C + 49.0 * 27.0 * C), 0);
+  }
   k_enc_bwd_tc<<<grid, kThr, smem, s>>>(a);
   const int stride = bwd_stride(a.C);
-  note_launch(s);
+  note_launch(s, "k_reduce_enc", 0, 0);
   k_reduce_enc<<<(stride + 63) / 64, 256, 0, s>>>(a.part, grid, a.C, a.gw2, a.gb2, a.gw1, a.gb1);
   return (int)cudaGetLastError();
 }

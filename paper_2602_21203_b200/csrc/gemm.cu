@@ -689,6 +689,7 @@ void GemmBuilder::seg(GProb& p, const Mat& A, int a_mn, int a_k, const Mat& Bm, 
   s.a_k = a_k;
   s.b_k = b_k;
   s.nkb = (K + 63) / 64;
+  s.k = K;
   p.nseg++;
 }
 
@@ -843,7 +844,15 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  note_launch(s);
+  {
+    static const char* names[9] = {"k_gemm<ln_relu>", "k_gemm<ln_tanh>", "k_gemm<bias>", "k_gemm<tg_fwd>",
+                                   "k_gemm<bwd_ln_relu>", "k_gemm<bwd_ln_tanh>", "k_gemm<relu_mask>",
+                                   "k_gemm<tg_bwd>", "k_gemm<dw>"};
+    double flops = 0;
+    for (int i = 0; i < b.nprob; ++i)
+      for (int k = 0; k < b.p[i].nseg; ++k) flops += 2.0 * b.p[i].M * (double)(b.p[i].N - b.p[i].acc_col0) * b.p[i].seg[k].k;
+    note_launch(s, names[epi], flops, 0);
+  }
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, b);
   static const bool dbg = getenv("SQUINT_DEBUG_SYNC") != nullptr;
   if (dbg) {

@@ -41,6 +41,7 @@ struct GSeg {
   int a_mn, b_mn;  // 1: operand is MN-major (matrix rows run along K)
   int a_k, b_k;    // K coordinate of the segment start inside the A / B matrix
   int nkb;         // 64-wide K blocks in the segment
+  int k;           // real K of the segment (algorithmic FLOP count)
 };
 
 struct GProb {

@@ -142,12 +142,12 @@ __global__ void __launch_bounds__(256) k_actor_q(const __grid_constant__ ActorQA
 int launch_target_ce(const TargetCEArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(float) * 2 * a.N * kRows;
   cudaFuncSetAttribute(k_target_ce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  note_launch(s); k_target_ce<<<(a.B + kRows - 1) / kRows, 256, smem, s>>>(a);
+  note_launch(s, "k_target_ce", 0, 0); k_target_ce<<<(a.B + kRows - 1) / kRows, 256, smem, s>>>(a);
   return (int)cudaGetLastError();
 }
 
 int launch_actor_q(const ActorQArgs& a, cudaStream_t s) {
-  note_launch(s); k_actor_q<<<(a.B + kRows - 1) / kRows, 256, 0, s>>>(a);
+  note_launch(s, "k_actor_q", 0, 0); k_actor_q<<<(a.B + kRows - 1) / kRows, 256, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 

@@ -9,7 +9,7 @@
 #include "common.cuh"
 
 namespace sq {
-
+struct LaunchInfo;
 static std::atomic<long> g_launches{0};
 static void** g_events = nullptr;  // cudaEvent_t[n_phases][reps][2]
 static int g_phases = 0, g_reps = 0;
@@ -18,10 +18,16 @@ static int g_phases = 0, g_reps = 0;
 // right before each launch, so event k..k+1 brackets launch k (kernel + any gap before k+1).
 static void** g_lev = nullptr;
 static int g_lev_n = 0, g_lev_used = 0;
+struct LaunchInfo {
+  const char* name;
+  double flops, bytes;
+};
+static LaunchInfo g_info[8192];
 
-void note_launch(cudaStream_t s) {
+void note_launch(cudaStream_t s, const char* name, double flops, double bytes) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (g_lev && g_lev_used < g_lev_n) {
+    if (g_lev_used < 8192) g_info[g_lev_used] = LaunchInfo{name, flops, bytes};
     cudaError_t e = cudaEventRecordWithFlags((cudaEvent_t)g_lev[g_lev_used++], s, cudaEventRecordExternal);
     if (e != cudaSuccess) {
       fprintf(stderr, "[squint] launch event %d: %s\n", g_lev_used - 1, cudaGetErrorString(e));
@@ -45,6 +51,23 @@ PhaseScope::~PhaseScope() {
 extern "C" {
 
 SQUINT_API long squint_launch_count(void) { return sq::launch_count(); }
+
+// Closes the launch timeline: records the next event with no launch (end of the last kernel).
+SQUINT_API squint_status squint_record_launch_event(squint_stream_t s) {
+  if (sq::g_lev && sq::g_lev_used < sq::g_lev_n) {
+    if (sq::g_lev_used < 8192) sq::g_info[sq::g_lev_used] = sq::LaunchInfo{"(end)", 0, 0};
+    cudaEventRecordWithFlags((cudaEvent_t)sq::g_lev[sq::g_lev_used++], (cudaStream_t)s, cudaEventRecordExternal);
+  }
+  return SQUINT_OK;
+}
+// Name and algorithmic work of launch i of the current/last timeline.
+SQUINT_API squint_status squint_launch_info(int i, const char** name, double* flops, double* bytes) {
+  if (i < 0 || i >= 8192 || !name || !flops || !bytes) return SQUINT_EINVAL;
+  *name = sq::g_info[i].name ? sq::g_info[i].name : "";
+  *flops = sq::g_info[i].flops;
+  *bytes = sq::g_info[i].bytes;
+  return SQUINT_OK;
+}
 
 SQUINT_API int squint_set_launch_events(void** events, int n) {
   const int used = sq::g_lev_used;

@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(256) k_polyak_sh(float4* __restrict__ t4, cons
 
 int launch_shadow(const float* master, const ShadowTable& t, cudaStream_t s) {
   if (t.n == 0) return 0;
-  note_launch(s); k_shadow<<<148 * 2, 256, 0, s>>>(master, t);
+  note_launch(s, "k_shadow", 0, 0); k_shadow<<<148 * 2, 256, 0, s>>>(master, t);
   return (int)cudaGetLastError();
 }
 
@@ -287,7 +287,7 @@ int launch_adam_shadow(float* p, const float* g, float* m, float* v, int64_t n, 
                        cudaStream_t s) {
   ShadowTable none;
   memset(&none, 0, sizeof(none));
-  note_launch(s);
+  note_launch(s, "k_adam", 0, 28.0 * (double)n);
   k_adam_sh<<<kAdamBlocks, 256, 0, s>>>(reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
                                         reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n / 4, lr, b1, b2,
                                         eps, c1, c2, sumsq_part, t ? *t : none);
@@ -301,25 +301,25 @@ int launch_polyak_shadow(float* target, const float* online, int64_t n, float ta
   memset(&none, 0, sizeof(none));
   int64_t blocks = (n / 4 + 255) / 256;
   if (blocks > 148 * 4) blocks = 148 * 4;
-  note_launch(s);
+  note_launch(s, "k_polyak", 0, 12.0 * (double)n);
   k_polyak_sh<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<float4*>(target), reinterpret_cast<const float4*>(online),
                                                n / 4, tau, t ? *t : none);
   return (int)cudaGetLastError();
 }
 
 int launch_row_sums(const float* logp, const float* row_loss, int B, float* extras, cudaStream_t s) {
-  note_launch(s); k_row_sums<<<1, 256, 0, s>>>(logp, row_loss, B, extras);
+  note_launch(s, "k_row_sums", 0, 0); k_row_sums<<<1, 256, 0, s>>>(logp, row_loss, B, extras);
   return (int)cudaGetLastError();
 }
 
 int launch_scalars(const ScalarsArgs& a, cudaStream_t s) {
-  note_launch(s); k_scalars<<<1, 256, 0, s>>>(a);
+  note_launch(s, "k_scalars", 0, 0); k_scalars<<<1, 256, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 
 int launch_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
                 const float* c1, const float* c2, float* sumsq_part, cudaStream_t s) {
-  note_launch(s); k_adam<<<kAdamBlocks, 256, 0, s>>>(reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
+  note_launch(s, "k_adam", 0, 28.0 * (double)n); k_adam<<<kAdamBlocks, 256, 0, s>>>(reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
                                      reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n / 4, lr, b1, b2,
                                      eps, c1, c2, sumsq_part);
   return (int)cudaGetLastError();
@@ -330,17 +330,17 @@ int launch_polyak(float* target, const float* online, int64_t n, float tau, cuda
   int64_t blocks = (n / 4 + 255) / 256;
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  note_launch(s); k_polyak<<<(unsigned)blocks, 256, 0, s>>>(target, online, n, tau);
+  note_launch(s, "k_polyak", 0, 12.0 * (double)n); k_polyak<<<(unsigned)blocks, 256, 0, s>>>(target, online, n, tau);
   return (int)cudaGetLastError();
 }
 
 int launch_metrics(const MetricsArgs& a, cudaStream_t s) {
-  note_launch(s); k_metrics<<<1, 256, 0, s>>>(a);
+  note_launch(s, "k_metrics", 0, 0); k_metrics<<<1, 256, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 
 int launch_lpi_sums(const float* row_lpi, const float* row_q, int B, float* out2, cudaStream_t s) {
-  note_launch(s); k_lpi_sums<<<1, 256, 0, s>>>(row_lpi, row_q, B, out2);
+  note_launch(s, "k_lpi_sums", 0, 0); k_lpi_sums<<<1, 256, 0, s>>>(row_lpi, row_q, B, out2);
   return (int)cudaGetLastError();
 }
 

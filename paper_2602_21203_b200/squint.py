@@ -80,6 +80,8 @@ def _load():
         "squint_set_phase_events": (st, [C.POINTER(vp), i32, i32]),
         "squint_phase_name": (C.c_char_p, [i32]),
         "squint_set_launch_events": (i32, [C.POINTER(vp), i32]),
+        "squint_record_launch_event": (st, [vp]),
+        "squint_launch_info": (st, [i32, C.POINTER(C.c_char_p), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -93,7 +95,7 @@ EXPORTED = ["squint_last_error", "squint_version", "squint_param_layout", "squin
             "squint_workspace_region", "squint_act_workspace_bytes", "squint_comm_unique_id", "squint_comm_init",
             "squint_comm_destroy", "squint_insert", "squint_act", "squint_update", "squint_soft_update",
             "squint_launch_count", "squint_set_phase_events", "squint_phase_name", "squint_selftest_gemm",
-            "squint_set_launch_events"]
+            "squint_set_launch_events", "squint_record_launch_event", "squint_launch_info"]
 N_PHASES = 16
 
 
@@ -137,6 +139,37 @@ class PhaseTimer:
                     pass
             if hit:
                 out[phase_name(k)] = tot
+        return out
+
+
+class LaunchTimeline:
+    """CUDA events around every libsquint launch (squint_set_launch_events), for per-kernel
+    device durations inside a captured graph.  Capture the work between start() and stop(stream)."""
+
+    def __init__(self, n=4096):
+        self.n = n
+        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+        for e in self.events:
+            e.record()
+        torch.cuda.synchronize()
+        self._arr = (C.c_void_p * n)(*[e.cuda_event for e in self.events])
+        self.used = 0
+
+    def start(self):
+        LIB.squint_set_launch_events(self._arr, self.n)
+
+    def stop(self, stream=None):
+        LIB.squint_record_launch_event(_stream(stream))
+        self.used = LIB.squint_set_launch_events(None, 0)
+        return self.used
+
+    def durations(self):
+        """[(name, flops, bytes, us)] for each recorded launch (after the events completed)."""
+        out = []
+        for i in range(self.used - 1):
+            nm, fl, by = C.c_char_p(), C.c_double(), C.c_double()
+            _check(LIB.squint_launch_info(i, C.byref(nm), C.byref(fl), C.byref(by)))
+            out.append((nm.value.decode(), fl.value, by.value, self.events[i].elapsed_time(self.events[i + 1]) * 1e3))
         return out
 
 
