@@ -42,6 +42,7 @@ struct EncFwdArgs {
   __nv_bfloat16* y1b;      // tensor-core path: conv1 activations of source 0, bf16 HWC [B][49][C]
   GatherJob gj[2][4];
   int ngj[2];
+  const uint8_t* wtiles;   // tensor-core path: conv weights as swizzled bf16 smem images (k_conv_tiles)
 };
 
 struct EncBwdArgs {
@@ -57,6 +58,7 @@ struct EncBwdArgs {
   float* part;             // partial weight grads [nchunk][C*C*9 + C + C*c*9 + C]
   int nchunk;
   float* gw1; float* gb1; float* gw2; float* gb2;  // final grads (CRITIC layout)
+  const uint8_t* wtiles;   // tensor-core path: conv weights as swizzled bf16 smem images (k_conv_tiles)
 };
 
 int launch_enc_fwd(const EncFwdArgs& a, cudaStream_t s);
@@ -69,6 +71,10 @@ int launch_enc_bwd(const EncBwdArgs& a, cudaStream_t s);
 // and a fixed-order reduction (deterministic).
 int launch_enc_bwd_tc(const EncBwdArgs& a, cudaStream_t s);
 size_t enc_bwd_tc_partial_floats(int C, int B);
+// Conv weights (fp32 master, Q7 layouts) -> the bf16 128B-swizzled smem images the tensor-core
+// encoder kernels bulk-copy: forward [W1 tile | W2 tiles], backward [W2^T tiles].
+size_t conv_tiles_bytes(int C);
+int launch_conv_tiles(const float* w1, const float* w2, int C, uint8_t* tiles, cudaStream_t s);
 size_t enc_bwd_partial_floats(int C, int c_in, int nchunk);
 int enc_bwd_nchunk(int B);
 

@@ -18,6 +18,9 @@ namespace {
 
 constexpr int kRows = 8;  // rows (warps) per block
 
+// Row values live in registers: lane holds atoms k = lane + 32 i, i < NPL (all loads of a row are
+// issued together; every reduction is a fixed-order warp butterfly).
+template <int NPL>
 __global__ void __launch_bounds__(256) k_target_ce(const __grid_constant__ TargetCEArgs a) {
   extern __shared__ float sm[];
   const int N = a.N, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -25,113 +28,158 @@ __global__ void __launch_bounds__(256) k_target_ce(const __grid_constant__ Targe
   float* bj = pb + N;          // b_j [N]
   const int row = blockIdx.x * kRows + w;
   if (row >= a.B) return;
-  const float dz = (a.v_max - a.v_min) / (float)(N - 1);
-  const float alpha0 = expf(a.log_alpha[0]);
   const int64_t ridx = a.idx[row];
+  float tl[2][NPL], ol[2][NPL];
+#pragma unroll
+  for (int hd = 0; hd < 2; ++hd)
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      const int k = lane + 32 * i;
+      tl[hd][i] = k < N ? a.tlogits[((int64_t)hd * a.B + row) * N + k] : -INFINITY;
+      ol[hd][i] = k < N ? a.logits[((int64_t)hd * a.B + row) * N + k] : -INFINITY;
+    }
   const float r = a.reward[ridx];
   const float nd = a.done[ridx] ? 0.f : 1.f;
-  const float shift = alpha0 * a.logp_next[row];
-  // target heads -> pbar
+  const float dz = (a.v_max - a.v_min) / (float)(N - 1);
+  const float shift = expf(a.log_alpha[0]) * a.logp_next[row];
+  // pbar = (softmax l1_bar + softmax l2_bar) / 2
+  float pbar[NPL];
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) pbar[i] = 0.f;
+#pragma unroll
   for (int hd = 0; hd < 2; ++hd) {
-    const float* l = a.tlogits + ((int64_t)hd * a.B + row) * N;
     float mx = -INFINITY;
-    for (int k = lane; k < N; k += 32) mx = fmaxf(mx, l[k]);
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) mx = fmaxf(mx, tl[hd][i]);
     mx = warp_max(mx);
-    float s = 0.f;
-    for (int k = lane; k < N; k += 32) s += expf(l[k] - mx);
-    s = warp_sum(s);
-    const float inv = 1.f / s;
-    for (int k = lane; k < N; k += 32) {
-      const float p = expf(l[k] - mx) * inv;
-      pb[k] = (hd == 0) ? 0.5f * p : pb[k] + 0.5f * p;
+    float e[NPL], sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      e[i] = (lane + 32 * i < N) ? expf(tl[hd][i] - mx) : 0.f;
+      sum += e[i];
     }
+    sum = warp_sum(sum);
+    const float inv = 1.f / sum;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) pbar[i] += 0.5f * e[i] * inv;
   }
-  for (int j = lane; j < N; j += 32) {
-    const float zj = a.v_min + (float)j * dz;
-    float g = r + nd * a.gamma * (zj - shift);
-    g = fminf(fmaxf(g, a.v_min), a.v_max);
-    float b = (g - a.v_min) / dz;
-    bj[j] = fminf(fmaxf(b, 0.f), (float)(N - 1));
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int j = lane + 32 * i;
+    if (j < N) {
+      const float zj = a.v_min + (float)j * dz;
+      float g = r + nd * a.gamma * (zj - shift);
+      g = fminf(fmaxf(g, a.v_min), a.v_max);
+      const float b = (g - a.v_min) / dz;
+      bj[j] = fminf(fmaxf(b, 0.f), (float)(N - 1));
+      pb[j] = pbar[i];
+    }
   }
   __syncwarp();
-  float* mrow = a.m + (int64_t)row * N;
-  // b_j is non-decreasing in j (g_j is increasing in z_j and clipping preserves order), so the
-  // atoms j with |b_j - k| < 1 form a contiguous range: binary search its start, then add the
-  // same terms in the same (ascending j) order as the full sum.
-  for (int k = lane; k < N; k += 32) {
-    const float kf = (float)k;
-    int lo = 0, hi = N;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (bj[mid] - kf > -1.f) hi = mid;
-      else lo = mid + 1;
-    }
+  // m_k = sum_j pbar_j max(0, 1 - |b_j - k|).  b_j is non-decreasing in j (g_j increases with z_j
+  // and clipping preserves order), so the contributing j form a contiguous range: binary search
+  // its start, then add the terms in ascending j as the full sum would.
+  float m[NPL];
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int k = lane + 32 * i;
     float acc = 0.f;
-    for (int j = lo; j < N; ++j) {
-      const float wgt = 1.f - fabsf(bj[j] - kf);
-      if (bj[j] - kf >= 1.f) break;
-      if (wgt > 0.f) acc = fmaf(pb[j], wgt, acc);
+    if (k < N) {
+      const float kf = (float)k;
+      int lo = 0, hi = N;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (bj[mid] - kf > -1.f) hi = mid;
+        else lo = mid + 1;
+      }
+      for (int j = lo; j < N; ++j) {
+        const float d = bj[j] - kf;
+        if (d >= 1.f) break;
+        const float wgt = 1.f - fabsf(d);
+        if (wgt > 0.f) acc = fmaf(pb[j], wgt, acc);
+      }
+      a.m[(int64_t)row * N + k] = acc;
     }
-    mrow[k] = acc;
+    m[i] = acc;
   }
-  __syncwarp();
-  // online heads: CE and gradient
+  // online heads: CE and dL/dl = (softmax - m) * scale
   float loss = 0.f;
+#pragma unroll
   for (int hd = 0; hd < 2; ++hd) {
-    const float* l = a.logits + ((int64_t)hd * a.B + row) * N;
-    float* dl = a.dlogits_bf ? nullptr : a.dlogits + ((int64_t)hd * a.B + row) * N;
-    __nv_bfloat16* dlb = a.dlogits_bf ? a.dlogits_bf + ((int64_t)hd * a.B + row) * a.ld_dl : nullptr;
     float mx = -INFINITY;
-    for (int k = lane; k < N; k += 32) mx = fmaxf(mx, l[k]);
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) mx = fmaxf(mx, ol[hd][i]);
     mx = warp_max(mx);
-    float s = 0.f;
-    for (int k = lane; k < N; k += 32) s += expf(l[k] - mx);
-    s = warp_sum(s);
-    const float lse = mx + logf(s), inv = 1.f / s;
+    float e[NPL], sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      e[i] = (lane + 32 * i < N) ? expf(ol[hd][i] - mx) : 0.f;
+      sum += e[i];
+    }
+    sum = warp_sum(sum);
+    const float lse = mx + logf(sum), inv = 1.f / sum;
     float ce = 0.f;
-    for (int k = lane; k < N; k += 32) {
-      const float mk = mrow[k];
-      ce -= mk * (l[k] - lse);
-      const float g = (expf(l[k] - mx) * inv - mk) * a.scale;
-      if (dlb) dlb[k] = __float2bfloat16_rn(g); else dl[k] = g;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      const int k = lane + 32 * i;
+      if (k < N) {
+        ce -= m[i] * (ol[hd][i] - lse);
+        const float g = (e[i] * inv - m[i]) * a.scale;
+        if (a.dlogits_bf) a.dlogits_bf[((int64_t)hd * a.B + row) * a.ld_dl + k] = __float2bfloat16_rn(g);
+        else a.dlogits[((int64_t)hd * a.B + row) * N + k] = g;
+      }
     }
     loss += warp_sum(ce);
   }
   if (lane == 0) a.row_loss[row] = loss * a.scale;
 }
 
+template <int NPL>
 __global__ void __launch_bounds__(256) k_actor_q(const __grid_constant__ ActorQArgs a) {
   const int N = a.N, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int row = blockIdx.x * kRows + w;
   if (row >= a.B) return;
   const float dz = (a.v_max - a.v_min) / (float)(N - 1);
-  float q[2];
+  float l[2][NPL];
+#pragma unroll
+  for (int hd = 0; hd < 2; ++hd)
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      const int k = lane + 32 * i;
+      l[hd][i] = k < N ? a.logits[((int64_t)hd * a.B + row) * N + k] : -INFINITY;
+    }
+  float q0 = 0.f, q1 = 0.f;
+#pragma unroll
   for (int hd = 0; hd < 2; ++hd) {
-    const float* l = a.logits + ((int64_t)hd * a.B + row) * N;
     float mx = -INFINITY;
-    for (int k = lane; k < N; k += 32) mx = fmaxf(mx, l[k]);
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) mx = fmaxf(mx, l[hd][i]);
     mx = warp_max(mx);
-    float s = 0.f, sz = 0.f;
-    for (int k = lane; k < N; k += 32) {
-      const float e = expf(l[k] - mx);
-      s += e;
-      sz += e * (a.v_min + (float)k * dz);
+    float e[NPL], s = 0.f, sz = 0.f;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      const int k = lane + 32 * i;
+      e[i] = k < N ? expf(l[hd][i] - mx) : 0.f;
+      s += e[i];
+      sz += e[i] * (a.v_min + (float)k * dz);
     }
     s = warp_sum(s);
     sz = warp_sum(sz);
-    const float inv = 1.f / s;
-    q[hd] = sz * inv;
-    float* dl = a.dlogits_bf ? nullptr : a.dlogits + ((int64_t)hd * a.B + row) * N;
-    __nv_bfloat16* dlb = a.dlogits_bf ? a.dlogits_bf + ((int64_t)hd * a.B + row) * a.ld_dl : nullptr;
+    const float inv = 1.f / s, q = sz * inv;
+    if (hd == 0) q0 = q; else q1 = q;
     const float c = -0.5f * a.scale;
-    for (int k = lane; k < N; k += 32) {
-      const float p = expf(l[k] - mx) * inv;
-      const float g = c * p * ((a.v_min + (float)k * dz) - q[hd]);
-      if (dlb) dlb[k] = __float2bfloat16_rn(g); else dl[k] = g;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      const int k = lane + 32 * i;
+      if (k < N) {
+        const float g = c * e[i] * inv * ((a.v_min + (float)k * dz) - q);
+        if (a.dlogits_bf) a.dlogits_bf[((int64_t)hd * a.B + row) * a.ld_dl + k] = __float2bfloat16_rn(g);
+        else a.dlogits[((int64_t)hd * a.B + row) * N + k] = g;
+      }
     }
   }
   if (lane == 0) {
-    const float qm = 0.5f * (q[0] + q[1]);
+    const float qm = 0.5f * (q0 + q1);
     a.row_q[row] = qm;
     a.row_lpi[row] = (a.alpha1[0] * a.logp[row] - qm) * a.scale;
   }
@@ -141,13 +189,27 @@ __global__ void __launch_bounds__(256) k_actor_q(const __grid_constant__ ActorQA
 
 int launch_target_ce(const TargetCEArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(float) * 2 * a.N * kRows;
-  cudaFuncSetAttribute(k_target_ce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  note_launch(s, "k_target_ce", 0, 0); k_target_ce<<<(a.B + kRows - 1) / kRows, 256, smem, s>>>(a);
+  const int npl = (a.N + 31) / 32;
+  const dim3 grid((a.B + kRows - 1) / kRows);
+  note_launch(s, "k_target_ce", 0, 0);
+#define SQ_TCE(n)                                                                              \
+  {                                                                                            \
+    cudaFuncSetAttribute(k_target_ce<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    k_target_ce<n><<<grid, 256, smem, s>>>(a);                                                 \
+  }
+  if (npl <= 2) SQ_TCE(2) else if (npl <= 4) SQ_TCE(4) else if (npl <= 8) SQ_TCE(8) else SQ_TCE(16)
+#undef SQ_TCE
   return (int)cudaGetLastError();
 }
 
 int launch_actor_q(const ActorQArgs& a, cudaStream_t s) {
-  note_launch(s, "k_actor_q", 0, 0); k_actor_q<<<(a.B + kRows - 1) / kRows, 256, 0, s>>>(a);
+  const int npl = (a.N + 31) / 32;
+  const dim3 grid((a.B + kRows - 1) / kRows);
+  note_launch(s, "k_actor_q", 0, 0);
+  if (npl <= 2) k_actor_q<2><<<grid, 256, 0, s>>>(a);
+  else if (npl <= 4) k_actor_q<4><<<grid, 256, 0, s>>>(a);
+  else if (npl <= 8) k_actor_q<8><<<grid, 256, 0, s>>>(a);
+  else k_actor_q<16><<<grid, 256, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 

@@ -57,7 +57,7 @@ struct BfLay {
   size_t tlogits, logits, logits1, m, tgo_ac, a_cur, logp_cur, logp_next, row_loss, row_q, row_lpi;
   size_t part_q2[2], part_q1[2], part_pq, part_a2, part_a1, part_pp;
   size_t grad_critic, grad_actor, adam_part, scal, lpi_sums;
-  size_t y1b, img0, dA1enc, enc_part;
+  size_t y1b, img0, dA1enc, enc_part, wtiles;
   ShadowPlan sh[3];  // critic, target, actor
   size_t total;
 };
@@ -191,6 +191,7 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
   w.img0 = P.take((size_t)B * d.img_c * d.img_h * d.img_w);
   w.dA1enc = 0;
   w.enc_part = fl(enc_bwd_tc_partial_floats(C, B));
+  w.wtiles = P.take(conv_tiles_bytes(C));
   w.sh[0] = shadow_plan(P, d, L, SQUINT_GROUP_CRITIC);
   w.sh[1] = shadow_plan(P, d, L, SQUINT_GROUP_TARGET);
   w.sh[2] = shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
@@ -346,6 +347,8 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
 
   // a3-a5: gather + shift + encoder (obs, next_obs); replay rows of s, a, s' into the layer
   // input matrices
+  uint8_t* wtiles = reinterpret_cast<uint8_t*>(c.ws + w.wtiles);
+  BF_CK(launch_conv_tiles(crit + L.off(gC, "enc.conv1.w"), crit + L.off(gC, "enc.conv2.w"), C, wtiles, s));
   {
     PhaseScope ps(3, rep, s);
     EncFwdArgs e;
@@ -378,6 +381,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     e.gj[1][0] = GatherJob{R.next_proprio, P, c.bp(w.Xt), w.Xt.ld, Lt, 1};
     e.gj[1][1] = GatherJob{R.next_proprio, P, c.bp(w.Xan), w.Xan.ld, Lt, 1};
     e.ngj[1] = 2;
+    e.wtiles = wtiles;
     BF_CK(launch_enc_fwd_tc(e, s));
   }
   // a6: projections Linear -> LN -> tanh (Q8): critic(h), target(h'), actor(h'), actor(h)
@@ -569,6 +573,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     e.img = reinterpret_cast<const uint8_t*>(c.ws + w.img0);
     e.w2 = crit + L.off(gC, "enc.conv2.w");
     e.part = c.F(w.enc_part);
+    e.wtiles = wtiles;
     e.gw1 = gc + L.off(gC, "enc.conv1.w");
     e.gb1 = gc + L.off(gC, "enc.conv1.b");
     e.gw2 = gc + L.off(gC, "enc.conv2.w");
@@ -833,6 +838,7 @@ size_t bf16_act_workspace_bytes(const squint_dims& d, int64_t n) {
   P.take((size_t)n * ld8(Ha) * 2);
   P.take((size_t)n * ld8(Ha) * 2);
   shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
+  P.take(conv_tiles_bytes(d.conv_ch));
   return P.top + 256;
 }
 
@@ -851,11 +857,14 @@ squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const flo
   BM H1{P.take((size_t)n * ld8(Ha) * 2), M, Ha, ld8(Ha)};
   BM H2{P.take((size_t)n * ld8(Ha) * 2), M, Ha, ld8(Ha)};
   ShadowPlan sp = shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
+  uint8_t* wtiles = reinterpret_cast<uint8_t*>(ws + P.take(conv_tiles_bytes(d.conv_ch)));
   Ctx c{d, L, ws, s};
   const int gC = SQUINT_GROUP_CRITIC, gA = SQUINT_GROUP_ACTOR;
   std::optional<PhaseScope> ps;
   ps.emplace(1, 0, s);
   BF_CK(launch_shadow(actor_params, table_at(c, sp), s));
+  BF_CK(launch_conv_tiles(critic_params + L.off(gC, "enc.conv1.w"), critic_params + L.off(gC, "enc.conv2.w"),
+                          d.conv_ch, wtiles, s));
   {
     EncFwdArgs a;
     memset(&a, 0, sizeof(a));
@@ -878,6 +887,7 @@ squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const flo
     a.pad = d.pad;
     a.gj[0][0] = GatherJob{proprio, d.proprio_dim, c.bp(Xa), Xa.ld, Lt, 0};
     a.ngj[0] = 1;
+    a.wtiles = wtiles;
     BF_CK(launch_enc_fwd_tc(a, s));
   }
   ps.reset();
