@@ -233,8 +233,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   tc::fence_after_sync();
   const uint32_t tmem = tmem_slot;
   stamp(1);
-  tc::pdl_trigger();
+  int npre = 0;  // stages whose B (weights / long-finished activations) was loaded before the wait
+  if (b.prefetch_b && warp == 0 && lane == 0) {
+    // B never comes from the immediately preceding kernel (host contract), and every earlier
+    // kernel has completed: the preceding kernel triggers its dependents only after its own wait.
+    int kb = 0;
+    for (int s = 0; s < P.nseg && kb < S; ++s) {
+      const GSeg& G = P.seg[s];
+      const TileGeo geo = tile_geo(P, nreal, G.b_mn);
+      for (int l = 0; l < G.nkb && kb < S; ++l, ++kb) {
+        uint8_t* Bs = smem + kb * b.stage_bytes + kABytes;
+        tc::mbar_expect_tx(&full_bar[kb], kABytes + geo.bbytes);
+        for (int i = 0; i < geo.nbox_b; ++i) {
+          if (!G.b_mn)
+            tc::tma_load_2d(Bs + i * geo.bnb * 128, &b.maps[G.bmap], G.b_k + 64 * l, P.b_n + n0 + geo.bnb * i, &full_bar[kb]);
+          else
+            tc::tma_load_2d(Bs + i * 8192, &b.maps[G.bmap], P.b_n + n0 + 64 * i, G.b_k + 64 * l, &full_bar[kb]);
+        }
+      }
+    }
+    npre = kb;
+  }
   tc::pdl_wait();
+  tc::pdl_trigger();
   stamp(2);
   // per-column epilogue parameters -> smem (overlaps the main loop; read after the done barrier)
   if (warp >= 2) {
@@ -260,7 +281,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
         if (kb >= S) tc::mbar_wait(&empty_bar[st], ((kb / S) - 1) & 1);
         uint8_t* As = smem + st * b.stage_bytes;
         uint8_t* Bs = As + kABytes;
-        tc::mbar_expect_tx(&full_bar[st], kABytes + geo.bbytes);
+        const bool pre = kb < npre;  // B already in flight, transaction bytes already expected
+        if (!pre) tc::mbar_expect_tx(&full_bar[st], kABytes + geo.bbytes);
         const int kc = 64 * l;
         if (!G.a_mn) {
           tc::tma_load_2d(As, am, G.a_k + kc, P.a_m + m0, &full_bar[st]);
@@ -268,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
           tc::tma_load_2d(As, am, P.a_m + m0, G.a_k + kc, &full_bar[st]);
           tc::tma_load_2d(As + 8192, am, P.a_m + m0 + 64, G.a_k + kc, &full_bar[st]);
         }
-        for (int i = 0; i < geo.nbox_b; ++i) {
+        for (int i = 0; i < geo.nbox_b && !pre; ++i) {
           if (!G.b_mn)
             tc::tma_load_2d(Bs + i * geo.bnb * 128, bm, G.b_k + kc, P.b_n + n0 + geo.bnb * i, &full_bar[st]);
           else
@@ -425,27 +447,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
       pair_store(sl, &b.maps[P.omap], n0 + g * 64, row0, q, hh);
     }
   } else if constexpr (EPI == GE_LN_RELU || EPI == GE_LN_TANH) {
-    float s1 = 0.f;
+    // one pass for the row moments (bf16 outputs: E[u^2] - mean^2 in fp32 is ample), one pass to
+    // normalise and store
+    float s1 = 0.f, s2 = 0.f;
     for (int ch = hh; ch < nch; ch += 2) {
       tc::tmem_ld32(trow + ch * 32, v);
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int cc = ch * 32 + j;
-        if (cc < nreal) s1 += v[j] + s_bias[cc];
+        const float u = v[j] + s_bias[cc];
+        if (cc < nreal) s1 += u, s2 += u * u;
       }
     }
-    const float mean = row_total(s1, 0) / (float)N;
-    float s2 = 0.f;
-    for (int ch = hh; ch < nch; ch += 2) {
-      tc::tmem_ld32(trow + ch * 32, v);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int cc = ch * 32 + j;
-        const float dd = v[j] + s_bias[cc] - mean;
-        if (cc < nreal) s2 += dd * dd;
-      }
-    }
-    const float rs = rsqrtf(row_total(s2, 1) / (float)N + P.ln_eps);
+    float t1, t2;
+    row_total2(s1, s2, t1, t2);
+    const float mean = t1 / (float)N;
+    const float rs = rsqrtf(fmaxf(t2 / (float)N - mean * mean, 0.f) + P.ln_eps);
     if (rv && hh == 0 && n0 == 0 && P.rstd) P.rstd[r] = rs;
     const bool tma_out = (N & 7) == 0;
     for (int g = 0; g < ngrp; ++g) {

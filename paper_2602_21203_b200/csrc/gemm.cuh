@@ -97,6 +97,8 @@ struct GBatch {
   int nprob, ntiles, nmaps;
   int stage_bytes, nstages;
   int cs;  // cluster size: LayerNorm rows split over cs CTAs (statistics exchanged through DSMEM)
+  int prefetch_b;  // 1: B operands may be loaded before griddepcontrol.wait (not written by the
+                   // immediately preceding kernel); set through GemmBuilder::prefetch_b
   unsigned long long* dbg;  // optional per-CTA phase timestamps (globaltimer ns) [tile][8]
 };
 
@@ -105,10 +107,11 @@ struct GemmBuilder {
   GBatch b;
   Mat segA[kGemmMaxProb][3], segB[kGemmMaxProb][3];  // operands, mapped at launch
   int err = 0;
-  GemmBuilder() {
+  GemmBuilder(int prefetch_b = 0) {
     b.nprob = 0;
     b.nmaps = 0;
     b.ntiles = 0;
+    b.prefetch_b = prefetch_b;
   }
   GProb& add(int M, int N, int epi);
   // K segment: A(m, k) from `A` (K-major if !a_mn) and B(n, k) from `Bm`.

@@ -387,7 +387,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
   // a6: projections Linear -> LN -> tanh (Q8): critic(h), target(h'), actor(h'), actor(h)
   {
     PhaseScope ps(4, rep, s);
-    GemmBuilder gb;
+    GemmBuilder gb(1);
     GProb* p = &fwd(gb, c.mat(w.Xh), cproj, GE_LN_TANH, c.bp(w.Xq), w.Xq.ld, le);
     p->xh = c.bp(w.XHpq), p->ldx = w.XHpq.ld, p->rstd = c.F(w.Rpq);
     fwd(gb, c.mat(w.Xhn), tproj, GE_LN_TANH, c.bp(w.Xt), w.Xt.ld, le);
@@ -400,21 +400,21 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
   {
     PhaseScope ps(5, rep, s);
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       fwd(gb, c.mat(w.Xan), am.l1, GE_LN_RELU, c.bp(w.H1an), w.H1an.ld, le);
       GProb& p = fwd(gb, c.mat(w.Xac), am.l1, GE_LN_RELU, c.bp(w.H1ac), w.H1ac.ld, le);
       p.xh = c.bp(w.XH1ac), p.ldx = w.XH1ac.ld, p.rstd = c.F(w.R1ac);
       BF_CK(gemm_launch(gb, s));
     }
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       fwd(gb, c.mat(w.H1an), am.l2, GE_LN_RELU, c.bp(w.H2an), w.H2an.ld, le);
       GProb& p = fwd(gb, c.mat(w.H1ac), am.l2, GE_LN_RELU, c.bp(w.H2ac), w.H2ac.ld, le);
       p.xh = c.bp(w.XH2ac), p.ldx = w.XH2ac.ld, p.rstd = c.F(w.R2ac);
       BF_CK(gemm_launch(gb, s));
     }
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       GProb& pn = fwd(gb, c.mat(w.H2an), am.l3, GE_TG_FWD, nullptr, 0, le);
       pn.eps = eps_next;
       pn.act_bf = c.bp(w.Xt) + Lt + P;
@@ -438,7 +438,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
   {
     PhaseScope ps(6, rep, s);
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       for (int i = 0; i < 2; ++i) fwd(gb, c.mat(w.Xt), tq[i].l1, GE_LN_RELU, c.bp(w.tqH1[i]), w.tqH1[i].ld, le);
       for (int i = 0; i < 2; ++i) {
         GProb& p = fwd(gb, c.mat(w.Xq), cq[i].l1, GE_LN_RELU, c.bp(w.qH1[i]), w.qH1[i].ld, le);
@@ -447,7 +447,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       BF_CK(gemm_launch(gb, s));
     }
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       for (int i = 0; i < 2; ++i)
         fwd(gb, c.mat(w.tqH1[i]), tq[i].l2, GE_LN_RELU, c.bp(w.tqH2[i]), w.tqH2[i].ld, le);
       for (int i = 0; i < 2; ++i) {
@@ -457,7 +457,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       BF_CK(gemm_launch(gb, s));
     }
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       for (int i = 0; i < 2; ++i) {
         GProb& p = fwd(gb, c.mat(w.tqH2[i]), tq[i].l3, GE_BIAS_F32, nullptr, 0, le);
         p.outf = c.F(w.tlogits) + (size_t)i * B * N;
@@ -500,7 +500,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
   {
     PhaseScope ps(8, rep, s);
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       for (int i = 0; i < 2; ++i) {
         GProb& p = dx(gb, c.half(w.dlog, i), cq[i].l3.w, 0, Hc, GE_BWD_LN_RELU);
         bwd_ln(p, cq[i].l2, c.bp(w.qXH2[i]), w.qXH2[i].ld, c.F(w.qR2[i]), c.bp(w.dA2c[i]), w.dA2c[i].ld,
@@ -509,7 +509,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       BF_CK(gemm_launch(gb, s));
     }
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       for (int i = 0; i < 2; ++i) {
         GProb& p = dx(gb, c.mat(w.dA2c[i]), cq[i].l2.w, 0, Hc, GE_BWD_LN_RELU);
         bwd_ln(p, cq[i].l1, c.bp(w.qXH1[i]), w.qXH1[i].ld, c.F(w.qR1[i]), c.bp(w.dA1c[i]), w.dA1c[i].ld,
@@ -519,7 +519,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     }
     {
       // dz = sum_i dA1_i W1_i[:, :L] (K-concatenation of the two heads) -> tanh + LN of the projection
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       GProb& p = dx(gb, c.mat(w.dA1c[0]), cq[0].l1.w, 0, Lt, GE_BWD_LN_TANH);
       gb.seg(p, c.mat(w.dA1c[1]), 0, 0, cq[1].l1.w, 1, 0, Hc);
       bwd_ln(p, cproj, c.bp(w.XHpq), w.XHpq.ld, c.F(w.Rpq), c.bp(w.dAp), w.dAp.ld, c.F(w.part_pq));
@@ -527,7 +527,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     }
     {
       // dh = dAp Wp, masked by ReLU'(conv2) (h > 0), HWC
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       GProb& p = dx(gb, c.mat(w.dAp), cproj.w, 0, F, GE_RELU_MASK);
       p.y = c.bp(w.Xh);
       p.ldy = w.Xh.ld;
@@ -538,7 +538,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
   }
   {
     PhaseScope ps(9, rep, s);
-    GemmBuilder gb;
+    GemmBuilder gb(1);
     for (int i = 0; i < 2; ++i) {
       const std::string hp_ = kHeads[i];
       GProb& p3 = dw(gb, c.half(w.dlog, i), c.mat(w.qH2[i]), ling(L, gc, gC, hp_ + ".l3", ""), Hc);
@@ -619,13 +619,13 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     const Lin cproj1 = proj(c, w.sh[0], crit, gC, "critic");  // same buffers, now theta+
     const Mlp cq1[2] = {mlp(c, w.sh[0], crit, gC, kHeads[0]), mlp(c, w.sh[0], crit, gC, kHeads[1])};
     {
-      GemmBuilder gb;
+      GemmBuilder gb(0);  // theta+ shadow was written by the immediately preceding Adam kernel
       GProb& p = fwd(gb, c.mat(w.Xh), cproj1, GE_LN_TANH, c.bp(w.Xq1), w.Xq1.ld, le);
       p.xh = c.bp(w.XHpq1), p.ldx = w.XHpq1.ld, p.rstd = c.F(w.Rpq1);
       BF_CK(gemm_launch(gb, s));
     }
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       for (int i = 0; i < 2; ++i) {
         GProb& p = fwd(gb, c.mat(w.Xq1), cq1[i].l1, GE_LN_RELU, c.bp(w.q1H1[i]), w.q1H1[i].ld, le);
         p.xh = c.bp(w.q1XH1[i]), p.ldx = w.q1XH1[i].ld, p.rstd = c.F(w.q1R1[i]);
@@ -633,7 +633,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       BF_CK(gemm_launch(gb, s));
     }
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       for (int i = 0; i < 2; ++i) {
         GProb& p = fwd(gb, c.mat(w.q1H1[i]), cq1[i].l2, GE_LN_RELU, c.bp(w.q1H2[i]), w.q1H2[i].ld, le);
         p.xh = c.bp(w.q1XH2[i]), p.ldx = w.q1XH2[i].ld, p.rstd = c.F(w.q1R2[i]);
@@ -641,7 +641,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       BF_CK(gemm_launch(gb, s));
     }
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       for (int i = 0; i < 2; ++i) {
         GProb& p = fwd(gb, c.mat(w.q1H2[i]), cq1[i].l3, GE_BIAS_F32, nullptr, 0, le);
         p.outf = c.F(w.logits1) + (size_t)i * B * N;
@@ -671,7 +671,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     const Mlp cq1[2] = {mlp(c, w.sh[0], crit, gC, kHeads[0]), mlp(c, w.sh[0], crit, gC, kHeads[1])};
     (void)cproj1;
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       for (int i = 0; i < 2; ++i) {
         GProb& p = dx(gb, c.half(w.dlog1, i), cq1[i].l3.w, 0, Hc, GE_BWD_LN_RELU);
         bwd_ln(p, cq1[i].l2, c.bp(w.q1XH2[i]), w.q1XH2[i].ld, c.F(w.q1R2[i]), c.bp(w.dA2a[i]), w.dA2a[i].ld,
@@ -680,7 +680,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       BF_CK(gemm_launch(gb, s));
     }
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       for (int i = 0; i < 2; ++i) {
         GProb& p = dx(gb, c.mat(w.dA2a[i]), cq1[i].l2.w, 0, Hc, GE_BWD_LN_RELU);
         bwd_ln(p, cq1[i].l1, c.bp(w.q1XH1[i]), w.q1XH1[i].ld, c.F(w.q1R1[i]), c.bp(w.dA1a[i]), w.dA1a[i].ld,
@@ -690,7 +690,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     }
     {
       // dL/da~ = sum_i dA1_i W1_i[:, L+P : L+P+A] -> tanh-Gaussian backward (+ the log pi path)
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       GProb& p = dx(gb, c.mat(w.dA1a[0]), cq1[0].l1.w, Lt + P, A, GE_TG_BWD);
       gb.seg(p, c.mat(w.dA1a[1]), 0, 0, cq1[1].l1.w, 1, 0, Hc);
       p.tgo = c.F(w.tgo_ac);
@@ -703,19 +703,19 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       BF_CK(gemm_launch(gb, s));
     }
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       GProb& p = dx(gb, c.mat(w.dO), am.l3.w, 0, Ha, GE_BWD_LN_RELU);
       bwd_ln(p, am.l2, c.bp(w.XH2ac), w.XH2ac.ld, c.F(w.R2ac), c.bp(w.adA2), w.adA2.ld, c.F(w.part_a2));
       BF_CK(gemm_launch(gb, s));
     }
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       GProb& p = dx(gb, c.mat(w.adA2), am.l2.w, 0, Ha, GE_BWD_LN_RELU);
       bwd_ln(p, am.l1, c.bp(w.XH1ac), w.XH1ac.ld, c.F(w.R1ac), c.bp(w.adA1), w.adA1.ld, c.F(w.part_a1));
       BF_CK(gemm_launch(gb, s));
     }
     {
-      GemmBuilder gb;
+      GemmBuilder gb(1);
       GProb& p = dx(gb, c.mat(w.adA1), am.l1.w, 0, Lt, GE_BWD_LN_TANH);
       bwd_ln(p, aproj, c.bp(w.XHpp), w.XHpp.ld, c.F(w.Rpp), c.bp(w.adAp), w.adAp.ld, c.F(w.part_pp));
       BF_CK(gemm_launch(gb, s));
@@ -724,7 +724,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
   float* ga = c.F(w.grad_actor);
   {
     PhaseScope ps(14, rep, s);
-    GemmBuilder gb;
+    GemmBuilder gb(1);
     GProb& p3 = dw(gb, c.mat(w.dO), c.mat(w.H2ac), ling(L, ga, gA, "actor.l3", ""), Ha);
     p3.colsum = c.bp(w.dO);
     p3.ld_colsum = w.dO.ld;
@@ -895,22 +895,22 @@ squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const flo
   const Lin ap = proj(c, sp, actor_params, gA, "actor");
   const Mlp am = mlp(c, sp, actor_params, gA, "actor");
   {
-    GemmBuilder gb;
+    GemmBuilder gb(1);
     fwd(gb, c.mat(Xh), ap, GE_LN_TANH, c.bp(Xa), Xa.ld, hp.ln_eps);
     BF_CK(gemm_launch(gb, s));
   }
   {
-    GemmBuilder gb;
+    GemmBuilder gb(1);
     fwd(gb, c.mat(Xa), am.l1, GE_LN_RELU, c.bp(H1), H1.ld, hp.ln_eps);
     BF_CK(gemm_launch(gb, s));
   }
   {
-    GemmBuilder gb;
+    GemmBuilder gb(1);
     fwd(gb, c.mat(H1), am.l2, GE_LN_RELU, c.bp(H2), H2.ld, hp.ln_eps);
     BF_CK(gemm_launch(gb, s));
   }
   {
-    GemmBuilder gb;
+    GemmBuilder gb(1);
     GProb& p = fwd(gb, c.mat(H2), am.l3, GE_TG_FWD, nullptr, 0, hp.ln_eps);
     p.eps = eps;
     p.act = action_out;
@@ -929,7 +929,7 @@ extern "C" squint_status squint_selftest_gemm(const void* A, int a_rows, int a_c
                                               float* out, squint_stream_t stream) {
   using namespace sq;
   if (!A || !B || !out || M < 1 || N < 1 || K < 1) return set_error(SQUINT_EINVAL, "selftest_gemm: bad argument");
-  GemmBuilder gb;
+  GemmBuilder gb(0);
   GProb& p = gb.add(M, N, GE_DW);
   gb.seg(p, Mat{A, a_rows, a_cols, a_ld}, a_mn, 0, Mat{B, b_rows, b_cols, b_ld}, b_mn, 0, K);
   p.outf = out;
