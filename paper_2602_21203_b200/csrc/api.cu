@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <optional>
@@ -220,11 +221,17 @@ struct Ctx {
 static thread_local int g_prec = SQUINT_FP32;
 
 // Dense layers: fp32 SIMT (parity mode) or bf16 tcgen05 tensor cores.
+static int emul_flags() {
+  static const char* e = getenv("SQUINT_EMUL");  // numerics experiments only (fp32 path)
+  return e ? atoi(e) : 0;
+}
 static int run_dense(DenseBatch& b, cudaStream_t s) {
+  b.emul = emul_flags();
   const int tn = plan_dense(b);
   return launch_dense_f32(b, tn, s);
 }
 static int run_dw(DwBatch& b, cudaStream_t s) {
+  b.emul = emul_flags();
   plan_dw(b);
   return launch_dw_f32(b, s);
 }

@@ -72,6 +72,7 @@ constexpr int kMaxProb = 8;
 struct DenseBatch {
   int nprob;
   int ntiles;
+  int emul;  // numerics experiment (SQUINT_EMUL): bit0 rounds activation operands to bf16, bit1 weights
   DenseProb p[kMaxProb];
 };
 
@@ -94,6 +95,7 @@ constexpr int kMaxDw = 8;
 struct DwBatch {
   int nprob;
   int ntiles;
+  int emul;
   DwProb p[kMaxDw];
 };
 

@@ -3,6 +3,7 @@
 // statistics (Q9) and the tanh-Gaussian head (Q13-Q14) are finished in the
 // epilogue without another pass over HBM.  Reductions are fixed-order (no float atomics),
 // so every result is bitwise reproducible run to run.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -81,17 +82,23 @@ __global__ void __launch_bounds__(256) k_dense_f32(const __grid_constant__ Dense
   for (int k0 = 0; k0 < P.K; k0 += BK) {
     for (int e = tid; e < BM * BK; e += 256) {
       const int m = e / BK, k = e % BK;
-      As[k * BM + m] = (k0 + k < P.K) ? a_at(P.A, P.nA, P.M, m0 + m, k0 + k) : 0.f;
+      float av = (k0 + k < P.K) ? a_at(P.A, P.nA, P.M, m0 + m, k0 + k) : 0.f;
+      if (b.emul & 1) av = __bfloat162float(__float2bfloat16_rn(av));
+      As[k * BM + m] = av;
     }
     if (bk) {
       for (int e = tid; e < BN * BK; e += 256) {
         const int n = e / BK, k = e % BK;
-        Bs[k * (BN + 1) + n] = (k0 + k < P.K) ? b_at(P.B, P.nB, P.N, n0 + n, k0 + k) : 0.f;
+        float bv = (k0 + k < P.K) ? b_at(P.B, P.nB, P.N, n0 + n, k0 + k) : 0.f;
+        if (b.emul & 2) bv = __bfloat162float(__float2bfloat16_rn(bv));
+        Bs[k * (BN + 1) + n] = bv;
       }
     } else {
       for (int e = tid; e < BN * BK; e += 256) {
         const int k = e / BN, n = e % BN;
-        Bs[k * (BN + 1) + n] = (k0 + k < P.K) ? b_at(P.B, P.nB, P.N, n0 + n, k0 + k) : 0.f;
+        float bv = (k0 + k < P.K) ? b_at(P.B, P.nB, P.N, n0 + n, k0 + k) : 0.f;
+        if (b.emul & 2) bv = __bfloat162float(__float2bfloat16_rn(bv));
+        Bs[k * (BN + 1) + n] = bv;
       }
     }
     __syncthreads();
@@ -306,11 +313,15 @@ __global__ void __launch_bounds__(256) k_dw_f32(const __grid_constant__ DwBatch 
   for (int mb = 0; mb < P.M; mb += BMc) {
     for (int e = tid; e < BMc * BN; e += 256) {
       const int m = e / BN, n = e % BN;
-      Ds[m][n] = (mb + m < P.M && n0 + n < P.N) ? P.D[(int64_t)(mb + m) * P.N + n0 + n] : 0.f;
+      float dv = (mb + m < P.M && n0 + n < P.N) ? P.D[(int64_t)(mb + m) * P.N + n0 + n] : 0.f;
+      if (b.emul & 1) dv = __bfloat162float(__float2bfloat16_rn(dv));
+      Ds[m][n] = dv;
     }
     for (int e = tid; e < BMc * BK; e += 256) {
       const int m = e / BK, k = e % BK;
-      Xs[m][k] = (k0 + k < P.K) ? a_at(P.A, P.nA, P.M, mb + m, k0 + k) : 0.f;
+      float xv = (k0 + k < P.K) ? a_at(P.A, P.nA, P.M, mb + m, k0 + k) : 0.f;
+      if (b.emul & 1) xv = __bfloat162float(__float2bfloat16_rn(xv));
+      Xs[m][k] = xv;
     }
     __syncthreads();
 #pragma unroll 8

@@ -202,22 +202,80 @@ def test_act_bf16(n):
     compare("logp bf16", lp.cpu().numpy(), lp_ref, 2e-2)
 
 
+def _rel_l2(got, ref):
+    num = sum(float(np.sum((np.asarray(got[n], np.float64) - r) ** 2)) for n, r in ref.items())
+    den = sum(float(np.sum(np.asarray(r, np.float64) ** 2)) for r in ref.values())
+    return (num / max(den, 1e-300)) ** 0.5
+
+
+def _check_update_bf16(pr, L, met_gpu, st_ref, met_ref, trace):
+    """bf16 tensor-core mode (DESIGN.md R-tol-bf16).  Losses / metrics, the target distribution,
+    log-probs and the updated parameters at the north-star bar 2e-2 (mean Q against a scale of at
+    least v_max / 10); gradients and the Adam steps (parameter deltas, m_hat / sqrt(v_hat) of the
+    gradient) at 3e-2 relative L2 per group and gradients at 8e-2 per tensor: rounding only the
+    weights to bf16 (SQUINT_EMUL=2 on the fp32 path) already moves the c2 critic gradient by
+    1.4e-2 (group) / 3.0e-2 (worst tensor) on these inputs."""
+    tol = 2e-2
+    qscale = 0.1 * max(abs(pr.dims["v_min"]), abs(pr.dims["v_max"]))
+    for j in range(pr.utd):
+        for k, name in enumerate(["L_Q", "L_pi", "L_alpha", "alpha", "meanQ", "entropy", "gradnorm"]):
+            if name == "meanQ":  # E_p[z] is a cancelling sum over a +-v_max support: scale >= v_max / 10
+                assert abs(met_gpu[j, k] - met_ref[j, k]) <= tol * max(abs(met_ref[j, k]), qscale), name
+                continue
+            compare(f"metric {name}[{j}]", met_gpu[j, k], met_ref[j, k], tol)
+        assert met_gpu[j, 7] == 0.0
+    tr = trace[-1]
+    compare("m", L.region("m").cpu().numpy().reshape(tr["m"].shape), tr["m"], tol)
+    compare("logp", L.region("logp").cpu().numpy(), tr["logp"], tol)
+    compare("logp_next", L.region("logp_next").cpu().numpy(), tr["logp_next"], tol)
+    for grp in ("critic", "actor"):
+        g = group_values(L, grp, "grad")
+        ref = tr["grad_" + grp]
+        e = _rel_l2(g, ref)
+        assert e <= 3e-2, f"grad {grp}: group relative L2 {e:.3e} > 3e-2"
+        for n, r in ref.items():
+            en = _rel_l2({n: g[n]}, {n: r})
+            assert en <= 8e-2, f"grad {grp} {n}: relative L2 {en:.3e} > 8e-2"
+    for grp in ("critic", "actor", "target"):
+        got = group_values(L, grp)
+        for n, ref in st_ref[grp].items():
+            compare(f"{grp} {n}", got[n], ref, tol)
+        if grp != "target":
+            d_got = {n: got[n] - pr.vals[(grp, n)] for n in st_ref[grp]}
+            d_ref = {n: st_ref[grp][n] - np.asarray(pr.vals[(grp, n)], np.float64) for n in st_ref[grp]}
+            e = _rel_l2(d_got, d_ref)  # m_hat / sqrt(v_hat) of the gradient: the gradient's bound
+            assert e <= 3e-2, f"Adam step {grp}: relative L2 {e:.3e} > 3e-2"
+    compare("log_alpha", L.log_alpha.cpu().numpy()[0], st_ref["log_alpha"], 1e-4)
+    assert L.step.cpu().tolist() == list(st_ref["step"])
+
+
 def _bf16_case(cfg, seed, utd=1, capacity=None, **over):
     pr = Problem(cfg, capacity=capacity, utd=utd, seed=seed, **over)
     L = pr.gpu_setup(precision=P.BF16)
     met = pr.gpu_update(L)
     trace = []
     st_ref, met_ref = pr.oracle_update(trace)
-    _check_update(pr, L, met, st_ref, met_ref, trace, tol_loss=2e-2, tol=2e-2, check_delta=False)
+    _check_update_bf16(pr, L, met, st_ref, met_ref, trace)
 
 
 def test_update_c2_full_batch_utd2_bf16():
     _bf16_case("c2", seed=3, utd=2, capacity=4096)
 
 
-def test_update_c2_full_batch_bf16():
+@pytest.mark.parametrize("seed", [2, 7])
+def test_update_c2_full_batch_bf16(seed):
     """BASELINE configs[2] shapes at the full batch 512 (101 atoms), as bench.py runs them."""
-    _bf16_case("c2", seed=2, capacity=4096)
+    _bf16_case("c2", seed=seed, capacity=4096)
+
+
+@pytest.mark.parametrize("batch", [1, 37, 300])
+def test_update_ragged_batch_bf16(batch):
+    _bf16_case("c2", seed=5, capacity=4096, batch=batch)
+
+
+def test_update_c3_shapes_bf16():
+    """BASELINE configs[3] layer shapes (C = 64, critic 512-512) at a per-rank batch of 512."""
+    _bf16_case("c3", seed=4, capacity=4096, batch=512)
 
 
 # ---- bf16 GEMM engine (TMA + tcgen05) self-test: both operand majors, ragged tails -------
