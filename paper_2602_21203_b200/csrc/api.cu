@@ -625,6 +625,7 @@ static squint_status update_one(const Ctx& c, const squint_replay& R, const int6
   SQ_CK(launch_polyak(st.critic_target, st.critic + L.enc_end, L.gsize[SQUINT_GROUP_TARGET], hp.tau, s));
   {
     MetricsArgs m;
+    memset(&m, 0, sizeof(m));
     m.B = B;
     m.inv_btotal = inv_btotal;
     m.row_lpi = c.F(w.row_lpi);

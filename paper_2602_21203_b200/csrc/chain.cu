@@ -1,0 +1,475 @@
+// chain.cu -- fused MLP chains (see chain.cuh): one launch per head / actor pass.
+//
+// Shared memory per CTA: A (4 K blocks x 128 rows x 128 B, K-major 128B swizzle) = the first
+// layer's input (TMA) and afterwards the broadcast destination for the next layer's input;
+// B double buffer (this layer's and the next layer's weight slice, TMA); per-warp-pair epilogue
+// boxes; LayerNorm-backward column partials.  Barriers: A landed, B landed (x2), MMA done,
+// next-A complete (64 KB from the 4 CTAs), x_hat box loads (per warp pair).
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "chain.cuh"
+#include "common.cuh"
+#include "gemm_dev.cuh"
+#include "tc.cuh"
+
+namespace sq {
+
+namespace {
+
+using namespace gd;
+constexpr int kThr = 256;
+constexpr int kCS = 4;                       // cluster size (64-column slices of 256)
+constexpr uint32_t kAreg = 0;                // 64 KB
+constexpr uint32_t kBreg = 65536;            // 2 x 32 KB
+constexpr uint32_t kSlots = kBreg + 65536;   // 4 pairs x 2 layer parities x 2 boxes x 4 KB
+constexpr uint32_t kColacc = kSlots + 65536; // [4][3][64] floats
+constexpr uint32_t kSmem = kColacc + 4 * 3 * 64 * 4;
+constexpr float kLog2Pi = 1.8378770664093453f;
+constexpr float kSquashEps = 1e-6f;
+
+__device__ __forceinline__ uint32_t b_bytes(const CLayer& L) {
+  return L.b_mn ? (uint32_t)L.nkb * 8192u : (uint32_t)(L.nkb * L.slice * 128);
+}
+// this CTA's weight slice of layer L (columns n0 .. n0 + slice) into dst, completion on bar
+__device__ __forceinline__ void issue_b(const CBatch& b, const CLayer& L, int n0, uint8_t* dst, uint64_t* bar) {
+  tc::mbar_expect_tx(bar, b_bytes(L));
+  for (int kb = 0; kb < L.nkb; ++kb) {
+    if (L.b_mn)
+      tc::tma_load_2d(dst + kb * 8192, &b.maps[L.bmap], n0, 64 * kb, bar);
+    else
+      tc::tma_load_2d(dst + kb * L.slice * 128, &b.maps[L.bmap], 64 * kb, n0, bar);
+  }
+}
+
+__global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatch b) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t aload, bfull[2], done, anext, ld_bar[4];
+  __shared__ uint32_t tmem_slot;
+  __shared__ float red[2][2][128];
+  __shared__ float cl_red[2][kCS][128];
+  __shared__ __align__(16) float s_bias[64], s_g[64], s_beta[64];
+
+  const int rank = blockIdx.x % kCS, cl = blockIdx.x / kCS;
+  int pi = 0;
+  while (pi + 1 < b.nprob && cl >= b.p[pi + 1].c0) ++pi;
+  const CProb& P = b.p[pi];
+  const int mt = cl - P.c0, m0 = mt * 128;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = warp & 3, hh = warp >> 2, rl = q * 32 + lane;
+  const int row0 = m0 + q * 32, r = row0 + lane;
+  const bool rv = r < P.M;
+  const int nl = P.nlayers;
+  auto stamp = [&](int k) {
+    if (b.dbg && tid == 0 && k < 16) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      b.dbg[blockIdx.x * 16 + k] = t;
+    }
+  };
+  stamp(0);
+
+  if (warp == 0) tc::tmem_alloc(&tmem_slot, 64);
+  if (tid == 32) {
+    tc::mbar_init(&aload, 1);
+    tc::mbar_init(&bfull[0], 1);
+    tc::mbar_init(&bfull[1], 1);
+    tc::mbar_init(&done, 1);
+    tc::mbar_init(&anext, 1);
+    for (int i = 0; i < 4; ++i) tc::mbar_init(&ld_bar[i], 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 2 && lane == 0) {
+    tc::tma_prefetch_desc(&b.maps[P.amap]);
+    for (int l = 0; l < nl; ++l) tc::tma_prefetch_desc(&b.maps[P.L[l].bmap]);
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();  // peers' barriers are initialised before any DSMEM traffic
+  tc::fence_after_sync();
+  stamp(1);
+  const uint32_t tmem = tmem_slot;
+  uint8_t* A = sm + kAreg;
+  // a CTA computes layer l unless l is the tanh-Gaussian head (rank 0 only); inactive CTAs load
+  // nothing for that layer
+  auto active_l = [&](int l) { return P.L[l].epi != GE_TG_FWD || rank == 0; };
+  if (tid == 0 && b.prefetch_b) {  // weights: never written by the immediately preceding kernel
+    issue_b(b, P.L[0], rank * P.L[0].slice, sm + kBreg, &bfull[0]);
+    if (nl > 1 && active_l(1)) issue_b(b, P.L[1], rank * P.L[1].slice, sm + kBreg + 32768, &bfull[1]);
+  }
+  tc::pdl_wait();
+  tc::pdl_trigger();
+  if (tid == 0) {
+    if (!b.prefetch_b) {
+      issue_b(b, P.L[0], rank * P.L[0].slice, sm + kBreg, &bfull[0]);
+      if (nl > 1 && active_l(1)) issue_b(b, P.L[1], rank * P.L[1].slice, sm + kBreg + 32768, &bfull[1]);
+    }
+    stamp(2);
+    tc::mbar_expect_tx(&aload, (uint32_t)P.L[0].nkb * 16384u);
+    for (int kb = 0; kb < P.L[0].nkb; ++kb) tc::tma_load_2d(A + kb * 16384, &b.maps[P.amap], 64 * kb, m0, &aload);
+  }
+  // the pair's boxes alternate between two sets by layer parity: a box bulk-copied to the peers in
+  // layer l is rewritten only in layer l + 2, after layer l + 1's cluster barrier proved every
+  // peer received it
+  uint8_t* pslots_base = sm + kSlots + q * 16384;
+  float* colacc = reinterpret_cast<float*>(sm + kColacc);
+  const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+  int nbwd = 0;  // backward layers so far (x_hat load barrier phase)
+
+  auto row_total2 = [&](float p1, float p2, float& t1, float& t2) {
+    red[0][hh][rl] = p1;
+    red[1][hh][rl] = p2;
+    __syncthreads();
+    t1 = red[0][0][rl] + red[0][1][rl];
+    t2 = red[1][0][rl] + red[1][1][rl];
+    if (hh == 0)
+      for (int rk = 0; rk < kCS; ++rk) {
+        tc::dsmem_st(&cl_red[0][rank][rl], (uint32_t)rk, t1);
+        tc::dsmem_st(&cl_red[1][rank][rl], (uint32_t)rk, t2);
+      }
+    tc::cluster_sync();
+    t1 = t2 = 0.f;
+#pragma unroll
+    for (int rk = 0; rk < kCS; ++rk) {
+      t1 += cl_red[0][rk][rl];
+      t2 += cl_red[1][rk][rl];
+    }
+  };
+  // both warps of pair q wrote the box: make it visible to the async proxy; the pair's first warp
+  // then stores it to global memory and / or bulk-copies it to the 4 CTAs' next-layer A.
+  auto box_out = [&](uint8_t* slot, int omap, int col, bool bcast) {
+    tc::fence_async_smem();
+    tc::named_bar(1 + q, 64);
+    if (hh == 0 && lane == 0) {
+      if (omap >= 0) {
+        tc::tma_store_2d(&b.maps[omap], slot, col, row0);
+        tc::bulk_commit();
+      }
+      if (bcast)
+        for (int rk = 0; rk < kCS; ++rk)
+          tc::bulk_s2cluster(tc::mapa(A + rank * 16384 + q * 4096, (uint32_t)rk), slot, 4096,
+                             tc::mapa(&anext, (uint32_t)rk));
+    }
+  };
+
+  for (int l = 0; l < nl; ++l) {
+    const CLayer& L = P.L[l];
+    const int epi = L.epi;
+    const bool active = active_l(l);
+    const int n0 = rank * L.slice;
+    const int nreal = min(L.slice, L.N - n0);
+    const bool bcast = l + 1 < nl;
+    uint8_t* pslots = pslots_base + (l & 1) * 8192;
+    if (tid < L.slice) {
+      const int gc = n0 + tid;
+      const bool ok = gc < L.N;
+      s_bias[tid] = (ok && L.bias) ? L.bias[gc] : 0.f;
+      s_g[tid] = (ok && L.g) ? L.g[gc] : 0.f;
+      s_beta[tid] = (ok && L.beta) ? L.beta[gc] : 0.f;
+    }
+    // ---- MMA: A (smem) x this CTA's weight slice -> TMEM ----------------------------------------
+    // every CTA waits for its broadcast input even when it does not use it: no DSMEM copy may
+    // still be landing in this CTA's shared memory when it exits
+    if (tid == 0 && l >= 1) tc::mbar_wait(&anext, (l - 1) & 1);
+    if (tid == 0 && active && nreal > 0) {
+      if (l == 0) tc::mbar_wait(&aload, 0);
+      tc::mbar_wait(&bfull[l & 1], (l >> 1) & 1);
+      tc::fence_after_sync();
+      const uint32_t a0 = tc::smem_u32(A), b0 = tc::smem_u32(sm + kBreg + (l & 1) * 32768);
+      const uint32_t id = tc::idesc_bf16_major(128, L.slice, 0, L.b_mn);
+      for (int kb = 0; kb < L.nkb; ++kb)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t ad = tc::sdesc_sw128(a0 + kb * 16384 + 32 * k, 16, 1024);
+          const uint64_t bd = L.b_mn ? tc::sdesc_sw128(b0 + kb * 8192 + 2048 * k, 8192, 1024)
+                                     : tc::sdesc_sw128(b0 + kb * L.slice * 128 + 32 * k, 16, 1024);
+          tc::mma_bf16(tmem, ad, bd, id, (kb | k) != 0);
+        }
+      tc::mma_commit(&done);
+    }
+    stamp(3 + 4 * l);
+    if (tid == 0 && bcast) tc::mbar_expect_tx(&anext, kCS * 4 * 4096);  // before the stats barrier
+    if (active && nreal > 0) {
+      tc::mbar_wait(&done, l & 1);
+      tc::fence_after_sync();
+    }
+    __syncthreads();  // s_bias / s_g / s_beta staged; layer l's MMAs done
+    stamp(4 + 4 * l);
+    if (tid == 0 && l + 2 < nl && active_l(l + 2))  // layer l's B buffer is free: prefetch layer l + 2
+      issue_b(b, P.L[l + 2], rank * P.L[l + 2].slice, sm + kBreg + (l & 1) * 32768, &bfull[l & 1]);
+
+    float v[32], a[32];
+    if (epi == GE_LN_RELU || epi == GE_LN_TANH) {
+      // slice 64: warp (q, hh) owns columns 32 hh .. 32 hh + 31 of rows row0 ..
+      tc::tmem_ld32(trow + hh * 32, v);
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float u = v[j] + s_bias[hh * 32 + j];
+        s1 += u;
+        s2 += u * u;
+      }
+      float t1, t2;
+      row_total2(s1, s2, t1, t2);
+      stamp(5 + 4 * l);
+      const float mean = t1 / (float)L.N;
+      const float rs = rsqrtf(fmaxf(t2 / (float)L.N - mean * mean, 0.f) + L.ln_eps);
+      if (rv && hh == 0 && rank == 0 && L.rstd) L.rstd[r] = rs;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int cc = hh * 32 + j;
+        const float x = (v[j] + s_bias[cc] - mean) * rs;
+        const float n = fmaf(x, s_g[cc], s_beta[cc]);
+        a[j] = x;
+        v[j] = (epi == GE_LN_RELU) ? fmaxf(n, 0.f) : tanh_fast(n);
+      }
+      uint8_t* sy = pslots;
+      uint8_t* sx = pslots + 4096;
+      if (l >= 1 && hh == 0 && lane == 0) tc::bulk_wait_read<0>();  // the pair's boxes of layer l-1
+      tc::named_bar(1 + q, 64);
+      box_put(sy, hh, v);
+      if (L.xmap >= 0) box_put(sx, hh, a);
+      box_out(sy, L.omap, n0, bcast);
+      if (L.xmap >= 0) box_out(sx, L.xmap, n0, false);
+    } else if (epi == GE_BWD_LN_RELU || epi == GE_BWD_LN_TANH) {
+      uint8_t* sl = pslots;
+      if (l >= 1 && hh == 0 && lane == 0) tc::bulk_wait_read<0>();
+      tc::named_bar(1 + q, 64);
+      if (hh == 0 && lane == 0) {
+        tc::mbar_expect_tx(&ld_bar[q], 4096);
+        tc::tma_load_2d(sl, &b.maps[L.xmap], n0, row0, &ld_bar[q]);
+      }
+      tc::mbar_wait(&ld_bar[q], nbwd & 1);
+      ++nbwd;
+      tc::tmem_ld32(trow + hh * 32, v);
+      box_get(sl, hh, a);
+      float pg[32], pb[32], s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int cc = hh * 32 + j;
+        const float x = rv ? a[j] : 0.f;
+        const float n = fmaf(x, s_g[cc], s_beta[cc]);
+        const float dn = rv ? ((epi == GE_BWD_LN_RELU) ? (n > 0.f ? v[j] : 0.f) : v[j] * sech2_fast(n)) : 0.f;
+        const float dxh = dn * s_g[cc];
+        s1 += dxh;
+        s2 += dxh * x;
+        pg[j] = dn * x;
+        pb[j] = dn;
+      }
+      const float cg = colsum32(pg);
+      const float cb = colsum32(pb);
+      colacc[(q * 3 + 1) * 64 + hh * 32 + lane] = cg;
+      colacc[(q * 3 + 2) * 64 + hh * 32 + lane] = cb;
+      float m1, m2;
+      row_total2(s1, s2, m1, m2);
+      stamp(5 + 4 * l);
+      m1 /= (float)L.N;
+      m2 /= (float)L.N;
+      const float rs = rv ? L.rstd[r] : 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int cc = hh * 32 + j;
+        const float x = rv ? a[j] : 0.f;
+        const float n = fmaf(x, s_g[cc], s_beta[cc]);
+        const float dn = rv ? ((epi == GE_BWD_LN_RELU) ? (n > 0.f ? v[j] : 0.f) : v[j] * sech2_fast(n)) : 0.f;
+        v[j] = rv ? rs * (dn * s_g[cc] - m1 - x * m2) : 0.f;
+        a[j] = v[j];
+      }
+      box_put(sl, hh, v);
+      const float cx = colsum32(a);
+      colacc[(q * 3 + 0) * 64 + hh * 32 + lane] = cx;
+      box_out(sl, L.omap, n0, bcast);
+      __syncthreads();
+      if (L.part)
+        for (int e = tid; e < 3 * 64; e += kThr) {
+          const int kk = e / 64, c = e - kk * 64;
+          float s = 0.f;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) s += colacc[(qq * 3 + kk) * 64 + c];
+          L.part[((int64_t)mt * 3 + kk) * L.N + n0 + c] = s;
+        }
+    } else if (epi == GE_BIAS_F32) {
+      if (hh == 0 && nreal > 0) {  // slice 32: one chunk
+        tc::tmem_ld32(trow, v);
+        if (rv) {
+          float* o = L.outf + (int64_t)r * L.ldf + n0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < nreal) o[j] = v[j] + s_bias[j];
+        }
+      }
+    } else if (epi == GE_TG_FWD) {
+      if (rank == 0 && hh == 0) {
+        // staging in the A region: the head is the last layer, its MMA is done, no copy targets A
+        float* T = reinterpret_cast<float*>(sm + kAreg) + warp * 32 * 17;
+        float v16[16];
+        tc::tmem_ld16(trow, v16);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) T[lane * 17 + j] = v16[j];
+        __syncwarp();
+        const float* o = T + lane * 17;
+        if (rv) {
+          const int Ad = L.N / 2;
+          float lp = 0.f;
+          for (int d = 0; d < Ad; ++d) {
+            const float mu = o[d] + s_bias[d], lg = o[Ad + d] + s_bias[Ad + d];
+            if (L.tgo) {
+              L.tgo[(int64_t)r * 2 * Ad + d] = mu;
+              L.tgo[(int64_t)r * 2 * Ad + Ad + d] = lg;
+            }
+            const float log_std = L.lo + 0.5f * (L.hi - L.lo) * (tanhf(lg) + 1.f);
+            const float sd = expf(log_std);
+            const float e = L.eps ? L.eps[(int64_t)r * Ad + d] : 0.f;
+            const float u = fmaf(sd, e, mu);
+            const float at = tanhf(u);
+            if (L.act) L.act[(int64_t)r * Ad + d] = at;
+            if (L.act_bf) L.act_bf[(int64_t)r * L.ld_act_bf + d] = __float2bfloat16_rn(at);
+            lp += -0.5f * e * e - log_std - 0.5f * kLog2Pi - logf(sech2f(u) + kSquashEps);
+          }
+          if (L.logp) L.logp[r] = lp;
+        }
+      }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    stamp(6 + 4 * l);
+  }
+  if (lane == 0) tc::bulk_wait_read<0>();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();  // every outgoing bulk copy has landed in its destination CTA
+  stamp(15);
+  if (warp == 0) tc::tmem_dealloc(tmem, 64);
+}
+
+}  // namespace
+
+bool chain_supported(int hidden) { return hidden == 256; }
+
+static unsigned long long* g_cdbg = nullptr;
+static int g_cdbg_n = 0;
+int chain_debug_times(unsigned long long* host, int max_entries) {
+  if (!g_cdbg) return 0;
+  cudaDeviceSynchronize();
+  const int n = g_cdbg_n * 16 < max_entries ? g_cdbg_n * 16 : max_entries;
+  cudaMemcpy(host, g_cdbg, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return n;
+}
+
+CProb& ChainBuilder::add(int M, const Mat& A) {
+  if (b.nprob >= kChainMaxProb) {
+    err = 1;
+    return b.p[kChainMaxProb - 1];
+  }
+  CProb& p = b.p[b.nprob];
+  memset(&p, 0, sizeof(p));
+  amat[b.nprob] = A;
+  p.M = M;
+  b.nprob++;
+  return p;
+}
+
+CLayer& ChainBuilder::layer(CProb& p, int epi, const Mat& W, int b_mn, int N, int K, const Mat& O, const Mat& X) {
+  const int pi = (int)(&p - b.p);
+  if (p.nlayers >= kChainMaxLayers) {
+    err = 2;
+    return p.L[kChainMaxLayers - 1];
+  }
+  const int l = p.nlayers++;
+  CLayer& L = p.L[l];
+  memset(&L, 0, sizeof(L));
+  L.epi = epi;
+  L.N = N;
+  L.K = K;
+  L.nkb = (K + 63) / 64;
+  L.b_mn = b_mn;
+  L.ln_eps = 1e-5f;
+  L.slice = (epi == GE_BIAS_F32) ? 32 : (epi == GE_TG_FWD ? 16 : 64);
+  L.omap = L.xmap = -1;
+  wmat[pi][l] = W;
+  omat[pi][l] = O;
+  xmat[pi][l] = X;
+  return L;
+}
+
+int chain_launch(ChainBuilder& cb, cudaStream_t s) {
+  CBatch& b = cb.b;
+  if (cb.err || b.nprob == 0) return cb.err ? -1 : 0;
+  int nm = 0, ncl = 0;
+  double flops = 0;
+  for (int i = 0; i < b.nprob; ++i) {
+    CProb& p = b.p[i];
+    if (p.nlayers < 1) return -1;
+    p.c0 = ncl;
+    ncl += (p.M + 127) / 128;
+    if (nm + 1 > kChainMaxMaps || tmap_get(cb.amat[i], 128, &b.maps[nm])) return -1;
+    p.amap = nm++;
+    for (int l = 0; l < p.nlayers; ++l) {
+      CLayer& L = p.L[l];
+      const bool ln = L.epi == GE_LN_RELU || L.epi == GE_LN_TANH || L.epi == GE_BWD_LN_RELU || L.epi == GE_BWD_LN_TANH;
+      if (L.nkb > 4 || (ln && L.N != 256) || (L.epi == GE_BIAS_F32 && L.N > 128) ||
+          (L.epi == GE_TG_FWD && (L.N > 16 || l != p.nlayers - 1)) || (l > 0 && p.L[l - 1].N != L.K))
+        return -1;
+      if (l + 1 < p.nlayers && !ln) return -1;  // only LayerNorm layers feed a next layer
+      if (nm + 3 > kChainMaxMaps) return -1;
+      if (tmap_get(cb.wmat[i][l], L.b_mn ? 64 : L.slice, &b.maps[nm])) return -1;
+      L.bmap = nm++;
+      if (cb.omat[i][l].ptr) {
+        if (tmap_get(cb.omat[i][l], 32, &b.maps[nm])) return -1;
+        L.omap = nm++;
+      }
+      if (cb.xmat[i][l].ptr) {
+        if (tmap_get(cb.xmat[i][l], 32, &b.maps[nm])) return -1;
+        L.xmap = nm++;
+      } else if (L.epi == GE_BWD_LN_RELU || L.epi == GE_BWD_LN_TANH) {
+        return -1;
+      }
+      flops += 2.0 * p.M * (double)L.N * L.K;
+    }
+  }
+  b.nclusters = ncl;
+  b.dbg = nullptr;
+  {
+    static const char* env = getenv("SQUINT_CHAIN_DBG");
+    static int no = 0;
+    if (env && no++ == atoi(env)) {
+      if (!g_cdbg) cudaMalloc(&g_cdbg, 1024 * 16 * sizeof(unsigned long long));
+      cudaMemset(g_cdbg, 0, 1024 * 16 * sizeof(unsigned long long));
+      g_cdbg_n = ncl * kCS;
+      b.dbg = g_cdbg;
+    }
+  }
+  const size_t smem = kSmem + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(ncl * kCS);
+  cfg.blockDim = dim3(kThr);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr2[2];
+  attr2[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr2[0].val.programmaticStreamSerializationAllowed = 1;
+  attr2[1].id = cudaLaunchAttributeClusterDimension;
+  attr2[1].val.clusterDim.x = kCS;
+  attr2[1].val.clusterDim.y = 1;
+  attr2[1].val.clusterDim.z = 1;
+  cfg.attrs = attr2;
+  cfg.numAttrs = 2;
+  note_launch(s, "k_chain", flops, 0);
+  return (int)cudaLaunchKernelEx(&cfg, k_chain, b);
+}
+
+}  // namespace sq
+
+extern "C" __attribute__((visibility("default"))) int squint_debug_chain_times(unsigned long long* host, int max_entries) {
+  return sq::chain_debug_times(host, max_entries);
+}

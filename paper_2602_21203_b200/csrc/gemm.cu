@@ -23,11 +23,13 @@
 #include "common.cuh"
 #include "gemm.cuh"
 #include "tc.cuh"
+#include "gemm_dev.cuh"
 
 namespace sq {
 
 namespace {
 
+using namespace gd;
 constexpr int kThreads = 256;
 constexpr int kMaxStages = 8;
 constexpr int kABytes = 16384;  // 128 x 64 bf16
@@ -37,126 +39,6 @@ constexpr int kColaccOff = 4 * 4 * 4096;                  // after the 4 warp pa
 constexpr int kEpiBytes = kColaccOff + 4 * 3 * 512 * 4;    // + LN-bwd column partials [4][3][512]
 
 int g_pdl = 1;
-
-__device__ __forceinline__ int round16(int x) { return (x + 15) & ~15; }
-
-// ---- per-thread row I/O: thread = one tile row, 32 consecutive columns ---------------------
-// Vector (16-byte) accesses when the row segment is aligned and complete, predicated scalar
-// accesses for tails; global loads are issued together (memory-level parallelism).
-__device__ __forceinline__ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-
-__device__ __forceinline__ void row_ld_f32(const float* __restrict__ p, int ncv, float (&v)[32]) {
-  if (ncv == 32 && al16(p)) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float4 f = __ldg(reinterpret_cast<const float4*>(p) + j);
-      v[4 * j] = f.x, v[4 * j + 1] = f.y, v[4 * j + 2] = f.z, v[4 * j + 3] = f.w;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = j < ncv ? __ldg(p + j) : 0.f;
-  }
-}
-__device__ __forceinline__ void row_ld_bf16(const bf16* __restrict__ p, int ncv, float (&v)[32]) {
-  if (ncv == 32 && al16(p)) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint4 u = __ldg(reinterpret_cast<const uint4*>(p) + j);
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 f = __bfloat1622float2(h[k]);
-        v[8 * j + 2 * k] = f.x, v[8 * j + 2 * k + 1] = f.y;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = j < ncv ? __bfloat162float(p[j]) : 0.f;
-  }
-}
-__device__ __forceinline__ void row_st_f32(float* p, int ncv, const float (&v)[32]) {
-  if (ncv == 32 && al16(p)) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      reinterpret_cast<float4*>(p)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-  } else {
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < ncv) p[j] = v[j];
-  }
-}
-__device__ __forceinline__ void row_st_bf16(bf16* p, int ncv, const float (&v)[32]) {
-  if (ncv == 32 && al16(p)) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float f[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) f[k] = v[8 * j + k];
-      reinterpret_cast<uint4*>(p)[j] = tc::pack_bf16x8(f);
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < ncv) p[j] = __float2bfloat16_rn(v[j]);
-  }
-}
-// Column sums over the warp's 32 rows by a butterfly transpose-reduce (31 shuffles): on return
-// lane l holds sum over lanes of v[l].  v is destroyed.
-__device__ __forceinline__ float colsum32(float (&v)[32]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const bool up = (lane & s) != 0;
-#pragma unroll
-    for (int j = 0; j < s; ++j) {
-      const float send = up ? v[j] : v[j + s];
-      const float keep = up ? v[j + s] : v[j];
-      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
-    }
-  }
-  return v[0];
-}
-
-// ---- epilogue staging: per-warp ring of four 64-column x 32-row bf16 boxes (128B swizzle) ---
-// A lane owns one row of the box; the tile moves between smem and global memory by TMA.
-constexpr int kSlotBytes = 4096;
-__device__ __forceinline__ uint32_t box_off(int row, int chunk16) {
-  return (uint32_t)(row * 128 + ((chunk16 ^ (row & 7)) << 4));
-}
-// write 32 values (columns 32c .. 32c+31 of the box) of this lane's row
-__device__ __forceinline__ void box_put(uint8_t* slot, int c, const float (&v)[32]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    float f[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) f[k] = v[8 * j + k];
-    *reinterpret_cast<uint4*>(slot + box_off(lane, 4 * c + j)) = tc::pack_bf16x8(f);
-  }
-}
-__device__ __forceinline__ void box_get(const uint8_t* slot, int c, float (&v)[32]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint4 u = *reinterpret_cast<const uint4*>(slot + box_off(lane, 4 * c + j));
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float2 f = __bfloat1622float2(h[k]);
-      v[8 * j + 2 * k] = f.x, v[8 * j + 2 * k + 1] = f.y;
-    }
-  }
-}
-// both warps of pair q have written their halves of the box: make it visible to the TMA unit
-// and store it from the pair's first warp
-__device__ __forceinline__ void pair_store(uint8_t* slot, const void* map, int col, int row, int q, int hh) {
-  tc::fence_async_smem();
-  tc::named_bar(1 + q, 64);
-  if (hh == 0 && (threadIdx.x & 31) == 0) {
-    tc::tma_store_2d(map, slot, col, row);
-    tc::bulk_commit();
-  }
-}
 
 struct TileGeo {
   int nt, nbox_b, bbytes, bnb;
@@ -188,7 +70,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   __shared__ uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], done_bar, ld_bar[8];
   __shared__ uint32_t tmem_slot;
   __shared__ float red[2][2][128];
-  __shared__ float cl_red[2][128];  // this CTA's per-row partials, read by the cluster peers
+  __shared__ float cl_red[2][4][128];  // per-row partials of each cluster CTA, pushed by the CTAs
   __shared__ __align__(16) float s_bias[512], s_g[512], s_beta[512];  // per-column epilogue params
 
   const int tile = blockIdx.x;
@@ -347,18 +229,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   // per-row totals over the whole LayerNorm row: the two column halves of this CTA (smem), then
   // the CTAs of the cluster (distributed shared memory, summed in rank order: every CTA gets the
   // same bits)
-  auto row_total = [&](float part, int k) -> float {
-    red[k][hh][rl] = part;
-    __syncthreads();
-    float t = red[k][0][rl] + red[k][1][rl];
-    if (b.cs > 1) {
-      if (hh == 0) cl_red[k][rl] = t;
-      tc::cluster_sync();
-      t = 0.f;
-      for (int rk = 0; rk < b.cs; ++rk) t += tc::dsmem_ld(&cl_red[k][rl], (uint32_t)rk);
-    }
-    return t;
-  };
+  // per-row totals over the whole LayerNorm row: the two column halves of this CTA (smem), then
+  // the CTAs of the cluster.  Push model: every CTA stores its row partials into each peer's
+  // cl_red[k][rank] (distributed shared memory), one cluster barrier, then local reads summed in
+  // rank order (every CTA gets the same bits; no remote access after the barrier).
   auto row_total2 = [&](float p1, float p2, float& t1, float& t2) {
     red[0][hh][rl] = p1;
     red[1][hh][rl] = p2;
@@ -366,12 +240,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     t1 = red[0][0][rl] + red[0][1][rl];
     t2 = red[1][0][rl] + red[1][1][rl];
     if (b.cs > 1) {
-      if (hh == 0) cl_red[0][rl] = t1, cl_red[1][rl] = t2;
+      const uint32_t me = (uint32_t)(blockIdx.x % b.cs);
+      if (hh == 0)
+        for (int rk = 0; rk < b.cs; ++rk) {
+          tc::dsmem_st(&cl_red[0][me][rl], (uint32_t)rk, t1);
+          tc::dsmem_st(&cl_red[1][me][rl], (uint32_t)rk, t2);
+        }
       tc::cluster_sync();
       t1 = t2 = 0.f;
       for (int rk = 0; rk < b.cs; ++rk) {
-        t1 += tc::dsmem_ld(&cl_red[0][rl], (uint32_t)rk);
-        t2 += tc::dsmem_ld(&cl_red[1][rl], (uint32_t)rk);
+        t1 += cl_red[0][rk][rl];
+        t2 += cl_red[1][rk][rl];
       }
     }
   };
@@ -459,8 +338,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
         if (cc < nreal) s1 += u, s2 += u * u;
       }
     }
+    stamp(5);
     float t1, t2;
     row_total2(s1, s2, t1, t2);
+    stamp(6);
     const float mean = t1 / (float)N;
     const float rs = rsqrtf(fmaxf(t2 / (float)N - mean * mean, 0.f) + P.ln_eps);
     if (rv && hh == 0 && n0 == 0 && P.rstd) P.rstd[r] = rs;
@@ -628,10 +509,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     }
   }
 
-  if (lane == 0) tc::bulk_wait_all();  // TMA stores have finished reading this CTA's smem
+  stamp(7);
+  if (lane == 0) tc::bulk_wait_read<0>();  // TMA stores have finished reading this CTA's smem
   tc::fence_before_sync();
   __syncthreads();
-  if (b.cs > 1) tc::cluster_sync();  // peers are done reading cl_red
   stamp(4);
   if (warp == 0) tc::tmem_dealloc(tmem, ncols);
 }

@@ -163,7 +163,8 @@ __global__ void __launch_bounds__(256) k_metrics(const __grid_constant__ Metrics
     lpi = a.extras2[0];
     q = a.extras2[1];
   }
-  for (int i = threadIdx.x; i < kAdamBlocks; i += blockDim.x) gs += a.sumsq_part[i];
+  const int npart = a.npart > 0 ? a.npart : kAdamBlocks;
+  for (int i = threadIdx.x; i < npart; i += blockDim.x) gs += a.sumsq_part[i];
   gs = block_sum(gs, red);
   if (threadIdx.x == 0) {
     const float LQ = a.scal[S_LQ], La = a.scal[S_LALPHA];
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(256) k_adam_sh(float4* __restrict__ p, const f
                                                  float4* __restrict__ m, float4* __restrict__ v, int64_t n4, float lr,
                                                  float b1, float b2, float eps, const float* __restrict__ c1p,
                                                  const float* __restrict__ c2p, float* __restrict__ part,
-                                                 const __grid_constant__ ShadowTable t) {
+                                                 const __grid_constant__ ShadowTable t, int base) {
   __shared__ float red[32];
   const float c1 = c1p[0], c2 = c2p[0];
   float ss = 0.f;
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(256) k_adam_sh(float4* __restrict__ p, const f
     if (t.n) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int sl = shadow_slot(t, (int)(4 * i + k));
+        const int sl = shadow_slot(t, base + (int)(4 * i + k));
         if (sl >= 0) t.base[sl] = __float2bfloat16_rn(pf[k]);
       }
     }
@@ -284,13 +285,13 @@ int launch_shadow(const float* master, const ShadowTable& t, cudaStream_t s) {
 
 int launch_adam_shadow(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
                        float eps, const float* c1, const float* c2, float* sumsq_part, const ShadowTable* t,
-                       cudaStream_t s) {
+                       cudaStream_t s, int64_t base, int nblocks) {
   ShadowTable none;
   memset(&none, 0, sizeof(none));
   note_launch(s, "k_adam", 0, 28.0 * (double)n);
-  k_adam_sh<<<kAdamBlocks, 256, 0, s>>>(reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
-                                        reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n / 4, lr, b1, b2,
-                                        eps, c1, c2, sumsq_part, t ? *t : none);
+  k_adam_sh<<<nblocks, 256, 0, s>>>(reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
+                                    reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n / 4, lr, b1, b2, eps,
+                                    c1, c2, sumsq_part, t ? *t : none, (int)base);
   return (int)cudaGetLastError();
 }
 

@@ -40,6 +40,7 @@ int launch_scalars(const ScalarsArgs& a, cudaStream_t s);
 // c2 = 1/(1-b2^t) read from scal.  n % 4 == 0, 16-byte aligned.  If sumsq_part != NULL,
 // writes sum(g^2) per block (kAdamBlocks entries, fixed order).
 constexpr int kAdamBlocks = 296;
+constexpr int kEncAdamBlocks = 16;  // the encoder's slice of the critic Adam (bf16 path, own stream)
 int launch_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
                 const float* c1, const float* c2, float* sumsq_part, cudaStream_t s);
 // target = (1 - tau) target + tau online; any n, any alignment.
@@ -63,9 +64,10 @@ struct ShadowTable {
 // Full refresh of one group's shadow from its fp32 master.
 int launch_shadow(const float* master, const ShadowTable& t, cudaStream_t s);
 // Adam (as launch_adam) that also writes the updated weights' bf16 shadow (t may be NULL).
+// `base` = flat group index of p[0] (shadow lookups), `nblocks` = grid (= partial sums written).
 int launch_adam_shadow(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
                        float eps, const float* c1, const float* c2, float* sumsq_part, const ShadowTable* t,
-                       cudaStream_t s);
+                       cudaStream_t s, int64_t base = 0, int nblocks = kAdamBlocks);
 // Polyak over a 16-byte aligned buffer (n % 4 == 0) that also refreshes the target shadow.
 int launch_polyak_shadow(float* target, const float* online, int64_t n, float tau, const ShadowTable* t,
                          cudaStream_t s);
@@ -79,6 +81,7 @@ struct MetricsArgs {
   const float* scal;
   const float* extras;
   float* out;            // [8]
+  int npart;             // number of Adam partial sums of squares (0 -> kAdamBlocks)
   int reduce_local;      // 1: sum row_lpi/row_q here; 0: read pre-reduced sums from extras2
   const float* extras2;  // [2] = (sum row_lpi, sum row_q) when reduce_local == 0
 };

@@ -204,6 +204,26 @@ __device__ __forceinline__ float dsmem_ld(const float* local, uint32_t rank) {
   (void)r;
   return v;
 }
+// store a float at the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ void dsmem_st(float* local, uint32_t rank, float v) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(local)), "r"(rank));
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+// shared::cluster address of `local` in CTA `rank`
+__device__ __forceinline__ uint32_t mapa(const void* local, uint32_t rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(local)), "r"(rank));
+  return a;
+}
+// bulk copy local shared memory -> shared memory of a cluster CTA, completion (bytes) on the
+// destination CTA's mbarrier (both cluster addresses from mapa)
+__device__ __forceinline__ void bulk_s2cluster(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst),
+               "r"(smem_u32(src)), "r"(bytes), "r"(mbar)
+               : "memory");
+}
 // named barrier over `count` threads
 __device__ __forceinline__ void named_bar(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");

@@ -14,6 +14,7 @@
 // column-permuted to match, and their gradient is written back in the master's CHW order.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <optional>
 #include <string>
@@ -22,6 +23,7 @@
 #include "comm.hpp"
 #include "common.cuh"
 #include "encoder.cuh"
+#include "chain.cuh"
 #include "gemm.cuh"
 #include "heads.cuh"
 #include "layout.hpp"
@@ -184,7 +186,7 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
   w.part_pp = fl(mt * 3 * Lt);
   w.grad_critic = fl(L.gsize[SQUINT_GROUP_CRITIC] + kExtra);
   w.grad_actor = fl(L.gsize[SQUINT_GROUP_ACTOR] + kExtra);
-  w.adam_part = fl(kAdamBlocks);
+  w.adam_part = fl(kAdamBlocks + kEncAdamBlocks);
   w.scal = fl(kScal);
   w.lpi_sums = fl(2);
   w.y1b = P.take((size_t)B * P1 * C * 2);
@@ -199,11 +201,30 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
   return w;
 }
 
+// Per-thread auxiliary stream and events: the encoder backward and the encoder's Adam slice run
+// on a branch forked from the caller's stream (graph capture turns this into parallel graph
+// nodes) while the actor-loss chain proceeds; the branch joins before the metrics kernel.
+struct Aux {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, scal = nullptr, join = nullptr;
+  bool ok() {
+    if (s) return true;
+    return cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&scal, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
+  }
+};
+thread_local Aux t_aux;
+
 struct Ctx {
   const squint_dims& d;
   const Layout& L;
   char* ws;
   cudaStream_t s;
+  bool chain;      // fused forward MLP chains (hidden width 256) instead of one launch per layer
+  bool chain_bwd;  // fused backward chains (off by default: measured slower than per-layer launches)
+  Aux* aux;        // auxiliary branch (NULL: everything on the caller's stream)
   Mat mat(const BM& m) const { return Mat{ws + m.off, m.rows, m.cols, m.ld}; }
   bf16* bp(const BM& m) const { return reinterpret_cast<bf16*>(ws + m.off); }
   float* F(size_t off) const { return reinterpret_cast<float*>(ws + off); }
@@ -307,6 +328,31 @@ void bwd_ln(GProb& p, const Lin& W, bf16* xh, int ldx, float* rstd, bf16* out, i
   p.part = part;
 }
 
+Mat none_mat() { return Mat{nullptr, 0, 0, 0}; }
+
+
+// a LayerNorm layer (forward) of a fused chain
+CLayer& ch_fwd(ChainBuilder& cb, CProb& p, int epi, const Lin& W, int N, int K, const Mat& O, const Mat& X, float* rstd,
+               float ln_eps) {
+  CLayer& L = cb.layer(p, epi, W.w, 0, N, K, O, X);
+  L.bias = W.b;
+  L.g = W.g;
+  L.beta = W.beta;
+  L.rstd = rstd;
+  L.ln_eps = ln_eps;
+  return L;
+}
+// a dX = dY W layer with the LayerNorm backward of the layer below (`ln` holds its g, beta)
+CLayer& ch_bwd(ChainBuilder& cb, CProb& p, int epi, const Mat& W, const Lin& ln, int N, int K, const Mat& O,
+               const Mat& X, float* rstd, float* part) {
+  CLayer& L = cb.layer(p, epi, W, 1, N, K, O, X);
+  L.g = ln.g;
+  L.beta = ln.beta;
+  L.rstd = rstd;
+  L.part = part;
+  return L;
+}
+
 #define BF_CK(expr)                                                                                     \
   do {                                                                                                  \
     int _e = (int)(expr);                                                                               \
@@ -397,7 +443,35 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     BF_CK(gemm_launch(gb, s));
   }
   // a7: actor MLP on s' (target sample) and on s (alpha / actor losses)
-  {
+  if (c.chain) {
+    PhaseScope ps(5, rep, s);
+    ChainBuilder cb(1);
+    CProb& pn = cb.add(B, c.mat(w.Xan));
+    ch_fwd(cb, pn, GE_LN_RELU, am.l1, Ha, npi, none_mat(), none_mat(), nullptr, le);
+    ch_fwd(cb, pn, GE_LN_RELU, am.l2, Ha, Ha, none_mat(), none_mat(), nullptr, le);
+    CLayer& tn = cb.layer(pn, GE_TG_FWD, am.l3.w, 0, 2 * A, Ha, none_mat(), none_mat());
+    tn.bias = am.l3.b;
+    tn.eps = eps_next;
+    tn.act_bf = c.bp(w.Xt) + Lt + P;
+    tn.ld_act_bf = w.Xt.ld;
+    tn.logp = c.F(w.logp_next);
+    tn.lo = hp.log_std_min;
+    tn.hi = hp.log_std_max;
+    CProb& pc = cb.add(B, c.mat(w.Xac));
+    ch_fwd(cb, pc, GE_LN_RELU, am.l1, Ha, npi, c.mat(w.H1ac), c.mat(w.XH1ac), c.F(w.R1ac), le);
+    ch_fwd(cb, pc, GE_LN_RELU, am.l2, Ha, Ha, c.mat(w.H2ac), c.mat(w.XH2ac), c.F(w.R2ac), le);
+    CLayer& tc_ = cb.layer(pc, GE_TG_FWD, am.l3.w, 0, 2 * A, Ha, none_mat(), none_mat());
+    tc_.bias = am.l3.b;
+    tc_.eps = eps_cur;
+    tc_.act = c.F(w.a_cur);
+    tc_.act_bf = c.bp(w.Xq1) + Lt + P;
+    tc_.ld_act_bf = w.Xq1.ld;
+    tc_.logp = c.F(w.logp_cur);
+    tc_.tgo = c.F(w.tgo_ac);
+    tc_.lo = hp.log_std_min;
+    tc_.hi = hp.log_std_max;
+    BF_CK(chain_launch(cb, s));
+  } else {
     PhaseScope ps(5, rep, s);
     {
       GemmBuilder gb(1);
@@ -435,7 +509,29 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     }
   }
   // a8: target heads on (z', s', a~') and online heads on (z, s, a)
-  {
+  if (c.chain) {
+    PhaseScope ps(6, rep, s);
+    ChainBuilder cb(1);
+    for (int i = 0; i < 2; ++i) {
+      CProb& p = cb.add(B, c.mat(w.Xt));
+      ch_fwd(cb, p, GE_LN_RELU, tq[i].l1, Hc, nq, none_mat(), none_mat(), nullptr, le);
+      ch_fwd(cb, p, GE_LN_RELU, tq[i].l2, Hc, Hc, none_mat(), none_mat(), nullptr, le);
+      CLayer& l3 = cb.layer(p, GE_BIAS_F32, tq[i].l3.w, 0, N, Hc, none_mat(), none_mat());
+      l3.bias = tq[i].l3.b;
+      l3.outf = c.F(w.tlogits) + (size_t)i * B * N;
+      l3.ldf = N;
+    }
+    for (int i = 0; i < 2; ++i) {
+      CProb& p = cb.add(B, c.mat(w.Xq));
+      ch_fwd(cb, p, GE_LN_RELU, cq[i].l1, Hc, nq, c.mat(w.qH1[i]), c.mat(w.qXH1[i]), c.F(w.qR1[i]), le);
+      ch_fwd(cb, p, GE_LN_RELU, cq[i].l2, Hc, Hc, c.mat(w.qH2[i]), c.mat(w.qXH2[i]), c.F(w.qR2[i]), le);
+      CLayer& l3 = cb.layer(p, GE_BIAS_F32, cq[i].l3.w, 0, N, Hc, none_mat(), none_mat());
+      l3.bias = cq[i].l3.b;
+      l3.outf = c.F(w.logits) + (size_t)i * B * N;
+      l3.ldf = N;
+    }
+    BF_CK(chain_launch(cb, s));
+  } else {
     PhaseScope ps(6, rep, s);
     {
       GemmBuilder gb(1);
@@ -499,6 +595,17 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
   float* gc = c.F(w.grad_critic);
   {
     PhaseScope ps(8, rep, s);
+    if (c.chain_bwd) {
+      ChainBuilder cb(1);
+      for (int i = 0; i < 2; ++i) {
+        CProb& p = cb.add(B, c.half(w.dlog, i));
+        ch_bwd(cb, p, GE_BWD_LN_RELU, cq[i].l3.w, cq[i].l2, Hc, N, c.mat(w.dA2c[i]), c.mat(w.qXH2[i]), c.F(w.qR2[i]),
+               c.F(w.part_q2[i]));
+        ch_bwd(cb, p, GE_BWD_LN_RELU, cq[i].l2.w, cq[i].l1, Hc, Hc, c.mat(w.dA1c[i]), c.mat(w.qXH1[i]),
+               c.F(w.qR1[i]), c.F(w.part_q1[i]));
+      }
+      BF_CK(chain_launch(cb, s));
+    } else {
     {
       GemmBuilder gb(1);
       for (int i = 0; i < 2; ++i) {
@@ -516,6 +623,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
                c.F(w.part_q1[i]));
       }
       BF_CK(gemm_launch(gb, s));
+    }
     }
     {
       // dz = sum_i dA1_i W1_i[:, :L] (K-concatenation of the two heads) -> tanh + LN of the projection
@@ -535,6 +643,35 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       p.ldo = w.dh.ld;
       BF_CK(gemm_launch(gb, s));
     }
+  }
+  // encoder backward: on the auxiliary branch when single-GPU (overlaps the critic dW GEMM and
+  // the actor-loss chain), inline when the gradients are all-reduced
+  const bool branch = comm == nullptr && c.aux != nullptr;
+  cudaStream_t es = branch ? c.aux->s : s;
+  if (branch) {
+    BF_CK(cudaEventRecord(c.aux->fork, s));
+    BF_CK(cudaStreamWaitEvent(es, c.aux->fork, 0));
+  }
+  {
+    PhaseScope ps(10, rep, es);
+    EncBwdArgs e;
+    memset(&e, 0, sizeof(e));
+    e.B = B;
+    e.C = C;
+    e.c_in = d.img_c;
+    e.H = d.img_h;
+    e.dA2_hwc = c.bp(w.dh);
+    e.dA2_ld = w.dh.ld;
+    e.y1_hwc = reinterpret_cast<const bf16*>(c.ws + w.y1b);
+    e.img = reinterpret_cast<const uint8_t*>(c.ws + w.img0);
+    e.w2 = crit + L.off(gC, "enc.conv2.w");
+    e.part = c.F(w.enc_part);
+    e.wtiles = wtiles;
+    e.gw1 = gc + L.off(gC, "enc.conv1.w");
+    e.gb1 = gc + L.off(gC, "enc.conv1.b");
+    e.gw2 = gc + L.off(gC, "enc.conv2.w");
+    e.gb2 = gc + L.off(gC, "enc.conv2.b");
+    BF_CK(launch_enc_bwd_tc(e, es));
   }
   {
     PhaseScope ps(9, rep, s);
@@ -558,27 +695,6 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     pp.perm_c = C;
     pp.perm_p = P2;
     BF_CK(gemm_launch(gb, s));
-  }
-  {
-    PhaseScope ps(10, rep, s);
-    EncBwdArgs e;
-    memset(&e, 0, sizeof(e));
-    e.B = B;
-    e.C = C;
-    e.c_in = d.img_c;
-    e.H = d.img_h;
-    e.dA2_hwc = c.bp(w.dh);
-    e.dA2_ld = w.dh.ld;
-    e.y1_hwc = reinterpret_cast<const bf16*>(c.ws + w.y1b);
-    e.img = reinterpret_cast<const uint8_t*>(c.ws + w.img0);
-    e.w2 = crit + L.off(gC, "enc.conv2.w");
-    e.part = c.F(w.enc_part);
-    e.wtiles = wtiles;
-    e.gw1 = gc + L.off(gC, "enc.conv1.w");
-    e.gb1 = gc + L.off(gC, "enc.conv1.b");
-    e.gw2 = gc + L.off(gC, "enc.conv2.w");
-    e.gb2 = gc + L.off(gC, "enc.conv2.b");
-    BF_CK(launch_enc_bwd_tc(e, s));
   }
   float* extras = gc + L.gsize[gC];
   float* scal = c.F(w.scal);
@@ -610,8 +726,24 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     a.loss_scale = inv_btotal;
     a.scal = scal;
     BF_CK(launch_scalars(a, s));
-    BF_CK(launch_adam_shadow(st.critic, gc, st.m_critic, st.v_critic, L.gsize[gC], hp.lr_critic, hp.beta1, hp.beta2,
-                             hp.adam_eps, scal + S_C1_CRITIC, scal + S_C2_CRITIC, c.F(w.adam_part), &shC, s));
+    if (branch) {
+      // heads + projection on the main stream (the actor loss needs theta+ of those only), the
+      // encoder slice on the branch once its gradient is reduced
+      const int64_t e0 = L.enc_end;
+      BF_CK(launch_adam_shadow(st.critic + e0, gc + e0, st.m_critic + e0, st.v_critic + e0, L.gsize[gC] - e0,
+                               hp.lr_critic, hp.beta1, hp.beta2, hp.adam_eps, scal + S_C1_CRITIC, scal + S_C2_CRITIC,
+                               c.F(w.adam_part), &shC, s, e0, kAdamBlocks));
+      BF_CK(cudaEventRecord(c.aux->scal, s));
+      BF_CK(cudaStreamWaitEvent(es, c.aux->scal, 0));
+      BF_CK(launch_adam_shadow(st.critic, gc, st.m_critic, st.v_critic, e0, hp.lr_critic, hp.beta1, hp.beta2,
+                               hp.adam_eps, scal + S_C1_CRITIC, scal + S_C2_CRITIC, c.F(w.adam_part) + kAdamBlocks,
+                               nullptr, es, 0, kEncAdamBlocks));
+      BF_CK(cudaEventRecord(c.aux->join, es));
+    } else {
+      BF_CK(launch_adam_shadow(st.critic, gc, st.m_critic, st.v_critic, L.gsize[gC], hp.lr_critic, hp.beta1,
+                               hp.beta2, hp.adam_eps, scal + S_C1_CRITIC, scal + S_C2_CRITIC, c.F(w.adam_part), &shC,
+                               s));
+    }
   }
   // a12: actor loss against theta+ on sg(h) (Q19)
   {
@@ -624,6 +756,19 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       p.xh = c.bp(w.XHpq1), p.ldx = w.XHpq1.ld, p.rstd = c.F(w.Rpq1);
       BF_CK(gemm_launch(gb, s));
     }
+    if (c.chain) {
+      ChainBuilder cb(1);
+      for (int i = 0; i < 2; ++i) {
+        CProb& p = cb.add(B, c.mat(w.Xq1));
+        ch_fwd(cb, p, GE_LN_RELU, cq1[i].l1, Hc, nq, none_mat(), c.mat(w.q1XH1[i]), c.F(w.q1R1[i]), le);
+        ch_fwd(cb, p, GE_LN_RELU, cq1[i].l2, Hc, Hc, none_mat(), c.mat(w.q1XH2[i]), c.F(w.q1R2[i]), le);
+        CLayer& l3 = cb.layer(p, GE_BIAS_F32, cq1[i].l3.w, 0, N, Hc, none_mat(), none_mat());
+        l3.bias = cq1[i].l3.b;
+        l3.outf = c.F(w.logits1) + (size_t)i * B * N;
+        l3.ldf = N;
+      }
+      BF_CK(chain_launch(cb, s));
+    } else {
     {
       GemmBuilder gb(1);
       for (int i = 0; i < 2; ++i) {
@@ -649,6 +794,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       }
       BF_CK(gemm_launch(gb, s));
     }
+    }
     ActorQArgs q;
     memset(&q, 0, sizeof(q));
     q.B = B;
@@ -670,6 +816,17 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     const Lin cproj1 = proj(c, w.sh[0], crit, gC, "critic");
     const Mlp cq1[2] = {mlp(c, w.sh[0], crit, gC, kHeads[0]), mlp(c, w.sh[0], crit, gC, kHeads[1])};
     (void)cproj1;
+    if (c.chain_bwd) {
+      ChainBuilder cb(1);
+      for (int i = 0; i < 2; ++i) {
+        CProb& p = cb.add(B, c.half(w.dlog1, i));
+        ch_bwd(cb, p, GE_BWD_LN_RELU, cq1[i].l3.w, cq1[i].l2, Hc, N, none_mat(), c.mat(w.q1XH2[i]), c.F(w.q1R2[i]),
+               nullptr);
+        ch_bwd(cb, p, GE_BWD_LN_RELU, cq1[i].l2.w, cq1[i].l1, Hc, Hc, c.mat(w.dA1a[i]), c.mat(w.q1XH1[i]),
+               c.F(w.q1R1[i]), nullptr);
+      }
+      BF_CK(chain_launch(cb, s));
+    } else {
     {
       GemmBuilder gb(1);
       for (int i = 0; i < 2; ++i) {
@@ -688,6 +845,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       }
       BF_CK(gemm_launch(gb, s));
     }
+    }
     {
       // dL/da~ = sum_i dA1_i W1_i[:, L+P : L+P+A] -> tanh-Gaussian backward (+ the log pi path)
       GemmBuilder gb(1);
@@ -702,6 +860,15 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       p.ldo = w.dO.ld;
       BF_CK(gemm_launch(gb, s));
     }
+    if (c.chain_bwd) {
+      ChainBuilder cb(1);
+      CProb& p = cb.add(B, c.mat(w.dO));
+      ch_bwd(cb, p, GE_BWD_LN_RELU, am.l3.w, am.l2, Ha, 2 * A, c.mat(w.adA2), c.mat(w.XH2ac), c.F(w.R2ac),
+             c.F(w.part_a2));
+      ch_bwd(cb, p, GE_BWD_LN_RELU, am.l2.w, am.l1, Ha, Ha, c.mat(w.adA1), c.mat(w.XH1ac), c.F(w.R1ac),
+             c.F(w.part_a1));
+      BF_CK(chain_launch(cb, s));
+    } else {
     {
       GemmBuilder gb(1);
       GProb& p = dx(gb, c.mat(w.dO), am.l3.w, 0, Ha, GE_BWD_LN_RELU);
@@ -713,6 +880,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       GProb& p = dx(gb, c.mat(w.adA2), am.l2.w, 0, Ha, GE_BWD_LN_RELU);
       bwd_ln(p, am.l1, c.bp(w.XH1ac), w.XH1ac.ld, c.F(w.R1ac), c.bp(w.adA1), w.adA1.ld, c.F(w.part_a1));
       BF_CK(gemm_launch(gb, s));
+    }
     }
     {
       GemmBuilder gb(1);
@@ -754,9 +922,11 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
                            hp.adam_eps, scal + S_C1_ACTOR, scal + S_C2_ACTOR, nullptr, &shA, s));
   // a14: Polyak over every critic tensor except the encoder (+ target shadow)
   BF_CK(launch_polyak_shadow(st.critic_target, st.critic + L.enc_end, L.gsize[gT], hp.tau, &shT, s));
+  if (branch) BF_CK(cudaStreamWaitEvent(s, c.aux->join, 0));  // join the encoder branch
   {
     MetricsArgs m;
     memset(&m, 0, sizeof(m));
+    m.npart = branch ? kAdamBlocks + kEncAdamBlocks : kAdamBlocks;
     m.B = B;
     m.inv_btotal = inv_btotal;
     m.row_lpi = c.F(w.row_lpi);
@@ -813,7 +983,12 @@ squint_status bf16_update(const squint_dims& d, const squint_hparams& hp, const 
   Layout L = make_layout(d);
   BfLay w = plan_bf(d, L);
   if (workspace_bytes < w.total) return set_error(SQUINT_EINVAL, "workspace too small (see squint_workspace_bytes)");
-  Ctx c{d, L, reinterpret_cast<char*>(workspace), s};
+  static const bool no_chain = getenv("SQUINT_NO_CHAIN") != nullptr;
+  static const bool bwd_chain = getenv("SQUINT_BWD_CHAIN") != nullptr;
+  const bool chain_ok = !no_chain && chain_supported(d.critic_hidden) && chain_supported(d.actor_hidden);
+  static const bool no_branch = getenv("SQUINT_NO_BRANCH") != nullptr;
+  Ctx c{d, L, reinterpret_cast<char*>(workspace), s, chain_ok, chain_ok && bwd_chain,
+        (!no_branch && t_aux.ok()) ? &t_aux : nullptr};
   const int nranks = comm ? comm_nranks(comm) : 1;
   const float inv_btotal = 1.0f / ((float)d.batch * (float)nranks);
   // bf16 shadows of the current master weights
@@ -858,7 +1033,7 @@ squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const flo
   BM H2{P.take((size_t)n * ld8(Ha) * 2), M, Ha, ld8(Ha)};
   ShadowPlan sp = shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
   uint8_t* wtiles = reinterpret_cast<uint8_t*>(ws + P.take(conv_tiles_bytes(d.conv_ch)));
-  Ctx c{d, L, ws, s};
+  Ctx c{d, L, ws, s, false, false, nullptr};
   const int gC = SQUINT_GROUP_CRITIC, gA = SQUINT_GROUP_ACTOR;
   std::optional<PhaseScope> ps;
   ps.emplace(1, 0, s);
