@@ -323,13 +323,15 @@ def run_gpu(args):
 
     # per-kernel device time inside the step: a second capture of the same step with a CUDA event
     # before every libsquint launch (libsquint's launch timeline), replayed after the timed region.
-    # Events between kernels add small gaps and stop programmatic-launch overlap, so these
-    # durations are slightly pessimistic; shares are taken against their own sum.
+    # The timeline capture runs the update on one stream (no encoder-backward branch); events
+    # between kernels add small gaps and stop programmatic-launch overlap, so these durations
+    # are pessimistic; shares are taken against their own sum.
     kern = {}
     if use_graph and not args.no_timeline:
         tl = S.LaunchTimeline(4096)
         s2 = torch.cuda.Stream(device=dev)
         s2.wait_stream(torch.cuda.current_stream())
+        event_overhead_us = tl.calibrate(s2)
         gtl = torch.cuda.CUDAGraph()
         with torch.cuda.stream(s2):
             tl.start()
@@ -423,6 +425,7 @@ def run_gpu(args):
         roof["launches_per_step"] = round(e["n"], 2)
         roof["us_per_launch"] = e["us"] / e["n"]
         roof["share_of_step"] = e["us"] / tot_us if tot_us > 0 else None
+        roof["timeline_event_overhead_us"] = event_overhead_us
     kernels_us = {k: round(v["us"], 2) for k, v in sorted(kern.items(), key=lambda kv: -kv[1]["us"])}
     cpu = None
     if world == 1 and not args.no_cpu:

@@ -216,6 +216,9 @@ struct Aux {
   }
 };
 thread_local Aux t_aux;
+// instrumentation (squint_set_option): 0 disables the auxiliary branch, so a launch timeline's
+// consecutive events bracket consecutive launches of one stream
+int g_branch_enabled = 1;
 
 struct Ctx {
   const squint_dims& d;
@@ -988,7 +991,7 @@ squint_status bf16_update(const squint_dims& d, const squint_hparams& hp, const 
   const bool chain_ok = !no_chain && chain_supported(d.critic_hidden) && chain_supported(d.actor_hidden);
   static const bool no_branch = getenv("SQUINT_NO_BRANCH") != nullptr;
   Ctx c{d, L, reinterpret_cast<char*>(workspace), s, chain_ok, chain_ok && bwd_chain,
-        (!no_branch && t_aux.ok()) ? &t_aux : nullptr};
+        (!no_branch && g_branch_enabled && t_aux.ok()) ? &t_aux : nullptr};
   const int nranks = comm ? comm_nranks(comm) : 1;
   const float inv_btotal = 1.0f / ((float)d.batch * (float)nranks);
   // bf16 shadows of the current master weights
@@ -1118,4 +1121,13 @@ extern "C" squint_status squint_selftest_gemm(const void* A, int a_rows, int a_c
 
 extern "C" SQUINT_API int squint_debug_gemm_times(unsigned long long* host, int max_entries) {
   return sq::gemm_debug_times(host, max_entries);
+}
+
+// Instrumentation options (host): key 1 = auxiliary branch of the bf16 update (1 on, 0 off).
+extern "C" SQUINT_API squint_status squint_set_option(int key, int value) {
+  if (key == 1) {
+    sq::g_branch_enabled = value != 0;
+    return SQUINT_OK;
+  }
+  return sq::set_error(SQUINT_EINVAL, "unknown option");
 }

@@ -81,6 +81,7 @@ def _load():
         "squint_phase_name": (C.c_char_p, [i32]),
         "squint_set_launch_events": (i32, [C.POINTER(vp), i32]),
         "squint_record_launch_event": (st, [vp]),
+        "squint_set_option": (st, [i32, i32]),
         "squint_launch_info": (st, [i32, C.POINTER(C.c_char_p), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
@@ -95,7 +96,8 @@ EXPORTED = ["squint_last_error", "squint_version", "squint_param_layout", "squin
             "squint_workspace_region", "squint_act_workspace_bytes", "squint_comm_unique_id", "squint_comm_init",
             "squint_comm_destroy", "squint_insert", "squint_act", "squint_update", "squint_soft_update",
             "squint_launch_count", "squint_set_phase_events", "squint_phase_name", "squint_selftest_gemm",
-            "squint_set_launch_events", "squint_record_launch_event", "squint_launch_info"]
+            "squint_set_launch_events", "squint_record_launch_event", "squint_launch_info",
+            "squint_set_option"]
 N_PHASES = 16
 
 
@@ -156,20 +158,42 @@ class LaunchTimeline:
         self.used = 0
 
     def start(self):
+        LIB.squint_set_option(1, 0)  # single-stream update while the timeline is captured
         LIB.squint_set_launch_events(self._arr, self.n)
 
     def stop(self, stream=None):
         LIB.squint_record_launch_event(_stream(stream))
         self.used = LIB.squint_set_launch_events(None, 0)
+        LIB.squint_set_option(1, 1)
         return self.used
 
+    def calibrate(self, stream, n=64, reps=10):
+        """Device time of an interval between two consecutive timeline events with no kernel
+        (graph-captured like the real timeline): subtracted from every launch interval."""
+        g = torch.cuda.CUDAGraph()
+        LIB.squint_set_launch_events(self._arr, n)
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(n):
+                LIB.squint_record_launch_event(_stream(stream))
+        LIB.squint_set_launch_events(None, 0)
+        tot = 0.0
+        for _ in range(reps):
+            g.replay()
+            torch.cuda.synchronize()
+            tot += self.events[0].elapsed_time(self.events[n - 1]) * 1e3 / (n - 1)
+        self.overhead_us = tot / reps
+        return self.overhead_us
+
     def durations(self):
-        """[(name, flops, bytes, us)] for each recorded launch (after the events completed)."""
+        """[(name, flops, bytes, us)] for each recorded launch (after the events completed); the
+        calibrated per-event overhead (calibrate()) is subtracted."""
         out = []
+        oh = getattr(self, "overhead_us", 0.0)
         for i in range(self.used - 1):
             nm, fl, by = C.c_char_p(), C.c_double(), C.c_double()
             _check(LIB.squint_launch_info(i, C.byref(nm), C.byref(fl), C.byref(by)))
-            out.append((nm.value.decode(), fl.value, by.value, self.events[i].elapsed_time(self.events[i + 1]) * 1e3))
+            us = self.events[i].elapsed_time(self.events[i + 1]) * 1e3
+            out.append((nm.value.decode(), fl.value, by.value, max(us - oh, 0.0)))
         return out
 
 
