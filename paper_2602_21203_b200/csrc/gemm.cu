@@ -32,6 +32,7 @@ namespace {
 using namespace gd;
 constexpr int kThreads = 256;
 constexpr int kMaxStages = 8;
+constexpr int kDbgSlots = 16;  // globaltimer stamps per CTA (SQUINT_GEMM_DBG)
 constexpr int kABytes = 16384;  // 128 x 64 bf16
 constexpr float kLog2Pi = 1.8378770664093453f;
 constexpr float kSquashEps = 1e-6f;
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     if (b.dbg && tid == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      b.dbg[blockIdx.x * 8 + k] = t;
+      b.dbg[blockIdx.x * kDbgSlots + k] = t;
     }
   };
   stamp(0);
@@ -277,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
         }
       }
     }
+    stamp(5);
     if constexpr (EPI == GE_DW) {
       if (n0 == 0 && hh == 0 && rv) {
         float db = 0.f, dg = 0.f, dbe = 0.f;
@@ -382,12 +384,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
         tc::tma_load_2d(pslots + g * kSlotBytes, &b.maps[P.xmap], n0 + g * 64, row0, &ld_bar[q]);
     }
     tc::mbar_wait(&ld_bar[q], 0);
+    stamp(5);
     float s1 = 0.f, s2 = 0.f;
     for (int g = 0; g < ngrp; ++g) {
       const int ch = 2 * g + hh;
       if (ch < nch) {
         const int c0 = ch * 32, ncv = min(32, nreal - c0);
         tc::tmem_ld32(trow + ch * 32, v);
+        if (g == 0) stamp(8);
         box_get(pslots + g * kSlotBytes, hh, a);
         float pg[32], pb[32];
 #pragma unroll
@@ -403,14 +407,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
           pg[j] = dn * x;
           pb[j] = dn;
         }
+        if (g == 0) stamp(9);
         const float cg = colsum32(pg);
         const float cb = colsum32(pb);
+        if (g == 0) stamp(10);
         colacc[(q * 3 + 1) * 512 + c0 + lane] = cg;
         colacc[(q * 3 + 2) * 512 + c0 + lane] = cb;
       }
     }
     float m1, m2;
+    stamp(11);
     row_total2(s1, s2, m1, m2);
+    stamp(6);
     m1 /= (float)N;
     m2 /= (float)N;
     const float rs = rv ? P.rstd[r] : 0.f;
@@ -431,11 +439,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
           v[j] = ok ? rs * (dn * s_g[cc] - m1 - x * m2) : 0.f;
           a[j] = v[j];
         }
+        if (g == 0) stamp(12);
         box_put(sl, hh, v);
         const float cx = colsum32(a);
         colacc[(q * 3 + 0) * 512 + c0 + lane] = cx;
+        if (g == 0) stamp(13);
       }
       pair_store(sl, &b.maps[P.omap], n0 + g * 64, row0, q, hh);
+      if (g == 0) stamp(14);
     }
     __syncthreads();
     if (P.part) {
@@ -517,7 +528,441 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   if (warp == 0) tc::tmem_dealloc(tmem, ncols);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Split-K variant for narrow row-complete layers (N <= 64 with long K: the projection LayerNorm,
+// its backward, the tanh-Gaussian head and its backward).  With one 128-row tile per CTA those
+// launches ran on 4-16 SMs, serial over up to 13 K blocks, with a 32-element-per-thread
+// epilogue.  Here a cluster of ks CTAs shares one tile: CTA kr accumulates K blocks
+// [kr T / ks, (kr + 1) T / ks) in its own TMEM, every warp quarter pushes its 32 accumulator rows
+// (fp32, 8 KB) by bulk copy into the shared memory of the CTA that owns those rows (rank
+// q ks / 4; completion counted in bytes on the owner's mbarrier), and each CTA sums the ks
+// partial tiles of its 128 / ks rows in rank order (deterministic) and runs the epilogue with
+// 8 threads per row (8 columns each; row statistics by shuffles).  Column partials of the
+// LayerNorm backward are written per 128 / ks-row block: part[(mtile ks + kr)][3][N].
+constexpr int kSkRecvBytes = 32768;  // 128 rows x 64 fp32 columns, in ks slots of 128 / ks rows
+
+__device__ __forceinline__ uint32_t sk_off(int row, int chunk) {  // 64-float rows, 16-byte chunks
+  return (uint32_t)(row * 256 + ((chunk ^ (row & 7)) << 4));
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1) k_gemm_sk(const __grid_constant__ GBatch b) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], done_bar, recv_bar;
+  __shared__ uint32_t tmem_slot;
+  __shared__ __align__(16) float s_bias[64], s_g[64], s_beta[64];
+  __shared__ float s_col[8][3][64];
+
+  const int ks = b.ks;
+  const uint32_t kr = tc::cluster_rank();
+  const int tile = blockIdx.x / ks;
+  int pi = 0;
+  while (pi + 1 < b.nprob && tile >= b.p[pi + 1].tile0) ++pi;
+  const GProb& P = b.p[pi];
+  const int mt = tile - P.tile0;
+  const int m0 = mt * 128;
+  const int nreal = P.N;
+  const int nt = round16(nreal);
+  const int R = 128 / ks;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int S = b.nstages;
+  uint8_t* recv = smem + (b.nstages * b.stage_bytes > kSkRecvBytes ? b.nstages * b.stage_bytes : kSkRecvBytes);
+  auto stamp = [&](int k) {
+    if (b.dbg && tid == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      b.dbg[blockIdx.x * kDbgSlots + k] = t;
+    }
+  };
+  stamp(0);
+  int T = 0;
+  for (int s = 0; s < P.nseg; ++s) T += P.seg[s].nkb;
+  const int kb0 = (int)kr * T / ks, kb1 = ((int)kr + 1) * T / ks;
+
+  if (warp == 0) tc::tmem_alloc(&tmem_slot, 64);
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < S; ++i) {
+      tc::mbar_init(&full_bar[i], 1);
+      tc::mbar_init(&empty_bar[i], 1);
+    }
+    tc::mbar_init(&done_bar, 1);
+    tc::mbar_init(&recv_bar, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 2 && lane < P.nseg) {
+    tc::tma_prefetch_desc(&b.maps[P.seg[lane].amap]);
+    tc::tma_prefetch_desc(&b.maps[P.seg[lane].bmap]);
+  }
+  tc::fence_before_sync();
+  tc::cluster_sync();  // every CTA's recv_bar is initialised before any peer copies into it
+  tc::fence_after_sync();
+  const uint32_t tmem = tmem_slot;
+  stamp(1);
+  // walk this CTA's K blocks: (segment, block within the segment) for global block kb
+  auto seg_of = [&](int kb, int& l) {
+    int s = 0;
+    while (kb >= P.seg[s].nkb) kb -= P.seg[s++].nkb;
+    l = kb;
+    return s;
+  };
+  int npre = 0;
+  if (b.prefetch_b && warp == 0 && lane == 0) {
+    for (int kb = kb0; kb < kb1 && kb - kb0 < S; ++kb) {
+      int l;
+      const GSeg& G = P.seg[seg_of(kb, l)];
+      const TileGeo geo = tile_geo(P, nreal, G.b_mn);
+      uint8_t* Bs = smem + (kb - kb0) * b.stage_bytes + kABytes;
+      tc::mbar_expect_tx(&full_bar[kb - kb0], kABytes + geo.bbytes);
+      for (int i = 0; i < geo.nbox_b; ++i) {
+        if (!G.b_mn)
+          tc::tma_load_2d(Bs + i * geo.bnb * 128, &b.maps[G.bmap], G.b_k + 64 * l, P.b_n + geo.bnb * i, &full_bar[kb - kb0]);
+        else
+          tc::tma_load_2d(Bs + i * 8192, &b.maps[G.bmap], P.b_n + 64 * i, G.b_k + 64 * l, &full_bar[kb - kb0]);
+      }
+      ++npre;
+    }
+  }
+  tc::pdl_wait();
+  tc::pdl_trigger();
+  stamp(2);
+  // per-row epilogue inputs, loaded while the main loop runs: thread (row tid / 8 + 32 it,
+  // column group tid % 8); R / 32 <= 2 rows per thread
+  const int cg = tid & 7, c0 = cg * 8;
+  const int nit = R / 32;
+  uint4 xpre[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+  float rspre[2] = {0.f, 0.f};
+  float tg_pre[2][2][3];  // tanh-Gaussian: [it][d = cg, cg + 8][mu | l | eps]
+  for (int it = 0; it < nit; ++it) {
+    const int r = m0 + (int)kr * R + (tid >> 3) + 32 * it;
+    if (r >= P.M) continue;
+    if constexpr (EPI == GE_BWD_LN_TANH || EPI == GE_BWD_LN_RELU) {
+      if (c0 < nreal) xpre[it] = *reinterpret_cast<const uint4*>(P.xh + (int64_t)r * P.ldx + c0);
+      rspre[it] = P.rstd[r];
+    } else if constexpr (EPI == GE_TG_FWD || EPI == GE_TG_BWD) {
+      const int A = EPI == GE_TG_FWD ? P.N / 2 : P.N - P.acc_col0;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int d = cg + 8 * u;
+        tg_pre[it][u][0] = tg_pre[it][u][1] = tg_pre[it][u][2] = 0.f;
+        if (d < A) {
+          if (EPI == GE_TG_BWD) {
+            tg_pre[it][u][0] = P.tgo[(int64_t)r * 2 * A + d];
+            tg_pre[it][u][1] = P.tgo[(int64_t)r * 2 * A + A + d];
+          }
+          if (P.eps) tg_pre[it][u][2] = P.eps[(int64_t)r * A + d];
+        }
+      }
+    }
+  }
+  float dlp = 0.f;
+  if constexpr (EPI == GE_TG_BWD) dlp = P.dlogp_scale[0];
+  if (warp >= 2) {
+    for (int c = tid - 64; c < nt; c += kThreads - 64) {
+      const bool ok = c < P.N;
+      s_bias[c] = (ok && P.bias) ? P.bias[c] : 0.f;
+      s_g[c] = (ok && P.g) ? P.g[c] : 0.f;
+      s_beta[c] = (ok && P.beta) ? P.beta[c] : 0.f;
+    }
+  }
+  if (warp == 0 && lane == 0) {
+    tc::mbar_expect_tx(&recv_bar, kSkRecvBytes);
+    for (int kb = kb0; kb < kb1; ++kb) {
+      const int i = kb - kb0, st = i % S;
+      int l;
+      const GSeg& G = P.seg[seg_of(kb, l)];
+      const TileGeo geo = tile_geo(P, nreal, G.b_mn);
+      if (i >= S) tc::mbar_wait(&empty_bar[st], ((i / S) - 1) & 1);
+      uint8_t* As = smem + st * b.stage_bytes;
+      uint8_t* Bs = As + kABytes;
+      const bool pre = i < npre;
+      if (!pre) tc::mbar_expect_tx(&full_bar[st], kABytes + geo.bbytes);
+      const int kc = 64 * l;
+      if (!G.a_mn) {
+        tc::tma_load_2d(As, &b.maps[G.amap], G.a_k + kc, P.a_m + m0, &full_bar[st]);
+      } else {
+        tc::tma_load_2d(As, &b.maps[G.amap], P.a_m + m0, G.a_k + kc, &full_bar[st]);
+        tc::tma_load_2d(As + 8192, &b.maps[G.amap], P.a_m + m0 + 64, G.a_k + kc, &full_bar[st]);
+      }
+      for (int j = 0; j < geo.nbox_b && !pre; ++j) {
+        if (!G.b_mn)
+          tc::tma_load_2d(Bs + j * geo.bnb * 128, &b.maps[G.bmap], G.b_k + kc, P.b_n + geo.bnb * j, &full_bar[st]);
+        else
+          tc::tma_load_2d(Bs + j * 8192, &b.maps[G.bmap], P.b_n + 64 * j, G.b_k + kc, &full_bar[st]);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    for (int kb = kb0; kb < kb1; ++kb) {
+      const int i = kb - kb0, st = i % S;
+      int l;
+      const GSeg& G = P.seg[seg_of(kb, l)];
+      const uint32_t id = tc::idesc_bf16_major(128, nt, G.a_mn, G.b_mn);
+      tc::mbar_wait(&full_bar[st], (i / S) & 1);
+      tc::fence_after_sync();
+      const uint32_t a0 = tc::smem_u32(smem + st * b.stage_bytes), b0 = a0 + kABytes;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t ad = G.a_mn ? tc::sdesc_sw128(a0 + 2048 * k, 8192, 1024) : tc::sdesc_sw128(a0 + 32 * k, 16, 1024);
+        const uint64_t bd = G.b_mn ? tc::sdesc_sw128(b0 + 2048 * k, 8192, 1024) : tc::sdesc_sw128(b0 + 32 * k, 16, 1024);
+        tc::mma_bf16(tmem, ad, bd, id, (i | k) != 0);
+      }
+      tc::mma_commit(&empty_bar[st]);
+    }
+    tc::mma_commit(&done_bar);
+  }
+  __syncwarp();
+  tc::mbar_wait(&done_bar, 0);
+  tc::fence_after_sync();
+  stamp(3);
+
+  // ---- push the partial tile: warp quarter q's rows go to the CTA owning them ----
+  {
+    const int q = warp & 3, hh = warp >> 2;
+    uint8_t* stg = smem + q * 8192;  // operand ring is free once the MMAs completed
+    if (hh * 32 < nt) {
+      float v[32];
+      tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + hh * 32, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        *reinterpret_cast<float4*>(stg + sk_off(lane, hh * 8 + j)) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+    tc::fence_async_smem();
+    tc::named_bar(1 + q, 64);
+    if (hh == 0 && lane == 0) {
+      const uint32_t owner = (uint32_t)(q * ks / 4);
+      const int rowoff = q * 32 - (int)owner * R;
+      tc::bulk_s2cluster(tc::mapa(recv + ((int)kr * R + rowoff) * 256, owner), stg, 8192, tc::mapa(&recv_bar, owner));
+    }
+  }
+  __syncthreads();  // s_bias / s_g / s_beta visible
+  tc::mbar_wait(&recv_bar, 0);
+  stamp(5);
+
+  // every copy into this CTA has landed; arriving now (waiting only at exit) tells the peers
+  // their outgoing copies are complete without a barrier on the critical path
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  // ---- epilogue over this CTA's rows [kr R, kr R + R) of the tile ----
+  const int N = P.N;
+  auto recv_sum8 = [&](int rr, float (&acc)[8]) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    for (int k = 0; k < ks; ++k) {
+      const uint8_t* base = recv + (k * R) * 256;
+      const float4 lo = *reinterpret_cast<const float4*>(base + sk_off(rr, 2 * cg));
+      const float4 hi = *reinterpret_cast<const float4*>(base + sk_off(rr, 2 * cg + 1));
+      acc[0] += lo.x, acc[1] += lo.y, acc[2] += lo.z, acc[3] += lo.w;
+      acc[4] += hi.x, acc[5] += hi.y, acc[6] += hi.z, acc[7] += hi.w;
+    }
+  };
+  auto recv_col = [&](int rr, int c) {
+    float v = 0.f;
+    for (int k = 0; k < ks; ++k)
+      v += *reinterpret_cast<const float*>(recv + (k * R) * 256 + sk_off(rr, c >> 2) + (c & 3) * 4);
+    return v;
+  };
+  if constexpr (EPI == GE_LN_TANH || EPI == GE_LN_RELU || EPI == GE_BWD_LN_TANH || EPI == GE_BWD_LN_RELU) {
+    float cp[3][8];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) cp[k][j] = 0.f;
+    for (int it = 0; it < nit; ++it) {
+      const int rr = (tid >> 3) + 32 * it;
+      float acc[8];
+      recv_sum8(rr, acc);
+      if (it == 0) stamp(8);
+      const int r = m0 + (int)kr * R + rr;
+      const bool rv = r < P.M;
+      if constexpr (EPI == GE_LN_TANH || EPI == GE_LN_RELU) {
+        float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          acc[j] += s_bias[c0 + j];
+          if (c0 + j < nreal) s1 += acc[j], s2 += acc[j] * acc[j];
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        }
+        const float mean = s1 / (float)N;
+        const float rs = rsqrtf(fmaxf(s2 / (float)N - mean * mean, 0.f) + P.ln_eps);
+        float y[8], xh[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          xh[j] = (acc[j] - mean) * rs;
+          const float n = fmaf(xh[j], s_g[c0 + j], s_beta[c0 + j]);
+          y[j] = (EPI == GE_LN_RELU) ? fmaxf(n, 0.f) : tanh_fast(n);
+        }
+        if (rv && c0 < nreal) {
+          const int ncv = min(8, nreal - c0);
+          bf16* o = P.out + (int64_t)r * P.ldo + c0;
+          if (ncv == 8 && al16(o)) *reinterpret_cast<uint4*>(o) = tc::pack_bf16x8(y);
+          else
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (j < ncv) o[j] = __float2bfloat16_rn(y[j]);
+          if (P.xh) {
+            bf16* x = P.xh + (int64_t)r * P.ldx + c0;
+            if (ncv == 8 && al16(x)) *reinterpret_cast<uint4*>(x) = tc::pack_bf16x8(xh);
+            else
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (j < ncv) x[j] = __float2bfloat16_rn(xh[j]);
+          }
+          if (cg == 0 && P.rstd) P.rstd[r] = rs;
+        }
+      } else {
+        float x[8];
+        {
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&xpre[it]);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float2 f = __bfloat1622float2(h[k]);
+            x[2 * k] = f.x, x[2 * k + 1] = f.y;
+          }
+        }
+        float dn[8], s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const bool ok = rv && c0 + j < nreal;
+          x[j] = ok ? x[j] : 0.f;
+          const float n = fmaf(x[j], s_g[c0 + j], s_beta[c0 + j]);
+          dn[j] = ok ? ((EPI == GE_BWD_LN_RELU) ? (n > 0.f ? acc[j] : 0.f) : acc[j] * sech2_fast(n)) : 0.f;
+          const float dxh = dn[j] * s_g[c0 + j];
+          s1 += dxh;
+          s2 += dxh * x[j];
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        }
+        if (it == 0) stamp(9);
+        const float m1 = s1 / (float)N, m2 = s2 / (float)N;
+        const float rs = rspre[it];
+        float dx[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const bool ok = rv && c0 + j < nreal;
+          dx[j] = ok ? rs * (dn[j] * s_g[c0 + j] - m1 - x[j] * m2) : 0.f;
+          cp[0][j] += dx[j];
+          cp[1][j] += dn[j] * x[j];
+          cp[2][j] += dn[j];
+        }
+        if (rv && c0 < nreal) {
+          const int ncv = min(8, nreal - c0);
+          bf16* o = P.out + (int64_t)r * P.ldo + c0;
+          if (ncv == 8 && al16(o)) *reinterpret_cast<uint4*>(o) = tc::pack_bf16x8(dx);
+          else
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (j < ncv) o[j] = __float2bfloat16_rn(dx[j]);
+        }
+      }
+    }
+    stamp(10);
+    if constexpr (EPI == GE_BWD_LN_TANH || EPI == GE_BWD_LN_RELU) {
+      if (P.part) {
+        // column sums over the CTA's rows: lanes 8 apart share a column group; then the 8 warps
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            cp[k][j] += __shfl_xor_sync(0xffffffffu, cp[k][j], 8);
+            cp[k][j] += __shfl_xor_sync(0xffffffffu, cp[k][j], 16);
+          }
+        if (lane < 8)
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) s_col[warp][k][c0 + j] = cp[k][j];
+        stamp(11);
+        __syncthreads();
+        stamp(12);
+        for (int e = tid; e < 3 * nreal; e += kThreads) {
+          const int k = e / nreal, c = e - k * nreal;
+          float s = 0.f;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) s += s_col[w][k][c];
+          P.part[((int64_t)(mt * ks + (int)kr) * 3 + k) * N + c] = s;
+        }
+      }
+    }
+  } else if constexpr (EPI == GE_TG_FWD || EPI == GE_TG_BWD) {
+    // 8 threads per row, action dimension d = tid % 8 (+ 8)
+    for (int it = 0; it < nit; ++it) {
+      const int rr = (tid >> 3) + 32 * it;
+      const int r = m0 + (int)kr * R + rr;
+      const bool rv = r < P.M;
+      if constexpr (EPI == GE_TG_FWD) {
+        const int A = N / 2;
+        float lp = 0.f;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int d = cg + 8 * u;
+          if (rv && d < A) {
+            const float mu = recv_col(rr, d) + s_bias[d], l = recv_col(rr, A + d) + s_bias[A + d];
+            if (P.tgo) {
+              P.tgo[(int64_t)r * 2 * A + d] = mu;
+              P.tgo[(int64_t)r * 2 * A + A + d] = l;
+            }
+            const float tl = tanhf(l);
+            const float log_std = P.lo + 0.5f * (P.hi - P.lo) * (tl + 1.f);
+            const float sd = expf(log_std);
+            const float e = tg_pre[it][u][2];
+            const float uu = fmaf(sd, e, mu);
+            const float at = tanhf(uu);
+            if (P.act) P.act[(int64_t)r * A + d] = at;
+            if (P.act_bf) P.act_bf[(int64_t)r * P.ld_act_bf + d] = __float2bfloat16_rn(at);
+            lp += -0.5f * e * e - log_std - 0.5f * kLog2Pi - logf(sech2f(uu) + kSquashEps);
+          }
+        }
+        // butterfly over the 8-lane group (deterministic order)
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) lp += __shfl_xor_sync(0xffffffffu, lp, o);
+        if (rv && cg == 0 && P.logp) P.logp[r] = lp;
+      } else {
+        const int A = N - P.acc_col0;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int d = cg + 8 * u;
+          if (rv && d < A) {
+            const float mu = tg_pre[it][u][0], l = tg_pre[it][u][1], e = tg_pre[it][u][2];
+            const float tl = tanhf(l);
+            const float log_std = P.lo + 0.5f * (P.hi - P.lo) * (tl + 1.f);
+            const float sd = expf(log_std);
+            const float uu = fmaf(sd, e, mu);
+            const float a1 = tanhf(uu);
+            const float om = sech2f(uu);
+            const float du = recv_col(rr, P.acc_col0 + d) * om + dlp * (2.f * a1 * om / (om + kSquashEps));
+            const float dls = du * sd * e - dlp;
+            P.out[(int64_t)r * P.ldo + d] = __float2bfloat16_rn(du);
+            P.out[(int64_t)r * P.ldo + A + d] = __float2bfloat16_rn(dls * 0.5f * (P.hi - P.lo) * sech2f(l));
+          }
+        }
+      }
+    }
+  }
+  stamp(7);
+  tc::fence_before_sync();
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // peers' copies from this CTA done
+  stamp(4);
+  if (warp == 0) tc::tmem_dealloc(tmem, 64);
+}
+
 typedef void (*GemmKernel)(GBatch);
+GemmKernel kernel_sk_for(int epi) {
+  switch (epi) {
+    case GE_LN_RELU: return k_gemm_sk<GE_LN_RELU>;
+    case GE_LN_TANH: return k_gemm_sk<GE_LN_TANH>;
+    case GE_TG_FWD: return k_gemm_sk<GE_TG_FWD>;
+    case GE_BWD_LN_RELU: return k_gemm_sk<GE_BWD_LN_RELU>;
+    case GE_BWD_LN_TANH: return k_gemm_sk<GE_BWD_LN_TANH>;
+    case GE_TG_BWD: return k_gemm_sk<GE_TG_BWD>;
+  }
+  return nullptr;
+}
 GemmKernel kernel_for(int epi) {
   switch (epi) {
     case GE_LN_RELU: return k_gemm<GE_LN_RELU>;
@@ -554,7 +999,7 @@ static int g_dbg_tiles = 0;
 int gemm_debug_times(unsigned long long* host, int max_entries) {
   if (!g_dbg_dev) return 0;
   cudaDeviceSynchronize();
-  const int n = g_dbg_tiles * 8 < max_entries ? g_dbg_tiles * 8 : max_entries;
+  const int n = g_dbg_tiles * kDbgSlots < max_entries ? g_dbg_tiles * kDbgSlots : max_entries;
   cudaMemcpy(host, g_dbg_dev, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   return n;
 }
@@ -600,7 +1045,21 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   const int epi0 = b.p[0].epi;
   const bool ln_launch = epi0 == GE_LN_RELU || epi0 == GE_LN_TANH || epi0 == GE_BWD_LN_RELU || epi0 == GE_BWD_LN_TANH;
   b.cs = 1;
-  if (ln_launch) {
+  // split-K clusters for narrow row-complete layers with several K blocks (k_gemm_sk)
+  b.ks = 1;
+  {
+    static const bool no_sk = getenv("SQUINT_NO_SPLITK") != nullptr;
+    bool ok = !no_sk && kernel_sk_for(epi0) != nullptr;
+    int minkb = 1 << 30;
+    for (int i = 0; i < b.nprob && ok; ++i) {
+      int k = 0;
+      for (int j = 0; j < b.p[i].nseg; ++j) k += b.p[i].seg[j].nkb;
+      minkb = k < minkb ? k : minkb;
+      ok = ((b.p[i].N + 15) & ~15) <= 64;
+    }
+    if (ok) b.ks = minkb >= 4 ? 4 : (minkb >= 2 ? 2 : 1);
+  }
+  if (ln_launch && b.ks == 1) {
     int cs = 8;
     for (int i = 0; i < b.nprob; ++i) {
       const int n = b.p[i].N;
@@ -622,6 +1081,7 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     if (row_complete(p.epi)) {
       if (n16 > 512) return -1;
       p.bn = b.cs > 1 ? p.N / b.cs : n16;
+      if (b.ks > 1 && n16 > 64) return -1;
     } else if (p.epi == GE_DW) {
       p.bn = n16 >= 256 ? 64 : (n16 > 128 ? 128 : n16);
     } else {
@@ -645,6 +1105,7 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     for (int j = 0; j < b.p[i].nseg; ++j) k += b.p[i].seg[j].nkb;
     maxkb = k > maxkb ? k : maxkb;
   }
+  if (b.ks > 1) maxkb = (maxkb + b.ks - 1) / b.ks;  // K blocks per cluster CTA
   S = S > maxkb ? maxkb : S;
   S = S < 2 ? 2 : S;
   if ((size_t)S * b.stage_bytes > 200 * 1024) return -1;
@@ -669,6 +1130,7 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     p.omap = p.xmap = p.ymap = -1;
     const bool ln = p.epi == GE_LN_RELU || p.epi == GE_LN_TANH;
     const bool bwd = p.epi == GE_BWD_LN_RELU || p.epi == GE_BWD_LN_TANH;
+    if (b.ks > 1) continue;  // the split-K epilogue stores directly
     if (ln || bwd || p.epi == GE_RELU_MASK) {
       if (b.nmaps + 3 > kGemmMaxMaps || !p.out) return -1;
       if (tmap_get(Mat{p.out, p.M, p.N, p.ldo}, 32, &b.maps[b.nmaps])) return -1;
@@ -684,18 +1146,24 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     }
   }
   size_t smem = (size_t)S * b.stage_bytes;
-  if (smem < (size_t)kEpiBytes) smem = kEpiBytes;
+  if (b.ks > 1) {
+    if (smem < (size_t)kSkRecvBytes) smem = kSkRecvBytes;
+    smem += kSkRecvBytes;
+  } else if (smem < (size_t)kEpiBytes) {
+    smem = kEpiBytes;
+  }
   smem += 1024;
   const int epi = b.p[0].epi;
   for (int i = 1; i < b.nprob; ++i)
     if (b.p[i].epi != epi) return -1;  // one epilogue kind per launch (template instance)
-  GemmKernel kern = kernel_for(epi);
+  GemmKernel kern = b.ks > 1 ? kernel_sk_for(epi) : kernel_for(epi);
   if (!kern) return -1;
-  static size_t attr_smem[16] = {0};  // opt-in limit set so far per instance
-  if (smem > attr_smem[epi]) {
+  static size_t attr_smem[32] = {0};  // opt-in limit set so far per instance
+  const int ai = epi + (b.ks > 1 ? 16 : 0);
+  if (smem > attr_smem[ai]) {
     cudaError_t ae = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ae != cudaSuccess) return (int)ae;
-    attr_smem[epi] = smem;
+    attr_smem[ai] = smem;
   }
   b.dbg = nullptr;
   {
@@ -707,21 +1175,21 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
       const int me = launch_no++;
       const bool all = dbg_env[0] == 'a';
       if (!g_dbg_dev) {
-        cudaMalloc(&g_dbg_dev, 256 * 64 * 8 * sizeof(unsigned long long));
-        cudaMemset(g_dbg_dev, 0, 256 * 64 * 8 * sizeof(unsigned long long));
+        cudaMalloc(&g_dbg_dev, 256 * 64 * kDbgSlots * sizeof(unsigned long long));
+        cudaMemset(g_dbg_dev, 0, 256 * 64 * kDbgSlots * sizeof(unsigned long long));
       }
       if (all) {
-        b.dbg = g_dbg_dev + (size_t)(me % 256) * 64 * 8;
+        b.dbg = g_dbg_dev + (size_t)(me % 256) * 64 * kDbgSlots;
         g_dbg_tiles = 256 * 64;
       } else if (me == atoi(dbg_env)) {
-        g_dbg_tiles = b.ntiles < 4096 ? b.ntiles : 4096;
+        g_dbg_tiles = b.ntiles * b.ks < 4096 ? b.ntiles * b.ks : 4096;
         b.dbg = g_dbg_dev;
       }
     }
   }
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3(b.ntiles);
+  cfg.gridDim = dim3(b.ntiles * b.ks);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -733,9 +1201,9 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
-  if (b.cs > 1) {
+  if (b.cs > 1 || b.ks > 1) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = b.cs;
+    attr[na].val.clusterDim.x = b.cs > 1 ? b.cs : b.ks;
     attr[na].val.clusterDim.y = 1;
     attr[na].val.clusterDim.z = 1;
     ++na;
@@ -746,16 +1214,18 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     static const char* names[9] = {"k_gemm<ln_relu>", "k_gemm<ln_tanh>", "k_gemm<bias>", "k_gemm<tg_fwd>",
                                    "k_gemm<bwd_ln_relu>", "k_gemm<bwd_ln_tanh>", "k_gemm<relu_mask>",
                                    "k_gemm<tg_bwd>", "k_gemm<dw>"};
+    static const char* sk_names[9] = {"k_gemm_sk<ln_relu>", "k_gemm_sk<ln_tanh>", "", "k_gemm_sk<tg_fwd>",
+                                      "k_gemm_sk<bwd_ln_relu>", "k_gemm_sk<bwd_ln_tanh>", "", "k_gemm_sk<tg_bwd>", ""};
     double flops = 0;
     for (int i = 0; i < b.nprob; ++i)
       for (int k = 0; k < b.p[i].nseg; ++k) flops += 2.0 * b.p[i].M * (double)(b.p[i].N - b.p[i].acc_col0) * b.p[i].seg[k].k;
-    note_launch(s, names[epi], flops, 0);
+    note_launch(s, b.ks > 1 ? sk_names[epi] : names[epi], flops, 0);
   }
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, b);
   static const bool dbg = getenv("SQUINT_DEBUG_SYNC") != nullptr;
   if (dbg) {
     cudaError_t se = cudaStreamSynchronize(s);
-    fprintf(stderr, "[squint] k_gemm nprob=%d tiles=%d stages=%d stage_bytes=%d -> %s\n", b.nprob, b.ntiles, S,
+    fprintf(stderr, "[squint] k_gemm nprob=%d tiles=%d ks=%d stages=%d stage_bytes=%d -> %s\n", b.nprob, b.ntiles, b.ks, S,
             b.stage_bytes, cudaGetErrorString(se));
     for (int i = 0; i < b.nprob; ++i) {
       const GProb& p = b.p[i];

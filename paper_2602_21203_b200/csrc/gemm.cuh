@@ -97,6 +97,8 @@ struct GBatch {
   int nprob, ntiles, nmaps;
   int stage_bytes, nstages;
   int cs;  // cluster size: LayerNorm rows split over cs CTAs (statistics exchanged through DSMEM)
+  int ks;  // split-K cluster size (k_gemm_sk; set by gemm_launch): bwd-LN column partials are
+           // then written per 128 / ks rows, [mtiles * ks][3][N]
   int prefetch_b;  // 1: B operands may be loaded before griddepcontrol.wait (not written by the
                    // immediately preceding kernel); set through GemmBuilder::prefetch_b
   unsigned long long* dbg;  // optional per-CTA phase timestamps (globaltimer ns) [tile][8]
@@ -112,6 +114,8 @@ struct GemmBuilder {
     b.nmaps = 0;
     b.ntiles = 0;
     b.prefetch_b = prefetch_b;
+    b.ks = 1;
+    b.cs = 1;
   }
   GProb& add(int M, int N, int epi);
   // K segment: A(m, k) from `A` (K-major if !a_mn) and B(n, k) from `Bm`.

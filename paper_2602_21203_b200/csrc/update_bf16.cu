@@ -180,10 +180,10 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
     w.part_q2[i] = fl(mt * 3 * Hc);
     w.part_q1[i] = fl(mt * 3 * Hc);
   }
-  w.part_pq = fl(mt * 3 * Lt);
+  w.part_pq = fl(4 * mt * 3 * Lt);
   w.part_a2 = fl(mt * 3 * Ha);
   w.part_a1 = fl(mt * 3 * Ha);
-  w.part_pp = fl(mt * 3 * Lt);
+  w.part_pp = fl(4 * mt * 3 * Lt);
   w.grad_critic = fl(L.gsize[SQUINT_GROUP_CRITIC] + kExtra);
   w.grad_actor = fl(L.gsize[SQUINT_GROUP_ACTOR] + kExtra);
   w.adam_part = fl(kAdamBlocks + kEncAdamBlocks);
@@ -596,6 +596,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
   }
   // a10: critic backward: heads -> critic projection -> ReLU'(conv2)
   float* gc = c.F(w.grad_critic);
+  int ks_pq = 1, ks_pp = 1;
   {
     PhaseScope ps(8, rep, s);
     if (c.chain_bwd) {
@@ -635,6 +636,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       gb.seg(p, c.mat(w.dA1c[1]), 0, 0, cq[1].l1.w, 1, 0, Hc);
       bwd_ln(p, cproj, c.bp(w.XHpq), w.XHpq.ld, c.F(w.Rpq), c.bp(w.dAp), w.dAp.ld, c.F(w.part_pq));
       BF_CK(gemm_launch(gb, s));
+      ks_pq = gb.b.ks;  // split-K launch: column partials per 128 / ks rows
     }
     {
       // dh = dAp Wp, masked by ReLU'(conv2) (h > 0), HWC
@@ -694,7 +696,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     }
     GProb& pp = dw(gb, c.mat(w.dAp), c.mat(w.Xh), ling(L, gc, gC, "critic.proj", "critic.proj.ln"), F);
     pp.part_in = c.F(w.part_pq);
-    pp.part_tiles = mt;
+    pp.part_tiles = mt * ks_pq;
     pp.perm_c = C;
     pp.perm_p = P2;
     BF_CK(gemm_launch(gb, s));
@@ -890,6 +892,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       GProb& p = dx(gb, c.mat(w.adA1), am.l1.w, 0, Lt, GE_BWD_LN_TANH);
       bwd_ln(p, aproj, c.bp(w.XHpp), w.XHpp.ld, c.F(w.Rpp), c.bp(w.adAp), w.adAp.ld, c.F(w.part_pp));
       BF_CK(gemm_launch(gb, s));
+      ks_pp = gb.b.ks;
     }
   }
   float* ga = c.F(w.grad_actor);
@@ -908,7 +911,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     p1.part_tiles = mt;
     GProb& pp = dw(gb, c.mat(w.adAp), c.mat(w.Xh), ling(L, ga, gA, "actor.proj", "actor.proj.ln"), F);
     pp.part_in = c.F(w.part_pp);
-    pp.part_tiles = mt;
+    pp.part_tiles = mt * ks_pp;
     pp.perm_c = C;
     pp.perm_p = P2;
     BF_CK(gemm_launch(gb, s));
