@@ -3,9 +3,38 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <utility>
+
 #define SQ_DEV __device__ __forceinline__
 
 namespace sq {
+
+// Programmatic dependent launch: a kernel launched by launch_pdl may start while its stream
+// predecessor is still running; it must call grid_wait() before touching anything a predecessor
+// wrote (griddepcontrol.wait: predecessor grids complete, their writes visible) and then
+// grid_trigger() so its own dependents may launch.  Both are no-ops without the launch attribute.
+SQ_DEV void grid_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SQ_DEV void grid_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+inline bool pdl_enabled() {
+  static const bool off = std::getenv("SQUINT_NO_PDL") != nullptr;
+  return !off;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 constexpr int kWarp = 32;
 

@@ -33,6 +33,8 @@ SQ_DEV void sum16(const uint4 v, uint32_t& lo, uint32_t& hi) {
 __global__ void __launch_bounds__(256) k_insert_f8(const uint8_t* __restrict__ frames, int64_t n, int c, int h,
                                                    int w, const int64_t* __restrict__ slots,
                                                    uint8_t* __restrict__ ring) {
+  grid_wait();
+  grid_trigger();
   const int ho = h / 8, wo = w / 8, chunks = w / 16;
   const int64_t items = n * c * ho * chunks;
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
@@ -411,7 +413,7 @@ int launch_insert(const uint8_t* frames, int64_t n, int c, int h, int w, int fac
     const int64_t items = n * c * (h / 8) * (w / 16);
     int64_t blocks = (items + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    note_launch(s, "k_insert_f8", 0, (double)n * c * h * w + (double)n * c * (h / 8) * (w / 8)); k_insert_f8<<<(unsigned)blocks, 256, 0, s>>>(frames, n, c, h, w, slots, ring);
+    note_launch(s, "k_insert_f8", 0, (double)n * c * h * w + (double)n * c * (h / 8) * (w / 8)); launch_pdl(k_insert_f8, dim3((unsigned)blocks), dim3(256), 0, s, frames, n, c, h, w, slots, ring);
   } else {
     const int64_t items = n * c * (h / factor) * (w / factor);
     int64_t blocks = (items + 255) / 256;

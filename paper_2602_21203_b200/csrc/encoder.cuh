@@ -59,6 +59,8 @@ struct EncBwdArgs {
   int nchunk;
   float* gw1; float* gb1; float* gw2; float* gb2;  // final grads (CRITIC layout)
   const uint8_t* wtiles;   // tensor-core path: conv weights as swizzled bf16 smem images (k_conv_tiles)
+  int max_ctas;            // tensor-core path: grid cap (0: one CTA per SM); fewer when the kernel
+                           // runs beside other work on a graph branch
 };
 
 int launch_enc_fwd(const EncFwdArgs& a, cudaStream_t s);

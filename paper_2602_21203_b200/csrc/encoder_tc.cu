@@ -58,6 +58,8 @@ __host__ __device__ inline uint32_t bwd_woff(int C) { return (fwd_wbytes(C) + 10
 // bwd: W2T tiles [kb][c][k = t*C + o].  Element (row, k) of a tile at sw(row, k / 8) + 2 (k % 8).
 __global__ void __launch_bounds__(256) k_conv_tiles(const float* __restrict__ w1, const float* __restrict__ w2, int C,
                                                     uint8_t* __restrict__ out) {
+  grid_wait();
+  grid_trigger();
   const int nkb2 = nkb2_of(C);
   const int n1 = C * 8, n2 = nkb2 * C * 8;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n1 + 2 * n2; e += gridDim.x * blockDim.x) {
@@ -134,6 +136,8 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ 
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
+  grid_wait();  // weight tiles and inputs come from earlier kernels
+  grid_trigger();
   if (tid == 0) {
     tc::mbar_expect_tx(&wbar, fwd_wbytes(C));
     tc::bulk_load_1d(sm + L::w, a.wtiles, fwd_wbytes(C), &wbar);
@@ -375,6 +379,8 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ 
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
+  grid_wait();
+  grid_trigger();
   if (tid == 0) {
     tc::mbar_expect_tx(&wbar, bwd_wbytes(C));
     tc::bulk_load_1d(sm + L::w, a.wtiles + bwd_woff(C), bwd_wbytes(C), &wbar);
@@ -609,6 +615,8 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ 
 __global__ void __launch_bounds__(256) k_reduce_enc(const float* __restrict__ part, int nchunk, int C,
                                                     float* __restrict__ gw2, float* __restrict__ gb2,
                                                     float* __restrict__ gw1, float* __restrict__ gb1) {
+  grid_wait();
+  grid_trigger();
   __shared__ float red[4][64];
   const int stride = part_rows(C) * C;
   const int i = blockIdx.x * 64 + (threadIdx.x & 63), sl = threadIdx.x >> 6;
@@ -640,14 +648,14 @@ int launch_fwd_c(const EncFwdArgs& a, cudaStream_t s) {
   cudaFuncSetAttribute(k_enc_fwd_tc<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int total = ((a.B + kGF - 1) / kGF) * a.nsrc;
   const int grid = total < 148 ? total : 148;
-  k_enc_fwd_tc<C><<<grid, kThr, smem, s>>>(a);
+  launch_pdl(k_enc_fwd_tc<C>, grid, dim3(kThr), smem, s, a);
   return (int)cudaGetLastError();
 }
 template <int C>
 int launch_bwd_c(const EncBwdArgs& a, int grid, int dbg, cudaStream_t s) {
   const size_t smem = BwdL<C>::total + 1024;
   cudaFuncSetAttribute(k_enc_bwd_tc<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_enc_bwd_tc<C><<<grid, kThr, smem, s>>>(a, dbg);
+  launch_pdl(k_enc_bwd_tc<C>, grid, dim3(kThr), smem, s, a, dbg);
   return (int)cudaGetLastError();
 }
 
@@ -657,7 +665,7 @@ size_t conv_tiles_bytes(int C) { return bwd_woff(C) + bwd_wbytes(C); }
 
 int launch_conv_tiles(const float* w1, const float* w2, int C, uint8_t* tiles, cudaStream_t s) {
   note_launch(s, "k_conv_tiles", 0, 0);
-  k_conv_tiles<<<64, 256, 0, s>>>(w1, w2, C, tiles);
+  launch_pdl(k_conv_tiles, dim3(64), dim3(256), 0, s, w1, w2, C, tiles);
   return (int)cudaGetLastError();
 }
 
@@ -683,7 +691,8 @@ int launch_enc_bwd_tc(const EncBwdArgs& a, cudaStream_t s) {
   if (a.B == 0) return 0;
   if ((a.C != 32 && a.C != 64) || a.H != 16 || a.c_in != 3 || !a.wtiles) return (int)cudaErrorInvalidValue;
   const int ngroups = (a.B + kGB - 1) / kGB;
-  const int grid = ngroups < 148 ? ngroups : 148;
+  const int cap = a.max_ctas > 0 && a.max_ctas < 148 ? a.max_ctas : 148;
+  const int grid = ngroups < cap ? ngroups : cap;
   static const bool dbg = getenv("SQUINT_ENC_DBG") != nullptr;
   {
     const double C = a.C;
@@ -693,7 +702,7 @@ int launch_enc_bwd_tc(const EncBwdArgs& a, cudaStream_t s) {
   if (e) return e;
   const int stride = part_rows(a.C) * a.C;
   note_launch(s, "k_reduce_enc", 0, 0);
-  k_reduce_enc<<<(stride + 63) / 64, 256, 0, s>>>(a.part, grid, a.C, a.gw2, a.gb2, a.gw1, a.gb1);
+  launch_pdl(k_reduce_enc, dim3((stride + 63) / 64), dim3(256), 0, s, a.part, grid, a.C, a.gw2, a.gb2, a.gw1, a.gb1);
   return (int)cudaGetLastError();
 }
 

@@ -22,6 +22,8 @@ constexpr int kRows = 8;  // rows (warps) per block
 // issued together; every reduction is a fixed-order warp butterfly).
 template <int NPL>
 __global__ void __launch_bounds__(256) k_target_ce(const __grid_constant__ TargetCEArgs a) {
+  grid_wait();
+  grid_trigger();
   extern __shared__ float sm[];
   const int N = a.N, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float* pb = sm + w * 2 * N;  // pbar [N]
@@ -136,6 +138,8 @@ __global__ void __launch_bounds__(256) k_target_ce(const __grid_constant__ Targe
 
 template <int NPL>
 __global__ void __launch_bounds__(256) k_actor_q(const __grid_constant__ ActorQArgs a) {
+  grid_wait();
+  grid_trigger();
   const int N = a.N, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int row = blockIdx.x * kRows + w;
   if (row >= a.B) return;
@@ -195,7 +199,7 @@ int launch_target_ce(const TargetCEArgs& a, cudaStream_t s) {
 #define SQ_TCE(n)                                                                              \
   {                                                                                            \
     cudaFuncSetAttribute(k_target_ce<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    k_target_ce<n><<<grid, 256, smem, s>>>(a);                                                 \
+    launch_pdl(k_target_ce<n>, grid, dim3(256), smem, s, a);                                                 \
   }
   if (npl <= 2) SQ_TCE(2) else if (npl <= 4) SQ_TCE(4) else if (npl <= 8) SQ_TCE(8) else SQ_TCE(16)
 #undef SQ_TCE
@@ -206,10 +210,10 @@ int launch_actor_q(const ActorQArgs& a, cudaStream_t s) {
   const int npl = (a.N + 31) / 32;
   const dim3 grid((a.B + kRows - 1) / kRows);
   note_launch(s, "k_actor_q", 0, 0);
-  if (npl <= 2) k_actor_q<2><<<grid, 256, 0, s>>>(a);
-  else if (npl <= 4) k_actor_q<4><<<grid, 256, 0, s>>>(a);
-  else if (npl <= 8) k_actor_q<8><<<grid, 256, 0, s>>>(a);
-  else k_actor_q<16><<<grid, 256, 0, s>>>(a);
+  if (npl <= 2) launch_pdl(k_actor_q<2>, grid, dim3(256), 0, s, a);
+  else if (npl <= 4) launch_pdl(k_actor_q<4>, grid, dim3(256), 0, s, a);
+  else if (npl <= 8) launch_pdl(k_actor_q<8>, grid, dim3(256), 0, s, a);
+  else launch_pdl(k_actor_q<16>, grid, dim3(256), 0, s, a);
   return (int)cudaGetLastError();
 }
 

@@ -14,6 +14,8 @@ namespace {
 
 __global__ void __launch_bounds__(256) k_row_sums(const float* __restrict__ logp, const float* __restrict__ row_loss,
                                                   int B, float* __restrict__ extras) {
+  grid_wait();
+  grid_trigger();
   __shared__ float red[32];
   float a = 0.f, b = 0.f;
   for (int i = threadIdx.x; i < B; i += blockDim.x) {
@@ -33,6 +35,8 @@ __global__ void __launch_bounds__(256) k_row_sums(const float* __restrict__ logp
 __device__ __forceinline__ float bias_corr(float beta, int64_t t) { return -1.f / expm1f((float)t * log1pf(beta - 1.f)); }
 
 __global__ void __launch_bounds__(256) k_scalars(const __grid_constant__ ScalarsArgs a) {
+  grid_wait();
+  grid_trigger();
   __shared__ float red[32];
   float sl = 0.f, sq = 0.f;
   if (a.compute_sums) {
@@ -82,6 +86,8 @@ __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, const floa
                                               float4* __restrict__ m, float4* __restrict__ v, int64_t n4, float lr,
                                               float b1, float b2, float eps, const float* __restrict__ c1p,
                                               const float* __restrict__ c2p, float* __restrict__ part) {
+  grid_wait();
+  grid_trigger();
   __shared__ float red[32];
   const float c1 = c1p[0], c2 = c2p[0];
   float ss = 0.f;
@@ -110,6 +116,8 @@ __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, const floa
 
 __global__ void __launch_bounds__(256) k_polyak(float* __restrict__ t, const float* __restrict__ o, int64_t n,
                                                 float tau) {
+  grid_wait();
+  grid_trigger();
   const float keep = 1.f - tau;
   const bool vec = ((reinterpret_cast<uintptr_t>(t) | reinterpret_cast<uintptr_t>(o)) & 15) == 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -135,6 +143,8 @@ __global__ void __launch_bounds__(256) k_polyak(float* __restrict__ t, const flo
 
 __global__ void __launch_bounds__(256) k_lpi_sums(const float* __restrict__ row_lpi, const float* __restrict__ row_q,
                                                   int B, float* __restrict__ out2) {
+  grid_wait();
+  grid_trigger();
   __shared__ float red[32];
   float a = 0.f, b = 0.f;
   for (int i = threadIdx.x; i < B; i += blockDim.x) {
@@ -150,6 +160,8 @@ __global__ void __launch_bounds__(256) k_lpi_sums(const float* __restrict__ row_
 }
 
 __global__ void __launch_bounds__(256) k_metrics(const __grid_constant__ MetricsArgs a) {
+  grid_wait();
+  grid_trigger();
   __shared__ float red[32];
   float lpi = 0.f, q = 0.f, gs = 0.f;
   if (a.reduce_local) {
@@ -200,6 +212,8 @@ __device__ __forceinline__ int shadow_slot(const ShadowTable& t, int i) {
 }
 
 __global__ void __launch_bounds__(256) k_shadow(const float* __restrict__ master, const __grid_constant__ ShadowTable t) {
+  grid_wait();
+  grid_trigger();
   for (int k = 0; k < t.n; ++k) {
     const ShadowEnt& e = t.e[k];
     const int n = e.rows * e.cols;
@@ -220,6 +234,8 @@ __global__ void __launch_bounds__(256) k_adam_sh(float4* __restrict__ p, const f
                                                  float b1, float b2, float eps, const float* __restrict__ c1p,
                                                  const float* __restrict__ c2p, float* __restrict__ part,
                                                  const __grid_constant__ ShadowTable t, int base) {
+  grid_wait();
+  grid_trigger();
   __shared__ float red[32];
   const float c1 = c1p[0], c2 = c2p[0];
   float ss = 0.f;
@@ -255,6 +271,8 @@ __global__ void __launch_bounds__(256) k_adam_sh(float4* __restrict__ p, const f
 
 __global__ void __launch_bounds__(256) k_polyak_sh(float4* __restrict__ t4, const float4* __restrict__ o4, int64_t n4,
                                                    float tau, const __grid_constant__ ShadowTable t) {
+  grid_wait();
+  grid_trigger();
   const float keep = 1.f - tau;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     float4 a = t4[i];
@@ -279,7 +297,7 @@ __global__ void __launch_bounds__(256) k_polyak_sh(float4* __restrict__ t4, cons
 
 int launch_shadow(const float* master, const ShadowTable& t, cudaStream_t s) {
   if (t.n == 0) return 0;
-  note_launch(s, "k_shadow", 0, 0); k_shadow<<<148 * 2, 256, 0, s>>>(master, t);
+  note_launch(s, "k_shadow", 0, 0); launch_pdl(k_shadow, dim3(148 * 2), dim3(256), 0, s, master, t);
   return (int)cudaGetLastError();
 }
 
@@ -289,7 +307,7 @@ int launch_adam_shadow(float* p, const float* g, float* m, float* v, int64_t n, 
   ShadowTable none;
   memset(&none, 0, sizeof(none));
   note_launch(s, "k_adam", 0, 28.0 * (double)n);
-  k_adam_sh<<<nblocks, 256, 0, s>>>(reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
+  launch_pdl(k_adam_sh, dim3(nblocks), dim3(256), 0, s, reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
                                     reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n / 4, lr, b1, b2, eps,
                                     c1, c2, sumsq_part, t ? *t : none, (int)base);
   return (int)cudaGetLastError();
@@ -303,24 +321,24 @@ int launch_polyak_shadow(float* target, const float* online, int64_t n, float ta
   int64_t blocks = (n / 4 + 255) / 256;
   if (blocks > 148 * 4) blocks = 148 * 4;
   note_launch(s, "k_polyak", 0, 12.0 * (double)n);
-  k_polyak_sh<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<float4*>(target), reinterpret_cast<const float4*>(online),
+  launch_pdl(k_polyak_sh, dim3((unsigned)blocks), dim3(256), 0, s, reinterpret_cast<float4*>(target), reinterpret_cast<const float4*>(online),
                                                n / 4, tau, t ? *t : none);
   return (int)cudaGetLastError();
 }
 
 int launch_row_sums(const float* logp, const float* row_loss, int B, float* extras, cudaStream_t s) {
-  note_launch(s, "k_row_sums", 0, 0); k_row_sums<<<1, 256, 0, s>>>(logp, row_loss, B, extras);
+  note_launch(s, "k_row_sums", 0, 0); launch_pdl(k_row_sums, dim3(1), dim3(256), 0, s, logp, row_loss, B, extras);
   return (int)cudaGetLastError();
 }
 
 int launch_scalars(const ScalarsArgs& a, cudaStream_t s) {
-  note_launch(s, "k_scalars", 0, 0); k_scalars<<<1, 256, 0, s>>>(a);
+  note_launch(s, "k_scalars", 0, 0); launch_pdl(k_scalars, dim3(1), dim3(256), 0, s, a);
   return (int)cudaGetLastError();
 }
 
 int launch_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
                 const float* c1, const float* c2, float* sumsq_part, cudaStream_t s) {
-  note_launch(s, "k_adam", 0, 28.0 * (double)n); k_adam<<<kAdamBlocks, 256, 0, s>>>(reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
+  note_launch(s, "k_adam", 0, 28.0 * (double)n); launch_pdl(k_adam, dim3(kAdamBlocks), dim3(256), 0, s, reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
                                      reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n / 4, lr, b1, b2,
                                      eps, c1, c2, sumsq_part);
   return (int)cudaGetLastError();
@@ -331,17 +349,17 @@ int launch_polyak(float* target, const float* online, int64_t n, float tau, cuda
   int64_t blocks = (n / 4 + 255) / 256;
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  note_launch(s, "k_polyak", 0, 12.0 * (double)n); k_polyak<<<(unsigned)blocks, 256, 0, s>>>(target, online, n, tau);
+  note_launch(s, "k_polyak", 0, 12.0 * (double)n); launch_pdl(k_polyak, dim3((unsigned)blocks), dim3(256), 0, s, target, online, n, tau);
   return (int)cudaGetLastError();
 }
 
 int launch_metrics(const MetricsArgs& a, cudaStream_t s) {
-  note_launch(s, "k_metrics", 0, 0); k_metrics<<<1, 256, 0, s>>>(a);
+  note_launch(s, "k_metrics", 0, 0); launch_pdl(k_metrics, dim3(1), dim3(256), 0, s, a);
   return (int)cudaGetLastError();
 }
 
 int launch_lpi_sums(const float* row_lpi, const float* row_q, int B, float* out2, cudaStream_t s) {
-  note_launch(s, "k_lpi_sums", 0, 0); k_lpi_sums<<<1, 256, 0, s>>>(row_lpi, row_q, B, out2);
+  note_launch(s, "k_lpi_sums", 0, 0); launch_pdl(k_lpi_sums, dim3(1), dim3(256), 0, s, row_lpi, row_q, B, out2);
   return (int)cudaGetLastError();
 }
 

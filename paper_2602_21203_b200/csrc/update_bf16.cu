@@ -638,24 +638,26 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       BF_CK(gemm_launch(gb, s));
       ks_pq = gb.b.ks;  // split-K launch: column partials per 128 / ks rows
     }
-    {
-      // dh = dAp Wp, masked by ReLU'(conv2) (h > 0), HWC
-      GemmBuilder gb(1);
-      GProb& p = dx(gb, c.mat(w.dAp), cproj.w, 0, F, GE_RELU_MASK);
-      p.y = c.bp(w.Xh);
-      p.ldy = w.Xh.ld;
-      p.out = c.bp(w.dh);
-      p.ldo = w.dh.ld;
-      BF_CK(gemm_launch(gb, s));
-    }
   }
-  // encoder backward: on the auxiliary branch when single-GPU (overlaps the critic dW GEMM and
-  // the actor-loss chain), inline when the gradients are all-reduced
+  // encoder backward (dh GEMM + conv backward): on the auxiliary branch when single-GPU
+  // (overlaps the critic dW GEMM and the actor-loss chain), inline when the gradients are
+  // all-reduced
   const bool branch = comm == nullptr && c.aux != nullptr;
   cudaStream_t es = branch ? c.aux->s : s;
   if (branch) {
     BF_CK(cudaEventRecord(c.aux->fork, s));
     BF_CK(cudaStreamWaitEvent(es, c.aux->fork, 0));
+  }
+  {
+    // dh = dAp Wp, masked by ReLU'(conv2) (h > 0), HWC
+    PhaseScope ps(8, rep, es);
+    GemmBuilder gb(1);
+    GProb& p = dx(gb, c.mat(w.dAp), cproj.w, 0, F, GE_RELU_MASK);
+    p.y = c.bp(w.Xh);
+    p.ldy = w.Xh.ld;
+    p.out = c.bp(w.dh);
+    p.ldo = w.dh.ld;
+    BF_CK(gemm_launch(gb, es));
   }
   {
     PhaseScope ps(10, rep, es);
@@ -676,6 +678,9 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     e.gb1 = gc + L.off(gC, "enc.conv1.b");
     e.gw2 = gc + L.off(gC, "enc.conv2.w");
     e.gb2 = gc + L.off(gC, "enc.conv2.b");
+    // on the branch, leave SMs to the critic dW GEMM and the actor-loss launches beside it
+    static const int bwd_ctas = getenv("SQUINT_ENC_BWD_CTAS") ? atoi(getenv("SQUINT_ENC_BWD_CTAS")) : 80;
+    e.max_ctas = branch ? bwd_ctas : 0;
     BF_CK(launch_enc_bwd_tc(e, es));
   }
   {
