@@ -351,28 +351,46 @@ def run_gpu(args):
                 e["flops"] += fl / R
                 e["bytes"] += by / R
 
-    # e2e: same step through the C ABI from pinned host buffers (H2D inputs, D2H results)
+    # e2e: the environment loop through the public API from pinned host buffers.  Step t acts on
+    # o_t (uploaded by step t-1), reads the actions back, uploads the new observation o_{t+1}
+    # (the env's output: stored as next_obs now and acted on at step t+1, so each frame batch
+    # crosses PCIe once) and the step's small inputs, inserts o_{t+1} and runs the UTD updates.
+    # The frame upload runs on a copy stream beside the updates (which sample the ring as it was
+    # before o_{t+1} is inserted); the insert waits for it.  Results (actions, log pi, metrics) go
+    # back to pinned host memory every step.
     e2e = None
     if not args.no_e2e:
-        h_fr = [pools[p][0].cpu().pin_memory() for p in range(NPOOL)]
-        h_nx = [pools[p][1].cpu().pin_memory() for p in range(NPOOL)]
+        h_fr = [pools[p][1].cpu().pin_memory() for p in range(NPOOL)]
         h_in = [t.cpu().pin_memory() for t in (idx_all, sh_all, eps_all, aeps_all, prop_all, slots_all)]
         h_out = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (act_out, logp_out, metrics)]
-        dfr, dnx = pools[0][0].clone(), pools[0][1].clone()
+        dbuf = [pools[0][0].clone(), pools[0][1].clone()]
         stage = [idx_s, sh_s, eps_s, aeps_s, prop_s, slots_s]
+        main = torch.cuda.current_stream()
+        cps = torch.cuda.Stream(device=dev)
+        acted = [torch.cuda.Event(), torch.cuda.Event()]
+        copied = torch.cuda.Event()
 
         def e2e_step(k):
-            dfr.copy_(h_fr[k % NPOOL], non_blocking=True)
-            dnx.copy_(h_nx[k % NPOOL], non_blocking=True)
+            cur, nxt = dbuf[k % 2], dbuf[(k + 1) % 2]
             for dst, src in zip(stage, h_in):
                 dst.copy_(src[k], non_blocking=True)
-            P.squint_act(L.dims, L.hp, L.actor, L.critic, dfr, prop_s, aeps_s, act_out, logp_out, act_ws,
+            P.squint_act(L.dims, L.hp, L.actor, L.critic, cur, prop_s, aeps_s, act_out, logp_out, act_ws,
                          ring=obs_ring, slots=slots_s)
-            P.squint_insert(dnx, 8, slots_s, next_ring)
-            L.update(replay, idx_s, sh_s, eps_s, metrics)
-            for dst, src in zip(h_out, (act_out, logp_out, metrics)):
+            acted[k % 2].record(main)
+            for dst, src in zip(h_out[:2], (act_out, logp_out)):
                 dst.copy_(src, non_blocking=True)
+            # o_{t+1} -> the buffer step t-1 acted on (that act has been issued and is waited for)
+            cps.wait_event(acted[(k + 1) % 2])
+            with torch.cuda.stream(cps):
+                nxt.copy_(h_fr[k % NPOOL], non_blocking=True)
+                copied.record(cps)
+            L.update(replay, idx_s, sh_s, eps_s, metrics)
+            main.wait_event(copied)
+            P.squint_insert(nxt, 8, slots_s, next_ring)
+            h_out[2].copy_(metrics, non_blocking=True)
 
+        dbuf[0].copy_(h_fr[NPOOL - 1], non_blocking=True)  # o_0
+        acted[1].record(main)
         for w in range(W):
             e2e_step(w)
         torch.cuda.synchronize()
@@ -389,10 +407,12 @@ def run_gpu(args):
             t = torch.tensor([ems], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-        h2d = (pools[0][0].numel() + pools[0][1].numel() + sum(x[0].numel() * x.element_size() for x in h_in))
+        h2d = h_fr[0].numel() + sum(x[0].numel() * x.element_size() for x in h_in)
         d2h = sum(x.numel() * x.element_size() for x in h_out)
         e2e = {"value": world * UTD * K / (ems / 1e3), "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / K}
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / K,
+               "loop": "act(o_t) -> D2H actions -> H2D o_{t+1} (copy stream, beside the updates) -> "
+                       "insert(o_{t+1}) after the updates"}
 
     if rank != 0:
         if world > 1:
