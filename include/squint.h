@@ -126,7 +126,10 @@ SQUINT_API squint_status squint_param_layout(const squint_dims* dims, squint_ten
 SQUINT_API squint_status squint_workspace_bytes(const squint_dims* dims, int utd, size_t* bytes);
 
 /* Offset/bytes of a named workspace region (debug/test access to intermediates):
- * 0 = critic gradient (CRITIC layout), 1 = actor gradient (ACTOR layout),
+ * 0 = critic gradient (CRITIC layout), 1 = actor gradient (ACTOR layout) -- in SQUINT_BF16
+ *     precision the projection weights' gradients (critic.proj.w, actor.proj.w, [latent][25C])
+ *     are stored pixel-major, column pix * C + c (the bf16 encoder's HWC flatten order; the
+ *     optimizer gathers them), every other tensor as in squint_param_layout,
  * 2 = target distribution m [B, n_atoms], 3 = h [B, 25C], 4 = log pi (current) [B],
  * 5 = log pi' (next) [B], 6 = actions a~ [B, A], 7 = scalars [16]. */
 SQUINT_API squint_status squint_workspace_region(const squint_dims* dims, int region, size_t* offset, size_t* bytes);

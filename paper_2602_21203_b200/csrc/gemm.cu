@@ -86,8 +86,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   const int n1 = nt > 256 ? 256 : nt, n2 = nt - n1;
   uint32_t ncols = 32;
   while ((int)ncols < nt) ncols <<= 1;
+  // weight gradient with a plain bias: column sums of D from an N = 16 MMA against ones
+  const bool ones = EPI == GE_DW && P.bias_ones && n0 == 0;
+  const uint32_t ones_col = ncols;
+  if (ones) ncols *= 2;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int S = b.nstages;
+  uint8_t* ones_tile = smem + (S * b.stage_bytes > kEpiBytes ? S * b.stage_bytes : kEpiBytes);  // 16 x 64 bf16
   auto stamp = [&](int k) {
     if (b.dbg && tid == 0) {
       unsigned long long t;
@@ -110,6 +115,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   if (warp == 2 && lane < P.nseg) {
     tc::tma_prefetch_desc(&b.maps[P.seg[lane].amap]);
     tc::tma_prefetch_desc(&b.maps[P.seg[lane].bmap]);
+  }
+  if (ones && warp == 3) {
+    // all elements 1.0 (so the swizzle is irrelevant); visible to the tensor core (async proxy)
+    for (int i = lane; i < 2048 / 16; i += 32)
+      reinterpret_cast<uint4*>(ones_tile)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    tc::fence_async_smem();
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -188,6 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
       const GSeg& G = P.seg[s];
       const uint32_t id1 = tc::idesc_bf16_major(128, n1, G.a_mn, G.b_mn);
       const uint32_t id2 = tc::idesc_bf16_major(128, n2 > 0 ? n2 : 16, G.a_mn, G.b_mn);
+      const uint32_t id_ones = tc::idesc_bf16_major(128, 16, G.a_mn, 0);
       for (int l = 0; l < G.nkb; ++l, ++kb) {
         const int st = kb % S;
         tc::mbar_wait(&full_bar[st], (kb / S) & 1);
@@ -204,6 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
                                         : tc::sdesc_sw128(b0 + 32768 + 32 * k, 16, 1024);
             tc::mma_bf16(tmem + 256, ad, bd2, id2, acc);
           }
+          if (ones) tc::mma_bf16(tmem + ones_col, ad, tc::sdesc_sw128(tc::smem_u32(ones_tile) + 32 * k, 16, 1024), id_ones, acc);
         }
         tc::mma_commit(&empty_bar[st]);
       }
@@ -257,50 +270,45 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   };
 
   if constexpr (EPI == GE_BIAS_F32 || EPI == GE_DW) {
+    // fp32 rows through a per-warp 32 x 33 transpose tile: each store instruction writes 32
+    // consecutive floats of one row (coalesced for any row pitch)
+    float* T = reinterpret_cast<float*>(smem) + warp * 32 * 33;
+    const int nvr = min(32, P.M - row0);
     for (int ch = hh; ch < nch; ch += 2) {
       const int c0 = n0 + ch * 32, ncv = min(32, n0 + nreal - c0);
       tc::tmem_ld32(trow + ch * 32, v);
       if constexpr (EPI == GE_BIAS_F32) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] += s_bias[ch * 32 + j];
-        if (rv) row_st_f32(P.outf + (int64_t)r * P.ldf + c0, ncv, v);
-      } else {
-        if (rv) {
-          if (P.perm_c == 0) {
-            row_st_f32(P.outf + (int64_t)r * P.ldf + c0, ncv, v);
-          } else {
+      }
+      __syncwarp();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int c = c0 + j, pix = c / P.perm_c, chn = c - pix * P.perm_c;
-              if (j < ncv) P.outf[(int64_t)r * P.ldf + chn * P.perm_p + pix] = v[j];
+      for (int j = 0; j < 32; ++j) T[lane * 33 + j] = v[j];
+      __syncwarp();
+      if (lane < ncv)
+        for (int i = 0; i < nvr; ++i) P.outf[(int64_t)(row0 + i) * P.ldf + c0 + lane] = T[i * 33 + lane];
+    }
+    if constexpr (EPI == GE_DW) {
+      if (n0 == 0 && hh == 0) {
+        float db = 0.f, dg = 0.f, dbe = 0.f;
+        if (ones) {
+          float o[16];
+          tc::tmem_ld16(trow + ones_col, o);
+          db = o[0];
+        }
+        if (rv) {
+          if (P.part_in) {
+            for (int t = 0; t < P.part_tiles; ++t) {
+              const float* pp = P.part_in + (int64_t)t * 3 * P.M;
+              db += pp[r];
+              dg += pp[P.M + r];
+              dbe += pp[2 * P.M + r];
             }
           }
+          if (P.db) P.db[r] = db;
+          if (P.dg) P.dg[r] = dg;
+          if (P.dbeta) P.dbeta[r] = dbe;
         }
-      }
-    }
-    stamp(5);
-    if constexpr (EPI == GE_DW) {
-      if (n0 == 0 && hh == 0 && rv) {
-        float db = 0.f, dg = 0.f, dbe = 0.f;
-        if (P.part_in) {
-          for (int t = 0; t < P.part_tiles; ++t) {
-            const float* pp = P.part_in + (int64_t)t * 3 * P.M;
-            db += pp[r];
-            dg += pp[P.M + r];
-            dbe += pp[2 * P.M + r];
-          }
-        } else if (P.colsum) {
-          float acc4[4] = {0.f, 0.f, 0.f, 0.f};
-          int i = 0;
-          for (; i + 4 <= P.colsum_rows; i += 4)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) acc4[u] += __bfloat162float(P.colsum[(int64_t)(i + u) * P.ld_colsum + r]);
-          for (; i < P.colsum_rows; ++i) acc4[0] += __bfloat162float(P.colsum[(int64_t)i * P.ld_colsum + r]);
-          db = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
-        }
-        if (P.db) P.db[r] = db;
-        if (P.dg) P.dg[r] = dg;
-        if (P.dbeta) P.dbeta[r] = dbe;
       }
     }
   } else if constexpr (EPI == GE_RELU_MASK) {
@@ -1152,6 +1160,7 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   } else if (smem < (size_t)kEpiBytes) {
     smem = kEpiBytes;
   }
+  if (b.p[0].epi == GE_DW) smem += 2048;  // ones tile (bias gradients)
   smem += 1024;
   const int epi = b.p[0].epi;
   for (int i = 1; i < b.nprob; ++i)

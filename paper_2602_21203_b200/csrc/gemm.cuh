@@ -33,7 +33,7 @@ enum GEpi : int {
   GE_BWD_LN_TANH = 5,  // same with tanh
   GE_RELU_MASK = 6,    // out = acc * (y > 0)
   GE_TG_BWD = 7,       // acc = dL/da (A cols) -> out = dL/d[mu | l] (2A cols)
-  GE_DW = 8,           // outf[n][perm(k)] = acc (weight gradient); tile-column 0 adds bias/LN grads
+  GE_DW = 8,           // outf[n][k] = acc (weight gradient); tile-column 0 adds bias/LN grads
 };
 
 struct GSeg {
@@ -81,10 +81,8 @@ struct GProb {
   float* dbeta;
   const float* part_in;      // bwd-LN partials of this layer [part_tiles][3][M]
   int part_tiles;
-  const bf16* colsum;        // else db[n] = sum_r colsum[r * ld_colsum + n], r < colsum_rows
-  int ld_colsum, colsum_rows;
-  int perm_c;                // > 0: column k = pix * perm_c + ch is stored at ch * perm_p + pix
-  int perm_p;
+  int bias_ones;             // else db[n] = sum_m D[m][n]: an extra N = 16 MMA of the D tile against
+                             // a shared-memory tile of ones (tile column 0 only)
   int omap, xmap, ymap;      // epilogue tensor maps (set by gemm_launch): out, xh, y (64 x 32 boxes)
 };
 

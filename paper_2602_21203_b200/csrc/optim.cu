@@ -233,14 +233,38 @@ __global__ void __launch_bounds__(256) k_adam_sh(float4* __restrict__ p, const f
                                                  float4* __restrict__ m, float4* __restrict__ v, int64_t n4, float lr,
                                                  float b1, float b2, float eps, const float* __restrict__ c1p,
                                                  const float* __restrict__ c2p, float* __restrict__ part,
-                                                 const __grid_constant__ ShadowTable t, int base) {
+                                                 const __grid_constant__ ShadowTable t, int base, int grad_perm) {
   grid_wait();
   grid_trigger();
   __shared__ float red[32];
   const float c1 = c1p[0], c2 = c2p[0];
+  // grad_perm: the gradient of a shadow entry with a column permutation (the projection weight)
+  // is stored in the shadow's (pixel-major) column order, row pitch = cols: gathered here
+  int pe = -1;
+  int64_t plo = 0, phi = 0;
+  if (grad_perm)
+    for (int k = 0; k < t.n; ++k)
+      if (t.e[k].perm_c > 0) {
+        pe = k;
+        plo = t.e[k].src - base;
+        phi = plo + (int64_t)t.e[k].rows * t.e[k].cols;
+      }
+  const float* gs = reinterpret_cast<const float*>(g);
   float ss = 0.f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-    float4 gg = g[i], mm = m[i], vv = v[i], pp = p[i];
+    float4 gg, mm = m[i], vv = v[i], pp = p[i];
+    if (pe >= 0 && 4 * i >= plo && 4 * i < phi) {
+      const ShadowEnt& e = t.e[pe];
+      float* gf = reinterpret_cast<float*>(&gg);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int l = (int)(4 * i + k - plo), row = l / e.cols, col = l - row * e.cols;
+        const int ch = col / e.perm_p, pix = col - ch * e.perm_p;
+        gf[k] = gs[plo + (int64_t)row * e.cols + pix * e.perm_c + ch];
+      }
+    } else {
+      gg = g[i];
+    }
     float* gf = reinterpret_cast<float*>(&gg);
     float* mf = reinterpret_cast<float*>(&mm);
     float* vf = reinterpret_cast<float*>(&vv);
@@ -303,13 +327,13 @@ int launch_shadow(const float* master, const ShadowTable& t, cudaStream_t s) {
 
 int launch_adam_shadow(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
                        float eps, const float* c1, const float* c2, float* sumsq_part, const ShadowTable* t,
-                       cudaStream_t s, int64_t base, int nblocks) {
+                       cudaStream_t s, int64_t base, int nblocks, int grad_perm) {
   ShadowTable none;
   memset(&none, 0, sizeof(none));
   note_launch(s, "k_adam", 0, 28.0 * (double)n);
   launch_pdl(k_adam_sh, dim3(nblocks), dim3(256), 0, s, reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
                                     reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n / 4, lr, b1, b2, eps,
-                                    c1, c2, sumsq_part, t ? *t : none, (int)base);
+                                    c1, c2, sumsq_part, t ? *t : none, (int)base, grad_perm);
   return (int)cudaGetLastError();
 }
 

@@ -65,9 +65,11 @@ struct ShadowTable {
 int launch_shadow(const float* master, const ShadowTable& t, cudaStream_t s);
 // Adam (as launch_adam) that also writes the updated weights' bf16 shadow (t may be NULL).
 // `base` = flat group index of p[0] (shadow lookups), `nblocks` = grid (= partial sums written).
+// grad_perm: gradients of permuted shadow entries (the projection weight) are stored in the
+// shadow's column order (pixel-major, row pitch = cols) and gathered through the permutation.
 int launch_adam_shadow(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
                        float eps, const float* c1, const float* c2, float* sumsq_part, const ShadowTable* t,
-                       cudaStream_t s, int64_t base = 0, int nblocks = kAdamBlocks);
+                       cudaStream_t s, int64_t base = 0, int nblocks = kAdamBlocks, int grad_perm = 0);
 // Polyak over a 16-byte aligned buffer (n % 4 == 0) that also refreshes the target shadow.
 int launch_polyak_shadow(float* target, const float* online, int64_t n, float tau, const ShadowTable* t,
                          cudaStream_t s);

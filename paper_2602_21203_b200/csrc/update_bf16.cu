@@ -689,9 +689,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     for (int i = 0; i < 2; ++i) {
       const std::string hp_ = kHeads[i];
       GProb& p3 = dw(gb, c.half(w.dlog, i), c.mat(w.qH2[i]), ling(L, gc, gC, hp_ + ".l3", ""), Hc);
-      p3.colsum = c.halfp(w.dlog, i);
-      p3.ld_colsum = w.dlog.ld;
-      p3.colsum_rows = B;
+      p3.bias_ones = 1;
       GProb& p2 = dw(gb, c.mat(w.dA2c[i]), c.mat(w.qH1[i]), ling(L, gc, gC, hp_ + ".l2", hp_ + ".ln2"), Hc);
       p2.part_in = c.F(w.part_q2[i]);
       p2.part_tiles = mt;
@@ -702,8 +700,6 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     GProb& pp = dw(gb, c.mat(w.dAp), c.mat(w.Xh), ling(L, gc, gC, "critic.proj", "critic.proj.ln"), F);
     pp.part_in = c.F(w.part_pq);
     pp.part_tiles = mt * ks_pq;
-    pp.perm_c = C;
-    pp.perm_p = P2;
     BF_CK(gemm_launch(gb, s));
   }
   float* extras = gc + L.gsize[gC];
@@ -742,7 +738,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       const int64_t e0 = L.enc_end;
       BF_CK(launch_adam_shadow(st.critic + e0, gc + e0, st.m_critic + e0, st.v_critic + e0, L.gsize[gC] - e0,
                                hp.lr_critic, hp.beta1, hp.beta2, hp.adam_eps, scal + S_C1_CRITIC, scal + S_C2_CRITIC,
-                               c.F(w.adam_part), &shC, s, e0, kAdamBlocks));
+                               c.F(w.adam_part), &shC, s, e0, kAdamBlocks, 1));
       BF_CK(cudaEventRecord(c.aux->scal, s));
       BF_CK(cudaStreamWaitEvent(es, c.aux->scal, 0));
       BF_CK(launch_adam_shadow(st.critic, gc, st.m_critic, st.v_critic, e0, hp.lr_critic, hp.beta1, hp.beta2,
@@ -752,7 +748,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     } else {
       BF_CK(launch_adam_shadow(st.critic, gc, st.m_critic, st.v_critic, L.gsize[gC], hp.lr_critic, hp.beta1,
                                hp.beta2, hp.adam_eps, scal + S_C1_CRITIC, scal + S_C2_CRITIC, c.F(w.adam_part), &shC,
-                               s));
+                               s, 0, kAdamBlocks, 1));
     }
   }
   // a12: actor loss against theta+ on sg(h) (Q19)
@@ -905,9 +901,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     PhaseScope ps(14, rep, s);
     GemmBuilder gb(1);
     GProb& p3 = dw(gb, c.mat(w.dO), c.mat(w.H2ac), ling(L, ga, gA, "actor.l3", ""), Ha);
-    p3.colsum = c.bp(w.dO);
-    p3.ld_colsum = w.dO.ld;
-    p3.colsum_rows = B;
+    p3.bias_ones = 1;
     GProb& p2 = dw(gb, c.mat(w.adA2), c.mat(w.H1ac), ling(L, ga, gA, "actor.l2", "actor.ln2"), Ha);
     p2.part_in = c.F(w.part_a2);
     p2.part_tiles = mt;
@@ -917,8 +911,6 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     GProb& pp = dw(gb, c.mat(w.adAp), c.mat(w.Xh), ling(L, ga, gA, "actor.proj", "actor.proj.ln"), F);
     pp.part_in = c.F(w.part_pp);
     pp.part_tiles = mt * ks_pp;
-    pp.perm_c = C;
-    pp.perm_p = P2;
     BF_CK(gemm_launch(gb, s));
   }
   float* lpis = c.F(w.lpi_sums);
@@ -930,7 +922,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     lpis = ax;
   }
   BF_CK(launch_adam_shadow(st.actor, ga, st.m_actor, st.v_actor, L.gsize[gA], hp.lr_actor, hp.beta1, hp.beta2,
-                           hp.adam_eps, scal + S_C1_ACTOR, scal + S_C2_ACTOR, nullptr, &shA, s));
+                           hp.adam_eps, scal + S_C1_ACTOR, scal + S_C2_ACTOR, nullptr, &shA, s, 0, kAdamBlocks, 1));
   // a14: Polyak over every critic tensor except the encoder (+ target shadow)
   BF_CK(launch_polyak_shadow(st.critic_target, st.critic + L.enc_end, L.gsize[gT], hp.tau, &shT, s));
   if (branch) BF_CK(cudaStreamWaitEvent(s, c.aux->join, 0));  // join the encoder branch

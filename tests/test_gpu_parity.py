@@ -230,6 +230,10 @@ def _check_update_bf16(pr, L, met_gpu, st_ref, met_ref, trace):
     compare("logp_next", L.region("logp_next").cpu().numpy(), tr["logp_next"], tol)
     for grp in ("critic", "actor"):
         g = group_values(L, grp, "grad")
+        # bf16 mode stores the projection weight gradient pixel-major (squint.h, region 0/1)
+        pw = f"{grp}.proj.w"
+        C = pr.dims["conv_ch"]
+        g[pw] = g[pw].reshape(g[pw].shape[0], -1, C).transpose(0, 2, 1).reshape(g[pw].shape)
         ref = tr["grad_" + grp]
         e = _rel_l2(g, ref)
         assert e <= 3e-2, f"grad {grp}: group relative L2 {e:.3e} > 3e-2"
