@@ -47,10 +47,10 @@ __device__ __forceinline__ void issue_b(const CBatch& b, const CLayer& L, int n0
 __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatch b) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t aload, bfull[2], done, anext, ld_bar[4];
+  __shared__ uint64_t aload, bfull[2], done, anext, ld_bar[4], stats_bar;
   __shared__ uint32_t tmem_slot;
   __shared__ float red[2][2][128];
-  __shared__ float cl_red[2][kCS][128];
+  __shared__ float2 cl_red[kCS][128];  // per-row (sum, sum of squares) partials pushed by each CTA
   __shared__ __align__(16) float s_bias[64], s_g[64], s_beta[64];
 
   const int rank = blockIdx.x % kCS, cl = blockIdx.x / kCS;
@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
     tc::mbar_init(&done, 1);
     tc::mbar_init(&anext, 1);
     for (int i = 0; i < 4; ++i) tc::mbar_init(&ld_bar[i], 1);
+    tc::mbar_init(&stats_bar, 1);
     tc::fence_mbar_init();
   }
   if (warp == 2 && lane == 0) {
@@ -118,28 +119,36 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
   const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
   int nbwd = 0;  // backward layers so far (x_hat load barrier phase)
 
+  // Row totals over the cluster: each CTA pushes its per-row partials into every CTA's cl_red
+  // with st.async (completion counted on the receiver's stats_bar), then sums the kCS entries in
+  // rank order (every CTA gets the same bits).  Receiving all partials of a layer also proves each
+  // peer finished that layer's MMA and consumed this CTA's previous broadcast (ordering the reuse
+  // of A and cl_red); no cluster-wide barrier.
+  int nstat = 0;
   auto row_total2 = [&](float p1, float p2, float& t1, float& t2) {
+    if (tid == 0) tc::mbar_expect_tx(&stats_bar, kCS * 128 * 8);
     red[0][hh][rl] = p1;
     red[1][hh][rl] = p2;
     __syncthreads();
     t1 = red[0][0][rl] + red[0][1][rl];
     t2 = red[1][0][rl] + red[1][1][rl];
     if (hh == 0)
-      for (int rk = 0; rk < kCS; ++rk) {
-        tc::dsmem_st(&cl_red[0][rank][rl], (uint32_t)rk, t1);
-        tc::dsmem_st(&cl_red[1][rank][rl], (uint32_t)rk, t2);
-      }
-    tc::cluster_sync();
+      for (int rk = 0; rk < kCS; ++rk)
+        tc::st_async_v2(tc::mapa(&cl_red[rank][rl], (uint32_t)rk), t1, t2, tc::mapa(&stats_bar, (uint32_t)rk));
+    tc::mbar_wait(&stats_bar, nstat & 1);
+    ++nstat;
     t1 = t2 = 0.f;
 #pragma unroll
     for (int rk = 0; rk < kCS; ++rk) {
-      t1 += cl_red[0][rk][rl];
-      t2 += cl_red[1][rk][rl];
+      t1 += cl_red[rk][rl].x;
+      t2 += cl_red[rk][rl].y;
     }
   };
   // both warps of pair q wrote the box: make it visible to the async proxy; the pair's first warp
   // then stores it to global memory and / or bulk-copies it to the 4 CTAs' next-layer A.
-  auto box_out = [&](uint8_t* slot, int omap, int col, bool bcast) {
+  // peers_only: the box already sits in this CTA's A (forward layers write their slice in
+  // place), so only the other kCS - 1 CTAs receive copies
+  auto box_out = [&](uint8_t* slot, int omap, int col, bool bcast, bool peers_only = false) {
     tc::fence_async_smem();
     tc::named_bar(1 + q, 64);
     if (hh == 0 && lane == 0) {
@@ -149,8 +158,9 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
       }
       if (bcast)
         for (int rk = 0; rk < kCS; ++rk)
-          tc::bulk_s2cluster(tc::mapa(A + rank * 16384 + q * 4096, (uint32_t)rk), slot, 4096,
-                             tc::mapa(&anext, (uint32_t)rk));
+          if (!peers_only || rk != rank)
+            tc::bulk_s2cluster(tc::mapa(A + rank * 16384 + q * 4096, (uint32_t)rk), slot, 4096,
+                               tc::mapa(&anext, (uint32_t)rk));
     }
   };
 
@@ -190,12 +200,17 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
       tc::mma_commit(&done);
     }
     stamp(3 + 4 * l);
-    if (tid == 0 && bcast) tc::mbar_expect_tx(&anext, kCS * 4 * 4096);  // before the stats barrier
+    // forward LayerNorm layers write their own slice in place: kCS - 1 incoming slices
+    const bool fwd_ln = epi == GE_LN_RELU || epi == GE_LN_TANH;
+    if (tid == 0 && bcast) tc::mbar_expect_tx(&anext, (fwd_ln ? kCS - 1 : kCS) * 4 * 4096);
     if (active && nreal > 0) {
       tc::mbar_wait(&done, l & 1);
       tc::fence_after_sync();
     }
     __syncthreads();  // s_bias / s_g / s_beta staged; layer l's MMAs done
+    // last layer: every copy into this CTA has landed; arrive now, wait at exit (all copies out of
+    // this CTA have then landed too)
+    if (l == nl - 1) tc::cluster_arrive_relaxed();
     stamp(4 + 4 * l);
     if (tid == 0 && l + 2 < nl && active_l(l + 2))  // layer l's B buffer is free: prefetch layer l + 2
       issue_b(b, P.L[l + 2], rank * P.L[l + 2].slice, sm + kBreg + (l & 1) * 32768, &bfull[l & 1]);
@@ -225,13 +240,16 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
         a[j] = x;
         v[j] = (epi == GE_LN_RELU) ? fmaxf(n, 0.f) : tanh_fast(n);
       }
-      uint8_t* sy = pslots;
+      // y straight into this CTA's slice (K block `rank`) of the next layer's A: this layer's MMA
+      // is done, and the stats exchange above proved every peer finished reading the previous
+      // broadcast of that slice
+      uint8_t* sy = A + rank * 16384 + q * 4096;
       uint8_t* sx = pslots + 4096;
-      if (l >= 1 && hh == 0 && lane == 0) tc::bulk_wait_read<0>();  // the pair's boxes of layer l-1
+      if (l >= 1 && hh == 0 && lane == 0) tc::bulk_wait_read<0>();  // the pair's stores of layer l-1
       tc::named_bar(1 + q, 64);
       box_put(sy, hh, v);
       if (L.xmap >= 0) box_put(sx, hh, a);
-      box_out(sy, L.omap, n0, bcast);
+      box_out(sy, L.omap, n0, bcast, true);
       if (L.xmap >= 0) box_out(sx, L.xmap, n0, false);
     } else if (epi == GE_BWD_LN_RELU || epi == GE_BWD_LN_TANH) {
       uint8_t* sl = pslots;
@@ -291,14 +309,17 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
           L.part[((int64_t)mt * 3 + kk) * L.N + n0 + c] = s;
         }
     } else if (epi == GE_BIAS_F32) {
-      if (hh == 0 && nreal > 0) {  // slice 32: one chunk
+      if (hh == 0 && nreal > 0) {  // slice 32: one chunk, stored row by row through a transpose tile
+        // staging in the idle B buffer (the last layer has no next weights)
+        float* T = reinterpret_cast<float*>(sm + kBreg + ((l + 1) & 1) * 32768) + q * 32 * 33;
         tc::tmem_ld32(trow, v);
-        if (rv) {
-          float* o = L.outf + (int64_t)r * L.ldf + n0;
+        __syncwarp();
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < nreal) o[j] = v[j] + s_bias[j];
-        }
+        for (int j = 0; j < 32; ++j) T[lane * 33 + j] = v[j] + s_bias[j];
+        __syncwarp();
+        const int nvr = min(32, P.M - row0);
+        if (lane < nreal)
+          for (int i = 0; i < nvr; ++i) L.outf[(int64_t)(row0 + i) * L.ldf + n0 + lane] = T[i * 33 + lane];
       }
     } else if (epi == GE_TG_FWD) {
       if (rank == 0 && hh == 0) {
@@ -339,8 +360,7 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
   }
   if (lane == 0) tc::bulk_wait_read<0>();
   tc::fence_before_sync();
-  __syncthreads();
-  tc::cluster_sync();  // every outgoing bulk copy has landed in its destination CTA
+  tc::cluster_wait();  // every outgoing bulk copy has landed in its destination CTA
   stamp(15);
   if (warp == 0) tc::tmem_dealloc(tmem, 64);
 }

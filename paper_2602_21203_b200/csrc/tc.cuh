@@ -248,5 +248,17 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// asynchronous 8-byte store into a cluster CTA's shared memory, completion (bytes) on that
+// CTA's mbarrier (both cluster addresses from mapa)
+__device__ __forceinline__ void st_async_v2(uint32_t dst, float a, float b, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(dst), "f"(a),
+               "f"(b), "r"(mbar)
+               : "memory");
+}
+// split cluster barrier: arrive (no memory ordering) now, wait later
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 }  // namespace tc
 }  // namespace sq
