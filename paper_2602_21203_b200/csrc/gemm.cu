@@ -68,16 +68,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   // pointer arithmetic on the __shared__ array (not integer casts) keeps the address space
   // known to the compiler (LDS/STS, no aliasing with global accesses)
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], done_bar, ld_bar[8];
+  __shared__ uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], done_bar, ld_bar[8], stats_bar;
   __shared__ uint32_t tmem_slot;
   __shared__ float red[2][2][128];
-  __shared__ float cl_red[2][4][128];  // per-row partials of each cluster CTA, pushed by the CTAs
+  __shared__ float2 cl_red[4][128];  // per-row (sum, sum of squares) of each cluster CTA, pushed by the CTAs
   __shared__ __align__(16) float s_bias[512], s_g[512], s_beta[512];  // per-column epilogue params
+  // This CTA's problem descriptor, copied once into shared memory: indexed reads of the large
+  // __grid_constant__ batch go through the constant cache and miss there (hundreds of cycles
+  // each, measured ~0.35 us per producer-loop iteration)
+  __shared__ __align__(16) GProb sP;
 
   const int tile = blockIdx.x;
   int pi = 0;
   while (pi + 1 < b.nprob && tile >= b.p[pi + 1].tile0) ++pi;
-  const GProb& P = b.p[pi];
+  {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(&b.p[pi]);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(&sP);
+    for (int i = threadIdx.x; i < (int)(sizeof(GProb) / 4); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const GProb& P = sP;
   const int lt = tile - P.tile0;
   const int mt = lt / P.tiles_n;
   const int m0 = mt * 128, n0 = (lt % P.tiles_n) * P.bn;
@@ -100,6 +110,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
       b.dbg[blockIdx.x * kDbgSlots + k] = t;
     }
   };
+  auto stamp_any = [&](int k) {  // recorded by the calling thread
+    if (b.dbg) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      b.dbg[blockIdx.x * kDbgSlots + k] = t;
+    }
+  };
   stamp(0);
 
   if (warp == 0) tc::tmem_alloc(&tmem_slot, ncols);
@@ -110,11 +127,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     }
     tc::mbar_init(&done_bar, 1);
     for (int i = 0; i < 8; ++i) tc::mbar_init(&ld_bar[i], 1);
+    tc::mbar_init(&stats_bar, 1);
     tc::fence_mbar_init();
   }
   if (warp == 2 && lane < P.nseg) {
     tc::tma_prefetch_desc(&b.maps[P.seg[lane].amap]);
     tc::tma_prefetch_desc(&b.maps[P.seg[lane].bmap]);
+  }
+  if (warp == 2 && lane >= 8 && lane < 11) {  // epilogue maps: a descriptor fetch on first use stalls the TMA queue
+    const int m = lane == 8 ? P.omap : (lane == 9 ? P.xmap : P.ymap);
+    if (m >= 0) tc::tma_prefetch_desc(&b.maps[m]);
   }
   if (ones && warp == 3) {
     // all elements 1.0 (so the swizzle is irrelevant); visible to the tensor core (async proxy)
@@ -123,7 +145,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     tc::fence_async_smem();
   }
   tc::fence_before_sync();
-  __syncthreads();
+  if (b.cs > 1) tc::cluster_sync();  // peers' stats_bar initialised before any st.async reaches it
+  else __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = tmem_slot;
   stamp(1);
@@ -151,6 +174,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   tc::pdl_wait();
   tc::pdl_trigger();
   stamp(2);
+  // LayerNorm backward: the pair's x_hat boxes (TMA) and the row's 1/sigma, fetched while the
+  // main loop runs (b.xpre_off: their shared-memory home past the operand ring)
+  float rs_pre = 0.f;
+  if constexpr (EPI == GE_BWD_LN_RELU || EPI == GE_BWD_LN_TANH) {
+    const int q0 = warp & 3, r0 = m0 + q0 * 32 + lane;
+    if (r0 < P.M) rs_pre = P.rstd[r0];
+    if (b.xpre_off && warp < 4 && lane == 0) {
+      const int ng = (nreal + 63) / 64;
+      uint8_t* xs = smem + b.xpre_off + q0 * 4 * kSlotBytes;
+      tc::mbar_expect_tx(&ld_bar[q0], ng * kSlotBytes);
+      for (int g = 0; g < ng; ++g) tc::tma_load_2d(xs + g * kSlotBytes, &b.maps[P.xmap], n0 + g * 64, m0 + q0 * 32, &ld_bar[q0]);
+      stamp(10);
+    }
+  }
   // per-column epilogue parameters -> smem (overlaps the main loop; read after the done barrier)
   if (warp >= 2) {
     for (int c = tid - 64; c < nt; c += kThreads - 64) {
@@ -178,7 +215,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
         const bool pre = kb < npre;  // B already in flight, transaction bytes already expected
         if (!pre) tc::mbar_expect_tx(&full_bar[st], kABytes + geo.bbytes);
         const int kc = 64 * l;
-        if (!G.a_mn) {
+        if (b.mcast) {
+          // the cluster's CTAs share the A tile: K block kb is fetched once, by rank kb % cs, for all
+          if (kb % b.cs == (int)(blockIdx.x % b.cs)) {
+            const uint16_t mask = (uint16_t)((1u << b.cs) - 1u);
+            if (!G.a_mn) {
+              tc::tma_load_2d_mc(As, am, G.a_k + kc, P.a_m + m0, &full_bar[st], mask);
+            } else {
+              tc::tma_load_2d_mc(As, am, P.a_m + m0, G.a_k + kc, &full_bar[st], mask);
+              tc::tma_load_2d_mc(As + 8192, am, P.a_m + m0 + 64, G.a_k + kc, &full_bar[st], mask);
+            }
+          }
+        } else if (!G.a_mn) {
           tc::tma_load_2d(As, am, G.a_k + kc, P.a_m + m0, &full_bar[st]);
         } else {
           tc::tma_load_2d(As, am, P.a_m + m0, G.a_k + kc, &full_bar[st]);
@@ -190,8 +238,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
           else
             tc::tma_load_2d(Bs + i * 8192, bm, P.b_n + n0 + 64 * i, G.b_k + kc, &full_bar[st]);
         }
+        // if (kb < 4) stamp(12 + kb);
       }
     }
+    stamp_any(11);
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
     int kb = 0;
@@ -203,6 +253,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
       for (int l = 0; l < G.nkb; ++l, ++kb) {
         const int st = kb % S;
         tc::mbar_wait(&full_bar[st], (kb / S) & 1);
+        if (kb == 0) stamp_any(8);
+        stamp_any(9);
         tc::fence_after_sync();
         const uint32_t a0 = tc::smem_u32(smem + st * b.stage_bytes), b0 = a0 + kABytes;
 #pragma unroll
@@ -224,9 +276,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     tc::mma_commit(&done_bar);
   }
   __syncwarp();
-  tc::mbar_wait(&done_bar, 0);
+  // one poller: 256 threads spinning in try_wait compete with the TMA's complete_tx traffic on
+  // the shared-memory barrier unit; the rest wait in bar.sync
+  if (tid == 0) tc::mbar_wait(&done_bar, 0);
+  __syncthreads();  // MMAs done; s_bias / s_g / s_beta visible
   tc::fence_after_sync();
-  __syncthreads();  // s_bias / s_g / s_beta visible
   stamp(3);
 
   // ---------------- epilogue ----------------
@@ -247,7 +301,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   // the CTAs of the cluster.  Push model: every CTA stores its row partials into each peer's
   // cl_red[k][rank] (distributed shared memory), one cluster barrier, then local reads summed in
   // rank order (every CTA gets the same bits; no remote access after the barrier).
+  // (st.async into every cluster CTA's cl_red[rank], completion counted on its stats_bar; the
+  // receiver sums the cs entries in rank order: every CTA gets the same bits, no cluster barrier)
   auto row_total2 = [&](float p1, float p2, float& t1, float& t2) {
+    if (b.cs > 1 && tid == 0) tc::mbar_expect_tx(&stats_bar, b.cs * 128 * 8);
     red[0][hh][rl] = p1;
     red[1][hh][rl] = p2;
     __syncthreads();
@@ -256,15 +313,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     if (b.cs > 1) {
       const uint32_t me = (uint32_t)(blockIdx.x % b.cs);
       if (hh == 0)
-        for (int rk = 0; rk < b.cs; ++rk) {
-          tc::dsmem_st(&cl_red[0][me][rl], (uint32_t)rk, t1);
-          tc::dsmem_st(&cl_red[1][me][rl], (uint32_t)rk, t2);
-        }
-      tc::cluster_sync();
+        for (int rk = 0; rk < b.cs; ++rk)
+          tc::st_async_v2(tc::mapa(&cl_red[me][rl], (uint32_t)rk), t1, t2, tc::mapa(&stats_bar, (uint32_t)rk));
+      tc::mbar_wait(&stats_bar, 0);
       t1 = t2 = 0.f;
       for (int rk = 0; rk < b.cs; ++rk) {
-        t1 += cl_red[0][rk][rl];
-        t2 += cl_red[1][rk][rl];
+        t1 += cl_red[rk][rl].x;
+        t2 += cl_red[rk][rl].y;
       }
     }
   };
@@ -385,22 +440,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     }
   } else if constexpr (EPI == GE_BWD_LN_RELU || EPI == GE_BWD_LN_TANH) {
     float* colacc = reinterpret_cast<float*>(smem + kColaccOff);  // [4][3][512]
-    // the pair's x_hat boxes (<= 4) by TMA on one transaction barrier
-    if (hh == 0 && lane == 0) {
+    // the pair's x_hat boxes (<= 4) by TMA on one transaction barrier (prefetched when possible)
+    uint8_t* xs = b.xpre_off ? smem + b.xpre_off + q * 4 * kSlotBytes : pslots;
+    if (!b.xpre_off && hh == 0 && lane == 0) {
       tc::mbar_expect_tx(&ld_bar[q], ngrp * kSlotBytes);
       for (int g = 0; g < ngrp; ++g)
-        tc::tma_load_2d(pslots + g * kSlotBytes, &b.maps[P.xmap], n0 + g * 64, row0, &ld_bar[q]);
+        tc::tma_load_2d(xs + g * kSlotBytes, &b.maps[P.xmap], n0 + g * 64, row0, &ld_bar[q]);
     }
     tc::mbar_wait(&ld_bar[q], 0);
     stamp(5);
+    // pass 1: dn = dL/d(g x_hat + beta) through the activation, the row sums of dxh = dn g and
+    // dxh x_hat, column partials of dn x_hat and dn.  With one 64-column group the warp keeps
+    // (dn, x_hat) in v / a for pass 2.
     float s1 = 0.f, s2 = 0.f;
     for (int g = 0; g < ngrp; ++g) {
       const int ch = 2 * g + hh;
       if (ch < nch) {
         const int c0 = ch * 32, ncv = min(32, nreal - c0);
         tc::tmem_ld32(trow + ch * 32, v);
-        if (g == 0) stamp(8);
-        box_get(pslots + g * kSlotBytes, hh, a);
+        box_get(xs + g * kSlotBytes, hh, a);
         float pg[32], pb[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -414,47 +472,50 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
           s2 += dxh * x;
           pg[j] = dn * x;
           pb[j] = dn;
+          v[j] = dn;
+          a[j] = x;
         }
-        if (g == 0) stamp(9);
         const float cg = colsum32(pg);
         const float cb = colsum32(pb);
-        if (g == 0) stamp(10);
         colacc[(q * 3 + 1) * 512 + c0 + lane] = cg;
         colacc[(q * 3 + 2) * 512 + c0 + lane] = cb;
       }
     }
     float m1, m2;
-    stamp(11);
     row_total2(s1, s2, m1, m2);
     stamp(6);
     m1 /= (float)N;
     m2 /= (float)N;
-    const float rs = rv ? P.rstd[r] : 0.f;
+    const float rs = rv ? rs_pre : 0.f;
     for (int g = 0; g < ngrp; ++g) {
-      uint8_t* sl = pslots + g * kSlotBytes;
+      uint8_t* sl = xs + g * kSlotBytes;
       const int ch = 2 * g + hh;
       if (ch < nch) {
         const int c0 = ch * 32, ncv = min(32, nreal - c0);
-        tc::tmem_ld32(trow + ch * 32, v);
-        box_get(sl, hh, a);
+        if (ngrp > 1) {  // recompute (dn, x_hat) of this group
+          tc::tmem_ld32(trow + ch * 32, v);
+          box_get(sl, hh, a);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int cc = c0 + j;
+            const bool ok = rv && (j < ncv);
+            const float x = ok ? a[j] : 0.f;
+            const float n = fmaf(x, s_g[cc], s_beta[cc]);
+            v[j] = ok ? ((EPI == GE_BWD_LN_RELU) ? (n > 0.f ? v[j] : 0.f) : v[j] * sech2_fast(n)) : 0.f;
+            a[j] = x;
+          }
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const int cc = c0 + j;
           const bool ok = rv && (j < ncv);
-          const float x = ok ? a[j] : 0.f;
-          const float n = fmaf(x, s_g[cc], s_beta[cc]);
-          const float dn = ok ? ((EPI == GE_BWD_LN_RELU) ? (n > 0.f ? v[j] : 0.f) : v[j] * sech2_fast(n)) : 0.f;
-          v[j] = ok ? rs * (dn * s_g[cc] - m1 - x * m2) : 0.f;
+          v[j] = ok ? rs * (v[j] * s_g[c0 + j] - m1 - a[j] * m2) : 0.f;
           a[j] = v[j];
         }
-        if (g == 0) stamp(12);
         box_put(sl, hh, v);
         const float cx = colsum32(a);
         colacc[(q * 3 + 0) * 512 + c0 + lane] = cx;
-        if (g == 0) stamp(13);
       }
       pair_store(sl, &b.maps[P.omap], n0 + g * 64, row0, q, hh);
-      if (g == 0) stamp(14);
     }
     __syncthreads();
     if (P.part) {
@@ -719,7 +780,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_sk(const __grid_constant__
     tc::mma_commit(&done_bar);
   }
   __syncwarp();
-  tc::mbar_wait(&done_bar, 0);
+  if (tid == 0) tc::mbar_wait(&done_bar, 0);
+  __syncthreads();
   tc::fence_after_sync();
   stamp(3);
 
@@ -1050,6 +1112,8 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   if (b.nprob == 0) return 0;
   // plan tiles.  LayerNorm epilogues need whole rows: with N >= 128 the row is split over a
   // cluster of cs CTAs of 64-column multiples (more SMs share the epilogue work).
+  static const bool no_pre = getenv("SQUINT_NO_PREFETCH_B") != nullptr;
+  if (no_pre) b.prefetch_b = 0;
   const int epi0 = b.p[0].epi;
   const bool ln_launch = epi0 == GE_LN_RELU || epi0 == GE_LN_TANH || epi0 == GE_BWD_LN_RELU || epi0 == GE_BWD_LN_TANH;
   b.cs = 1;
@@ -1118,6 +1182,12 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   S = S < 2 ? 2 : S;
   if ((size_t)S * b.stage_bytes > 200 * 1024) return -1;
   b.nstages = S;
+  // A multicast across a LayerNorm cluster (its CTAs share the rows): only without ring reuse,
+  // so no stage is refilled before every CTA's MMAs consumed it
+  {
+    static const bool no_mc = getenv("SQUINT_NO_MCAST") != nullptr;
+    b.mcast = (!no_mc && b.cs > 1 && b.ks == 1 && maxkb <= S) ? 1 : 0;
+  }
   // tensor maps
   b.nmaps = 0;
   for (int i = 0; i < b.nprob; ++i) {
@@ -1161,6 +1231,20 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     smem = kEpiBytes;
   }
   if (b.p[0].epi == GE_DW) smem += 2048;  // ones tile (bias gradients)
+  // LayerNorm backward: x_hat boxes prefetched past the ring when they fit
+  b.xpre_off = 0;
+  if (b.ks == 1 && (b.p[0].epi == GE_BWD_LN_RELU || b.p[0].epi == GE_BWD_LN_TANH)) {
+    int ng = 0;
+    for (int i = 0; i < b.nprob; ++i) {
+      const int g = (b.p[i].bn + 63) / 64;
+      ng = g > ng ? g : ng;
+    }
+    const size_t xb = (size_t)4 * 4 * 4096;  // 4 pairs x (up to) 4 boxes
+    if (ng <= 4 && smem + xb + 1024 <= 227 * 1024) {
+      b.xpre_off = (int)smem;
+      smem += xb;
+    }
+  }
   smem += 1024;
   const int epi = b.p[0].epi;
   for (int i = 1; i < b.nprob; ++i)

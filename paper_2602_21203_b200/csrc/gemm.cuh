@@ -97,6 +97,8 @@ struct GBatch {
   int cs;  // cluster size: LayerNorm rows split over cs CTAs (statistics exchanged through DSMEM)
   int ks;  // split-K cluster size (k_gemm_sk; set by gemm_launch): bwd-LN column partials are
            // then written per 128 / ks rows, [mtiles * ks][3][N]
+  int mcast;       // cluster CTAs share the A tile: each K block is loaded once and multicast
+  int xpre_off;    // LayerNorm backward: smem offset of the prefetched x_hat boxes (0: loaded after the main loop)
   int prefetch_b;  // 1: B operands may be loaded before griddepcontrol.wait (not written by the
                    // immediately preceding kernel); set through GemmBuilder::prefetch_b
   unsigned long long* dbg;  // optional per-CTA phase timestamps (globaltimer ns) [tile][8]

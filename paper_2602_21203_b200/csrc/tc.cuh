@@ -156,6 +156,17 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* map, int
       : "memory");
 }
 
+// 2D tile load multicast to the cluster CTAs in `mask`: the box lands at the same shared-memory
+// offset in each of them and completes bytes on each one's mbarrier at the offset of `bar`
+__device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const void* map, int c0, int c1, uint64_t* bar,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, "
+      "{%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+
 // smem -> global tensor store (bulk-group completion), and the group bookkeeping
 __device__ __forceinline__ void tma_store_2d(const void* map, void* smem_src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(

@@ -34,7 +34,9 @@ namespace sq {
 
 namespace {
 
-inline int ld8(int x) { return (x + 7) & ~7; }
+// row pitch of the bf16 workspace matrices and weight shadows: 128 bytes (64 elements), so every
+// TMA box row starts on a 128-byte line (unaligned pitches cost ~30-40 % of the TMA rate)
+inline int ldp(int x) { return (x + 63) & ~63; }
 inline int mtiles(int m) { return (m + 127) / 128; }
 
 struct BM {  // bf16 matrix inside the workspace
@@ -78,7 +80,7 @@ ShadowPlan shadow_plan(WsPlan& P, const squint_dims& d, const Layout& L, int grp
       x.src = t.off;
       x.rows = t.shape[0];
       x.cols = t.shape[1];
-      x.ld = ld8(x.cols);
+      x.ld = ldp(x.cols);
       x.dst = (int64_t)e;
       x.perm_c = perm ? C : 0;
       x.perm_p = perm ? P2 : 0;
@@ -108,7 +110,7 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
   const int nq = Lt + d.proprio_dim + A, npi = Lt + d.proprio_dim;
   const size_t f = sizeof(float);
   auto bm = [&](int rows, int cols) {
-    BM m{0, rows, cols, ld8(cols)};
+    BM m{0, rows, cols, ldp(cols)};
     m.off = P.take((size_t)rows * m.ld * 2);
     return m;
   };
@@ -1011,10 +1013,10 @@ size_t bf16_act_workspace_bytes(const squint_dims& d, int64_t n) {
   Layout L = make_layout(d);
   WsPlan P;
   const int F = flat_dim(d), npi = d.latent + d.proprio_dim, Ha = d.actor_hidden;
-  P.take((size_t)n * ld8(F) * 2);
-  P.take((size_t)n * ld8(npi) * 2);
-  P.take((size_t)n * ld8(Ha) * 2);
-  P.take((size_t)n * ld8(Ha) * 2);
+  P.take((size_t)n * ldp(F) * 2);
+  P.take((size_t)n * ldp(npi) * 2);
+  P.take((size_t)n * ldp(Ha) * 2);
+  P.take((size_t)n * ldp(Ha) * 2);
   shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
   P.take(conv_tiles_bytes(d.conv_ch));
   return P.top + 256;
@@ -1030,10 +1032,10 @@ squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const flo
   WsPlan P;
   const int F = flat_dim(d), Lt = d.latent, npi = Lt + d.proprio_dim, Ha = d.actor_hidden, M = (int)n;
   char* ws = reinterpret_cast<char*>(workspace);
-  BM Xh{P.take((size_t)n * ld8(F) * 2), M, F, ld8(F)};
-  BM Xa{P.take((size_t)n * ld8(npi) * 2), M, npi, ld8(npi)};
-  BM H1{P.take((size_t)n * ld8(Ha) * 2), M, Ha, ld8(Ha)};
-  BM H2{P.take((size_t)n * ld8(Ha) * 2), M, Ha, ld8(Ha)};
+  BM Xh{P.take((size_t)n * ldp(F) * 2), M, F, ldp(F)};
+  BM Xa{P.take((size_t)n * ldp(npi) * 2), M, npi, ldp(npi)};
+  BM H1{P.take((size_t)n * ldp(Ha) * 2), M, Ha, ldp(Ha)};
+  BM H2{P.take((size_t)n * ldp(Ha) * 2), M, Ha, ldp(Ha)};
   ShadowPlan sp = shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
   uint8_t* wtiles = reinterpret_cast<uint8_t*>(ws + P.take(conv_tiles_bytes(d.conv_ch)));
   Ctx c{d, L, ws, s, false, false, nullptr};
