@@ -477,6 +477,7 @@ static squint_status update_one(const Ctx& c, const squint_replay& R, const int6
   {
     PhaseScope ps(11, rep, s);
     ScalarsArgs a;
+    memset(&a, 0, sizeof(a));
     a.B = B;
     a.inv_btotal = inv_btotal;
     a.logp = c.F(w.logp_cur);

@@ -38,6 +38,10 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
 
 constexpr int kWarp = 32;
 
+// Adam bias correction 1 / (1 - beta^t) = -1 / expm1(t ln(beta)), ln(beta) = log1p(beta - 1)
+// (beta - 1 exact): float, no cancellation
+SQ_DEV float bias_corr(float beta, int64_t t) { return -1.f / expm1f((float)t * log1pf(beta - 1.f)); }
+
 SQ_DEV float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

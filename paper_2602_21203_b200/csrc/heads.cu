@@ -11,6 +11,7 @@
 
 #include "common.cuh"
 #include "heads.cuh"
+#include "optim.cuh"
 
 namespace sq {
 
@@ -29,6 +30,13 @@ __global__ void __launch_bounds__(256) k_target_ce(const __grid_constant__ Targe
   float* pb = sm + w * 2 * N;  // pbar [N]
   float* bj = pb + N;          // b_j [N]
   const int row = blockIdx.x * kRows + w;
+  if (a.step && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t tc = ++a.step[0], ta = ++a.step[1];
+    a.scal[S_C1_CRITIC] = bias_corr(a.beta1, tc);
+    a.scal[S_C2_CRITIC] = bias_corr(a.beta2, tc);
+    a.scal[S_C1_ACTOR] = bias_corr(a.beta1, ta);
+    a.scal[S_C2_ACTOR] = bias_corr(a.beta2, ta);
+  }
   if (row >= a.B) return;
   const int64_t ridx = a.idx[row];
   float tl[2][NPL], ol[2][NPL];

@@ -21,6 +21,11 @@ struct TargetCEArgs {
   __nv_bfloat16* dlogits_bf;  // ... or bf16 [2][B][ld_dl] (bf16 path; used when non-NULL)
   int ld_dl;
   float* row_loss;         // [B]
+  // optional (step != NULL): block 0 takes the critic and actor Adam steps, step[0..1] += 1, and
+  // writes their bias corrections into scal (so the optimizers need not wait for the alpha step)
+  int64_t* step;
+  float* scal;
+  float beta1, beta2;
 };
 
 struct ActorQArgs {

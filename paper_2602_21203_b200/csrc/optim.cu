@@ -30,9 +30,6 @@ __global__ void __launch_bounds__(256) k_row_sums(const float* __restrict__ logp
   }
 }
 
-// Adam bias correction 1 / (1 - beta^t) = -1 / expm1(t ln(beta)), ln(beta) = log1p(beta - 1)
-// (beta - 1 exact): float, no cancellation
-__device__ __forceinline__ float bias_corr(float beta, int64_t t) { return -1.f / expm1f((float)t * log1pf(beta - 1.f)); }
 
 __global__ void __launch_bounds__(256) k_scalars(const __grid_constant__ ScalarsArgs a) {
   grid_wait();
@@ -75,6 +72,7 @@ __global__ void __launch_bounds__(256) k_scalars(const __grid_constant__ Scalars
   a.scal[S_MEAN_LOGP] = mean_logp;
   a.scal[S_LALPHA] = loss;
   a.scal[S_LQ] = sq;
+  if (a.steps_done) return;  // critic / actor steps and corrections already taken (k_target_ce)
   const int64_t tc = ++a.step[0], ta = ++a.step[1];
   a.scal[S_C1_CRITIC] = bias_corr(a.beta1, tc);
   a.scal[S_C2_CRITIC] = bias_corr(a.beta2, tc);
@@ -318,6 +316,43 @@ __global__ void __launch_bounds__(256) k_polyak_sh(float4* __restrict__ t4, cons
 }
 
 }  // namespace
+
+// up to three (master, table) pairs in one launch (blockIdx.y = pair)
+struct ShadowJobs {
+  const float* master[3];
+  ShadowTable t[3];
+};
+__global__ void __launch_bounds__(256) k_shadow3(const __grid_constant__ ShadowJobs j) {
+  grid_wait();
+  grid_trigger();
+  const ShadowTable& t = j.t[blockIdx.y];
+  const float* __restrict__ master = j.master[blockIdx.y];
+  for (int k = 0; k < t.n; ++k) {
+    const ShadowEnt& e = t.e[k];
+    const int n = e.rows * e.cols;
+    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < n; l += gridDim.x * blockDim.x) {
+      const int row = l / e.cols, col = l - row * e.cols;
+      int cc = col;
+      if (e.perm_c > 0) {
+        const int ch = col / e.perm_p, pix = col - ch * e.perm_p;
+        cc = pix * e.perm_c + ch;
+      }
+      t.base[(int)e.dst + row * e.ld + cc] = __float2bfloat16_rn(master[e.src + l]);
+    }
+  }
+}
+
+int launch_shadow3(const float* const master[3], const ShadowTable* const t[3], cudaStream_t s) {
+  ShadowJobs j;
+  memset(&j, 0, sizeof(j));
+  for (int i = 0; i < 3; ++i) {
+    j.master[i] = master[i];
+    if (t[i]) j.t[i] = *t[i];
+  }
+  note_launch(s, "k_shadow", 0, 0);
+  launch_pdl(k_shadow3, dim3(148, 3), dim3(256), 0, s, j);
+  return (int)cudaGetLastError();
+}
 
 int launch_shadow(const float* master, const ShadowTable& t, cudaStream_t s) {
   if (t.n == 0) return 0;

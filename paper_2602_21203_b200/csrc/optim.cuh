@@ -31,6 +31,7 @@ struct ScalarsArgs {
   float lr_alpha, beta1, beta2, adam_eps, target_entropy;
   float loss_scale;      // 1 / global batch
   float* scal;           // [kScal]
+  int steps_done;        // 1: step[0], step[1] and their bias corrections were taken earlier
 };
 
 int launch_row_sums(const float* logp, const float* row_loss, int B, float* extras, cudaStream_t s);
@@ -63,6 +64,8 @@ struct ShadowTable {
 };
 // Full refresh of one group's shadow from its fp32 master.
 int launch_shadow(const float* master, const ShadowTable& t, cudaStream_t s);
+// the three group shadows in one launch (a NULL table is skipped)
+int launch_shadow3(const float* const master[3], const ShadowTable* const t[3], cudaStream_t s);
 // Adam (as launch_adam) that also writes the updated weights' bf16 shadow (t may be NULL).
 // `base` = flat group index of p[0] (shadow lookups), `nblocks` = grid (= partial sums written).
 // grad_perm: gradients of permuted shadow entries (the projection weight) are stored in the

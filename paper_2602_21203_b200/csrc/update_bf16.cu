@@ -208,12 +208,13 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
 // nodes) while the actor-loss chain proceeds; the branch joins before the metrics kernel.
 struct Aux {
   cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, scal = nullptr, join = nullptr;
+  cudaEvent_t fork = nullptr, scal = nullptr, join = nullptr, alpha = nullptr;
   bool ok() {
     if (s) return true;
     return cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
            cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&scal, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&alpha, cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
   }
 };
@@ -399,7 +400,10 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
   // a3-a5: gather + shift + encoder (obs, next_obs); replay rows of s, a, s' into the layer
   // input matrices
   uint8_t* wtiles = reinterpret_cast<uint8_t*>(c.ws + w.wtiles);
-  BF_CK(launch_conv_tiles(crit + L.off(gC, "enc.conv1.w"), crit + L.off(gC, "enc.conv2.w"), C, wtiles, s));
+  // conv weight tiles: with the auxiliary branch they were written at the end of the previous
+  // update's branch (or by the call prologue)
+  const bool branch = comm == nullptr && c.aux != nullptr;
+  if (!branch) BF_CK(launch_conv_tiles(crit + L.off(gC, "enc.conv1.w"), crit + L.off(gC, "enc.conv2.w"), C, wtiles, s));
   {
     PhaseScope ps(3, rep, s);
     EncFwdArgs e;
@@ -594,6 +598,11 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     t.dlogits_bf = c.bp(w.dlog);
     t.ld_dl = w.dlog.ld;
     t.row_loss = c.F(w.row_loss);
+    // the critic / actor Adam steps and bias corrections (the alpha step runs later)
+    t.step = st.step;
+    t.scal = c.F(w.scal);
+    t.beta1 = hp.beta1;
+    t.beta2 = hp.beta2;
     BF_CK(launch_target_ce(t, s));
   }
   // a10: critic backward: heads -> critic projection -> ReLU'(conv2)
@@ -644,11 +653,41 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
   // encoder backward (dh GEMM + conv backward): on the auxiliary branch when single-GPU
   // (overlaps the critic dW GEMM and the actor-loss chain), inline when the gradients are
   // all-reduced
-  const bool branch = comm == nullptr && c.aux != nullptr;
   cudaStream_t es = branch ? c.aux->s : s;
+  float* extras = gc + L.gsize[gC];
+  float* scal = c.F(w.scal);
+  auto scalars = [&](cudaStream_t ss) -> squint_status {
+    // a11 temperature step (Q17) from the row sums
+    ScalarsArgs a;
+    memset(&a, 0, sizeof(a));
+    a.B = B;
+    a.inv_btotal = inv_btotal;
+    a.logp = c.F(w.logp_cur);
+    a.row_loss = c.F(w.row_loss);
+    a.extras = extras;
+    a.compute_sums = comm ? 0 : 1;
+    a.log_alpha = st.log_alpha;
+    a.m_alpha = st.m_alpha;
+    a.v_alpha = st.v_alpha;
+    a.step = st.step;
+    a.lr_alpha = hp.lr_alpha;
+    a.beta1 = hp.beta1;
+    a.beta2 = hp.beta2;
+    a.adam_eps = hp.adam_eps;
+    a.target_entropy = hp.target_entropy;
+    a.loss_scale = inv_btotal;
+    a.scal = scal;
+    a.steps_done = 1;
+    BF_CK(launch_scalars(a, ss));
+    return SQUINT_OK;
+  };
   if (branch) {
     BF_CK(cudaEventRecord(c.aux->fork, s));
     BF_CK(cudaStreamWaitEvent(es, c.aux->fork, 0));
+    // the alpha step first on the branch: only the actor loss (k_actor_q) waits for it
+    squint_status r = scalars(es);
+    if (r != SQUINT_OK) return r;
+    BF_CK(cudaEventRecord(c.aux->alpha, es));
   }
   {
     // dh = dAp Wp, masked by ReLU'(conv2) (h > 0), HWC
@@ -704,8 +743,6 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     pp.part_tiles = mt * ks_pq;
     BF_CK(gemm_launch(gb, s));
   }
-  float* extras = gc + L.gsize[gC];
-  float* scal = c.F(w.scal);
   if (comm) {
     BF_CK(launch_row_sums(c.F(w.logp_cur), c.F(w.row_loss), B, extras, s));
     if (comm_allreduce_sum(comm, gc, L.gsize[gC] + kExtra, s) != 0) return set_error(SQUINT_ENCCL, comm_error());
@@ -714,26 +751,10 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
   // a11 temperature step + Adam bias corrections; a13 Adam on the critic group (+ shadow)
   {
     PhaseScope ps(11, rep, s);
-    ScalarsArgs a;
-    memset(&a, 0, sizeof(a));
-    a.B = B;
-    a.inv_btotal = inv_btotal;
-    a.logp = c.F(w.logp_cur);
-    a.row_loss = c.F(w.row_loss);
-    a.extras = extras;
-    a.compute_sums = comm ? 0 : 1;
-    a.log_alpha = st.log_alpha;
-    a.m_alpha = st.m_alpha;
-    a.v_alpha = st.v_alpha;
-    a.step = st.step;
-    a.lr_alpha = hp.lr_alpha;
-    a.beta1 = hp.beta1;
-    a.beta2 = hp.beta2;
-    a.adam_eps = hp.adam_eps;
-    a.target_entropy = hp.target_entropy;
-    a.loss_scale = inv_btotal;
-    a.scal = scal;
-    BF_CK(launch_scalars(a, s));
+    if (!branch) {
+      squint_status r = scalars(s);
+      if (r != SQUINT_OK) return r;
+    }
     if (branch) {
       // heads + projection on the main stream (the actor loss needs theta+ of those only), the
       // encoder slice on the branch once its gradient is reduced
@@ -746,6 +767,10 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       BF_CK(launch_adam_shadow(st.critic, gc, st.m_critic, st.v_critic, e0, hp.lr_critic, hp.beta1, hp.beta2,
                                hp.adam_eps, scal + S_C1_CRITIC, scal + S_C2_CRITIC, c.F(w.adam_part) + kAdamBlocks,
                                nullptr, es, 0, kEncAdamBlocks));
+      // a14 Polyak (needs only theta+ of the heads and projection) and the next update's conv
+      // weight tiles (needs the stepped encoder) on the branch as well
+      BF_CK(launch_polyak_shadow(st.critic_target, st.critic + L.enc_end, L.gsize[gT], hp.tau, &shT, es));
+      BF_CK(launch_conv_tiles(crit + L.off(gC, "enc.conv1.w"), crit + L.off(gC, "enc.conv2.w"), C, wtiles, es));
       BF_CK(cudaEventRecord(c.aux->join, es));
     } else {
       BF_CK(launch_adam_shadow(st.critic, gc, st.m_critic, st.v_critic, L.gsize[gC], hp.lr_critic, hp.beta1,
@@ -817,6 +842,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     q.ld_dl = w.dlog1.ld;
     q.row_q = c.F(w.row_q);
     q.row_lpi = c.F(w.row_lpi);
+    if (branch) BF_CK(cudaStreamWaitEvent(s, c.aux->alpha, 0));  // alpha+ from the branch
     BF_CK(launch_actor_q(q, s));
   }
   {
@@ -926,7 +952,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
   BF_CK(launch_adam_shadow(st.actor, ga, st.m_actor, st.v_actor, L.gsize[gA], hp.lr_actor, hp.beta1, hp.beta2,
                            hp.adam_eps, scal + S_C1_ACTOR, scal + S_C2_ACTOR, nullptr, &shA, s, 0, kAdamBlocks, 1));
   // a14: Polyak over every critic tensor except the encoder (+ target shadow)
-  BF_CK(launch_polyak_shadow(st.critic_target, st.critic + L.enc_end, L.gsize[gT], hp.tau, &shT, s));
+  if (!branch) BF_CK(launch_polyak_shadow(st.critic_target, st.critic + L.enc_end, L.gsize[gT], hp.tau, &shT, s));
   if (branch) BF_CK(cudaStreamWaitEvent(s, c.aux->join, 0));  // join the encoder branch
   {
     MetricsArgs m;
@@ -996,10 +1022,18 @@ squint_status bf16_update(const squint_dims& d, const squint_hparams& hp, const 
         (!no_branch && g_branch_enabled && t_aux.ok()) ? &t_aux : nullptr};
   const int nranks = comm ? comm_nranks(comm) : 1;
   const float inv_btotal = 1.0f / ((float)d.batch * (float)nranks);
-  // bf16 shadows of the current master weights
-  BF_CK(launch_shadow(st.critic, table_at(c, w.sh[0]), s));
-  BF_CK(launch_shadow(st.critic_target, table_at(c, w.sh[1]), s));
-  BF_CK(launch_shadow(st.actor, table_at(c, w.sh[2]), s));
+  // bf16 shadows of the current master weights (and the conv weight tiles, which with the
+  // auxiliary branch are otherwise produced at the end of the previous update)
+  {
+    const ShadowTable t0 = table_at(c, w.sh[0]), t1 = table_at(c, w.sh[1]), t2 = table_at(c, w.sh[2]);
+    const float* const masters[3] = {st.critic, st.critic_target, st.actor};
+    const ShadowTable* const tabs[3] = {&t0, &t1, &t2};
+    BF_CK(launch_shadow3(masters, tabs, s));
+    if (comm == nullptr && c.aux != nullptr)
+      BF_CK(launch_conv_tiles(st.critic + L.off(SQUINT_GROUP_CRITIC, "enc.conv1.w"),
+                              st.critic + L.off(SQUINT_GROUP_CRITIC, "enc.conv2.w"), d.conv_ch,
+                              reinterpret_cast<uint8_t*>(c.ws + w.wtiles), s));
+  }
   const size_t B = d.batch, A = d.action_dim;
   for (int j = 0; j < utd; ++j) {
     squint_status r = update_one(c, w, hp, R, idx + j * B, shifts + j * B * 4, eps + j * 2 * B * A, st, metrics + j * 8,
