@@ -47,7 +47,8 @@ __device__ __forceinline__ void issue_b(const CBatch& b, const CLayer& L, int n0
 __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatch b) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t aload, bfull[2], done, anext, ld_bar[4], stats_bar;
+  __shared__ uint64_t aload, bfull[2], done, anext, ld_bar[8], stats_bar;
+  __shared__ float s_rs[kChainMaxLayers][128];  // backward LayerNorm layers: 1/sigma of the tile rows
   __shared__ uint32_t tmem_slot;
   __shared__ float red[2][2][128];
   __shared__ float2 cl_red[kCS][128];  // per-row (sum, sum of squares) partials pushed by each CTA
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
     tc::mbar_init(&bfull[1], 1);
     tc::mbar_init(&done, 1);
     tc::mbar_init(&anext, 1);
-    for (int i = 0; i < 4; ++i) tc::mbar_init(&ld_bar[i], 1);
+    for (int i = 0; i < 8; ++i) tc::mbar_init(&ld_bar[i], 1);
     tc::mbar_init(&stats_bar, 1);
     tc::fence_mbar_init();
   }
@@ -102,6 +103,21 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
   }
   tc::pdl_wait();
   tc::pdl_trigger();
+  // backward LayerNorm layers: x_hat boxes of the first two layers (TMA, one barrier per layer
+  // parity and warp pair) and every layer's 1/sigma, fetched while the first A / MMA proceed
+  auto bwd_l = [&](int l) { return P.L[l].epi == GE_BWD_LN_RELU || P.L[l].epi == GE_BWD_LN_TANH; };
+  auto issue_xhat = [&](int l) {  // by the warp pair's leader
+    const int qq = warp & 3;
+    tc::mbar_expect_tx(&ld_bar[(l & 1) * 4 + qq], 4096);
+    tc::tma_load_2d(sm + kSlots + qq * 16384 + (l & 1) * 8192, &b.maps[P.L[l].xmap], rank * P.L[l].slice, m0 + qq * 32,
+                    &ld_bar[(l & 1) * 4 + qq]);
+  };
+  if (warp < 4 && lane == 0)
+    for (int l = 0; l < nl && l < 2; ++l)
+      if (bwd_l(l)) issue_xhat(l);
+  if (warp < 4)
+    for (int l = 0; l < nl; ++l)
+      if (bwd_l(l)) s_rs[l][rl] = rv ? P.L[l].rstd[r] : 0.f;
   if (tid == 0) {
     if (!b.prefetch_b) {
       issue_b(b, P.L[0], rank * P.L[0].slice, sm + kBreg, &bfull[0]);
@@ -117,7 +133,6 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
   uint8_t* pslots_base = sm + kSlots + q * 16384;
   float* colacc = reinterpret_cast<float*>(sm + kColacc);
   const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-  int nbwd = 0;  // backward layers so far (x_hat load barrier phase)
 
   // Row totals over the cluster: each CTA pushes its per-row partials into every CTA's cl_red
   // with st.async (completion counted on the receiver's stats_bar), then sums the kCS entries in
@@ -201,8 +216,8 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
     }
     stamp(3 + 4 * l);
     // forward LayerNorm layers write their own slice in place: kCS - 1 incoming slices
-    const bool fwd_ln = epi == GE_LN_RELU || epi == GE_LN_TANH;
-    if (tid == 0 && bcast) tc::mbar_expect_tx(&anext, (fwd_ln ? kCS - 1 : kCS) * 4 * 4096);
+    // LayerNorm layers (forward and backward) write their own slice in place: kCS - 1 incoming
+    if (tid == 0 && bcast) tc::mbar_expect_tx(&anext, (kCS - 1) * 4 * 4096);
     if (active && nreal > 0) {
       tc::mbar_wait(&done, l & 1);
       tc::fence_after_sync();
@@ -252,17 +267,12 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
       box_out(sy, L.omap, n0, bcast, true);
       if (L.xmap >= 0) box_out(sx, L.xmap, n0, false);
     } else if (epi == GE_BWD_LN_RELU || epi == GE_BWD_LN_TANH) {
-      uint8_t* sl = pslots;
-      if (l >= 1 && hh == 0 && lane == 0) tc::bulk_wait_read<0>();
-      tc::named_bar(1 + q, 64);
-      if (hh == 0 && lane == 0) {
-        tc::mbar_expect_tx(&ld_bar[q], 4096);
-        tc::tma_load_2d(sl, &b.maps[L.xmap], n0, row0, &ld_bar[q]);
-      }
-      tc::mbar_wait(&ld_bar[q], nbwd & 1);
-      ++nbwd;
+      // pass 1: dn through the activation, row sums of dxh = dn g and dxh x_hat, column partials of
+      // dn x_hat and dn; (dn, x_hat) stay in v / a for pass 2
+      uint8_t* xs = pslots;
+      tc::mbar_wait(&ld_bar[(l & 1) * 4 + q], (l >> 1) & 1);
       tc::tmem_ld32(trow + hh * 32, v);
-      box_get(sl, hh, a);
+      box_get(xs, hh, a);
       float pg[32], pb[32], s1 = 0.f, s2 = 0.f;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -275,6 +285,8 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
         s2 += dxh * x;
         pg[j] = dn * x;
         pb[j] = dn;
+        v[j] = dn;
+        a[j] = x;
       }
       const float cg = colsum32(pg);
       const float cb = colsum32(pb);
@@ -285,20 +297,20 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
       stamp(5 + 4 * l);
       m1 /= (float)L.N;
       m2 /= (float)L.N;
-      const float rs = rv ? L.rstd[r] : 0.f;
+      const float rs = s_rs[l][rl];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const int cc = hh * 32 + j;
-        const float x = rv ? a[j] : 0.f;
-        const float n = fmaf(x, s_g[cc], s_beta[cc]);
-        const float dn = rv ? ((epi == GE_BWD_LN_RELU) ? (n > 0.f ? v[j] : 0.f) : v[j] * sech2_fast(n)) : 0.f;
-        v[j] = rv ? rs * (dn * s_g[cc] - m1 - x * m2) : 0.f;
+        v[j] = rv ? rs * (v[j] * s_g[hh * 32 + j] - m1 - a[j] * m2) : 0.f;
         a[j] = v[j];
       }
-      box_put(sl, hh, v);
+      // dA straight into this CTA's slice of the next layer's A (as the forward layers do)
+      uint8_t* sy = A + rank * 16384 + q * 4096;
+      if (l >= 1 && hh == 0 && lane == 0) tc::bulk_wait_read<0>();  // the pair's stores of layer l-1
+      tc::named_bar(1 + q, 64);
+      box_put(sy, hh, v);
       const float cx = colsum32(a);
       colacc[(q * 3 + 0) * 64 + hh * 32 + lane] = cx;
-      box_out(sl, L.omap, n0, bcast);
+      box_out(sy, L.omap, n0, bcast, true);
       __syncthreads();
       if (L.part)
         for (int e = tid; e < 3 * 64; e += kThr) {
@@ -357,6 +369,7 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
     tc::fence_before_sync();
     __syncthreads();
     stamp(6 + 4 * l);
+    if (l + 2 < nl && bwd_l(l + 2) && warp < 4 && lane == 0) issue_xhat(l + 2);  // parity slot now free
   }
   if (lane == 0) tc::bulk_wait_read<0>();
   tc::fence_before_sync();

@@ -1,13 +1,15 @@
 // heads.cu -- distributional critic machinery (a9, a10, a12), warp per row.
 //
 //  k_target_ce: pbar = (softmax l1_bar + softmax l2_bar)/2 (Q20); categorical projection of
-//      the atoms shifted by r + (1-d) gamma (z_j - alpha0 log pi') (Q21-Q23) in the
-//      deterministic "hat" gather form m_k = sum_j pbar_j max(0, 1 - |b_j - k|), which is
-//      the floor/ceil split of S:280 written without scatter (so no atomics, bitwise
+//      the atoms shifted by r + (1-d) gamma (z_j - alpha0 log pi') (Q21-Q23) in the "hat" form
+//      m_k = sum_j pbar_j max(0, 1 - |b_j - k|) (the floor/ceil split of S:280 with an integral
+//      b_j landing whole), as a warp segmented scan over the sorted atoms (no atomics, bitwise
 //      reproducible); then CE of both online heads (Q24) and dL/dl = (softmax - m) s.
 //  k_actor_q: Q_i = sum_k softmax(l_i^+)_k z_k (Q25), dL_pi/dl_i = -s/2 p (z - Q_i),
 //      per-row terms of L_pi = s sum_b [alpha+ log pi_b - (Q1 + Q2)/2].
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 #include "heads.cuh"
@@ -25,10 +27,16 @@ template <int NPL>
 __global__ void __launch_bounds__(256) k_target_ce(const __grid_constant__ TargetCEArgs a) {
   grid_wait();
   grid_trigger();
-  extern __shared__ float sm[];
+  auto stamp = [&](int k) {
+    if (a.dbg && (threadIdx.x & 31) == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.dbg[(blockIdx.x * kRows + (threadIdx.x >> 5)) * 4 + k] = t;
+    }
+  };
+  stamp(0);
+  extern __shared__ float sm_acc[];
   const int N = a.N, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float* pb = sm + w * 2 * N;  // pbar [N]
-  float* bj = pb + N;          // b_j [N]
   const int row = blockIdx.x * kRows + w;
   if (a.step && blockIdx.x == 0 && threadIdx.x == 0) {
     const int64_t tc = ++a.step[0], ta = ++a.step[1];
@@ -50,6 +58,7 @@ __global__ void __launch_bounds__(256) k_target_ce(const __grid_constant__ Targe
     }
   const float r = a.reward[ridx];
   const float nd = a.done[ridx] ? 0.f : 1.f;
+  stamp(1);
   const float dz = (a.v_max - a.v_min) / (float)(N - 1);
   const float shift = expf(a.log_alpha[0]) * a.logp_next[row];
   // pbar = (softmax l1_bar + softmax l2_bar) / 2
@@ -73,41 +82,88 @@ __global__ void __launch_bounds__(256) k_target_ce(const __grid_constant__ Targe
 #pragma unroll
     for (int i = 0; i < NPL; ++i) pbar[i] += 0.5f * e[i] * inv;
   }
+  // Categorical projection (Q21-Q23) in the hat form m_k = sum_j pbar_j max(0, 1 - |b_j - k|):
+  // atom j gives a_j = pbar_j (1 - f_j) to bin l_j = floor(b_j) and h_j = pbar_j f_j to bin
+  // l_j + 1 (an integral b_j lands whole on l_j).  b_j is non-decreasing in j (g_j increases with
+  // z_j; clipping keeps the order), so the atoms of one bin form a contiguous run: a segmented
+  // scan over the atoms in j order (4 consecutive atoms per lane, then a warp scan of the lanes'
+  // trailing runs as affine maps) yields every run's totals at its last atom; then
+  // m_k = A(k) + H(k - 1).  Fixed-order fp32 sums (bitwise reproducible), O(log) depth however
+  // many atoms pile up in one bin (clipped support).
+  float* pbs = reinterpret_cast<float*>(sm_acc) + w * 3 * 32 * NPL;  // pbar | A | H, 32 NPL each
+  float* As = pbs + 32 * NPL;
+  float* Hs = As + 32 * NPL;
 #pragma unroll
   for (int i = 0; i < NPL; ++i) {
     const int j = lane + 32 * i;
+    pbs[j] = j < N ? pbar[i] : 0.f;
+  }
+  for (int k = lane; k < 32 * NPL; k += 32) As[k] = Hs[k] = 0.f;
+  __syncwarp();
+  int key[NPL];
+  float sa[NPL], sh[NPL];
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int j = NPL * lane + i;
+    float va = 0.f, vh = 0.f;
+    key[i] = N + 1;  // padding atoms: a run past the support, never stored
     if (j < N) {
       const float zj = a.v_min + (float)j * dz;
       float g = r + nd * a.gamma * (zj - shift);
       g = fminf(fmaxf(g, a.v_min), a.v_max);
-      const float b = (g - a.v_min) / dz;
-      bj[j] = fminf(fmaxf(b, 0.f), (float)(N - 1));
-      pb[j] = pbar[i];
+      const float b = fminf(fmaxf((g - a.v_min) / dz, 0.f), (float)(N - 1));
+      const float fl = floorf(b);
+      const float f = b - fl;
+      key[i] = (int)fl;
+      va = pbs[j] * (1.f - f);
+      vh = pbs[j] * f;
+    }
+    // lane-local segmented inclusive scan
+    const bool cont = i > 0 && key[i] == key[i - 1];
+    sa[i] = va + (cont ? sa[i - 1] : 0.f);
+    sh[i] = vh + (cont ? sh[i - 1] : 0.f);
+  }
+  // trailing-run totals across lanes: S(x) = tail(x) + c(x) S(x - 1), c(x) = [lane x is one run
+  // continuing lane x - 1's last run]; composed as affine maps in a Hillis-Steele scan
+  const int kprev = __shfl_up_sync(0xffffffffu, key[NPL - 1], 1);
+  const int knext = __shfl_down_sync(0xffffffffu, key[0], 1);
+  float Ba = sa[NPL - 1], Bh = sh[NPL - 1];
+  int cc = (lane > 0 && key[0] == key[NPL - 1] && kprev == key[0]) ? 1 : 0;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float ua = __shfl_up_sync(0xffffffffu, Ba, off);
+    const float uh = __shfl_up_sync(0xffffffffu, Bh, off);
+    const int uc = __shfl_up_sync(0xffffffffu, cc, off);
+    if (lane >= off) {
+      if (cc) {
+        Ba += ua;
+        Bh += uh;
+      }
+      cc &= uc;
+    }
+  }
+  // carry into this lane's first run from the lanes before it
+  const float pa = __shfl_up_sync(0xffffffffu, Ba, 1), ph = __shfl_up_sync(0xffffffffu, Bh, 1);
+  const bool carry = lane > 0 && kprev == key[0];
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const bool first_run = key[i] == key[0];
+    const float ta = sa[i] + ((carry && first_run) ? pa : 0.f);
+    const float th = sh[i] + ((carry && first_run) ? ph : 0.f);
+    const bool run_end = i < NPL - 1 ? key[i + 1] != key[i] : (lane == 31 || knext != key[NPL - 1]);
+    if (run_end && key[i] < N) {
+      As[key[i]] = ta;
+      Hs[key[i]] = th;
     }
   }
   __syncwarp();
-  // m_k = sum_j pbar_j max(0, 1 - |b_j - k|).  b_j is non-decreasing in j (g_j increases with z_j
-  // and clipping preserves order), so the contributing j form a contiguous range: binary search
-  // its start, then add the terms in ascending j as the full sum would.
   float m[NPL];
 #pragma unroll
   for (int i = 0; i < NPL; ++i) {
     const int k = lane + 32 * i;
     float acc = 0.f;
     if (k < N) {
-      const float kf = (float)k;
-      int lo = 0, hi = N;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (bj[mid] - kf > -1.f) hi = mid;
-        else lo = mid + 1;
-      }
-      for (int j = lo; j < N; ++j) {
-        const float d = bj[j] - kf;
-        if (d >= 1.f) break;
-        const float wgt = 1.f - fabsf(d);
-        if (wgt > 0.f) acc = fmaf(pb[j], wgt, acc);
-      }
+      acc = As[k] + (k > 0 ? Hs[k - 1] : 0.f);
       a.m[(int64_t)row * N + k] = acc;
     }
     m[i] = acc;
@@ -142,6 +198,7 @@ __global__ void __launch_bounds__(256) k_target_ce(const __grid_constant__ Targe
     loss += warp_sum(ce);
   }
   if (lane == 0) a.row_loss[row] = loss * a.scale;
+  stamp(3);
 }
 
 template <int NPL>
@@ -199,8 +256,15 @@ __global__ void __launch_bounds__(256) k_actor_q(const __grid_constant__ ActorQA
 
 }  // namespace
 
-int launch_target_ce(const TargetCEArgs& a, cudaStream_t s) {
-  const size_t smem = sizeof(float) * 2 * a.N * kRows;
+static unsigned long long* g_tce_dbg = nullptr;
+int launch_target_ce(const TargetCEArgs& a_in, cudaStream_t s) {
+  TargetCEArgs a = a_in;
+  static const bool dbg = getenv("SQUINT_TCE_DBG") != nullptr;
+  if (dbg) {
+    if (!g_tce_dbg) cudaMalloc(&g_tce_dbg, 4096 * 4 * sizeof(unsigned long long));
+    a.dbg = g_tce_dbg;
+  }
+  const size_t smem = sizeof(float) * 3 * 32 * ((a.N + 31) / 32 <= 2 ? 2 : (a.N + 31) / 32 <= 4 ? 4 : (a.N + 31) / 32 <= 8 ? 8 : 16) * kRows;
   const int npl = (a.N + 31) / 32;
   const dim3 grid((a.B + kRows - 1) / kRows);
   note_launch(s, "k_target_ce", 0, 0);
@@ -226,3 +290,10 @@ int launch_actor_q(const ActorQArgs& a, cudaStream_t s) {
 }
 
 }  // namespace sq
+
+extern "C" __attribute__((visibility("default"))) int squint_debug_tce(unsigned long long* host, int n) {
+  if (!sq::g_tce_dbg) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, sq::g_tce_dbg, (size_t)n * 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return n;
+}

@@ -26,6 +26,7 @@ struct TargetCEArgs {
   int64_t* step;
   float* scal;
   float beta1, beta2;
+  unsigned long long* dbg;  // optional per-warp globaltimer stamps [B][4] (SQUINT_TCE_DBG)
 };
 
 struct ActorQArgs {
