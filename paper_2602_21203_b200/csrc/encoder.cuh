@@ -43,6 +43,7 @@ struct EncFwdArgs {
   GatherJob gj[2][4];
   int ngj[2];
   const uint8_t* wtiles;   // tensor-core path: conv weights as swizzled bf16 smem images (k_conv_tiles)
+  int dbg;                 // phase timestamps (SQUINT_ENC_DBG; set by the launcher)
 };
 
 struct EncBwdArgs {

@@ -94,15 +94,44 @@ __global__ void __launch_bounds__(256) k_conv_tiles(const float* __restrict__ w1
   }
 }
 
+__device__ unsigned long long g_enc_stamps[160][16];  // debug: per-CTA phase timestamps (SQUINT_ENC_DBG)
+__device__ __forceinline__ void enc_stamp(bool on, int k) {
+  if (on && threadIdx.x == 0 && blockIdx.x < 160) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_enc_stamps[blockIdx.x][k] = t;
+  }
+}
 // ---- forward ---------------------------------------------------------------------------------
 template <int C>
 struct FwdL {
   static constexpr uint32_t w = 0;
   static constexpr uint32_t ring = (C * 128 + ((9 * C + 63) / 64) * C * 128 + 1023) & ~1023u;  // A1 / A2 stages
   static constexpr uint32_t y1 = ring + 65536;
-  static constexpr uint32_t xs = y1 + ((kGF * 49 * C * 2 + 1023) & ~1023u);
+  // conv1 output as the conv2 A operand: rows = (image, 7x7 pixel) flattened, C bf16 per row,
+  // K-major with the 64-byte (C = 32) / 128-byte (C = 64) swizzle; 416 rows cover the three
+  // 128-row output tiles plus the largest tap shift (2 * 7 + 2)
+  static constexpr uint32_t y1_rows = 416;
+  static constexpr uint32_t xs = y1 + ((y1_rows * C * 2 + 1023) & ~1023u);
   static constexpr uint32_t total = xs + kGF * 768;
 };
+// byte offset of (row, 16-byte chunk) in a K-major swizzled tile with C-channel rows (C * 2 bytes):
+// the hardware XORs address bits [4, 4 + b) with bits [7, 7 + b) (b = 2 for 64-byte rows, 3 for
+// 128-byte rows), so a descriptor may start at any row
+template <int C>
+__device__ __forceinline__ uint32_t y1_off(int row, int chunk) {
+  const uint32_t a = (uint32_t)(row * C * 2 + chunk * 16);
+  return C == 32 ? a ^ (((a >> 7) & 3u) << 4) : a ^ (((a >> 7) & 7u) << 4);
+}
+__device__ __forceinline__ uint64_t sdesc_sw(uint32_t saddr, int rowbytes) {  // K-major, SW64 / SW128
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(((8u * rowbytes) >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)(rowbytes == 128 ? 2u : 4u) << 61;
+  return d;
+}
 
 // byte x of a 16-byte row held as a uint4
 __device__ __forceinline__ uint32_t byte_of(const uint4& v, int x) {
@@ -113,25 +142,29 @@ __device__ __forceinline__ uint32_t byte_of(const uint4& v, int x) {
 template <int C>
 __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ EncFwdArgs a) {
   using L = FwdL<C>;
-  constexpr int nkb2 = (9 * C + 63) / 64;
   constexpr uint32_t kCols = C == 32 ? 256u : 512u;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared pointer
-  __shared__ uint64_t wbar, bar1, bar2, empty[2];
+  __shared__ uint64_t wbar, bar1, bar2;
   __shared__ uint32_t tmem_slot;
+  __shared__ int s_koff[32];  // conv1 tap k = ci*9 + ki*3 + kj -> input byte offset ci*256 + ki*16 + kj
   const int H = a.H;  // 16
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = warp & 3, hh = warp >> 2;
   const int ngroups = (a.B + kGF - 1) / kGF;
   const int total = ngroups * a.nsrc;
+  // forward phases in stamp slots 10..15 (the backward uses 0..9)
+  enc_stamp(a.dbg, 10);
 
   if (warp == 0) tc::tmem_alloc(&tmem_slot, kCols);
   if (tid == 32) {
     tc::mbar_init(&wbar, 1);
     tc::mbar_init(&bar1, 1);
     tc::mbar_init(&bar2, 1);
-    tc::mbar_init(&empty[0], 1);
-    tc::mbar_init(&empty[1], 1);
     tc::fence_mbar_init();
+  }
+  if (warp == 2) {
+    const int k = lane, ci = k / 9, t = k - ci * 9, ki = t / 3, kj = t - ki * 3;
+    s_koff[k] = k < 27 ? ci * 256 + ki * 16 + kj : 0;
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -143,12 +176,11 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ 
     tc::bulk_load_1d(sm + L::w, a.wtiles, fwd_wbytes(C), &wbar);
   }
   const uint32_t tmem = tmem_slot;
-  const uint32_t t_c1 = tmem, t_c2 = tmem + 3 * C;  // conv1: 3 tiles x C cols; conv2: 2 tiles x C cols
+  const uint32_t t_c1 = tmem, t_c2 = tmem + 3 * C;  // conv1, conv2: 3 row tiles x C columns each
   const uint32_t id_c = tc::idesc_bf16(128, C);
   uint8_t* xs = sm + L::xs;
-  bf16_t* y1s = reinterpret_cast<bf16_t*>(sm + L::y1);
   const float inv255 = 1.0f / 255.0f;
-  int it2 = 0, gi = 0;
+  int gi = 0;
 
   for (int job = blockIdx.x; job < total; job += gridDim.x, ++gi) {
     const int src = job / ngroups, g = job - src * ngroups;
@@ -215,15 +247,22 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ 
       }
     }
     __syncthreads();
-    // ---- 2. conv1 im2col: 3 row tiles, K 0..31 from the image, 32..63 zero --------------------
+    enc_stamp(a.dbg && gi == 0, 11);
+    // ---- 2. conv1 im2col: 3 row tiles, K 0..26 from the image (k = ci*9 + ki*3 + kj at byte
+    // offset koff[k] from the output pixel's top-left input byte), 27..63 zero -----------------
     for (int e = tid; e < 384 * 8; e += kThr) {
       const int r = e >> 3, ch = e & 7;
-      const int i = r / 49, p = r - i * 49, oy = p / 7, ox = p - oy * 7;
       float f[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int k = ch * 8 + j, ci = k / 9, t = k - ci * 9, ki = t / 3, kj = t - ki * 3;
-        f[j] = (r < kGF * 49 && k < 27) ? (float)xs[(i * 3 + ci) * 256 + (2 * oy + ki) * 16 + 2 * ox + kj] : 0.f;
+      for (int j = 0; j < 8; ++j) f[j] = 0.f;
+      if (ch < 4 && r < kGF * 49) {
+        const int i = r / 49, p = r - i * 49, oy = p / 7, ox = p - oy * 7;
+        const uint8_t* px = xs + i * 768 + 2 * oy * 16 + 2 * ox;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = ch * 8 + j;
+          if (k < 27) f[j] = (float)px[s_koff[k]];
+        }
       }
       *reinterpret_cast<uint4*>(sm + L::ring + (r >> 7) * 16384 + sw(r & 127, ch)) = tc::pack_bf16x8(f);
     }
@@ -243,6 +282,7 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ 
     }
     tc::mbar_wait(&bar1, gi & 1);
     tc::fence_after_sync();
+    enc_stamp(a.dbg && gi == 0, 12);
     // ---- 3. conv1 epilogue: warp (q, hh) -> tiles hh, hh + 2 ------------------------------------
     for (int t = hh; t < 3; t += 2) {
       const int r = t * 128 + q * 32 + lane;
@@ -261,63 +301,57 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ 
 #pragma unroll
             for (int j = 0; j < 8; ++j) f[j] = v[j8 * 8 + j];
             const uint4 u = tc::pack_bf16x8(f);
-            *reinterpret_cast<uint4*>(y1s + (i * 49 + p) * C + c0 + j8 * 8) = u;
+            *reinterpret_cast<uint4*>(sm + L::y1 + y1_off<C>(r, (c0 + j8 * 8) / 8)) = u;
             if (a.y1b && src == 0 && b < a.B)
               *reinterpret_cast<uint4*>(a.y1b + ((int64_t)b * 49 + p) * C + c0 + j8 * 8) = u;
           }
         }
       }
     }
+    tc::fence_async_smem();  // y1 (generic stores) -> the tensor core's operand reads
     tc::fence_before_sync();
     __syncthreads();
-    // ---- 4. conv2: per K block both row tiles, ring of 2 stages -----------------------------------
-    for (int kb = 0; kb < nkb2; ++kb, ++it2) {
-      const int st = it2 & 1;
-      if (it2 >= 2) tc::mbar_wait(&empty[st], ((it2 >> 1) - 1) & 1);
-      uint8_t* A2 = sm + L::ring + st * 32768;
-      for (int e = tid; e < 256 * 8; e += kThr) {
-        const int r = e >> 3, ch = e & 7;
-        const int k = kb * 64 + ch * 8, t = k / C, c = k - t * C;
-        uint4 u = make_uint4(0, 0, 0, 0);
-        if (r < kGF * 25 && t < 9) {
-          const int i = r / 25, p = r - i * 25, oy = p / 5, ox = p - oy * 5, ki = t / 3, kj = t - ki * 3;
-          u = *reinterpret_cast<const uint4*>(y1s + (i * 49 + (oy + ki) * 7 + ox + kj) * C + c);
+    enc_stamp(a.dbg && gi == 0, 13);
+    // ---- 4. conv2 as nine row-shifted GEMMs: output position o = i*49 + oy*7 + ox of the full 7x7
+    // grid reads y1 row o + ki*7 + kj for tap (ki, kj), so tap t's A operand is y1 itself started
+    // t's shift rows later (no im2col); positions with oy or ox > 4 are computed and dropped ----
+    if (tid == 0) {
+      tc::fence_after_sync();
+      const uint32_t y0 = tc::smem_u32(sm + L::y1), w0 = tc::smem_u32(sm + L::w + C * 128);
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+        for (int tap = 0; tap < 9; ++tap) {
+          const int shift = (tap / 3) * 7 + tap % 3;
+          // W2 K-block layout: k = tap * C + c in blocks of 64 (128-byte swizzled rows)
+          const int kb = (tap * C) / 64, koff = (tap * C) % 64;
+#pragma unroll
+          for (int k = 0; k < C / 16; ++k)
+            tc::mma_bf16(t_c2 + t * C, sdesc_sw(y0 + (t * 128 + shift) * C * 2 + 32 * k, C * 2),
+                         tc::sdesc_k128(w0 + kb * C * 128 + (koff + 16 * k) * 2), id_c, (tap | k) != 0);
         }
-        *reinterpret_cast<uint4*>(A2 + (r >> 7) * 16384 + sw(r & 127, ch)) = u;
-      }
-      tc::fence_async_smem();
-      tc::fence_before_sync();
-      __syncthreads();
-      if (tid == 0) {
-        tc::fence_after_sync();
-        const uint32_t a0 = tc::smem_u32(A2), w0 = tc::smem_u32(sm + L::w + C * 128 + kb * C * 128);
-#pragma unroll
-        for (int t = 0; t < 2; ++t)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            tc::mma_bf16(t_c2 + t * C, tc::sdesc_k128(a0 + t * 16384 + 32 * k), tc::sdesc_k128(w0 + 32 * k), id_c,
-                         (kb | k) != 0);
-        tc::mma_commit(&empty[st]);
-        if (kb == nkb2 - 1) tc::mma_commit(&bar2);
-      }
+      tc::mma_commit(&bar2);
     }
     tc::mbar_wait(&bar2, gi & 1);
     tc::fence_after_sync();
-    // ---- 5. conv2 epilogue: warp (q, hh) -> tile hh ---------------------------------------------
+    enc_stamp(a.dbg && gi == 0, 14);
+    // ---- 5. conv2 epilogue: warp (q, hh) -> tiles hh, hh + 2; valid 5x5 positions -> h (HWC) ----
     {
-      const int r = hh * 128 + q * 32 + lane, i = r / 25, p = r - i * 25, b = b0 + i;
       bf16_t* hout = a.hb[src];
+      for (int t = hh; t < 3; t += 2) {
+        const int r = t * 128 + q * 32 + lane, i = r / 49, p = r - i * 49, oy = p / 7, ox = p - oy * 7, b = b0 + i;
+        const bool ok = i < kGF && oy < 5 && ox < 5 && b < a.B;
 #pragma unroll
-      for (int c0 = 0; c0 < C; c0 += 32) {
-        float v[32];
-        tc::tmem_ld32(t_c2 + hh * C + c0 + ((uint32_t)(q * 32) << 16), v);
-        if (r < kGF * 25 && b < a.B) {
+        for (int c0 = 0; c0 < C; c0 += 32) {
+          float v[32];
+          tc::tmem_ld32(t_c2 + t * C + c0 + ((uint32_t)(q * 32) << 16), v);
+          if (ok) {
 #pragma unroll
-          for (int j8 = 0; j8 < 4; ++j8) {
-            float f[8];
+            for (int j8 = 0; j8 < 4; ++j8) {
+              float f[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) f[j] = fmaxf(v[j8 * 8 + j] + a.b2[c0 + j8 * 8 + j], 0.f);
-            *reinterpret_cast<uint4*>(hout + (int64_t)b * a.h_ld + p * C + c0 + j8 * 8) = tc::pack_bf16x8(f);
+              for (int j = 0; j < 8; ++j) f[j] = fmaxf(v[j8 * 8 + j] + a.b2[c0 + j8 * 8 + j], 0.f);
+              *reinterpret_cast<uint4*>(hout + (int64_t)b * a.h_ld + (oy * 5 + ox) * C + c0 + j8 * 8) = tc::pack_bf16x8(f);
+            }
           }
         }
       }
@@ -329,6 +363,7 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ 
   if (tid == 0 && gi == 0) tc::mbar_wait(&wbar, 0);  // never exit with the bulk copy in flight
   tc::fence_before_sync();
   __syncthreads();
+  enc_stamp(a.dbg, 15);
   if (warp == 0) tc::tmem_dealloc(tmem, kCols);
 }
 
@@ -345,14 +380,7 @@ struct BwdL {
 };
 __host__ __device__ constexpr int part_rows(int C) { return 9 * C + 1 + 28; }  // dW2 (+ db2), dW1 (+ db1)
 
-__device__ unsigned long long g_enc_stamps[160][16];  // debug: per-CTA phase timestamps (SQUINT_ENC_DBG)
-__device__ __forceinline__ void enc_stamp(bool on, int k) {
-  if (on && threadIdx.x == 0 && blockIdx.x < 160) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_enc_stamps[blockIdx.x][k] = t;
-  }
-}
+
 
 template <int C>
 __global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ EncBwdArgs a, int dbg) {
@@ -679,7 +707,10 @@ int launch_enc_fwd_tc(const EncFwdArgs& a, cudaStream_t s) {
     const double bytes = a.mode == 1 ? img * (3.0 * 128 * 128 + 2.0 * 25 * C) : img * (768.0 + 2.0 * 25 * C);
     note_launch(s, "k_enc_fwd_tc", flops, bytes);
   }
-  return a.C == 32 ? launch_fwd_c<32>(a, s) : launch_fwd_c<64>(a, s);
+  static const bool dbg = getenv("SQUINT_ENC_DBG") != nullptr;
+  EncFwdArgs b = a;
+  b.dbg = dbg ? 1 : 0;
+  return b.C == 32 ? launch_fwd_c<32>(b, s) : launch_fwd_c<64>(b, s);
 }
 
 size_t enc_bwd_tc_partial_floats(int C, int B) {
