@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
   }
   tc::fence_before_sync();
   __syncthreads();
-  tc::cluster_sync();  // peers' barriers are initialised before any DSMEM traffic
+  tc::cluster_sync_init();  // peers' barriers are initialised before any DSMEM traffic
   tc::fence_after_sync();
   stamp(1);
   const uint32_t tmem = tmem_slot;

@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     tc::fence_async_smem();
   }
   tc::fence_before_sync();
-  if (b.cs > 1) tc::cluster_sync();  // peers' stats_bar initialised before any st.async reaches it
+  if (b.cs > 1) tc::cluster_sync_init();  // peers' stats_bar initialised before any st.async reaches it
   else __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = tmem_slot;
@@ -664,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_sk(const __grid_constant__
     tc::tma_prefetch_desc(&b.maps[P.seg[lane].bmap]);
   }
   tc::fence_before_sync();
-  tc::cluster_sync();  // every CTA's recv_bar is initialised before any peer copies into it
+  tc::cluster_sync_init();  // every CTA's recv_bar is initialised before any peer copies into it
   tc::fence_after_sync();
   const uint32_t tmem = tmem_slot;
   stamp(1);

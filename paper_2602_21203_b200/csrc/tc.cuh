@@ -271,5 +271,10 @@ __device__ __forceinline__ void cluster_arrive_relaxed() {
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+// prologue barrier after mbarrier initialisation: fence.mbarrier_init.release.cluster already
+// releases the inits, so a relaxed arrive suffices (a release arrive costs a GPU-scope fence)
+__device__ __forceinline__ void cluster_sync_init() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 }  // namespace tc
 }  // namespace sq
