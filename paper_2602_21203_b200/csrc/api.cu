@@ -8,6 +8,7 @@
 #include <cstring>
 #include <optional>
 #include <string>
+#include <vector>
 
 #include "../../include/squint.h"
 #include "comm.hpp"
@@ -871,9 +872,68 @@ squint_status squint_update(const squint_dims* dims, const squint_hparams* hp, c
       !state->v_critic || !state->m_actor || !state->v_actor || !state->m_alpha || !state->v_alpha || !state->step)
     return fail(SQUINT_EINVAL, "NULL state field");
   Comm* cm = reinterpret_cast<Comm*>(comm);
-  if (dims->precision == SQUINT_BF16)
-    return bf16_update(*dims, *hp, *replay, idx, shifts, eps, utd, *state, metrics, workspace, workspace_bytes, cm,
-                       (cudaStream_t)stream);
+  if (dims->precision == SQUINT_BF16) {
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) {
+      cudaGetLastError();
+      cs = cudaStreamCaptureStatusActive;  // unknown: launch directly
+    }
+    static const bool no_graph = getenv("SQUINT_NO_GRAPH") != nullptr || getenv("SQUINT_DEBUG_SYNC") != nullptr;
+    const bool branch = bf16_prepare();
+    if (no_graph || cm || cs != cudaStreamCaptureStatusNone || instrumentation_active())
+      return bf16_update(*dims, *hp, *replay, idx, shifts, eps, utd, *state, metrics, workspace, workspace_bytes, cm, s);
+    // the ~30 launches per update are captured once per distinct argument set and replayed as a
+    // CUDA graph (host cost of a call: one graph launch)
+    std::string key;
+    auto put = [&](const void* p, size_t n) { key.append(reinterpret_cast<const char*>(p), n); };
+    put(dims, sizeof(*dims));
+    put(hp, sizeof(*hp));
+    put(replay, sizeof(*replay));
+    put(state, sizeof(*state));
+    const void* ptrs[6] = {idx, shifts, eps, metrics, workspace, nullptr};
+    put(ptrs, sizeof(ptrs));
+    put(&utd, sizeof(utd));
+    put(&workspace_bytes, sizeof(workspace_bytes));
+    put(&branch, sizeof(branch));
+    struct Entry {
+      std::string key;
+      cudaGraphExec_t exec;
+    };
+    static thread_local std::vector<Entry> cache;
+    cudaGraphExec_t exec = nullptr;
+    for (auto& e : cache)
+      if (e.key == key) exec = e.exec;
+    if (!exec) {
+      // captured on a private stream (the caller's may be the legacy default stream, which cannot
+      // capture); the graph is then launched on the caller's stream
+      static thread_local cudaStream_t cap = nullptr;
+      if (!cap && cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(SQUINT_ECUDA, "update graph: capture stream");
+      if (cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+        return fail(SQUINT_ECUDA, "update graph: begin capture failed");
+      squint_status r = bf16_update(*dims, *hp, *replay, idx, shifts, eps, utd, *state, metrics, workspace,
+                                    workspace_bytes, cm, cap);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(cap, &g);
+      if (r != SQUINT_OK || ce != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        return r != SQUINT_OK ? r : fail(SQUINT_ECUDA, std::string("update graph capture: ") + cudaGetErrorString(ce));
+      }
+      const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+      cudaGraphDestroy(g);
+      if (ie != cudaSuccess) return fail(SQUINT_ECUDA, std::string("update graph instantiate: ") + cudaGetErrorString(ie));
+      if (cache.size() >= 8) {
+        cudaGraphExecDestroy(cache.front().exec);
+        cache.erase(cache.begin());
+      }
+      cache.push_back(Entry{key, exec});
+    }
+    const cudaError_t le = cudaGraphLaunch(exec, s);
+    if (le != cudaSuccess) return fail(SQUINT_ECUDA, std::string("update graph launch: ") + cudaGetErrorString(le));
+    return SQUINT_OK;
+  }
   Layout L = make_layout(*dims);
   WsLay w = plan_ws(*dims, L);
   if (workspace_bytes < w.total) return fail(SQUINT_EINVAL, "workspace too small (see squint_workspace_bytes)");

@@ -36,6 +36,7 @@ void note_launch(cudaStream_t s, const char* name, double flops, double bytes) {
   }
 }
 long launch_count() { return g_launches.load(); }
+bool instrumentation_active() { return g_lev != nullptr || g_events != nullptr; }
 
 PhaseScope::PhaseScope(int phase, int rep, cudaStream_t st) : idx(-1), s(st) {
   if (!g_events || phase >= g_phases || rep >= g_reps) return;

@@ -975,6 +975,11 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
 
 }  // namespace
 
+bool bf16_prepare() {
+  static const bool no_branch = getenv("SQUINT_NO_BRANCH") != nullptr;
+  return !no_branch && g_branch_enabled && t_aux.ok();
+}
+
 size_t bf16_workspace_bytes(const squint_dims& d) {
   Layout L = make_layout(d);
   return plan_bf(d, L).total;

@@ -19,6 +19,10 @@ squint_status bf16_update(const squint_dims& d, const squint_hparams& hp, const 
                           const int64_t* idx, const uint8_t* shifts, const float* eps, int utd,
                           const squint_state& st, float* metrics, void* workspace, size_t workspace_bytes, Comm* comm,
                           cudaStream_t s);
+// Creates the auxiliary stream/events of the encoder-backward branch (outside any capture) and
+// returns whether the branch is in use.
+bool bf16_prepare();
+bool instrumentation_active();  // instrument.cu: launch / phase events requested
 size_t bf16_act_workspace_bytes(const squint_dims& d, int64_t n);
 squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const float* actor_params,
                        const float* critic_params, const uint8_t* frames, int64_t n, int factor, const float* proprio,
