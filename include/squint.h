@@ -181,6 +181,11 @@ SQUINT_API squint_status squint_act(const squint_dims* dims, const squint_hparam
  * comm: NULL for one GPU, else a handle from squint_comm_init; then B is the per-rank
  * batch, losses are scaled by 1/(B*nranks) and gradients/metric sums are SUM
  * all-reduced over ranks (Q33).
+ * SQUINT_BF16 with comm == NULL, outside a stream capture: the call's ~30 launches per update
+ * are captured once per distinct argument set (all pointers, dims, hparams, utd) into a
+ * CUDA graph kept in a small per-thread cache (8 entries) and replayed on `stream`; calls with
+ * changed arguments capture anew.  SQUINT_NO_GRAPH=1 launches directly.  Inside a caller's
+ * capture the launches join that capture.
  * Errors: EINVAL (utd < 1, batch < 1, gamma/tau outside [0,1], size < 1, bad support),
  * ESHAPE (dims inconsistent), EUNSUPPORTED (shape/precision not built). */
 SQUINT_API squint_status squint_update(const squint_dims* dims, const squint_hparams* hp, const squint_replay* replay,
