@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     }
     npre = kb;
   }
+  if (warp == 0) npre = __shfl_sync(0xffffffffu, npre, 0);  // the producer loop runs warp-wide
   tc::pdl_wait();
   tc::pdl_trigger();
   stamp(2);
@@ -199,81 +200,88 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     }
   }
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer ----------------
-    int kb = 0;
+  // Producer and MMA issuer: single threads running tight loops.  Everything loop-invariant
+  // (tensor-map addresses, tile coordinates, byte counts) is hoisted per segment and the stage
+  // index advances without divisions: the TMA and MMA instructions take uniform-register operands,
+  // and per-iteration operand conversions had made issuing ~3x slower than the TMA unit.
+  if (warp == 0) {
+    // ---------------- TMA producer (whole warp, one elected lane issues) ----------------
+    const int sbytes = b.stage_bytes, rank = b.mcast ? (int)(blockIdx.x % b.cs) : 0, cs = b.cs;
+    const uint16_t mask = (uint16_t)((1u << cs) - 1u);
+    int kb = 0, st = 0, ph = 0;
     for (int s = 0; s < P.nseg; ++s) {
-      const GSeg& G = P.seg[s];
+      const GSeg G = P.seg[s];
       const TileGeo geo = tile_geo(P, nreal, G.b_mn);
       const void* am = &b.maps[G.amap];
       const void* bm = &b.maps[G.bmap];
+      const int am0 = P.a_m + m0, bn0 = P.b_n + n0;
+      const uint32_t tx = kABytes + geo.bbytes;
       for (int l = 0; l < G.nkb; ++l, ++kb) {
-        const int st = kb % S;
-        if (kb >= S) tc::mbar_wait(&empty_bar[st], ((kb / S) - 1) & 1);
-        uint8_t* As = smem + st * b.stage_bytes;
+        if (kb >= S) tc::mbar_wait(&empty_bar[st], ph ^ 1);
+        uint8_t* As = smem + st * sbytes;
         uint8_t* Bs = As + kABytes;
         const bool pre = kb < npre;  // B already in flight, transaction bytes already expected
-        if (!pre) tc::mbar_expect_tx(&full_bar[st], kABytes + geo.bbytes);
-        const int kc = 64 * l;
+        const int kc = G.a_k + 64 * l, kcb = G.b_k + 64 * l;
+        if (!pre) tc::mbar_expect_tx_e(&full_bar[st], tx);
         if (b.mcast) {
           // the cluster's CTAs share the A tile: K block kb is fetched once, by rank kb % cs, for all
-          if (kb % b.cs == (int)(blockIdx.x % b.cs)) {
-            const uint16_t mask = (uint16_t)((1u << b.cs) - 1u);
+          if ((kb & (cs - 1)) == rank) {
             if (!G.a_mn) {
-              tc::tma_load_2d_mc(As, am, G.a_k + kc, P.a_m + m0, &full_bar[st], mask);
+              tc::tma_load_2d_mc_e(As, am, kc, am0, &full_bar[st], mask);
             } else {
-              tc::tma_load_2d_mc(As, am, P.a_m + m0, G.a_k + kc, &full_bar[st], mask);
-              tc::tma_load_2d_mc(As + 8192, am, P.a_m + m0 + 64, G.a_k + kc, &full_bar[st], mask);
+              tc::tma_load_2d_mc_e(As, am, am0, kc, &full_bar[st], mask);
+              tc::tma_load_2d_mc_e(As + 8192, am, am0 + 64, kc, &full_bar[st], mask);
             }
           }
         } else if (!G.a_mn) {
-          tc::tma_load_2d(As, am, G.a_k + kc, P.a_m + m0, &full_bar[st]);
+          tc::tma_load_2d_e(As, am, kc, am0, &full_bar[st]);
         } else {
-          tc::tma_load_2d(As, am, P.a_m + m0, G.a_k + kc, &full_bar[st]);
-          tc::tma_load_2d(As + 8192, am, P.a_m + m0 + 64, G.a_k + kc, &full_bar[st]);
+          tc::tma_load_2d_e(As, am, am0, kc, &full_bar[st]);
+          tc::tma_load_2d_e(As + 8192, am, am0 + 64, kc, &full_bar[st]);
         }
-        for (int i = 0; i < geo.nbox_b && !pre; ++i) {
+        if (!pre) {
           if (!G.b_mn)
-            tc::tma_load_2d(Bs + i * geo.bnb * 128, bm, G.b_k + kc, P.b_n + n0 + geo.bnb * i, &full_bar[st]);
+            for (int i = 0; i < geo.nbox_b; ++i)
+              tc::tma_load_2d_e(Bs + i * geo.bnb * 128, bm, kcb, bn0 + geo.bnb * i, &full_bar[st]);
           else
-            tc::tma_load_2d(Bs + i * 8192, bm, P.b_n + n0 + 64 * i, G.b_k + kc, &full_bar[st]);
+            for (int i = 0; i < geo.nbox_b; ++i) tc::tma_load_2d_e(Bs + i * 8192, bm, bn0 + 64 * i, kcb, &full_bar[st]);
         }
-        // if (kb < 4) stamp(12 + kb);
+        if (++st == S) st = 0, ph ^= 1;
       }
     }
-    stamp_any(11);
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer ----------------
-    int kb = 0;
+    if (lane == 0) stamp_any(11);
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
+    const uint32_t smem0 = tc::smem_u32(smem), sbytes = (uint32_t)b.stage_bytes;
+    const uint32_t ones0 = tc::smem_u32(ones_tile);
+    int kb = 0, st = 0, ph = 0;
     for (int s = 0; s < P.nseg; ++s) {
       const GSeg& G = P.seg[s];
       const uint32_t id1 = tc::idesc_bf16_major(128, n1, G.a_mn, G.b_mn);
       const uint32_t id2 = tc::idesc_bf16_major(128, n2 > 0 ? n2 : 16, G.a_mn, G.b_mn);
       const uint32_t id_ones = tc::idesc_bf16_major(128, 16, G.a_mn, 0);
+      // K-advance per 16-wide step: 2 KB through an MN-major operand's rows, 32 B inside a K-major row
+      const uint32_t astep = G.a_mn ? 2048u : 32u, bstep = G.b_mn ? 2048u : 32u;
+      const uint32_t albo = G.a_mn ? 8192u : 16u, blbo = G.b_mn ? 8192u : 16u;
       for (int l = 0; l < G.nkb; ++l, ++kb) {
-        const int st = kb % S;
-        tc::mbar_wait(&full_bar[st], (kb / S) & 1);
-        if (kb == 0) stamp_any(8);
-        stamp_any(9);
+        tc::mbar_wait(&full_bar[st], ph);
+        if (lane == 0 && kb == 0) stamp_any(8);
+        if (lane == 0) stamp_any(9);
         tc::fence_after_sync();
-        const uint32_t a0 = tc::smem_u32(smem + st * b.stage_bytes), b0 = a0 + kABytes;
+        const uint32_t a0 = smem0 + st * sbytes, b0 = a0 + kABytes;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const uint64_t ad = G.a_mn ? tc::sdesc_sw128(a0 + 2048 * k, 8192, 1024) : tc::sdesc_sw128(a0 + 32 * k, 16, 1024);
-          const uint64_t bd = G.b_mn ? tc::sdesc_sw128(b0 + 2048 * k, 8192, 1024) : tc::sdesc_sw128(b0 + 32 * k, 16, 1024);
+          const uint64_t ad = tc::sdesc_sw128(a0 + astep * k, albo, 1024);
           const uint32_t acc = (kb | k) != 0;
-          tc::mma_bf16(tmem, ad, bd, id1, acc);
-          if (n2 > 0) {
-            const uint64_t bd2 = G.b_mn ? tc::sdesc_sw128(b0 + 32768 + 2048 * k, 8192, 1024)
-                                        : tc::sdesc_sw128(b0 + 32768 + 32 * k, 16, 1024);
-            tc::mma_bf16(tmem + 256, ad, bd2, id2, acc);
-          }
-          if (ones) tc::mma_bf16(tmem + ones_col, ad, tc::sdesc_sw128(tc::smem_u32(ones_tile) + 32 * k, 16, 1024), id_ones, acc);
+          if (!(b.dbg && b.dbg_nomma)) tc::mma_bf16_e(tmem, ad, tc::sdesc_sw128(b0 + bstep * k, blbo, 1024), id1, acc);
+          if (n2 > 0) tc::mma_bf16_e(tmem + 256, ad, tc::sdesc_sw128(b0 + 32768 + bstep * k, blbo, 1024), id2, acc);
+          if (ones) tc::mma_bf16_e(tmem + ones_col, ad, tc::sdesc_sw128(ones0 + 32 * k, 16, 1024), id_ones, acc);
         }
-        tc::mma_commit(&empty_bar[st]);
+        tc::mma_commit_e(&empty_bar[st]);
+        if (++st == S) st = 0, ph ^= 1;
       }
     }
-    tc::mma_commit(&done_bar);
+    tc::mma_commit_e(&done_bar);
   }
   __syncwarp();
   // one poller: 256 threads spinning in try_wait compete with the TMA's complete_tx traffic on
@@ -1263,6 +1271,8 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     // SQUINT_GEMM_DBG=k: only launch k records; SQUINT_GEMM_DBG=all: every launch gets its own
     // 64-tile slot (launch i at slot i % 256), for whole-update kernel-span timelines.
     static const char* dbg_env = getenv("SQUINT_GEMM_DBG");
+    static const char* nomma = getenv("SQUINT_GEMM_NOMMA");  // timing experiments only
+    b.dbg_nomma = nomma ? atoi(nomma) : 0;
     static int launch_no = 0;
     if (dbg_env) {
       const int me = launch_no++;

@@ -101,7 +101,8 @@ struct GBatch {
   int xpre_off;    // LayerNorm backward: smem offset of the prefetched x_hat boxes (0: loaded after the main loop)
   int prefetch_b;  // 1: B operands may be loaded before griddepcontrol.wait (not written by the
                    // immediately preceding kernel); set through GemmBuilder::prefetch_b
-  unsigned long long* dbg;  // optional per-CTA phase timestamps (globaltimer ns) [tile][8]
+  unsigned long long* dbg;  // optional per-CTA phase timestamps (globaltimer ns) [tile][16]
+  int dbg_nomma;            // with dbg: skip the MMAs (timing experiments; results invalid)
 };
 
 // Host-side builder: operands are registered as Mats; maps are created per use.
