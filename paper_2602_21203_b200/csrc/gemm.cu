@@ -700,6 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_sk(const __grid_constant__
       ++npre;
     }
   }
+  if (warp == 0) npre = __shfl_sync(0xffffffffu, npre, 0);  // the producer loop runs warp-wide
   tc::pdl_wait();
   tc::pdl_trigger();
   stamp(2);
@@ -742,50 +743,59 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_sk(const __grid_constant__
       s_beta[c] = (ok && P.beta) ? P.beta[c] : 0.f;
     }
   }
-  if (warp == 0 && lane == 0) {
-    tc::mbar_expect_tx(&recv_bar, kSkRecvBytes);
+  if (warp == 0) {
+    // producer: warp-uniform loop, one elected lane issues (see k_gemm)
+    tc::mbar_expect_tx_e(&recv_bar, kSkRecvBytes);
+    const int sbytes = b.stage_bytes;
+    int st = 0, ph = 0;
     for (int kb = kb0; kb < kb1; ++kb) {
-      const int i = kb - kb0, st = i % S;
+      const int i = kb - kb0;
       int l;
       const GSeg& G = P.seg[seg_of(kb, l)];
       const TileGeo geo = tile_geo(P, nreal, G.b_mn);
-      if (i >= S) tc::mbar_wait(&empty_bar[st], ((i / S) - 1) & 1);
-      uint8_t* As = smem + st * b.stage_bytes;
+      if (i >= S) tc::mbar_wait(&empty_bar[st], ph ^ 1);
+      uint8_t* As = smem + st * sbytes;
       uint8_t* Bs = As + kABytes;
       const bool pre = i < npre;
-      if (!pre) tc::mbar_expect_tx(&full_bar[st], kABytes + geo.bbytes);
+      if (!pre) tc::mbar_expect_tx_e(&full_bar[st], kABytes + geo.bbytes);
       const int kc = 64 * l;
       if (!G.a_mn) {
-        tc::tma_load_2d(As, &b.maps[G.amap], G.a_k + kc, P.a_m + m0, &full_bar[st]);
+        tc::tma_load_2d_e(As, &b.maps[G.amap], G.a_k + kc, P.a_m + m0, &full_bar[st]);
       } else {
-        tc::tma_load_2d(As, &b.maps[G.amap], P.a_m + m0, G.a_k + kc, &full_bar[st]);
-        tc::tma_load_2d(As + 8192, &b.maps[G.amap], P.a_m + m0 + 64, G.a_k + kc, &full_bar[st]);
+        tc::tma_load_2d_e(As, &b.maps[G.amap], P.a_m + m0, G.a_k + kc, &full_bar[st]);
+        tc::tma_load_2d_e(As + 8192, &b.maps[G.amap], P.a_m + m0 + 64, G.a_k + kc, &full_bar[st]);
       }
-      for (int j = 0; j < geo.nbox_b && !pre; ++j) {
-        if (!G.b_mn)
-          tc::tma_load_2d(Bs + j * geo.bnb * 128, &b.maps[G.bmap], G.b_k + kc, P.b_n + geo.bnb * j, &full_bar[st]);
-        else
-          tc::tma_load_2d(Bs + j * 8192, &b.maps[G.bmap], P.b_n + 64 * j, G.b_k + kc, &full_bar[st]);
+      if (!pre) {
+        for (int j = 0; j < geo.nbox_b; ++j) {
+          if (!G.b_mn)
+            tc::tma_load_2d_e(Bs + j * geo.bnb * 128, &b.maps[G.bmap], G.b_k + kc, P.b_n + geo.bnb * j, &full_bar[st]);
+          else
+            tc::tma_load_2d_e(Bs + j * 8192, &b.maps[G.bmap], P.b_n + 64 * j, G.b_k + kc, &full_bar[st]);
+        }
       }
+      if (++st == S) st = 0, ph ^= 1;
     }
-  } else if (warp == 1 && lane == 0) {
+  } else if (warp == 1) {
+    int st = 0, ph = 0;
+    const uint32_t smem0 = tc::smem_u32(smem), sbytes = (uint32_t)b.stage_bytes;
     for (int kb = kb0; kb < kb1; ++kb) {
-      const int i = kb - kb0, st = i % S;
+      const int i = kb - kb0;
       int l;
       const GSeg& G = P.seg[seg_of(kb, l)];
       const uint32_t id = tc::idesc_bf16_major(128, nt, G.a_mn, G.b_mn);
-      tc::mbar_wait(&full_bar[st], (i / S) & 1);
+      const uint32_t astep = G.a_mn ? 2048u : 32u, bstep = G.b_mn ? 2048u : 32u;
+      const uint32_t albo = G.a_mn ? 8192u : 16u, blbo = G.b_mn ? 8192u : 16u;
+      tc::mbar_wait(&full_bar[st], ph);
       tc::fence_after_sync();
-      const uint32_t a0 = tc::smem_u32(smem + st * b.stage_bytes), b0 = a0 + kABytes;
+      const uint32_t a0 = smem0 + st * sbytes, b0 = a0 + kABytes;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint64_t ad = G.a_mn ? tc::sdesc_sw128(a0 + 2048 * k, 8192, 1024) : tc::sdesc_sw128(a0 + 32 * k, 16, 1024);
-        const uint64_t bd = G.b_mn ? tc::sdesc_sw128(b0 + 2048 * k, 8192, 1024) : tc::sdesc_sw128(b0 + 32 * k, 16, 1024);
-        tc::mma_bf16(tmem, ad, bd, id, (i | k) != 0);
-      }
-      tc::mma_commit(&empty_bar[st]);
+      for (int k = 0; k < 4; ++k)
+        tc::mma_bf16_e(tmem, tc::sdesc_sw128(a0 + astep * k, albo, 1024), tc::sdesc_sw128(b0 + bstep * k, blbo, 1024), id,
+                       (i | k) != 0);
+      tc::mma_commit_e(&empty_bar[st]);
+      if (++st == S) st = 0, ph ^= 1;
     }
-    tc::mma_commit(&done_bar);
+    tc::mma_commit_e(&done_bar);
   }
   __syncwarp();
   if (tid == 0) tc::mbar_wait(&done_bar, 0);
