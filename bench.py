@@ -247,11 +247,22 @@ def run_gpu(args):
     obs_ring = R["obs"]
     next_ring = R["next_obs"]
 
+    side = torch.cuda.Stream(device=dev)
+    ins_fork, ins_done = torch.cuda.Event(), torch.cuda.Event()
+
     def step(pool, stream=None):
+        # act (o_t) and the insert of o_{t+1} are independent: the insert (HBM-bound) runs on a
+        # side stream beside the act's MLP; the updates wait for both (they may sample the new rows)
         fr, nx = pools[pool]
+        cur = stream if stream is not None else torch.cuda.current_stream()
+        ins_fork.record(cur)
+        side.wait_event(ins_fork)
+        with torch.cuda.stream(side):
+            P.squint_insert(nx, 8, slots_s, next_ring, stream=side)
+            ins_done.record(side)
         P.squint_act(L.dims, L.hp, L.actor, L.critic, fr, prop_s, aeps_s, act_out, logp_out, act_ws,
                      ring=obs_ring, slots=slots_s, stream=stream)
-        P.squint_insert(nx, 8, slots_s, next_ring, stream=stream)
+        cur.wait_event(ins_done)
         L.update(replay, idx_s, sh_s, eps_s, metrics, stream=stream)
 
     def load_inputs(k):

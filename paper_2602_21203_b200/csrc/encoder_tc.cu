@@ -213,27 +213,45 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ 
       }
     } else {
       // squint: 8x8 block sums of 128x128 frames, round half to even (Q1), optional ring write
+      // (img, ch, oy, 16-byte column chunk) items; a thread keeps the loads of kU items (kU x 8 x
+      // 16 bytes) in flight before reducing them: the frames stream from HBM once, and the per-SM
+      // memory-level parallelism sets the rate
       const uint8_t* Fr = a.src[0];
-      for (int e = tid; e < kGF * 3 * 16 * 8; e += kThr) {  // (img, ch, oy, 16-byte column chunk)
-        const int ck = e & 7, t1 = e >> 3, oy = t1 & 15, t2 = t1 >> 4, cc = t2 % 3, i = t2 / 3;
-        const int b = b0 + i;
-        uint32_t lo = 0, hi = 0;
-        if (b < a.B) {
-          const uint8_t* s = Fr + (((int64_t)b * 3 + cc) * 128 + oy * 8) * 128 + ck * 16;
-          uint4 v[8];
+      constexpr int kItems = kGF * 3 * 16 * 8, kU = 3;
+      for (int e0 = tid; e0 < kItems; e0 += kU * kThr) {
+        uint4 v[kU][8];
 #pragma unroll
-          for (int r = 0; r < 8; ++r) v[r] = __ldcs(reinterpret_cast<const uint4*>(s + r * 128));
+        for (int u = 0; u < kU; ++u) {
+          const int e = e0 + u * kThr;
+          const int ck = e & 7, t1 = e >> 3, oy = t1 & 15, t2 = t1 >> 4, cc = t2 % 3, i = t2 / 3;
+          const int b = b0 + i;
+          if (e < kItems && b < a.B) {
+            const uint8_t* s = Fr + (((int64_t)b * 3 + cc) * 128 + oy * 8) * 128 + ck * 16;
 #pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            lo = __dp4a(v[r].x, 0x01010101u, __dp4a(v[r].y, 0x01010101u, lo));
-            hi = __dp4a(v[r].z, 0x01010101u, __dp4a(v[r].w, 0x01010101u, hi));
+            for (int r = 0; r < 8; ++r) v[u][r] = __ldcs(reinterpret_cast<const uint4*>(s + r * 128));
+          } else {
+#pragma unroll
+            for (int r = 0; r < 8; ++r) v[u][r] = make_uint4(0, 0, 0, 0);
           }
         }
-        const uint32_t q0 = rhe64(lo), q1 = rhe64(hi);
-        const int p = (i * 3 + cc) * 256 + oy * 16 + 2 * ck;
-        *reinterpret_cast<uint16_t*>(xs + p) = (uint16_t)(q0 | (q1 << 8));
-        if (b < a.B && a.ring)
-          *reinterpret_cast<uint16_t*>(a.ring + (a.slots[b] * 3 + cc) * 256 + oy * 16 + 2 * ck) = (uint16_t)(q0 | (q1 << 8));
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int e = e0 + u * kThr;
+          if (e >= kItems) continue;
+          const int ck = e & 7, t1 = e >> 3, oy = t1 & 15, t2 = t1 >> 4, cc = t2 % 3, i = t2 / 3;
+          const int b = b0 + i;
+          uint32_t lo = 0, hi = 0;
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            lo = __dp4a(v[u][r].x, 0x01010101u, __dp4a(v[u][r].y, 0x01010101u, lo));
+            hi = __dp4a(v[u][r].z, 0x01010101u, __dp4a(v[u][r].w, 0x01010101u, hi));
+          }
+          const uint32_t q0 = rhe64(lo), q1 = rhe64(hi);
+          const int p = (i * 3 + cc) * 256 + oy * 16 + 2 * ck;
+          *reinterpret_cast<uint16_t*>(xs + p) = (uint16_t)(q0 | (q1 << 8));
+          if (b < a.B && a.ring)
+            *reinterpret_cast<uint16_t*>(a.ring + (a.slots[b] * 3 + cc) * 256 + oy * 16 + 2 * ck) = (uint16_t)(q0 | (q1 << 8));
+        }
       }
     }
     for (int jb = 0; jb < a.ngj[src]; ++jb) {

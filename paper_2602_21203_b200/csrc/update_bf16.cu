@@ -1118,6 +1118,23 @@ squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const flo
     fwd(gb, c.mat(Xh), ap, GE_LN_TANH, c.bp(Xa), Xa.ld, hp.ln_eps);
     BF_CK(gemm_launch(gb, s));
   }
+  static const bool no_chain = getenv("SQUINT_NO_CHAIN") != nullptr;
+  if (!no_chain && chain_supported(Ha)) {
+    // the whole actor MLP + tanh-Gaussian head in one fused chain launch
+    ChainBuilder cb(1);
+    CProb& pa = cb.add(M, c.mat(Xa));
+    ch_fwd(cb, pa, GE_LN_RELU, am.l1, Ha, npi, none_mat(), none_mat(), nullptr, hp.ln_eps);
+    ch_fwd(cb, pa, GE_LN_RELU, am.l2, Ha, Ha, none_mat(), none_mat(), nullptr, hp.ln_eps);
+    CLayer& tg = cb.layer(pa, GE_TG_FWD, am.l3.w, 0, 2 * d.action_dim, Ha, none_mat(), none_mat());
+    tg.bias = am.l3.b;
+    tg.eps = eps;
+    tg.act = action_out;
+    tg.logp = logp_out;
+    tg.lo = hp.log_std_min;
+    tg.hi = hp.log_std_max;
+    BF_CK(chain_launch(cb, s));
+    return SQUINT_OK;
+  }
   {
     GemmBuilder gb(1);
     fwd(gb, c.mat(Xa), am.l1, GE_LN_RELU, c.bp(H1), H1.ld, hp.ln_eps);
