@@ -208,13 +208,14 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
 // nodes) while the actor-loss chain proceeds; the branch joins before the metrics kernel.
 struct Aux {
   cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, scal = nullptr, join = nullptr, alpha = nullptr;
+  cudaEvent_t fork = nullptr, scal = nullptr, join = nullptr, alpha = nullptr, qdone = nullptr;
   bool ok() {
     if (s) return true;
     return cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
            cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&scal, cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&alpha, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&qdone, cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
   }
 };
@@ -771,7 +772,6 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       // weight tiles (needs the stepped encoder) on the branch as well
       BF_CK(launch_polyak_shadow(st.critic_target, st.critic + L.enc_end, L.gsize[gT], hp.tau, &shT, es));
       BF_CK(launch_conv_tiles(crit + L.off(gC, "enc.conv1.w"), crit + L.off(gC, "enc.conv2.w"), C, wtiles, es));
-      BF_CK(cudaEventRecord(c.aux->join, es));
     } else {
       BF_CK(launch_adam_shadow(st.critic, gc, st.m_critic, st.v_critic, L.gsize[gC], hp.lr_critic, hp.beta1,
                                hp.beta2, hp.adam_eps, scal + S_C1_CRITIC, scal + S_C2_CRITIC, c.F(w.adam_part), &shC,
@@ -844,6 +844,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     q.row_lpi = c.F(w.row_lpi);
     if (branch) BF_CK(cudaStreamWaitEvent(s, c.aux->alpha, 0));  // alpha+ from the branch
     BF_CK(launch_actor_q(q, s));
+    if (branch) BF_CK(cudaEventRecord(c.aux->qdone, s));  // the metrics run on the branch
   }
   {
     PhaseScope ps(13, rep, s);
@@ -953,8 +954,11 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
                            hp.adam_eps, scal + S_C1_ACTOR, scal + S_C2_ACTOR, nullptr, &shA, s, 0, kAdamBlocks, 1));
   // a14: Polyak over every critic tensor except the encoder (+ target shadow)
   if (!branch) BF_CK(launch_polyak_shadow(st.critic_target, st.critic + L.enc_end, L.gsize[gT], hp.tau, &shT, s));
-  if (branch) BF_CK(cudaStreamWaitEvent(s, c.aux->join, 0));  // join the encoder branch
   {
+    // metrics need the alpha step, all critic Adam partials and the actor-loss rows: on the
+    // branch (after k_actor_q) they stay off the main stream's actor backward
+    cudaStream_t ms = branch ? es : s;
+    if (branch) BF_CK(cudaStreamWaitEvent(es, c.aux->qdone, 0));
     MetricsArgs m;
     memset(&m, 0, sizeof(m));
     m.npart = branch ? kAdamBlocks + kEncAdamBlocks : kAdamBlocks;
@@ -968,7 +972,11 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     m.out = metrics;
     m.reduce_local = comm ? 0 : 1;
     m.extras2 = lpis;
-    BF_CK(launch_metrics(m, s));
+    BF_CK(launch_metrics(m, ms));
+    if (branch) {
+      BF_CK(cudaEventRecord(c.aux->join, es));
+      BF_CK(cudaStreamWaitEvent(s, c.aux->join, 0));  // join the branch before the next update
+    }
   }
   return SQUINT_OK;
 }
