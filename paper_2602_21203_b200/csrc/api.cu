@@ -879,7 +879,9 @@ squint_status squint_update(const squint_dims* dims, const squint_hparams* hp, c
       cudaGetLastError();
       cs = cudaStreamCaptureStatusActive;  // unknown: launch directly
     }
-    static const bool no_graph = getenv("SQUINT_NO_GRAPH") != nullptr || getenv("SQUINT_DEBUG_SYNC") != nullptr;
+    // (the debug switches allocate or synchronise inside their launches: no capture with them)
+    static const bool no_graph = getenv("SQUINT_NO_GRAPH") || getenv("SQUINT_DEBUG_SYNC") || getenv("SQUINT_GEMM_DBG") ||
+                                 getenv("SQUINT_CHAIN_DBG") || getenv("SQUINT_ENC_DBG") || getenv("SQUINT_TCE_DBG");
     const bool branch = bf16_prepare();
     if (no_graph || cm || cs != cudaStreamCaptureStatusNone || instrumentation_active())
       return bf16_update(*dims, *hp, *replay, idx, shifts, eps, utd, *state, metrics, workspace, workspace_bytes, cm, s);

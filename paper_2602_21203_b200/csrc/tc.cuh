@@ -308,6 +308,11 @@ __device__ __forceinline__ void st_async_v2(uint32_t dst, float a, float b, uint
                "f"(b), "r"(mbar)
                : "memory");
 }
+__device__ __forceinline__ void st_async_v4(uint32_t dst, float a, float b, float c, float d, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(dst),
+               "f"(a), "f"(b), "f"(c), "f"(d), "r"(mbar)
+               : "memory");
+}
 // split cluster barrier: arrive (no memory ordering) now, wait later
 __device__ __forceinline__ void cluster_arrive_relaxed() {
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");

@@ -58,7 +58,7 @@ struct BfLay {
   BM dlog, dlog1;  // [2B][N] (head i = rows i*B ...)
   BM dA2c[2], dA1c[2], dA2a[2], dA1a[2], dAp, dh, dO, adA2, adA1, adAp;
   size_t R1ac, R2ac, Rpq, Rpp, Rpq1, qR1[2], qR2[2], q1R1[2], q1R2[2];
-  size_t tlogits, logits, logits1, m, tgo_ac, a_cur, logp_cur, logp_next, row_loss, row_q, row_lpi;
+  size_t tlogits, logits, logits1, m, tgo_ac, a_cur, logp_cur, logp_next, row_loss, row_q, row_lpi, q_heads;
   size_t part_q2[2], part_q1[2], part_pq, part_a2, part_a1, part_pp;
   size_t grad_critic, grad_actor, adam_part, scal, lpi_sums;
   size_t y1b, img0, dA1enc, enc_part, wtiles;
@@ -177,6 +177,7 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
   w.row_loss = fl(B);
   w.row_q = fl(B);
   w.row_lpi = fl(B);
+  w.q_heads = fl(2 * B);
   const size_t mt = mtiles(B);
   for (int i = 0; i < 2; ++i) {
     w.part_q2[i] = fl(mt * 3 * Hc);
@@ -778,7 +779,12 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
                                s, 0, kAdamBlocks, 1));
     }
   }
-  // a12: actor loss against theta+ on sg(h) (Q19)
+  // a12: actor loss against theta+ on sg(h) (Q19).  SQUINT_FUSE_Q=1 (single GPU, chains): the
+  // actor-Q step (softmax, Q_i, dL_pi/dl) runs in the theta+ chain's last layer instead of
+  // k_actor_q -- off by default: the cross-CTA softmax exchange waits for the cluster's slowest
+  // CTA and measured ~2 us slower per update than the separate kernel
+  static const bool fuse_env = getenv("SQUINT_FUSE_Q") != nullptr;
+  const bool fuse_q = fuse_env && c.chain && comm == nullptr;
   {
     PhaseScope ps(12, rep, s);
     const Lin cproj1 = proj(c, w.sh[0], crit, gC, "critic");  // same buffers, now theta+
@@ -799,6 +805,14 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
         l3.bias = cq1[i].l3.b;
         l3.outf = c.F(w.logits1) + (size_t)i * B * N;
         l3.ldf = N;
+        if (fuse_q) {  // k_actor_q's work in the chain's last layer (Q25)
+          l3.q_out = c.F(w.q_heads) + (size_t)i * B;
+          l3.dq = c.halfp(w.dlog1, i);
+          l3.ld_dq = w.dlog1.ld;
+          l3.v_min = d.v_min;
+          l3.v_max = d.v_max;
+          l3.q_scale = -0.5f * inv_btotal;
+        }
       }
       BF_CK(chain_launch(cb, s));
     } else {
@@ -842,8 +856,10 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     q.ld_dl = w.dlog1.ld;
     q.row_q = c.F(w.row_q);
     q.row_lpi = c.F(w.row_lpi);
-    if (branch) BF_CK(cudaStreamWaitEvent(s, c.aux->alpha, 0));  // alpha+ from the branch
-    BF_CK(launch_actor_q(q, s));
+    if (!fuse_q) {
+      if (branch) BF_CK(cudaStreamWaitEvent(s, c.aux->alpha, 0));  // alpha+ from the branch
+      BF_CK(launch_actor_q(q, s));
+    }
     if (branch) BF_CK(cudaEventRecord(c.aux->qdone, s));  // the metrics run on the branch
   }
   {
@@ -889,6 +905,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       p.tgo = c.F(w.tgo_ac);
       p.eps = eps_cur;
       p.dlogp_scale = scal + S_ALPHA1_SCALE;
+      if (fuse_q && branch) BF_CK(cudaStreamWaitEvent(s, c.aux->alpha, 0));  // alpha+ from the branch
       p.lo = hp.log_std_min;
       p.hi = hp.log_std_max;
       p.out = c.bp(w.dO);
@@ -966,6 +983,10 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     m.inv_btotal = inv_btotal;
     m.row_lpi = c.F(w.row_lpi);
     m.row_q = c.F(w.row_q);
+    if (fuse_q) {
+      m.q_heads = c.F(w.q_heads);
+      m.logp = c.F(w.logp_cur);
+    }
     m.sumsq_part = c.F(w.adam_part);
     m.scal = scal;
     m.extras = extras;
