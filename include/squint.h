@@ -221,9 +221,11 @@ SQUINT_API const char* squint_phase_name(int k);
  * launch (i < n), so consecutive events bracket one launch including any gap after it.
  * Returns the number of events recorded since the previous call; NULL/0 disables. */
 SQUINT_API int squint_set_launch_events(void** events, int n);
-/* Host options for instrumentation: key 1 = run the bf16 update's encoder-backward branch on an
+/* Host options (per process): key 1 = run the bf16 update's encoder-backward branch on an
  * auxiliary stream (1, default) or inline on the caller's stream (0; a launch timeline then
- * brackets consecutive launches of one stream). */
+ * brackets consecutive launches of one stream); key 2 = pipeline each update's critic-side
+ * forward (encoder, critic/target projections, online heads) onto the previous update's branch
+ * (0, default; needs key 1).  Errors: EINVAL for an unknown key. */
 SQUINT_API squint_status squint_set_option(int key, int value);
 /* Records the next timeline event on `stream` without a launch (closes the last interval). */
 SQUINT_API squint_status squint_record_launch_event(squint_stream_t stream);

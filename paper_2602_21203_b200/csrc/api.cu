@@ -898,6 +898,8 @@ squint_status squint_update(const squint_dims* dims, const squint_hparams* hp, c
     put(&utd, sizeof(utd));
     put(&workspace_bytes, sizeof(workspace_bytes));
     put(&branch, sizeof(branch));
+    const int opts = bf16_options();
+    put(&opts, sizeof(opts));
     struct Entry {
       std::string key;
       cudaGraphExec_t exec;

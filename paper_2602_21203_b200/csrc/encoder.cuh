@@ -44,6 +44,7 @@ struct EncFwdArgs {
   int ngj[2];
   const uint8_t* wtiles;   // tensor-core path: conv weights as swizzled bf16 smem images (k_conv_tiles)
   int dbg;                 // phase timestamps (SQUINT_ENC_DBG; set by the launcher)
+  int max_ctas;            // tensor-core path: grid cap (0: one CTA per job, at most one per SM)
 };
 
 struct EncBwdArgs {

@@ -693,7 +693,8 @@ int launch_fwd_c(const EncFwdArgs& a, cudaStream_t s) {
   const size_t smem = FwdL<C>::total + 1024;
   cudaFuncSetAttribute(k_enc_fwd_tc<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int total = ((a.B + kGF - 1) / kGF) * a.nsrc;
-  const int grid = total < 148 ? total : 148;
+  const int cap = a.max_ctas > 0 && a.max_ctas < 148 ? a.max_ctas : 148;
+  const int grid = total < cap ? total : cap;
   launch_pdl(k_enc_fwd_tc<C>, grid, dim3(kThr), smem, s, a);
   return (int)cudaGetLastError();
 }

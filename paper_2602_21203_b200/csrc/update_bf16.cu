@@ -52,6 +52,7 @@ struct ShadowPlan {
 
 struct BfLay {
   BM Xh, Xhn, Xq, Xt, Xq1, Xan, Xac;
+  BM Xh_alt, Xq1_alt, Xac_alt;  // odd updates (the pipelined forward of update j+1 runs beside j)
   BM H1an, H2an, H1ac, H2ac;
   BM tqH1[2], tqH2[2], qH1[2], qH2[2], q1H1[2], q1H2[2];
   BM XH1ac, XH2ac, XHpq, XHpp, XHpq1, qXH1[2], qXH2[2], q1XH1[2], q1XH2[2];  // bf16 LN caches x_hat
@@ -122,6 +123,9 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
   w.Xq1 = bm(B, nq);
   w.Xan = bm(B, npi);
   w.Xac = bm(B, npi);
+  w.Xh_alt = bm(B, F);
+  w.Xq1_alt = bm(B, nq);
+  w.Xac_alt = bm(B, npi);
   w.H1an = bm(B, Ha);
   w.H2an = bm(B, Ha);
   w.H1ac = bm(B, Ha);
@@ -210,6 +214,7 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
 struct Aux {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, scal = nullptr, join = nullptr, alpha = nullptr, qdone = nullptr;
+  cudaEvent_t enc = nullptr, chn = nullptr;  // pipelined forward of the next update: encoder + projections, online heads
   bool ok() {
     if (s) return true;
     return cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
@@ -217,6 +222,8 @@ struct Aux {
            cudaEventCreateWithFlags(&scal, cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&alpha, cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&qdone, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&enc, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&chn, cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
   }
 };
@@ -224,6 +231,10 @@ thread_local Aux t_aux;
 // instrumentation (squint_set_option): 0 disables the auxiliary branch, so a launch timeline's
 // consecutive events bracket consecutive launches of one stream
 int g_branch_enabled = 1;
+// option 2: pipeline the next update's critic-side forward onto the branch (early_fwd); off by
+// default -- on B200 it measured even with the separate forward (the encoder backward that
+// precedes it on the branch and the SMs it occupies set the pace), kept for other shapes
+int g_pipe_enabled = 0;
 
 struct Ctx {
   const squint_dims& d;
@@ -375,9 +386,116 @@ ShadowTable table_at(const Ctx& c, const ShadowPlan& sp) {
   return t;
 }
 
-squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp, const squint_replay& R,
+// one update's random inputs
+struct UpdIn {
+  const int64_t* idx;
+  const uint8_t* sh;
+  const float* eps;
+  int rep;
+};
+
+// Update j's buffers: the matrices the pipelined forward of update j + 1 writes while update j's
+// actor pass still reads them alternate by update parity.
+BfLay with_parity(const BfLay& w, int par) {
+  BfLay v = w;
+  if (par & 1) {
+    v.Xh = w.Xh_alt;
+    v.Xq1 = w.Xq1_alt;
+    v.Xac = w.Xac_alt;
+  }
+  return v;
+}
+
+// The part of an update's forward that depends only on the critic (theta), the target (theta_bar)
+// and the replay rows, not on the actor: gather + shift + encoder (obs and next_obs), the critic
+// and target projections and the online heads.  Pipelined (single GPU, chains): issued on the
+// auxiliary branch of the previous update, beside its actor pass; enc_ev / chn_ev mark the
+// encoder + projections and the online heads.
+squint_status early_fwd(const Ctx& c, const BfLay& w_in, const squint_hparams& hp, const squint_replay& R,
+                        const UpdIn& u, const squint_state& st, int par, cudaStream_t ss, int enc_ctas,
+                        cudaEvent_t enc_ev, cudaEvent_t chn_ev) {
+  const BfLay w = with_parity(w_in, par);
+  const squint_dims& d = c.d;
+  const Layout& L = c.L;
+  const int B = d.batch, Lt = d.latent, Hc = d.critic_hidden, N = d.n_atoms, A = d.action_dim, P = d.proprio_dim,
+            C = d.conv_ch;
+  const int nq = Lt + P + A;
+  const float le = hp.ln_eps;
+  const int gC = SQUINT_GROUP_CRITIC, gT = SQUINT_GROUP_TARGET;
+  const float* crit = st.critic;
+  const float* tgt = st.critic_target;
+  const Lin cproj = proj(c, w.sh[0], crit, gC, "critic"), tproj = proj(c, w.sh[1], tgt, gT, "critic");
+  const Mlp cq[2] = {mlp(c, w.sh[0], crit, gC, kHeads[0]), mlp(c, w.sh[0], crit, gC, kHeads[1])};
+  {
+    PhaseScope ps(3, u.rep, ss);
+    EncFwdArgs e;
+    memset(&e, 0, sizeof(e));
+    e.mode = 0;
+    e.src[0] = R.obs;
+    e.src[1] = R.next_obs;
+    e.idx = u.idx;
+    e.shifts = u.sh;
+    e.B = B;
+    e.nsrc = 2;
+    e.w1 = crit + L.off(gC, "enc.conv1.w");
+    e.b1 = crit + L.off(gC, "enc.conv1.b");
+    e.w2 = crit + L.off(gC, "enc.conv2.w");
+    e.b2 = crit + L.off(gC, "enc.conv2.b");
+    e.hb[0] = c.bp(w.Xh);
+    e.hb[1] = c.bp(w.Xhn);
+    e.h_ld = w.Xh.ld;
+    e.y1b = reinterpret_cast<bf16*>(c.ws + w.y1b);
+    e.img0 = reinterpret_cast<uint8_t*>(c.ws + w.img0);
+    e.C = C;
+    e.c_in = d.img_c;
+    e.H = d.img_h;
+    e.pad = d.pad;
+    e.gj[0][0] = GatherJob{R.proprio, P, c.bp(w.Xq), w.Xq.ld, Lt, 1};
+    e.gj[0][1] = GatherJob{R.action, A, c.bp(w.Xq), w.Xq.ld, Lt + P, 1};
+    e.gj[0][2] = GatherJob{R.proprio, P, c.bp(w.Xac), w.Xac.ld, Lt, 1};
+    e.gj[0][3] = GatherJob{R.proprio, P, c.bp(w.Xq1), w.Xq1.ld, Lt, 1};
+    e.ngj[0] = 4;
+    e.gj[1][0] = GatherJob{R.next_proprio, P, c.bp(w.Xt), w.Xt.ld, Lt, 1};
+    e.gj[1][1] = GatherJob{R.next_proprio, P, c.bp(w.Xan), w.Xan.ld, Lt, 1};
+    e.ngj[1] = 2;
+    e.wtiles = reinterpret_cast<uint8_t*>(c.ws + w.wtiles);
+    e.max_ctas = enc_ctas;
+    BF_CK(launch_enc_fwd_tc(e, ss));
+  }
+  {
+    PhaseScope ps(4, u.rep, ss);
+    GemmBuilder gb(1);
+    GProb* p = &fwd(gb, c.mat(w.Xh), cproj, GE_LN_TANH, c.bp(w.Xq), w.Xq.ld, le);
+    p->xh = c.bp(w.XHpq), p->ldx = w.XHpq.ld, p->rstd = c.F(w.Rpq);
+    fwd(gb, c.mat(w.Xhn), tproj, GE_LN_TANH, c.bp(w.Xt), w.Xt.ld, le);
+    BF_CK(gemm_launch(gb, ss));
+  }
+  if (enc_ev) BF_CK(cudaEventRecord(enc_ev, ss));
+  {
+    PhaseScope ps(6, u.rep, ss);
+    ChainBuilder cb(1);
+    for (int i = 0; i < 2; ++i) {
+      CProb& p = cb.add(B, c.mat(w.Xq));
+      ch_fwd(cb, p, GE_LN_RELU, cq[i].l1, Hc, nq, c.mat(w.qH1[i]), c.mat(w.qXH1[i]), c.F(w.qR1[i]), le);
+      ch_fwd(cb, p, GE_LN_RELU, cq[i].l2, Hc, Hc, c.mat(w.qH2[i]), c.mat(w.qXH2[i]), c.F(w.qR2[i]), le);
+      CLayer& l3 = cb.layer(p, GE_BIAS_F32, cq[i].l3.w, 0, N, Hc, none_mat(), none_mat());
+      l3.bias = cq[i].l3.b;
+      l3.outf = c.F(w.logits) + (size_t)i * B * N;
+      l3.ldf = N;
+    }
+    BF_CK(chain_launch(cb, ss));
+  }
+  if (chn_ev) BF_CK(cudaEventRecord(chn_ev, ss));
+  return SQUINT_OK;
+}
+
+// pipe: the early forward of this update already ran (early_fwd); next: the following update's
+// inputs (its early forward is issued on this update's branch), NULL for the last update
+squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& hp, const squint_replay& R,
                          const int64_t* idx, const uint8_t* sh, const float* eps, const squint_state& st,
-                         float* metrics, Comm* comm, float inv_btotal, int rep) {
+                         float* metrics, Comm* comm, float inv_btotal, int rep, int par, bool pipe,
+                         const UpdIn* next) {
+  const BfLay w = with_parity(w_in, par);
   const squint_dims& d = c.d;
   const Layout& L = c.L;
   cudaStream_t s = c.s;
@@ -406,7 +524,18 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
   // update's branch (or by the call prologue)
   const bool branch = comm == nullptr && c.aux != nullptr;
   if (!branch) BF_CK(launch_conv_tiles(crit + L.off(gC, "enc.conv1.w"), crit + L.off(gC, "enc.conv2.w"), C, wtiles, s));
-  {
+  if (pipe) {
+    // encoder, critic/target projections and online heads came from early_fwd (on the previous
+    // update's branch, or the call prologue): the actor projections need the encoder output
+    BF_CK(cudaStreamWaitEvent(s, c.aux->enc, 0));
+    PhaseScope ps(4, rep, s);
+    GemmBuilder gb(1);
+    fwd(gb, c.mat(w.Xhn), aproj, GE_LN_TANH, c.bp(w.Xan), w.Xan.ld, le);
+    GProb& p = fwd(gb, c.mat(w.Xh), aproj, GE_LN_TANH, c.bp(w.Xac), w.Xac.ld, le);
+    p.xh = c.bp(w.XHpp), p.ldx = w.XHpp.ld, p.rstd = c.F(w.Rpp);
+    BF_CK(gemm_launch(gb, s));
+  }
+  if (!pipe) {
     PhaseScope ps(3, rep, s);
     EncFwdArgs e;
     memset(&e, 0, sizeof(e));
@@ -442,7 +571,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     BF_CK(launch_enc_fwd_tc(e, s));
   }
   // a6: projections Linear -> LN -> tanh (Q8): critic(h), target(h'), actor(h'), actor(h)
-  {
+  if (!pipe) {
     PhaseScope ps(4, rep, s);
     GemmBuilder gb(1);
     GProb* p = &fwd(gb, c.mat(w.Xh), cproj, GE_LN_TANH, c.bp(w.Xq), w.Xq.ld, le);
@@ -532,7 +661,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       l3.outf = c.F(w.tlogits) + (size_t)i * B * N;
       l3.ldf = N;
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 2 && !pipe; ++i) {
       CProb& p = cb.add(B, c.mat(w.Xq));
       ch_fwd(cb, p, GE_LN_RELU, cq[i].l1, Hc, nq, c.mat(w.qH1[i]), c.mat(w.qXH1[i]), c.F(w.qR1[i]), le);
       ch_fwd(cb, p, GE_LN_RELU, cq[i].l2, Hc, Hc, c.mat(w.qH2[i]), c.mat(w.qXH2[i]), c.F(w.qR2[i]), le);
@@ -542,6 +671,7 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       l3.ldf = N;
     }
     BF_CK(chain_launch(cb, s));
+    if (pipe) BF_CK(cudaStreamWaitEvent(s, c.aux->chn, 0));  // online logits (early_fwd)
   } else {
     PhaseScope ps(6, rep, s);
     {
@@ -656,6 +786,9 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
   // (overlaps the critic dW GEMM and the actor-loss chain), inline when the gradients are
   // all-reduced
   cudaStream_t es = branch ? c.aux->s : s;
+  // pipelined: the previous update's branch (its metrics and this update's early forward) must
+  // be done before this update's weight gradients and Adam overwrite what it reads
+  if (pipe && rep > 0) BF_CK(cudaStreamWaitEvent(s, c.aux->join, 0));
   float* extras = gc + L.gsize[gC];
   float* scal = c.F(w.scal);
   auto scalars = [&](cudaStream_t ss) -> squint_status {
@@ -773,6 +906,13 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
       // weight tiles (needs the stepped encoder) on the branch as well
       BF_CK(launch_polyak_shadow(st.critic_target, st.critic + L.enc_end, L.gsize[gT], hp.tau, &shT, es));
       BF_CK(launch_conv_tiles(crit + L.off(gC, "enc.conv1.w"), crit + L.off(gC, "enc.conv2.w"), C, wtiles, es));
+      if (pipe && next) {
+        // the next update's critic-side forward, beside this update's actor pass (encoder grid
+        // capped so the main stream's launches keep SMs)
+        static const int fwd_ctas = getenv("SQUINT_ENC_FWD_CTAS") ? atoi(getenv("SQUINT_ENC_FWD_CTAS")) : 74;
+        squint_status r = early_fwd(c, w_in, hp, R, *next, st, par ^ 1, es, fwd_ctas, c.aux->enc, c.aux->chn);
+        if (r != SQUINT_OK) return r;
+      }
     } else {
       BF_CK(launch_adam_shadow(st.critic, gc, st.m_critic, st.v_critic, L.gsize[gC], hp.lr_critic, hp.beta1,
                                hp.beta2, hp.adam_eps, scal + S_C1_CRITIC, scal + S_C2_CRITIC, c.F(w.adam_part), &shC,
@@ -996,7 +1136,8 @@ squint_status update_one(const Ctx& c, const BfLay& w, const squint_hparams& hp,
     BF_CK(launch_metrics(m, ms));
     if (branch) {
       BF_CK(cudaEventRecord(c.aux->join, es));
-      BF_CK(cudaStreamWaitEvent(s, c.aux->join, 0));  // join the branch before the next update
+      // join the branch now, or (pipelined, not the last update) in the next update before its fork
+      if (!pipe || !next) BF_CK(cudaStreamWaitEvent(s, c.aux->join, 0));
     }
   }
   return SQUINT_OK;
@@ -1008,6 +1149,7 @@ bool bf16_prepare() {
   static const bool no_branch = getenv("SQUINT_NO_BRANCH") != nullptr;
   return !no_branch && g_branch_enabled && t_aux.ok();
 }
+int bf16_options() { return g_branch_enabled | (g_pipe_enabled << 1); }
 
 size_t bf16_workspace_bytes(const squint_dims& d) {
   Layout L = make_layout(d);
@@ -1069,9 +1211,18 @@ squint_status bf16_update(const squint_dims& d, const squint_hparams& hp, const 
                               reinterpret_cast<uint8_t*>(c.ws + w.wtiles), s));
   }
   const size_t B = d.batch, A = d.action_dim;
+  static const bool env_pipe = getenv("SQUINT_PIPE") != nullptr;
+  const bool pipe = (env_pipe || g_pipe_enabled) && comm == nullptr && c.aux != nullptr && c.chain;
+  auto in = [&](int j) { return UpdIn{idx + j * B, shifts + j * B * 4, eps + j * 2 * B * A, j}; };
+  if (pipe) {
+    const UpdIn u0 = in(0);
+    squint_status r = early_fwd(c, w, hp, R, u0, st, 0, s, 0, c.aux->enc, c.aux->chn);
+    if (r != SQUINT_OK) return r;
+  }
   for (int j = 0; j < utd; ++j) {
+    const UpdIn nx = in(j + 1);
     squint_status r = update_one(c, w, hp, R, idx + j * B, shifts + j * B * 4, eps + j * 2 * B * A, st, metrics + j * 8,
-                                 comm, inv_btotal, j);
+                                 comm, inv_btotal, j, j & 1, pipe, j + 1 < utd ? &nx : nullptr);
     if (r != SQUINT_OK) return r;
   }
   return SQUINT_OK;
@@ -1214,6 +1365,10 @@ extern "C" SQUINT_API int squint_debug_gemm_times(unsigned long long* host, int 
 extern "C" SQUINT_API squint_status squint_set_option(int key, int value) {
   if (key == 1) {
     sq::g_branch_enabled = value != 0;
+    return SQUINT_OK;
+  }
+  if (key == 2) {
+    sq::g_pipe_enabled = value != 0;
     return SQUINT_OK;
   }
   return sq::set_error(SQUINT_EINVAL, "unknown option");

@@ -262,6 +262,16 @@ def _bf16_case(cfg, seed, utd=1, capacity=None, **over):
     _check_update_bf16(pr, L, met, st_ref, met_ref, trace)
 
 
+def test_update_c2_pipelined_utd3_bf16():
+    # option 2: each update's critic-side forward issued on the previous update's branch
+    # (parity-alternating buffers); same results bar the fixed reduction orders
+    P.squint.LIB.squint_set_option(2, 1)
+    try:
+        _bf16_case("c2", seed=3, utd=3, capacity=4096)
+    finally:
+        P.squint.LIB.squint_set_option(2, 0)
+
+
 def test_update_c2_full_batch_utd2_bf16():
     _bf16_case("c2", seed=3, utd=2, capacity=4096)
 
