@@ -204,7 +204,60 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   // (tensor-map addresses, tile coordinates, byte counts) is hoisted per segment and the stage
   // index advances without divisions: the TMA and MMA instructions take uniform-register operands,
   // and per-iteration operand conversions had made issuing ~3x slower than the TMA unit.
-  if (warp == 0) {
+  const bool wide = EPI == GE_DW && b.wide > 1;
+  if (wide && warp == 0) {
+    // ---------------- wide producer (weight gradients: both operands MN-major) ----------------
+    // one TMA box covers KW = b.wide K blocks (64 MN x 64 KW K rows): 4x fewer, larger boxes;
+    // stage = [A rows 0-63 | A rows 64-127 | B column groups], each KW x 8 KB
+    const int KW = b.wide, sbytes = b.stage_bytes;
+    const GSeg G = P.seg[0];
+    const TileGeo geo = tile_geo(P, nreal, 1);
+    const void* am = &b.maps[G.amap];
+    const void* bm = &b.maps[G.bmap];
+    const int am0 = P.a_m + m0, bn0 = P.b_n + n0, nsb = (G.nkb + KW - 1) / KW;
+    const uint32_t tx = (uint32_t)((2 + geo.nbox_b) * KW * 8192);
+    int st = 0, ph = 0;
+    for (int sb = 0; sb < nsb; ++sb) {
+      if (sb >= S) tc::mbar_wait(&empty_bar[st], ph ^ 1);
+      uint8_t* As = smem + st * sbytes;
+      const int kc = G.a_k + 64 * KW * sb, kcb = G.b_k + 64 * KW * sb;
+      tc::mbar_expect_tx_e(&full_bar[st], tx);
+      tc::tma_load_2d_e(As, am, am0, kc, &full_bar[st]);
+      tc::tma_load_2d_e(As + KW * 8192, am, am0 + 64, kc, &full_bar[st]);
+      for (int i = 0; i < geo.nbox_b; ++i)
+        tc::tma_load_2d_e(As + (2 + i) * KW * 8192, bm, bn0 + 64 * i, kcb, &full_bar[st]);
+      if (++st == S) st = 0, ph ^= 1;
+    }
+    if (lane == 0) stamp_any(11);
+  } else if (wide && warp == 1) {
+    // ---------------- wide MMA issuer ----------------
+    const int KW = b.wide;
+    const GSeg G = P.seg[0];
+    const uint32_t id1 = tc::idesc_bf16_major(128, n1, 1, 1), id_ones = tc::idesc_bf16_major(128, 16, 1, 0);
+    const uint32_t smem0 = tc::smem_u32(smem), sbytes = (uint32_t)b.stage_bytes, lbo = (uint32_t)KW * 8192u;
+    const uint32_t ones0 = tc::smem_u32(ones_tile);
+    const int nsb = (G.nkb + KW - 1) / KW;
+    int st = 0, ph = 0, kb = 0;
+    for (int sb = 0; sb < nsb; ++sb) {
+      tc::mbar_wait(&full_bar[st], ph);
+      if (lane == 0 && sb == 0) stamp_any(8);
+      if (lane == 0) stamp_any(9);
+      tc::fence_after_sync();
+      const uint32_t a0 = smem0 + st * sbytes, b0 = a0 + 2 * lbo;
+      for (int j = 0; j < KW && kb < G.nkb; ++j, ++kb) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t ad = tc::sdesc_sw128(a0 + j * 8192 + 2048 * k, lbo, 1024);
+          const uint32_t acc = (kb | k) != 0;
+          tc::mma_bf16_e(tmem, ad, tc::sdesc_sw128(b0 + j * 8192 + 2048 * k, lbo, 1024), id1, acc);
+          if (ones) tc::mma_bf16_e(tmem + ones_col, ad, tc::sdesc_sw128(ones0 + 32 * k, 16, 1024), id_ones, acc);
+        }
+      }
+      tc::mma_commit_e(&empty_bar[st]);
+      if (++st == S) st = 0, ph ^= 1;
+    }
+    tc::mma_commit_e(&done_bar);
+  } else if (warp == 0) {
     // ---------------- TMA producer (whole warp, one elected lane issues) ----------------
     const int sbytes = b.stage_bytes, rank = b.mcast ? (int)(blockIdx.x % b.cs) : 0, cs = b.cs;
     const uint16_t mask = (uint16_t)((1u << cs) - 1u);
@@ -1187,6 +1240,28 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   }
   b.ntiles = t;
   b.stage_bytes = kABytes + bmax;
+  // weight gradients (one segment, both operands MN-major): wide TMA boxes of KW K blocks
+  b.wide = 1;
+  if (epi0 == GE_DW) {
+    static const bool no_wide = getenv("SQUINT_NO_WIDE") != nullptr;
+    bool ok = !no_wide;
+    int nbb = 0, maxk = 0;
+    for (int i = 0; i < b.nprob && ok; ++i) {
+      const GProb& p = b.p[i];
+      ok = p.nseg == 1 && p.seg[0].a_mn && p.seg[0].b_mn;
+      nbb = host_bbytes(p, 1) / 8192 > nbb ? host_bbytes(p, 1) / 8192 : nbb;
+      maxk = p.seg[0].nkb > maxk ? p.seg[0].nkb : maxk;
+    }
+    for (int kw = 4; ok && kw >= 2; kw >>= 1) {
+      const int sbytes = (2 + nbb) * kw * 8192;
+      if (maxk >= kw && 2 * sbytes + 2048 <= 200 * 1024) {
+        b.wide = kw;
+        b.stage_bytes = sbytes;
+        b.prefetch_b = 0;  // the pre-wait B prefetch assumes the one-K-block stage layout
+        break;
+      }
+    }
+  }
   int S = (200 * 1024) / b.stage_bytes;
   S = S > kMaxStages ? kMaxStages : S;
   int maxkb = 0;  // no more stages than K blocks
@@ -1196,6 +1271,7 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     maxkb = k > maxkb ? k : maxkb;
   }
   if (b.ks > 1) maxkb = (maxkb + b.ks - 1) / b.ks;  // K blocks per cluster CTA
+  if (b.wide > 1) maxkb = (maxkb + b.wide - 1) / b.wide;  // stages hold b.wide K blocks
   S = S > maxkb ? maxkb : S;
   S = S < 2 ? 2 : S;
   if ((size_t)S * b.stage_bytes > 200 * 1024) return -1;
@@ -1214,9 +1290,9 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     for (int k = 0; k < p.nseg; ++k) {
       GSeg& g = p.seg[k];
       if (b.nmaps + 2 > kGemmMaxMaps) return -1;
-      if (tmap_get(gb.segA[i][k], g.a_mn ? 64 : 128, &b.maps[b.nmaps])) return -1;
+      if (tmap_get(gb.segA[i][k], g.a_mn ? 64 * b.wide : 128, &b.maps[b.nmaps])) return -1;
       g.amap = b.nmaps++;
-      if (tmap_get(gb.segB[i][k], g.b_mn ? 64 : (bn16 > 256 ? 256 : bn16), &b.maps[b.nmaps])) return -1;
+      if (tmap_get(gb.segB[i][k], g.b_mn ? 64 * b.wide : (bn16 > 256 ? 256 : bn16), &b.maps[b.nmaps])) return -1;
       g.bmap = b.nmaps++;
     }
   }

@@ -98,6 +98,7 @@ struct GBatch {
   int ks;  // split-K cluster size (k_gemm_sk; set by gemm_launch): bwd-LN column partials are
            // then written per 128 / ks rows, [mtiles * ks][3][N]
   int mcast;       // cluster CTAs share the A tile: each K block is loaded once and multicast
+  int wide;        // GE_DW: K blocks per TMA box / stage (1: one box per 64-row K block)
   int xpre_off;    // LayerNorm backward: smem offset of the prefetched x_hat boxes (0: loaded after the main loop)
   int prefetch_b;  // 1: B operands may be loaded before griddepcontrol.wait (not written by the
                    // immediately preceding kernel); set through GemmBuilder::prefetch_b
@@ -117,6 +118,7 @@ struct GemmBuilder {
     b.prefetch_b = prefetch_b;
     b.ks = 1;
     b.cs = 1;
+    b.wide = 1;
   }
   GProb& add(int M, int N, int epi);
   // K segment: A(m, k) from `A` (K-major if !a_mn) and B(n, k) from `Bm`.
