@@ -1,13 +1,15 @@
 """bench.py -- Squint hot path on B200: SAC gradient updates/s (BASELINE.json metric).
 
 One step = one Algorithm-1 iteration at BASELINE configs[2]:
-  squint_act   on N_env = 1024 rendered 3x128x128 frames (squint + encoder + actor + sample,
-               with the squinted obs written into the 1M replay ring: a16 + a1),
-  squint_insert of the 1024 next frames into the ring's next_obs (a1),
+  squint_insert2 of the N_env = 1024 new rendered 3x128x128 frames o_{t+1}: squinted once into
+               the ring's next_obs rows and into the 16x16 rows the next act encodes (a1, f2),
+  squint_act   on the 1024 squinted o_t (encoder + actor + sample, o_t written into the 1M
+               replay ring's obs rows: a16 + a1),
   squint_update with UTD 4 at batch 512 (a2-a15), 101 atoms on [-20, 20].
+(--act-full: the act squints a second 128x128 batch itself, the insert writes next_obs only.)
 value = updates/s summed over ranks (weak scaling: every rank owns a 512-sample shard of
 the 512*N global batch; gradients are NCCL all-reduced).  Inputs live in HBM before the
-timed region; the replay ring (1.66 GB per rank) and three rotating 100 MB frame pools
+timed region; the replay ring (1.66 GB per rank) and four rotating 50 MB frame pools
 exceed the 126 MB L2.  Launch: python bench.py [--gpus N --steps K --warmup W]
 (torchrun for N > 1).  --impl reference times the CPU oracle instead (rank 0 only).
 """
@@ -144,37 +146,6 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------
-# algorithmic work per phase (per update unless noted) for the roofline line
-# ---------------------------------------------------------------------------------------
-def phase_work(d, n_env):
-    B, C, L, P, A = d["batch"], d["conv_ch"], d["latent"], d["proprio_dim"], d["action_dim"]
-    Hc, Ha, N = d["critic_hidden"], d["actor_hidden"], d["n_atoms"]
-    P1, P2 = 49, 25
-    F = C * P2
-    nq, npi = L + P + A, L + P
-    conv = P1 * C * 27 + P2 * C * 9 * C                      # MACs per image
-    mlp_q = nq * Hc + Hc * Hc + Hc * N
-    mlp_a = npi * Ha + Ha * Ha + Ha * 2 * A
-    fl = {
-        "enc_fwd": 2 * 2 * B * conv,
-        "proj_fwd": 2 * 4 * B * L * F,
-        "actor_fwd": 2 * 2 * B * mlp_a,
-        "heads_fwd": 2 * 4 * B * mlp_q,
-        "critic_bwd": 2 * (2 * B * (N * Hc + Hc * Hc) + B * 2 * Hc * L + B * L * F),
-        "critic_dw": 2 * (2 * B * mlp_q + B * L * F),
-        "enc_bwd": 2 * B * (P2 * C * 9 * C * 2 + P1 * C * 27),
-        "actor_loss": 2 * (B * L * F + 2 * B * mlp_q),
-        "actor_bwd": 2 * (2 * B * (N * Hc + Hc * Hc + Hc * A) + B * (2 * A * Ha + Ha * Ha + Ha * L)),
-        "actor_dw": 2 * (B * mlp_a + B * L * F),
-        "act_encode": 2 * n_env * conv,
-        "act_mlp": 2 * n_env * (L * F + mlp_a),
-    }
-    by = {"insert": n_env * 3 * 128 * 128 + n_env * 768,
-          "act_encode": n_env * 3 * 128 * 128 + n_env * 768 + n_env * F * 4}
-    return fl, by
-
-
-# ---------------------------------------------------------------------------------------
 # the GPU arm
 # ---------------------------------------------------------------------------------------
 def run_gpu(args):
@@ -230,13 +201,18 @@ def run_gpu(args):
     aeps_all = torch.randn((T, N_ENV, A), generator=gi, device=dev)
     prop_all = torch.randn((T, N_ENV, d["proprio_dim"]), generator=gi, device=dev)
     slots_all = torch.stack([(torch.arange(N_ENV, device=dev) + k * N_ENV) % cap for k in range(T)])
-    # three rotating frame pools (act frames + next frames), 3 x 100 MB > L2
-    NPOOL = 3
-    pools = []
-    for p in range(NPOOL):
-        fr = torch.as_tensor(SI.make_frames(N_ENV, 128, seed=10 + p)).to(dev)
-        nx = torch.as_tensor(SI.make_frames(N_ENV, 128, seed=20 + p)).to(dev)
-        pools.append((fr, nx))
+    # rotating pools of rendered frames o_{t+1} (4 x 50 MB > L2).  Algorithm 1 reads each new
+    # observation once: squint_insert2 squints o_{t+1} into the finished transition's
+    # next_obs row and into a 16x16 staging buffer that the next step's act encodes (factor 1),
+    # writing it on into that transition's obs row.  --act-full: the round-1 step instead (act
+    # squints a second frame batch itself; the insert writes next_obs only).
+    NPOOL = 4
+    pools = [torch.as_tensor(SI.make_frames(N_ENV, 128, seed=20 + p)).to(dev) for p in range(NPOOL)]
+    act_pool = [torch.as_tensor(SI.make_frames(N_ENV, 128, seed=10 + p)).to(dev) for p in range(NPOOL)] \
+        if args.act_full else None
+    stage = [torch.empty((N_ENV, 3, 16, 16), dtype=torch.uint8, device=dev) for _ in range(2)]
+    stage_slots = torch.arange(N_ENV, device=dev, dtype=torch.int64)
+    NG = NPOOL  # graphs: pool j % NPOOL, staging parity j % 2 (NPOOL even)
     # static per-step buffers that the graphs read
     idx_s, sh_s, eps_s = idx_all[0].clone(), sh_all[0].clone(), eps_all[0].clone()
     aeps_s, prop_s, slots_s = aeps_all[0].clone(), prop_all[0].clone(), slots_all[0].clone()
@@ -246,20 +222,26 @@ def run_gpu(args):
     act_ws = torch.zeros(P.act_workspace_bytes(L.dims, N_ENV), dtype=torch.uint8, device=dev)
     obs_ring = R["obs"]
     next_ring = R["next_obs"]
+    # o_0, squinted
+    P.squint_insert(pools[NPOOL - 1], 8, stage_slots, stage[0])
 
     side = torch.cuda.Stream(device=dev)
     ins_fork, ins_done = torch.cuda.Event(), torch.cuda.Event()
 
-    def step(pool, stream=None):
+    def step(j, stream=None):
         # act (o_t) and the insert of o_{t+1} are independent: the insert (HBM-bound) runs on a
         # side stream beside the act's MLP; the updates wait for both (they may sample the new rows)
-        fr, nx = pools[pool]
+        nx, par = pools[j % NPOOL], j % 2
         cur = stream if stream is not None else torch.cuda.current_stream()
         ins_fork.record(cur)
         side.wait_event(ins_fork)
         with torch.cuda.stream(side):
-            P.squint_insert(nx, 8, slots_s, next_ring, stream=side)
+            if args.act_full:
+                P.squint_insert(nx, 8, slots_s, next_ring, stream=side)
+            else:
+                P.squint_insert2(nx, 8, slots_s, next_ring, stage_slots, stage[1 - par], stream=side)
             ins_done.record(side)
+        fr = act_pool[j % NPOOL] if args.act_full else stage[par]
         P.squint_act(L.dims, L.hp, L.actor, L.critic, fr, prop_s, aeps_s, act_out, logp_out, act_ws,
                      ring=obs_ring, slots=slots_s, stream=stream)
         cur.wait_event(ins_done)
@@ -289,19 +271,19 @@ def run_gpu(args):
             step(0)  # warm on the capture stream
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
-        for p in range(NPOOL):
+        for j in range(NG):
             gph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gph):
-                step(p)
+                step(j)
             graphs.append(gph)
         torch.cuda.synchronize()
 
     def run_one(k):
         load_inputs(k)
         if use_graph:
-            graphs[k % NPOOL].replay()
+            graphs[k % NG].replay()
         else:
-            step(k % NPOOL)
+            step(k % NG)
 
     for w in range(W):
         run_one(w)
@@ -363,57 +345,71 @@ def run_gpu(args):
                 e["bytes"] += by / R
 
     # e2e: the environment loop through the public API from pinned host buffers.  Step t acts on
-    # o_t (uploaded by step t-1), reads the actions back, uploads the new observation o_{t+1}
-    # (the env's output: stored as next_obs now and acted on at step t+1, so each frame batch
-    # crosses PCIe once) and the step's small inputs, inserts o_{t+1} and runs the UTD updates.
-    # The frame upload runs on a copy stream beside the updates (which sample the ring as it was
-    # before o_{t+1} is inserted); the insert waits for it.  Results (actions, log pi, metrics) go
-    # back to pinned host memory every step.
+    # o_t (squinted by step t-1's insert2), reads the actions back, uploads the new observation
+    # o_{t+1} (the env's output; each frame batch crosses PCIe once) and the step's small inputs,
+    # runs the UTD updates and inserts o_{t+1} once: next_obs of transition t and the staging rows
+    # the next act encodes.  The frame upload runs on copy streams beside the act and the updates
+    # (which sample the ring as it was before o_{t+1} is inserted); the insert waits for it.
+    # Results (actions, log pi, metrics) go back to pinned host memory every step.
     e2e = None
     if not args.no_e2e:
-        h_fr = [pools[p][1].cpu().pin_memory() for p in range(NPOOL)]
+        h_fr = [pools[p].cpu().pin_memory() for p in range(NPOOL)]
         h_in = [t.cpu().pin_memory() for t in (idx_all, sh_all, eps_all, aeps_all, prop_all, slots_all)]
         h_out = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (act_out, logp_out, metrics)]
-        dbuf = [pools[0][0].clone(), pools[0][1].clone()]
-        stage = [idx_s, sh_s, eps_s, aeps_s, prop_s, slots_s]
+        dbuf = [pools[0].clone(), pools[1].clone()]
+        # the step's small inputs (one buffer set: double-buffering them lets the next upload start
+        # early and share the link with this one, which delays this step's insert -- measured slower)
+        stage_in = [idx_s, sh_s, eps_s, aeps_s, prop_s, slots_s]
         main = torch.cuda.current_stream()
         # the frame upload in two halves on two copy streams (one DMA stream does not saturate
         # the link: 47 vs 54 GB/s measured), the small per-step inputs on a stream of their own
         cps = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
         ins = torch.cuda.Stream(device=dev)
-        acted = [torch.cuda.Event(), torch.cuda.Event()]
+        freed = [torch.cuda.Event(), torch.cuda.Event()]  # dbuf[i] read by its last consumer
         copied = [torch.cuda.Event(), torch.cuda.Event()]
         inputs_in = torch.cuda.Event()
         half = h_fr[0].shape[0] // 2
 
         def e2e_step(k):
-            cur, nxt = dbuf[k % 2], dbuf[(k + 1) % 2]
+            nxt = dbuf[k % 2]
+            idx, sh, eps, aeps, prop, slots = stage_in
             with torch.cuda.stream(ins):
-                for dst, src in zip(stage, h_in):
+                for dst, src in zip(stage_in, h_in):
                     dst.copy_(src[k], non_blocking=True)
                 inputs_in.record(ins)
-            main.wait_event(inputs_in)
-            P.squint_act(L.dims, L.hp, L.actor, L.critic, cur, prop_s, aeps_s, act_out, logp_out, act_ws,
-                         ring=obs_ring, slots=slots_s)
-            acted[k % 2].record(main)
-            for dst, src in zip(h_out[:2], (act_out, logp_out)):
-                dst.copy_(src, non_blocking=True)
-            # o_{t+1} -> the buffer step t-1 acted on (that act has been issued and is waited for)
+            # o_{t+1} -> dbuf[k % 2] once step k-2's insert (or, --act-full, step k-1's act) read it,
+            # queued behind the small inputs (the copy engine serves them in order: a 50 MB upload
+            # issued first would hold the act's inputs back by a millisecond)
             for c, sl in enumerate((slice(0, half), slice(half, None))):
-                cps[c].wait_event(acted[(k + 1) % 2])
+                cps[c].wait_event(freed[k % 2])
+                cps[c].wait_event(inputs_in)
                 with torch.cuda.stream(cps[c]):
                     nxt[sl].copy_(h_fr[k % NPOOL][sl], non_blocking=True)
                     copied[c].record(cps[c])
-            L.update(replay, idx_s, sh_s, eps_s, metrics)
+            main.wait_event(inputs_in)
+            fr = dbuf[(k + 1) % 2] if args.act_full else stage[k % 2]
+            P.squint_act(L.dims, L.hp, L.actor, L.critic, fr, prop, aeps, act_out, logp_out, act_ws,
+                         ring=obs_ring, slots=slots)
+            if args.act_full:
+                freed[(k + 1) % 2].record(main)
+            for dst, src in zip(h_out[:2], (act_out, logp_out)):
+                dst.copy_(src, non_blocking=True)
+            L.update(replay, idx, sh, eps, metrics)
             main.wait_event(copied[0])
             main.wait_event(copied[1])
-            P.squint_insert(nxt, 8, slots_s, next_ring)
+            if args.act_full:
+                P.squint_insert(nxt, 8, slots, next_ring)
+            else:
+                P.squint_insert2(nxt, 8, slots, next_ring, stage_slots, stage[(k + 1) % 2])
+                freed[k % 2].record(main)
             h_out[2].copy_(metrics, non_blocking=True)
             # the next step's small inputs overwrite the staging buffers once this step used them
             ins.wait_stream(main)
 
-        dbuf[0].copy_(h_fr[NPOOL - 1], non_blocking=True)  # o_0
-        acted[1].record(main)
+        dbuf[1].copy_(h_fr[NPOOL - 1], non_blocking=True)  # o_0 (--act-full acts on it)
+        P.squint_insert(dbuf[1], 8, stage_slots, stage[0])  # o_0, squinted
+        for e in freed:
+            e.record(main)
         for w in range(W):
             e2e_step(w)
         torch.cuda.synchronize()
@@ -436,8 +432,9 @@ def run_gpu(args):
         d2h = sum(x.numel() * x.element_size() for x in h_out)
         e2e = {"value": world * UTD * K / (ems / 1e3), "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / K, "host_enqueue_ms_per_step": host_ms,
-               "loop": "act(o_t) -> D2H actions -> H2D o_{t+1} (copy stream, beside the updates) -> "
-                       "insert(o_{t+1}) after the updates"}
+               "loop": ("act(o_t) -> D2H actions -> H2D o_{t+1} (copy streams, beside the act and the updates) -> "
+                        + ("insert(o_{t+1}) after the updates" if args.act_full else
+                           "insert2(o_{t+1}: next_obs + the next act's squinted rows) after the updates"))}
 
     if rank != 0:
         if world > 1:
@@ -481,9 +478,10 @@ def run_gpu(args):
     line = {"metric": METRIC, "value": world * UTD * K / (ms / 1e3), "unit": "updates/s", "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": {P.FP32: "f32", P.BF16: "bf16"}[precision], "data": "synthetic",
-            "config": {"workload": "c2: Algorithm-1 step = act(1024 envs, 128x128) + insert(1024) + 4 updates at "
-                                   "B=512 per rank, 101 atoms, 1M ring", "global_batch": B * world, "utd": UTD,
-                       "n_env": N_ENV, "parallelism": f"dp{world}", "l2": "ring 1.66 GB + 3 rotating 100 MB frame pools > L2",
+            "config": {"workload": "c2: Algorithm-1 step = insert2(1024 new 128x128 frames) + act(1024 envs) + "
+                                   "4 updates at B=512 per rank, 101 atoms, 1M ring"
+                                   + (" (act squints its own frames)" if args.act_full else ""), "global_batch": B * world, "utd": UTD,
+                       "n_env": N_ENV, "parallelism": f"dp{world}", "l2": "ring 1.66 GB + rotating frame pools (4 x 50 MB) > L2",
                        "graph": use_graph},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": int(launches_per_step * K), "kernels_us_per_step": kernels_us}
@@ -504,6 +502,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=3)
     ap.add_argument("--no-timeline", action="store_true")
+    ap.add_argument("--act-full", action="store_true")  # round-1 step: act squints its own frame batch
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps

@@ -155,6 +155,18 @@ SQUINT_API squint_status squint_insert(const uint8_t* frames, int64_t n, int c, 
                             const int64_t* slots, uint8_t* ring, int64_t capacity,
                             squint_stream_t stream);
 
+/* a1 twice from one read of the frames: the squinted frames go to
+ * ring[slots[f]] and to ring2[slots2[f]] (both [capacity, c, h/factor, w/factor]).  In the
+ * Algorithm-1 loop the new observation o_{t+1} is the finished transition's next_obs (ring =
+ * next_obs, slots = this step's slots) and the next transition's obs (ring2 = obs, slots2 = the
+ * next step's slots); squint_act at the next step can then read the squinted rows (factor 1)
+ * instead of squinting the full frames again.  Same preconditions and errors as squint_insert;
+ * ring2 and slots2 are both NULL (then exactly squint_insert) or both non-NULL (EINVAL
+ * otherwise); capacity bounds both slot arrays (the smaller ring's row count). */
+SQUINT_API squint_status squint_insert2(const uint8_t* frames, int64_t n, int c, int h, int w, int factor,
+                                        const int64_t* slots, uint8_t* ring, const int64_t* slots2, uint8_t* ring2,
+                                        int64_t capacity, squint_stream_t stream);
+
 /* ---- a16: batched rollout inference (Algorithm 1 L4-5) -------------------
  * frames u8 [n, img_c, frame_h, frame_w] with frame_h = img_h * f, frame_w = img_w * f
  * (f >= 1; f = 1 means already squinted); proprio [n, P]; eps [n, A] N(0,1) noise or

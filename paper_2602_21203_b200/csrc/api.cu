@@ -741,8 +741,10 @@ squint_status squint_act_workspace_bytes(const squint_dims* dims, int64_t n, siz
   return SQUINT_OK;
 }
 
-squint_status squint_insert(const uint8_t* frames, int64_t n, int c, int h, int w, int factor, const int64_t* slots,
-                            uint8_t* ring, int64_t capacity, squint_stream_t stream) {
+squint_status squint_insert2(const uint8_t* frames, int64_t n, int c, int h, int w, int factor, const int64_t* slots,
+                             uint8_t* ring, const int64_t* slots2, uint8_t* ring2, int64_t capacity,
+                             squint_stream_t stream) {
+  if (!ring2 != !slots2) return fail(SQUINT_EINVAL, "ring2 and slots2 must both be given or both be NULL");
   if (n < 0) return fail(SQUINT_EINVAL, "n must be >= 0");
   if (factor < 1) return fail(SQUINT_EINVAL, "factor must be >= 1");
   if (capacity < 1) return fail(SQUINT_EINVAL, "capacity must be >= 1");
@@ -755,8 +757,13 @@ squint_status squint_insert(const uint8_t* frames, int64_t n, int c, int h, int 
   if (factor == 8 && (w % 16) == 0 && ((h / 8) * (w / 8) % 2))
     return fail(SQUINT_EINVAL, "odd output row length not supported by the vector path");
   PhaseScope ps(0, 0, (cudaStream_t)stream);
-  SQ_CK(launch_insert(frames, n, c, h, w, factor, slots, ring, (cudaStream_t)stream));
+  SQ_CK(launch_insert(frames, n, c, h, w, factor, slots, ring, (cudaStream_t)stream, slots2, ring2));
   return SQUINT_OK;
+}
+
+squint_status squint_insert(const uint8_t* frames, int64_t n, int c, int h, int w, int factor, const int64_t* slots,
+                            uint8_t* ring, int64_t capacity, squint_stream_t stream) {
+  return squint_insert2(frames, n, c, h, w, factor, slots, ring, nullptr, nullptr, capacity, stream);
 }
 
 squint_status squint_soft_update(float* target, const float* online, int64_t n, float tau, squint_stream_t stream) {

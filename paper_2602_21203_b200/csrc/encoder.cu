@@ -32,7 +32,8 @@ SQ_DEV void sum16(const uint4 v, uint32_t& lo, uint32_t& hi) {
 // column chunk over 8 rows).
 __global__ void __launch_bounds__(256) k_insert_f8(const uint8_t* __restrict__ frames, int64_t n, int c, int h,
                                                    int w, const int64_t* __restrict__ slots,
-                                                   uint8_t* __restrict__ ring) {
+                                                   uint8_t* __restrict__ ring, const int64_t* __restrict__ slots2,
+                                                   uint8_t* __restrict__ ring2) {
   grid_wait();
   grid_trigger();
   const int ho = h / 8, wo = w / 8, chunks = w / 16;
@@ -54,14 +55,17 @@ __global__ void __launch_bounds__(256) k_insert_f8(const uint8_t* __restrict__ f
     for (int r = 0; r < 8; ++r) sum16(v[r], lo, hi);
     const uint32_t q0 = (lo + 31u + ((lo >> 6) & 1u)) >> 6;  // RHE(lo / 64)
     const uint32_t q1 = (hi + 31u + ((hi >> 6) & 1u)) >> 6;
-    uint8_t* dst = ring + (slots[f] * c + cc) * (int64_t)(ho * wo) + oy * wo + ch * 2;
-    *reinterpret_cast<uint16_t*>(dst) = (uint16_t)(q0 | (q1 << 8));
+    const uint16_t q = (uint16_t)(q0 | (q1 << 8));
+    const int64_t off = (int64_t)cc * (ho * wo) + oy * wo + ch * 2;
+    *reinterpret_cast<uint16_t*>(ring + slots[f] * c * (int64_t)(ho * wo) + off) = q;
+    if (ring2) *reinterpret_cast<uint16_t*>(ring2 + slots2[f] * c * (int64_t)(ho * wo) + off) = q;
   }
 }
 
 // generic factor: one thread per output pixel
 __global__ void k_insert_generic(const uint8_t* __restrict__ frames, int64_t n, int c, int h, int w, int f,
-                                 const int64_t* __restrict__ slots, uint8_t* __restrict__ ring) {
+                                 const int64_t* __restrict__ slots, uint8_t* __restrict__ ring,
+                                 const int64_t* __restrict__ slots2, uint8_t* __restrict__ ring2) {
   const int ho = h / f, wo = w / f;
   const int64_t items = n * c * ho * wo;
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
@@ -76,7 +80,9 @@ __global__ void k_insert_generic(const uint8_t* __restrict__ frames, int64_t n, 
     uint32_t s = 0;
     for (int a = 0; a < f; ++a)
       for (int b = 0; b < f; ++b) s += src[(int64_t)a * w + b];
-    ring[(slots[fr] * c + cc) * (int64_t)(ho * wo) + oy * wo + ox] = (uint8_t)rhe_div(s, (uint32_t)(f * f));
+    const uint8_t q = (uint8_t)rhe_div(s, (uint32_t)(f * f));
+    ring[(slots[fr] * c + cc) * (int64_t)(ho * wo) + oy * wo + ox] = q;
+    if (ring2) ring2[(slots2[fr] * c + cc) * (int64_t)(ho * wo) + oy * wo + ox] = q;
   }
 }
 
@@ -407,18 +413,18 @@ int launch_enc_bwd(const EncBwdArgs& a, cudaStream_t s) {
 }
 
 int launch_insert(const uint8_t* frames, int64_t n, int c, int h, int w, int factor, const int64_t* slots,
-                  uint8_t* ring, cudaStream_t s) {
+                  uint8_t* ring, cudaStream_t s, const int64_t* slots2, uint8_t* ring2) {
   if (n == 0) return 0;
   if (factor == 8 && (w % 16) == 0) {
     const int64_t items = n * c * (h / 8) * (w / 16);
     int64_t blocks = (items + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    note_launch(s, "k_insert_f8", 0, (double)n * c * h * w + (double)n * c * (h / 8) * (w / 8)); launch_pdl(k_insert_f8, dim3((unsigned)blocks), dim3(256), 0, s, frames, n, c, h, w, slots, ring);
+    note_launch(s, "k_insert_f8", 0, (double)n * c * h * w + (ring2 ? 2.0 : 1.0) * n * c * (h / 8) * (w / 8)); launch_pdl(k_insert_f8, dim3((unsigned)blocks), dim3(256), 0, s, frames, n, c, h, w, slots, ring, slots2, ring2);
   } else {
     const int64_t items = n * c * (h / factor) * (w / factor);
     int64_t blocks = (items + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    note_launch(s, "k_insert_generic", 0, (double)n * c * h * w + (double)n * c * (h / factor) * (w / factor)); k_insert_generic<<<(unsigned)blocks, 256, 0, s>>>(frames, n, c, h, w, factor, slots, ring);
+    note_launch(s, "k_insert_generic", 0, (double)n * c * h * w + (ring2 ? 2.0 : 1.0) * n * c * (h / factor) * (w / factor)); k_insert_generic<<<(unsigned)blocks, 256, 0, s>>>(frames, n, c, h, w, factor, slots, ring, slots2, ring2);
   }
   return (int)cudaGetLastError();
 }

@@ -82,7 +82,8 @@ int launch_conv_tiles(const float* w1, const float* w2, int C, uint8_t* tiles, c
 size_t enc_bwd_partial_floats(int C, int c_in, int nchunk);
 int enc_bwd_nchunk(int B);
 
+// ring2 / slots2 (optional): a second destination written with the same squinted frames
 int launch_insert(const uint8_t* frames, int64_t n, int c, int h, int w, int factor, const int64_t* slots,
-                  uint8_t* ring, cudaStream_t s);
+                  uint8_t* ring, cudaStream_t s, const int64_t* slots2 = nullptr, uint8_t* ring2 = nullptr);
 
 }  // namespace sq

@@ -211,6 +211,18 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ 
         }
         *reinterpret_cast<uint4*>(xs + i * 768 + cc * 256 + y * 16) = o;
       }
+    } else if (a.factor == 1) {
+      // frames already at the stored resolution (squinted by squint_insert2): 768-byte copies
+      const uint8_t* Fr = a.src[0];
+      for (int e = tid; e < kGF * 48; e += kThr) {
+        const int i = e / 48, rem = e - i * 48, b = b0 + i;
+        uint4 o = make_uint4(0, 0, 0, 0);
+        if (b < a.B) {
+          o = __ldcs(reinterpret_cast<const uint4*>(Fr + (int64_t)b * 768) + rem);
+          if (a.ring) reinterpret_cast<uint4*>(a.ring + a.slots[b] * 768)[rem] = o;
+        }
+        reinterpret_cast<uint4*>(xs + i * 768)[rem] = o;
+      }
     } else {
       // squint: 8x8 block sums of 128x128 frames, round half to even (Q1), optional ring write
       // (img, ch, oy, 16-byte column chunk) items; a thread keeps the loads of kU items (kU x 8 x
@@ -719,11 +731,11 @@ int launch_conv_tiles(const float* w1, const float* w2, int C, uint8_t* tiles, c
 int launch_enc_fwd_tc(const EncFwdArgs& a, cudaStream_t s) {
   if (a.B == 0) return 0;
   if ((a.C != 32 && a.C != 64) || a.H != 16 || a.c_in != 3 || !a.wtiles) return (int)cudaErrorInvalidValue;
-  if (a.mode == 1 && a.factor != 8) return (int)cudaErrorInvalidValue;
+  if (a.mode == 1 && a.factor != 8 && a.factor != 1) return (int)cudaErrorInvalidValue;
   {
     const double img = (double)a.B * a.nsrc, C = a.C;
     const double flops = 2.0 * img * (49.0 * C * 27.0 + 25.0 * 9.0 * C * C);
-    const double bytes = a.mode == 1 ? img * (3.0 * 128 * 128 + 2.0 * 25 * C) : img * (768.0 + 2.0 * 25 * C);
+    const double bytes = (a.mode == 1 && a.factor == 8) ? img * (3.0 * 128 * 128 + 2.0 * 25 * C) : img * (768.0 + 2.0 * 25 * C);
     note_launch(s, "k_enc_fwd_tc", flops, bytes);
   }
   static const bool dbg = getenv("SQUINT_ENC_DBG") != nullptr;

@@ -94,6 +94,15 @@ def test_insert_shape_errors_before_launch():
     assert b"divisible" in S.LIB.squint_last_error() or True
 
 
+def test_insert2_arg_errors():
+    null, one = C.c_void_p(0), C.c_void_p(16)
+    # ring2 without slots2 (and the reverse) is rejected even for n == 0
+    assert S.LIB.squint_insert2(null, 0, 3, 128, 128, 8, null, null, null, one, 10, null) == 1
+    assert S.LIB.squint_insert2(null, 0, 3, 128, 128, 8, null, null, one, null, 10, null) == 1
+    assert S.LIB.squint_insert2(null, 4, 3, 130, 128, 8, null, null, null, null, 10, null) == 2
+    assert S.LIB.squint_insert2(null, 0, 3, 128, 128, 8, null, null, null, null, 10, null) == 0
+
+
 def test_soft_update_arg_errors():
     null = C.c_void_p(0)
     assert S.LIB.squint_soft_update(null, null, 10, 1.5, null) == 1

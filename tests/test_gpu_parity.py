@@ -60,6 +60,25 @@ def test_insert_tie_and_constant():
     assert (r[2] == 77).all() and r[0, 0, 0, 0] == 2 and r[0, 1, 0, 0] == 0
 
 
+@pytest.mark.parametrize("n,hw,factor", [(37, 128, 8), (5, 48, 3), (1024, 128, 8)])
+def test_insert2_both_rings_bit_exact(n, hw, factor):
+    """f2: one squint, two destinations (next_obs[slots], obs[slots2]) -- each ring equals
+    the oracle's insert into it, untouched rows keep their fill."""
+    frames = SI.make_frames(n, hw, seed=n + 3)
+    cap = 2 * n + 5
+    slots = SI.make_slots(n, cap, seed=n + 1)
+    slots2 = (slots + 1) % cap
+    r1 = np.full((cap, 3, hw // factor, hw // factor), 9, np.uint8)
+    r2 = np.full_like(r1, 11)
+    e1, e2 = O.insert(frames, factor, slots, r1), O.insert(frames, factor, slots2, r2)
+    g1, g2 = torch.as_tensor(r1).to(DEV), torch.as_tensor(r2).to(DEV)
+    P.squint_insert2(torch.as_tensor(frames).to(DEV), factor, torch.as_tensor(slots).to(DEV), g1,
+                     torch.as_tensor(slots2).to(DEV), g2)
+    torch.cuda.synchronize()
+    assert np.array_equal(g1.cpu().numpy(), e1)
+    assert np.array_equal(g2.cpu().numpy(), e2)
+
+
 # ---- a14 soft update ------------------------------------------------------------------
 @pytest.mark.parametrize("n,tau", [(1, 0.005), (1000, 0.005), (4097, 0.5), (33, 0.0), (33, 1.0)])
 def test_soft_update(n, tau):
@@ -200,6 +219,39 @@ def test_act_bf16(n):
     torch.cuda.synchronize()
     compare("action bf16", act.cpu().numpy(), a_ref, 2e-2)
     compare("logp bf16", lp.cpu().numpy(), lp_ref, 2e-2)
+
+
+@pytest.mark.parametrize("n", [37, 1024])
+def test_act_bf16_presquinted_factor1(n):
+    """f2: act on frames already squinted into a ring row (factor 1) -- parity with the oracle's
+    act on the same 16x16 frames, bitwise identical to act on the 128x128 originals (the squint
+    is the only step that differs), and the factor-1 ring write copies the rows unchanged."""
+    pr = Problem("c0", seed=5)
+    L = pr.gpu_setup(precision=P.BF16)
+    big = SI.make_frames(n, 128, seed=n + 11)
+    small = O.area_downsample(big, 8)
+    prop = SI.make_proprio(n, 12, seed=n)
+    eps = np.random.default_rng(n).standard_normal((n, 6)).astype(np.float32)
+    st = O.init_state(pr.specs, pr.vals)
+    a_ref, lp_ref, s_ref = O.act(pr.d, pr.h, st["critic"], st["actor"], small, prop, eps)
+    assert np.array_equal(s_ref, small)
+    dims = P.make_dims(pr.dims, P.BF16)
+    hp = P.make_hparams(pr.hp)
+    ws = torch.zeros(P.act_workspace_bytes(dims, n), dtype=torch.uint8, device=DEV)
+    out = []
+    ring = torch.zeros((n + 3, 3, 16, 16), dtype=torch.uint8, device=DEV)
+    slots = torch.arange(n, device=DEV, dtype=torch.int64).flip(0) + 2
+    for fr, rg in ((small, ring), (big, None)):
+        act = torch.zeros((n, 6), device=DEV)
+        lp = torch.zeros(n, device=DEV)
+        P.squint_act(dims, hp, L.actor, L.critic, torch.as_tensor(fr).to(DEV), torch.as_tensor(prop).to(DEV),
+                     torch.as_tensor(eps).to(DEV), act, lp, ws, ring=rg, slots=None if rg is None else slots)
+        torch.cuda.synchronize()
+        out.append((act.cpu().numpy(), lp.cpu().numpy()))
+    compare("action bf16 f1", out[0][0], a_ref, 2e-2)
+    compare("logp bf16 f1", out[0][1], lp_ref, 2e-2)
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert np.array_equal(ring[slots].cpu().numpy(), small)
 
 
 def _rel_l2(got, ref):
