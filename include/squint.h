@@ -167,6 +167,30 @@ SQUINT_API squint_status squint_insert2(const uint8_t* frames, int64_t n, int c,
                                         const int64_t* slots, uint8_t* ring, const int64_t* slots2, uint8_t* ring2,
                                         int64_t capacity, squint_stream_t stream);
 
+/* a1 with the renderer-side variants of SURVEY §8(f) f4, fused before the squint.
+ *   layout  SQUINT_LAYOUT_CHW: frames u8 [n, c, h, w] (as squint_insert);
+ *           SQUINT_LAYOUT_HWC: frames u8 [n, h, w, c] (what renderers emit); the ring
+ *           rows are CHW [c, h/factor, w/factor] either way.
+ *   jitter  NULL, or f32 [n, 3] = (brightness, contrast, saturation) factors per frame, > 0,
+ *           drawn by the caller (per episode or per step); needs c == 3.  Applied to
+ *           the full-resolution frame before squinting, in this order (DESIGN.md reading
+ *           R-jit; P:267 names "lighting and color jitter", S:55-63 the three factors):
+ *             x1 = u8(b x);  m = sum_p grey(x1) / (h w);  x2 = u8(c x1 + (1 - c) m);
+ *             x3 = u8(s x2 + (1 - s) grey(x2));  squint(x3)
+ *           u8(v) = truncate(clamp(v, 0, 255)), grey(x) = u8((0.2989 R + 0.587 G) + 0.114 B),
+ *           every f32 product and sum rounded separately.  (1, 1, 1) is a bitwise no-op.
+ *   factor  1 is the direct-render path (Fig. 2: frames rendered at the stored resolution).
+ * ring2 / slots2 as in squint_insert2.  CHW without jitter is exactly squint_insert2; the
+ * other cases stage each frame in shared memory (one CTA per frame) and need c <= 4 and
+ * c*h*w <= 200 KB (SQUINT_EUNSUPPORTED otherwise).  Errors: EINVAL (layout, NULL, jitter with
+ * c != 3, ring2 without slots2), ESHAPE (divisibility). */
+#define SQUINT_LAYOUT_CHW 0
+#define SQUINT_LAYOUT_HWC 1
+SQUINT_API squint_status squint_insert_ex(const uint8_t* frames, int64_t n, int c, int h, int w, int factor,
+                                          int layout, const float* jitter, const int64_t* slots, uint8_t* ring,
+                                          const int64_t* slots2, uint8_t* ring2, int64_t capacity,
+                                          squint_stream_t stream);
+
 /* ---- a16: batched rollout inference (Algorithm 1 L4-5) -------------------
  * frames u8 [n, img_c, frame_h, frame_w] with frame_h = img_h * f, frame_w = img_w * f
  * (f >= 1; f = 1 means already squinted); proprio [n, P]; eps [n, A] N(0,1) noise or

@@ -22,7 +22,8 @@ __all__ = [
     "tanh_gaussian_bwd", "softmax", "log_softmax", "make_support", "categorical_project",
     "expected_value", "cross_entropy", "adam_step", "polyak", "target_distribution",
     "critic_loss_and_grads", "actor_forward", "alpha_loss_and_grad", "actor_loss_and_grads",
-    "update", "act", "insert", "soft_update", "init_state",
+    "update", "act", "insert", "soft_update", "init_state", "GREY_W", "grey_u8", "color_jitter",
+    "insert_ex",
 ]
 
 LOG_2PI = math.log(2.0 * math.pi)
@@ -163,6 +164,61 @@ def insert(frames, factor, slots, ring):
     ring = ring.copy()
     ring[np.asarray(slots)] = area_downsample(frames, factor)
     return ring
+
+
+# --------------------------------------------------------------------------------------
+# f4: renderer-side insert variants.  Colour jitter: P:267 names "lighting
+# and color jitter alterations" and nothing more; S:55-63 fixes three factors (brightness,
+# contrast, saturation) with a [1, 1] identity, clamping to [0, 255], and S:84 applies the
+# jitter to the full-resolution frame before squinting.  The formulas and their order are
+# reading R-jit: single-precision arithmetic with every product and sum
+# rounded on its own and an 8-bit image after every step, because the integer pixel values
+# the jitter produces are decided in the kernel's precision (the paper fixes none).
+# --------------------------------------------------------------------------------------
+GREY_W = (np.float32(0.2989), np.float32(0.587), np.float32(0.114))  # R-jit: Rec. 601 luma weights
+
+
+def _u8(x):
+    """u8(v) = truncate(clamp(v, 0, 255)) of a float32 array."""
+    return np.clip(x, np.float32(0), np.float32(255)).astype(np.uint8)
+
+
+def grey_u8(img):
+    """grey(x) = u8((0.2989 R + 0.587 G) + 0.114 B) of a u8 [3, H, W] image, float32, left to right."""
+    r, g, b = (img[k].astype(np.float32) for k in range(3))
+    return _u8((GREY_W[0] * r + GREY_W[1] * g) + GREY_W[2] * b)
+
+
+def color_jitter(frames, factors):
+    """frames u8 [N, 3, H, W], factors float32 [N, 3] = (brightness b, contrast c, saturation s).
+
+    Per frame, in this order (R-jit):
+      x1 = u8(b x)
+      m  = (sum over pixels of grey(x1)) / (H W)        (the integer sum is exact in float32)
+      x2 = u8(c x1 + (1 - c) m)
+      x3 = u8(s x2 + (1 - s) grey(x2))
+    """
+    frames = np.asarray(frames)
+    factors = np.asarray(factors, np.float32)
+    out = np.empty_like(frames)
+    one = np.float32(1)
+    for k in range(frames.shape[0]):
+        b, c, s = factors[k]
+        x1 = _u8(b * frames[k].astype(np.float32))
+        m = np.float32(int(grey_u8(x1).astype(np.int64).sum())) / np.float32(x1.shape[1] * x1.shape[2])
+        x2 = _u8(c * x1.astype(np.float32) + (one - c) * m)
+        g2 = grey_u8(x2).astype(np.float32)
+        out[k] = _u8(s * x2.astype(np.float32) + (one - s) * g2[None])
+    return out
+
+
+def insert_ex(frames, factor, slots, ring, hwc=False, jitter=None):
+    """squint_insert_ex: HWC frames are read as their CHW transpose; the optional jitter
+    runs on the full-resolution frame before the squint; then ``insert``."""
+    x = np.ascontiguousarray(np.asarray(frames).transpose(0, 3, 1, 2)) if hwc else np.asarray(frames)
+    if jitter is not None:
+        x = color_jitter(x, jitter)
+    return insert(x, factor, slots, ring)
 
 
 def normalize_pixels(u8):

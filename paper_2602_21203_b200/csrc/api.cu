@@ -761,6 +761,29 @@ squint_status squint_insert2(const uint8_t* frames, int64_t n, int c, int h, int
   return SQUINT_OK;
 }
 
+squint_status squint_insert_ex(const uint8_t* frames, int64_t n, int c, int h, int w, int factor, int layout,
+                               const float* jitter, const int64_t* slots, uint8_t* ring, const int64_t* slots2,
+                               uint8_t* ring2, int64_t capacity, squint_stream_t stream) {
+  if (layout != SQUINT_LAYOUT_CHW && layout != SQUINT_LAYOUT_HWC) return fail(SQUINT_EINVAL, "unknown frame layout");
+  if (!ring2 != !slots2) return fail(SQUINT_EINVAL, "ring2 and slots2 must both be given or both be NULL");
+  if (n < 0) return fail(SQUINT_EINVAL, "n must be >= 0");
+  if (factor < 1) return fail(SQUINT_EINVAL, "factor must be >= 1");
+  if (capacity < 1) return fail(SQUINT_EINVAL, "capacity must be >= 1");
+  if (c < 1 || h < 1 || w < 1) return fail(SQUINT_ESHAPE, "frame dims must be positive");
+  if (h % factor || w % factor) return fail(SQUINT_ESHAPE, "frame size not divisible by factor (S:41)");
+  if (jitter && c != 3) return fail(SQUINT_EINVAL, "colour jitter needs RGB frames (c == 3)");
+  if (layout == SQUINT_LAYOUT_CHW && !jitter)
+    return squint_insert2(frames, n, c, h, w, factor, slots, ring, slots2, ring2, capacity, stream);
+  if (c > 4 || (int64_t)c * h * w > 200 * 1024)
+    return fail(SQUINT_EUNSUPPORTED, "HWC / jitter insert: c <= 4 and c*h*w <= 200 KB per frame");
+  if (n > 0x7fffffff) return fail(SQUINT_EUNSUPPORTED, "n > 2^31 - 1");
+  if (n == 0) return SQUINT_OK;
+  if (!frames || !slots || !ring) return fail(SQUINT_EINVAL, "NULL pointer");
+  PhaseScope ps(0, 0, (cudaStream_t)stream);
+  SQ_CK(launch_insert_ex(frames, n, c, h, w, factor, layout, jitter, slots, ring, (cudaStream_t)stream, slots2, ring2));
+  return SQUINT_OK;
+}
+
 squint_status squint_insert(const uint8_t* frames, int64_t n, int c, int h, int w, int factor, const int64_t* slots,
                             uint8_t* ring, int64_t capacity, squint_stream_t stream) {
   return squint_insert2(frames, n, c, h, w, factor, slots, ring, nullptr, nullptr, capacity, stream);

@@ -412,6 +412,111 @@ int launch_enc_bwd(const EncBwdArgs& a, cudaStream_t s) {
   return (int)cudaGetLastError();
 }
 
+// ---- f4 insert variants: HWC frames and colour jitter fused before the squint ----------------
+// One CTA per frame: the frame is staged once in shared memory (one HBM read), the jitter's
+// frame statistic (mean grey level after the brightness step) is reduced from it, and each thread
+// then squints whole output pixels (all channels at once: saturation mixes the channels).
+// Jitter (reading R-jit): per frame (b, c, s) > 0, in this order,
+//   x1 = u8(b x);  m = sum(grey(x1)) / (h w);  x2 = u8(c x1 + (1 - c) m);  x3 = u8(s x2 + (1 - s) grey(x2))
+// with u8(v) = truncate(clamp(v, 0, 255)) and grey(x) = u8((0.2989 R + 0.587 G) + 0.114 B), every
+// float32 operation rounded on its own (no contraction) so the integer decisions match the oracle.
+namespace {
+constexpr float kGreyR = 0.2989f, kGreyG = 0.587f, kGreyB = 0.114f;
+__device__ __forceinline__ float u8f(float v) { return truncf(fminf(fmaxf(v, 0.f), 255.f)); }
+__device__ __forceinline__ float grey_u8(float r, float g, float b) {
+  return truncf(__fadd_rn(__fadd_rn(__fmul_rn(kGreyR, r), __fmul_rn(kGreyG, g)), __fmul_rn(kGreyB, b)));
+}
+// c*x + (1-c)*m with each product and the sum rounded separately
+__device__ __forceinline__ float blend(float cf, float x, float omc, float m) {
+  return u8f(__fadd_rn(__fmul_rn(cf, x), __fmul_rn(omc, m)));
+}
+}  // namespace
+
+__global__ void __launch_bounds__(256) k_insert_ex(const uint8_t* __restrict__ frames, int c, int h, int w, int f,
+                                                   int hwc, const float* __restrict__ jitter,
+                                                   const int64_t* __restrict__ slots, uint8_t* __restrict__ ring,
+                                                   const int64_t* __restrict__ slots2, uint8_t* __restrict__ ring2) {
+  extern __shared__ __align__(16) uint8_t sfr[];
+  __shared__ uint32_t wsum[8];
+  grid_wait();
+  grid_trigger();
+  const int fr = blockIdx.x, tid = threadIdx.x;
+  const int64_t fb = (int64_t)c * h * w;
+  const uint8_t* src = frames + fr * fb;
+  if ((fb & 15) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    for (int64_t i = tid; i < fb / 16; i += 256)
+      reinterpret_cast<uint4*>(sfr)[i] = __ldcs(reinterpret_cast<const uint4*>(src) + i);
+  } else {
+    for (int64_t i = tid; i < fb; i += 256) sfr[i] = src[i];
+  }
+  __syncthreads();
+  const int hw = h * w;
+  // element (channel ch, pixel p) of the staged frame
+  auto px = [&](int ch, int p) -> float { return (float)sfr[hwc ? p * c + ch : ch * hw + p]; };
+  float bf = 1.f, cf = 1.f, sf = 1.f, m = 0.f;
+  if (jitter) {
+    bf = jitter[fr * 3 + 0], cf = jitter[fr * 3 + 1], sf = jitter[fr * 3 + 2];
+    uint32_t gs = 0;
+    for (int p = tid; p < hw; p += 256)
+      gs += (uint32_t)grey_u8(u8f(__fmul_rn(bf, px(0, p))), u8f(__fmul_rn(bf, px(1, p))), u8f(__fmul_rn(bf, px(2, p))));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
+    if ((tid & 31) == 0) wsum[tid >> 5] = gs;
+    __syncthreads();
+    uint32_t t = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += wsum[i];
+    m = __fdiv_rn((float)t, (float)hw);  // the integer sum is exact in fp32 up to 2^24
+  }
+  const float omc = __fsub_rn(1.f, cf), oms = __fsub_rn(1.f, sf);
+  const int ho = h / f, wo = w / f, npo = ho * wo;
+  for (int o = tid; o < npo; o += 256) {
+    const int oy = o / wo, ox = o - oy * wo;
+    uint32_t acc[4] = {0u, 0u, 0u, 0u};
+    for (int a = 0; a < f; ++a)
+      for (int bb = 0; bb < f; ++bb) {
+        const int p = (oy * f + a) * w + ox * f + bb;
+        if (jitter) {
+          float x[3];
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) x[ch] = u8f(__fmul_rn(bf, px(ch, p)));
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) x[ch] = blend(cf, x[ch], omc, m);
+          const float g2 = grey_u8(x[0], x[1], x[2]);
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) acc[ch] += (uint32_t)blend(sf, x[ch], oms, g2);
+        } else {
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch)
+            if (ch < c) acc[ch] += (uint32_t)px(ch, p);
+        }
+      }
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch)
+      if (ch < c) {
+        const uint8_t q = (uint8_t)rhe_div(acc[ch], (uint32_t)(f * f));
+        ring[(slots[fr] * c + ch) * (int64_t)npo + o] = q;
+        if (ring2) ring2[(slots2[fr] * c + ch) * (int64_t)npo + o] = q;
+      }
+  }
+}
+
+int launch_insert_ex(const uint8_t* frames, int64_t n, int c, int h, int w, int factor, int hwc, const float* jitter,
+                     const int64_t* slots, uint8_t* ring, cudaStream_t s, const int64_t* slots2, uint8_t* ring2) {
+  if (n == 0) return 0;
+  const size_t smem = (size_t)c * h * w;
+  if (c > 4 || (jitter && c != 3) || smem > 200 * 1024 || n > 0x7fffffff) return (int)cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_insert_ex, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  note_launch(s, "k_insert_ex", 0, (double)n * c * h * w + (ring2 ? 2.0 : 1.0) * n * c * (h / factor) * (w / factor));
+  launch_pdl(k_insert_ex, dim3((unsigned)n), dim3(256), smem, s, frames, c, h, w, factor, hwc, jitter, slots, ring,
+             slots2, ring2);
+  return (int)cudaGetLastError();
+}
+
 int launch_insert(const uint8_t* frames, int64_t n, int c, int h, int w, int factor, const int64_t* slots,
                   uint8_t* ring, cudaStream_t s, const int64_t* slots2, uint8_t* ring2) {
   if (n == 0) return 0;

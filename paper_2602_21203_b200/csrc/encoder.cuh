@@ -82,6 +82,11 @@ int launch_conv_tiles(const float* w1, const float* w2, int C, uint8_t* tiles, c
 size_t enc_bwd_partial_floats(int C, int c_in, int nchunk);
 int enc_bwd_nchunk(int B);
 
+// f4 variants: HWC frames (hwc = 1) and/or colour jitter (jitter [n,3] = brightness, contrast,
+// saturation per frame; c == 3) fused before the squint; one CTA per frame (c*h*w <= 200 KB)
+int launch_insert_ex(const uint8_t* frames, int64_t n, int c, int h, int w, int factor, int hwc, const float* jitter,
+                     const int64_t* slots, uint8_t* ring, cudaStream_t s, const int64_t* slots2 = nullptr,
+                     uint8_t* ring2 = nullptr);
 // ring2 / slots2 (optional): a second destination written with the same squinted frames
 int launch_insert(const uint8_t* frames, int64_t n, int c, int h, int w, int factor, const int64_t* slots,
                   uint8_t* ring, cudaStream_t s, const int64_t* slots2 = nullptr, uint8_t* ring2 = nullptr);

@@ -71,6 +71,7 @@ def _load():
         "squint_comm_destroy": (st, [vp]),
         "squint_insert": (st, [vp, i64, i32, i32, i32, i32, vp, vp, i64, vp]),
         "squint_insert2": (st, [vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, i64, vp]),
+        "squint_insert_ex": (st, [vp, i64, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp]),
         "squint_act": (st, [C.POINTER(Dims), C.POINTER(HParams), vp, vp, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp,
                             i64, vp, vp]),
         "squint_update": (st, [C.POINTER(Dims), C.POINTER(HParams), C.POINTER(Replay), vp, vp, vp, i32,
@@ -95,7 +96,7 @@ def _load():
 LIB = _load()
 EXPORTED = ["squint_last_error", "squint_version", "squint_param_layout", "squint_workspace_bytes",
             "squint_workspace_region", "squint_act_workspace_bytes", "squint_comm_unique_id", "squint_comm_init",
-            "squint_comm_destroy", "squint_insert", "squint_insert2", "squint_act", "squint_update", "squint_soft_update",
+            "squint_comm_destroy", "squint_insert", "squint_insert2", "squint_insert_ex", "squint_act", "squint_update", "squint_soft_update",
             "squint_launch_count", "squint_set_phase_events", "squint_phase_name", "squint_selftest_gemm",
             "squint_set_launch_events", "squint_record_launch_event", "squint_launch_info",
             "squint_set_option"]
@@ -268,6 +269,21 @@ def squint_insert2(frames: torch.Tensor, factor: int, slots: torch.Tensor, ring:
     n, c, h, w = frames.shape
     _check(LIB.squint_insert2(_ptr(frames), n, c, h, w, factor, _ptr(slots), _ptr(ring), _ptr(slots2), _ptr(ring2),
                               min(ring.shape[0], ring2.shape[0]), _stream(stream)))
+
+
+LAYOUT_CHW, LAYOUT_HWC = 0, 1
+
+
+def squint_insert_ex(frames: torch.Tensor, factor: int, slots: torch.Tensor, ring: torch.Tensor, hwc: bool = False,
+                     jitter=None, slots2=None, ring2=None, stream=None):
+    """frames [n, c, h, w] (or [n, h, w, c] with hwc=True); jitter None or f32 [n, 3]."""
+    if hwc:
+        n, h, w, c = frames.shape
+    else:
+        n, c, h, w = frames.shape
+    cap = ring.shape[0] if ring2 is None else min(ring.shape[0], ring2.shape[0])
+    _check(LIB.squint_insert_ex(_ptr(frames), n, c, h, w, factor, LAYOUT_HWC if hwc else LAYOUT_CHW, _ptr(jitter),
+                                _ptr(slots), _ptr(ring), _ptr(slots2), _ptr(ring2), cap, _stream(stream)))
 
 
 def squint_soft_update(target: torch.Tensor, online: torch.Tensor, tau: float, stream=None):

@@ -167,6 +167,12 @@ def make_frames(n, hw=128, seed=0, channels=3):
     return np.ascontiguousarray(np.clip(base + np.rint(field).astype(np.int16), 0, 255).astype(np.uint8))
 
 
+def make_jitter(n, seed=5, lo=0.6, hi=1.4):
+    """f32 [n, 3] colour-jitter factors (brightness, contrast, saturation), each U[lo, hi]
+    (S:31-34 intervals; the paper gives no ranges -- reading R-jit)."""
+    return _rng(seed + 11).uniform(lo, hi, (n, 3)).astype(np.float32)
+
+
 def make_slots(n, capacity, seed=2):
     """Distinct write slots (Q4)."""
     return _rng(seed).choice(capacity, n, replace=False).astype(np.int64)

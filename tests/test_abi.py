@@ -103,6 +103,18 @@ def test_insert2_arg_errors():
     assert S.LIB.squint_insert2(null, 0, 3, 128, 128, 8, null, null, null, null, 10, null) == 0
 
 
+def test_insert_ex_arg_errors():
+    null, one = C.c_void_p(0), C.c_void_p(16)
+    f = S.LIB.squint_insert_ex
+    assert f(null, 0, 3, 128, 128, 8, 2, null, null, null, null, null, 10, null) == 1      # unknown layout
+    assert f(null, 0, 4, 128, 128, 8, 0, one, null, null, null, null, 10, null) == 1      # jitter needs c == 3
+    assert f(null, 0, 3, 130, 128, 8, 1, null, null, null, null, null, 10, null) == 2
+    assert f(null, 0, 8, 128, 128, 8, 1, null, null, null, null, null, 10, null) == 5     # c > 4 unsupported
+    assert f(null, 0, 3, 512, 512, 8, 1, null, null, null, null, null, 10, null) == 5     # > 200 KB per frame
+    assert f(null, 0, 3, 128, 128, 8, 1, null, null, null, null, one, 10, null) == 1      # ring2 without slots2
+    assert f(null, 0, 3, 128, 128, 8, 1, one, null, null, null, null, 10, null) == 0      # n == 0 no-op
+
+
 def test_soft_update_arg_errors():
     null = C.c_void_p(0)
     assert S.LIB.squint_soft_update(null, null, 10, 1.5, null) == 1

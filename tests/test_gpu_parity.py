@@ -79,6 +79,43 @@ def test_insert2_both_rings_bit_exact(n, hw, factor):
     assert np.array_equal(g2.cpu().numpy(), e2)
 
 
+@pytest.mark.parametrize("n,hw,factor,hwc,jit", [
+    (37, 128, 8, False, True), (37, 128, 8, True, False), (37, 128, 8, True, True), (5, 64, 4, True, True),
+    (9, 16, 1, True, False), (9, 16, 1, False, True), (3, 48, 3, False, True), (1024, 128, 8, True, True)])
+def test_insert_ex_variants_bit_exact(n, hw, factor, hwc, jit):
+    """f4: HWC frames and colour jitter fused before the squint, factor 1 = direct render --
+    bit-exact against the oracle (both rings, untouched rows unchanged)."""
+    chw = SI.make_frames(n, hw, seed=n + 5)
+    frames = np.ascontiguousarray(chw.transpose(0, 2, 3, 1)) if hwc else chw
+    jitter = SI.make_jitter(n, seed=n) if jit else None
+    cap = n + 7
+    slots = SI.make_slots(n, cap, seed=n + 2)
+    slots2 = (slots + 3) % cap
+    r1 = np.full((cap, 3, hw // factor, hw // factor), 5, np.uint8)
+    r2 = np.full_like(r1, 6)
+    e1 = O.insert_ex(frames, factor, slots, r1, hwc=hwc, jitter=jitter)
+    e2 = O.insert_ex(frames, factor, slots2, r2, hwc=hwc, jitter=jitter)
+    g1, g2 = torch.as_tensor(r1).to(DEV), torch.as_tensor(r2).to(DEV)
+    P.squint_insert_ex(torch.as_tensor(frames).to(DEV), factor, torch.as_tensor(slots).to(DEV), g1, hwc=hwc,
+                       jitter=None if jitter is None else torch.as_tensor(jitter).to(DEV),
+                       slots2=torch.as_tensor(slots2).to(DEV), ring2=g2)
+    torch.cuda.synchronize()
+    assert np.array_equal(g1.cpu().numpy(), e1)
+    assert np.array_equal(g2.cpu().numpy(), e2)
+
+
+def test_insert_ex_identity_jitter_equals_plain_insert():
+    frames = SI.make_frames(64, 128, seed=1)
+    slots = torch.arange(64, device=DEV)
+    a = torch.zeros((64, 3, 16, 16), dtype=torch.uint8, device=DEV)
+    b = torch.zeros_like(a)
+    ft = torch.as_tensor(frames).to(DEV)
+    P.squint_insert(ft, 8, slots, a)
+    P.squint_insert_ex(ft, 8, slots, b, jitter=torch.ones((64, 3), device=DEV))
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
 # ---- a14 soft update ------------------------------------------------------------------
 @pytest.mark.parametrize("n,tau", [(1, 0.005), (1000, 0.005), (4097, 0.5), (33, 0.0), (33, 1.0)])
 def test_soft_update(n, tau):
