@@ -420,20 +420,27 @@ int launch_enc_bwd(const EncBwdArgs& a, cudaStream_t s) {
 //   x1 = u8(b x);  m = sum(grey(x1)) / (h w);  x2 = u8(c x1 + (1 - c) m);  x3 = u8(s x2 + (1 - s) grey(x2))
 // with u8(v) = truncate(clamp(v, 0, 255)) and grey(x) = u8((0.2989 R + 0.587 G) + 0.114 B), every
 // float32 operation rounded on its own (no contraction) so the integer decisions match the oracle.
+// ALU form: bytes become exact floats by one PRMT into the 2^23 mantissa (no I2F), and u8() is a
+// clamp plus one round-down add of 2^23 (the integer lands in the low mantissa bits: no F2I).
 namespace {
-constexpr float kGreyR = 0.2989f, kGreyG = 0.587f, kGreyB = 0.114f;
-__device__ __forceinline__ float u8f(float v) { return truncf(fminf(fmaxf(v, 0.f), 255.f)); }
-__device__ __forceinline__ float grey_u8(float r, float g, float b) {
-  return truncf(__fadd_rn(__fadd_rn(__fmul_rn(kGreyR, r), __fmul_rn(kGreyG, g)), __fmul_rn(kGreyB, b)));
+constexpr float kGreyR = 0.2989f, kGreyG = 0.587f, kGreyB = 0.114f, kMagic = 8388608.f;
+constexpr uint32_t kMagicBits = 0x4B000000u;
+// byte k of w as an exact float
+__device__ __forceinline__ float bytef(uint32_t w, int k) {
+  return __fsub_rn(__uint_as_float(__byte_perm(w, kMagicBits, 0x7540u | (uint32_t)k)), kMagic);
 }
-// c*x + (1-c)*m with each product and the sum rounded separately
-__device__ __forceinline__ float blend(float cf, float x, float omc, float m) {
-  return u8f(__fadd_rn(__fmul_rn(cf, x), __fmul_rn(omc, m)));
+// 2^23 + u8(v): the value is (result - 2^23), the integer is (bits - kMagicBits)
+__device__ __forceinline__ float u8m(float v) { return __fadd_rd(fminf(fmaxf(v, 0.f), 255.f), kMagic); }
+__device__ __forceinline__ float grey_m(float r, float g, float b) {
+  return __fadd_rd(__fadd_rn(__fadd_rn(__fmul_rn(kGreyR, r), __fmul_rn(kGreyG, g)), __fmul_rn(kGreyB, b)), kMagic);
 }
+__device__ __forceinline__ uint32_t mbits(float m) { return __float_as_uint(m) - kMagicBits; }
+__device__ __forceinline__ float mval(float m) { return __fsub_rn(m, kMagic); }
 }  // namespace
 
+template <bool HWC, bool JIT>
 __global__ void __launch_bounds__(256) k_insert_ex(const uint8_t* __restrict__ frames, int c, int h, int w, int f,
-                                                   int hwc, const float* __restrict__ jitter,
+                                                   const float* __restrict__ jitter,
                                                    const int64_t* __restrict__ slots, uint8_t* __restrict__ ring,
                                                    const int64_t* __restrict__ slots2, uint8_t* __restrict__ ring2) {
   extern __shared__ __align__(16) uint8_t sfr[];
@@ -441,7 +448,8 @@ __global__ void __launch_bounds__(256) k_insert_ex(const uint8_t* __restrict__ f
   grid_wait();
   grid_trigger();
   const int fr = blockIdx.x, tid = threadIdx.x;
-  const int64_t fb = (int64_t)c * h * w;
+  const int hw = h * w;
+  const int64_t fb = (int64_t)c * hw;
   const uint8_t* src = frames + fr * fb;
   if ((fb & 15) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
     for (int64_t i = tid; i < fb / 16; i += 256)
@@ -450,15 +458,50 @@ __global__ void __launch_bounds__(256) k_insert_ex(const uint8_t* __restrict__ f
     for (int64_t i = tid; i < fb; i += 256) sfr[i] = src[i];
   }
   __syncthreads();
-  const int hw = h * w;
-  // element (channel ch, pixel p) of the staged frame
-  auto px = [&](int ch, int p) -> float { return (float)sfr[hwc ? p * c + ch : ch * hw + p]; };
-  float bf = 1.f, cf = 1.f, sf = 1.f, m = 0.f;
-  if (jitter) {
+  // byte offset of (channel ch, pixel p) in the staged frame
+  auto off = [&](int ch, int p) -> int { return HWC ? p * 3 + ch : ch * hw + p; };
+  float bf = 1.f, cf = 1.f, sf = 1.f, cm = 0.f;
+  if constexpr (JIT) {
+    // pass 1: x1 = u8(b x) written back in place; sum of grey(x1)
     bf = jitter[fr * 3 + 0], cf = jitter[fr * 3 + 1], sf = jitter[fr * 3 + 2];
     uint32_t gs = 0;
-    for (int p = tid; p < hw; p += 256)
-      gs += (uint32_t)grey_u8(u8f(__fmul_rn(bf, px(0, p))), u8f(__fmul_rn(bf, px(1, p))), u8f(__fmul_rn(bf, px(2, p))));
+    if ((hw & 3) == 0) {
+      uint32_t* s32 = reinterpret_cast<uint32_t*>(sfr);
+      for (int g = tid; g < hw / 4; g += 256) {
+        uint32_t wd[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) wd[k] = HWC ? s32[g * 3 + k] : s32[(k * hw) / 4 + g];
+        uint32_t o[3] = {0u, 0u, 0u};
+        float x1[4][3];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const int bi = HWC ? 3 * i + ch : 4 * ch + i;  // byte index within wd
+            const float m = u8m(__fmul_rn(bf, bytef(wd[bi >> 2], bi & 3)));
+            o[bi >> 2] |= mbits(m) << (8 * (bi & 3));
+            x1[i][ch] = mval(m);
+          }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) gs += mbits(grey_m(x1[i][0], x1[i][1], x1[i][2]));
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          if (HWC) s32[g * 3 + k] = o[k];
+          else s32[(k * hw) / 4 + g] = o[k];
+        }
+      }
+    } else {
+      for (int p = tid; p < hw; p += 256) {
+        float x1[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          const float m = u8m(__fmul_rn(bf, (float)sfr[off(ch, p)]));
+          sfr[off(ch, p)] = (uint8_t)mbits(m);
+          x1[ch] = mval(m);
+        }
+        gs += mbits(grey_m(x1[0], x1[1], x1[2]));
+      }
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
     if ((tid & 31) == 0) wsum[tid >> 5] = gs;
@@ -466,31 +509,63 @@ __global__ void __launch_bounds__(256) k_insert_ex(const uint8_t* __restrict__ f
     uint32_t t = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) t += wsum[i];
-    m = __fdiv_rn((float)t, (float)hw);  // the integer sum is exact in fp32 up to 2^24
+    // the integer sum is exact in fp32 up to 2^24; (1 - c) m is one rounded product
+    cm = __fmul_rn(__fsub_rn(1.f, cf), __fdiv_rn((float)t, (float)hw));
   }
-  const float omc = __fsub_rn(1.f, cf), oms = __fsub_rn(1.f, sf);
+  const float oms = __fsub_rn(1.f, sf);
+  // one pixel (channel values x[0..2], x1 when jittered) into the channel sums
+  auto add_px = [&](const float* x, uint32_t* acc) {
+    float x2[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) x2[ch] = mval(u8m(__fadd_rn(__fmul_rn(cf, x[ch]), cm)));
+    const float sg = __fmul_rn(oms, mval(grey_m(x2[0], x2[1], x2[2])));
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) acc[ch] += mbits(u8m(__fadd_rn(__fmul_rn(sf, x2[ch]), sg)));
+  };
   const int ho = h / f, wo = w / f, npo = ho * wo;
+  const bool vec8 = f == 8 && (!JIT || c == 3) && (HWC ? c == 3 : true);
   for (int o = tid; o < npo; o += 256) {
     const int oy = o / wo, ox = o - oy * wo;
     uint32_t acc[4] = {0u, 0u, 0u, 0u};
-    for (int a = 0; a < f; ++a)
-      for (int bb = 0; bb < f; ++bb) {
-        const int p = (oy * f + a) * w + ox * f + bb;
-        if (jitter) {
+    if (vec8 && (JIT || HWC)) {
+      // 8 rows x 8 pixels x 3 channels: 24 bytes per row in 8-byte loads
+      for (int a = 0; a < 8; ++a) {
+        const int p0 = (oy * 8 + a) * w + ox * 8;
+        uint32_t wd[6];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const uint2 v = HWC ? reinterpret_cast<const uint2*>(sfr + p0 * 3)[k]
+                              : *reinterpret_cast<const uint2*>(sfr + k * hw + p0);
+          wd[2 * k] = v.x, wd[2 * k + 1] = v.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
           float x[3];
 #pragma unroll
-          for (int ch = 0; ch < 3; ++ch) x[ch] = u8f(__fmul_rn(bf, px(ch, p)));
-#pragma unroll
-          for (int ch = 0; ch < 3; ++ch) x[ch] = blend(cf, x[ch], omc, m);
-          const float g2 = grey_u8(x[0], x[1], x[2]);
-#pragma unroll
-          for (int ch = 0; ch < 3; ++ch) acc[ch] += (uint32_t)blend(sf, x[ch], oms, g2);
-        } else {
-#pragma unroll
-          for (int ch = 0; ch < 4; ++ch)
-            if (ch < c) acc[ch] += (uint32_t)px(ch, p);
+          for (int ch = 0; ch < 3; ++ch) {
+            const int bi = HWC ? 3 * i + ch : 8 * ch + i;
+            x[ch] = JIT ? bytef(wd[bi >> 2], bi & 3) : 0.f;
+            if (!JIT) acc[ch] += (wd[bi >> 2] >> (8 * (bi & 3))) & 0xFFu;
+          }
+          if (JIT) add_px(x, acc);
         }
       }
+    } else {
+      for (int a = 0; a < f; ++a)
+        for (int bb = 0; bb < f; ++bb) {
+          const int p = (oy * f + a) * w + ox * f + bb;
+          if constexpr (JIT) {
+            float x[3];
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) x[ch] = (float)sfr[off(ch, p)];
+            add_px(x, acc);
+          } else {
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch)
+              if (ch < c) acc[ch] += sfr[HWC ? p * c + ch : ch * hw + p];
+          }
+        }
+    }
 #pragma unroll
     for (int ch = 0; ch < 4; ++ch)
       if (ch < c) {
@@ -506,14 +581,11 @@ int launch_insert_ex(const uint8_t* frames, int64_t n, int c, int h, int w, int 
   if (n == 0) return 0;
   const size_t smem = (size_t)c * h * w;
   if (c > 4 || (jitter && c != 3) || smem > 200 * 1024 || n > 0x7fffffff) return (int)cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_insert_ex, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  auto kern = hwc ? (jitter ? k_insert_ex<true, true> : k_insert_ex<true, false>)
+                  : (jitter ? k_insert_ex<false, true> : k_insert_ex<false, false>);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   note_launch(s, "k_insert_ex", 0, (double)n * c * h * w + (ring2 ? 2.0 : 1.0) * n * c * (h / factor) * (w / factor));
-  launch_pdl(k_insert_ex, dim3((unsigned)n), dim3(256), smem, s, frames, c, h, w, factor, hwc, jitter, slots, ring,
-             slots2, ring2);
+  launch_pdl(kern, dim3((unsigned)n), dim3(256), smem, s, frames, c, h, w, factor, jitter, slots, ring, slots2, ring2);
   return (int)cudaGetLastError();
 }
 
