@@ -22,7 +22,7 @@ __all__ = [
     "tanh_gaussian_bwd", "softmax", "log_softmax", "make_support", "categorical_project",
     "expected_value", "cross_entropy", "adam_step", "polyak", "target_distribution",
     "critic_loss_and_grads", "actor_forward", "alpha_loss_and_grad", "actor_loss_and_grads",
-    "update", "act", "insert", "soft_update", "init_state", "GREY_W", "grey_u8", "color_jitter",
+    "update", "act", "insert", "soft_update", "init_state", "target_probs", "GREY_W", "grey_u8", "color_jitter",
     "insert_ex",
 ]
 
@@ -73,6 +73,7 @@ class HParams:
     beta2: float = 0.999
     adam_eps: float = 1e-8
     target_entropy: float = -6.0
+    target_mode: int = 0  # 0: average of the twin target heads (Q20); 1: CDQ-min (f3)
     ln_eps: float = 1e-5
     log_std_min: float = -5.0
     log_std_max: float = 2.0
@@ -498,15 +499,29 @@ def _head_input(*parts):
     return np.concatenate(parts, axis=1)
 
 
+def target_probs(p1, p2, z, mode=0):
+    """The twin target heads' distributions -> the one that is projected.
+
+    mode 0 (the paper's choice, "the average rather than CDQ", Algorithm 1 line 13, Q20):
+    pbar = (p1 + p2) / 2.  mode 1 (CDQ ablation, f3): per sample the head with the
+    smaller expected value sum_k p_ik z_k (ties: head 1)."""
+    if mode == 0:
+        return 0.5 * (p1 + p2)
+    q1, q2 = expected_value(p1, z), expected_value(p2, z)
+    return np.where((q2 < q1)[:, None], p2, p1)
+
+
 def target_distribution(d, hp, tgt, actor, hn, sn, r, done, eps_next, alpha0):
-    """Lines 11-13: a' ~ pi(.|z', s'), pbar = mean_i softmax(head_bar_i), m = Proj(...)."""
+    """Lines 11-13: a' ~ pi(.|z', s'), pbar = mean_i softmax(head_bar_i) (or CDQ-min,
+    ``hp.target_mode``), m = Proj(...)."""
     zpn, _ = projection_fwd(actor, "actor", hn, hp.ln_eps)
     out_n, _ = mlp_fwd(actor, "actor", _head_input(zpn, sn), hp.ln_eps)
     an, logpn, _ = tanh_gaussian_fwd(out_n, eps_next, hp.log_std_min, hp.log_std_max)
     zqn, _ = projection_fwd(tgt, "critic", hn, hp.ln_eps)
     x0 = _head_input(zqn, sn, an)
-    pbar = 0.5 * (softmax(mlp_fwd(tgt, "critic.q1", x0, hp.ln_eps)[0])
-                  + softmax(mlp_fwd(tgt, "critic.q2", x0, hp.ln_eps)[0]))          # Q20
+    z, _ = make_support(d.v_min, d.v_max, d.n_atoms)
+    pbar = target_probs(softmax(mlp_fwd(tgt, "critic.q1", x0, hp.ln_eps)[0]),
+                        softmax(mlp_fwd(tgt, "critic.q2", x0, hp.ln_eps)[0]), z, hp.target_mode)  # Q20
     not_done = 1.0 - done.astype(np.float64)                                          # Q22
     m = categorical_project(pbar, r, not_done, hp.gamma, alpha0 * logpn, d.v_min, d.v_max)  # Q21
     return m, logpn

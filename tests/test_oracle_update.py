@@ -253,3 +253,58 @@ def test_act_mean_action_and_sample():
     e = np.random.default_rng(1).standard_normal((3, d.action_dim))
     a1, lp1, _ = O.act(d, hp, st["critic"], st["actor"], frames, prop, e)
     assert not np.allclose(a0, a1)
+
+
+# ---- f3: CDQ-min target ------------------------------------------------
+def _cdq_target(d, st, b, mode, alpha0=0.7):
+    hp = O.HParams(target_entropy=-float(d.action_dim), target_mode=mode)
+    hn, _ = O.encoder_fwd(st["critic"], O.normalize_pixels(b["On"]))
+    return O.target_distribution(d, hp, st["target"], st["actor"], hn, b["sn"], b["r"], b["done"], b["eps"][0],
+                                 alpha0)
+
+
+def test_cdq_identical_heads_equals_average_spec395():
+    d, hp, specs, st, R = tiny_setup(seed=11)
+    for k in list(st["target"]):
+        if k.startswith("critic.q2"):
+            st["target"][k] = st["target"][k.replace("critic.q2", "critic.q1")].copy()
+    b = _batch(d, R)
+    m0, _ = _cdq_target(d, st, b, 0)
+    m1, _ = _cdq_target(d, st, b, 1)
+    assert np.array_equal(m0, m1)
+
+
+def test_cdq_target_mean_is_min_head_mean_spec395():
+    """Wide support (no clipping): the projection keeps the mean, so the CDQ target's mean is
+    r + (1-d) gamma min_i E_i (alpha = 0) and never exceeds the average target's mean."""
+    d, hp, specs, st, R = tiny_setup(seed=12, v_min=-60.0, v_max=60.0)
+    b = _batch(d, R)
+    b["r"] = 0.5 * b["r"]  # r + gamma z_j stays inside [-60, 60]
+    z, _ = O.make_support(d.v_min, d.v_max, d.n_atoms)
+    m0, _ = _cdq_target(d, st, b, 0, alpha0=0.0)  # no entropy shift: no atom leaves the support
+    m1, _ = _cdq_target(d, st, b, 1, alpha0=0.0)
+    # the heads' own expectations, from a separate forward of the target nets
+    hn, _ = O.encoder_fwd(st["critic"], O.normalize_pixels(b["On"]))
+    zpn, _ = O.projection_fwd(st["actor"], "actor", hn, 1e-5)
+    out_n, _ = O.mlp_fwd(st["actor"], "actor", np.concatenate([zpn, b["sn"]], 1), 1e-5)
+    an, _, _ = O.tanh_gaussian_fwd(out_n, b["eps"][0], -5.0, 2.0)
+    zq, _ = O.projection_fwd(st["target"], "critic", hn, 1e-5)
+    x0 = np.concatenate([zq, b["sn"], an], 1)
+    E = [O.softmax(O.mlp_fwd(st["target"], f"critic.q{i}", x0, 1e-5)[0]) @ z for i in (1, 2)]
+    nd = 1.0 - b["done"].astype(np.float64)
+    want = b["r"] + nd * 0.99 * np.minimum(E[0], E[1])
+    assert np.abs(m1 @ z - want).max() < 1e-9
+    assert (m1 @ z <= m0 @ z + 1e-12).all()
+    assert (E[0] != E[1]).all()  # distinct heads: the selection is exercised
+
+
+def test_cdq_picks_lower_mean_head_hand_case():
+    z = np.linspace(-10, 10, 21)
+    p1 = np.zeros((3, 21)); p2 = np.zeros((3, 21))
+    p1[0, 15] = p2[0, 5] = 1.0      # head 2 lower
+    p1[1, 4] = p2[1, 16] = 1.0      # head 1 lower
+    p1[2, 10] = p2[2, 10] = 1.0     # tie -> head 1
+    p2[2, 10] = 0.5; p2[2, 9] = 0.25; p2[2, 11] = 0.25  # same mean, different spread
+    out = O.target_probs(p1, p2, z, 1)
+    assert np.array_equal(out[0], p2[0]) and np.array_equal(out[1], p1[1]) and np.array_equal(out[2], p1[2])
+    assert np.array_equal(O.target_probs(p1, p2, z, 0), 0.5 * (p1 + p2))
