@@ -86,7 +86,11 @@ typedef struct {
   float target_entropy; /* H_t, -A (Q15)                                  */
   float ln_eps;         /* 1e-5 (Q9)                                      */
   float log_std_min, log_std_max; /* -5, 2 (Q13)                          */
+  int target_mode;      /* SQUINT_TARGET_AVG (the paper's, Algorithm 1
+                           line 13) | SQUINT_TARGET_CDQ: per sample the target
+                           head with the smaller expected value (f3) */
 } squint_hparams;
+enum { SQUINT_TARGET_AVG = 0, SQUINT_TARGET_CDQ = 1 };
 
 /* Replay ring, structure of arrays, caller-owned. */
 typedef struct {

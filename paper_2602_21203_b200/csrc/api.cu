@@ -367,6 +367,7 @@ static squint_status update_one(const Ctx& c, const squint_replay& R, const int6
     t.v_min = d.v_min;
     t.v_max = d.v_max;
     t.gamma = hp.gamma;
+    t.cdq = hp.target_mode == SQUINT_TARGET_CDQ;
     t.scale = inv_btotal;
     t.tlogits = c.F(w.tlogits);
     t.logits = c.F(w.logits);
@@ -649,6 +650,7 @@ static bool check_hp(const squint_hparams& h, std::string* e) {
   if (!(h.beta1 >= 0.f && h.beta1 < 1.f && h.beta2 >= 0.f && h.beta2 < 1.f)) return *e = "Adam betas in [0, 1)", false;
   if (!(h.adam_eps >= 0.f) || !(h.ln_eps > 0.f)) return *e = "eps must be positive", false;
   if (!(h.log_std_min < h.log_std_max)) return *e = "log_std_min must be < log_std_max", false;
+  if (h.target_mode != SQUINT_TARGET_AVG && h.target_mode != SQUINT_TARGET_CDQ) return *e = "unknown target_mode", false;
   return true;
 }
 

@@ -61,10 +61,12 @@ __global__ void __launch_bounds__(256) k_target_ce(const __grid_constant__ Targe
   stamp(1);
   const float dz = (a.v_max - a.v_min) / (float)(N - 1);
   const float shift = expf(a.log_alpha[0]) * a.logp_next[row];
-  // pbar = (softmax l1_bar + softmax l2_bar) / 2
+  // pbar = (softmax l1_bar + softmax l2_bar) / 2, or (CDQ, f3) the softmax of the head with the
+  // smaller expected value sum_k p_k z_k (ties: head 1)
   float pbar[NPL];
 #pragma unroll
   for (int i = 0; i < NPL; ++i) pbar[i] = 0.f;
+  float phd[2][NPL], ev[2];
 #pragma unroll
   for (int hd = 0; hd < 2; ++hd) {
     float mx = -INFINITY;
@@ -79,8 +81,23 @@ __global__ void __launch_bounds__(256) k_target_ce(const __grid_constant__ Targe
     }
     sum = warp_sum(sum);
     const float inv = 1.f / sum;
+    if (a.cdq) {
+      float q = 0.f;
 #pragma unroll
-    for (int i = 0; i < NPL; ++i) pbar[i] += 0.5f * e[i] * inv;
+      for (int i = 0; i < NPL; ++i) {
+        phd[hd][i] = e[i] * inv;
+        q += phd[hd][i] * (a.v_min + (float)(lane + 32 * i) * dz);
+      }
+      ev[hd] = warp_sum(q);
+    } else {
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) pbar[i] += 0.5f * e[i] * inv;
+    }
+  }
+  if (a.cdq) {
+    const int pick = ev[1] < ev[0] ? 1 : 0;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) pbar[i] = pick ? phd[1][i] : phd[0][i];
   }
   // Categorical projection (Q21-Q23) in the hat form m_k = sum_j pbar_j max(0, 1 - |b_j - k|):
   // atom j gives a_j = pbar_j (1 - f_j) to bin l_j = floor(b_j) and h_j = pbar_j f_j to bin

@@ -27,6 +27,7 @@ struct TargetCEArgs {
   float* scal;
   float beta1, beta2;
   unsigned long long* dbg;  // optional per-warp globaltimer stamps [B][4] (SQUINT_TCE_DBG)
+  int cdq;                  // 1: project the head with the smaller expected value (f3)
 };
 
 struct ActorQArgs {

@@ -718,6 +718,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     t.v_min = d.v_min;
     t.v_max = d.v_max;
     t.gamma = hp.gamma;
+    t.cdq = hp.target_mode == SQUINT_TARGET_CDQ;
     t.scale = inv_btotal;
     t.tlogits = c.F(w.tlogits);
     t.logits = c.F(w.logits);

@@ -34,7 +34,11 @@ class Dims(C.Structure):
 
 class HParams(C.Structure):
     _fields_ = [(n, C.c_float) for n in ("gamma", "tau", "lr_critic", "lr_actor", "lr_alpha", "beta1", "beta2",
-                                         "adam_eps", "target_entropy", "ln_eps", "log_std_min", "log_std_max")]
+                                         "adam_eps", "target_entropy", "ln_eps", "log_std_min", "log_std_max")] + [
+        ("target_mode", C.c_int)]
+
+
+TARGET_AVG, TARGET_CDQ = 0, 1
 
 
 class Replay(C.Structure):
@@ -225,7 +229,7 @@ def make_dims(d: dict, precision=FP32) -> Dims:
 
 
 def make_hparams(h: dict) -> HParams:
-    return HParams(*[h[n] for n, _ in HParams._fields_])
+    return HParams(*[h.get(n, 0) if n == "target_mode" else h[n] for n, _ in HParams._fields_])
 
 
 def param_layout(dims: Dims):

@@ -40,9 +40,9 @@ def oracle_state(specs, vals, m=None, v=None, steps=None):
 class Problem:
     """One seeded update problem: replay, params, Adam state, idx/shift/eps."""
 
-    def __init__(self, cfg="c0", capacity=None, utd=1, seed=0, prewarm=True, perturb=True, **dim_over):
+    def __init__(self, cfg="c0", capacity=None, utd=1, seed=0, prewarm=True, perturb=True, hp_over=None, **dim_over):
         self.dims = SI.dims_of(cfg, **dim_over)
-        self.hp = SI.hp_of(cfg)
+        self.hp = SI.hp_of(cfg, **(hp_over or {}))
         self.hp["target_entropy"] = -float(self.dims["action_dim"])
         self.d = O.Dims(**self.dims)
         self.h = O.HParams(**self.hp)

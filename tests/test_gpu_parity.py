@@ -226,6 +226,17 @@ def test_update_c2_shapes_b64_fp32():
     _check_update(pr, L, met, st_ref, met_ref, trace)
 
 
+@pytest.mark.parametrize("utd", [1, 3])
+def test_update_c0_cdq_fp32(utd):
+    """f3: CDQ-min target through the fp32 path, at the fp32 bars."""
+    pr = Problem("c0", utd=utd, seed=4, hp_over={"target_mode": 1})
+    L = pr.gpu_setup()
+    met = pr.gpu_update(L)
+    trace = []
+    st_ref, met_ref = pr.oracle_update(trace)
+    _check_update(pr, L, met, st_ref, met_ref, trace)
+
+
 def test_update_deterministic_bitwise():
     pr = Problem("c0", utd=2, seed=7)
     outs = []
@@ -374,6 +385,10 @@ def test_update_c2_full_batch_bf16(seed):
 @pytest.mark.parametrize("batch", [1, 37, 300])
 def test_update_ragged_batch_bf16(batch):
     _bf16_case("c2", seed=5, capacity=4096, batch=batch)
+
+
+def test_update_c2_cdq_bf16():
+    _bf16_case("c2", seed=5, utd=2, capacity=4096, hp_over={"target_mode": 1})
 
 
 def test_update_c3_shapes_bf16():
