@@ -22,7 +22,7 @@ __all__ = [
     "tanh_gaussian_bwd", "softmax", "log_softmax", "make_support", "categorical_project",
     "expected_value", "cross_entropy", "adam_step", "polyak", "target_distribution",
     "critic_loss_and_grads", "actor_forward", "alpha_loss_and_grad", "actor_loss_and_grads",
-    "update", "act", "insert", "soft_update", "init_state", "target_probs", "GREY_W", "grey_u8", "color_jitter",
+    "update", "act", "insert", "soft_update", "init_state", "target_probs", "target_value", "GREY_W", "grey_u8", "color_jitter",
     "insert_ex",
 ]
 
@@ -47,6 +47,11 @@ class Dims:
     v_min: float = -10.0
     v_max: float = 10.0
     batch: int = 32
+    critic_kind: int = 0  # 0: distributional C51; 1: scalar MSE critic (Eqs. 1-2, Algorithm 1; f3)
+
+    @property
+    def head_out(self):  # critic head width: n_atoms logits, or one Q value
+        return 1 if self.critic_kind == 1 else self.n_atoms
 
     @property
     def conv1_out(self):  # conv 3x3 stride 2 valid (Q7): 16 -> 7
@@ -115,8 +120,8 @@ def param_specs(d: Dims):
     n_in_q = d.latent + d.proprio_dim + d.action_dim   # Q11
     n_in_pi = d.latent + d.proprio_dim                  # Q12
     critic_tail = (_proj_specs("critic", d.flat, d.latent)
-                   + _mlp_specs("critic.q1", n_in_q, d.critic_hidden, d.n_atoms)
-                   + _mlp_specs("critic.q2", n_in_q, d.critic_hidden, d.n_atoms))
+                   + _mlp_specs("critic.q1", n_in_q, d.critic_hidden, d.head_out)
+                   + _mlp_specs("critic.q2", n_in_q, d.critic_hidden, d.head_out))
     actor = (_proj_specs("actor", d.flat, d.latent)
              + _mlp_specs("actor", n_in_pi, d.actor_hidden, 2 * d.action_dim))
     out = [("critic",) + s for s in enc + critic_tail]
@@ -527,8 +532,29 @@ def target_distribution(d, hp, tgt, actor, hn, sn, r, done, eps_next, alpha0):
     return m, logpn
 
 
+def target_value(d, hp, tgt, actor, hn, sn, r, done, eps_next, alpha0):
+    """f3 scalar critic, Algorithm 1 lines 11-13 as printed (Eq. 1):
+    a' ~ pi(.|z', s'), y = r + (1-d) gamma/2 sum_i (Qbar_i(z', s', a') - alpha_0 log pi(a'|.))
+    (the (1-d) mask is Q22).  CDQ (hp.target_mode 1; "elementwise min of expected
+    values (scalar)"): y = r + (1-d) gamma (min_i Qbar_i - alpha_0 log pi)."""
+    zpn, _ = projection_fwd(actor, "actor", hn, hp.ln_eps)
+    out_n, _ = mlp_fwd(actor, "actor", _head_input(zpn, sn), hp.ln_eps)
+    an, logpn, _ = tanh_gaussian_fwd(out_n, eps_next, hp.log_std_min, hp.log_std_max)
+    zqn, _ = projection_fwd(tgt, "critic", hn, hp.ln_eps)
+    x0 = _head_input(zqn, sn, an)
+    q1 = mlp_fwd(tgt, "critic.q1", x0, hp.ln_eps)[0][:, 0]
+    q2 = mlp_fwd(tgt, "critic.q2", x0, hp.ln_eps)[0][:, 0]
+    not_done = 1.0 - done.astype(np.float64)
+    if hp.target_mode == 0:
+        y = r + not_done * hp.gamma / 2.0 * ((q1 - alpha0 * logpn) + (q2 - alpha0 * logpn))
+    else:
+        y = r + not_done * hp.gamma * (np.minimum(q1, q2) - alpha0 * logpn)
+    return y, logpn
+
+
 def critic_loss_and_grads(d, hp, critic, O, s, a, m, scale):
     """Line 15 (distributional, Q24): L_Q = sum_i mean_b CE(m, l_i); grads for psi, theta.
+    Scalar critic (d.critic_kind 1, f3): L_Q = sum_i mean_b (Q_i - y)^2 with m = y [B].
 
     ``scale`` multiplies the per-sample gradient (1/B for the full batch; 1/B_global
     for a data-parallel shard, Q33).  Returns (loss computed with ``scale``, grads, h)."""
@@ -540,8 +566,14 @@ def critic_loss_and_grads(d, hp, critic, O, s, a, m, scale):
     dzq = np.zeros_like(zq)
     for i in (1, 2):
         logits, cache = mlp_fwd(critic, f"critic.q{i}", x0, hp.ln_eps)
-        loss += float(-(m * log_softmax(logits)).sum(axis=1).sum() * scale)
-        dlogits = (softmax(logits) - m) * scale
+        if d.critic_kind == 1:
+            # f3 scalar critic, line 15 / Eq. 2: (Q_i - y)^2 per sample, m holds y [B]
+            q = logits[:, 0]
+            loss += float(((q - m) ** 2).sum() * scale)
+            dlogits = (2.0 * (q - m) * scale)[:, None]
+        else:
+            loss += float(-(m * log_softmax(logits)).sum(axis=1).sum() * scale)
+            dlogits = (softmax(logits) - m) * scale
         gi, dx0 = mlp_bwd(dlogits, cache, f"critic.q{i}", critic)
         grads.update(gi)
         dzq += dx0[:, :d.latent]
@@ -568,18 +600,23 @@ def alpha_loss_and_grad(hp, log_alpha, mean_logp):
 
 def actor_loss_and_grads(d, hp, critic_new, actor, h, s, a, logp, caches, alpha1, scale):
     """Lines 19-22 (Q25): L_pi = mean_b [alpha+ log pi - (Q1+Q2)/2] on critic theta+."""
-    z, _ = make_support(d.v_min, d.v_max, d.n_atoms)
     zq, _ = projection_fwd(critic_new, "critic", h, hp.ln_eps)
     x0 = _head_input(zq, s, a)
     qs = []
     da = np.zeros_like(a)
     for i in (1, 2):
         logits, cache = mlp_fwd(critic_new, f"critic.q{i}", x0, hp.ln_eps)
-        pr = softmax(logits)
-        q = expected_value(pr, z)
+        if d.critic_kind == 1:  # f3 scalar critic: the head's output is Q_i (line 22)
+            q = logits[:, 0]
+            dq = -0.5 * scale * np.ones_like(q)
+            dlogits = dq[:, None]
+        else:
+            z, _ = make_support(d.v_min, d.v_max, d.n_atoms)
+            pr = softmax(logits)
+            q = expected_value(pr, z)
+            dq = -0.5 * scale * np.ones_like(q)
+            dlogits = pr * (z[None, :] - q[:, None]) * dq[:, None]   # softmax Jacobian times z
         qs.append(q)
-        dq = -0.5 * scale * np.ones_like(q)
-        dlogits = pr * (z[None, :] - q[:, None]) * dq[:, None]   # softmax Jacobian times z
         _, dx0 = mlp_bwd(dlogits, cache, f"critic.q{i}", critic_new)
         da += dx0[:, d.latent + d.proprio_dim:]
     qmean = 0.5 * (qs[0] + qs[1])
@@ -652,7 +689,10 @@ def _update_one(d, hp, R, idx, shift, eps, st):
     # Line 10: both encodings with the current psi; h' carries no gradient.
     hn, _ = encoder_fwd(st["critic"], normalize_pixels(On))
     # Lines 11-13: target distribution (alpha_0, pre-step phi, theta_bar).
-    m, logpn = target_distribution(d, hp, st["target"], st["actor"], hn, sn, r, done, eps[0], alpha0)
+    if d.critic_kind == 1:  # f3 scalar critic: m carries the TD target y [B]
+        m, logpn = target_value(d, hp, st["target"], st["actor"], hn, sn, r, done, eps[0], alpha0)
+    else:
+        m, logpn = target_distribution(d, hp, st["target"], st["actor"], hn, sn, r, done, eps[0], alpha0)
     # Lines 14-15: critic + encoder step.
     LQ, gc, h = critic_loss_and_grads(d, hp, st["critic"], O, s, a, m, scale)
     gnorm = _flat_norm(gc)

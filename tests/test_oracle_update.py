@@ -308,3 +308,79 @@ def test_cdq_picks_lower_mean_head_hand_case():
     out = O.target_probs(p1, p2, z, 1)
     assert np.array_equal(out[0], p2[0]) and np.array_equal(out[1], p1[1]) and np.array_equal(out[2], p1[2])
     assert np.array_equal(O.target_probs(p1, p2, z, 0), 0.5 * (p1 + p2))
+
+
+# ---- f3: scalar MSE critic (Eqs. 1-2, Algorithm 1 lines 13, 15, 22) ---------------------
+def test_mse_critic_loss_fd_all_tensors():
+    d, hp, specs, st, R = tiny_setup(seed=21, critic_kind=1)
+    assert st["critic"]["critic.q1.l3.w"].shape == (1, d.critic_hidden)
+    b = _batch(d, R)
+    y = np.random.default_rng(0).standard_normal(d.batch)
+    crit = st["critic"]
+    f = lambda: O.critic_loss_and_grads(d, hp, crit, b["O"], b["s"], b["a"], y, 1.0 / d.batch)[0]
+    L, g, _ = O.critic_loss_and_grads(d, hp, crit, b["O"], b["s"], b["a"], y, 1.0 / d.batch)
+    assert set(g) == {n for grp, n, *_ in specs if grp == "critic"}
+    for k in sorted(g):
+        _fd(f, crit[k], g[k])
+
+
+def test_mse_loss_and_zero_grad_at_target():
+    """L = sum_i mean_b (Q_i - y)^2 (Eq. 2); with y = Q_1 head 1 gets no gradient, head 2 does."""
+    d, hp, specs, st, R = tiny_setup(seed=22, critic_kind=1)
+    b = _batch(d, R)
+    crit = st["critic"]
+    h, _ = O.encoder_fwd(crit, O.normalize_pixels(b["O"]))
+    zq, _ = O.projection_fwd(crit, "critic", h, hp.ln_eps)
+    x0 = np.concatenate([zq, b["s"], b["a"]], 1)
+    q1 = O.mlp_fwd(crit, "critic.q1", x0, hp.ln_eps)[0][:, 0]
+    q2 = O.mlp_fwd(crit, "critic.q2", x0, hp.ln_eps)[0][:, 0]
+    y = q1.copy()
+    L, g, _ = O.critic_loss_and_grads(d, hp, crit, b["O"], b["s"], b["a"], y, 1.0 / d.batch)
+    assert abs(L - ((q2 - y) ** 2).mean()) < 1e-12
+    for k in [n for n in g if n.startswith("critic.q1.")]:
+        assert np.abs(g[k]).max() < 1e-15, k
+    assert np.abs(g["critic.q2.l3.w"]).max() > 1e-6
+    # d L / d b3 of head 2 = 2 mean(Q_2 - y) (the output bias enters Q_2 with slope 1)
+    assert abs(g["critic.q2.l3.b"][0] - 2 * (q2 - y).mean()) < 1e-12
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_mse_target_constant_heads_closed_form(mode):
+    """Target heads with zero output weights: Qbar_i = c_i, so y = r + (1-d) gamma (c - alpha
+    log pi') with c = (c1 + c2)/2 (Algorithm 1 line 13) or min(c1, c2) (CDQ)."""
+    d, hp, specs, st, R = tiny_setup(seed=23, critic_kind=1)
+    hp = O.HParams(target_entropy=-float(d.action_dim), target_mode=mode)
+    b = _batch(d, R)
+    b["done"] = np.array([0, 1, 0], np.uint8)
+    for i, c in ((1, 1.7), (2, -0.4)):
+        st["target"][f"critic.q{i}.l3.w"][:] = 0.0
+        st["target"][f"critic.q{i}.l3.b"][:] = c
+    hn, _ = O.encoder_fwd(st["critic"], O.normalize_pixels(b["On"]))
+    y, logpn = O.target_value(d, hp, st["target"], st["actor"], hn, b["sn"], b["r"], b["done"], b["eps"][0], 0.3)
+    zpn, _ = O.projection_fwd(st["actor"], "actor", hn, hp.ln_eps)
+    out, _ = O.mlp_fwd(st["actor"], "actor", np.concatenate([zpn, b["sn"]], 1), hp.ln_eps)
+    _, lp, _ = O.tanh_gaussian_fwd(out, b["eps"][0], hp.log_std_min, hp.log_std_max)
+    c = 0.65 if mode == 0 else -0.4
+    want = b["r"] + np.array([1.0, 0.0, 1.0]) * hp.gamma * (c - 0.3 * lp)
+    assert np.abs(y - want).max() < 1e-12
+    assert y[1] == b["r"][1]
+
+
+def test_mse_actor_loss_fd():
+    d, hp, specs, st, R = tiny_setup(seed=24, critic_kind=1)
+    b = _batch(d, R)
+    h, _ = O.encoder_fwd(st["critic"], O.normalize_pixels(b["O"]))
+    act, crit = st["actor"], st["critic"]
+
+    def f():
+        a, lp, c = O.actor_forward(d, hp, act, h, b["s"], b["eps"][1])
+        return O.actor_loss_and_grads(d, hp, crit, act, h, b["s"], a, lp, c, 0.3, 1.0 / d.batch)[0]
+    a, lp, c = O.actor_forward(d, hp, act, h, b["s"], b["eps"][1])
+    L, g, q = O.actor_loss_and_grads(d, hp, crit, act, h, b["s"], a, lp, c, 0.3, 1.0 / d.batch)
+    # L_pi = mean_b [alpha log pi - (Q1 + Q2)/2] with Q_i the heads' outputs (line 22)
+    zq, _ = O.projection_fwd(crit, "critic", h, hp.ln_eps)
+    x0 = np.concatenate([zq, b["s"], a], 1)
+    qm = 0.5 * sum(O.mlp_fwd(crit, f"critic.q{i}", x0, hp.ln_eps)[0][:, 0] for i in (1, 2))
+    assert abs(L - (0.3 * lp - qm).mean()) < 1e-12
+    for k in sorted(g):
+        _fd(f, act[k], g[k])
