@@ -76,7 +76,13 @@ typedef struct {
   float v_min, v_max;           /* atom support, v_min < v_max           */
   int batch;                    /* per-rank batch B                              */
   int precision;                /* SQUINT_FP32 | SQUINT_BF16                     */
+  int critic_kind;              /* SQUINT_CRITIC_C51 (the paper's distributional
+                                   critic) | SQUINT_CRITIC_MSE: scalar heads
+                                   (width 1) trained on the squared TD error of
+                                   Eqs. 1-2 / Algorithm 1 (f3); n_atoms, v_min,
+                                   v_max are then unused                          */
 } squint_dims;
+enum { SQUINT_CRITIC_C51 = 0, SQUINT_CRITIC_MSE = 1 };
 
 typedef struct {
   float gamma;          /* discount, 0 <= gamma <= 1                     */

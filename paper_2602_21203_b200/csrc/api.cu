@@ -61,7 +61,7 @@ static WsLay plan_ws(const squint_dims& d, const Layout& L) {
   WsPlan P;
   WsLay w;
   const size_t B = d.batch, F = flat_dim(d), Lt = d.latent, Hc = d.critic_hidden, Ha = d.actor_hidden,
-               N = d.n_atoms, A = d.action_dim, C = d.conv_ch, P1 = conv1_out(d) * conv1_out(d);
+               N = head_out(d), A = d.action_dim, C = d.conv_ch, P1 = conv1_out(d) * conv1_out(d);
   const size_t f = sizeof(float);
   auto proj = [&]() { return ProjC{P.take(B * Lt * f), P.take(B * Lt * f), P.take(B * f)}; };
   auto mlp = [&](size_t H) {
@@ -246,7 +246,7 @@ static squint_status update_one(const Ctx& c, const squint_replay& R, const int6
   const Layout& L = c.L;
   const WsLay& w = c.w;
   cudaStream_t s = c.s;
-  const int B = d.batch, F = flat_dim(d), Lt = d.latent, Hc = d.critic_hidden, Ha = d.actor_hidden, N = d.n_atoms,
+  const int B = d.batch, F = flat_dim(d), Lt = d.latent, Hc = d.critic_hidden, Ha = d.actor_hidden, N = head_out(d),
             A = d.action_dim, P = d.proprio_dim, C = d.conv_ch;
   const int nq = Lt + P + A, npi = Lt + P;
   const float* eps_next = eps;
@@ -368,6 +368,7 @@ static squint_status update_one(const Ctx& c, const squint_replay& R, const int6
     t.v_max = d.v_max;
     t.gamma = hp.gamma;
     t.cdq = hp.target_mode == SQUINT_TARGET_CDQ;
+    t.mse = d.critic_kind == SQUINT_CRITIC_MSE;
     t.scale = inv_btotal;
     t.tlogits = c.F(w.tlogits);
     t.logits = c.F(w.logits);
@@ -527,6 +528,7 @@ static squint_status update_one(const Ctx& c, const squint_replay& R, const int6
     SQ_CK(run_dense(b, s));
     ActorQArgs q;
     memset(&q, 0, sizeof(q));
+    q.mse = d.critic_kind == SQUINT_CRITIC_MSE;
     q.B = B;
     q.N = N;
     q.v_min = d.v_min;
@@ -712,7 +714,7 @@ squint_status squint_workspace_region(const squint_dims* dims, int region, size_
   switch (region) {
     case 0: *offset = w.grad_critic; *bytes = L.gsize[0] * f; break;
     case 1: *offset = w.grad_actor; *bytes = L.gsize[1] * f; break;
-    case 2: *offset = w.m; *bytes = B * dims->n_atoms * f; break;
+    case 2: *offset = w.m; *bytes = B * head_out(*dims) * f; break;
     case 3: *offset = w.h; *bytes = B * flat_dim(*dims) * f; break;
     case 4: *offset = w.logp_cur; *bytes = B * f; break;
     case 5: *offset = w.logp_next; *bytes = B * f; break;

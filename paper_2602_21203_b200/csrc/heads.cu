@@ -7,6 +7,8 @@
 //      reproducible); then CE of both online heads (Q24) and dL/dl = (softmax - m) s.
 //  k_actor_q: Q_i = sum_k softmax(l_i^+)_k z_k (Q25), dL_pi/dl_i = -s/2 p (z - Q_i),
 //      per-row terms of L_pi = s sum_b [alpha+ log pi_b - (Q1 + Q2)/2].
+//  k_target_mse / k_actor_q_mse: the scalar-critic variants (f3; Eqs. 1-2, Algorithm 1 lines
+//      13, 15, 22), thread per row.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -271,11 +273,68 @@ __global__ void __launch_bounds__(256) k_actor_q(const __grid_constant__ ActorQA
   }
 }
 
+// f3 scalar critic.  y = r + (1-d) gamma/2 sum_i (Qbar_i - alpha_0 log pi') (Algorithm 1 line 13,
+// Q22 mask) or, CDQ, r + (1-d) gamma (min_i Qbar_i - alpha_0 log pi');
+// L_Q = s sum_i sum_b (Q_i - y)^2, dL/dQ_i = 2 s (Q_i - y) (line 15, Eq. 2).
+__global__ void __launch_bounds__(256) k_target_mse(const __grid_constant__ TargetCEArgs a) {
+  grid_wait();
+  grid_trigger();
+  if (a.step && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t tc = ++a.step[0], ta = ++a.step[1];
+    a.scal[S_C1_CRITIC] = bias_corr(a.beta1, tc);
+    a.scal[S_C2_CRITIC] = bias_corr(a.beta2, tc);
+    a.scal[S_C1_ACTOR] = bias_corr(a.beta1, ta);
+    a.scal[S_C2_ACTOR] = bias_corr(a.beta2, ta);
+  }
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= a.B) return;
+  const int64_t ridx = a.idx[row];
+  const float nd = a.done[ridx] ? 0.f : 1.f;
+  const float sh = expf(a.log_alpha[0]) * a.logp_next[row];
+  const float t0 = a.tlogits[row], t1 = a.tlogits[a.B + row];
+  const float v = a.cdq ? fminf(t0, t1) - sh : 0.5f * ((t0 - sh) + (t1 - sh));
+  const float y = a.reward[ridx] + nd * a.gamma * v;
+  a.m[row] = y;
+  float loss = 0.f;
+#pragma unroll
+  for (int hd = 0; hd < 2; ++hd) {
+    const float e = a.logits[(int64_t)hd * a.B + row] - y;
+    loss += e * e;
+    const float g = 2.f * e * a.scale;
+    if (a.dlogits_bf) a.dlogits_bf[((int64_t)hd * a.B + row) * a.ld_dl] = __float2bfloat16_rn(g);
+    else a.dlogits[(int64_t)hd * a.B + row] = g;
+  }
+  a.row_loss[row] = loss * a.scale;
+}
+
+// L_pi = s sum_b [alpha+ log pi_b - (Q1 + Q2)/2] with Q_i the heads' outputs (line 22)
+__global__ void __launch_bounds__(256) k_actor_q_mse(const __grid_constant__ ActorQArgs a) {
+  grid_wait();
+  grid_trigger();
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= a.B) return;
+  const float g = -0.5f * a.scale;
+#pragma unroll
+  for (int hd = 0; hd < 2; ++hd) {
+    if (a.dlogits_bf) a.dlogits_bf[((int64_t)hd * a.B + row) * a.ld_dl] = __float2bfloat16_rn(g);
+    else a.dlogits[(int64_t)hd * a.B + row] = g;
+  }
+  const float qm = 0.5f * (a.logits[row] + a.logits[a.B + row]);
+  a.row_q[row] = qm;
+  a.row_lpi[row] = (a.alpha1[0] * a.logp[row] - qm) * a.scale;
+}
+
 }  // namespace
 
 static unsigned long long* g_tce_dbg = nullptr;
 int launch_target_ce(const TargetCEArgs& a_in, cudaStream_t s) {
   TargetCEArgs a = a_in;
+  if (a.mse) {
+    if (a.N != 1) return (int)cudaErrorInvalidValue;
+    note_launch(s, "k_target_mse", 0, 0);
+    launch_pdl(k_target_mse, dim3((a.B + 255) / 256), dim3(256), 0, s, a);
+    return (int)cudaGetLastError();
+  }
   static const bool dbg = getenv("SQUINT_TCE_DBG") != nullptr;
   if (dbg) {
     if (!g_tce_dbg) cudaMalloc(&g_tce_dbg, 4096 * 4 * sizeof(unsigned long long));
@@ -296,6 +355,12 @@ int launch_target_ce(const TargetCEArgs& a_in, cudaStream_t s) {
 }
 
 int launch_actor_q(const ActorQArgs& a, cudaStream_t s) {
+  if (a.mse) {
+    if (a.N != 1) return (int)cudaErrorInvalidValue;
+    note_launch(s, "k_actor_q_mse", 0, 0);
+    launch_pdl(k_actor_q_mse, dim3((a.B + 255) / 256), dim3(256), 0, s, a);
+    return (int)cudaGetLastError();
+  }
   const int npl = (a.N + 31) / 32;
   const dim3 grid((a.B + kRows - 1) / kRows);
   note_launch(s, "k_actor_q", 0, 0);

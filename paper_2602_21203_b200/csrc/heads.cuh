@@ -28,6 +28,7 @@ struct TargetCEArgs {
   float beta1, beta2;
   unsigned long long* dbg;  // optional per-warp globaltimer stamps [B][4] (SQUINT_TCE_DBG)
   int cdq;                  // 1: project the head with the smaller expected value (f3)
+  int mse;                  // 1: scalar critic (N == 1): m = y [B], dL/dQ_i = 2 s (Q_i - y) (f3)
 };
 
 struct ActorQArgs {
@@ -41,6 +42,7 @@ struct ActorQArgs {
   int ld_dl;
   float* row_q;            // [B]
   float* row_lpi;          // [B]
+  int mse;                 // 1: scalar critic, Q_i = logits (N == 1), dL_pi/dQ_i = -s/2 (f3)
 };
 
 int launch_target_ce(const TargetCEArgs& a, cudaStream_t s);

@@ -23,12 +23,14 @@ bool check_dims(const squint_dims& d, std::string* err) {
   if (d.pad < 0 || d.pad > 8) return fail("pad must be in [0, 8]");
   if (d.conv_ch < 1 || d.latent < 2 || d.proprio_dim < 0 || d.action_dim < 1) return fail("invalid layer width");
   if (d.critic_hidden < 2 || d.actor_hidden < 2) return fail("hidden width must be >= 2");
-  if (d.n_atoms < 2) return fail("n_atoms must be >= 2 (S:272)");
-  if (!(d.v_min < d.v_max)) return fail("v_min must be < v_max (S:272)");
+  if (d.critic_kind != SQUINT_CRITIC_C51 && d.critic_kind != SQUINT_CRITIC_MSE) return fail("unknown critic_kind");
+  const bool c51 = d.critic_kind == SQUINT_CRITIC_C51;
+  if (c51 && d.n_atoms < 2) return fail("n_atoms must be >= 2 (S:272)");
+  if (c51 && !(d.v_min < d.v_max)) return fail("v_min must be < v_max (S:272)");
   if (d.batch < 1) return fail("batch must be >= 1");
   if (d.precision != SQUINT_FP32 && d.precision != SQUINT_BF16) return fail("unknown precision");
   if (d.critic_hidden > 512 || d.actor_hidden > 512) return fail("hidden width > 512 not built");
-  if (d.n_atoms > 512 || d.latent > 512) return fail("n_atoms/latent > 512 not built");
+  if ((c51 && d.n_atoms > 512) || d.latent > 512) return fail("n_atoms/latent > 512 not built");
   if (2 * d.action_dim > 64) return fail("action_dim > 32 not built");
   if (d.img_c * d.img_h * d.img_w > 4096) return fail("stored image larger than 4096 bytes not built");
   (void)buf;
@@ -83,8 +85,8 @@ Layout make_layout(const squint_dims& d) {
   const int nq = d.latent + d.proprio_dim + d.action_dim, npi = d.latent + d.proprio_dim;
   auto critic_tail = [&](int g) {
     b.proj(g, "critic", F, d.latent);
-    b.mlp(g, "critic.q1", nq, d.critic_hidden, d.n_atoms);
-    b.mlp(g, "critic.q2", nq, d.critic_hidden, d.n_atoms);
+    b.mlp(g, "critic.q1", nq, d.critic_hidden, head_out(d));
+    b.mlp(g, "critic.q2", nq, d.critic_hidden, head_out(d));
   };
   b.add(SQUINT_GROUP_CRITIC, "enc.conv1.w", {C, d.img_c, 3, 3});
   b.add(SQUINT_GROUP_CRITIC, "enc.conv1.b", {C});

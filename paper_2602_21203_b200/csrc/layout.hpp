@@ -34,6 +34,8 @@ struct Layout {
 bool check_dims(const squint_dims& d, std::string* err);
 Layout make_layout(const squint_dims& d);
 
+// critic head width: n_atoms logits (C51) or one Q value (scalar MSE critic, f3)
+inline int head_out(const squint_dims& d) { return d.critic_kind == SQUINT_CRITIC_MSE ? 1 : d.n_atoms; }
 inline int conv1_out(const squint_dims& d) { return (d.img_h - 3) / 2 + 1; }
 inline int conv2_out(const squint_dims& d) { return conv1_out(d) - 2; }
 inline int flat_dim(const squint_dims& d) { return d.conv_ch * conv2_out(d) * conv2_out(d); }

@@ -106,7 +106,7 @@ ShadowPlan shadow_plan(WsPlan& P, const squint_dims& d, const Layout& L, int grp
 BfLay plan_bf(const squint_dims& d, const Layout& L) {
   WsPlan P;
   BfLay w;
-  const int B = d.batch, F = flat_dim(d), Lt = d.latent, Hc = d.critic_hidden, Ha = d.actor_hidden, N = d.n_atoms,
+  const int B = d.batch, F = flat_dim(d), Lt = d.latent, Hc = d.critic_hidden, Ha = d.actor_hidden, N = head_out(d),
             A = d.action_dim, C = d.conv_ch, P1 = conv1_out(d) * conv1_out(d);
   const int nq = Lt + d.proprio_dim + A, npi = Lt + d.proprio_dim;
   const size_t f = sizeof(float);
@@ -417,7 +417,7 @@ squint_status early_fwd(const Ctx& c, const BfLay& w_in, const squint_hparams& h
   const BfLay w = with_parity(w_in, par);
   const squint_dims& d = c.d;
   const Layout& L = c.L;
-  const int B = d.batch, Lt = d.latent, Hc = d.critic_hidden, N = d.n_atoms, A = d.action_dim, P = d.proprio_dim,
+  const int B = d.batch, Lt = d.latent, Hc = d.critic_hidden, N = head_out(d), A = d.action_dim, P = d.proprio_dim,
             C = d.conv_ch;
   const int nq = Lt + P + A;
   const float le = hp.ln_eps;
@@ -499,7 +499,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   const squint_dims& d = c.d;
   const Layout& L = c.L;
   cudaStream_t s = c.s;
-  const int B = d.batch, F = flat_dim(d), Lt = d.latent, Hc = d.critic_hidden, Ha = d.actor_hidden, N = d.n_atoms,
+  const int B = d.batch, F = flat_dim(d), Lt = d.latent, Hc = d.critic_hidden, Ha = d.actor_hidden, N = head_out(d),
             A = d.action_dim, P = d.proprio_dim, C = d.conv_ch;
   const int nq = Lt + P + A, npi = Lt + P;
   const int P2 = conv2_out(d) * conv2_out(d);
@@ -719,6 +719,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     t.v_max = d.v_max;
     t.gamma = hp.gamma;
     t.cdq = hp.target_mode == SQUINT_TARGET_CDQ;
+    t.mse = d.critic_kind == SQUINT_CRITIC_MSE;
     t.scale = inv_btotal;
     t.tlogits = c.F(w.tlogits);
     t.logits = c.F(w.logits);
@@ -925,7 +926,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   // k_actor_q -- off by default: the cross-CTA softmax exchange waits for the cluster's slowest
   // CTA and measured ~2 us slower per update than the separate kernel
   static const bool fuse_env = getenv("SQUINT_FUSE_Q") != nullptr;
-  const bool fuse_q = fuse_env && c.chain && comm == nullptr;
+  const bool fuse_q = fuse_env && c.chain && comm == nullptr && d.critic_kind == SQUINT_CRITIC_C51;
   {
     PhaseScope ps(12, rep, s);
     const Lin cproj1 = proj(c, w.sh[0], crit, gC, "critic");  // same buffers, now theta+
@@ -985,6 +986,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     }
     ActorQArgs q;
     memset(&q, 0, sizeof(q));
+    q.mse = d.critic_kind == SQUINT_CRITIC_MSE;
     q.B = B;
     q.N = N;
     q.v_min = d.v_min;
@@ -1164,7 +1166,7 @@ bool bf16_region(const squint_dims& d, int region, size_t* offset, size_t* bytes
   switch (region) {
     case 0: *offset = w.grad_critic; *bytes = L.gsize[0] * f; break;
     case 1: *offset = w.grad_actor; *bytes = L.gsize[1] * f; break;
-    case 2: *offset = w.m; *bytes = B * d.n_atoms * f; break;
+    case 2: *offset = w.m; *bytes = B * head_out(d) * f; break;
     case 3: *offset = w.Xh.off; *bytes = (size_t)w.Xh.rows * w.Xh.ld * 2; break;
     case 4: *offset = w.logp_cur; *bytes = B * f; break;
     case 5: *offset = w.logp_next; *bytes = B * f; break;
@@ -1177,7 +1179,7 @@ bool bf16_region(const squint_dims& d, int region, size_t* offset, size_t* bytes
 
 squint_status bf16_check(const squint_dims& d) {
   if (d.action_dim > 16) return set_error(SQUINT_EUNSUPPORTED, "bf16 path: action_dim > 16 not built");
-  if (d.critic_hidden > 512 || d.actor_hidden > 512 || d.n_atoms > 256 || d.latent > 256)
+  if (d.critic_hidden > 512 || d.actor_hidden > 512 || head_out(d) > 256 || d.latent > 256)
     return set_error(SQUINT_EUNSUPPORTED, "bf16 path: layer width not built");
   return SQUINT_OK;
 }

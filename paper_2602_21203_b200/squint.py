@@ -29,7 +29,11 @@ class Dims(C.Structure):
     _fields_ = [("img_c", C.c_int), ("img_h", C.c_int), ("img_w", C.c_int), ("pad", C.c_int), ("conv_ch", C.c_int),
                 ("latent", C.c_int), ("proprio_dim", C.c_int), ("action_dim", C.c_int),
                 ("critic_hidden", C.c_int), ("actor_hidden", C.c_int), ("n_atoms", C.c_int),
-                ("v_min", C.c_float), ("v_max", C.c_float), ("batch", C.c_int), ("precision", C.c_int)]
+                ("v_min", C.c_float), ("v_max", C.c_float), ("batch", C.c_int), ("precision", C.c_int),
+                ("critic_kind", C.c_int)]
+
+
+CRITIC_C51, CRITIC_MSE = 0, 1
 
 
 class HParams(C.Structure):
@@ -225,7 +229,7 @@ def _stream(stream=None):
 def make_dims(d: dict, precision=FP32) -> Dims:
     return Dims(d["img_c"], d["img_h"], d["img_w"], d["pad"], d["conv_ch"], d["latent"], d["proprio_dim"],
                 d["action_dim"], d["critic_hidden"], d["actor_hidden"], d["n_atoms"], d["v_min"], d["v_max"],
-                d["batch"], precision)
+                d["batch"], precision, d.get("critic_kind", CRITIC_C51))
 
 
 def make_hparams(h: dict) -> HParams:

@@ -33,9 +33,9 @@ def test_version():
     assert b"sm_100a" in S.LIB.squint_version()
 
 
-@pytest.mark.parametrize("cfg", ["c0", "c2", "c3"])
-def test_layout_matches_oracle_specs(cfg):
-    d = SI.dims_of(cfg)
+@pytest.mark.parametrize("cfg,kind", [("c0", 0), ("c2", 0), ("c3", 0), ("c0", 1), ("c2", 1)])
+def test_layout_matches_oracle_specs(cfg, kind):
+    d = SI.dims_of(cfg, critic_kind=kind)
     lay, gs = P.param_layout(P.make_dims(d))
     specs = O.param_specs(O.Dims(**d))
     gmap = {"critic": S.GROUP_CRITIC, "actor": S.GROUP_ACTOR, "alpha": S.GROUP_ALPHA, "target": S.GROUP_TARGET}
@@ -78,11 +78,13 @@ def _status(fn, *a):
 
 def test_invalid_dims_rejected():
     d = SI.dims_of("c0")
-    for k, v in [("n_atoms", 1), ("batch", 0), ("v_min", 20.0)]:
+    for k, v in [("n_atoms", 1), ("batch", 0), ("v_min", 20.0), ("critic_kind", 2)]:
         bad = dict(d, **{k: v})
         with pytest.raises(S.SquintError) as e:
             P.param_layout(P.make_dims(bad))
         assert e.value.status == 1
+    # the scalar critic ignores the atom support (f3)
+    P.param_layout(P.make_dims(dict(d, critic_kind=1, n_atoms=1, v_min=3.0, v_max=-3.0)))
 
 
 def test_insert_shape_errors_before_launch():

@@ -237,6 +237,17 @@ def test_update_c0_cdq_fp32(utd):
     _check_update(pr, L, met, st_ref, met_ref, trace)
 
 
+@pytest.mark.parametrize("mode,utd,batch", [(0, 2, 32), (1, 2, 32), (0, 1, 37)])
+def test_update_c0_mse_fp32(mode, utd, batch):
+    """f3: scalar MSE critic (Eqs. 1-2, Algorithm 1), average or CDQ-min target, fp32 bars."""
+    pr = Problem("c0", utd=utd, seed=6 + mode, batch=batch, critic_kind=1, hp_over={"target_mode": mode})
+    L = pr.gpu_setup()
+    met = pr.gpu_update(L)
+    trace = []
+    st_ref, met_ref = pr.oracle_update(trace)
+    _check_update(pr, L, met, st_ref, met_ref, trace)
+
+
 def test_update_deterministic_bitwise():
     pr = Problem("c0", utd=2, seed=7)
     outs = []
@@ -389,6 +400,11 @@ def test_update_ragged_batch_bf16(batch):
 
 def test_update_c2_cdq_bf16():
     _bf16_case("c2", seed=5, utd=2, capacity=4096, hp_over={"target_mode": 1})
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_update_c2_mse_bf16(mode):
+    _bf16_case("c2", seed=8, utd=2, capacity=4096, critic_kind=1, hp_over={"target_mode": mode})
 
 
 def test_update_c3_shapes_bf16():
