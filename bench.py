@@ -56,12 +56,21 @@ def blas_threads():
 # ---------------------------------------------------------------------------------------
 # CPU oracle sample (cpu_baseline leg and --impl reference)
 # ---------------------------------------------------------------------------------------
-def oracle_sample(seed=0, n_frames=N_ENV // UTD):
+def variant(args):
+    """(dims, hparams, label) of the workload: c2, or one of its f3/f4 variants."""
+    d = SI.dims_of(CFG, critic_kind=1 if args.critic == "mse" else 0)
+    hp = SI.hp_of(CFG, target_mode=1 if args.target == "cdq" else 0)
+    parts = ([] if args.critic == "c51" else ["scalar MSE critic"]) + ([] if args.target == "avg" else ["CDQ-min target"]) \
+        + ([] if args.insert == "chw" else [{"hwc": "HWC frames", "jitter": "colour jitter",
+                                             "hwc-jitter": "HWC frames + colour jitter"}[args.insert]])
+    return d, hp, ("; variant: " + ", ".join(parts)) if parts else ""
+
+
+def oracle_sample(args, seed=0, n_frames=N_ENV // UTD):
     """One update's share of a step on the CPU oracle: act + insert on n_frames frames and
     one c2 update (B = 512) on rows gathered from a seeded replay sample."""
     import oracle as O
-    d = SI.dims_of(CFG)
-    hp = SI.hp_of(CFG)
+    d, hp, _ = variant(args)
     D, H = O.Dims(**d), O.HParams(**hp)
     specs = O.param_specs(D)
     vals = SI.make_params(specs, seed=1)
@@ -77,7 +86,10 @@ def oracle_sample(seed=0, n_frames=N_ENV // UTD):
     ae = np.random.default_rng(seed).standard_normal((n_frames, d["action_dim"])).astype(np.float32)
     t0 = time.perf_counter()
     O.act(D, H, st["critic"], st["actor"], frames, prop, ae)
-    O.area_downsample(nxt, 8)
+    hwc = args.insert.startswith("hwc")
+    jit = SI.make_jitter(n_frames, seed=seed) if args.insert.endswith("jitter") else None
+    O.insert_ex(np.ascontiguousarray(nxt.transpose(0, 2, 3, 1)) if hwc else nxt, 8, np.arange(n_frames),
+                np.zeros((n_frames, 3, 16, 16), np.uint8), hwc=hwc, jitter=jit)
     O.update(D, H, R, idx, sh, eps, st)
     return time.perf_counter() - t0
 
@@ -87,8 +99,8 @@ def run_reference(args):
     if rank != 0:
         return
     for w in range(args.warmup):
-        oracle_sample(seed=w)
-    ts = [oracle_sample(seed=100 + k) for k in range(args.steps)]
+        oracle_sample(args, seed=w)
+    ts = [oracle_sample(args, seed=100 + k) for k in range(args.steps)]
     tot = sum(ts)
     value = args.steps / tot  # one update per sample
     cores = blas_threads()
@@ -96,7 +108,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "c2 update share of an Algorithm-1 step (CPU oracle)", "global_batch": 512,
+            "config": {"workload": "c2 update share of an Algorithm-1 step (CPU oracle)" + variant(args)[2], "global_batch": 512,
                        "utd": 1, "n_env_frames": N_ENV // UTD},
             "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -161,8 +173,7 @@ def run_gpu(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     precision = {"fp32": P.FP32, "bf16": P.BF16}[args.precision]
-    d = SI.dims_of(CFG)
-    hp = SI.hp_of(CFG)
+    d, hp, vlabel = variant(args)
     B, A = d["batch"], d["action_dim"]
     cap = SI.CONFIGS[CFG]["capacity"]
     K, W = args.steps, args.warmup
@@ -207,7 +218,11 @@ def run_gpu(args):
     # writing it on into that transition's obs row.  --act-full: the round-1 step instead (act
     # squints a second frame batch itself; the insert writes next_obs only).
     NPOOL = 4
+    hwc = args.insert.startswith("hwc")
     pools = [torch.as_tensor(SI.make_frames(N_ENV, 128, seed=20 + p)).to(dev) for p in range(NPOOL)]
+    if hwc:  # what renderers emit (f4)
+        pools = [x.permute(0, 2, 3, 1).contiguous() for x in pools]
+    jit = torch.as_tensor(SI.make_jitter(N_ENV)).to(dev) if args.insert.endswith("jitter") else None
     act_pool = [torch.as_tensor(SI.make_frames(N_ENV, 128, seed=10 + p)).to(dev) for p in range(NPOOL)] \
         if args.act_full else None
     stage = [torch.empty((N_ENV, 3, 16, 16), dtype=torch.uint8, device=dev) for _ in range(2)]
@@ -222,8 +237,16 @@ def run_gpu(args):
     act_ws = torch.zeros(P.act_workspace_bytes(L.dims, N_ENV), dtype=torch.uint8, device=dev)
     obs_ring = R["obs"]
     next_ring = R["next_obs"]
+    def insert_new(frames, slots, stage_dst, stream=None):
+        # o_{t+1} -> next_obs[slots] and the next act's rows, one squint (f2; f4 variants)
+        if args.insert == "chw":
+            P.squint_insert2(frames, 8, slots, next_ring, stage_slots, stage_dst, stream=stream)
+        else:
+            P.squint_insert_ex(frames, 8, slots, next_ring, hwc=hwc, jitter=jit, slots2=stage_slots, ring2=stage_dst,
+                               stream=stream)
+
     # o_0, squinted
-    P.squint_insert(pools[NPOOL - 1], 8, stage_slots, stage[0])
+    P.squint_insert_ex(pools[NPOOL - 1], 8, stage_slots, stage[0], hwc=hwc, jitter=jit)
 
     side = torch.cuda.Stream(device=dev)
     ins_fork, ins_done = torch.cuda.Event(), torch.cuda.Event()
@@ -239,7 +262,7 @@ def run_gpu(args):
             if args.act_full:
                 P.squint_insert(nx, 8, slots_s, next_ring, stream=side)
             else:
-                P.squint_insert2(nx, 8, slots_s, next_ring, stage_slots, stage[1 - par], stream=side)
+                insert_new(nx, slots_s, stage[1 - par], stream=side)
             ins_done.record(side)
         fr = act_pool[j % NPOOL] if args.act_full else stage[par]
         P.squint_act(L.dims, L.hp, L.actor, L.critic, fr, prop_s, aeps_s, act_out, logp_out, act_ws,
@@ -400,14 +423,14 @@ def run_gpu(args):
             if args.act_full:
                 P.squint_insert(nxt, 8, slots, next_ring)
             else:
-                P.squint_insert2(nxt, 8, slots, next_ring, stage_slots, stage[(k + 1) % 2])
+                insert_new(nxt, slots, stage[(k + 1) % 2])
                 freed[k % 2].record(main)
             h_out[2].copy_(metrics, non_blocking=True)
             # the next step's small inputs overwrite the staging buffers once this step used them
             ins.wait_stream(main)
 
         dbuf[1].copy_(h_fr[NPOOL - 1], non_blocking=True)  # o_0 (--act-full acts on it)
-        P.squint_insert(dbuf[1], 8, stage_slots, stage[0])  # o_0, squinted
+        P.squint_insert_ex(dbuf[1], 8, stage_slots, stage[0], hwc=hwc, jitter=jit)  # o_0, squinted
         for e in freed:
             e.record(main)
         for w in range(W):
@@ -471,7 +494,7 @@ def run_gpu(args):
     kernels_us = {k: round(v["us"], 2) for k, v in sorted(kern.items(), key=lambda kv: -kv[1]["us"])}
     cpu = None
     if world == 1 and not args.no_cpu:
-        ts = [oracle_sample(seed=s) for s in range(args.cpu_samples)]
+        ts = [oracle_sample(args, seed=s) for s in range(args.cpu_samples)]
         cpu = {"value": len(ts) / sum(ts), "unit": "updates/s", "cores": blas_threads(), "kind": "oracle",
                "sample": f"{len(ts)} x (oracle act+insert on {N_ENV // UTD} frames + 1 update at B=512), "
                          f"{sum(ts):.1f} s float64 NumPy"}
@@ -480,7 +503,7 @@ def run_gpu(args):
             "vs_baseline": None, "dtype": {P.FP32: "f32", P.BF16: "bf16"}[precision], "data": "synthetic",
             "config": {"workload": "c2: Algorithm-1 step = insert2(1024 new 128x128 frames) + act(1024 envs) + "
                                    "4 updates at B=512 per rank, 101 atoms, 1M ring"
-                                   + (" (act squints its own frames)" if args.act_full else ""), "global_batch": B * world, "utd": UTD,
+                                   + (" (act squints its own frames)" if args.act_full else "") + vlabel, "global_batch": B * world, "utd": UTD,
                        "n_env": N_ENV, "parallelism": f"dp{world}", "l2": "ring 1.66 GB + rotating frame pools (4 x 50 MB) > L2",
                        "graph": use_graph},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
@@ -503,7 +526,13 @@ def main():
     ap.add_argument("--cpu-samples", type=int, default=3)
     ap.add_argument("--no-timeline", action="store_true")
     ap.add_argument("--act-full", action="store_true")  # round-1 step: act squints its own frame batch
+    # f3 / f4 variants (not the headline workload): critic head, target rule, insert input
+    ap.add_argument("--critic", default="c51", choices=["c51", "mse"])
+    ap.add_argument("--target", default="avg", choices=["avg", "cdq"])
+    ap.add_argument("--insert", default="chw", choices=["chw", "hwc", "jitter", "hwc-jitter"])
     args = ap.parse_args()
+    if args.act_full and args.insert != "chw":
+        ap.error("--act-full acts on CHW frames: use it with --insert chw")
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
     if args.impl == "reference":
