@@ -60,7 +60,8 @@ def dp_update_one(d, hp, R, idx, shift, eps, st, b_global):
     alpha0 = math.exp(st["log_alpha"])
     scale = 1.0 / b_global
     hn, _ = O.encoder_fwd(st["critic"], O.normalize_pixels(On))
-    m, _ = O.target_distribution(d, hp, st["target"], st["actor"], hn, sn, r, done, eps[0], alpha0)
+    tgt = O.target_value if d.critic_kind == 1 else O.target_distribution  # f3 variants
+    m, _ = tgt(d, hp, st["target"], st["actor"], hn, sn, r, done, eps[0], alpha0)
     LQ, gc, h = O.critic_loss_and_grads(d, hp, st["critic"], Ob, s, a, m, scale)
     # pre-step phi on sg(h): the current-state sample does not depend on the critic step (Q18)
     at, logp, caches = O.actor_forward(d, hp, st["actor"], h, s, eps[1])
@@ -88,9 +89,9 @@ def dp_update_one(d, hp, R, idx, shift, eps, st, b_global):
     return st
 
 
-def _problem(b_local, utd):
-    dims = SI.dims_of("c0", batch=b_local)
-    hp = SI.hp_of("c0")
+def _problem(b_local, utd, kind=0, mode=0):
+    dims = SI.dims_of("c0", batch=b_local, critic_kind=kind)
+    hp = SI.hp_of("c0", target_mode=mode)
     hp["target_entropy"] = -float(dims["action_dim"])
     d, h = O.Dims(**dims), O.HParams(**hp)
     specs = O.param_specs(d)
@@ -124,11 +125,11 @@ def _state_vec(st):
     return np.concatenate(parts)
 
 
-def _worker(rank, port, b_local, utd, out_dir):
+def _worker(rank, port, b_local, utd, out_dir, kind=0, mode=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
-    d, h, dims, R, st, idx, sh, eps = _problem(b_local, utd)
+    d, h, dims, R, st, idx, sh, eps = _problem(b_local, utd, kind, mode)
     for j in range(utd):
         st = dp_update_one(d, h, R, idx[rank][j], sh[rank][j], eps[rank][j], st, b_local * WORLD)
     np.save(os.path.join(out_dir, f"state{rank}.npy"), _state_vec(st))
@@ -144,14 +145,15 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("b_local,utd", [(3, 1), (4, 2)])
-def test_dp_gloo_world2_matches_global_batch(tmp_path, b_local, utd):
-    mp.spawn(_worker, args=(_free_port(), b_local, utd, str(tmp_path)), nprocs=WORLD, join=True)
+@pytest.mark.parametrize("b_local,utd,kind,mode", [(3, 1, 0, 0), (4, 2, 0, 0), (3, 1, 0, 1), (3, 2, 1, 0), (3, 1, 1, 1)])
+def test_dp_gloo_world2_matches_global_batch(tmp_path, b_local, utd, kind, mode):
+    """kind 1: scalar MSE critic, mode 1: CDQ-min target (f3) -- the same exchange protocol."""
+    mp.spawn(_worker, args=(_free_port(), b_local, utd, str(tmp_path), kind, mode), nprocs=WORLD, join=True)
     s0 = np.load(tmp_path / "state0.npy")
     s1 = np.load(tmp_path / "state1.npy")
     assert np.array_equal(s0, s1), "data-parallel replicas diverged"
     # single process, global batch = rank-major concatenation of the shards (Q33)
-    d, h, dims, R, st, idx, sh, eps = _problem(b_local, utd)
+    d, h, dims, R, st, idx, sh, eps = _problem(b_local, utd, kind, mode)
     dg = O.Dims(**dict(dims, batch=b_local * WORLD))
     gidx = np.concatenate(idx, axis=1)
     gsh = np.concatenate(sh, axis=1)
