@@ -388,39 +388,44 @@ def run_gpu(args):
         for t, off in zip(srcs, offs):
             nb = t[0].numel() * t.element_size()
             h_pack[:, off:off + nb] = t.reshape(T, -1).contiguous().cpu().view(torch.uint8)
-        d_pack = torch.zeros(o, dtype=torch.uint8, device=dev)
-        stage_in = [d_pack[off:off + t[0].numel() * t.element_size()].view(t.dtype).view(t[0].shape)
-                    for t, off in zip(srcs, offs)]
+        # two device staging sets: step k+1's inputs are staged during step k
+        d_pack = [torch.zeros(o, dtype=torch.uint8, device=dev) for _ in range(2)]
+        stage_in = [[dp[off:off + t[0].numel() * t.element_size()].view(t.dtype).view(t[0].shape)
+                     for t, off in zip(srcs, offs)] for dp in d_pack]
         h_out = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (act_out, logp_out, metrics)]
         dbuf = [pools[0].clone(), pools[1].clone()]
-        # (one staging set: double-buffering the small inputs lets the next upload start early and
-        # share the link with this one, which delays this step's insert -- measured slower)
         main = torch.cuda.current_stream()
+        # the small inputs travel through the SMs (squint_stage_pinned: a kernel reading pinned
+        # host memory), not a copy engine, so they never queue behind a frame upload; the read
+        # shares the link with the upload (~0.2 ms for 100 KB), so it runs one step ahead on a
+        # stream of its own
+        stg = torch.cuda.Stream(device=dev)
+        staged = [torch.cuda.Event(), torch.cuda.Event()]  # d_pack[i] holds its step's inputs
+        used = [torch.cuda.Event(), torch.cuda.Event()]    # d_pack[i] read by its step
+
+        def stage_inputs(k):
+            if k < T:
+                stg.wait_event(used[k % 2])
+                P.squint_stage_pinned(d_pack[k % 2], h_pack[k], stream=stg)
+                staged[k % 2].record(stg)
         # the frame upload in two halves on two copy streams (one DMA stream does not saturate
-        # the link: 47 vs 54 GB/s measured), the small per-step inputs on a stream of their own
+        # the link: 47 vs 54 GB/s measured)
         cps = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
-        ins = torch.cuda.Stream(device=dev)
         freed = [torch.cuda.Event(), torch.cuda.Event()]  # dbuf[i] read by its last consumer
         copied = [torch.cuda.Event(), torch.cuda.Event()]
-        inputs_in = torch.cuda.Event()
         half = h_fr[0].shape[0] // 2
 
         def e2e_step(k):
             nxt = dbuf[k % 2]
-            idx, sh, eps, aeps, prop, slots = stage_in
-            with torch.cuda.stream(ins):
-                d_pack.copy_(h_pack[k], non_blocking=True)
-                inputs_in.record(ins)
-            # o_{t+1} -> dbuf[k % 2] once step k-2's insert (or, --act-full, step k-1's act) read it,
-            # queued behind the small inputs (the copy engine serves them in order: a 50 MB upload
-            # issued first would hold the act's inputs back by a millisecond)
+            idx, sh, eps, aeps, prop, slots = stage_in[k % 2]
+            stage_inputs(k + 1)
+            main.wait_event(staged[k % 2])
+            # o_{t+1} -> dbuf[k % 2] once step k-2's insert (or, --act-full, step k-1's act) read it
             for c, sl in enumerate((slice(0, half), slice(half, None))):
                 cps[c].wait_event(freed[k % 2])
-                cps[c].wait_event(inputs_in)
                 with torch.cuda.stream(cps[c]):
                     nxt[sl].copy_(h_fr[k % NPOOL][sl], non_blocking=True)
                     copied[c].record(cps[c])
-            main.wait_event(inputs_in)
             fr = dbuf[(k + 1) % 2] if args.act_full else stage[k % 2]
             P.squint_act(L.dims, L.hp, L.actor, L.critic, fr, prop, aeps, act_out, logp_out, act_ws,
                          ring=obs_ring, slots=slots)
@@ -436,14 +441,14 @@ def run_gpu(args):
             else:
                 insert_new(nxt, slots, stage[(k + 1) % 2])
                 freed[k % 2].record(main)
+            used[k % 2].record(main)
             h_out[2].copy_(metrics, non_blocking=True)
-            # the next step's small inputs overwrite the staging buffers once this step used them
-            ins.wait_stream(main)
 
         dbuf[1].copy_(h_fr[NPOOL - 1], non_blocking=True)  # o_0 (--act-full acts on it)
         P.squint_insert_ex(dbuf[1], 8, stage_slots, stage[0], hwc=hwc, jitter=jit)  # o_0, squinted
-        for e in freed:
+        for e in freed + used:
             e.record(main)
+        stage_inputs(0)
         for w in range(W):
             e2e_step(w)
         torch.cuda.synchronize()

@@ -244,6 +244,15 @@ SQUINT_API squint_status squint_update(const squint_dims* dims, const squint_hpa
 SQUINT_API squint_status squint_soft_update(float* target, const float* online, int64_t n, float tau,
                                  squint_stream_t stream);
 
+/* ---- runtime: stage a step's small inputs from pinned host memory by a kernel ----------
+ * dst (device) <- src (page-locked host memory, cudaHostAlloc / cudaHostRegister), `bytes`
+ * bytes, read over PCIe by the SMs (16-byte loads when both pointers are 16-byte aligned)
+ * rather than by a copy engine: in an environment loop the per-step indices / noise / proprio
+ * (~100 KB) then do not queue behind the next 50 MB frame upload on the DMA engine.
+ * Asynchronous on `stream`; src must stay valid until the kernel has run.
+ * Errors: EINVAL (NULL with bytes > 0, src not page-locked host memory). */
+SQUINT_API squint_status squint_stage_pinned(void* dst, const void* src, size_t bytes, squint_stream_t stream);
+
 /* Self-test of the bf16 tensor-core GEMM engine (gemm.cu), used by the GPU tests:
  * out[m][n] = sum_{k<K} A(m, k) B(n, k), fp32 [M][N] row-major (device), where A and B are
  * bf16 row-major device matrices (rows x cols, ld elements per row) read K-major

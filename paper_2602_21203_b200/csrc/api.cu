@@ -793,6 +793,18 @@ squint_status squint_insert(const uint8_t* frames, int64_t n, int c, int h, int 
   return squint_insert2(frames, n, c, h, w, factor, slots, ring, nullptr, nullptr, capacity, stream);
 }
 
+squint_status squint_stage_pinned(void* dst, const void* src, size_t bytes, squint_stream_t stream) {
+  if (bytes == 0) return SQUINT_OK;
+  if (!dst || !src) return fail(SQUINT_EINVAL, "NULL pointer");
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, src) != cudaSuccess || at.type != cudaMemoryTypeHost || !at.devicePointer) {
+    cudaGetLastError();
+    return fail(SQUINT_EINVAL, "src is not page-locked host memory");
+  }
+  SQ_CK(launch_stage_pinned(dst, at.devicePointer, bytes, (cudaStream_t)stream));
+  return SQUINT_OK;
+}
+
 squint_status squint_soft_update(float* target, const float* online, int64_t n, float tau, squint_stream_t stream) {
   if (n < 0) return fail(SQUINT_EINVAL, "n must be >= 0");
   if (!(tau >= 0.f && tau <= 1.f)) return fail(SQUINT_EINVAL, "tau must be in [0, 1]");

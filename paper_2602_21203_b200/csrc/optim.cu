@@ -381,6 +381,31 @@ int launch_adam_shadow(float* p, const float* g, float* m, float* v, int64_t n, 
   return (int)cudaGetLastError();
 }
 
+__global__ void __launch_bounds__(256) k_stage_pinned(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                                                      size_t bytes) {
+  grid_wait();
+  grid_trigger();
+  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    const size_t n16 = bytes / 16;
+    for (size_t i = tid; i < n16; i += nt)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    for (size_t i = n16 * 16 + tid; i < bytes; i += nt) dst[i] = src[i];
+  } else {
+    for (size_t i = tid; i < bytes; i += nt) dst[i] = src[i];
+  }
+}
+
+int launch_stage_pinned(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  size_t blocks = (bytes / 16 + 255) / 256;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 148) blocks = 148;
+  note_launch(s, "k_stage_pinned", 0, (double)bytes);
+  launch_pdl(k_stage_pinned, dim3((unsigned)blocks), dim3(256), 0, s, reinterpret_cast<uint8_t*>(dst),
+             reinterpret_cast<const uint8_t*>(src), bytes);
+  return (int)cudaGetLastError();
+}
+
 int launch_polyak_shadow(float* target, const float* online, int64_t n, float tau, const ShadowTable* t,
                          cudaStream_t s) {
   if (n == 0) return 0;

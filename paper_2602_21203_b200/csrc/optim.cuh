@@ -74,6 +74,8 @@ int launch_adam_shadow(float* p, const float* g, float* m, float* v, int64_t n, 
                        float eps, const float* c1, const float* c2, float* sumsq_part, const ShadowTable* t,
                        cudaStream_t s, int64_t base = 0, int nblocks = kAdamBlocks, int grad_perm = 0);
 // Polyak over a 16-byte aligned buffer (n % 4 == 0) that also refreshes the target shadow.
+// dst (device) <- src (device-mapped pinned host memory), read by the SMs over PCIe
+int launch_stage_pinned(void* dst, const void* src, size_t bytes, cudaStream_t s);
 int launch_polyak_shadow(float* target, const float* online, int64_t n, float tau, const ShadowTable* t,
                          cudaStream_t s);
 

@@ -85,6 +85,7 @@ def _load():
         "squint_update": (st, [C.POINTER(Dims), C.POINTER(HParams), C.POINTER(Replay), vp, vp, vp, i32,
                                C.POINTER(State), vp, vp, sz, vp, vp]),
         "squint_soft_update": (st, [vp, vp, i64, f32, vp]),
+        "squint_stage_pinned": (st, [vp, vp, sz, vp]),
         "squint_selftest_gemm": (st, [vp, i32, i32, i32, i32, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp]),
         "squint_launch_count": (C.c_long, []),
         "squint_set_phase_events": (st, [C.POINTER(vp), i32, i32]),
@@ -104,7 +105,7 @@ def _load():
 LIB = _load()
 EXPORTED = ["squint_last_error", "squint_version", "squint_param_layout", "squint_workspace_bytes",
             "squint_workspace_region", "squint_act_workspace_bytes", "squint_comm_unique_id", "squint_comm_init",
-            "squint_comm_destroy", "squint_insert", "squint_insert2", "squint_insert_ex", "squint_act", "squint_update", "squint_soft_update",
+            "squint_comm_destroy", "squint_insert", "squint_insert2", "squint_insert_ex", "squint_act", "squint_update", "squint_soft_update", "squint_stage_pinned",
             "squint_launch_count", "squint_set_phase_events", "squint_phase_name", "squint_selftest_gemm",
             "squint_set_launch_events", "squint_record_launch_event", "squint_launch_info",
             "squint_set_option"]
@@ -292,6 +293,15 @@ def squint_insert_ex(frames: torch.Tensor, factor: int, slots: torch.Tensor, rin
     cap = ring.shape[0] if ring2 is None else min(ring.shape[0], ring2.shape[0])
     _check(LIB.squint_insert_ex(_ptr(frames), n, c, h, w, factor, LAYOUT_HWC if hwc else LAYOUT_CHW, _ptr(jitter),
                                 _ptr(slots), _ptr(ring), _ptr(slots2), _ptr(ring2), cap, _stream(stream)))
+
+
+def squint_stage_pinned(dst: torch.Tensor, src: torch.Tensor, stream=None):
+    """dst (device) <- src (pinned host), read by a kernel (squint.h)."""
+    if not src.is_pinned():
+        raise ValueError("squint_stage_pinned: src must be pinned host memory")
+    nb = src.numel() * src.element_size()
+    assert dst.numel() * dst.element_size() >= nb
+    _check(LIB.squint_stage_pinned(_ptr(dst), _ptr(src), nb, _stream(stream)))
 
 
 def squint_soft_update(target: torch.Tensor, online: torch.Tensor, tau: float, stream=None):

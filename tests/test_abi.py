@@ -117,6 +117,12 @@ def test_insert_ex_arg_errors():
     assert f(null, 0, 3, 128, 128, 8, 1, one, null, null, null, null, 10, null) == 0      # n == 0 no-op
 
 
+def test_stage_pinned_rejects_pageable_host_memory():
+    buf = (C.c_uint8 * 64)()
+    assert S.LIB.squint_stage_pinned(C.c_void_p(16), C.cast(buf, C.c_void_p), 64, None) == 1
+    assert S.LIB.squint_stage_pinned(None, None, 0, None) == 0
+
+
 def test_soft_update_arg_errors():
     null = C.c_void_p(0)
     assert S.LIB.squint_soft_update(null, null, 10, 1.5, null) == 1

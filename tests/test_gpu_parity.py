@@ -116,6 +116,16 @@ def test_insert_ex_identity_jitter_equals_plain_insert():
     assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("nbytes,off", [(1, 0), (100_000, 0), (4099, 3), (64, 16)])
+def test_stage_pinned_copies_bytes(nbytes, off):
+    src = torch.randint(0, 256, (nbytes + off,), dtype=torch.uint8).pin_memory()
+    dst = torch.full((nbytes + 32,), 7, dtype=torch.uint8, device=DEV)
+    P.squint.squint_stage_pinned(dst[off:off + nbytes], src[off:])
+    torch.cuda.synchronize()
+    assert torch.equal(dst[off:off + nbytes].cpu(), src[off:])
+    assert (dst[off + nbytes:].cpu() == 7).all() and (dst[:off].cpu() == 7).all()
+
+
 # ---- a14 soft update ------------------------------------------------------------------
 @pytest.mark.parametrize("n,tau", [(1, 0.005), (1000, 0.005), (4097, 0.5), (33, 0.0), (33, 1.0)])
 def test_soft_update(n, tau):
