@@ -141,13 +141,14 @@ def test_soft_update(n, tau):
 
 
 # ---- a16 act --------------------------------------------------------------------------
-@pytest.mark.parametrize("n,sample", [(1, True), (37, True), (64, False)])
-def test_act_fp32(n, sample):
+@pytest.mark.parametrize("n,sample,hw", [(1, True, 128), (37, True, 128), (64, False, 128), (37, True, 16)])
+def test_act_fp32(n, sample, hw):
+    """hw 16: frames already at the stored resolution (factor 1: insert2 / direct render)."""
     d = SI.dims_of("c0", batch=1)
     hp = SI.hp_of("c0")
     pr = Problem("c0", seed=5)
     L = pr.gpu_setup()
-    frames = SI.make_frames(n, 128, seed=n)
+    frames = SI.make_frames(n, hw, seed=n)
     prop = SI.make_proprio(n, 12, seed=n)
     eps = np.random.default_rng(n).standard_normal((n, 6)).astype(np.float32) if sample else None
     st = O.init_state(pr.specs, pr.vals)
