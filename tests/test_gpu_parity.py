@@ -291,6 +291,34 @@ def test_act_bf16(n):
     compare("logp bf16", lp.cpu().numpy(), lp_ref, 2e-2)
 
 
+def test_act_bf16_c4_full_size_sampled():
+    """BASELINE configs c4 at full size: act on 4096 rendered 3x128x128 frames in one call (the
+    launch configuration of the rollout), ring written for all rows; 96 sampled rows checked
+    against the oracle one by one (rows are independent), every ring row bit-exact."""
+    c = SI.CONFIGS["c4"]
+    n = c["n_frames"]
+    pr = Problem("c0", seed=5)
+    L = pr.gpu_setup(precision=P.BF16)
+    frames = SI.make_frames(n, c["frame_hw"], seed=44)
+    prop = SI.make_proprio(n, 12, seed=44)
+    eps = np.random.default_rng(44).standard_normal((n, 6)).astype(np.float32)
+    dims = P.make_dims(pr.dims, P.BF16)
+    ws = torch.zeros(P.act_workspace_bytes(dims, n), dtype=torch.uint8, device=DEV)
+    act = torch.zeros((n, 6), device=DEV)
+    lp = torch.zeros(n, device=DEV)
+    ring = torch.zeros((n + 100, 3, 16, 16), dtype=torch.uint8, device=DEV)
+    slots = torch.as_tensor(SI.make_slots(n, n + 100, seed=45)).to(DEV)
+    P.squint_act(dims, P.make_hparams(pr.hp), L.actor, L.critic, torch.as_tensor(frames).to(DEV),
+                 torch.as_tensor(prop).to(DEV), torch.as_tensor(eps).to(DEV), act, lp, ws, ring=ring, slots=slots)
+    torch.cuda.synchronize()
+    assert np.array_equal(ring[slots].cpu().numpy(), O.area_downsample(frames, 8))
+    rows = np.sort(np.random.default_rng(46).choice(n, 96, replace=False))
+    st = O.init_state(pr.specs, pr.vals)
+    a_ref, lp_ref, _ = O.act(pr.d, pr.h, st["critic"], st["actor"], frames[rows], prop[rows], eps[rows])
+    compare("action bf16 c4 sampled", act.cpu().numpy()[rows], a_ref, 2e-2)
+    compare("logp bf16 c4 sampled", lp.cpu().numpy()[rows], lp_ref, 2e-2)
+
+
 @pytest.mark.parametrize("n", [37, 1024])
 def test_act_bf16_presquinted_factor1(n):
     """f2: act on frames already squinted into a ring row (factor 1) -- parity with the oracle's
