@@ -426,6 +426,13 @@ def test_update_c2_full_batch_utd2_bf16():
     _bf16_case("c2", seed=3, utd=2, capacity=4096)
 
 
+def test_update_c2_bench_configuration_bf16():
+    """The configuration bench.py times, at full size: 1M-row replay ring, B = 512, UTD 4, one
+    squint_update call (cached CUDA graph, forked branch) -- against the oracle on the same
+    seeded ring."""
+    _bf16_case("c2", seed=9, utd=4, capacity=SI.CONFIGS["c2"]["capacity"])
+
+
 @pytest.mark.parametrize("seed", [2, 7])
 def test_update_c2_full_batch_bf16(seed):
     """BASELINE configs[2] shapes at the full batch 512 (101 atoms), as bench.py runs them."""
