@@ -62,7 +62,8 @@ def variant(args):
     hp = SI.hp_of(CFG, target_mode=1 if args.target == "cdq" else 0)
     parts = ([] if args.critic == "c51" else ["scalar MSE critic"]) + ([] if args.target == "avg" else ["CDQ-min target"]) \
         + ([] if args.insert == "chw" else [{"hwc": "HWC frames", "jitter": "colour jitter",
-                                             "hwc-jitter": "HWC frames + colour jitter"}[args.insert]])
+                                             "hwc-jitter": "HWC frames + colour jitter"}[args.insert]]) \
+        + (["replay capacity (P:189)"] if args.capacity else [])
     return d, hp, ("; variant: " + ", ".join(parts)) if parts else ""
 
 
@@ -175,7 +176,7 @@ def run_gpu(args):
     precision = {"fp32": P.FP32, "bf16": P.BF16}[args.precision]
     d, hp, vlabel = variant(args)
     B, A = d["batch"], d["action_dim"]
-    cap = SI.CONFIGS[CFG]["capacity"]
+    cap = args.capacity or SI.CONFIGS[CFG]["capacity"]
     K, W = args.steps, args.warmup
 
     L = P.Learner(d, hp, precision=precision, device=dev, utd=UTD)
@@ -518,9 +519,10 @@ def run_gpu(args):
             "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": {P.FP32: "f32", P.BF16: "bf16"}[precision], "data": "synthetic",
             "config": {"workload": "c2: Algorithm-1 step = insert2(1024 new 128x128 frames) + act(1024 envs) + "
-                                   "4 updates at B=512 per rank, 101 atoms, 1M ring"
+                                   f"4 updates at B=512 per rank, 101 atoms, {cap:,}-row ring"
                                    + (" (act squints its own frames)" if args.act_full else "") + vlabel, "global_batch": B * world, "utd": UTD,
-                       "n_env": N_ENV, "parallelism": f"dp{world}", "l2": "ring 1.66 GB + rotating frame pools (4 x 50 MB) > L2",
+                       "n_env": N_ENV, "parallelism": f"dp{world}", "capacity": cap,
+                       "l2": f"ring {cap * 1662 / 1e9:.2f} GB + rotating frame pools (4 x 50 MB) > L2",
                        "graph": use_graph},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": int(launches_per_step * K), "kernels_us_per_step": kernels_us}
@@ -546,6 +548,7 @@ def main():
     ap.add_argument("--critic", default="c51", choices=["c51", "mse"])
     ap.add_argument("--target", default="avg", choices=["avg", "cdq"])
     ap.add_argument("--insert", default="chw", choices=["chw", "hwc", "jitter", "hwc-jitter"])
+    ap.add_argument("--capacity", type=int, default=0)  # replay rows (0: configs' 1M; f3: 100K axis)
     args = ap.parse_args()
     if args.act_full and args.insert != "chw":
         ap.error("--act-full acts on CHW frames: use it with --insert chw")
