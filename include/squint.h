@@ -280,7 +280,11 @@ SQUINT_API int squint_set_launch_events(void** events, int n);
  * auxiliary stream (1, default) or inline on the caller's stream (0; a launch timeline then
  * brackets consecutive launches of one stream); key 2 = pipeline each update's critic-side
  * forward (encoder, critic/target projections, online heads) onto the previous update's branch
- * (0, default; needs key 1).  Errors: EINVAL for an unknown key. */
+ * (0, default; needs key 1); key 3 = validate the device-side preconditions before each call
+ * (0, default): sampled indices in [0, replay.size), insert / act slots in [0, capacity) and
+ * pairwise distinct -- a check kernel plus a stream synchronisation per call, returning
+ * SQUINT_EINVAL with a message instead of undefined behaviour (skipped inside a stream
+ * capture).  Errors: EINVAL for an unknown key. */
 SQUINT_API squint_status squint_set_option(int key, int value);
 /* Records the next timeline event on `stream` without a launch (closes the last interval). */
 SQUINT_API squint_status squint_record_launch_event(squint_stream_t stream);

@@ -2,6 +2,7 @@
 // workspace layout, and the launch sequence of one SAC update (Algorithm 1 L9-24).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -656,6 +657,39 @@ static bool check_hp(const squint_hparams& h, std::string* e) {
   return true;
 }
 
+// ---- option 3: device-side precondition checks (squint.h) ---------------------------------
+__device__ unsigned int g_check_bad;
+__global__ void k_check_range(const int64_t* __restrict__ v, int64_t n, int64_t hi) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (v[i] < 0 || v[i] >= hi) atomicOr(&g_check_bad, 1u);
+}
+__global__ void k_check_distinct(const int64_t* __restrict__ v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t j = i + 1; j < n; ++j)
+      if (v[j] == v[i]) atomicOr(&g_check_bad, 2u);
+}
+// Range check of v[0..n) against [0, hi) and (distinct) pairwise distinctness; synchronises s.
+static squint_status check_indices(const int64_t* v, int64_t n, int64_t hi, bool distinct, const char* what,
+                                   cudaStream_t s) {
+  if (!g_check_enabled || n <= 0 || !v) return SQUINT_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return SQUINT_OK;  // no synchronising check inside a capture
+  }
+  const unsigned int zero = 0;
+  SQ_CK(cudaMemcpyToSymbolAsync(g_check_bad, &zero, sizeof(zero), 0, cudaMemcpyHostToDevice, s));
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 1024);
+  k_check_range<<<blocks, 256, 0, s>>>(v, n, hi);
+  if (distinct) k_check_distinct<<<blocks, 256, 0, s>>>(v, n);
+  unsigned int bad = 0;
+  SQ_CK(cudaMemcpyFromSymbolAsync(&bad, g_check_bad, sizeof(bad), 0, cudaMemcpyDeviceToHost, s));
+  SQ_CK(cudaStreamSynchronize(s));
+  if (bad & 1u) return set_error(SQUINT_EINVAL, std::string(what) + ": index out of range (precondition check)");
+  if (bad & 2u) return set_error(SQUINT_EINVAL, std::string(what) + ": slots not distinct (precondition check)");
+  return SQUINT_OK;
+}
+
 }  // namespace sq
 
 using namespace sq;
@@ -760,6 +794,11 @@ squint_status squint_insert2(const uint8_t* frames, int64_t n, int c, int h, int
     return fail(SQUINT_EINVAL, "frames must be 16-byte aligned");
   if (factor == 8 && (w % 16) == 0 && ((h / 8) * (w / 8) % 2))
     return fail(SQUINT_EINVAL, "odd output row length not supported by the vector path");
+  {
+    squint_status r = check_indices(slots, n, capacity, true, "squint_insert slots", (cudaStream_t)stream);
+    if (r == SQUINT_OK) r = check_indices(slots2, n, capacity, true, "squint_insert2 slots2", (cudaStream_t)stream);
+    if (r != SQUINT_OK) return r;
+  }
   PhaseScope ps(0, 0, (cudaStream_t)stream);
   SQ_CK(launch_insert(frames, n, c, h, w, factor, slots, ring, (cudaStream_t)stream, slots2, ring2));
   return SQUINT_OK;
@@ -783,6 +822,11 @@ squint_status squint_insert_ex(const uint8_t* frames, int64_t n, int c, int h, i
   if (n > 0x7fffffff) return fail(SQUINT_EUNSUPPORTED, "n > 2^31 - 1");
   if (n == 0) return SQUINT_OK;
   if (!frames || !slots || !ring) return fail(SQUINT_EINVAL, "NULL pointer");
+  {
+    squint_status r = check_indices(slots, n, capacity, true, "squint_insert_ex slots", (cudaStream_t)stream);
+    if (r == SQUINT_OK) r = check_indices(slots2, n, capacity, true, "squint_insert_ex slots2", (cudaStream_t)stream);
+    if (r != SQUINT_OK) return r;
+  }
   PhaseScope ps(0, 0, (cudaStream_t)stream);
   SQ_CK(launch_insert_ex(frames, n, c, h, w, factor, layout, jitter, slots, ring, (cudaStream_t)stream, slots2, ring2));
   return SQUINT_OK;
@@ -831,6 +875,10 @@ squint_status squint_act(const squint_dims* dims, const squint_hparams* hp, cons
   if (n == 0) return SQUINT_OK;
   if (!actor_params || !critic_params || !frames || !proprio || !action_out || !workspace)
     return fail(SQUINT_EINVAL, "NULL pointer");
+  {
+    squint_status r = check_indices(slots, n, ring_capacity, true, "squint_act slots", (cudaStream_t)stream);
+    if (r != SQUINT_OK) return r;
+  }
   const int f = frame_h / dims->img_h;
   if (f == 8 && (frame_w % 16) == 0 && (reinterpret_cast<uintptr_t>(frames) & 15))
     return fail(SQUINT_EINVAL, "frames must be 16-byte aligned");
@@ -917,6 +965,11 @@ squint_status squint_update(const squint_dims* dims, const squint_hparams* hp, c
   if (!state->critic || !state->critic_target || !state->actor || !state->log_alpha || !state->m_critic ||
       !state->v_critic || !state->m_actor || !state->v_actor || !state->m_alpha || !state->v_alpha || !state->step)
     return fail(SQUINT_EINVAL, "NULL state field");
+  {
+    squint_status r = check_indices(idx, (int64_t)utd * dims->batch, replay->size, false, "squint_update idx",
+                                    (cudaStream_t)stream);
+    if (r != SQUINT_OK) return r;
+  }
   Comm* cm = reinterpret_cast<Comm*>(comm);
   if (dims->precision == SQUINT_BF16) {
     cudaStream_t s = (cudaStream_t)stream;

@@ -236,6 +236,7 @@ int g_branch_enabled = 1;
 // precedes it on the branch and the SMs it occupies set the pace), kept for other shapes
 int g_pipe_enabled = 0;
 
+
 struct Ctx {
   const squint_dims& d;
   const Layout& L;
@@ -1341,6 +1342,10 @@ squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const flo
   return SQUINT_OK;
 }
 
+// option 3: validate the device-side preconditions (index ranges, distinct slots) before each
+// call, synchronising the stream (a debugging aid, off by default; squint.h)
+int g_check_enabled = 0;
+
 }  // namespace sq
 
 extern "C" squint_status squint_selftest_gemm(const void* A, int a_rows, int a_cols, int a_ld, int a_mn, const void* B,
@@ -1372,6 +1377,10 @@ extern "C" SQUINT_API squint_status squint_set_option(int key, int value) {
   }
   if (key == 2) {
     sq::g_pipe_enabled = value != 0;
+    return SQUINT_OK;
+  }
+  if (key == 3) {
+    sq::g_check_enabled = value != 0;
     return SQUINT_OK;
   }
   return sq::set_error(SQUINT_EINVAL, "unknown option");

@@ -126,6 +126,29 @@ def test_stage_pinned_copies_bytes(nbytes, off):
     assert (dst[off + nbytes:].cpu() == 7).all() and (dst[:off].cpu() == 7).all()
 
 
+def test_precondition_checks_option3():
+    """squint_set_option(3): device-side preconditions (idx < size, distinct slots)
+    are validated and reported as EINVAL instead of undefined behaviour."""
+    S = P.squint
+    frames = torch.as_tensor(SI.make_frames(4, 128, seed=1)).to(DEV)
+    ring = torch.zeros((10, 3, 16, 16), dtype=torch.uint8, device=DEV)
+    S.LIB.squint_set_option(3, 1)
+    try:
+        P.squint_insert(frames, 8, torch.tensor([1, 2, 3, 4], device=DEV), ring)  # valid
+        for bad in ([1, 2, 2, 4], [1, 2, 3, 10], [-1, 2, 3, 4]):
+            with pytest.raises(S.SquintError) as e:
+                P.squint_insert(frames, 8, torch.tensor(bad, device=DEV), ring)
+            assert e.value.status == 1
+        pr = Problem("c0", utd=1, seed=0)
+        L = pr.gpu_setup()
+        pr.idx_t[0, 3] = pr.R["size"]  # one sampled index past the filled rows
+        with pytest.raises(S.SquintError) as e:
+            L.update(pr.replay, pr.idx_t, pr.sh_t, pr.eps_t, pr.metrics_t)
+        assert e.value.status == 1 and b"out of range" in S.LIB.squint_last_error()
+    finally:
+        S.LIB.squint_set_option(3, 0)
+
+
 # ---- a14 soft update ------------------------------------------------------------------
 @pytest.mark.parametrize("n,tau", [(1, 0.005), (1000, 0.005), (4097, 0.5), (33, 0.0), (33, 1.0)])
 def test_soft_update(n, tau):
