@@ -282,6 +282,38 @@ def test_update_c0_mse_fp32(mode, utd, batch):
     _check_update(pr, L, met, st_ref, met_ref, trace)
 
 
+@pytest.mark.parametrize("case", ["all_done", "reward_clip", "gamma0", "gamma1_tau1", "alpha_large", "tau0"])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_update_degenerate_cases(case, precision):
+    """Degenerate cases of the method: every transition terminal (targets = r), rewards far
+    outside the support (all target mass clipped onto the edge atoms), gamma = 0, gamma = tau = 1,
+    a large temperature, tau = 0 (target frozen)."""
+    hp_over = {"gamma0": {"gamma": 0.0}, "gamma1_tau1": {"gamma": 1.0, "tau": 1.0}, "tau0": {"tau": 0.0}}.get(case, {})
+    cfg, kw = ("c0", {}) if precision == "fp32" else ("c2", {"capacity": 2048})
+    pr = Problem(cfg, utd=2, seed=12, hp_over=hp_over, **kw)
+    if case == "all_done":
+        pr.R["done"][:] = 1
+    if case == "reward_clip":
+        pr.R["reward"][:] = np.where(np.arange(pr.R["reward"].shape[0]) % 2 == 0, 60.0, -60.0).astype(np.float32)
+    if case == "alpha_large":
+        # alpha = e^3 (fp32) / e^1.5 (bf16): the target's atom shift alpha log pi' multiplies the
+        # bf16 error of log pi' by alpha, so the bf16 bar on m (2e-2) holds up to alpha ~ 5
+        la = 3.0 if precision == "fp32" else 1.5
+        pr.vals[("alpha", "log_alpha")] = np.full_like(np.asarray(pr.vals[("alpha", "log_alpha")]), la)
+    L = pr.gpu_setup(precision=P.BF16 if precision == "bf16" else P.FP32)
+    met = pr.gpu_update(L)
+    trace = []
+    st_ref, met_ref = pr.oracle_update(trace)
+    if precision == "fp32":
+        _check_update(pr, L, met, st_ref, met_ref, trace)
+    else:
+        _check_update_bf16(pr, L, met, st_ref, met_ref, trace)
+    if case == "tau0":  # Polyak with tau = 0 leaves the target bitwise unchanged
+        got = group_values(L, "target")
+        for n in got:
+            assert np.array_equal(got[n], np.asarray(pr.vals[("target", n)], np.float32).reshape(got[n].shape)), n
+
+
 def test_update_deterministic_bitwise():
     pr = Problem("c0", utd=2, seed=7)
     outs = []
