@@ -513,6 +513,12 @@ def test_update_c3_shapes_bf16():
     _bf16_case("c3", seed=4, capacity=4096, batch=512)
 
 
+def test_update_c3_full_batch_bf16():
+    """BASELINE configs[3] at its full single-GPU size: global batch 4096, C = 64, critic
+    512-512, 101 atoms (the maximum shapes the path is built for)."""
+    _bf16_case("c3", seed=6, capacity=8192)
+
+
 # ---- bf16 GEMM engine (TMA + tcgen05) self-test: both operand majors, ragged tails -------
 def _padded(x):
     """contiguous storage with a 16-byte multiple row pitch; returns (storage, logical cols)"""
