@@ -58,12 +58,14 @@ def blas_threads():
 # ---------------------------------------------------------------------------------------
 def variant(args):
     """(dims, hparams, label) of the workload: c2, or one of its f3/f4 variants."""
-    d = SI.dims_of(CFG, critic_kind=1 if args.critic == "mse" else 0)
-    hp = SI.hp_of(CFG, target_mode=1 if args.target == "cdq" else 0)
+    d = SI.dims_of(args.config, critic_kind=1 if args.critic == "mse" else 0)
+    hp = SI.hp_of(args.config, target_mode=1 if args.target == "cdq" else 0)
     parts = ([] if args.critic == "c51" else ["scalar MSE critic"]) + ([] if args.target == "avg" else ["CDQ-min target"]) \
         + ([] if args.insert == "chw" else [{"hwc": "HWC frames", "jitter": "colour jitter",
                                              "hwc-jitter": "HWC frames + colour jitter"}[args.insert]]) \
-        + (["replay capacity (P:189)"] if args.capacity else [])
+        + (["replay capacity (P:189)"] if args.capacity else []) \
+        + ([f"{args.config} shapes (batch {d['batch']}, C {d['conv_ch']}, critic {d['critic_hidden']})"]
+           if args.config != CFG else [])
     return d, hp, ("; variant: " + ", ".join(parts)) if parts else ""
 
 
@@ -105,11 +107,13 @@ def run_reference(args):
     tot = sum(ts)
     value = args.steps / tot  # one update per sample
     cores = blas_threads()
-    sample = f"per step: oracle act+insert on {N_ENV // UTD} frames + 1 update at B=512 (c2 shapes), float64 NumPy"
+    sample = (f"per step: oracle act+insert on {N_ENV // UTD} frames + 1 update at B={variant(args)[0]['batch']} "
+              f"({args.config} shapes), float64 NumPy")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "c2 update share of an Algorithm-1 step (CPU oracle)" + variant(args)[2], "global_batch": 512,
+            "config": {"workload": "c2 update share of an Algorithm-1 step (CPU oracle)" + variant(args)[2],
+                       "global_batch": variant(args)[0]["batch"],
                        "utd": 1, "n_env_frames": N_ENV // UTD},
             "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -176,7 +180,7 @@ def run_gpu(args):
     precision = {"fp32": P.FP32, "bf16": P.BF16}[args.precision]
     d, hp, vlabel = variant(args)
     B, A = d["batch"], d["action_dim"]
-    cap = args.capacity or SI.CONFIGS[CFG]["capacity"]
+    cap = args.capacity or SI.CONFIGS[args.config]["capacity"]
     K, W = args.steps, args.warmup
 
     L = P.Learner(d, hp, precision=precision, device=dev, utd=UTD)
@@ -513,13 +517,13 @@ def run_gpu(args):
     if world == 1 and not args.no_cpu:
         ts = [oracle_sample(args, seed=s) for s in range(args.cpu_samples)]
         cpu = {"value": len(ts) / sum(ts), "unit": "updates/s", "cores": blas_threads(), "kind": "oracle",
-               "sample": f"{len(ts)} x (oracle act+insert on {N_ENV // UTD} frames + 1 update at B=512), "
+               "sample": f"{len(ts)} x (oracle act+insert on {N_ENV // UTD} frames + 1 update at B={B}), "
                          f"{sum(ts):.1f} s float64 NumPy"}
     line = {"metric": METRIC, "value": world * UTD * K / (ms / 1e3), "unit": "updates/s", "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": {P.FP32: "f32", P.BF16: "bf16"}[precision], "data": "synthetic",
             "config": {"workload": "c2: Algorithm-1 step = insert2(1024 new 128x128 frames) + act(1024 envs) + "
-                                   f"4 updates at B=512 per rank, 101 atoms, {cap:,}-row ring"
+                                   f"4 updates at B={B} per rank, 101 atoms, {cap:,}-row ring"
                                    + (" (act squints its own frames)" if args.act_full else "") + vlabel, "global_batch": B * world, "utd": UTD,
                        "n_env": N_ENV, "parallelism": f"dp{world}", "capacity": cap,
                        "l2": f"ring {cap * 1662 / 1e9:.2f} GB + rotating frame pools (4 x 50 MB) > L2",
@@ -548,6 +552,7 @@ def main():
     ap.add_argument("--critic", default="c51", choices=["c51", "mse"])
     ap.add_argument("--target", default="avg", choices=["avg", "cdq"])
     ap.add_argument("--insert", default="chw", choices=["chw", "hwc", "jitter", "hwc-jitter"])
+    ap.add_argument("--config", default=CFG, choices=["c2", "c3"])  # c3: the DP shapes on one GPU (B 4096)
     ap.add_argument("--capacity", type=int, default=0)  # replay rows (0: configs' 1M; f3: 100K axis)
     args = ap.parse_args()
     if args.act_full and args.insert != "chw":
