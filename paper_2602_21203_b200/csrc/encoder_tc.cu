@@ -182,10 +182,12 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ 
   const float inv255 = 1.0f / 255.0f;
   int gi = 0;
 
-  for (int job = blockIdx.x; job < total; job += gridDim.x, ++gi) {
+  // ---- 1. images (u8) + replay row gathers of group `job` into xs (and global outputs); run
+  // for the next group while this group's MMAs and epilogues run (xs is free once the
+  // im2col has read it)
+  auto stage = [&](int job) {
     const int src = job / ngroups, g = job - src * ngroups;
     const int b0 = g * kGF;
-    // ---- 1. images (u8) + replay row gathers ------------------------------------------------
     if (a.mode == 0) {
       // one 16-pixel row per item: shifted crop with replicate padding from the source row
       const uint8_t* R = a.src[src];
@@ -276,6 +278,12 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ 
         }
       }
     }
+  };
+  if (blockIdx.x < total) stage(blockIdx.x);
+  for (int job = blockIdx.x; job < total; job += gridDim.x, ++gi) {
+    const int src = job / ngroups, g = job - src * ngroups;
+    const int b0 = g * kGF;
+    (void)src;
     __syncthreads();
     enc_stamp(a.dbg && gi == 0, 11);
     // ---- 2. conv1 im2col: 3 row tiles, K 0..26 from the image (k = ci*9 + ki*3 + kj at byte
@@ -310,6 +318,7 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ 
           tc::mma_bf16(t_c1 + t * C, tc::sdesc_k128(a0 + t * 16384 + 32 * k), tc::sdesc_k128(w0 + 32 * k), id_c, k);
       tc::mma_commit(&bar1);
     }
+    if (job + (int)gridDim.x < total) stage(job + (int)gridDim.x);  // overlaps the MMAs below
     tc::mbar_wait(&bar1, gi & 1);
     tc::fence_after_sync();
     enc_stamp(a.dbg && gi == 0, 12);
