@@ -10,7 +10,7 @@ Nothing here is blocked, fused or reordered for speed.
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 

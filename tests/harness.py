@@ -3,7 +3,6 @@ libsquint, and compares.  Test infrastructure only."""
 from __future__ import annotations
 
 import copy
-import re
 
 import numpy as np
 
