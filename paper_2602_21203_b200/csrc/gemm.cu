@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   __shared__ uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], done_bar, ld_bar[8], stats_bar;
   __shared__ uint32_t tmem_slot;
   __shared__ float red[2][2][128];
-  __shared__ float2 cl_red[4][128];  // per-row (sum, sum of squares) of each cluster CTA, pushed by the CTAs
+  __shared__ float2 cl_red[8][128];  // per-row (sum, sum of squares) of each cluster CTA, pushed by the CTAs
   __shared__ __align__(16) float s_bias[512], s_g[512], s_beta[512];  // per-column epilogue params
   // This CTA's problem descriptor, copied once into shared memory: indexed reads of the large
   // __grid_constant__ batch go through the constant cache and miss there (hundreds of cycles
@@ -501,6 +501,87 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     }
   } else if constexpr (EPI == GE_BWD_LN_RELU || EPI == GE_BWD_LN_TANH) {
     float* colacc = reinterpret_cast<float*>(smem + kColaccOff);  // [4][3][512]
+    if (P.bn == 32) {
+      // 8-CTA clusters (32 columns per CTA): warp (q, hh) takes columns 16 hh .. 16 hh + 15 of the
+      // slice, so each thread handles 16 values; outputs go straight to global memory (a 64-column
+      // TMA box would overlap the neighbour CTA's columns)
+      uint8_t* xs = b.xpre_off ? smem + b.xpre_off + q * 4 * kSlotBytes : pslots;
+      if (!b.xpre_off && hh == 0 && lane == 0) {
+        tc::mbar_expect_tx(&ld_bar[q], kSlotBytes);
+        tc::tma_load_2d(xs, &b.maps[P.xmap], n0, row0, &ld_bar[q]);
+      }
+      tc::mbar_wait(&ld_bar[q], 0);
+      stamp(5);
+      const int c0 = hh * 16;
+      float dn[16], xh[16], pg[16], pb[16];
+      tc::tmem_ld16(trow + c0, dn);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const uint4 u = *reinterpret_cast<const uint4*>(xs + gd::box_off(lane, 2 * hh + j));
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(h2[k]);
+          xh[8 * j + 2 * k] = f.x, xh[8 * j + 2 * k + 1] = f.y;
+        }
+      }
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int cc = c0 + j;
+        const bool ok = rv && (cc < nreal);
+        const float x = ok ? xh[j] : 0.f;
+        const float n = fmaf(x, s_g[cc], s_beta[cc]);
+        const float d = ok ? ((EPI == GE_BWD_LN_RELU) ? (n > 0.f ? dn[j] : 0.f) : dn[j] * sech2_fast(n)) : 0.f;
+        const float dxh = d * s_g[cc];
+        s1 += dxh;
+        s2 += dxh * x;
+        pg[j] = d * x;
+        pb[j] = d;
+        dn[j] = d;
+        xh[j] = x;
+      }
+      const float cg = gd::colsum16(pg), cb = gd::colsum16(pb);
+      if (lane < 16) {
+        colacc[(q * 3 + 1) * 512 + c0 + lane] = cg;
+        colacc[(q * 3 + 2) * 512 + c0 + lane] = cb;
+      }
+      float m1, m2;
+      row_total2(s1, s2, m1, m2);
+      stamp(6);
+      m1 /= (float)N;
+      m2 /= (float)N;
+      const float rs = rv ? rs_pre : 0.f;
+      float o[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const bool ok = rv && (c0 + j < nreal);
+        o[j] = ok ? rs * (dn[j] * s_g[c0 + j] - m1 - xh[j] * m2) : 0.f;
+        pg[j] = o[j];
+      }
+      if (rv && c0 < nreal) {
+        bf16* dst = P.out + (int64_t)r * P.ldo + n0 + c0;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          float f[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) f[k] = o[8 * j + k];
+          reinterpret_cast<uint4*>(dst)[j] = tc::pack_bf16x8(f);
+        }
+      }
+      const float cx = gd::colsum16(pg);
+      if (lane < 16) colacc[(q * 3 + 0) * 512 + c0 + lane] = cx;
+      __syncthreads();
+      if (P.part) {
+        for (int e = tid; e < 3 * nreal; e += kThreads) {
+          const int kk = e / nreal, c = e - kk * nreal;
+          float sacc = 0.f;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) sacc += colacc[(qq * 3 + kk) * 512 + c];
+          P.part[((int64_t)mt * 3 + kk) * N + n0 + c] = sacc;
+        }
+      }
+    } else {
     // the pair's x_hat boxes (<= 4) by TMA on one transaction barrier (prefetched when possible)
     uint8_t* xs = b.xpre_off ? smem + b.xpre_off + q * 4 * kSlotBytes : pslots;
     if (!b.xpre_off && hh == 0 && lane == 0) {
@@ -588,6 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
         P.part[((int64_t)mt * 3 + kk) * N + n0 + c] = s;
       }
     }
+    }  // bn == 64
   } else if constexpr (EPI == GE_TG_FWD) {
     float* T = reinterpret_cast<float*>(smem) + warp * 32 * 33;
     if (hh == 0) {
@@ -1210,7 +1292,16 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
       cs = c < cs ? c : cs;
     }
     static const bool no_cluster = getenv("SQUINT_NO_CLUSTER") != nullptr;
-    b.cs = no_cluster ? 1 : cs;
+    // LayerNorm backward over 256-column rows: 8-CTA clusters of 32 columns (16 per warp in the
+    // epilogue; measured per update 236 / 207 / 186 us with 1 / 2 / 4 CTAs per row)
+    static const bool no_cs8 = getenv("SQUINT_NO_BWD_CS8") != nullptr;
+    if (cs == 4 && !no_cs8 && (epi0 == GE_BWD_LN_RELU || epi0 == GE_BWD_LN_TANH)) {
+      bool all256 = true;
+      for (int i = 0; i < b.nprob; ++i) all256 = all256 && b.p[i].N % 256 == 0;
+      if (all256) cs = 8;
+    }
+    static const int cs_max = getenv("SQUINT_LN_CS_MAX") ? atoi(getenv("SQUINT_LN_CS_MAX")) : 8;  // experiments
+    b.cs = no_cluster ? 1 : (cs < cs_max ? cs : cs_max);
   }
   int t = 0, bmax = 0;
   for (int i = 0; i < b.nprob; ++i) {

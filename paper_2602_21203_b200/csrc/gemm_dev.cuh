@@ -91,6 +91,23 @@ __device__ __forceinline__ float colsum32(float (&v)[32]) {
   return v[0];
 }
 
+// column sums of 16 values per lane over the warp's 32 rows: every lane returns the sum of
+// column (lane & 15) (fixed-order butterfly, then the two 16-lane halves)
+__device__ __forceinline__ float colsum16(float (&v)[16]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 8; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int j = 0; j < s; ++j) {
+      const float send = up ? v[j] : v[j + s];
+      const float keep = up ? v[j + s] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+
 // ---- epilogue staging: per-warp ring of four 64-column x 32-row bf16 boxes (128B swizzle) ---
 // A lane owns one row of the box; the tile moves between smem and global memory by TMA.
 constexpr int kSlotBytes = 4096;
