@@ -1295,10 +1295,18 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     // LayerNorm backward over 256-column rows: 8-CTA clusters of 32 columns (16 per warp in the
     // epilogue; measured per update 236 / 207 / 186 us with 1 / 2 / 4 CTAs per row)
     static const bool no_cs8 = getenv("SQUINT_NO_BWD_CS8") != nullptr;
+    // (only for 256-wide rows: at 512 columns, 8 CTAs of 64 measured far slower than 4 of 128 --
+    // c3 1227 -> 976 updates/s with the forward and backward both at 8)
+    // and only while the 8-CTA tiling still fits one wave on the 148 SMs (c3's B = 4096 would
+    // need two)
     if (cs == 4 && !no_cs8 && (epi0 == GE_BWD_LN_RELU || epi0 == GE_BWD_LN_TANH)) {
-      bool all256 = true;
-      for (int i = 0; i < b.nprob; ++i) all256 = all256 && b.p[i].N % 256 == 0;
-      if (all256) cs = 8;
+      bool ok = true;
+      int ctas = 0;
+      for (int i = 0; i < b.nprob; ++i) {
+        ok = ok && b.p[i].N == 256;
+        ctas += 8 * ((b.p[i].M + 127) / 128);
+      }
+      if (ok && ctas <= 148) cs = 8;
     }
     static const int cs_max = getenv("SQUINT_LN_CS_MAX") ? atoi(getenv("SQUINT_LN_CS_MAX")) : 8;  // experiments
     b.cs = no_cluster ? 1 : (cs < cs_max ? cs : cs_max);
