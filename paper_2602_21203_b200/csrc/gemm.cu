@@ -842,13 +842,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_sk(const __grid_constant__
   // per-row epilogue inputs, loaded while the main loop runs: thread (row tid / 8 + 32 it,
   // column group tid % 8); R / 32 <= 2 rows per thread
   const int cg = tid & 7, c0 = cg * 8;
-  const int nit = R / 32;
+  const int nit = (R + 31) / 32;  // R = 16 (ks = 8): threads of rows tid / 8 >= R idle
   uint4 xpre[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
   float rspre[2] = {0.f, 0.f};
   float tg_pre[2][2][3];  // tanh-Gaussian: [it][d = cg, cg + 8][mu | l | eps]
   for (int it = 0; it < nit; ++it) {
     const int r = m0 + (int)kr * R + (tid >> 3) + 32 * it;
-    if (r >= P.M) continue;
+    if (r >= P.M || (tid >> 3) + 32 * it >= R) continue;
     if constexpr (EPI == GE_BWD_LN_TANH || EPI == GE_BWD_LN_RELU) {
       if (c0 < nreal) xpre[it] = *reinterpret_cast<const uint4*>(P.xh + (int64_t)r * P.ldx + c0);
       rspre[it] = P.rstd[r];
@@ -952,9 +952,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_sk(const __grid_constant__
     tc::fence_async_smem();
     tc::named_bar(1 + q, 64);
     if (hh == 0 && lane == 0) {
-      const uint32_t owner = (uint32_t)(q * ks / 4);
-      const int rowoff = q * 32 - (int)owner * R;
-      tc::bulk_s2cluster(tc::mapa(recv + ((int)kr * R + rowoff) * 256, owner), stg, 8192, tc::mapa(&recv_bar, owner));
+      if (ks <= 4) {
+        const uint32_t owner = (uint32_t)(q * ks / 4);
+        const int rowoff = q * 32 - (int)owner * R;
+        tc::bulk_s2cluster(tc::mapa(recv + ((int)kr * R + rowoff) * 256, owner), stg, 8192, tc::mapa(&recv_bar, owner));
+      } else {  // ks = 8: the quarter's 32 rows belong to two owners of 16 rows each
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const uint32_t owner = (uint32_t)(2 * q + h2);
+          tc::bulk_s2cluster(tc::mapa(recv + ((int)kr * R) * 256, owner), stg + h2 * 4096, 4096,
+                             tc::mapa(&recv_bar, owner));
+        }
+      }
     }
   }
   __syncthreads();  // s_bias / s_g / s_beta visible
@@ -992,10 +1000,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_sk(const __grid_constant__
     for (int it = 0; it < nit; ++it) {
       const int rr = (tid >> 3) + 32 * it;
       float acc[8];
-      recv_sum8(rr, acc);
+      recv_sum8(rr < R ? rr : R - 1, acc);
       if (it == 0) stamp(8);
       const int r = m0 + (int)kr * R + rr;
-      const bool rv = r < P.M;
+      const bool rv = r < P.M && rr < R;
       if constexpr (EPI == GE_LN_TANH || EPI == GE_LN_RELU) {
         float s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -1117,7 +1125,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_sk(const __grid_constant__
     for (int it = 0; it < nit; ++it) {
       const int rr = (tid >> 3) + 32 * it;
       const int r = m0 + (int)kr * R + rr;
-      const bool rv = r < P.M;
+      const bool rv = r < P.M && rr < R;
       if constexpr (EPI == GE_TG_FWD) {
         const int A = N / 2;
         float lp = 0.f;
@@ -1283,6 +1291,13 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
       ok = ((b.p[i].N + 15) & ~15) <= 64;
     }
     if (ok) b.ks = minkb >= 4 ? 4 : (minkb >= 2 ? 2 : 1);
+    // LayerNorm split-K over 8 CTAs (16 rows each) when every CTA still gets >= 1 K block
+    static const bool no_sk8 = getenv("SQUINT_NO_SK8") != nullptr;
+    int tiles8 = 0;
+    for (int i = 0; i < b.nprob; ++i) tiles8 += 8 * ((b.p[i].M + 127) / 128);
+    if (ok && !no_sk8 && minkb >= 8 && tiles8 <= 148 &&
+        (epi0 == GE_LN_TANH || epi0 == GE_LN_RELU || epi0 == GE_BWD_LN_TANH || epi0 == GE_BWD_LN_RELU))
+      b.ks = 8;  // (one wave on the 148 SMs; c2 4845 -> 4975 updates/s)
   }
   if (ln_launch && b.ks == 1) {
     int cs = 8;
