@@ -228,9 +228,10 @@ SQUINT_API squint_status squint_act(const squint_dims* dims, const squint_hparam
  * batch, losses are scaled by 1/(B*nranks) and gradients/metric sums are SUM
  * all-reduced over ranks (Q33).
  * SQUINT_BF16 with comm == NULL, outside a stream capture: the call's ~30 launches per update
- * are captured once per distinct argument set (all pointers, dims, hparams, utd) into a
+ * are captured once per distinct argument set (all pointers, dims, hparams, utd; not replay->size,
+ * which only bounds the host-side index check) into a
  * CUDA graph kept in a small per-thread cache (8 entries) and replayed on `stream`; calls with
- * changed arguments capture anew.  SQUINT_NO_GRAPH=1 launches directly.  Inside a caller's
+ * changed arguments capture anew.  SQUINT_NO_GRAPH=1 (debugging) launches directly.  Inside a caller's
  * capture the launches join that capture.
  * Errors: EINVAL (utd < 1, batch < 1, gamma/tau outside [0,1], size < 1, bad support),
  * ESHAPE (dims inconsistent), EUNSUPPORTED (shape/precision not built). */
@@ -284,7 +285,11 @@ SQUINT_API int squint_set_launch_events(void** events, int n);
  * (0, default): sampled indices in [0, replay.size), insert / act slots in [0, capacity) and
  * pairwise distinct -- a check kernel plus a stream synchronisation per call, returning
  * SQUINT_EINVAL with a message instead of undefined behaviour (skipped inside a stream
- * capture).  Errors: EINVAL for an unknown key. */
+ * capture); key 4 = numerics measurement on the SQUINT_FP32 path only (0, default): round the dense
+ * layers' GEMM operands to bf16 before the fp32 multiply-add -- bit 0 the activations / dY, bit 1
+ * the weights -- to measure how much of the bf16 path's deviation from the oracle bf16 operand
+ * rounding alone explains (reading R-tol-bf16).  Errors: EINVAL for an unknown key or
+ * value. */
 SQUINT_API squint_status squint_set_option(int key, int value);
 /* Records the next timeline event on `stream` without a launch (closes the last interval). */
 SQUINT_API squint_status squint_record_launch_event(squint_stream_t stream);

@@ -52,7 +52,6 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
   __shared__ uint32_t tmem_slot;
   __shared__ float red[2][2][128];
   __shared__ float2 cl_red[kCS][128];  // per-row (sum, sum of squares) partials pushed by each CTA
-  __shared__ float4 cl_q[2 * kCS][128];  // actor-loss epilogue: per-row (max, sum e, sum e z) per CTA half
   __shared__ __align__(16) float s_bias[64], s_g[64], s_beta[64];
 
   const int rank = blockIdx.x % kCS, cl = blockIdx.x / kCS;
@@ -321,64 +320,6 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
           for (int qq = 0; qq < 4; ++qq) s += colacc[(qq * 3 + kk) * 64 + c];
           L.part[((int64_t)mt * 3 + kk) * L.N + n0 + c] = s;
         }
-    } else if (epi == GE_BIAS_F32 && L.q_out) {
-      // actor-loss epilogue (Q25): the row's softmax over the N atoms spans the cluster (32 atoms
-      // per CTA, 16 per warp half): partial (max, sum e, sum e z) of each half exchanged by
-      // st.async, combined in (rank, half) order
-      const float dz = (L.v_max - L.v_min) / (float)(L.N - 1);
-      const int j0 = hh * 16, nv = min(16, nreal - j0);
-      float v16[16];
-      tc::tmem_ld16(trow + j0, v16);
-      float lm = -INFINITY, ls = 0.f, lt = 0.f;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        v16[j] = j < nv ? v16[j] + s_bias[j0 + j] : -INFINITY;
-        lm = fmaxf(lm, v16[j]);
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (j < nv) {
-          const float e = __expf(v16[j] - lm);
-          ls += e;
-          lt += e * (L.v_min + (float)(n0 + j0 + j) * dz);
-        }
-      if (tid == 0) tc::mbar_expect_tx(&stats_bar, kCS * 2 * 128 * 16);
-      for (int rk = 0; rk < kCS; ++rk)
-        tc::st_async_v4(tc::mapa(&cl_q[rank * 2 + hh][rl], (uint32_t)rk), lm, ls, lt, 0.f, tc::mapa(&stats_bar, (uint32_t)rk));
-      tc::mbar_wait(&stats_bar, nstat & 1);
-      ++nstat;
-      float M = -INFINITY;
-#pragma unroll
-      for (int e = 0; e < 2 * kCS; ++e) M = fmaxf(M, cl_q[e][rl].x);
-      float S = 0.f, T = 0.f;
-#pragma unroll
-      for (int e = 0; e < 2 * kCS; ++e) {
-        const float4 c = cl_q[e][rl];
-        const float f = c.y > 0.f ? __expf(c.x - M) : 0.f;
-        S += c.y * f;
-        T += c.z * f;
-      }
-      const float Q = T / S, inv = 1.f / S;
-      if (rv && nv > 0) {
-        if (rank == 0 && hh == 0) L.q_out[r] = Q;
-        __nv_bfloat16* o = L.dq + (int64_t)r * L.ld_dq + n0 + j0;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float pj = j < nv ? __expf(v16[j] - M) * inv : 0.f;
-          v16[j] = L.q_scale * pj * ((L.v_min + (float)(n0 + j0 + j) * dz) - Q);
-        }
-        if (nv == 16 && al16(o)) {
-#pragma unroll
-          for (int j8 = 0; j8 < 2; ++j8) {
-            float f[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) f[k] = v16[8 * j8 + k];
-            reinterpret_cast<uint4*>(o)[j8] = tc::pack_bf16x8(f);
-          }
-        } else {
-          for (int j = 0; j < nv; ++j) o[j] = __float2bfloat16_rn(v16[j]);
-        }
-      }
     } else if (epi == GE_BIAS_F32) {
       if (hh == 0 && nreal > 0) {  // slice 32: one chunk, stored row by row through a transpose tile
         // staging in the idle B buffer (the last layer has no next weights)

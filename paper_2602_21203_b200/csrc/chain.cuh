@@ -45,13 +45,6 @@ struct CLayer {
   float* logp;
   float* tgo;
   float lo, hi, ln_eps;
-  // actor-loss epilogue of a logits layer (GE_BIAS_F32 with q_out != NULL, Q25): instead of the
-  // logits, dq[m][k] = q_scale p_k (z_k - Q) (bf16, ld_dq) with p = softmax over the N atoms of
-  // the row (statistics exchanged across the cluster) and Q = sum_k p_k z_k -> q_out[m]
-  __nv_bfloat16* dq;
-  int ld_dq;
-  float* q_out;
-  float v_min, v_max, q_scale;
 };
 
 constexpr int kChainMaxLayers = 3;

@@ -16,10 +16,6 @@ namespace sq {
 // grid_trigger() so its own dependents may launch.  Both are no-ops without the launch attribute.
 SQ_DEV void grid_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 SQ_DEV void grid_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-inline bool pdl_enabled() {
-  static const bool off = std::getenv("SQUINT_NO_PDL") != nullptr;
-  return !off;
-}
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args&&... args) {
@@ -32,7 +28,7 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 

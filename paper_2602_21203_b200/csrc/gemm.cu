@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
         for (int k = 0; k < 4; ++k) {
           const uint64_t ad = tc::sdesc_sw128(a0 + astep * k, albo, 1024);
           const uint32_t acc = (kb | k) != 0;
-          if (!(b.dbg && b.dbg_nomma)) tc::mma_bf16_e(tmem, ad, tc::sdesc_sw128(b0 + bstep * k, blbo, 1024), id1, acc);
+          tc::mma_bf16_e(tmem, ad, tc::sdesc_sw128(b0 + bstep * k, blbo, 1024), id1, acc);
           if (n2 > 0) tc::mma_bf16_e(tmem + 256, ad, tc::sdesc_sw128(b0 + 32768 + bstep * k, blbo, 1024), id2, acc);
           if (ones) tc::mma_bf16_e(tmem + ones_col, ad, tc::sdesc_sw128(ones0 + 32 * k, 16, 1024), id_ones, acc);
         }
@@ -1273,16 +1273,13 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   if (b.nprob == 0) return 0;
   // plan tiles.  LayerNorm epilogues need whole rows: with N >= 128 the row is split over a
   // cluster of cs CTAs of 64-column multiples (more SMs share the epilogue work).
-  static const bool no_pre = getenv("SQUINT_NO_PREFETCH_B") != nullptr;
-  if (no_pre) b.prefetch_b = 0;
   const int epi0 = b.p[0].epi;
   const bool ln_launch = epi0 == GE_LN_RELU || epi0 == GE_LN_TANH || epi0 == GE_BWD_LN_RELU || epi0 == GE_BWD_LN_TANH;
   b.cs = 1;
   // split-K clusters for narrow row-complete layers with several K blocks (k_gemm_sk)
   b.ks = 1;
   {
-    static const bool no_sk = getenv("SQUINT_NO_SPLITK") != nullptr;
-    bool ok = !no_sk && kernel_sk_for(epi0) != nullptr;
+    bool ok = kernel_sk_for(epi0) != nullptr;
     int minkb = 1 << 30;
     for (int i = 0; i < b.nprob && ok; ++i) {
       int k = 0;
@@ -1292,13 +1289,15 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     }
     if (ok) b.ks = minkb >= 4 ? 4 : (minkb >= 2 ? 2 : 1);
     // LayerNorm split-K over 8 CTAs (16 rows each) when every CTA still gets >= 1 K block
-    static const bool no_sk8 = getenv("SQUINT_NO_SK8") != nullptr;
     int tiles8 = 0;
     for (int i = 0; i < b.nprob; ++i) tiles8 += 8 * ((b.p[i].M + 127) / 128);
-    if (ok && !no_sk8 && minkb >= 8 && tiles8 <= 148 &&
+    if (ok && minkb >= 8 && tiles8 <= 148 &&
         (epi0 == GE_LN_TANH || epi0 == GE_LN_RELU || epi0 == GE_BWD_LN_TANH || epi0 == GE_BWD_LN_RELU))
       b.ks = 8;  // (one wave on the 148 SMs; c2 4845 -> 4975 updates/s)
   }
+  if (b.ks > kGemmMaxSplitK) return -1;
+  for (int i = 0; i < b.nprob; ++i)  // column partials: [mtiles * ks][3][N] floats must fit
+    if (b.p[i].part && (int64_t)((b.p[i].M + 127) / 128) * b.ks * 3 * b.p[i].N > b.p[i].part_cap) return -1;
   if (ln_launch && b.ks == 1) {
     int cs = 8;
     for (int i = 0; i < b.nprob; ++i) {
@@ -1306,15 +1305,13 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
       const int c = n >= 256 && n % 256 == 0 ? 4 : (n >= 128 && n % 128 == 0 ? 2 : 1);
       cs = c < cs ? c : cs;
     }
-    static const bool no_cluster = getenv("SQUINT_NO_CLUSTER") != nullptr;
     // LayerNorm backward over 256-column rows: 8-CTA clusters of 32 columns (16 per warp in the
     // epilogue; measured per update 236 / 207 / 186 us with 1 / 2 / 4 CTAs per row)
-    static const bool no_cs8 = getenv("SQUINT_NO_BWD_CS8") != nullptr;
     // (only for 256-wide rows: at 512 columns, 8 CTAs of 64 measured far slower than 4 of 128 --
     // c3 1227 -> 976 updates/s with the forward and backward both at 8)
     // and only while the 8-CTA tiling still fits one wave on the 148 SMs (c3's B = 4096 would
     // need two)
-    if (cs == 4 && !no_cs8 && (epi0 == GE_BWD_LN_RELU || epi0 == GE_BWD_LN_TANH)) {
+    if (cs == 4 && (epi0 == GE_BWD_LN_RELU || epi0 == GE_BWD_LN_TANH)) {
       bool ok = true;
       int ctas = 0;
       for (int i = 0; i < b.nprob; ++i) {
@@ -1323,8 +1320,7 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
       }
       if (ok && ctas <= 148) cs = 8;
     }
-    static const int cs_max = getenv("SQUINT_LN_CS_MAX") ? atoi(getenv("SQUINT_LN_CS_MAX")) : 8;  // experiments
-    b.cs = no_cluster ? 1 : (cs < cs_max ? cs : cs_max);
+    b.cs = cs;
   }
   int t = 0, bmax = 0;
   for (int i = 0; i < b.nprob; ++i) {
@@ -1357,8 +1353,7 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   // weight gradients (one segment, both operands MN-major): wide TMA boxes of KW K blocks
   b.wide = 1;
   if (epi0 == GE_DW) {
-    static const bool no_wide = getenv("SQUINT_NO_WIDE") != nullptr;
-    bool ok = !no_wide;
+    bool ok = true;
     int nbb = 0, maxk = 0;
     for (int i = 0; i < b.nprob && ok; ++i) {
       const GProb& p = b.p[i];
@@ -1393,8 +1388,7 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   // A multicast across a LayerNorm cluster (its CTAs share the rows): only without ring reuse,
   // so no stage is refilled before every CTA's MMAs consumed it
   {
-    static const bool no_mc = getenv("SQUINT_NO_MCAST") != nullptr;
-    b.mcast = (!no_mc && b.cs > 1 && b.ks == 1 && maxkb <= S) ? 1 : 0;
+    b.mcast = (b.cs > 1 && b.ks == 1 && maxkb <= S) ? 1 : 0;
   }
   // tensor maps
   b.nmaps = 0;
@@ -1471,8 +1465,6 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     // SQUINT_GEMM_DBG=k: only launch k records; SQUINT_GEMM_DBG=all: every launch gets its own
     // 64-tile slot (launch i at slot i % 256), for whole-update kernel-span timelines.
     static const char* dbg_env = getenv("SQUINT_GEMM_DBG");
-    static const char* nomma = getenv("SQUINT_GEMM_NOMMA");  // timing experiments only
-    b.dbg_nomma = nomma ? atoi(nomma) : 0;
     static int launch_no = 0;
     if (dbg_env) {
       const int me = launch_no++;
@@ -1498,8 +1490,7 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   int na = 0;
-  static const bool no_pdl = getenv("SQUINT_NO_PDL") != nullptr;
-  if (g_pdl && !no_pdl) {
+  if (g_pdl) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;

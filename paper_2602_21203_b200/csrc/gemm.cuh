@@ -66,6 +66,7 @@ struct GProb {
   const bf16* y;   // GE_RELU_MASK: mask source (ld = ldy)
   int ldy;
   float* part;     // bwd LN: column partial sums [mtile][3][N] = (sum dx, sum dn xh, sum dn)
+  int64_t part_cap;  // floats available at `part` (gemm_launch rejects a plan that would overrun it)
   // tanh-Gaussian (A = action dim)
   const float* eps;     // [M][A]
   float* act;           // [M][A] fp32 action (may be NULL)
@@ -87,6 +88,9 @@ struct GProb {
 };
 
 constexpr int kGemmMaxProb = 8;
+// largest split-K cluster gemm_launch plans (k_gemm_sk): LayerNorm column partials of a split-K
+// launch take kGemmMaxSplitK * mtiles * 3 * N floats
+constexpr int kGemmMaxSplitK = 8;
 constexpr int kGemmMaxMaps = 64;
 
 struct GBatch {
@@ -103,7 +107,6 @@ struct GBatch {
   int prefetch_b;  // 1: B operands may be loaded before griddepcontrol.wait (not written by the
                    // immediately preceding kernel); set through GemmBuilder::prefetch_b
   unsigned long long* dbg;  // optional per-CTA phase timestamps (globaltimer ns) [tile][16]
-  int dbg_nomma;            // with dbg: skip the MMAs (timing experiments; results invalid)
 };
 
 // Host-side builder: operands are registered as Mats; maps are created per use.

@@ -162,16 +162,7 @@ __global__ void __launch_bounds__(256) k_metrics(const __grid_constant__ Metrics
   grid_trigger();
   __shared__ float red[32];
   float lpi = 0.f, q = 0.f, gs = 0.f;
-  if (a.reduce_local && a.q_heads) {
-    const float alpha1 = a.scal[S_ALPHA1];
-    for (int i = threadIdx.x; i < a.B; i += blockDim.x) {
-      const float qm = 0.5f * (a.q_heads[i] + a.q_heads[a.B + i]);
-      lpi += (alpha1 * a.logp[i] - qm) * a.inv_btotal;
-      q += qm;
-    }
-    lpi = block_sum(lpi, red);
-    q = block_sum(q, red);
-  } else if (a.reduce_local) {
+  if (a.reduce_local) {
     for (int i = threadIdx.x; i < a.B; i += blockDim.x) {
       lpi += a.row_lpi[i];
       q += a.row_q[i];

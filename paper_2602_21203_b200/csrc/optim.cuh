@@ -91,10 +91,6 @@ struct MetricsArgs {
   int npart;             // number of Adam partial sums of squares (0 -> kAdamBlocks)
   int reduce_local;      // 1: sum row_lpi/row_q here; 0: read pre-reduced sums from extras2
   const float* extras2;  // [2] = (sum row_lpi, sum row_q) when reduce_local == 0
-  // optional (reduce_local): per-head Q_i [2][B] from the fused actor-loss epilogue; then
-  // row_q = (Q_1 + Q_2) / 2 and row_lpi = (alpha+ log pi - row_q) / B_total are formed here
-  const float* q_heads;
-  const float* logp;     // [B] log pi (current state)
 };
 int launch_metrics(const MetricsArgs& a, cudaStream_t s);
 int launch_lpi_sums(const float* row_lpi, const float* row_q, int B, float* out2, cudaStream_t s);

@@ -39,6 +39,11 @@ namespace {
 inline int ldp(int x) { return (x + 63) & ~63; }
 inline int mtiles(int m) { return (m + 127) / 128; }
 
+struct FB {  // fp32 buffer inside the workspace
+  size_t off;
+  int64_t n;  // floats
+};
+
 struct BM {  // bf16 matrix inside the workspace
   size_t off;
   int rows, cols, ld;
@@ -59,8 +64,8 @@ struct BfLay {
   BM dlog, dlog1;  // [2B][N] (head i = rows i*B ...)
   BM dA2c[2], dA1c[2], dA2a[2], dA1a[2], dAp, dh, dO, adA2, adA1, adAp;
   size_t R1ac, R2ac, Rpq, Rpp, Rpq1, qR1[2], qR2[2], q1R1[2], q1R2[2];
-  size_t tlogits, logits, logits1, m, tgo_ac, a_cur, logp_cur, logp_next, row_loss, row_q, row_lpi, q_heads;
-  size_t part_q2[2], part_q1[2], part_pq, part_a2, part_a1, part_pp;
+  size_t tlogits, logits, logits1, m, tgo_ac, a_cur, logp_cur, logp_next, row_loss, row_q, row_lpi;
+  FB part_q2[2], part_q1[2], part_pq, part_a2, part_a1, part_pp;  // LayerNorm column partials
   size_t grad_critic, grad_actor, adam_part, scal, lpi_sums;
   size_t y1b, img0, dA1enc, enc_part, wtiles;
   ShadowPlan sh[3];  // critic, target, actor
@@ -116,6 +121,8 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
     return m;
   };
   auto fl = [&](size_t n) { return P.take(n * f); };
+  // column partials [mtiles * ks][3][N]: room for the largest split-K cluster gemm_launch plans
+  auto fb = [&](size_t n) { return FB{P.take(kGemmMaxSplitK * n * f), (int64_t)(kGemmMaxSplitK * n)}; };
   w.Xh = bm(B, F);
   w.Xhn = bm(B, F);
   w.Xq = bm(B, nq);
@@ -181,16 +188,15 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
   w.row_loss = fl(B);
   w.row_q = fl(B);
   w.row_lpi = fl(B);
-  w.q_heads = fl(2 * B);
   const size_t mt = mtiles(B);
   for (int i = 0; i < 2; ++i) {
-    w.part_q2[i] = fl(mt * 3 * Hc);
-    w.part_q1[i] = fl(mt * 3 * Hc);
+    w.part_q2[i] = fb(mt * 3 * Hc);
+    w.part_q1[i] = fb(mt * 3 * Hc);
   }
-  w.part_pq = fl(4 * mt * 3 * Lt);
-  w.part_a2 = fl(mt * 3 * Ha);
-  w.part_a1 = fl(mt * 3 * Ha);
-  w.part_pp = fl(4 * mt * 3 * Lt);
+  w.part_pq = fb(mt * 3 * Lt);
+  w.part_a2 = fb(mt * 3 * Ha);
+  w.part_a1 = fb(mt * 3 * Ha);
+  w.part_pp = fb(mt * 3 * Lt);
   w.grad_critic = fl(L.gsize[SQUINT_GROUP_CRITIC] + kExtra);
   w.grad_actor = fl(L.gsize[SQUINT_GROUP_ACTOR] + kExtra);
   w.adam_part = fl(kAdamBlocks + kEncAdamBlocks);
@@ -248,6 +254,7 @@ struct Ctx {
   Mat mat(const BM& m) const { return Mat{ws + m.off, m.rows, m.cols, m.ld}; }
   bf16* bp(const BM& m) const { return reinterpret_cast<bf16*>(ws + m.off); }
   float* F(size_t off) const { return reinterpret_cast<float*>(ws + off); }
+  float* F(const FB& b) const { return reinterpret_cast<float*>(ws + b.off); }
   // head i of a [2B][N] matrix
   Mat half(const BM& m, int i) const {
     return Mat{ws + m.off + (size_t)i * (m.rows / 2) * m.ld * 2, m.rows / 2, m.cols, m.ld};
@@ -337,7 +344,7 @@ GProb& dw(GemmBuilder& gb, const Mat& D, const Mat& X, const LinG& G, int nin) {
   p.dbeta = G.beta;
   return p;
 }
-void bwd_ln(GProb& p, const Lin& W, bf16* xh, int ldx, float* rstd, bf16* out, int ldo, float* part) {
+void bwd_ln(GProb& p, const Lin& W, bf16* xh, int ldx, float* rstd, bf16* out, int ldo, float* part, int64_t part_cap) {
   p.g = W.g;
   p.beta = W.beta;
   p.xh = xh;
@@ -346,6 +353,7 @@ void bwd_ln(GProb& p, const Lin& W, bf16* xh, int ldx, float* rstd, bf16* out, i
   p.out = out;
   p.ldo = ldo;
   p.part = part;
+  p.part_cap = part_cap;
 }
 
 Mat none_mat() { return Mat{nullptr, 0, 0, 0}; }
@@ -761,7 +769,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
       for (int i = 0; i < 2; ++i) {
         GProb& p = dx(gb, c.half(w.dlog, i), cq[i].l3.w, 0, Hc, GE_BWD_LN_RELU);
         bwd_ln(p, cq[i].l2, c.bp(w.qXH2[i]), w.qXH2[i].ld, c.F(w.qR2[i]), c.bp(w.dA2c[i]), w.dA2c[i].ld,
-               c.F(w.part_q2[i]));
+               c.F(w.part_q2[i]), w.part_q2[i].n);
       }
       BF_CK(gemm_launch(gb, s));
     }
@@ -770,7 +778,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
       for (int i = 0; i < 2; ++i) {
         GProb& p = dx(gb, c.mat(w.dA2c[i]), cq[i].l2.w, 0, Hc, GE_BWD_LN_RELU);
         bwd_ln(p, cq[i].l1, c.bp(w.qXH1[i]), w.qXH1[i].ld, c.F(w.qR1[i]), c.bp(w.dA1c[i]), w.dA1c[i].ld,
-               c.F(w.part_q1[i]));
+               c.F(w.part_q1[i]), w.part_q1[i].n);
       }
       BF_CK(gemm_launch(gb, s));
     }
@@ -780,7 +788,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
       GemmBuilder gb(1);
       GProb& p = dx(gb, c.mat(w.dA1c[0]), cq[0].l1.w, 0, Lt, GE_BWD_LN_TANH);
       gb.seg(p, c.mat(w.dA1c[1]), 0, 0, cq[1].l1.w, 1, 0, Hc);
-      bwd_ln(p, cproj, c.bp(w.XHpq), w.XHpq.ld, c.F(w.Rpq), c.bp(w.dAp), w.dAp.ld, c.F(w.part_pq));
+      bwd_ln(p, cproj, c.bp(w.XHpq), w.XHpq.ld, c.F(w.Rpq), c.bp(w.dAp), w.dAp.ld, c.F(w.part_pq), w.part_pq.n);
       BF_CK(gemm_launch(gb, s));
       ks_pq = gb.b.ks;  // split-K launch: column partials per 128 / ks rows
     }
@@ -860,8 +868,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     // on the branch, leave SMs to the critic dW GEMM and the actor-loss launches beside it at the
     // c2 batch (swept: 80 of 148 best at B = 512); at large batches (c3 on one GPU, B = 4096) the
     // branch is the longer path and takes every SM (148: +15 % updates/s over 80)
-    static const int bwd_env = getenv("SQUINT_ENC_BWD_CTAS") ? atoi(getenv("SQUINT_ENC_BWD_CTAS")) : 0;
-    const int bwd_ctas = bwd_env > 0 ? bwd_env : (B <= 1024 ? 80 : 148);
+    const int bwd_ctas = B <= 1024 ? 80 : 148;
     e.max_ctas = branch ? bwd_ctas : 0;
     BF_CK(launch_enc_bwd_tc(e, es));
   }
@@ -915,8 +922,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
       if (pipe && next) {
         // the next update's critic-side forward, beside this update's actor pass (encoder grid
         // capped so the main stream's launches keep SMs)
-        static const int fwd_ctas = getenv("SQUINT_ENC_FWD_CTAS") ? atoi(getenv("SQUINT_ENC_FWD_CTAS")) : 74;
-        squint_status r = early_fwd(c, w_in, hp, R, *next, st, par ^ 1, es, fwd_ctas, c.aux->enc, c.aux->chn);
+        squint_status r = early_fwd(c, w_in, hp, R, *next, st, par ^ 1, es, 74, c.aux->enc, c.aux->chn);
         if (r != SQUINT_OK) return r;
       }
     } else {
@@ -925,12 +931,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
                                s, 0, kAdamBlocks, 1));
     }
   }
-  // a12: actor loss against theta+ on sg(h) (Q19).  SQUINT_FUSE_Q=1 (single GPU, chains): the
-  // actor-Q step (softmax, Q_i, dL_pi/dl) runs in the theta+ chain's last layer instead of
-  // k_actor_q -- off by default: the cross-CTA softmax exchange waits for the cluster's slowest
-  // CTA and measured ~2 us slower per update than the separate kernel
-  static const bool fuse_env = getenv("SQUINT_FUSE_Q") != nullptr;
-  const bool fuse_q = fuse_env && c.chain && comm == nullptr && d.critic_kind == SQUINT_CRITIC_C51;
+  // a12: actor loss against theta+ on sg(h) (Q19)
   {
     PhaseScope ps(12, rep, s);
     const Lin cproj1 = proj(c, w.sh[0], crit, gC, "critic");  // same buffers, now theta+
@@ -951,14 +952,6 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
         l3.bias = cq1[i].l3.b;
         l3.outf = c.F(w.logits1) + (size_t)i * B * N;
         l3.ldf = N;
-        if (fuse_q) {  // k_actor_q's work in the chain's last layer (Q25)
-          l3.q_out = c.F(w.q_heads) + (size_t)i * B;
-          l3.dq = c.halfp(w.dlog1, i);
-          l3.ld_dq = w.dlog1.ld;
-          l3.v_min = d.v_min;
-          l3.v_max = d.v_max;
-          l3.q_scale = -0.5f * inv_btotal;
-        }
       }
       BF_CK(chain_launch(cb, s));
     } else {
@@ -1003,10 +996,8 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     q.ld_dl = w.dlog1.ld;
     q.row_q = c.F(w.row_q);
     q.row_lpi = c.F(w.row_lpi);
-    if (!fuse_q) {
-      if (branch) BF_CK(cudaStreamWaitEvent(s, c.aux->alpha, 0));  // alpha+ from the branch
-      BF_CK(launch_actor_q(q, s));
-    }
+    if (branch) BF_CK(cudaStreamWaitEvent(s, c.aux->alpha, 0));  // alpha+ from the branch
+    BF_CK(launch_actor_q(q, s));
     if (branch) BF_CK(cudaEventRecord(c.aux->qdone, s));  // the metrics run on the branch
   }
   {
@@ -1030,7 +1021,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
       for (int i = 0; i < 2; ++i) {
         GProb& p = dx(gb, c.half(w.dlog1, i), cq1[i].l3.w, 0, Hc, GE_BWD_LN_RELU);
         bwd_ln(p, cq1[i].l2, c.bp(w.q1XH2[i]), w.q1XH2[i].ld, c.F(w.q1R2[i]), c.bp(w.dA2a[i]), w.dA2a[i].ld,
-               nullptr);
+               nullptr, 0);
       }
       BF_CK(gemm_launch(gb, s));
     }
@@ -1039,7 +1030,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
       for (int i = 0; i < 2; ++i) {
         GProb& p = dx(gb, c.mat(w.dA2a[i]), cq1[i].l2.w, 0, Hc, GE_BWD_LN_RELU);
         bwd_ln(p, cq1[i].l1, c.bp(w.q1XH1[i]), w.q1XH1[i].ld, c.F(w.q1R1[i]), c.bp(w.dA1a[i]), w.dA1a[i].ld,
-               nullptr);
+               nullptr, 0);
       }
       BF_CK(gemm_launch(gb, s));
     }
@@ -1052,7 +1043,6 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
       p.tgo = c.F(w.tgo_ac);
       p.eps = eps_cur;
       p.dlogp_scale = scal + S_ALPHA1_SCALE;
-      if (fuse_q && branch) BF_CK(cudaStreamWaitEvent(s, c.aux->alpha, 0));  // alpha+ from the branch
       p.lo = hp.log_std_min;
       p.hi = hp.log_std_max;
       p.out = c.bp(w.dO);
@@ -1071,20 +1061,20 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     {
       GemmBuilder gb(1);
       GProb& p = dx(gb, c.mat(w.dO), am.l3.w, 0, Ha, GE_BWD_LN_RELU);
-      bwd_ln(p, am.l2, c.bp(w.XH2ac), w.XH2ac.ld, c.F(w.R2ac), c.bp(w.adA2), w.adA2.ld, c.F(w.part_a2));
+      bwd_ln(p, am.l2, c.bp(w.XH2ac), w.XH2ac.ld, c.F(w.R2ac), c.bp(w.adA2), w.adA2.ld, c.F(w.part_a2), w.part_a2.n);
       BF_CK(gemm_launch(gb, s));
     }
     {
       GemmBuilder gb(1);
       GProb& p = dx(gb, c.mat(w.adA2), am.l2.w, 0, Ha, GE_BWD_LN_RELU);
-      bwd_ln(p, am.l1, c.bp(w.XH1ac), w.XH1ac.ld, c.F(w.R1ac), c.bp(w.adA1), w.adA1.ld, c.F(w.part_a1));
+      bwd_ln(p, am.l1, c.bp(w.XH1ac), w.XH1ac.ld, c.F(w.R1ac), c.bp(w.adA1), w.adA1.ld, c.F(w.part_a1), w.part_a1.n);
       BF_CK(gemm_launch(gb, s));
     }
     }
     {
       GemmBuilder gb(1);
       GProb& p = dx(gb, c.mat(w.adA1), am.l1.w, 0, Lt, GE_BWD_LN_TANH);
-      bwd_ln(p, aproj, c.bp(w.XHpp), w.XHpp.ld, c.F(w.Rpp), c.bp(w.adAp), w.adAp.ld, c.F(w.part_pp));
+      bwd_ln(p, aproj, c.bp(w.XHpp), w.XHpp.ld, c.F(w.Rpp), c.bp(w.adAp), w.adAp.ld, c.F(w.part_pp), w.part_pp.n);
       BF_CK(gemm_launch(gb, s));
       ks_pp = gb.b.ks;
     }
@@ -1130,10 +1120,6 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     m.inv_btotal = inv_btotal;
     m.row_lpi = c.F(w.row_lpi);
     m.row_q = c.F(w.row_q);
-    if (fuse_q) {
-      m.q_heads = c.F(w.q_heads);
-      m.logp = c.F(w.logp_cur);
-    }
     m.sumsq_part = c.F(w.adam_part);
     m.scal = scal;
     m.extras = extras;
@@ -1152,10 +1138,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
 
 }  // namespace
 
-bool bf16_prepare() {
-  static const bool no_branch = getenv("SQUINT_NO_BRANCH") != nullptr;
-  return !no_branch && g_branch_enabled && t_aux.ok();
-}
+bool bf16_prepare() { return g_branch_enabled && t_aux.ok(); }
 int bf16_options() { return g_branch_enabled | (g_pipe_enabled << 1); }
 
 size_t bf16_workspace_bytes(const squint_dims& d) {
@@ -1197,12 +1180,9 @@ squint_status bf16_update(const squint_dims& d, const squint_hparams& hp, const 
   Layout L = make_layout(d);
   BfLay w = plan_bf(d, L);
   if (workspace_bytes < w.total) return set_error(SQUINT_EINVAL, "workspace too small (see squint_workspace_bytes)");
-  static const bool no_chain = getenv("SQUINT_NO_CHAIN") != nullptr;
-  static const bool bwd_chain = getenv("SQUINT_BWD_CHAIN") != nullptr;
-  const bool chain_ok = !no_chain && chain_supported(d.critic_hidden) && chain_supported(d.actor_hidden);
-  static const bool no_branch = getenv("SQUINT_NO_BRANCH") != nullptr;
-  Ctx c{d, L, reinterpret_cast<char*>(workspace), s, chain_ok, chain_ok && bwd_chain,
-        (!no_branch && g_branch_enabled && t_aux.ok()) ? &t_aux : nullptr};
+  const bool chain_ok = chain_supported(d.critic_hidden) && chain_supported(d.actor_hidden);
+  Ctx c{d, L, reinterpret_cast<char*>(workspace), s, chain_ok, false,
+        (g_branch_enabled && t_aux.ok()) ? &t_aux : nullptr};
   const int nranks = comm ? comm_nranks(comm) : 1;
   const float inv_btotal = 1.0f / ((float)d.batch * (float)nranks);
   // bf16 shadows of the current master weights (and the conv weight tiles, which with the
@@ -1218,8 +1198,7 @@ squint_status bf16_update(const squint_dims& d, const squint_hparams& hp, const 
                               reinterpret_cast<uint8_t*>(c.ws + w.wtiles), s));
   }
   const size_t B = d.batch, A = d.action_dim;
-  static const bool env_pipe = getenv("SQUINT_PIPE") != nullptr;
-  const bool pipe = (env_pipe || g_pipe_enabled) && comm == nullptr && c.aux != nullptr && c.chain;
+  const bool pipe = g_pipe_enabled && comm == nullptr && c.aux != nullptr && c.chain;
   auto in = [&](int j) { return UpdIn{idx + j * B, shifts + j * B * 4, eps + j * 2 * B * A, j}; };
   if (pipe) {
     const UpdIn u0 = in(0);
@@ -1305,8 +1284,7 @@ squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const flo
     fwd(gb, c.mat(Xh), ap, GE_LN_TANH, c.bp(Xa), Xa.ld, hp.ln_eps);
     BF_CK(gemm_launch(gb, s));
   }
-  static const bool no_chain = getenv("SQUINT_NO_CHAIN") != nullptr;
-  if (!no_chain && chain_supported(Ha)) {
+  if (chain_supported(Ha)) {
     // the whole actor MLP + tanh-Gaussian head in one fused chain launch
     ChainBuilder cb(1);
     CProb& pa = cb.add(M, c.mat(Xa));
@@ -1384,6 +1362,11 @@ extern "C" SQUINT_API squint_status squint_set_option(int key, int value) {
   }
   if (key == 3) {
     sq::g_check_enabled = value != 0;
+    return SQUINT_OK;
+  }
+  if (key == 4) {
+    if (value < 0 || value > 3) return sq::set_error(SQUINT_EINVAL, "option 4: value must be 0..3");
+    sq::g_emul = value;
     return SQUINT_OK;
   }
   return sq::set_error(SQUINT_EINVAL, "unknown option");

@@ -24,6 +24,7 @@ squint_status bf16_update(const squint_dims& d, const squint_hparams& hp, const 
 bool bf16_prepare();
 int bf16_options();  // squint_set_option state (part of the update graph cache key)
 extern int g_check_enabled;  // squint_set_option key 3
+extern int g_emul;           // squint_set_option key 4 (api.cu)
 bool instrumentation_active();  // instrument.cu: launch / phase events requested
 size_t bf16_act_workspace_bytes(const squint_dims& d, int64_t n);
 squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const float* actor_params,
