@@ -7,11 +7,20 @@ One step = one Algorithm-1 iteration at BASELINE configs[2]:
                replay ring's obs rows: a16 + a1),
   squint_update with UTD 4 at batch 512 (a2-a15), 101 atoms on [-20, 20].
 (--act-full: the act squints a second 128x128 batch itself, the insert writes next_obs only.)
-value = updates/s summed over ranks (weak scaling: every rank owns a 512-sample shard of
-the 512*N global batch; gradients are NCCL all-reduced).  Inputs live in HBM before the
-timed region; the replay ring (1.66 GB per rank) and four rotating 50 MB frame pools
-exceed the 126 MB L2.  Launch: python bench.py [--gpus N --steps K --warmup W]
-(torchrun for N > 1).  --impl reference times the CPU oracle instead (rank 0 only).
+
+value = optimizer updates/s of the GLOBAL batch (UTD * K / time).  With N > 1 ranks (torchrun)
+the global batch is split: --config c2 (default) keeps the metric's "batch 512" and gives each rank
+512 / N samples and 1024 / N environments (SURVEY §8(d) c3'); --config c3 splits BJ configs[3]'s
+global batch 4096 into 4096 / N.  Gradients are NCCL all-reduced (Q33); every rank samples its own
+seeded indices from its replica of the ring.  Scaling is therefore "strong"; samples/s =
+value * global batch is reported beside it.  Inputs live in HBM before the timed region; the
+replay ring (1.66 GB per rank) and four rotating 50 MB frame pools exceed the 126 MB L2.
+
+Beside the headline line's step, rank 0 times the other BJ configs (keys of the same JSON line):
+c1 (squint insert of 1024 frames into the 1M ring, µs/call, GB/s against HBM), c4 (rollout act on
+4096 128x128 frames: latency, frames/s, GB/s) and, at N = 1, c3 (the large-batch update on one GPU:
+updates/s and its dominant kernel's tensor roofline).  Launch: python bench.py [--gpus N --steps K
+--warmup W] (torchrun for N > 1).  --impl reference times the CPU oracle instead (rank 0 only).
 """
 from __future__ import annotations
 
@@ -110,7 +119,7 @@ def run_reference(args):
               f"({args.config} shapes), float64 NumPy")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "c2 update share of an Algorithm-1 step (CPU oracle)" + variant(args)[2],
                        "global_batch": variant(args)[0]["batch"],
                        "utd": 1, "n_env_frames": N_ENV // UTD},
@@ -178,6 +187,12 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=dev)
     precision = {"fp32": P.FP32, "bf16": P.BF16}[args.precision]
     d, hp, vlabel = variant(args)
+    # the global batch (configs[2]: 512, configs[3]: 4096) and the environments are split over ranks
+    gbatch = d["batch"]
+    if gbatch % world or N_ENV % world:
+        raise SystemExit(f"global batch {gbatch} / {N_ENV} envs not divisible by {world} ranks")
+    d["batch"] = gbatch // world
+    n_env = N_ENV // world
     B, A = d["batch"], d["action_dim"]
     cap = args.capacity or SI.CONFIGS[args.config]["capacity"]
     K, W = args.steps, args.warmup
@@ -213,9 +228,9 @@ def run_gpu(args):
     idx_all = torch.randint(0, cap, (T, UTD, B), generator=gi, device=dev, dtype=torch.int64)
     sh_all = torch.randint(0, 2 * d["pad"] + 1, (T, UTD, B, 4), generator=gi, device=dev, dtype=torch.uint8)
     eps_all = torch.randn((T, UTD, 2, B, A), generator=gi, device=dev)
-    aeps_all = torch.randn((T, N_ENV, A), generator=gi, device=dev)
-    prop_all = torch.randn((T, N_ENV, d["proprio_dim"]), generator=gi, device=dev)
-    slots_all = torch.stack([(torch.arange(N_ENV, device=dev) + k * N_ENV) % cap for k in range(T)])
+    aeps_all = torch.randn((T, n_env, A), generator=gi, device=dev)
+    prop_all = torch.randn((T, n_env, d["proprio_dim"]), generator=gi, device=dev)
+    slots_all = torch.stack([(torch.arange(n_env, device=dev) + k * n_env) % cap for k in range(T)])
     # rotating pools of rendered frames o_{t+1} (4 x 50 MB > L2).  Algorithm 1 reads each new
     # observation once: squint_insert2 squints o_{t+1} into the finished transition's
     # next_obs row and into a 16x16 staging buffer that the next step's act encodes (factor 1),
@@ -223,22 +238,22 @@ def run_gpu(args):
     # squints a second frame batch itself; the insert writes next_obs only).
     NPOOL = 4
     hwc = args.insert.startswith("hwc")
-    pools = [torch.as_tensor(SI.make_frames(N_ENV, 128, seed=20 + p)).to(dev) for p in range(NPOOL)]
+    pools = [torch.as_tensor(SI.make_frames(n_env, 128, seed=20 + p)).to(dev) for p in range(NPOOL)]
     if hwc:  # what renderers emit (f4)
         pools = [x.permute(0, 2, 3, 1).contiguous() for x in pools]
-    jit = torch.as_tensor(SI.make_jitter(N_ENV)).to(dev) if args.insert.endswith("jitter") else None
-    act_pool = [torch.as_tensor(SI.make_frames(N_ENV, 128, seed=10 + p)).to(dev) for p in range(NPOOL)] \
+    jit = torch.as_tensor(SI.make_jitter(n_env)).to(dev) if args.insert.endswith("jitter") else None
+    act_pool = [torch.as_tensor(SI.make_frames(n_env, 128, seed=10 + p)).to(dev) for p in range(NPOOL)] \
         if args.act_full else None
-    stage = [torch.empty((N_ENV, 3, 16, 16), dtype=torch.uint8, device=dev) for _ in range(2)]
-    stage_slots = torch.arange(N_ENV, device=dev, dtype=torch.int64)
+    stage = [torch.empty((n_env, 3, 16, 16), dtype=torch.uint8, device=dev) for _ in range(2)]
+    stage_slots = torch.arange(n_env, device=dev, dtype=torch.int64)
     NG = NPOOL  # graphs: pool j % NPOOL, staging parity j % 2 (NPOOL even)
     # static per-step buffers that the graphs read
     idx_s, sh_s, eps_s = idx_all[0].clone(), sh_all[0].clone(), eps_all[0].clone()
     aeps_s, prop_s, slots_s = aeps_all[0].clone(), prop_all[0].clone(), slots_all[0].clone()
     metrics = torch.zeros((UTD, 8), device=dev)
-    act_out = torch.zeros((N_ENV, A), device=dev)
-    logp_out = torch.zeros((N_ENV,), device=dev)
-    act_ws = torch.zeros(P.act_workspace_bytes(L.dims, N_ENV), dtype=torch.uint8, device=dev)
+    act_out = torch.zeros((n_env, A), device=dev)
+    logp_out = torch.zeros((n_env,), device=dev)
+    act_ws = torch.zeros(P.act_workspace_bytes(L.dims, n_env), dtype=torch.uint8, device=dev)
     obs_ring = R["obs"]
     next_ring = R["next_obs"]
     def insert_new(frames, slots, stage_dst, stream=None):
@@ -346,30 +361,10 @@ def run_gpu(args):
     # The timeline capture runs the update on one stream (no encoder-backward branch); events
     # between kernels add small gaps and stop programmatic-launch overlap, so these durations
     # are pessimistic; shares are taken against their own sum.
-    kern = {}
+    kern, event_overhead_us = {}, None
     if use_graph and not args.no_timeline:
-        tl = S.LaunchTimeline(4096)
-        s2 = torch.cuda.Stream(device=dev)
-        s2.wait_stream(torch.cuda.current_stream())
-        event_overhead_us = tl.calibrate(s2)
-        gtl = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(s2):
-            tl.start()
-        with torch.cuda.graph(gtl, stream=s2):
-            step(0, stream=s2)
-            tl.stop(s2)
-        torch.cuda.synchronize()
-        R = 10
-        for r in range(R):
-            load_inputs(W + (r % K))
-            gtl.replay()
-            torch.cuda.synchronize()
-            for name, fl, by, us in tl.durations():
-                e = kern.setdefault(name, {"us": 0.0, "n": 0, "flops": 0.0, "bytes": 0.0})
-                e["us"] += us / R
-                e["n"] += 1.0 / R
-                e["flops"] += fl / R
-                e["bytes"] += by / R
+        kern, event_overhead_us = timeline(S, torch, dev, lambda st: step(0, stream=st), reps=10,
+                                           load=lambda r: load_inputs(W + (r % K)))
 
     # e2e: the environment loop through the public API from pinned host buffers.  Step t acts on
     # o_t (squinted by step t-1's insert2), reads the actions back, uploads the new observation
@@ -473,7 +468,7 @@ def run_gpu(args):
             ems = float(t.item())
         h2d = h_fr[0].numel() + h_pack[0].numel()
         d2h = sum(x.numel() * x.element_size() for x in h_out)
-        e2e = {"value": world * UTD * K / (ems / 1e3), "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": UTD * K / (ems / 1e3), "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / K, "host_enqueue_ms_per_step": host_ms,
                "loop": ("act(o_t) -> D2H actions -> H2D o_{t+1} (copy streams, beside the act and the updates) -> "
                         + ("insert(o_{t+1}) after the updates" if args.act_full else
@@ -484,54 +479,225 @@ def run_gpu(args):
             dist.destroy_process_group()
         return
 
-    # roofline of the dominant kernel (largest device time per step in the timeline)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     traffic_tab = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))) if os.path.exists(
         os.path.join(ROOT, "profiles", "traffic.json")) else {}
-    step_ms = ms / K
-    roof = None
-    if kern:
-        tot_us = sum(e["us"] for e in kern.values())
-        dom = max(kern, key=lambda k: kern[k]["us"])
-        e = kern[dom]
-        t_launch = e["us"] / e["n"] * 1e-6  # seconds per launch
-        if e["flops"] > 0:
-            peak = peaks.get("bf16_tflops_sustained", 1400.0)  # kernel timed inside a long step
-            roof = {"bound": "tensor", "achieved": e["flops"] / e["n"] / t_launch / 1e12, "peak": peak,
-                    "unit": "TFLOP/s", "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (of measured)"}
-        else:
-            peak = peaks.get("hbm_gbs", 6650.0)
-            roof = {"bound": "hbm", "achieved": e["bytes"] / e["n"] / t_launch / 1e9, "peak": peak, "unit": "GB/s",
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
-        roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["traffic"] = traffic_tab.get(dom)
-        roof["kernel"] = dom
-        roof["launches_per_step"] = round(e["n"], 2)
-        roof["us_per_launch"] = e["us"] / e["n"]
-        roof["share_of_step"] = e["us"] / tot_us if tot_us > 0 else None
+    roof = roofline_of(kern, peaks, traffic_tab)
+    if roof:
         roof["timeline_event_overhead_us"] = event_overhead_us
     kernels_us = {k: round(v["us"], 2) for k, v in sorted(kern.items(), key=lambda kv: -kv[1]["us"])}
+    # the other BASELINE configs on this GPU (rank 0): c1 insert, c4 act, c3 update (N = 1)
+    extra = {}
+    if not args.no_sub:
+        extra["c1_insert"] = bench_c1(P, torch, dev, pools, cap, K, W, peaks)
+        extra["c4_act"] = bench_c4(P, torch, dev, L, d, K, W, peaks)
+        if world == 1 and args.config == CFG and args.critic == "c51" and args.target == "avg":
+            extra["c3_update"] = bench_c3(P, S, torch, dev, replay, cap, K, W, peaks, traffic_tab)
     cpu = None
     if world == 1 and not args.no_cpu:
-        ts = [oracle_sample(args, seed=s) for s in range(args.cpu_samples)]
-        cpu = {"value": len(ts) / sum(ts), "unit": "updates/s", "cores": blas_threads(), "kind": "oracle",
-               "sample": f"{len(ts)} x (oracle act+insert on {N_ENV // UTD} frames + 1 update at B={B}), "
-                         f"{sum(ts):.1f} s float64 NumPy"}
-    line = {"metric": METRIC, "value": world * UTD * K / (ms / 1e3), "unit": "updates/s", "n_gpus": world,
-            "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+        cpu = cpu_baseline(args, B)
+    value = UTD * K / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": {P.FP32: "f32", P.BF16: "bf16"}[precision], "data": "synthetic",
-            "config": {"workload": "c2: Algorithm-1 step = insert2(1024 new 128x128 frames) + act(1024 envs) + "
-                                   f"4 updates at B={B} per rank, 101 atoms, {cap:,}-row ring"
-                                   + (" (act squints its own frames)" if args.act_full else "") + vlabel, "global_batch": B * world, "utd": UTD,
+            "samples_per_s": value * gbatch,
+            "config": {"workload": f"{args.config}: Algorithm-1 step = insert2({n_env} new 128x128 frames) + act({n_env} envs) + "
+                                   f"{UTD} updates at global batch {gbatch} ({B} per rank), "
+                                   f"{d['n_atoms']} atoms, {cap:,}-row ring"
+                                   + (" (act squints its own frames)" if args.act_full else "") + vlabel,
+                       "global_batch": gbatch, "batch_per_rank": B, "utd": UTD,
                        "n_env": N_ENV, "parallelism": f"dp{world}", "capacity": cap,
-                       "l2": f"ring {cap * 1662 / 1e9:.2f} GB + rotating frame pools (4 x 50 MB) > L2",
+                       "l2": f"ring {cap * 1662 / 1e9:.2f} GB + rotating frame pools (4 x {n_env * 49152 / 1e6:.0f} MB) > L2",
                        "graph": use_graph},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": int(launches_per_step * K), "kernels_us_per_step": kernels_us}
+    line.update(extra)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def roofline_of(kern, peaks, traffic_tab):
+    """Roofline of the dominant kernel (largest device time per step in a launch timeline)."""
+    if not kern:
+        return None
+    tot_us = sum(e["us"] for e in kern.values())
+    dom = max(kern, key=lambda k: kern[k]["us"])
+    e = kern[dom]
+    t_launch = e["us"] / e["n"] * 1e-6  # seconds per launch
+    if e["flops"] > 0:
+        peak = peaks.get("bf16_tflops_sustained", 1400.0)  # kernel timed inside a long step
+        roof = {"bound": "tensor", "achieved": e["flops"] / e["n"] / t_launch / 1e12, "peak": peak,
+                "unit": "TFLOP/s", "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (of measured)"}
+    else:
+        peak = peaks.get("hbm_gbs", 6650.0)
+        roof = {"bound": "hbm", "achieved": e["bytes"] / e["n"] / t_launch / 1e9, "peak": peak, "unit": "GB/s",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = traffic_tab.get(dom)
+    roof["kernel"] = dom
+    roof["launches_per_step"] = round(e["n"], 2)
+    roof["us_per_launch"] = e["us"] / e["n"]
+    roof["share_of_step"] = e["us"] / tot_us if tot_us > 0 else None
+    return roof
+
+
+def timeline(S, torch, dev, fn, reps=10, load=None):
+    """Per-kernel device time of fn(stream): one graph capture with an event before every libsquint
+    launch, replayed `reps` times (calibrated event overhead subtracted)."""
+    tl = S.LaunchTimeline(4096)
+    s2 = torch.cuda.Stream(device=dev)
+    s2.wait_stream(torch.cuda.current_stream())
+    oh = tl.calibrate(s2)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s2):
+        tl.start()
+    with torch.cuda.graph(g, stream=s2):
+        fn(s2)
+        tl.stop(s2)
+    torch.cuda.synchronize()
+    kern = {}
+    for r in range(reps):
+        if load:
+            load(r)
+        g.replay()
+        torch.cuda.synchronize()
+        for name, fl, by, us in tl.durations():
+            e = kern.setdefault(name, {"us": 0.0, "n": 0, "flops": 0.0, "bytes": 0.0})
+            e["us"] += us / reps
+            e["n"] += 1.0 / reps
+            e["flops"] += fl / reps
+            e["bytes"] += by / reps
+    return kern, oh
+
+
+def _time_graph(torch, fn, K, W, pre=None):
+    """ms per call of fn(j) captured as CUDA graphs (one per rotating input j % 2), CUDA events."""
+    graphs = []
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn(0)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    for j in range(2):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn(j)
+        graphs.append(g)
+    for w in range(W):
+        graphs[w % 2].replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for k in range(K):
+        graphs[k % 2].replay()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / K
+
+
+def bench_c1(P, torch, dev, pools, cap, K, W, peaks):
+    """BJ configs[1]: squint_insert of 1024 frames (50.3 MB, rotating pools > L2) into the 1M ring at
+    seeded distinct random slots.  HBM-bound: 49,152 B read + 768 B written per frame."""
+    n = pools[0].shape[0]
+    ring = torch.zeros((cap, 3, 16, 16), dtype=torch.uint8, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(2)
+    slots = [torch.randperm(cap, generator=g, device=dev)[:n].contiguous() for _ in range(2)]
+    frames = [pools[0], pools[1]]  # 2 x 50 MB alternate (plus the ring rows written)
+    ms = _time_graph(torch, lambda j: P.squint_insert(frames[j], 8, slots[j], ring), 4 * K, W)
+    by = n * (49152 + 768)
+    gbs = by / (ms * 1e-3) / 1e9
+    peak = peaks.get("hbm_gbs", 6650.0)
+    del ring
+    return {"workload": f"c1: squint_insert of {n} frames 3x128x128 -> {cap:,}-row ring (random distinct slots)",
+            "us_per_call": ms * 1e3, "frames_per_s": n / (ms * 1e-3),
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                         "bytes_per_call": by, "floor_us": by / (peak * 1e9) * 1e6,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}}
+
+
+def bench_c4(P, torch, dev, L, d, K, W, peaks):
+    """BJ configs[4]: rollout act on 4096 rendered 3x128x128 frames (201 MB per call; two pools > L2):
+    squint -> encoder -> actor projection + MLP -> tanh-Gaussian sample with seeded noise."""
+    n = 4096
+    g = torch.Generator(device=dev)
+    g.manual_seed(44)
+    frames = [torch.randint(0, 256, (n, 3, 128, 128), generator=g, device=dev, dtype=torch.uint8) for _ in range(2)]
+    prop = torch.randn((n, d["proprio_dim"]), generator=g, device=dev)
+    eps = torch.randn((n, d["action_dim"]), generator=g, device=dev)
+    act = torch.zeros((n, d["action_dim"]), device=dev)
+    lp = torch.zeros((n,), device=dev)
+    ws = torch.zeros(P.act_workspace_bytes(L.dims, n), dtype=torch.uint8, device=dev)
+    ms = _time_graph(torch, lambda j: P.squint_act(L.dims, L.hp, L.actor, L.critic, frames[j], prop, eps, act, lp, ws),
+                     2 * K, W)
+    by = n * 49152
+    gbs = by / (ms * 1e-3) / 1e9
+    peak = peaks.get("hbm_gbs", 6650.0)
+    del frames, ws
+    return {"workload": f"c4: squint_act on {n} frames 3x128x128 (+ proprio, seeded N(0,1) noise) -> actions, log pi",
+            "latency_us": ms * 1e3, "frames_per_s": n / (ms * 1e-3),
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                         "bytes_per_call": by, "floor_us": by / (peak * 1e9) * 1e6,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}}
+
+
+def bench_c3(P, S, torch, dev, replay, cap, K, W, peaks, traffic_tab):
+    """BJ configs[3] on one GPU (G = 1): the update at global batch 4096, C = 64, critic 512-512, 101
+    atoms, on the same 1M-row ring; updates/s and the dominant kernel's tensor roofline."""
+    d = SI.dims_of("c3")
+    hp = SI.hp_of("c3")
+    B, A = d["batch"], d["action_dim"]
+    L3 = P.Learner(d, hp, precision=P.BF16, device=dev, utd=1)
+    from paper_2602_21203_b200 import squint as S_
+    layout3 = [(S_.GROUP_NAMES[g], n, s) for g, n, off, s in L3.layout]
+    L3.load_values(SI.make_params(SI.specs_from_layout(layout3), seed=1))
+    gi = torch.Generator(device=dev)
+    gi.manual_seed(2)
+    idx = [torch.randint(0, cap, (1, B), generator=gi, device=dev, dtype=torch.int64) for _ in range(2)]
+    sh = [torch.randint(0, 2 * d["pad"] + 1, (1, B, 4), generator=gi, device=dev, dtype=torch.uint8) for _ in range(2)]
+    eps = [torch.randn((1, 2, B, A), generator=gi, device=dev) for _ in range(2)]
+    met = torch.zeros((1, 8), device=dev)
+    fn = lambda j, stream=None: L3.update(replay, idx[j], sh[j], eps[j], met, stream=stream)
+    ms = _time_graph(torch, fn, 2 * K, W)
+    kern, oh = timeline(S, torch, dev, lambda st: fn(0, st), reps=5)
+    roof = roofline_of(kern, peaks, traffic_tab)
+    flops = 74.05e9
+    return {"workload": f"c3 on one GPU: update at batch {B}, C {d['conv_ch']}, critic {d['critic_hidden']}-"
+                        f"{d['critic_hidden']}, {d['n_atoms']} atoms, {cap:,}-row ring",
+            "updates_per_s": 1e3 / ms, "ms_per_update": ms,
+            "tflops": flops / (ms * 1e-3) / 1e12, "tensor_frac_of_update": flops / (ms * 1e-3) / 1e12 /
+            peaks.get("bf16_tflops_sustained", 1400.0),
+            "roofline": roof, "kernels_us_per_update": {k: round(v["us"], 2) for k, v in
+                                                        sorted(kern.items(), key=lambda kv: -kv[1]["us"])}}
+
+
+def cpu_baseline(args, B):
+    """The oracle as it stands on this host: BLAS threads = all cores and = 1."""
+    import platform
+    model = platform.processor() or ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    ts = [oracle_sample(args, seed=s) for s in range(args.cpu_samples)]
+    out = {"value": len(ts) / sum(ts), "unit": "updates/s", "cores": blas_threads(), "kind": "oracle",
+           "sample": f"{len(ts)} x (oracle act+insert on {N_ENV // UTD} frames + 1 update at B={B}), "
+                     f"{sum(ts):.1f} s float64 NumPy", "cpu_count": os.cpu_count(), "cpu_model": model}
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1, user_api="blas"):
+            t1 = [oracle_sample(args, seed=s) for s in range(args.cpu_samples)]
+        out["value_1_thread"] = len(t1) / sum(t1)
+    except Exception as e:  # threadpoolctl missing: report why
+        out["value_1_thread"] = None
+        out["note_1_thread"] = str(e)
+    return out
 
 
 def main():
@@ -546,6 +712,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=3)
     ap.add_argument("--no-timeline", action="store_true")
+    ap.add_argument("--no-sub", action="store_true")  # skip the c1 / c4 / c3 side measurements
     ap.add_argument("--act-full", action="store_true")  # round-1 step: act squints its own frame batch
     # f3 / f4 variants (not the headline workload): critic head, target rule, insert input
     ap.add_argument("--critic", default="c51", choices=["c51", "mse"])

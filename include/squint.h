@@ -141,7 +141,9 @@ SQUINT_API squint_status squint_workspace_bytes(const squint_dims* dims, int utd
  *     are stored pixel-major, column pix * C + c (the bf16 encoder's HWC flatten order; the
  *     optimizer gathers them), every other tensor as in squint_param_layout,
  * 2 = target distribution m [B, n_atoms], 3 = h [B, 25C], 4 = log pi (current) [B],
- * 5 = log pi' (next) [B], 6 = actions a~ [B, A], 7 = scalars [16]. */
+ * 5 = log pi' (next) [B], 6 = actions a~ [B, A], 7 = scalars [16],
+ * 8 = the last update's gathered, shifted obs images u8 [B, C, H, W] (a3-a4; the conv1 weight
+ *     gradient's input), 9 = (SQUINT_BF16, with squint_set_option(5, 1)) the same for next_obs. */
 SQUINT_API squint_status squint_workspace_region(const squint_dims* dims, int region, size_t* offset, size_t* bytes);
 
 /* Workspace bytes needed by squint_act for n frames. */
@@ -288,8 +290,9 @@ SQUINT_API int squint_set_launch_events(void** events, int n);
  * capture); key 4 = numerics measurement on the SQUINT_FP32 path only (0, default): round the dense
  * layers' GEMM operands to bf16 before the fp32 multiply-add -- bit 0 the activations / dY, bit 1
  * the weights -- to measure how much of the bf16 path's deviation from the oracle bf16 operand
- * rounding alone explains (reading R-tol-bf16).  Errors: EINVAL for an unknown key or
- * value. */
+ * rounding alone explains (reading R-tol-bf16); key 5 = (SQUINT_BF16, 0 default) the
+ * encoder also stores the gathered, shifted next_obs images into workspace region 9 (test access to
+ * the a3-a4 integer work).  Errors: EINVAL for an unknown key or value. */
 SQUINT_API squint_status squint_set_option(int key, int value);
 /* Records the next timeline event on `stream` without a launch (closes the last interval). */
 SQUINT_API squint_status squint_record_launch_event(squint_stream_t stream);

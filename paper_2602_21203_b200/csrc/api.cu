@@ -755,6 +755,7 @@ squint_status squint_workspace_region(const squint_dims* dims, int region, size_
     case 5: *offset = w.logp_next; *bytes = B * f; break;
     case 6: *offset = w.a_cur; *bytes = B * dims->action_dim * f; break;
     case 7: *offset = w.scal; *bytes = kScal * f; break;
+    case 8: *offset = w.img0; *bytes = B * dims->img_c * dims->img_h * dims->img_w; break;
     default: return fail(SQUINT_EINVAL, "unknown region");
   }
   return SQUINT_OK;

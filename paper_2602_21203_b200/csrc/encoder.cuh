@@ -35,6 +35,8 @@ struct EncFwdArgs {
   float* y1;               // [B, C, P1] conv1 activations of source 0 (NULL: not stored)
   uint8_t* img0;           // [B, c, H, W] shifted images of source 0 (NULL: not stored)
   int C, c_in, H, pad;
+  uint8_t* img1;           // tensor-core path: [B, c, H, W] shifted images of source 1 (debug dump,
+                           // squint_set_option 5; NULL: not stored)
   // bf16 path: h written as bf16 in HWC flatten order hb[src][b * h_ld + pix * C + o]
   // (instead of fp32 CHW h), plus row gathers of the small replay fields per source.
   __nv_bfloat16* hb[2];

@@ -209,7 +209,8 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ 
             wv[k] = acc;
           }
           o = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-          if (src == 0 && a.img0) *reinterpret_cast<uint4*>(a.img0 + (int64_t)b * 768 + cc * 256 + y * 16) = o;
+          uint8_t* dump = src == 0 ? a.img0 : a.img1;
+          if (dump) *reinterpret_cast<uint4*>(dump + (int64_t)b * 768 + cc * 256 + y * 16) = o;
         }
         *reinterpret_cast<uint4*>(xs + i * 768 + cc * 256 + y * 16) = o;
       }

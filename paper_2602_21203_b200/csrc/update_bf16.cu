@@ -67,7 +67,7 @@ struct BfLay {
   size_t tlogits, logits, logits1, m, tgo_ac, a_cur, logp_cur, logp_next, row_loss, row_q, row_lpi;
   FB part_q2[2], part_q1[2], part_pq, part_a2, part_a1, part_pp;  // LayerNorm column partials
   size_t grad_critic, grad_actor, adam_part, scal, lpi_sums;
-  size_t y1b, img0, dA1enc, enc_part, wtiles;
+  size_t y1b, img0, img1, dA1enc, enc_part, wtiles;
   ShadowPlan sh[3];  // critic, target, actor
   size_t total;
 };
@@ -204,6 +204,7 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
   w.lpi_sums = fl(2);
   w.y1b = P.take((size_t)B * P1 * C * 2);
   w.img0 = P.take((size_t)B * d.img_c * d.img_h * d.img_w);
+  w.img1 = P.take((size_t)B * d.img_c * d.img_h * d.img_w);
   w.dA1enc = 0;
   w.enc_part = fl(enc_bwd_tc_partial_floats(C, B));
   w.wtiles = P.take(conv_tiles_bytes(C));
@@ -241,6 +242,8 @@ int g_branch_enabled = 1;
 // default -- on B200 it measured even with the separate forward (the encoder backward that
 // precedes it on the branch and the SMs it occupies set the pace), kept for other shapes
 int g_pipe_enabled = 0;
+// option 5: the encoder also stores the gathered, shifted next_obs images (workspace region 9)
+int g_dump_next = 0;
 
 
 struct Ctx {
@@ -455,6 +458,7 @@ squint_status early_fwd(const Ctx& c, const BfLay& w_in, const squint_hparams& h
     e.h_ld = w.Xh.ld;
     e.y1b = reinterpret_cast<bf16*>(c.ws + w.y1b);
     e.img0 = reinterpret_cast<uint8_t*>(c.ws + w.img0);
+    if (g_dump_next) e.img1 = reinterpret_cast<uint8_t*>(c.ws + w.img1);
     e.C = C;
     e.c_in = d.img_c;
     e.H = d.img_h;
@@ -564,6 +568,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     e.h_ld = w.Xh.ld;
     e.y1b = reinterpret_cast<bf16*>(c.ws + w.y1b);
     e.img0 = reinterpret_cast<uint8_t*>(c.ws + w.img0);
+    if (g_dump_next) e.img1 = reinterpret_cast<uint8_t*>(c.ws + w.img1);
     e.C = C;
     e.c_in = d.img_c;
     e.H = d.img_h;
@@ -1139,7 +1144,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
 }  // namespace
 
 bool bf16_prepare() { return g_branch_enabled && t_aux.ok(); }
-int bf16_options() { return g_branch_enabled | (g_pipe_enabled << 1); }
+int bf16_options() { return g_branch_enabled | (g_pipe_enabled << 1) | (g_dump_next << 2); }
 
 size_t bf16_workspace_bytes(const squint_dims& d) {
   Layout L = make_layout(d);
@@ -1159,6 +1164,8 @@ bool bf16_region(const squint_dims& d, int region, size_t* offset, size_t* bytes
     case 5: *offset = w.logp_next; *bytes = B * f; break;
     case 6: *offset = w.a_cur; *bytes = B * d.action_dim * f; break;
     case 7: *offset = w.scal; *bytes = kScal * f; break;
+    case 8: *offset = w.img0; *bytes = B * d.img_c * d.img_h * d.img_w; break;
+    case 9: *offset = w.img1; *bytes = B * d.img_c * d.img_h * d.img_w; break;
     default: return false;
   }
   return true;
@@ -1362,6 +1369,10 @@ extern "C" SQUINT_API squint_status squint_set_option(int key, int value) {
   }
   if (key == 3) {
     sq::g_check_enabled = value != 0;
+    return SQUINT_OK;
+  }
+  if (key == 5) {
+    sq::g_dump_next = value != 0;
     return SQUINT_OK;
   }
   if (key == 4) {

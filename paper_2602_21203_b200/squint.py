@@ -16,7 +16,8 @@ FP32, BF16 = 0, 1
 GROUP_CRITIC, GROUP_ACTOR, GROUP_ALPHA, GROUP_TARGET = 0, 1, 2, 3
 GROUP_NAMES = {GROUP_CRITIC: "critic", GROUP_ACTOR: "actor", GROUP_ALPHA: "alpha", GROUP_TARGET: "target"}
 STATUS = {0: "OK", 1: "EINVAL", 2: "ESHAPE", 3: "ECUDA", 4: "ENCCL", 5: "EUNSUPPORTED"}
-REGION = {"grad_critic": 0, "grad_actor": 1, "m": 2, "h": 3, "logp": 4, "logp_next": 5, "a_cur": 6, "scal": 7}
+REGION = {"grad_critic": 0, "grad_actor": 1, "m": 2, "h": 3, "logp": 4, "logp_next": 5, "a_cur": 6, "scal": 7,
+          "obs_shifted": 8, "next_obs_shifted": 9}
 
 
 class SquintError(RuntimeError):
@@ -419,6 +420,10 @@ class Learner:
     def region(self, name):
         off, nb = workspace_region(self.dims, name)
         return self.workspace[off:off + nb].view(torch.float32)
+
+    def region_u8(self, name):
+        off, nb = workspace_region(self.dims, name)
+        return self.workspace[off:off + nb]
 
     def update(self, replay: Replay, idx, shifts, eps, metrics, stream=None):
         squint_update(self.dims, self.hp, replay, idx, shifts, eps, self.state, metrics, self.workspace,
