@@ -61,7 +61,7 @@ def test_update_one_rank_comm(comm1, cfg, prec, over):
     for grp in ("critic", "actor", "target"):
         a, b = group_values(L, grp), group_values(L2, grp)
         for n in a:
-            compare(f"comm vs local {grp} {n}", a[n], b[n], 1e-5)
+            compare(f"comm vs local {grp} {n}", a[n], b[n], 1e-4)
 
 
 # ---- a3-a4: gather + random shift, bit-exact ----------------------------------------------------
