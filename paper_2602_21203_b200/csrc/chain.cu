@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
     if (b.dbg && tid == 0 && k < 16) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      b.dbg[blockIdx.x * 16 + k] = t;
+      b.dbg[blockIdx.x * 32 + k] = t;
     }
   };
   stamp(0);
@@ -382,14 +382,37 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
 
 bool chain_supported(int hidden) { return hidden == 256; }
 
+// Instrumentation (SQUINT_CHAIN_DBG, read once): "k" = the k-th chain launch of the process records
+// per-CTA globaltimer stamps; "all" = every launch i records into slot ring entry i % kDbgLaunches.
+// Entry layout: [launch][cta < 64][32 stamps].
 static unsigned long long* g_cdbg = nullptr;
 static int g_cdbg_n = 0;
+constexpr int kDbgLaunches = 64;
 int chain_debug_times(unsigned long long* host, int max_entries) {
   if (!g_cdbg) return 0;
   cudaDeviceSynchronize();
-  const int n = g_cdbg_n * 16 < max_entries ? g_cdbg_n * 16 : max_entries;
+  const int tot = kDbgLaunches * 64 * 32;
+  const int n = (g_cdbg_n > 0 ? g_cdbg_n : tot) < max_entries ? (g_cdbg_n > 0 ? g_cdbg_n : tot) : max_entries;
   cudaMemcpy(host, g_cdbg, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   return n;
+}
+unsigned long long* chain_dbg_for_launch(int nctas) {
+  static const char* env = getenv("SQUINT_CHAIN_DBG");
+  static int no = 0;
+  if (!env) return nullptr;
+  const int me = no++;
+  const size_t tot = (size_t)kDbgLaunches * 64 * 32;
+  if (!g_cdbg) {
+    cudaMalloc(&g_cdbg, tot * sizeof(unsigned long long));
+    cudaMemset(g_cdbg, 0, tot * sizeof(unsigned long long));
+  }
+  if (env[0] == 'a') {
+    g_cdbg_n = 0;
+    return nctas <= 64 ? g_cdbg + (size_t)(me % kDbgLaunches) * 64 * 32 : nullptr;
+  }
+  if (me != atoi(env)) return nullptr;
+  g_cdbg_n = nctas * 32;
+  return g_cdbg;
 }
 
 CProb& ChainBuilder::add(int M, const Mat& A) {
@@ -420,7 +443,7 @@ CLayer& ChainBuilder::layer(CProb& p, int epi, const Mat& W, int b_mn, int N, in
   L.nkb = (K + 63) / 64;
   L.b_mn = b_mn;
   L.ln_eps = 1e-5f;
-  L.slice = (epi == GE_BIAS_F32) ? 32 : (epi == GE_TG_FWD ? 16 : 64);
+  L.slice = row ? ((N + 15) & ~15) : (epi == GE_BIAS_F32) ? 32 : (epi == GE_TG_FWD ? 16 : 64);
   L.omap = L.xmap = -1;
   wmat[pi][l] = W;
   omat[pi][l] = O;
@@ -429,6 +452,7 @@ CLayer& ChainBuilder::layer(CProb& p, int epi, const Mat& W, int b_mn, int N, in
 }
 
 int chain_launch(ChainBuilder& cb, cudaStream_t s) {
+  if (cb.row) return rowchain_launch(cb, s);
   CBatch& b = cb.b;
   if (cb.err || b.nprob == 0) return cb.err ? -1 : 0;
   int nm = 0, ncl = 0;
@@ -464,17 +488,7 @@ int chain_launch(ChainBuilder& cb, cudaStream_t s) {
     }
   }
   b.nclusters = ncl;
-  b.dbg = nullptr;
-  {
-    static const char* env = getenv("SQUINT_CHAIN_DBG");
-    static int no = 0;
-    if (env && no++ == atoi(env)) {
-      if (!g_cdbg) cudaMalloc(&g_cdbg, 1024 * 16 * sizeof(unsigned long long));
-      cudaMemset(g_cdbg, 0, 1024 * 16 * sizeof(unsigned long long));
-      g_cdbg_n = ncl * kCS;
-      b.dbg = g_cdbg;
-    }
-  }
+  b.dbg = chain_dbg_for_launch(ncl * kCS);
   const size_t smem = kSmem + 1024;
   static bool attr = false;
   if (!attr) {

@@ -244,6 +244,9 @@ int g_branch_enabled = 1;
 int g_pipe_enabled = 0;
 // option 5: the encoder also stores the gathered, shifted next_obs images (workspace region 9)
 int g_dump_next = 0;
+// option 6: 0 = row-complete fused chains (k_rowchain, forward and backward), 1 = the 4-CTA cluster
+// chains of round 1 (forward only)
+int g_chain_kind = 0;
 
 
 struct Ctx {
@@ -252,8 +255,9 @@ struct Ctx {
   char* ws;
   cudaStream_t s;
   bool chain;      // fused forward MLP chains (hidden width 256) instead of one launch per layer
-  bool chain_bwd;  // fused backward chains (off by default: measured slower than per-layer launches)
+  bool chain_bwd;  // fused backward chains (row-complete chains only)
   Aux* aux;        // auxiliary branch (NULL: everything on the caller's stream)
+  bool row;        // chains are row-complete (k_rowchain) rather than 4-CTA cluster chains (k_chain)
   Mat mat(const BM& m) const { return Mat{ws + m.off, m.rows, m.cols, m.ld}; }
   bf16* bp(const BM& m) const { return reinterpret_cast<bf16*>(ws + m.off); }
   float* F(size_t off) const { return reinterpret_cast<float*>(ws + off); }
@@ -486,7 +490,7 @@ squint_status early_fwd(const Ctx& c, const BfLay& w_in, const squint_hparams& h
   if (enc_ev) BF_CK(cudaEventRecord(enc_ev, ss));
   {
     PhaseScope ps(6, u.rep, ss);
-    ChainBuilder cb(1);
+    ChainBuilder cb(1, c.row);
     for (int i = 0; i < 2; ++i) {
       CProb& p = cb.add(B, c.mat(w.Xq));
       ch_fwd(cb, p, GE_LN_RELU, cq[i].l1, Hc, nq, c.mat(w.qH1[i]), c.mat(w.qXH1[i]), c.F(w.qR1[i]), le);
@@ -599,7 +603,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   // a7: actor MLP on s' (target sample) and on s (alpha / actor losses)
   if (c.chain) {
     PhaseScope ps(5, rep, s);
-    ChainBuilder cb(1);
+    ChainBuilder cb(1, c.row);
     CProb& pn = cb.add(B, c.mat(w.Xan));
     ch_fwd(cb, pn, GE_LN_RELU, am.l1, Ha, npi, none_mat(), none_mat(), nullptr, le);
     ch_fwd(cb, pn, GE_LN_RELU, am.l2, Ha, Ha, none_mat(), none_mat(), nullptr, le);
@@ -665,7 +669,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   // a8: target heads on (z', s', a~') and online heads on (z, s, a)
   if (c.chain) {
     PhaseScope ps(6, rep, s);
-    ChainBuilder cb(1);
+    ChainBuilder cb(1, c.row);
     for (int i = 0; i < 2; ++i) {
       CProb& p = cb.add(B, c.mat(w.Xt));
       ch_fwd(cb, p, GE_LN_RELU, tq[i].l1, Hc, nq, none_mat(), none_mat(), nullptr, le);
@@ -759,7 +763,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   {
     PhaseScope ps(8, rep, s);
     if (c.chain_bwd) {
-      ChainBuilder cb(1);
+      ChainBuilder cb(1, c.row);
       for (int i = 0; i < 2; ++i) {
         CProb& p = cb.add(B, c.half(w.dlog, i));
         ch_bwd(cb, p, GE_BWD_LN_RELU, cq[i].l3.w, cq[i].l2, Hc, N, c.mat(w.dA2c[i]), c.mat(w.qXH2[i]), c.F(w.qR2[i]),
@@ -948,7 +952,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
       BF_CK(gemm_launch(gb, s));
     }
     if (c.chain) {
-      ChainBuilder cb(1);
+      ChainBuilder cb(1, c.row);
       for (int i = 0; i < 2; ++i) {
         CProb& p = cb.add(B, c.mat(w.Xq1));
         ch_fwd(cb, p, GE_LN_RELU, cq1[i].l1, Hc, nq, none_mat(), c.mat(w.q1XH1[i]), c.F(w.q1R1[i]), le);
@@ -1011,7 +1015,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     const Mlp cq1[2] = {mlp(c, w.sh[0], crit, gC, kHeads[0]), mlp(c, w.sh[0], crit, gC, kHeads[1])};
     (void)cproj1;
     if (c.chain_bwd) {
-      ChainBuilder cb(1);
+      ChainBuilder cb(1, c.row);
       for (int i = 0; i < 2; ++i) {
         CProb& p = cb.add(B, c.half(w.dlog1, i));
         ch_bwd(cb, p, GE_BWD_LN_RELU, cq1[i].l3.w, cq1[i].l2, Hc, N, none_mat(), c.mat(w.q1XH2[i]), c.F(w.q1R2[i]),
@@ -1055,7 +1059,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
       BF_CK(gemm_launch(gb, s));
     }
     if (c.chain_bwd) {
-      ChainBuilder cb(1);
+      ChainBuilder cb(1, c.row);
       CProb& p = cb.add(B, c.mat(w.dO));
       ch_bwd(cb, p, GE_BWD_LN_RELU, am.l3.w, am.l2, Ha, 2 * A, c.mat(w.adA2), c.mat(w.XH2ac), c.F(w.R2ac),
              c.F(w.part_a2));
@@ -1144,7 +1148,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
 }  // namespace
 
 bool bf16_prepare() { return g_branch_enabled && t_aux.ok(); }
-int bf16_options() { return g_branch_enabled | (g_pipe_enabled << 1) | (g_dump_next << 2); }
+int bf16_options() { return g_branch_enabled | (g_pipe_enabled << 1) | (g_dump_next << 2) | (g_chain_kind << 3); }
 
 size_t bf16_workspace_bytes(const squint_dims& d) {
   Layout L = make_layout(d);
@@ -1187,9 +1191,11 @@ squint_status bf16_update(const squint_dims& d, const squint_hparams& hp, const 
   Layout L = make_layout(d);
   BfLay w = plan_bf(d, L);
   if (workspace_bytes < w.total) return set_error(SQUINT_EINVAL, "workspace too small (see squint_workspace_bytes)");
-  const bool chain_ok = chain_supported(d.critic_hidden) && chain_supported(d.actor_hidden);
-  Ctx c{d, L, reinterpret_cast<char*>(workspace), s, chain_ok, false,
-        (g_branch_enabled && t_aux.ok()) ? &t_aux : nullptr};
+  const bool row = g_chain_kind == 0;
+  auto sup = [&](int h) { return row ? rowchain_supported(h) : chain_supported(h); };
+  const bool chain_ok = sup(d.critic_hidden) && sup(d.actor_hidden);
+  Ctx c{d, L, reinterpret_cast<char*>(workspace), s, chain_ok, chain_ok && row,
+        (g_branch_enabled && t_aux.ok()) ? &t_aux : nullptr, row};
   const int nranks = comm ? comm_nranks(comm) : 1;
   const float inv_btotal = 1.0f / ((float)d.batch * (float)nranks);
   // bf16 shadows of the current master weights (and the conv weight tiles, which with the
@@ -1250,7 +1256,8 @@ squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const flo
   BM H2{P.take((size_t)n * ldp(Ha) * 2), M, Ha, ldp(Ha)};
   ShadowPlan sp = shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
   uint8_t* wtiles = reinterpret_cast<uint8_t*>(ws + P.take(conv_tiles_bytes(d.conv_ch)));
-  Ctx c{d, L, ws, s, false, false, nullptr};
+  const bool row = g_chain_kind == 0;
+  Ctx c{d, L, ws, s, false, false, nullptr, row};
   const int gC = SQUINT_GROUP_CRITIC, gA = SQUINT_GROUP_ACTOR;
   std::optional<PhaseScope> ps;
   ps.emplace(1, 0, s);
@@ -1291,9 +1298,9 @@ squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const flo
     fwd(gb, c.mat(Xh), ap, GE_LN_TANH, c.bp(Xa), Xa.ld, hp.ln_eps);
     BF_CK(gemm_launch(gb, s));
   }
-  if (chain_supported(Ha)) {
+  if (row ? rowchain_supported(Ha) : chain_supported(Ha)) {
     // the whole actor MLP + tanh-Gaussian head in one fused chain launch
-    ChainBuilder cb(1);
+    ChainBuilder cb(1, c.row);
     CProb& pa = cb.add(M, c.mat(Xa));
     ch_fwd(cb, pa, GE_LN_RELU, am.l1, Ha, npi, none_mat(), none_mat(), nullptr, hp.ln_eps);
     ch_fwd(cb, pa, GE_LN_RELU, am.l2, Ha, Ha, none_mat(), none_mat(), nullptr, hp.ln_eps);
@@ -1369,6 +1376,10 @@ extern "C" SQUINT_API squint_status squint_set_option(int key, int value) {
   }
   if (key == 3) {
     sq::g_check_enabled = value != 0;
+    return SQUINT_OK;
+  }
+  if (key == 6) {
+    sq::g_chain_kind = value != 0;
     return SQUINT_OK;
   }
   if (key == 5) {
