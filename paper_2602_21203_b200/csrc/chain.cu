@@ -443,7 +443,7 @@ CLayer& ChainBuilder::layer(CProb& p, int epi, const Mat& W, int b_mn, int N, in
   L.nkb = (K + 63) / 64;
   L.b_mn = b_mn;
   L.ln_eps = 1e-5f;
-  L.slice = row ? ((N + 15) & ~15) : (epi == GE_BIAS_F32) ? 32 : (epi == GE_TG_FWD ? 16 : 64);
+  L.slice = (epi == GE_BIAS_F32) ? 32 : (epi == GE_TG_FWD ? 16 : 64);
   L.omap = L.xmap = -1;
   wmat[pi][l] = W;
   omat[pi][l] = O;
@@ -452,7 +452,6 @@ CLayer& ChainBuilder::layer(CProb& p, int epi, const Mat& W, int b_mn, int N, in
 }
 
 int chain_launch(ChainBuilder& cb, cudaStream_t s) {
-  if (cb.row) return rowchain_launch(cb, s);
   CBatch& b = cb.b;
   if (cb.err || b.nprob == 0) return cb.err ? -1 : 0;
   int nm = 0, ncl = 0;

@@ -45,9 +45,6 @@ struct CLayer {
   float* logp;
   float* tgo;
   float lo, hi, ln_eps;
-  // row-complete chains (k_rowchain): forward LayerNorm x_hat stored straight from registers
-  __nv_bfloat16* xh_out;
-  int ld_xh;
 };
 
 constexpr int kChainMaxLayers = 3;
@@ -75,14 +72,10 @@ struct ChainBuilder {
   Mat amat[kChainMaxProb];
   Mat wmat[kChainMaxProb][kChainMaxLayers], omat[kChainMaxProb][kChainMaxLayers], xmat[kChainMaxProb][kChainMaxLayers];
   int err = 0;
-  // row: row-complete chain (k_rowchain, rowchain.cu) -- one CTA per 128-row tile computes whole
-  // rows of every layer (no cluster exchange); otherwise the 4-CTA cluster chain (k_chain)
-  bool row = false;
-  explicit ChainBuilder(int prefetch_b = 1, bool row_ = false) {
+  explicit ChainBuilder(int prefetch_b = 1) {
     b.nprob = 0;
     b.nclusters = 0;
     b.prefetch_b = prefetch_b;
-    row = row_;
   }
   CProb& add(int M, const Mat& A);
   // Layer l of problem p: weight W (K-major [N][K] for forward, MN-major [K][N] for dX), output
@@ -92,10 +85,6 @@ struct ChainBuilder {
 
 // Returns 0 on success, a cudaError_t, or -1 on a planning error (unsupported shape).
 int chain_launch(ChainBuilder& cb, cudaStream_t s);
-int rowchain_launch(ChainBuilder& cb, cudaStream_t s);  // rowchain.cu (cb.row)
-// k_rowchain handles LayerNorm layers of width <= 256 (multiple of 64) and last layers of <= 256
-// columns, with every layer's K <= 256
-bool rowchain_supported(int hidden);
 // The chain handles hidden width 256 (4 x 64-column slices) with K <= 256 per layer.
 bool chain_supported(int hidden);
 int chain_debug_times(unsigned long long* host, int max_entries);

@@ -244,9 +244,6 @@ int g_branch_enabled = 1;
 int g_pipe_enabled = 0;
 // option 5: the encoder also stores the gathered, shifted next_obs images (workspace region 9)
 int g_dump_next = 0;
-// option 6: 0 = row-complete fused chains (k_rowchain, forward and backward), 1 = the 4-CTA cluster
-// chains of round 1 (forward only)
-int g_chain_kind = 0;
 
 
 struct Ctx {
@@ -255,9 +252,7 @@ struct Ctx {
   char* ws;
   cudaStream_t s;
   bool chain;      // fused forward MLP chains (hidden width 256) instead of one launch per layer
-  bool chain_bwd;  // fused backward chains (row-complete chains only)
   Aux* aux;        // auxiliary branch (NULL: everything on the caller's stream)
-  bool row;        // chains are row-complete (k_rowchain) rather than 4-CTA cluster chains (k_chain)
   Mat mat(const BM& m) const { return Mat{ws + m.off, m.rows, m.cols, m.ld}; }
   bf16* bp(const BM& m) const { return reinterpret_cast<bf16*>(ws + m.off); }
   float* F(size_t off) const { return reinterpret_cast<float*>(ws + off); }
@@ -377,17 +372,6 @@ CLayer& ch_fwd(ChainBuilder& cb, CProb& p, int epi, const Lin& W, int N, int K, 
   L.ln_eps = ln_eps;
   return L;
 }
-// a dX = dY W layer with the LayerNorm backward of the layer below (`ln` holds its g, beta)
-CLayer& ch_bwd(ChainBuilder& cb, CProb& p, int epi, const Mat& W, const Lin& ln, int N, int K, const Mat& O,
-               const Mat& X, float* rstd, float* part) {
-  CLayer& L = cb.layer(p, epi, W, 1, N, K, O, X);
-  L.g = ln.g;
-  L.beta = ln.beta;
-  L.rstd = rstd;
-  L.part = part;
-  return L;
-}
-
 #define BF_CK(expr)                                                                                     \
   do {                                                                                                  \
     int _e = (int)(expr);                                                                               \
@@ -490,7 +474,7 @@ squint_status early_fwd(const Ctx& c, const BfLay& w_in, const squint_hparams& h
   if (enc_ev) BF_CK(cudaEventRecord(enc_ev, ss));
   {
     PhaseScope ps(6, u.rep, ss);
-    ChainBuilder cb(1, c.row);
+    ChainBuilder cb(1);
     for (int i = 0; i < 2; ++i) {
       CProb& p = cb.add(B, c.mat(w.Xq));
       ch_fwd(cb, p, GE_LN_RELU, cq[i].l1, Hc, nq, c.mat(w.qH1[i]), c.mat(w.qXH1[i]), c.F(w.qR1[i]), le);
@@ -603,7 +587,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   // a7: actor MLP on s' (target sample) and on s (alpha / actor losses)
   if (c.chain) {
     PhaseScope ps(5, rep, s);
-    ChainBuilder cb(1, c.row);
+    ChainBuilder cb(1);
     CProb& pn = cb.add(B, c.mat(w.Xan));
     ch_fwd(cb, pn, GE_LN_RELU, am.l1, Ha, npi, none_mat(), none_mat(), nullptr, le);
     ch_fwd(cb, pn, GE_LN_RELU, am.l2, Ha, Ha, none_mat(), none_mat(), nullptr, le);
@@ -669,7 +653,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   // a8: target heads on (z', s', a~') and online heads on (z, s, a)
   if (c.chain) {
     PhaseScope ps(6, rep, s);
-    ChainBuilder cb(1, c.row);
+    ChainBuilder cb(1);
     for (int i = 0; i < 2; ++i) {
       CProb& p = cb.add(B, c.mat(w.Xt));
       ch_fwd(cb, p, GE_LN_RELU, tq[i].l1, Hc, nq, none_mat(), none_mat(), nullptr, le);
@@ -762,17 +746,6 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   int ks_pq = 1, ks_pp = 1;
   {
     PhaseScope ps(8, rep, s);
-    if (c.chain_bwd) {
-      ChainBuilder cb(1, c.row);
-      for (int i = 0; i < 2; ++i) {
-        CProb& p = cb.add(B, c.half(w.dlog, i));
-        ch_bwd(cb, p, GE_BWD_LN_RELU, cq[i].l3.w, cq[i].l2, Hc, N, c.mat(w.dA2c[i]), c.mat(w.qXH2[i]), c.F(w.qR2[i]),
-               c.F(w.part_q2[i]));
-        ch_bwd(cb, p, GE_BWD_LN_RELU, cq[i].l2.w, cq[i].l1, Hc, Hc, c.mat(w.dA1c[i]), c.mat(w.qXH1[i]),
-               c.F(w.qR1[i]), c.F(w.part_q1[i]));
-      }
-      BF_CK(chain_launch(cb, s));
-    } else {
     {
       GemmBuilder gb(1);
       for (int i = 0; i < 2; ++i) {
@@ -790,7 +763,6 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
                c.F(w.part_q1[i]), w.part_q1[i].n);
       }
       BF_CK(gemm_launch(gb, s));
-    }
     }
     {
       // dz = sum_i dA1_i W1_i[:, :L] (K-concatenation of the two heads) -> tanh + LN of the projection
@@ -952,7 +924,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
       BF_CK(gemm_launch(gb, s));
     }
     if (c.chain) {
-      ChainBuilder cb(1, c.row);
+      ChainBuilder cb(1);
       for (int i = 0; i < 2; ++i) {
         CProb& p = cb.add(B, c.mat(w.Xq1));
         ch_fwd(cb, p, GE_LN_RELU, cq1[i].l1, Hc, nq, none_mat(), c.mat(w.q1XH1[i]), c.F(w.q1R1[i]), le);
@@ -1014,17 +986,6 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     const Lin cproj1 = proj(c, w.sh[0], crit, gC, "critic");
     const Mlp cq1[2] = {mlp(c, w.sh[0], crit, gC, kHeads[0]), mlp(c, w.sh[0], crit, gC, kHeads[1])};
     (void)cproj1;
-    if (c.chain_bwd) {
-      ChainBuilder cb(1, c.row);
-      for (int i = 0; i < 2; ++i) {
-        CProb& p = cb.add(B, c.half(w.dlog1, i));
-        ch_bwd(cb, p, GE_BWD_LN_RELU, cq1[i].l3.w, cq1[i].l2, Hc, N, none_mat(), c.mat(w.q1XH2[i]), c.F(w.q1R2[i]),
-               nullptr);
-        ch_bwd(cb, p, GE_BWD_LN_RELU, cq1[i].l2.w, cq1[i].l1, Hc, Hc, c.mat(w.dA1a[i]), c.mat(w.q1XH1[i]),
-               c.F(w.q1R1[i]), nullptr);
-      }
-      BF_CK(chain_launch(cb, s));
-    } else {
     {
       GemmBuilder gb(1);
       for (int i = 0; i < 2; ++i) {
@@ -1043,7 +1004,6 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
       }
       BF_CK(gemm_launch(gb, s));
     }
-    }
     {
       // dL/da~ = sum_i dA1_i W1_i[:, L+P : L+P+A] -> tanh-Gaussian backward (+ the log pi path)
       GemmBuilder gb(1);
@@ -1058,15 +1018,6 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
       p.ldo = w.dO.ld;
       BF_CK(gemm_launch(gb, s));
     }
-    if (c.chain_bwd) {
-      ChainBuilder cb(1, c.row);
-      CProb& p = cb.add(B, c.mat(w.dO));
-      ch_bwd(cb, p, GE_BWD_LN_RELU, am.l3.w, am.l2, Ha, 2 * A, c.mat(w.adA2), c.mat(w.XH2ac), c.F(w.R2ac),
-             c.F(w.part_a2));
-      ch_bwd(cb, p, GE_BWD_LN_RELU, am.l2.w, am.l1, Ha, Ha, c.mat(w.adA1), c.mat(w.XH1ac), c.F(w.R1ac),
-             c.F(w.part_a1));
-      BF_CK(chain_launch(cb, s));
-    } else {
     {
       GemmBuilder gb(1);
       GProb& p = dx(gb, c.mat(w.dO), am.l3.w, 0, Ha, GE_BWD_LN_RELU);
@@ -1078,7 +1029,6 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
       GProb& p = dx(gb, c.mat(w.adA2), am.l2.w, 0, Ha, GE_BWD_LN_RELU);
       bwd_ln(p, am.l1, c.bp(w.XH1ac), w.XH1ac.ld, c.F(w.R1ac), c.bp(w.adA1), w.adA1.ld, c.F(w.part_a1), w.part_a1.n);
       BF_CK(gemm_launch(gb, s));
-    }
     }
     {
       GemmBuilder gb(1);
@@ -1148,7 +1098,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
 }  // namespace
 
 bool bf16_prepare() { return g_branch_enabled && t_aux.ok(); }
-int bf16_options() { return g_branch_enabled | (g_pipe_enabled << 1) | (g_dump_next << 2) | (g_chain_kind << 3); }
+int bf16_options() { return g_branch_enabled | (g_pipe_enabled << 1) | (g_dump_next << 2); }
 
 size_t bf16_workspace_bytes(const squint_dims& d) {
   Layout L = make_layout(d);
@@ -1191,11 +1141,8 @@ squint_status bf16_update(const squint_dims& d, const squint_hparams& hp, const 
   Layout L = make_layout(d);
   BfLay w = plan_bf(d, L);
   if (workspace_bytes < w.total) return set_error(SQUINT_EINVAL, "workspace too small (see squint_workspace_bytes)");
-  const bool row = g_chain_kind == 0;
-  auto sup = [&](int h) { return row ? rowchain_supported(h) : chain_supported(h); };
-  const bool chain_ok = sup(d.critic_hidden) && sup(d.actor_hidden);
-  Ctx c{d, L, reinterpret_cast<char*>(workspace), s, chain_ok, chain_ok && row,
-        (g_branch_enabled && t_aux.ok()) ? &t_aux : nullptr, row};
+  const bool chain_ok = chain_supported(d.critic_hidden) && chain_supported(d.actor_hidden);
+  Ctx c{d, L, reinterpret_cast<char*>(workspace), s, chain_ok, (g_branch_enabled && t_aux.ok()) ? &t_aux : nullptr};
   const int nranks = comm ? comm_nranks(comm) : 1;
   const float inv_btotal = 1.0f / ((float)d.batch * (float)nranks);
   // bf16 shadows of the current master weights (and the conv weight tiles, which with the
@@ -1256,8 +1203,7 @@ squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const flo
   BM H2{P.take((size_t)n * ldp(Ha) * 2), M, Ha, ldp(Ha)};
   ShadowPlan sp = shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
   uint8_t* wtiles = reinterpret_cast<uint8_t*>(ws + P.take(conv_tiles_bytes(d.conv_ch)));
-  const bool row = g_chain_kind == 0;
-  Ctx c{d, L, ws, s, false, false, nullptr, row};
+  Ctx c{d, L, ws, s, false, nullptr};
   const int gC = SQUINT_GROUP_CRITIC, gA = SQUINT_GROUP_ACTOR;
   std::optional<PhaseScope> ps;
   ps.emplace(1, 0, s);
@@ -1298,9 +1244,9 @@ squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const flo
     fwd(gb, c.mat(Xh), ap, GE_LN_TANH, c.bp(Xa), Xa.ld, hp.ln_eps);
     BF_CK(gemm_launch(gb, s));
   }
-  if (row ? rowchain_supported(Ha) : chain_supported(Ha)) {
+  if (chain_supported(Ha)) {
     // the whole actor MLP + tanh-Gaussian head in one fused chain launch
-    ChainBuilder cb(1, c.row);
+    ChainBuilder cb(1);
     CProb& pa = cb.add(M, c.mat(Xa));
     ch_fwd(cb, pa, GE_LN_RELU, am.l1, Ha, npi, none_mat(), none_mat(), nullptr, hp.ln_eps);
     ch_fwd(cb, pa, GE_LN_RELU, am.l2, Ha, Ha, none_mat(), none_mat(), nullptr, hp.ln_eps);
@@ -1376,10 +1322,6 @@ extern "C" SQUINT_API squint_status squint_set_option(int key, int value) {
   }
   if (key == 3) {
     sq::g_check_enabled = value != 0;
-    return SQUINT_OK;
-  }
-  if (key == 6) {
-    sq::g_chain_kind = value != 0;
     return SQUINT_OK;
   }
   if (key == 5) {
