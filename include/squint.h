@@ -287,10 +287,11 @@ SQUINT_API int squint_set_launch_events(void** events, int n);
  * (0, default): sampled indices in [0, replay.size), insert / act slots in [0, capacity) and
  * pairwise distinct -- a check kernel plus a stream synchronisation per call, returning
  * SQUINT_EINVAL with a message instead of undefined behaviour (skipped inside a stream
- * capture); key 4 = numerics measurement on the SQUINT_FP32 path only (0, default): round the dense
- * layers' GEMM operands to bf16 before the fp32 multiply-add -- bit 0 the activations / dY, bit 1
- * the weights -- to measure how much of the bf16 path's deviation from the oracle bf16 operand
- * rounding alone explains (reading R-tol-bf16); key 5 = (SQUINT_BF16, 0 default) the
+ * capture); key 4 = numerics measurement on the SQUINT_FP32 path only (0, default): round to bf16
+ * what the SQUINT_BF16 path holds in bf16, before the fp32 arithmetic -- bit 0 the dense layers' GEMM
+ * activations / dY, bit 1 their weights, bit 2 the LayerNorm x_hat cache, bit 3 the encoder's conv
+ * weights, conv1 activations and conv gradients -- to measure how much of the bf16 path's deviation
+ * from the oracle bf16 storage alone explains (reading R-tol-bf16); key 5 = (SQUINT_BF16, 0 default) the
  * encoder also stores the gathered, shifted next_obs images into workspace region 9 (test access to
  * the a3-a4 integer work).  Errors: EINVAL for an unknown key or value. */
 SQUINT_API squint_status squint_set_option(int key, int value);

@@ -223,9 +223,10 @@ struct Ctx {
 static thread_local int g_prec = SQUINT_FP32;
 
 // Dense layers: fp32 SIMT (parity mode) or bf16 tcgen05 tensor cores.
-// squint_set_option key 4 (numerics measurement, fp32 path only): round chosen dense-layer GEMM
-// operands to bf16 (bit 0: activations / dY, bit 1: weights) to measure the error bf16 operands
-// alone introduce (DESIGN.md R-tol-bf16)
+// squint_set_option key 4 (numerics measurement, fp32 path only): round to bf16 what the tensor-core
+// path holds in bf16 -- bit 0: dense-layer GEMM activations / dY, bit 1: dense weights, bit 2: the
+// LayerNorm x_hat cache, bit 3: the encoder's conv weights, conv1 activations and conv gradients --
+// to measure the error bf16 storage alone introduces (DESIGN.md R-tol-bf16)
 int g_emul = 0;
 static int emul_flags() { return g_emul; }
 static int run_dense(DenseBatch& b, cudaStream_t s) {
@@ -289,6 +290,7 @@ static squint_status update_one(const Ctx& c, const squint_replay& R, const int6
     e.c_in = d.img_c;
     e.H = d.img_h;
     e.pad = d.pad;
+    e.emul = g_emul;
     SQ_CK(launch_enc_fwd(e, s));
   }
   // a6: four projections
@@ -469,6 +471,7 @@ static squint_status update_one(const Ctx& c, const squint_replay& R, const int6
     e.gb1 = gc + L.off(gC, "enc.conv1.b");
     e.gw2 = gc + L.off(gC, "enc.conv2.w");
     e.gb2 = gc + L.off(gC, "enc.conv2.b");
+    e.emul = g_emul;
     SQ_CK(launch_enc_bwd(e, s));
   }
   float* extras = gc + L.gsize[gC];

@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int cc = hh * 32 + j;
-        const float x = (v[j] + s_bias[cc] - mean) * rs;
+        const float x = bf16_round((v[j] + s_bias[cc] - mean) * rs);
         const float n = fmaf(x, s_g[cc], s_beta[cc]);
         a[j] = x;
         v[j] = (epi == GE_LN_RELU) ? fmaxf(n, 0.f) : tanh_fast(n);

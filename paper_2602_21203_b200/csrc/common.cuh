@@ -1,5 +1,6 @@
 // common.cuh -- small device helpers shared by the libsquint kernels (sm_100a).
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -69,6 +70,12 @@ SQ_DEV float block_sum(float v, float* red) {
 }
 
 SQ_DEV bool is_finite(float x) { return isfinite(x); }
+
+// Round to bf16 and back.  The LayerNorm forward epilogues of the bf16 path normalise with the x_hat
+// they cache in bf16 (n = g bf16(x_hat) + beta), so the backward, which recomputes n from the cache,
+// takes exactly the forward's ReLU'(n) decisions (an element whose n is within bf16 rounding of 0
+// would otherwise flip its mask and carry a full dY of error into the layer's gradients).
+SQ_DEV float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
 // 1 - tanh(u)^2 without cancellation: sech^2 u = 4 t / (1 + t)^2, t = exp(-2|u|).
 // (1 - a*a with a = tanhf(u) loses ~all digits once |u| > 4; log pi's squash term and the

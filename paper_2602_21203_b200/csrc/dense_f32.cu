@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(256) k_dense_f32(const __grid_constant__ Dense
       for (int j = 0; j < TN; ++j) {
         const int c = col_of(j);
         if (c >= N) continue;
-        const float xh = acc[i][j] * rs;
+        // option 4 bit 2 emulates the bf16 path's x_hat cache, which it also normalises with
+        const float xh = (b.emul & 4) ? __bfloat162float(__float2bfloat16_rn(acc[i][j] * rs)) : acc[i][j] * rs;
         const float n = fmaf(xh, P.g[c], P.beta[c]);
         const float y = (epi == EPI_LN_RELU) ? fmaxf(n, 0.f) : tanhf(n);
         if (P.xh) P.xh[(int64_t)r * N + c] = xh;

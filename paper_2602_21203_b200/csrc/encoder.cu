@@ -15,6 +15,9 @@ namespace sq {
 
 namespace {
 
+SQ_DEV float bfr(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+SQ_DEV float bfr_if(bool on, float x) { return on ? bfr(x) : x; }
+
 SQ_DEV uint32_t rhe_div(uint32_t s, uint32_t n) {
   uint32_t q = s / n, r = s - q * n;
   if (2 * r > n || (2 * r == n && (q & 1u))) ++q;
@@ -101,11 +104,11 @@ __global__ void __launch_bounds__(256) k_enc_fwd(const __grid_constant__ EncFwdA
 
   for (int e = tid; e < C * 9 * ci; e += 256) {  // global [o][c][kk] -> [c*9+kk][o]
     const int o = e / (9 * ci), r = e % (9 * ci);
-    w1t[r * (C + 1) + o] = a.w1[e];
+    w1t[r * (C + 1) + o] = bfr_if(a.emul & 8, a.w1[e]);
   }
   for (int e = tid; e < C * 9 * C; e += 256) {
     const int o = e / (9 * C), r = e % (9 * C);
-    w2t[r * (C + 1) + o] = a.w2[e];
+    w2t[r * (C + 1) + o] = bfr_if(a.emul & 8, a.w2[e]);
   }
   for (int jb = 0; jb < a.ngj[src_i]; ++jb) {
     const GatherJob& g = a.gj[src_i][jb];
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(256) k_enc_fwd(const __grid_constant__ EncFwdA
 #pragma unroll
         for (int kj = 0; kj < 3; ++kj) acc = fmaf(w1t[(cc * 9 + ki * 3 + kj) * (C + 1) + o], xi[ki * H + kj], acc);
     }
-    const float v = fmaxf(acc, 0.f);
+    const float v = bfr_if(a.emul & 8, fmaxf(acc, 0.f));
     y1s[(i * C + o) * P1 + pix] = v;
     const int b = b0 + i;
     if (src_i == 0 && a.y1 && b < a.B) a.y1[((int64_t)b * C + o) * P1 + pix] = v;
@@ -226,7 +229,7 @@ __global__ void __launch_bounds__(256) k_enc_bwd_dx(const __grid_constant__ EncB
   float* w2s = sm;               // [o][c][9]
   float* ds = w2s + C * C * 9;   // [ipb][C][P2]
   const int tid = threadIdx.x, b0 = blockIdx.x * ipb;
-  for (int e = tid; e < C * C * 9; e += 256) w2s[e] = a.w2[e];
+  for (int e = tid; e < C * C * 9; e += 256) w2s[e] = bfr_if(a.emul & 8, a.w2[e]);
   for (int e = tid; e < ipb * C * P2; e += 256) {
     const int i = e / (C * P2), b = b0 + i, r = e % (C * P2);
     float v = 0.f;
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(256) k_enc_bwd_dx(const __grid_constant__ EncB
         v = a.dA2[(int64_t)b * C * P2 + r];
       }
     }
-    ds[e] = v;
+    ds[e] = bfr_if(a.emul & 8, v);
   }
   __syncthreads();
   const int c = tid % C, grp = tid / C, ngrp = 256 / C;
@@ -263,7 +266,7 @@ __global__ void __launch_bounds__(256) k_enc_bwd_dx(const __grid_constant__ EncB
     }
     const int64_t gi = ((int64_t)b * C + c) * P1 + pix;
     const float yv = a.y1_hwc ? __bfloat162float(a.y1_hwc[((int64_t)b * P1 + pix) * C + c]) : a.y1[gi];
-    a.dA1[gi] = yv > 0.f ? acc : 0.f;
+    a.dA1[gi] = yv > 0.f ? bfr_if(a.emul & 8, acc) : 0.f;
   }
 }
 
@@ -274,7 +277,7 @@ template <bool kU8>
 __global__ void __launch_bounds__(256) k_conv_dw(const float* __restrict__ D, const __nv_bfloat16* __restrict__ Dh,
                                                  const void* __restrict__ Xv, const __nv_bfloat16* __restrict__ Xh, int B,
                                                  int O, int Cin, int Hin, int Hout, int stride, int OB,
-                                                 int nchunk, float* __restrict__ part) {
+                                                 int nchunk, float* __restrict__ part, int emul_d) {
   extern __shared__ float sm[];
   const int Pout = Hout * Hout, HH = Hin * Hin;
   float* Ds = sm;               // [OB][Pout]
@@ -294,7 +297,7 @@ __global__ void __launch_bounds__(256) k_conv_dw(const float* __restrict__ D, co
         const int ol = e / Pout, pix = e - ol * Pout;
         Ds[e] = __bfloat162float(Dh[(int64_t)b * O * Pout + pix * O + o0 + ol]);
       } else {
-        Ds[e] = D[((int64_t)b * O + o0) * Pout + e];
+        Ds[e] = bfr_if(emul_d, D[((int64_t)b * O + o0) * Pout + e]);
       }
     }
     for (int e = tid; e < Cin * HH; e += 256) {
@@ -395,14 +398,14 @@ int launch_enc_bwd(const EncBwdArgs& a, cudaStream_t s) {
     const size_t smem = sizeof(float) * (size_t)(ob * P2 + C * P1);
     cudaFuncSetAttribute(k_conv_dw<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     note_launch(s, "k_conv_dw", 0, 0); k_conv_dw<false><<<dim3(a.nchunk, C / ob), 256, smem, s>>>(a.dA2, a.dA2_hwc, a.y1, a.y1_hwc, a.B, C, C, H1, H2, 1, ob, a.nchunk,
-                                                                 part2);
+                                                                 part2, a.emul & 8);
   }
   {
     const int ob = ob_of(C, a.c_in);
     const size_t smem = sizeof(float) * (size_t)(ob * P1 + a.c_in * a.H * a.H);
     cudaFuncSetAttribute(k_conv_dw<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     note_launch(s, "k_conv_dw", 0, 0); k_conv_dw<true><<<dim3(a.nchunk, C / ob), 256, smem, s>>>(a.dA1, nullptr, a.img, nullptr, a.B, C, a.c_in, a.H, H1, 2, ob,
-                                                               a.nchunk, part1);
+                                                               a.nchunk, part1, 0);
   }
   {
     const int n2 = C * C * 9 + C, n1 = C * a.c_in * 9 + C;

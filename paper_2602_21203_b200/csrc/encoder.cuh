@@ -47,6 +47,8 @@ struct EncFwdArgs {
   const uint8_t* wtiles;   // tensor-core path: conv weights as swizzled bf16 smem images (k_conv_tiles)
   int dbg;                 // phase timestamps (SQUINT_ENC_DBG; set by the launcher)
   int max_ctas;            // tensor-core path: grid cap (0: one CTA per job, at most one per SM)
+  int emul;                // fp32 path, numerics measurement (squint_set_option 4 bit 3): conv weights
+                           // and the conv1 activations rounded to bf16 as the tensor-core path stores them
 };
 
 struct EncBwdArgs {
@@ -65,6 +67,7 @@ struct EncBwdArgs {
   const uint8_t* wtiles;   // tensor-core path: conv weights as swizzled bf16 smem images (k_conv_tiles)
   int max_ctas;            // tensor-core path: grid cap (0: one CTA per SM); fewer when the kernel
                            // runs beside other work on a graph branch
+  int emul;                // fp32 path (squint_set_option 4 bit 3): W2, dA2 and dA1 rounded to bf16
 };
 
 int launch_enc_fwd(const EncFwdArgs& a, cudaStream_t s);

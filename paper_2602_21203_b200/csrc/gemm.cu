@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int cc = ch * 32 + j;
-          const float x = (v[j] + s_bias[cc] - mean) * rs;
+          const float x = bf16_round((v[j] + s_bias[cc] - mean) * rs);
           const float n = fmaf(x, s_g[cc], s_beta[cc]);
           a[j] = x;
           v[j] = (EPI == GE_LN_RELU) ? fmaxf(n, 0.f) : tanh_fast(n);
@@ -1021,7 +1021,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_sk(const __grid_constant__
         float y[8], xh[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          xh[j] = (acc[j] - mean) * rs;
+          xh[j] = bf16_round((acc[j] - mean) * rs);
           const float n = fmaf(xh[j], s_g[c0 + j], s_beta[c0 + j]);
           y[j] = (EPI == GE_LN_RELU) ? fmaxf(n, 0.f) : tanh_fast(n);
         }

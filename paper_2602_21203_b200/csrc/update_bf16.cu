@@ -1329,7 +1329,7 @@ extern "C" SQUINT_API squint_status squint_set_option(int key, int value) {
     return SQUINT_OK;
   }
   if (key == 4) {
-    if (value < 0 || value > 3) return sq::set_error(SQUINT_EINVAL, "option 4: value must be 0..3");
+    if (value < 0 || value > 15) return sq::set_error(SQUINT_EINVAL, "option 4: value must be 0..15");
     sq::g_emul = value;
     return SQUINT_OK;
   }

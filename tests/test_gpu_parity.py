@@ -296,9 +296,9 @@ def test_update_degenerate_cases(case, precision):
     if case == "reward_clip":
         pr.R["reward"][:] = np.where(np.arange(pr.R["reward"].shape[0]) % 2 == 0, 60.0, -60.0).astype(np.float32)
     if case == "alpha_large":
-        # alpha = e^3 (fp32) / e^1.5 (bf16): the target's atom shift alpha log pi' multiplies the
-        # bf16 error of log pi' by alpha, so the bf16 bar on m (2e-2) holds up to alpha ~ 5
-        la = 3.0 if precision == "fp32" else 1.5
+        # alpha = e^3: the target's atom shift alpha log pi' multiplies the bf16 error of log pi' by
+        # alpha; the bf16 bar on m is then its emulation floor (R-tol-bf16, R-tol-alpha)
+        la = 3.0
         pr.vals[("alpha", "log_alpha")] = np.full_like(np.asarray(pr.vals[("alpha", "log_alpha")]), la)
     L = pr.gpu_setup(precision=P.BF16 if precision == "bf16" else P.FP32)
     met = pr.gpu_update(L)
@@ -407,19 +407,68 @@ def test_act_bf16_presquinted_factor1(n):
     assert np.array_equal(ring[slots].cpu().numpy(), small)
 
 
+def _rel_max(got, ref):
+    """Scale-relative max error (Q34): max|got - ref| / max|ref|."""
+    ref = np.asarray(ref, np.float64)
+    return float(np.abs(np.asarray(got, np.float64) - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
 def _rel_l2(got, ref):
-    num = sum(float(np.sum((np.asarray(got[n], np.float64) - r) ** 2)) for n, r in ref.items())
-    den = sum(float(np.sum(np.asarray(r, np.float64) ** 2)) for r in ref.values())
-    return (num / max(den, 1e-300)) ** 0.5
+    ref = np.asarray(ref, np.float64)
+    return float(np.linalg.norm(np.asarray(got, np.float64) - ref) / max(np.linalg.norm(ref), 1e-30))
+
+
+def _errs(got, ref):
+    return (_rel_max(got, ref), _rel_l2(got, ref))
+
+
+def _proj_chw(pr, g):
+    # bf16 mode stores the projection weight gradients pixel-major (squint.h, regions 0 / 1)
+    C = pr.dims["conv_ch"]
+    for grp in ("critic", "actor"):
+        pw = f"{grp}.proj.w"
+        if pw in g:
+            g[pw] = g[pw].reshape(g[pw].shape[0], -1, C).transpose(0, 2, 1).reshape(g[pw].shape)
+    return g
+
+
+def _emulation_floor(pr, trace, st_ref):
+    """The same update on the fp32 path with every value the bf16 path stores in bf16 rounded to bf16
+    (squint_set_option 4 = 15: GEMM activations / dY, weights, the LayerNorm x_hat cache, the encoder's
+    weights and activations), against the same oracle: per tensor, the error bf16 storage alone causes
+    (DESIGN.md R-tol-bf16)."""
+    P.squint.LIB.squint_set_option(4, 15)
+    try:
+        L = pr.gpu_setup(precision=P.FP32)
+        pr.gpu_update(L)
+    finally:
+        P.squint.LIB.squint_set_option(4, 0)
+    tr = trace[-1]
+    fl = {}
+    for grp in ("critic", "actor"):
+        g = group_values(L, grp, "grad")
+        for n, r in tr["grad_" + grp].items():
+            fl[("grad", grp, n)] = _errs(g[n], r)
+        got = group_values(L, grp)
+        for n, r in st_ref[grp].items():
+            fl[("delta", grp, n)] = _errs(got[n] - pr.vals[(grp, n)], r - np.asarray(pr.vals[(grp, n)], np.float64))
+    for n in ("m", "logp", "logp_next"):
+        fl[n] = _errs(L.region(n).cpu().numpy().reshape(tr[n].shape), tr[n])
+    return fl
 
 
 def _check_update_bf16(pr, L, met_gpu, st_ref, met_ref, trace):
-    """bf16 tensor-core mode (DESIGN.md R-tol-bf16).  Losses / metrics, the target distribution,
-    log-probs and the updated parameters at the north-star bar 2e-2 (mean Q against a scale of at
-    least v_max / 10); gradients and the Adam steps (parameter deltas, m_hat / sqrt(v_hat) of the
-    gradient) at 3e-2 relative L2 per group and gradients at 8e-2 per tensor: rounding only the
-    weights to bf16 (SQUINT_EMUL=2 on the fp32 path) already moves the c2 critic gradient by
-    1.4e-2 (group) / 3.0e-2 (worst tensor) on these inputs."""
+    """bf16 tensor-core mode (DESIGN.md R-tol-bf16).  Losses / metrics at the north-star bar 2e-2 (mean Q
+    and L_alpha against the size of their terms).  Every other tensor -- the target distribution m, log pi,
+    log pi', each gradient tensor and each Adam step (the parameter change, Q27) -- element-wise against
+    its emulation floor: the error the same update has on the fp32 path with exactly the values the bf16
+    path stores in bf16 rounded to bf16 (squint_set_option 4 = 15), measured here on the same inputs.
+    Bars: scale-relative max error (Q34) <= max(2e-2, 2 x floor_max) and relative L2 <= max(2e-2,
+    1.5 x floor_L2).  Measured over 30 update cases / 2520 tensors (c2, ragged, CDQ, scalar critic,
+    utd 2, reward clipping, alpha = e^3, c3 shapes): median ratio bf16 / floor 1.00, 99th percentile 1.38
+    (max error) / 1.15 (L2), maximum 2.11 (on a tensor at 9e-5) / 1.63 (at 2.5e-3) -- the floor is one
+    realization of the same rounding noise, so a single case's ratio scatters around 1; no case of the
+    2520 exceeds either bar."""
     tol = 2e-2
     qscale = 0.1 * max(abs(pr.dims["v_min"]), abs(pr.dims["v_max"]))
     for j in range(pr.utd):
@@ -439,30 +488,25 @@ def _check_update_bf16(pr, L, met_gpu, st_ref, met_ref, trace):
             compare(f"metric {name}[{j}]", met_gpu[j, k], met_ref[j, k], tol)
         assert met_gpu[j, 7] == 0.0
     tr = trace[-1]
-    compare("m", L.region("m").cpu().numpy().reshape(tr["m"].shape), tr["m"], tol)
-    compare("logp", L.region("logp").cpu().numpy(), tr["logp"], tol)
-    compare("logp_next", L.region("logp_next").cpu().numpy(), tr["logp_next"], tol)
+    floor = _emulation_floor(pr, trace, st_ref)
+
+    def check(key, got, ref):
+        (em, e2), (fm, f2) = _errs(got, ref), floor[key]
+        assert em <= max(tol, 2.0 * fm), f"{key}: max error {em:.3e} > max(2e-2, 2 x floor {fm:.3e})"
+        assert e2 <= max(tol, 1.5 * f2), f"{key}: rel L2 {e2:.3e} > max(2e-2, 1.5 x floor {f2:.3e})"
+
+    for n in ("m", "logp", "logp_next"):
+        check(n, L.region(n).cpu().numpy().reshape(tr[n].shape), tr[n])
     for grp in ("critic", "actor"):
-        g = group_values(L, grp, "grad")
-        # bf16 mode stores the projection weight gradient pixel-major (squint.h, region 0/1)
-        pw = f"{grp}.proj.w"
-        C = pr.dims["conv_ch"]
-        g[pw] = g[pw].reshape(g[pw].shape[0], -1, C).transpose(0, 2, 1).reshape(g[pw].shape)
-        ref = tr["grad_" + grp]
-        e = _rel_l2(g, ref)
-        assert e <= 3e-2, f"grad {grp}: group relative L2 {e:.3e} > 3e-2"
-        for n, r in ref.items():
-            en = _rel_l2({n: g[n]}, {n: r})
-            assert en <= 8e-2, f"grad {grp} {n}: relative L2 {en:.3e} > 8e-2"
+        g = _proj_chw(pr, group_values(L, grp, "grad"))
+        for n, r in tr["grad_" + grp].items():
+            check(("grad", grp, n), g[n], r)
     for grp in ("critic", "actor", "target"):
         got = group_values(L, grp)
         for n, ref in st_ref[grp].items():
             compare(f"{grp} {n}", got[n], ref, tol)
-        if grp != "target":
-            d_got = {n: got[n] - pr.vals[(grp, n)] for n in st_ref[grp]}
-            d_ref = {n: st_ref[grp][n] - np.asarray(pr.vals[(grp, n)], np.float64) for n in st_ref[grp]}
-            e = _rel_l2(d_got, d_ref)  # m_hat / sqrt(v_hat) of the gradient: the gradient's bound
-            assert e <= 3e-2, f"Adam step {grp}: relative L2 {e:.3e} > 3e-2"
+            if grp != "target":  # the Adam step itself (parameter change, Q27)
+                check(("delta", grp, n), got[n] - pr.vals[(grp, n)], ref - np.asarray(pr.vals[(grp, n)], np.float64))
     compare("log_alpha", L.log_alpha.cpu().numpy()[0], st_ref["log_alpha"], 1e-4)
     assert L.step.cpu().tolist() == list(st_ref["step"])
 
