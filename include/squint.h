@@ -143,7 +143,8 @@ SQUINT_API squint_status squint_workspace_bytes(const squint_dims* dims, int utd
  * 2 = target distribution m [B, n_atoms], 3 = h [B, 25C], 4 = log pi (current) [B],
  * 5 = log pi' (next) [B], 6 = actions a~ [B, A], 7 = scalars [16],
  * 8 = the last update's gathered, shifted obs images u8 [B, C, H, W] (a3-a4; the conv1 weight
- *     gradient's input), 9 = (SQUINT_BF16, with squint_set_option(5, 1)) the same for next_obs. */
+ *     gradient's input), 9 = (SQUINT_BF16, with squint_set_option(5, 1)) the same for next_obs,
+ * 10 = (SQUINT_BF16) the obs images' conv1 activations, bf16 [B, 7 * 7, conv_ch] (pixel-major). */
 SQUINT_API squint_status squint_workspace_region(const squint_dims* dims, int region, size_t* offset, size_t* bytes);
 
 /* Workspace bytes needed by squint_act for n frames. */

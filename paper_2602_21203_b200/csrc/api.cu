@@ -219,8 +219,6 @@ struct Ctx {
   float* F(size_t off) const { return reinterpret_cast<float*>(ws + off); }
 };
 
-// Precision of the call in flight (set by the entry points; calls on one thread serialise).
-static thread_local int g_prec = SQUINT_FP32;
 
 // Dense layers: fp32 SIMT (parity mode) or bf16 tcgen05 tensor cores.
 // squint_set_option key 4 (numerics measurement, fp32 path only): round to bf16 what the tensor-core
@@ -889,7 +887,6 @@ squint_status squint_act(const squint_dims* dims, const squint_hparams* hp, cons
     return fail(SQUINT_EINVAL, "frames must be 16-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
   const squint_dims& d = *dims;
-  g_prec = d.precision;
   if (d.precision == SQUINT_BF16)
     return bf16_act(d, *hp, actor_params, critic_params, frames, n, f, proprio, eps, action_out, logp_out, ring, slots,
                     workspace, s);
@@ -1060,7 +1057,6 @@ squint_status squint_update(const squint_dims* dims, const squint_hparams* hp, c
     const uint8_t* sj = shifts + j * B * 4;
     const float* ej = eps + j * 2 * B * A;
     float* mj = metrics + j * 8;
-    g_prec = dims->precision;
     squint_status st = update_one(c, *replay, ij, sj, ej, *state, mj, cm, inv_btotal, j);
     if (st != SQUINT_OK) return st;
   }

@@ -407,6 +407,275 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ 
   if (warp == 0) tc::tmem_dealloc(tmem, kCols);
 }
 
+// ---- forward, warp-specialised and pipelined across a CTA's groups ------------------------------
+// (replay gather + shift, mode 0, and pre-squinted frames, mode 1 with factor 1.)  The round-1 kernel
+// above runs each group's phases back to back with the whole CTA; here they run in separate roles so
+// the tensor core works through one group's conv2 while the CUDA cores stage and im2col the next
+// group and run the previous group's epilogues:
+//   P  warps 0-3   images of group i -> xs (u8), conv1 im2col -> A1          (a1_full / a1_empty)
+//   E1 warps 4-7   conv1 accumulator T1 -> ReLU(acc / 255 + b1) -> y1 (smem) + y1b (global)
+//                                                       (t1_full / t1_empty, y1_full / y1_empty)
+//   E2 warps 8-11  conv2 accumulator T2 -> ReLU(acc + b2) -> h (global)      (t2_full / t2_empty)
+//   M  warp 12     conv1 MMAs (A1, W1) -> T1; conv2 as nine row-shifted MMAs per tile (y1, W2) -> T2
+// Every barrier completes once per group; TMEM holds T1 (3 C columns) and T2 (3 C columns).
+constexpr int kWsWarps = 13;
+template <int C>
+struct FwdW {
+  static constexpr uint32_t w = 0;
+  static constexpr uint32_t a1 = (C * 128 + ((9 * C + 63) / 64) * C * 128 + 1023) & ~1023u;  // 3 x 16 KB
+  static constexpr uint32_t y1 = a1 + 3 * 16384;
+  static constexpr uint32_t xs = y1 + ((416u * C * 2 + 1023) & ~1023u);
+  static constexpr uint32_t total = xs + kGF * 768;
+};
+
+template <int C>
+__global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_constant__ EncFwdArgs a) {
+  using L = FwdW<C>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t wbar, a1_full, a1_empty, t1_full, t1_empty, y1_full, y1_empty, t2_full, t2_empty;
+  __shared__ uint32_t tmem_slot;
+  __shared__ int s_koff[32];
+  __shared__ float s_b1[64], s_b2[64];
+  const int H = a.H;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ngroups = (a.B + kGF - 1) / kGF;
+  const int total = ngroups * a.nsrc;
+  const int nloc = blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  enc_stamp(a.dbg, 10);
+  if (warp == 0) tc::tmem_alloc(&tmem_slot, 512);
+  if (tid == 32) {
+    tc::mbar_init(&wbar, 1);
+    tc::mbar_init(&a1_full, 4);
+    tc::mbar_init(&a1_empty, 1);
+    tc::mbar_init(&t1_full, 1);
+    tc::mbar_init(&t1_empty, 4);
+    tc::mbar_init(&y1_full, 4);
+    tc::mbar_init(&y1_empty, 1);
+    tc::mbar_init(&t2_full, 1);
+    tc::mbar_init(&t2_empty, 4);
+    tc::fence_mbar_init();
+  }
+  if (warp == 2) {
+    const int k = lane, ci = k / 9, t = k - ci * 9, ki = t / 3, kj = t - ki * 3;
+    s_koff[k] = k < 27 ? ci * 256 + ki * 16 + kj : 0;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  grid_wait();  // weight tiles, inputs and biases come from earlier kernels
+  grid_trigger();
+  if (tid < C) {
+    s_b1[tid] = a.b1[tid];
+    s_b2[tid] = a.b2[tid];
+  }
+  if (tid == 32) {
+    tc::mbar_expect_tx(&wbar, fwd_wbytes(C));
+    tc::bulk_load_1d(sm + L::w, a.wtiles, fwd_wbytes(C), &wbar);
+  }
+  __syncthreads();  // s_b1, s_b2
+  const uint32_t tmem = tmem_slot;
+  const uint32_t t_c1 = tmem, t_c2 = tmem + 3 * C;
+  uint8_t* xs = sm + L::xs;
+
+  if (warp < 4) {
+    // ---- P: stage + conv1 im2col --------------------------------------------------------------------
+    const int pt = tid;  // 0..127
+    for (int i = 0; i < nloc; ++i) {
+      const int job = blockIdx.x + i * gridDim.x;
+      const int src = job / ngroups, g = job - src * ngroups, b0 = g * kGF;
+      tc::named_bar(1, 128);  // the previous group's im2col has read xs
+      if (a.mode == 0) {
+        const uint8_t* R = a.src[src];
+        for (int e = pt; e < kGF * 48; e += 128) {
+          const int ii = e / 48, rem = e - ii * 48, cc = rem >> 4, y = rem & 15;
+          const int b = b0 + ii;
+          uint4 o = make_uint4(0, 0, 0, 0);
+          if (b < a.B) {
+            const int64_t row = a.idx[b];
+            const int dx = a.shifts[b * 4 + 2 * src], dy = a.shifts[b * 4 + 2 * src + 1];
+            const int sy = min(max(y + dy - a.pad, 0), H - 1);
+            const uint4 v = *reinterpret_cast<const uint4*>(R + row * 768 + cc * 256 + sy * 16);
+            uint32_t wv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              uint32_t acc = 0;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) acc |= byte_of(v, min(max(4 * k + j + dx - a.pad, 0), H - 1)) << (8 * j);
+              wv[k] = acc;
+            }
+            o = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            uint8_t* dump = src == 0 ? a.img0 : a.img1;
+            if (dump) *reinterpret_cast<uint4*>(dump + (int64_t)b * 768 + cc * 256 + y * 16) = o;
+          }
+          *reinterpret_cast<uint4*>(xs + ii * 768 + cc * 256 + y * 16) = o;
+        }
+      } else {  // frames already at the stored resolution (factor 1): 768-byte copies
+        const uint8_t* Fr = a.src[0];
+        for (int e = pt; e < kGF * 48; e += 128) {
+          const int ii = e / 48, rem = e - ii * 48, b = b0 + ii;
+          uint4 o = make_uint4(0, 0, 0, 0);
+          if (b < a.B) {
+            o = __ldcs(reinterpret_cast<const uint4*>(Fr + (int64_t)b * 768) + rem);
+            if (a.ring) reinterpret_cast<uint4*>(a.ring + a.slots[b] * 768)[rem] = o;
+          }
+          reinterpret_cast<uint4*>(xs + ii * 768)[rem] = o;
+        }
+      }
+      for (int jb = 0; jb < a.ngj[src]; ++jb) {
+        const GatherJob& gj = a.gj[src][jb];
+        for (int e = pt; e < kGF * gj.width; e += 128) {
+          const int ii = e / gj.width, j = e - ii * gj.width, b = b0 + ii;
+          if (b < a.B) {
+            const int64_t row = gj.use_idx ? a.idx[b] : (int64_t)b;
+            gj.dst[(int64_t)b * gj.ld + gj.col + j] = __float2bfloat16_rn(gj.src[row * gj.width + j]);
+          }
+        }
+      }
+      tc::named_bar(1, 128);  // xs complete
+      if (i >= 1) tc::mbar_wait(&a1_empty, (i - 1) & 1);
+      // conv1 im2col: row (img, oy, ox), K 0..26 = (ci, ki, kj) at byte offset koff[k] from the output
+      // pixel's top-left input byte; K 27..31 zero (the MMAs read the first 64 bytes of each row)
+      for (int e = pt; e < 384 * 4; e += 128) {
+        const int r = e >> 2, ch = e & 3;
+        float f[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) f[j] = 0.f;
+        if (r < kGF * 49) {
+          const int ii = r / 49, p = r - ii * 49, oy = p / 7, ox = p - oy * 7;
+          const uint8_t* px = xs + ii * 768 + 2 * oy * 16 + 2 * ox;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int k = ch * 8 + j;
+            if (k < 27) f[j] = (float)px[s_koff[k]];
+          }
+        }
+        *reinterpret_cast<uint4*>(sm + L::a1 + (r >> 7) * 16384 + sw(r & 127, ch)) = tc::pack_bf16x8(f);
+      }
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&a1_full);
+      if (i == 0) enc_stamp(a.dbg, 11);
+    }
+  } else if (warp < 8) {
+    // ---- E1: conv1 epilogue -> y1 ---------------------------------------------------------------
+    const int q = warp & 3;
+    const float inv255 = 1.0f / 255.0f;
+    for (int i = 0; i < nloc; ++i) {
+      const int job = blockIdx.x + i * gridDim.x;
+      const int src = job / ngroups, g = job - src * ngroups, b0 = g * kGF;
+      tc::mbar_wait(&t1_full, i & 1);
+      if (i >= 1) tc::mbar_wait(&y1_empty, (i - 1) & 1);
+      tc::fence_after_sync();
+#pragma unroll 1
+      for (int t = 0; t < 3; ++t) {
+        const int r = t * 128 + q * 32 + lane;
+        const int ii = r / 49, p = r - ii * 49, b = b0 + ii;
+        const bool rv = r < kGF * 49;
+#pragma unroll
+        for (int c0 = 0; c0 < C; c0 += 32) {
+          float v[32];
+          tc::tmem_ld32(t_c1 + t * C + c0 + ((uint32_t)(q * 32) << 16), v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = fmaxf(fmaf(v[j], inv255, s_b1[c0 + j]), 0.f);
+          if (rv) {
+#pragma unroll
+            for (int j8 = 0; j8 < 4; ++j8) {
+              float f[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) f[j] = v[j8 * 8 + j];
+              const uint4 u = tc::pack_bf16x8(f);
+              *reinterpret_cast<uint4*>(sm + L::y1 + y1_off<C>(r, (c0 + j8 * 8) / 8)) = u;
+              if (a.y1b && src == 0 && b < a.B)
+                *reinterpret_cast<uint4*>(a.y1b + ((int64_t)b * 49 + p) * C + c0 + j8 * 8) = u;
+            }
+          }
+        }
+      }
+      tc::fence_async_smem();  // y1 (generic stores) -> the tensor core
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) {
+        tc::mbar_arrive(&y1_full);
+        tc::mbar_arrive(&t1_empty);
+      }
+      if (i == 0) enc_stamp(a.dbg && warp == 4, 12);
+    }
+  } else if (warp < 12) {
+    // ---- E2: conv2 epilogue -> h (valid 5x5 positions, HWC) ------------------------------------------
+    const int q = warp & 3;
+    for (int i = 0; i < nloc; ++i) {
+      const int job = blockIdx.x + i * gridDim.x;
+      const int src = job / ngroups, g = job - src * ngroups, b0 = g * kGF;
+      bf16_t* hout = a.hb[src];
+      tc::mbar_wait(&t2_full, i & 1);
+      tc::fence_after_sync();
+#pragma unroll 1
+      for (int t = 0; t < 3; ++t) {
+        const int r = t * 128 + q * 32 + lane, ii = r / 49, p = r - ii * 49, oy = p / 7, ox = p - oy * 7, b = b0 + ii;
+        const bool ok = ii < kGF && oy < 5 && ox < 5 && b < a.B;
+#pragma unroll
+        for (int c0 = 0; c0 < C; c0 += 32) {
+          float v[32];
+          tc::tmem_ld32(t_c2 + t * C + c0 + ((uint32_t)(q * 32) << 16), v);
+          if (ok) {
+#pragma unroll
+            for (int j8 = 0; j8 < 4; ++j8) {
+              float f[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) f[j] = fmaxf(v[j8 * 8 + j] + s_b2[c0 + j8 * 8 + j], 0.f);
+              *reinterpret_cast<uint4*>(hout + (int64_t)b * a.h_ld + (oy * 5 + ox) * C + c0 + j8 * 8) =
+                  tc::pack_bf16x8(f);
+            }
+          }
+        }
+      }
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&t2_empty);
+      if (i == 0) enc_stamp(a.dbg && warp == 8, 13);
+    }
+  } else {
+    // ---- M: the MMAs (whole warp, one elected lane issues) --------------------------------------------
+    const uint32_t id_c = tc::idesc_bf16(128, C);
+    const uint32_t a0 = tc::smem_u32(sm + L::a1), w0 = tc::smem_u32(sm + L::w), y0 = tc::smem_u32(sm + L::y1),
+                   w2 = w0 + C * 128;
+    if (nloc > 0) tc::mbar_wait(&wbar, 0);
+    for (int i = 0; i < nloc; ++i) {
+      tc::mbar_wait(&a1_full, i & 1);
+      if (i >= 1) tc::mbar_wait(&t1_empty, (i - 1) & 1);
+      tc::fence_after_sync();
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          tc::mma_bf16_e(t_c1 + t * C, tc::sdesc_k128(a0 + t * 16384 + 32 * k), tc::sdesc_k128(w0 + 32 * k), id_c, k);
+      tc::mma_commit_e(&a1_empty);
+      tc::mma_commit_e(&t1_full);
+      tc::mbar_wait(&y1_full, i & 1);
+      if (i >= 1) tc::mbar_wait(&t2_empty, (i - 1) & 1);
+      tc::fence_after_sync();
+      // conv2 as nine row-shifted GEMMs over the full 7x7 grid (see k_enc_fwd_tc)
+      for (int t = 0; t < 3; ++t)
+        for (int tap = 0; tap < 9; ++tap) {
+          const int shift = (tap / 3) * 7 + tap % 3;
+          const int kb = (tap * C) / 64, koff = (tap * C) % 64;
+#pragma unroll
+          for (int k = 0; k < C / 16; ++k)
+            tc::mma_bf16_e(t_c2 + t * C, sdesc_sw(y0 + (t * 128 + shift) * C * 2 + 32 * k, C * 2),
+                           tc::sdesc_k128(w2 + kb * C * 128 + (koff + 16 * k) * 2), id_c, (tap | k) != 0);
+        }
+      tc::mma_commit_e(&y1_empty);
+      tc::mma_commit_e(&t2_full);
+    }
+  }
+  if (tid == 32 && nloc == 0) tc::mbar_wait(&wbar, 0);  // never exit with the bulk copy in flight
+  tc::fence_before_sync();
+  __syncthreads();
+  enc_stamp(a.dbg, 15);
+  if (warp == 0) tc::tmem_dealloc(tmem, 512);
+}
+
 // ---- backward --------------------------------------------------------------------------------
 template <int C>
 struct BwdL {
@@ -712,6 +981,15 @@ __global__ void __launch_bounds__(256) k_reduce_enc(const float* __restrict__ pa
 
 template <int C>
 int launch_fwd_c(const EncFwdArgs& a, cudaStream_t s) {
+  if (a.mode == 0 || a.factor == 1) {  // the pipelined kernel (everything but the fused squint)
+    const size_t smem = FwdW<C>::total + 1024;
+    cudaFuncSetAttribute(k_enc_fwd_ws<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int total = ((a.B + kGF - 1) / kGF) * a.nsrc;
+    const int cap = a.max_ctas > 0 && a.max_ctas < 148 ? a.max_ctas : 148;
+    const int grid = total < cap ? total : cap;
+    launch_pdl(k_enc_fwd_ws<C>, grid, dim3(kWsWarps * 32), smem, s, a);
+    return (int)cudaGetLastError();
+  }
   const size_t smem = FwdL<C>::total + 1024;
   cudaFuncSetAttribute(k_enc_fwd_tc<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int total = ((a.B + kGF - 1) / kGF) * a.nsrc;

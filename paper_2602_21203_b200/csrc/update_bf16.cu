@@ -221,6 +221,7 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
 struct Aux {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, scal = nullptr, join = nullptr, alpha = nullptr, qdone = nullptr;
+  cudaEvent_t dh = nullptr;  // the branch's dh GEMM has read the critic projection's (pre-step) shadow
   cudaEvent_t enc = nullptr, chn = nullptr;  // pipelined forward of the next update: encoder + projections, online heads
   bool ok() {
     if (s) return true;
@@ -231,6 +232,7 @@ struct Aux {
            cudaEventCreateWithFlags(&qdone, cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&enc, cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&chn, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&dh, cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
   }
 };
@@ -260,9 +262,6 @@ struct Ctx {
   // head i of a [2B][N] matrix
   Mat half(const BM& m, int i) const {
     return Mat{ws + m.off + (size_t)i * (m.rows / 2) * m.ld * 2, m.rows / 2, m.cols, m.ld};
-  }
-  bf16* halfp(const BM& m, int i) const {
-    return reinterpret_cast<bf16*>(ws + m.off + (size_t)i * (m.rows / 2) * m.ld * 2);
   }
 };
 
@@ -826,6 +825,9 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     p.out = c.bp(w.dh);
     p.ldo = w.dh.ld;
     BF_CK(gemm_launch(gb, es));
+    // the critic Adam on the main stream rewrites this weight's bf16 shadow with theta+: it waits
+    // until the dh GEMM (backward through theta) has read it
+    if (branch) BF_CK(cudaEventRecord(c.aux->dh, es));
   }
   {
     PhaseScope ps(10, rep, es);
@@ -888,6 +890,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
       // heads + projection on the main stream (the actor loss needs theta+ of those only), the
       // encoder slice on the branch once its gradient is reduced
       const int64_t e0 = L.enc_end;
+      BF_CK(cudaStreamWaitEvent(s, c.aux->dh, 0));
       BF_CK(launch_adam_shadow(st.critic + e0, gc + e0, st.m_critic + e0, st.v_critic + e0, L.gsize[gC] - e0,
                                hp.lr_critic, hp.beta1, hp.beta2, hp.adam_eps, scal + S_C1_CRITIC, scal + S_C2_CRITIC,
                                c.F(w.adam_part), &shC, s, e0, kAdamBlocks, 1));
@@ -1120,6 +1123,7 @@ bool bf16_region(const squint_dims& d, int region, size_t* offset, size_t* bytes
     case 7: *offset = w.scal; *bytes = kScal * f; break;
     case 8: *offset = w.img0; *bytes = B * d.img_c * d.img_h * d.img_w; break;
     case 9: *offset = w.img1; *bytes = B * d.img_c * d.img_h * d.img_w; break;
+    case 10: *offset = w.y1b; *bytes = B * conv1_out(d) * conv1_out(d) * d.conv_ch * 2; break;
     default: return false;
   }
   return true;

@@ -17,7 +17,7 @@ GROUP_CRITIC, GROUP_ACTOR, GROUP_ALPHA, GROUP_TARGET = 0, 1, 2, 3
 GROUP_NAMES = {GROUP_CRITIC: "critic", GROUP_ACTOR: "actor", GROUP_ALPHA: "alpha", GROUP_TARGET: "target"}
 STATUS = {0: "OK", 1: "EINVAL", 2: "ESHAPE", 3: "ECUDA", 4: "ENCCL", 5: "EUNSUPPORTED"}
 REGION = {"grad_critic": 0, "grad_actor": 1, "m": 2, "h": 3, "logp": 4, "logp_next": 5, "a_cur": 6, "scal": 7,
-          "obs_shifted": 8, "next_obs_shifted": 9}
+          "obs_shifted": 8, "next_obs_shifted": 9, "y1": 10}
 
 
 class SquintError(RuntimeError):

@@ -129,3 +129,26 @@ def test_target_exact_landing_dyadic(precision):
     trace = []
     pr.oracle_update(trace)
     assert np.array_equal(trace[0]["m"], exp.astype(np.float64))
+
+
+# ---- races: the forked graph branch (encoder backward beside the critic dW / actor pass) --------
+@pytest.mark.parametrize("cfg,kw", [("c2", dict(capacity=4096)), ("c3", dict(capacity=4096, batch=512)),
+                                    ("c3", dict(capacity=8192))])
+def test_update_bf16_bitwise_reproducible(cfg, kw):
+    """The bf16 update with its forked branch is bitwise reproducible over repeated calls (fixed-order
+    reductions, no float atomics): a branch kernel reading a buffer the main stream rewrites (e.g. a
+    weight shadow stepped by Adam) would show up here as run-to-run differences."""
+    pr = Problem(cfg, utd=2, seed=6, **kw)
+    ref = None
+    for rep in range(6):
+        L = pr.gpu_setup(precision=P.BF16)
+        pr.gpu_update(L)
+        out = {g: L.buffer(b).cpu().numpy().copy() for g, b in (("critic", P.squint.GROUP_CRITIC),
+                                                                ("actor", P.squint.GROUP_ACTOR),
+                                                                ("target", P.squint.GROUP_TARGET))}
+        out["grad"] = L.grad(P.squint.GROUP_CRITIC).cpu().numpy().copy()
+        if ref is None:
+            ref = out
+        else:
+            for k in ref:
+                assert np.array_equal(ref[k], out[k]), (k, rep)
