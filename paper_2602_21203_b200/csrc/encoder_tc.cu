@@ -745,25 +745,39 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ 
   for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++gi) {
     const int b0 = g * kGB;
     const bool first = gi == 0;
-    // ---- load D2 (MN-major SW128, rows r2 = img * 25 + p), y1 rows (HWC), images ----------------
-    for (int e = tid; e < 128 * 8; e += kThr) {
-      const int r2 = e >> 3, ch = e & 7, i = r2 / 25, p = r2 - i * 25, b = b0 + i;
-      uint4 u = make_uint4(0, 0, 0, 0);
-      if (r2 < kGB * 25 && b < a.B && ch < cch)
-        u = *reinterpret_cast<const uint4*>(a.dA2_hwc + (int64_t)b * a.dA2_ld + p * C + ch * 8);
-      *reinterpret_cast<uint4*>(sm + L::d2s + (r2 >> 6) * 8192 + sw(r2 & 63, ch)) = u;
-    }
-    for (int e = tid; e < kGB * 49 * cch; e += kThr) {
-      const int r1 = e / cch, ch = e - r1 * cch, i = r1 / 49, p = r1 - i * 49, b = b0 + i;
-      uint4 u = make_uint4(0, 0, 0, 0);
-      if (b < a.B) u = *reinterpret_cast<const uint4*>(a.y1_hwc + ((int64_t)b * 49 + p) * C + ch * 8);
-      *reinterpret_cast<uint4*>(y1s + r1 * C + ch * 8) = u;
-    }
-    for (int e = tid; e < kGB * 48; e += kThr) {  // 16-byte chunks of the images
-      const int i = e / 48, b = b0 + i;
-      uint4 u = make_uint4(0, 0, 0, 0);
-      if (b < a.B) u = *reinterpret_cast<const uint4*>(a.img + (int64_t)b * 768 + (e - i * 48) * 16);
-      *reinterpret_cast<uint4*>(xs + e * 16) = u;
+    // ---- load D2 (MN-major SW128, rows r2 = img * 25 + p), y1 rows (HWC), images: every global load
+    // of the group is issued before any is stored (one memory latency instead of one per item) ----------
+    {
+      constexpr int n_d2 = 128 * 8 / kThr, n_y1 = (kGB * 49 * cch + kThr - 1) / kThr;
+      uint4 ud[n_d2], uy[n_y1], ux;
+#pragma unroll
+      for (int k = 0; k < n_d2; ++k) {
+        const int e = tid + k * kThr, r2 = e >> 3, ch = e & 7, i = r2 / 25, p = r2 - i * 25, b = b0 + i;
+        ud[k] = make_uint4(0, 0, 0, 0);
+        if (r2 < kGB * 25 && b < a.B && ch < cch)
+          ud[k] = *reinterpret_cast<const uint4*>(a.dA2_hwc + (int64_t)b * a.dA2_ld + p * C + ch * 8);
+      }
+#pragma unroll
+      for (int k = 0; k < n_y1; ++k) {
+        const int e = tid + k * kThr, r1 = e / cch, ch = e - r1 * cch, i = r1 / 49, p = r1 - i * 49, b = b0 + i;
+        uy[k] = make_uint4(0, 0, 0, 0);
+        if (e < kGB * 49 * cch && b < a.B)
+          uy[k] = *reinterpret_cast<const uint4*>(a.y1_hwc + ((int64_t)b * 49 + p) * C + ch * 8);
+      }
+      ux = make_uint4(0, 0, 0, 0);
+      if (tid < kGB * 48 && b0 + tid / 48 < a.B)  // 16-byte chunks of the images
+        ux = *reinterpret_cast<const uint4*>(a.img + (int64_t)(b0 + tid / 48) * 768 + (tid % 48) * 16);
+#pragma unroll
+      for (int k = 0; k < n_d2; ++k) {
+        const int e = tid + k * kThr, r2 = e >> 3, ch = e & 7;
+        *reinterpret_cast<uint4*>(sm + L::d2s + (r2 >> 6) * 8192 + sw(r2 & 63, ch)) = ud[k];
+      }
+#pragma unroll
+      for (int k = 0; k < n_y1; ++k) {
+        const int e = tid + k * kThr, r1 = e / cch, ch = e - r1 * cch;
+        if (e < kGB * 49 * cch) *reinterpret_cast<uint4*>(y1s + r1 * C + ch * 8) = uy[k];
+      }
+      if (tid < kGB * 48) *reinterpret_cast<uint4*>(xs + tid * 16) = ux;
     }
     __syncthreads();
     enc_stamp(dbg && first, 2);
@@ -771,19 +785,27 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ 
     for (int kb = 0; kb < nkb2; ++kb, ++it) {
       int st;
       uint8_t* A = stage_acquire(st);
-      for (int e = tid; e < 256 * 8; e += kThr) {
-        const int r1 = e >> 3, ch = e & 7;
-        const int k = kb * 64 + ch * 8, t = k / C, o0 = k - t * C;
-        uint4 u = make_uint4(0, 0, 0, 0);
-        if (r1 < kGB * 49 && t < 9) {
-          const int i = r1 / 49, p = r1 - i * 49, y = p / 7, x = p - y * 7, ki = t / 3, kj = t - ki * 3;
-          const int yy = y - ki, xx = x - kj;
-          if (yy >= 0 && yy < 5 && xx >= 0 && xx < 5) {
-            const int r2 = i * 25 + yy * 5 + xx;
-            u = *reinterpret_cast<const uint4*>(sm + L::d2s + (r2 >> 6) * 8192 + sw(r2 & 63, o0 >> 3));
+      {
+        uint4 u[256 * 8 / kThr];
+#pragma unroll
+        for (int n = 0; n < 256 * 8 / kThr; ++n) {
+          const int e = tid + n * kThr, r1 = e >> 3, ch = e & 7;
+          const int k = kb * 64 + ch * 8, t = k / C, o0 = k - t * C;
+          u[n] = make_uint4(0, 0, 0, 0);
+          if (r1 < kGB * 49 && t < 9) {
+            const int i = r1 / 49, p = r1 - i * 49, y = p / 7, x = p - y * 7, ki = t / 3, kj = t - ki * 3;
+            const int yy = y - ki, xx = x - kj;
+            if (yy >= 0 && yy < 5 && xx >= 0 && xx < 5) {
+              const int r2 = i * 25 + yy * 5 + xx;
+              u[n] = *reinterpret_cast<const uint4*>(sm + L::d2s + (r2 >> 6) * 8192 + sw(r2 & 63, o0 >> 3));
+            }
           }
         }
-        *reinterpret_cast<uint4*>(A + (r1 >> 7) * 16384 + sw(r1 & 127, ch)) = u;
+#pragma unroll
+        for (int n = 0; n < 256 * 8 / kThr; ++n) {
+          const int e = tid + n * kThr, r1 = e >> 3, ch = e & 7;
+          *reinterpret_cast<uint4*>(A + (r1 >> 7) * 16384 + sw(r1 & 127, ch)) = u[n];
+        }
       }
       built();
       if (tid == 0) {
@@ -806,21 +828,31 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ 
     for (int mt = 0; mt < nt2; ++mt, ++it) {
       int st;
       uint8_t* A = stage_acquire(st);
-      for (int e = tid; e < 2 * 2 * 64 * 8; e += kThr) {  // (kb, atom, K row, chunk)
-        const int kb = e >> 10, j = (e >> 9) & 1, rr = (e >> 3) & 63, ch = e & 7, r2 = kb * 64 + rr;
-        const int m0 = mt * 128 + j * 64 + ch * 8, t = m0 / C, c0 = m0 - t * C;
-        const int i = r2 / 25, p = r2 - i * 25;
-        const bool rv = r2 < kGB * 25 && b0 + i < a.B;
-        uint4 u = make_uint4(0, 0, 0, 0);
-        if (rv) {
-          if (t < 9) {
-            const int oy = p / 5, ox = p - oy * 5, ki = t / 3, kj = t - ki * 3;
-            u = *reinterpret_cast<const uint4*>(y1s + (i * 49 + (oy + ki) * 7 + ox + kj) * C + c0);
-          } else if (m0 == 9 * C) {
-            u.x = 0x3F80u;  // bf16 1.0 in element 0
+      {
+        uint4 u[2048 / kThr];
+#pragma unroll
+        for (int n = 0; n < 2048 / kThr; ++n) {  // (kb, atom, K row, chunk)
+          const int e = tid + n * kThr;
+          const int kb = e >> 10, j = (e >> 9) & 1, rr = (e >> 3) & 63, ch = e & 7, r2 = kb * 64 + rr;
+          const int m0 = mt * 128 + j * 64 + ch * 8, t = m0 / C, c0 = m0 - t * C;
+          const int i = r2 / 25, p = r2 - i * 25;
+          const bool rv = r2 < kGB * 25 && b0 + i < a.B;
+          u[n] = make_uint4(0, 0, 0, 0);
+          if (rv) {
+            if (t < 9) {
+              const int oy = p / 5, ox = p - oy * 5, ki = t / 3, kj = t - ki * 3;
+              u[n] = *reinterpret_cast<const uint4*>(y1s + (i * 49 + (oy + ki) * 7 + ox + kj) * C + c0);
+            } else if (m0 == 9 * C) {
+              u[n].x = 0x3F80u;  // bf16 1.0 in element 0
+            }
           }
         }
-        *reinterpret_cast<uint4*>(A + kb * 16384 + j * 8192 + sw(rr, ch)) = u;
+#pragma unroll
+        for (int n = 0; n < 2048 / kThr; ++n) {
+          const int e = tid + n * kThr;
+          const int kb = e >> 10, j = (e >> 9) & 1, rr = (e >> 3) & 63, ch = e & 7;
+          *reinterpret_cast<uint4*>(A + kb * 16384 + j * 8192 + sw(rr, ch)) = u[n];
+        }
       }
       built();
       if (tid == 0) {

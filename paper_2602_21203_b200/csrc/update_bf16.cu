@@ -68,7 +68,10 @@ struct BfLay {
   FB part_q2[2], part_q1[2], part_pq, part_a2, part_a1, part_pp;  // LayerNorm column partials
   size_t grad_critic, grad_actor, adam_part, scal, lpi_sums;
   size_t y1b, img0, img1, dA1enc, enc_part, wtiles;
-  ShadowPlan sh[3];  // critic, target, actor
+  // bf16 shadows: critic, target, actor, and a second critic set -- update j reads the critic set of
+  // parity j (theta) and its Adam writes the other one (theta+), so a kernel still reading theta on the
+  // forked branch (the dh GEMM) never races the main stream's Adam (with_parity swaps sh[0] / sh[3])
+  ShadowPlan sh[4];
   size_t total;
 };
 
@@ -211,6 +214,7 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
   w.sh[0] = shadow_plan(P, d, L, SQUINT_GROUP_CRITIC);
   w.sh[1] = shadow_plan(P, d, L, SQUINT_GROUP_TARGET);
   w.sh[2] = shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
+  w.sh[3] = shadow_plan(P, d, L, SQUINT_GROUP_CRITIC);
   w.total = P.top + 256;
   return w;
 }
@@ -221,7 +225,6 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
 struct Aux {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, scal = nullptr, join = nullptr, alpha = nullptr, qdone = nullptr;
-  cudaEvent_t dh = nullptr;  // the branch's dh GEMM has read the critic projection's (pre-step) shadow
   cudaEvent_t enc = nullptr, chn = nullptr;  // pipelined forward of the next update: encoder + projections, online heads
   bool ok() {
     if (s) return true;
@@ -232,7 +235,6 @@ struct Aux {
            cudaEventCreateWithFlags(&qdone, cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&enc, cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&chn, cudaEventDisableTiming) == cudaSuccess &&
-           cudaEventCreateWithFlags(&dh, cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
   }
 };
@@ -398,6 +400,8 @@ struct UpdIn {
 BfLay with_parity(const BfLay& w, int par) {
   BfLay v = w;
   if (par & 1) {
+    v.sh[0] = w.sh[3];
+    v.sh[3] = w.sh[0];
     v.Xh = w.Xh_alt;
     v.Xq1 = w.Xq1_alt;
     v.Xac = w.Xac_alt;
@@ -825,9 +829,6 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     p.out = c.bp(w.dh);
     p.ldo = w.dh.ld;
     BF_CK(gemm_launch(gb, es));
-    // the critic Adam on the main stream rewrites this weight's bf16 shadow with theta+: it waits
-    // until the dh GEMM (backward through theta) has read it
-    if (branch) BF_CK(cudaEventRecord(c.aux->dh, es));
   }
   {
     PhaseScope ps(10, rep, es);
@@ -878,7 +879,9 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     BF_CK(launch_row_sums(c.F(w.logp_cur), c.F(w.row_loss), B, extras, s));
     if (comm_allreduce_sum(comm, gc, L.gsize[gC] + kExtra, s) != 0) return set_error(SQUINT_ENCCL, comm_error());
   }
-  const ShadowTable shC = table_at(c, w.sh[0]), shT = table_at(c, w.sh[1]), shA = table_at(c, w.sh[2]);
+  // the critic Adam writes theta+ into the other critic shadow set (read by the actor pass below and by
+  // the next update); theta's set stays intact for the branch
+  const ShadowTable shC = table_at(c, w.sh[3]), shT = table_at(c, w.sh[1]), shA = table_at(c, w.sh[2]);
   // a11 temperature step + Adam bias corrections; a13 Adam on the critic group (+ shadow)
   {
     PhaseScope ps(11, rep, s);
@@ -890,7 +893,6 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
       // heads + projection on the main stream (the actor loss needs theta+ of those only), the
       // encoder slice on the branch once its gradient is reduced
       const int64_t e0 = L.enc_end;
-      BF_CK(cudaStreamWaitEvent(s, c.aux->dh, 0));
       BF_CK(launch_adam_shadow(st.critic + e0, gc + e0, st.m_critic + e0, st.v_critic + e0, L.gsize[gC] - e0,
                                hp.lr_critic, hp.beta1, hp.beta2, hp.adam_eps, scal + S_C1_CRITIC, scal + S_C2_CRITIC,
                                c.F(w.adam_part), &shC, s, e0, kAdamBlocks, 1));
@@ -918,8 +920,8 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   // a12: actor loss against theta+ on sg(h) (Q19)
   {
     PhaseScope ps(12, rep, s);
-    const Lin cproj1 = proj(c, w.sh[0], crit, gC, "critic");  // same buffers, now theta+
-    const Mlp cq1[2] = {mlp(c, w.sh[0], crit, gC, kHeads[0]), mlp(c, w.sh[0], crit, gC, kHeads[1])};
+    const Lin cproj1 = proj(c, w.sh[3], crit, gC, "critic");  // theta+ (the other shadow set)
+    const Mlp cq1[2] = {mlp(c, w.sh[3], crit, gC, kHeads[0]), mlp(c, w.sh[3], crit, gC, kHeads[1])};
     {
       GemmBuilder gb(0);  // theta+ shadow was written by the immediately preceding Adam kernel
       GProb& p = fwd(gb, c.mat(w.Xh), cproj1, GE_LN_TANH, c.bp(w.Xq1), w.Xq1.ld, le);
@@ -986,8 +988,8 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   }
   {
     PhaseScope ps(13, rep, s);
-    const Lin cproj1 = proj(c, w.sh[0], crit, gC, "critic");
-    const Mlp cq1[2] = {mlp(c, w.sh[0], crit, gC, kHeads[0]), mlp(c, w.sh[0], crit, gC, kHeads[1])};
+    const Lin cproj1 = proj(c, w.sh[3], crit, gC, "critic");
+    const Mlp cq1[2] = {mlp(c, w.sh[3], crit, gC, kHeads[0]), mlp(c, w.sh[3], crit, gC, kHeads[1])};
     (void)cproj1;
     {
       GemmBuilder gb(1);
