@@ -692,13 +692,13 @@ __host__ __device__ constexpr int part_rows(int C) { return 9 * C + 1 + 28; }  /
 
 
 template <int C>
-__global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ EncBwdArgs a, int dbg) {
+__global__ void __launch_bounds__(kThr + 32, 1) k_enc_bwd_tc(const __grid_constant__ EncBwdArgs a, int dbg) {
   using L = BwdL<C>;
   constexpr int nkb2 = (9 * C + 63) / 64, nt2 = (9 * C + 1 + 127) / 128, cch = C / 8;
   constexpr uint32_t kCols = C == 32 ? 256u : 512u;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t wbar, bar_dx, bar_grp, empty[2];
+  __shared__ uint64_t wbar, bar_dx, bar_grp, empty[2], full[2];
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = warp & 3, hh = warp >> 2;
   const int ngroups = (a.B + kGB - 1) / kGB;
@@ -711,6 +711,8 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ 
     tc::mbar_init(&bar_grp, 1);
     tc::mbar_init(&empty[0], 1);
     tc::mbar_init(&empty[1], 1);
+    tc::mbar_init(&full[0], kThr / 32);
+    tc::mbar_init(&full[1], kThr / 32);
     tc::fence_mbar_init();
   }
   tc::fence_before_sync();
@@ -736,12 +738,65 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ 
     if (it >= 2) tc::mbar_wait(&empty[st], ((it >> 1) - 1) & 1);
     return sm + L::ring + st * 32768;
   };
-  auto built = [&]() {
+  // warps 0-7 build the operand tiles and run the epilogues; warp 8 issues the MMAs (warp-uniform,
+  // elected lane): a built stage is published on full[st] (one arrive per builder warp), the MMAs
+  // release it on empty[st]
+  auto built = [&](int st) {
     tc::fence_async_smem();
     tc::fence_before_sync();
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(&full[st]);
   };
-
+  if (warp == kThr / 32) {
+    // ---- MMA warp ------------------------------------------------------------------------------------
+    int mit = 0, mgi = 0;
+    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++mgi) {
+      const bool first = mgi == 0;
+      auto take = [&]() {
+        const int st = mit & 1;
+        tc::mbar_wait(&full[st], (mit >> 1) & 1);
+        tc::fence_after_sync();
+        return tc::smem_u32(sm + L::ring + st * 32768);
+      };
+      for (int kb = 0; kb < nkb2; ++kb, ++mit) {
+        const uint32_t a0 = take();
+        if (mit == 0) tc::mbar_wait(&wbar, 0);
+        const uint32_t w0 = tc::smem_u32(sm + L::w + kb * C * 128);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tc::mma_bf16_e(t_dx + mt * C, tc::sdesc_k128(a0 + mt * 16384 + 32 * k), tc::sdesc_k128(w0 + 32 * k), id_k,
+                           (kb | k) != 0);
+        tc::mma_commit_e(&empty[mit & 1]);
+        if (kb == nkb2 - 1) tc::mma_commit_e(&bar_dx);
+      }
+      for (int mt = 0; mt < nt2; ++mt, ++mit) {
+        const uint32_t a0 = take(), b0s = tc::smem_u32(sm + L::d2s);
+#pragma unroll
+        for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tc::mma_bf16_e(t_w2 + mt * C, tc::sdesc_sw128(a0 + kb * 16384 + 2048 * k, 8192, 1024),
+                           tc::sdesc_sw128(b0s + kb * 8192 + 2048 * k, 8192, 1024), id_mn,
+                           !(first && kb == 0 && k == 0));
+        tc::mma_commit_e(&empty[mit & 1]);
+      }
+      for (int s2 = 0; s2 < 2; ++s2, ++mit) {
+        const uint32_t a0 = take(), b0s = tc::smem_u32(sm + L::a1s + 2 * s2 * 8192);
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tc::mma_bf16_e(t_w1, tc::sdesc_sw128(a0 + kk * 16384 + 2048 * k, 8192, 1024),
+                           tc::sdesc_sw128(b0s + kk * 8192 + 2048 * k, 8192, 1024), id_mn,
+                           !(first && s2 == 0 && kk == 0 && k == 0));
+        tc::mma_commit_e(&empty[mit & 1]);
+        if (s2 == 1) tc::mma_commit_e(&bar_grp);
+      }
+    }
+    if (mgi == 0) tc::mbar_wait(&wbar, 0);  // never exit with the bulk copy in flight
+  } else {
   for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++gi) {
     const int b0 = g * kGB;
     const bool first = gi == 0;
@@ -779,7 +834,7 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ 
       }
       if (tid < kGB * 48) *reinterpret_cast<uint4*>(xs + tid * 16) = ux;
     }
-    __syncthreads();
+    tc::named_bar(1, kThr);
     enc_stamp(dbg && first, 2);
     // ---- conv2 dX: per K block both row tiles ---------------------------------------------------
     for (int kb = 0; kb < nkb2; ++kb, ++it) {
@@ -807,20 +862,7 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ 
           *reinterpret_cast<uint4*>(A + (r1 >> 7) * 16384 + sw(r1 & 127, ch)) = u[n];
         }
       }
-      built();
-      if (tid == 0) {
-        if (it == 0) tc::mbar_wait(&wbar, 0);
-        tc::fence_after_sync();
-        const uint32_t a0 = tc::smem_u32(A), w0 = tc::smem_u32(sm + L::w + kb * C * 128);
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            tc::mma_bf16(t_dx + mt * C, tc::sdesc_k128(a0 + mt * 16384 + 32 * k), tc::sdesc_k128(w0 + 32 * k), id_k,
-                         (kb | k) != 0);
-        tc::mma_commit(&empty[st]);
-        if (kb == nkb2 - 1) tc::mma_commit(&bar_dx);
-      }
+      built(st);
     }
     enc_stamp(dbg && first, 3);
     // ---- conv2 dW (+ db2 via the ones row), accumulated across groups: per step one row tile,
@@ -854,19 +896,7 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ 
           *reinterpret_cast<uint4*>(A + kb * 16384 + j * 8192 + sw(rr, ch)) = u[n];
         }
       }
-      built();
-      if (tid == 0) {
-        tc::fence_after_sync();
-        const uint32_t a0 = tc::smem_u32(A), b0s = tc::smem_u32(sm + L::d2s);
-#pragma unroll
-        for (int kb = 0; kb < 2; ++kb)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            tc::mma_bf16(t_w2 + mt * C, tc::sdesc_sw128(a0 + kb * 16384 + 2048 * k, 8192, 1024),
-                         tc::sdesc_sw128(b0s + kb * 8192 + 2048 * k, 8192, 1024), id_mn,
-                         !(first && kb == 0 && k == 0));
-        tc::mma_commit(&empty[st]);
-      }
+      built(st);
     }
     enc_stamp(dbg && first, 4);
     // ---- dX epilogue: dA1 = dy1 * (y1 > 0) -> smem (MN-major rows r1); warp (q, hh) -> tile hh -----
@@ -907,8 +937,7 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ 
     }
     tc::fence_async_smem();
     tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
+    tc::named_bar(1, kThr);
     enc_stamp(dbg && first, 6);
     // ---- conv1 dW (+ db1), accumulated across groups: 2 steps of 2 K blocks -----------------------
     for (int s2 = 0; s2 < 2; ++s2, ++it) {
@@ -930,25 +959,12 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ 
         }
         *reinterpret_cast<uint4*>(A + kk * 16384 + j * 8192 + sw(rr, ch)) = tc::pack_bf16x8(f);
       }
-      built();
-      if (tid == 0) {
-        tc::fence_after_sync();
-        const uint32_t a0 = tc::smem_u32(A), b0s = tc::smem_u32(sm + L::a1s + 2 * s2 * 8192);
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            tc::mma_bf16(t_w1, tc::sdesc_sw128(a0 + kk * 16384 + 2048 * k, 8192, 1024),
-                         tc::sdesc_sw128(b0s + kk * 8192 + 2048 * k, 8192, 1024), id_mn,
-                         !(first && s2 == 0 && kk == 0 && k == 0));
-        tc::mma_commit(&empty[st]);
-        if (s2 == 1) tc::mma_commit(&bar_grp);
-      }
+      built(st);
     }
     enc_stamp(dbg && first, 7);
     tc::mbar_wait(&bar_grp, gi & 1);  // every MMA of the group done: smem inputs may be reused
     tc::fence_after_sync();
-    __syncthreads();
+    tc::named_bar(1, kThr);
     enc_stamp(dbg && first, 8);
   }
   // ---- per-CTA partials, row-major [row][o]: rows 0..9C = dW2 (t, c) (+ db2), then dW1 (ci, t) (+ db1)
@@ -972,7 +988,7 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_bwd_tc(const __grid_constant__ 
       }
     }
   }
-  if (tid == 0 && gi == 0) tc::mbar_wait(&wbar, 0);  // never exit with the bulk copy in flight
+  }  // builders
   tc::fence_before_sync();
   __syncthreads();
   enc_stamp(dbg, 9);
@@ -1034,7 +1050,7 @@ template <int C>
 int launch_bwd_c(const EncBwdArgs& a, int grid, int dbg, cudaStream_t s) {
   const size_t smem = BwdL<C>::total + 1024;
   cudaFuncSetAttribute(k_enc_bwd_tc<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  launch_pdl(k_enc_bwd_tc<C>, grid, dim3(kThr), smem, s, a, dbg);
+  launch_pdl(k_enc_bwd_tc<C>, grid, dim3(kThr + 32), smem, s, a, dbg);
   return (int)cudaGetLastError();
 }
 
