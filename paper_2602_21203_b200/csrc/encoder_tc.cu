@@ -426,6 +426,9 @@ struct FwdW {
   static constexpr uint32_t y1 = a1 + 3 * 16384;
   static constexpr uint32_t xs = y1 + ((416u * C * 2 + 1023) & ~1023u);
   static constexpr uint32_t total = xs + kGF * 768;
+  // fused squint (act, mode 1 with factor 8; C = 32 only): a 2-slot ring of rendered 3x128x128 frames
+  static constexpr uint32_t fring = (total + 1023) & ~1023u;
+  static constexpr uint32_t total_sq = fring + 2 * 49152;
 };
 
 template <int C>
@@ -433,7 +436,7 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
   using L = FwdW<C>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t wbar, a1_full, a1_empty, t1_full, t1_empty, y1_full, y1_empty, t2_full, t2_empty;
+  __shared__ uint64_t wbar, a1_full, a1_empty, t1_full, t1_empty, y1_full, y1_empty, t2_full, t2_empty, fbar[2];
   __shared__ uint32_t tmem_slot;
   __shared__ int s_koff[32];
   __shared__ float s_b1[64], s_b2[64];
@@ -454,6 +457,8 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
     tc::mbar_init(&y1_empty, 1);
     tc::mbar_init(&t2_full, 1);
     tc::mbar_init(&t2_empty, 4);
+    tc::mbar_init(&fbar[0], 1);
+    tc::mbar_init(&fbar[1], 1);
     tc::fence_mbar_init();
   }
   if (warp == 2) {
@@ -481,6 +486,26 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
   if (warp < 4) {
     // ---- P: stage + conv1 im2col --------------------------------------------------------------------
     const int pt = tid;  // 0..127
+    // fused squint: frame k of this CTA (k = i * kGF + ii) streams into ring slot k % 2 by one bulk copy
+    // (49,152 B, completion on fbar[k % 2]); the copy of frame k + 2 is issued once frame k is reduced
+    const bool squint = a.mode == 1 && a.factor == 8;
+    const int nfr = nloc * kGF;
+    auto frame_b = [&](int k) {  // image index of this CTA's frame k, or -1
+      const int job = blockIdx.x + (k / kGF) * gridDim.x;
+      const int b = (job % ngroups) * kGF + k % kGF;
+      return b < a.B ? b : -1;
+    };
+    auto issue_frame = [&](int k) {
+      const int b = k < nfr ? frame_b(k) : -1;
+      if (pt == 0 && b >= 0) {
+        tc::mbar_expect_tx(&fbar[k & 1], 49152u);
+        tc::bulk_load_1d(sm + L::fring + (k & 1) * 49152, a.src[0] + (int64_t)b * 49152, 49152u, &fbar[k & 1]);
+      }
+    };
+    if (squint) {
+      issue_frame(0);
+      issue_frame(1);
+    }
     for (int i = 0; i < nloc; ++i) {
       const int job = blockIdx.x + i * gridDim.x;
       const int src = job / ngroups, g = job - src * ngroups, b0 = g * kGF;
@@ -509,6 +534,35 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
             if (dump) *reinterpret_cast<uint4*>(dump + (int64_t)b * 768 + cc * 256 + y * 16) = o;
           }
           *reinterpret_cast<uint4*>(xs + ii * 768 + cc * 256 + y * 16) = o;
+        }
+      } else if (squint) {
+        // 8x8 block sums of each frame from shared memory, round half to even (Q1) -> xs (+ ring)
+        for (int ii = 0; ii < kGF; ++ii) {
+          const int k = i * kGF + ii, b = b0 + ii;
+          uint8_t* dst = xs + ii * 768;
+          if (b < a.B) {
+            tc::mbar_wait(&fbar[k & 1], (k >> 1) & 1);
+            const uint8_t* F = sm + L::fring + (k & 1) * 49152;
+            for (int e = pt; e < 3 * 16 * 8; e += 128) {  // (channel, output row, 16-byte column chunk)
+              const int ck = e & 7, oy = (e >> 3) & 15, cc = e >> 7;
+              const uint8_t* src = F + (cc * 128 + oy * 8) * 128 + ck * 16;
+              uint32_t lo = 0, hi = 0;
+#pragma unroll
+              for (int r = 0; r < 8; ++r) {
+                const uint4 v = *reinterpret_cast<const uint4*>(src + r * 128);
+                lo = __dp4a(v.x, 0x01010101u, __dp4a(v.y, 0x01010101u, lo));
+                hi = __dp4a(v.z, 0x01010101u, __dp4a(v.w, 0x01010101u, hi));
+              }
+              const uint16_t q = (uint16_t)(rhe64(lo) | (rhe64(hi) << 8));
+              const int off = cc * 256 + oy * 16 + 2 * ck;
+              *reinterpret_cast<uint16_t*>(dst + off) = q;
+              if (a.ring) *reinterpret_cast<uint16_t*>(a.ring + a.slots[b] * 768 + off) = q;
+            }
+          } else {
+            for (int e = pt; e < 48; e += 128) reinterpret_cast<uint4*>(dst)[e] = make_uint4(0, 0, 0, 0);
+          }
+          tc::named_bar(1, 128);  // slot k % 2 read by every P thread
+          issue_frame(k + 2);
         }
       } else {  // frames already at the stored resolution (factor 1): 768-byte copies
         const uint8_t* Fr = a.src[0];
@@ -1029,8 +1083,8 @@ __global__ void __launch_bounds__(256) k_reduce_enc(const float* __restrict__ pa
 
 template <int C>
 int launch_fwd_c(const EncFwdArgs& a, cudaStream_t s) {
-  if (a.mode == 0 || a.factor == 1) {  // the pipelined kernel (everything but the fused squint)
-    const size_t smem = FwdW<C>::total + 1024;
+  if (a.mode == 0 || a.factor == 1 || (a.factor == 8 && C == 32)) {  // the pipelined kernel
+    const size_t smem = (a.mode == 1 && a.factor == 8 ? FwdW<C>::total_sq : FwdW<C>::total) + 1024;
     cudaFuncSetAttribute(k_enc_fwd_ws<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int total = ((a.B + kGF - 1) / kGF) * a.nsrc;
     const int cap = a.max_ctas > 0 && a.max_ctas < 148 ? a.max_ctas : 148;
@@ -1072,7 +1126,8 @@ int launch_enc_fwd_tc(const EncFwdArgs& a, cudaStream_t s) {
     const double img = (double)a.B * a.nsrc, C = a.C;
     const double flops = 2.0 * img * (49.0 * C * 27.0 + 25.0 * 9.0 * C * C);
     const double bytes = (a.mode == 1 && a.factor == 8) ? img * (3.0 * 128 * 128 + 2.0 * 25 * C) : img * (768.0 + 2.0 * 25 * C);
-    note_launch(s, "k_enc_fwd_tc", flops, bytes);
+    const bool ws = a.mode == 0 || a.factor == 1 || (a.factor == 8 && a.C == 32);  // launch_fwd_c's choice
+    note_launch(s, ws ? "k_enc_fwd_ws" : "k_enc_fwd_tc", flops, bytes);
   }
   static const bool dbg = getenv("SQUINT_ENC_DBG") != nullptr;
   EncFwdArgs b = a;
