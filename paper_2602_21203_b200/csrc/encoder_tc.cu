@@ -733,26 +733,35 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
 // ---- backward --------------------------------------------------------------------------------
 template <int C>
 struct BwdL {
+  static constexpr int nst = C == 32 ? 4 : 2;  // ring stages of 16 KB (one K block of an operand tile)
   static constexpr uint32_t w = 0;
   static constexpr uint32_t d2s = (((9 * C + 63) / 64) * C * 128 + 1023) & ~1023u;
   static constexpr uint32_t a1s = d2s + 2 * 8192;
   static constexpr uint32_t ring = a1s + 4 * 8192;
-  static constexpr uint32_t y1s = ring + 2 * 32768;
+  static constexpr uint32_t d2p = ring + nst * 16384;  // D2 on zero-padded 9x9 grids, K-major rows
+  static constexpr uint32_t y1s = d2p + ((288u * C * 2 + 1023) & ~1023u);
   static constexpr uint32_t xs = y1s + ((kGB * 49 * C * 2 + 1023) & ~1023u);
   static constexpr uint32_t total = xs + kGB * 768;
 };
 __host__ __device__ constexpr int part_rows(int C) { return 9 * C + 1 + 28; }  // dW2 (+ db2), dW1 (+ db1)
 
-
-
+// Backward, one group of kGB = 4 images per CTA iteration.  Roles: warps 0-7 build operand tiles and
+// run the dX epilogue; warp 8 issues every MMA (warp-uniform, elected lane).
+//   conv2 dX as nine row-shifted GEMMs (no operand build): D2 of image i sits on a zero-padded 9x9 grid
+//     whose rows are i * 63 + Y * 9 + X (consecutive images share their two zero pad rows), so output
+//     (y, x) of the 7 x 9 grid, row o = i * 63 + y * 9 + x, reads D2pad row o + (2 - ki) * 9 + (2 - kj)
+//     for tap (ki, kj): tap t's A operand is the padded tile itself started that many rows later;
+//     B = W2 as [c][(t, o)]; positions x >= 7 are computed and dropped.  2 row tiles (252 rows).
+//   conv2 dW / conv1 dW: operand tiles built into a ring of 16 KB stages (one K block each) while the
+//     dX MMAs run; the dW accumulators stay in TMEM across the CTA's groups.
 template <int C>
 __global__ void __launch_bounds__(kThr + 32, 1) k_enc_bwd_tc(const __grid_constant__ EncBwdArgs a, int dbg) {
   using L = BwdL<C>;
-  constexpr int nkb2 = (9 * C + 63) / 64, nt2 = (9 * C + 1 + 127) / 128, cch = C / 8;
+  constexpr int nt2 = (9 * C + 1 + 127) / 128, cch = C / 8, NS = L::nst;
   constexpr uint32_t kCols = C == 32 ? 256u : 512u;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t wbar, bar_dx, bar_grp, empty[2], full[2];
+  __shared__ uint64_t wbar, bar_dx, bar_grp, d2_full, empty[NS], full[NS];
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = warp & 3, hh = warp >> 2;
   const int ngroups = (a.B + kGB - 1) / kGB;
@@ -763,12 +772,21 @@ __global__ void __launch_bounds__(kThr + 32, 1) k_enc_bwd_tc(const __grid_consta
     tc::mbar_init(&wbar, 1);
     tc::mbar_init(&bar_dx, 1);
     tc::mbar_init(&bar_grp, 1);
-    tc::mbar_init(&empty[0], 1);
-    tc::mbar_init(&empty[1], 1);
-    tc::mbar_init(&full[0], kThr / 32);
-    tc::mbar_init(&full[1], kThr / 32);
+    tc::mbar_init(&d2_full, kThr / 32);
+    for (int i = 0; i < NS; ++i) {
+      tc::mbar_init(&empty[i], 1);
+      tc::mbar_init(&full[i], kThr / 32);
+    }
     tc::fence_mbar_init();
   }
+  // dA1 rows 196 .. 255 (the K tail of conv1 dW) and, for C = 32, the unused half of every 128-byte
+  // row stay zero: written once here, never by the per-group epilogue
+  for (int e = tid; e < 256 * 8; e += kThr + 32) {
+    const int r1 = e >> 3, ch = e & 7;
+    if (r1 >= kGB * 49 || ch >= cch)
+      *reinterpret_cast<uint4*>(sm + L::a1s + (r1 >> 6) * 8192 + sw(r1 & 63, ch)) = make_uint4(0, 0, 0, 0);
+  }
+  tc::fence_async_smem();
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
@@ -786,263 +804,239 @@ __global__ void __launch_bounds__(kThr + 32, 1) k_enc_bwd_tc(const __grid_consta
   int it = 0, gi = 0;
   enc_stamp(dbg, 1);
 
-  // ring of two 32 KB stages: wait until the MMAs that read the stage two steps ago are done
-  auto stage_acquire = [&](int& st) -> uint8_t* {
-    st = it & 1;
-    if (it >= 2) tc::mbar_wait(&empty[st], ((it >> 1) - 1) & 1);
-    return sm + L::ring + st * 32768;
-  };
-  // warps 0-7 build the operand tiles and run the epilogues; warp 8 issues the MMAs (warp-uniform,
-  // elected lane): a built stage is published on full[st] (one arrive per builder warp), the MMAs
-  // release it on empty[st]
-  auto built = [&](int st) {
-    tc::fence_async_smem();
-    tc::fence_before_sync();
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive(&full[st]);
-  };
   if (warp == kThr / 32) {
     // ---- MMA warp ------------------------------------------------------------------------------------
     int mit = 0, mgi = 0;
+    const uint32_t d2p0 = tc::smem_u32(sm + L::d2p), w0 = tc::smem_u32(sm + L::w);
     for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++mgi) {
       const bool first = mgi == 0;
       auto take = [&]() {
-        const int st = mit & 1;
-        tc::mbar_wait(&full[st], (mit >> 1) & 1);
+        const int st = mit % NS;
+        tc::mbar_wait(&full[st], (mit / NS) & 1);
         tc::fence_after_sync();
-        return tc::smem_u32(sm + L::ring + st * 32768);
+        return tc::smem_u32(sm + L::ring + st * 16384);
       };
-      for (int kb = 0; kb < nkb2; ++kb, ++mit) {
-        const uint32_t a0 = take();
-        if (mit == 0) tc::mbar_wait(&wbar, 0);
-        const uint32_t w0 = tc::smem_u32(sm + L::w + kb * C * 128);
+      tc::mbar_wait(&d2_full, mgi & 1);
+      if (first) tc::mbar_wait(&wbar, 0);
+      tc::fence_after_sync();
+      for (int t = 0; t < 2; ++t)
+        for (int tap = 0; tap < 9; ++tap) {
+          const int shift = (2 - tap / 3) * 9 + (2 - tap % 3);
+          const int kb = (tap * C) / 64, koff = (tap * C) % 64;
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            tc::mma_bf16_e(t_dx + mt * C, tc::sdesc_k128(a0 + mt * 16384 + 32 * k), tc::sdesc_k128(w0 + 32 * k), id_k,
-                           (kb | k) != 0);
-        tc::mma_commit_e(&empty[mit & 1]);
-        if (kb == nkb2 - 1) tc::mma_commit_e(&bar_dx);
-      }
-      for (int mt = 0; mt < nt2; ++mt, ++mit) {
-        const uint32_t a0 = take(), b0s = tc::smem_u32(sm + L::d2s);
-#pragma unroll
-        for (int kb = 0; kb < 2; ++kb)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            tc::mma_bf16_e(t_w2 + mt * C, tc::sdesc_sw128(a0 + kb * 16384 + 2048 * k, 8192, 1024),
-                           tc::sdesc_sw128(b0s + kb * 8192 + 2048 * k, 8192, 1024), id_mn,
-                           !(first && kb == 0 && k == 0));
-        tc::mma_commit_e(&empty[mit & 1]);
-      }
-      for (int s2 = 0; s2 < 2; ++s2, ++mit) {
-        const uint32_t a0 = take(), b0s = tc::smem_u32(sm + L::a1s + 2 * s2 * 8192);
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk)
+          for (int k = 0; k < C / 16; ++k)
+            tc::mma_bf16_e(t_dx + t * C, sdesc_sw(d2p0 + (t * 128 + shift) * C * 2 + 32 * k, C * 2),
+                           tc::sdesc_k128(w0 + kb * C * 128 + (koff + 16 * k) * 2), id_k, (tap | k) != 0);
+        }
+      tc::mma_commit_e(&bar_dx);
+      for (int mt = 0; mt < nt2; ++mt)
+        for (int kb = 0; kb < 2; ++kb, ++mit) {
+          const uint32_t a0 = take(), b0s = tc::smem_u32(sm + L::d2s + kb * 8192);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            tc::mma_bf16_e(t_w1, tc::sdesc_sw128(a0 + kk * 16384 + 2048 * k, 8192, 1024),
-                           tc::sdesc_sw128(b0s + kk * 8192 + 2048 * k, 8192, 1024), id_mn,
-                           !(first && s2 == 0 && kk == 0 && k == 0));
-        tc::mma_commit_e(&empty[mit & 1]);
-        if (s2 == 1) tc::mma_commit_e(&bar_grp);
+            tc::mma_bf16_e(t_w2 + mt * C, tc::sdesc_sw128(a0 + 2048 * k, 8192, 1024),
+                           tc::sdesc_sw128(b0s + 2048 * k, 8192, 1024), id_mn, !(first && kb == 0 && k == 0));
+          tc::mma_commit_e(&empty[mit % NS]);
+        }
+      for (int s4 = 0; s4 < 4; ++s4, ++mit) {
+        const uint32_t a0 = take(), b0s = tc::smem_u32(sm + L::a1s + s4 * 8192);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc::mma_bf16_e(t_w1, tc::sdesc_sw128(a0 + 2048 * k, 8192, 1024), tc::sdesc_sw128(b0s + 2048 * k, 8192, 1024),
+                         id_mn, !(first && s4 == 0 && k == 0));
+        tc::mma_commit_e(&empty[mit % NS]);
+        if (s4 == 3) tc::mma_commit_e(&bar_grp);
       }
     }
     if (mgi == 0) tc::mbar_wait(&wbar, 0);  // never exit with the bulk copy in flight
   } else {
-  for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++gi) {
-    const int b0 = g * kGB;
-    const bool first = gi == 0;
-    // ---- load D2 (MN-major SW128, rows r2 = img * 25 + p), y1 rows (HWC), images: every global load
-    // of the group is issued before any is stored (one memory latency instead of one per item) ----------
-    {
-      constexpr int n_d2 = 128 * 8 / kThr, n_y1 = (kGB * 49 * cch + kThr - 1) / kThr;
-      uint4 ud[n_d2], uy[n_y1], ux;
-#pragma unroll
-      for (int k = 0; k < n_d2; ++k) {
-        const int e = tid + k * kThr, r2 = e >> 3, ch = e & 7, i = r2 / 25, p = r2 - i * 25, b = b0 + i;
-        ud[k] = make_uint4(0, 0, 0, 0);
-        if (r2 < kGB * 25 && b < a.B && ch < cch)
-          ud[k] = *reinterpret_cast<const uint4*>(a.dA2_hwc + (int64_t)b * a.dA2_ld + p * C + ch * 8);
-      }
-#pragma unroll
-      for (int k = 0; k < n_y1; ++k) {
-        const int e = tid + k * kThr, r1 = e / cch, ch = e - r1 * cch, i = r1 / 49, p = r1 - i * 49, b = b0 + i;
-        uy[k] = make_uint4(0, 0, 0, 0);
-        if (e < kGB * 49 * cch && b < a.B)
-          uy[k] = *reinterpret_cast<const uint4*>(a.y1_hwc + ((int64_t)b * 49 + p) * C + ch * 8);
-      }
-      ux = make_uint4(0, 0, 0, 0);
-      if (tid < kGB * 48 && b0 + tid / 48 < a.B)  // 16-byte chunks of the images
-        ux = *reinterpret_cast<const uint4*>(a.img + (int64_t)(b0 + tid / 48) * 768 + (tid % 48) * 16);
-#pragma unroll
-      for (int k = 0; k < n_d2; ++k) {
-        const int e = tid + k * kThr, r2 = e >> 3, ch = e & 7;
-        *reinterpret_cast<uint4*>(sm + L::d2s + (r2 >> 6) * 8192 + sw(r2 & 63, ch)) = ud[k];
-      }
-#pragma unroll
-      for (int k = 0; k < n_y1; ++k) {
-        const int e = tid + k * kThr, r1 = e / cch, ch = e - r1 * cch;
-        if (e < kGB * 49 * cch) *reinterpret_cast<uint4*>(y1s + r1 * C + ch * 8) = uy[k];
-      }
-      if (tid < kGB * 48) *reinterpret_cast<uint4*>(xs + tid * 16) = ux;
-    }
-    tc::named_bar(1, kThr);
-    enc_stamp(dbg && first, 2);
-    // ---- conv2 dX: per K block both row tiles ---------------------------------------------------
-    for (int kb = 0; kb < nkb2; ++kb, ++it) {
-      int st;
-      uint8_t* A = stage_acquire(st);
+    // ---- builders ------------------------------------------------------------------------------------
+    auto stage_acquire = [&](int& st) -> uint8_t* {
+      st = it % NS;
+      if (it >= NS) tc::mbar_wait(&empty[st], ((it / NS) - 1) & 1);
+      return sm + L::ring + st * 16384;
+    };
+    auto built = [&](int st) {
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&full[st]);
+    };
+    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++gi) {
+      const int b0 = g * kGB;
+      const bool first = gi == 0;
+      // ---- load D2 (dense MN-major rows r2 = img * 25 + p, for dW2; and on the padded grids, for dX),
+      // y1 rows (HWC), images: every global load of the group is issued before any is stored ----------
       {
-        uint4 u[256 * 8 / kThr];
+        constexpr int n_d2 = 128 * 8 / kThr, n_dp = (288 * cch + kThr - 1) / kThr,
+                      n_y1 = (kGB * 49 * cch + kThr - 1) / kThr;
+        uint4 ud[n_d2], up[n_dp], uy[n_y1], ux;
 #pragma unroll
-        for (int n = 0; n < 256 * 8 / kThr; ++n) {
-          const int e = tid + n * kThr, r1 = e >> 3, ch = e & 7;
-          const int k = kb * 64 + ch * 8, t = k / C, o0 = k - t * C;
-          u[n] = make_uint4(0, 0, 0, 0);
-          if (r1 < kGB * 49 && t < 9) {
-            const int i = r1 / 49, p = r1 - i * 49, y = p / 7, x = p - y * 7, ki = t / 3, kj = t - ki * 3;
-            const int yy = y - ki, xx = x - kj;
-            if (yy >= 0 && yy < 5 && xx >= 0 && xx < 5) {
-              const int r2 = i * 25 + yy * 5 + xx;
-              u[n] = *reinterpret_cast<const uint4*>(sm + L::d2s + (r2 >> 6) * 8192 + sw(r2 & 63, o0 >> 3));
+        for (int k = 0; k < n_d2; ++k) {
+          const int e = tid + k * kThr, r2 = e >> 3, ch = e & 7, i = r2 / 25, p = r2 - i * 25, b = b0 + i;
+          ud[k] = make_uint4(0, 0, 0, 0);
+          if (r2 < kGB * 25 && b < a.B && ch < cch)
+            ud[k] = *reinterpret_cast<const uint4*>(a.dA2_hwc + (int64_t)b * a.dA2_ld + p * C + ch * 8);
+        }
+#pragma unroll
+        for (int k = 0; k < n_dp; ++k) {
+          const int e = tid + k * kThr, R = e / cch, ch = e - R * cch;
+          const int i = R / 63, rem = R - i * 63, Y = rem / 9, X = rem - Y * 9, b = b0 + i;
+          up[k] = make_uint4(0, 0, 0, 0);
+          if (e < 288 * cch && i < kGB && b < a.B && Y >= 2 && Y < 7 && X >= 2 && X < 7)
+            up[k] = *reinterpret_cast<const uint4*>(a.dA2_hwc + (int64_t)b * a.dA2_ld + ((Y - 2) * 5 + X - 2) * C + ch * 8);
+        }
+#pragma unroll
+        for (int k = 0; k < n_y1; ++k) {
+          const int e = tid + k * kThr, r1 = e / cch, ch = e - r1 * cch, i = r1 / 49, p = r1 - i * 49, b = b0 + i;
+          uy[k] = make_uint4(0, 0, 0, 0);
+          if (e < kGB * 49 * cch && b < a.B)
+            uy[k] = *reinterpret_cast<const uint4*>(a.y1_hwc + ((int64_t)b * 49 + p) * C + ch * 8);
+        }
+        ux = make_uint4(0, 0, 0, 0);
+        if (tid < kGB * 48 && b0 + tid / 48 < a.B)  // 16-byte chunks of the images
+          ux = *reinterpret_cast<const uint4*>(a.img + (int64_t)(b0 + tid / 48) * 768 + (tid % 48) * 16);
+#pragma unroll
+        for (int k = 0; k < n_d2; ++k) {
+          const int e = tid + k * kThr, r2 = e >> 3, ch = e & 7;
+          *reinterpret_cast<uint4*>(sm + L::d2s + (r2 >> 6) * 8192 + sw(r2 & 63, ch)) = ud[k];
+        }
+#pragma unroll
+        for (int k = 0; k < n_dp; ++k) {
+          const int e = tid + k * kThr, R = e / cch, ch = e - R * cch;
+          if (e < 288 * cch) *reinterpret_cast<uint4*>(sm + L::d2p + y1_off<C>(R, ch)) = up[k];
+        }
+#pragma unroll
+        for (int k = 0; k < n_y1; ++k) {
+          const int e = tid + k * kThr, r1 = e / cch, ch = e - r1 * cch;
+          if (e < kGB * 49 * cch) *reinterpret_cast<uint4*>(y1s + r1 * C + ch * 8) = uy[k];
+        }
+        if (tid < kGB * 48) *reinterpret_cast<uint4*>(xs + tid * 16) = ux;
+      }
+      // d2p (and d2s) -> the tensor core; also orders this group after the previous group's dX
+      // epilogue (TMEM reads) for the MMA warp
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      tc::named_bar(1, kThr);
+      if (lane == 0) tc::mbar_arrive(&d2_full);
+      enc_stamp(dbg && first, 2);
+      // ---- conv2 dW (+ db2 via the ones row), accumulated across groups: one row tile x one K block
+      //      per stage, built while the dX MMAs run ------------------------------------------------------
+      for (int mt = 0; mt < nt2; ++mt)
+        for (int kb = 0; kb < 2; ++kb, ++it) {
+          int st;
+          uint8_t* A = stage_acquire(st);
+          uint4 u[1024 / kThr];
+#pragma unroll
+          for (int n = 0; n < 1024 / kThr; ++n) {  // (atom, K row, chunk)
+            const int e = tid + n * kThr;
+            const int j = e >> 9, rr = (e >> 3) & 63, ch = e & 7, r2 = kb * 64 + rr;
+            const int m0 = mt * 128 + j * 64 + ch * 8, t = m0 / C, c0 = m0 - t * C;
+            const int i = r2 / 25, p = r2 - i * 25;
+            const bool rv = r2 < kGB * 25 && b0 + i < a.B;
+            u[n] = make_uint4(0, 0, 0, 0);
+            if (rv) {
+              if (t < 9) {
+                const int oy = p / 5, ox = p - oy * 5, ki = t / 3, kj = t - ki * 3;
+                u[n] = *reinterpret_cast<const uint4*>(y1s + (i * 49 + (oy + ki) * 7 + ox + kj) * C + c0);
+              } else if (m0 == 9 * C) {
+                u[n].x = 0x3F80u;  // bf16 1.0 in element 0
+              }
+            }
+          }
+#pragma unroll
+          for (int n = 0; n < 1024 / kThr; ++n) {
+            const int e = tid + n * kThr;
+            const int j = e >> 9, rr = (e >> 3) & 63, ch = e & 7;
+            *reinterpret_cast<uint4*>(A + j * 8192 + sw(rr, ch)) = u[n];
+          }
+          built(st);
+        }
+      enc_stamp(dbg && first, 4);
+      // ---- dX epilogue: dA1 = dy1 * (y1 > 0) -> smem (MN-major rows r1); warp (q, hh) -> tile hh -----
+      tc::mbar_wait(&bar_dx, gi & 1);
+      tc::fence_after_sync();
+      enc_stamp(dbg && first, 5);
+      {
+        const int o = hh * 128 + q * 32 + lane, i = o / 63, rem = o - i * 63, y = rem / 9, x = rem - y * 9;
+        const bool ov = i < kGB && x < 7;
+        const int r1 = i * 49 + y * 7 + x;
+#pragma unroll
+        for (int c0 = 0; c0 < C; c0 += 32) {
+          float v[32];
+          tc::tmem_ld32(t_dx + hh * C + c0 + ((uint32_t)(q * 32) << 16), v);
+          if (ov) {
+#pragma unroll
+            for (int j8 = 0; j8 < 4; ++j8) {
+              float f[8];
+              const uint4 yv = *reinterpret_cast<const uint4*>(y1s + r1 * C + c0 + j8 * 8);
+              const __nv_bfloat162* yp = reinterpret_cast<const __nv_bfloat162*>(&yv);
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                const float2 yf = __bfloat1622float2(yp[jj]);
+                f[2 * jj] = yf.x > 0.f ? v[j8 * 8 + 2 * jj] : 0.f;
+                f[2 * jj + 1] = yf.y > 0.f ? v[j8 * 8 + 2 * jj + 1] : 0.f;
+              }
+              const int ch = (c0 >> 3) + j8;
+              *reinterpret_cast<uint4*>(sm + L::a1s + (r1 >> 6) * 8192 + sw(r1 & 63, ch)) = tc::pack_bf16x8(f);
             }
           }
         }
-#pragma unroll
-        for (int n = 0; n < 256 * 8 / kThr; ++n) {
-          const int e = tid + n * kThr, r1 = e >> 3, ch = e & 7;
-          *reinterpret_cast<uint4*>(A + (r1 >> 7) * 16384 + sw(r1 & 127, ch)) = u[n];
-        }
       }
-      built(st);
-    }
-    enc_stamp(dbg && first, 3);
-    // ---- conv2 dW (+ db2 via the ones row), accumulated across groups: per step one row tile,
-    //      both K blocks ---------------------------------------------------------------------------
-    for (int mt = 0; mt < nt2; ++mt, ++it) {
-      int st;
-      uint8_t* A = stage_acquire(st);
-      {
-        uint4 u[2048 / kThr];
-#pragma unroll
-        for (int n = 0; n < 2048 / kThr; ++n) {  // (kb, atom, K row, chunk)
-          const int e = tid + n * kThr;
-          const int kb = e >> 10, j = (e >> 9) & 1, rr = (e >> 3) & 63, ch = e & 7, r2 = kb * 64 + rr;
-          const int m0 = mt * 128 + j * 64 + ch * 8, t = m0 / C, c0 = m0 - t * C;
-          const int i = r2 / 25, p = r2 - i * 25;
-          const bool rv = r2 < kGB * 25 && b0 + i < a.B;
-          u[n] = make_uint4(0, 0, 0, 0);
-          if (rv) {
-            if (t < 9) {
-              const int oy = p / 5, ox = p - oy * 5, ki = t / 3, kj = t - ki * 3;
-              u[n] = *reinterpret_cast<const uint4*>(y1s + (i * 49 + (oy + ki) * 7 + ox + kj) * C + c0);
-            } else if (m0 == 9 * C) {
-              u[n].x = 0x3F80u;  // bf16 1.0 in element 0
-            }
-          }
-        }
-#pragma unroll
-        for (int n = 0; n < 2048 / kThr; ++n) {
-          const int e = tid + n * kThr;
-          const int kb = e >> 10, j = (e >> 9) & 1, rr = (e >> 3) & 63, ch = e & 7;
-          *reinterpret_cast<uint4*>(A + kb * 16384 + j * 8192 + sw(rr, ch)) = u[n];
-        }
-      }
-      built(st);
-    }
-    enc_stamp(dbg && first, 4);
-    // ---- dX epilogue: dA1 = dy1 * (y1 > 0) -> smem (MN-major rows r1); warp (q, hh) -> tile hh -----
-    tc::mbar_wait(&bar_dx, gi & 1);
-    tc::fence_after_sync();
-    enc_stamp(dbg && first, 5);
-    {
-      const int rr = q * 32 + lane, r1 = hh * 128 + rr;
-#pragma unroll
-      for (int c0 = 0; c0 < C; c0 += 32) {
-        float v[32];
-        tc::tmem_ld32(t_dx + hh * C + c0 + ((uint32_t)(q * 32) << 16), v);
-#pragma unroll
-        for (int j8 = 0; j8 < 4; ++j8) {
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      tc::named_bar(1, kThr);
+      enc_stamp(dbg && first, 6);
+      // ---- conv1 dW (+ db1), accumulated across groups: 4 steps of one K block (64 rows r1) ---------
+      for (int s4 = 0; s4 < 4; ++s4, ++it) {
+        int st;
+        uint8_t* A = stage_acquire(st);
+        for (int e = tid; e < 2 * 64 * 8; e += kThr) {
+          const int j = e >> 9, rr = (e >> 3) & 63, ch = e & 7, r1 = s4 * 64 + rr;
           float f[8];
-          if (r1 < kGB * 49) {
-            const uint4 yv = *reinterpret_cast<const uint4*>(y1s + r1 * C + c0 + j8 * 8);
-            const __nv_bfloat162* yp = reinterpret_cast<const __nv_bfloat162*>(&yv);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float2 yf = __bfloat1622float2(yp[j]);
-              f[2 * j] = yf.x > 0.f ? v[j8 * 8 + 2 * j] : 0.f;
-              f[2 * j + 1] = yf.y > 0.f ? v[j8 * 8 + 2 * j + 1] : 0.f;
+          for (int u = 0; u < 8; ++u) f[u] = 0.f;
+          const int i = r1 / 49, p = r1 - i * 49, y = p / 7, x = p - y * 7;
+          if (j == 0 && ch < 4 && r1 < kGB * 49 && b0 + i < a.B) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int m = ch * 8 + u, ci = m / 9, t = m - ci * 9, ki = t / 3, kj = t - ki * 3;
+              if (m < 27) f[u] = (float)xs[i * 768 + ci * 256 + (2 * y + ki) * 16 + 2 * x + kj];
+              else if (m == 27) f[u] = 1.f;
             }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) f[j] = 0.f;
           }
-          const int ch = (c0 >> 3) + j8;
-          *reinterpret_cast<uint4*>(sm + L::a1s + (r1 >> 6) * 8192 + sw(r1 & 63, ch)) = tc::pack_bf16x8(f);
+          *reinterpret_cast<uint4*>(A + j * 8192 + sw(rr, ch)) = tc::pack_bf16x8(f);
         }
+        built(st);
       }
-      if (C == 32) {  // dA1 MN-major rows hold 64 elements: zero the unused half
-#pragma unroll
-        for (int ch = 4; ch < 8; ++ch)
-          *reinterpret_cast<uint4*>(sm + L::a1s + (r1 >> 6) * 8192 + sw(r1 & 63, ch)) = make_uint4(0, 0, 0, 0);
-      }
+      enc_stamp(dbg && first, 7);
+      tc::mbar_wait(&bar_grp, gi & 1);  // every MMA of the group done: smem inputs may be reused
+      tc::fence_after_sync();
+      tc::named_bar(1, kThr);
+      enc_stamp(dbg && first, 8);
     }
-    tc::fence_async_smem();
-    tc::fence_before_sync();
-    tc::named_bar(1, kThr);
-    enc_stamp(dbg && first, 6);
-    // ---- conv1 dW (+ db1), accumulated across groups: 2 steps of 2 K blocks -----------------------
-    for (int s2 = 0; s2 < 2; ++s2, ++it) {
-      int st;
-      uint8_t* A = stage_acquire(st);
-      for (int e = tid; e < 2 * 2 * 64 * 8; e += kThr) {
-        const int kk = e >> 10, j = (e >> 9) & 1, rr = (e >> 3) & 63, ch = e & 7, r1 = (2 * s2 + kk) * 64 + rr;
-        float f[8];
+    // ---- per-CTA partials, row-major [row][o]: rows 0..9C = dW2 (t, c) (+ db2), then dW1 (ci, t) (+ db1)
+    float* part = a.part + (int64_t)blockIdx.x * part_rows(C) * C;
+    if (gi > 0) {
+      for (int mt = hh; mt < nt2 + 1; mt += 2) {
+        const bool w1 = mt == nt2;
+        const int m = q * 32 + lane + (w1 ? 0 : mt * 128);
+        const uint32_t base = (w1 ? t_w1 : t_w2 + mt * C) + ((uint32_t)(q * 32) << 16);
+        const int prow = w1 ? (m < 28 ? 9 * C + 1 + m : -1) : (m <= 9 * C ? m : -1);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) f[u] = 0.f;
-        const int i = r1 / 49, p = r1 - i * 49, y = p / 7, x = p - y * 7;
-        if (j == 0 && ch < 4 && r1 < kGB * 49 && b0 + i < a.B) {
+        for (int c0 = 0; c0 < C; c0 += 32) {
+          float v[32];
+          tc::tmem_ld32(base + c0, v);
+          if (prow >= 0) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int m = ch * 8 + u, ci = m / 9, t = m - ci * 9, ki = t / 3, kj = t - ki * 3;
-            if (m < 27) f[u] = (float)xs[i * 768 + ci * 256 + (2 * y + ki) * 16 + 2 * x + kj];
-            else if (m == 27) f[u] = 1.f;
+            for (int j = 0; j < 8; ++j)
+              reinterpret_cast<float4*>(part + (int64_t)prow * C + c0)[j] =
+                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
-        }
-        *reinterpret_cast<uint4*>(A + kk * 16384 + j * 8192 + sw(rr, ch)) = tc::pack_bf16x8(f);
-      }
-      built(st);
-    }
-    enc_stamp(dbg && first, 7);
-    tc::mbar_wait(&bar_grp, gi & 1);  // every MMA of the group done: smem inputs may be reused
-    tc::fence_after_sync();
-    tc::named_bar(1, kThr);
-    enc_stamp(dbg && first, 8);
-  }
-  // ---- per-CTA partials, row-major [row][o]: rows 0..9C = dW2 (t, c) (+ db2), then dW1 (ci, t) (+ db1)
-  float* part = a.part + (int64_t)blockIdx.x * part_rows(C) * C;
-  if (gi > 0) {
-    for (int mt = hh; mt < nt2 + 1; mt += 2) {
-      const bool w1 = mt == nt2;
-      const int m = q * 32 + lane + (w1 ? 0 : mt * 128);
-      const uint32_t base = (w1 ? t_w1 : t_w2 + mt * C) + ((uint32_t)(q * 32) << 16);
-      const int prow = w1 ? (m < 28 ? 9 * C + 1 + m : -1) : (m <= 9 * C ? m : -1);
-#pragma unroll
-      for (int c0 = 0; c0 < C; c0 += 32) {
-        float v[32];
-        tc::tmem_ld32(base + c0, v);
-        if (prow >= 0) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            reinterpret_cast<float4*>(part + (int64_t)prow * C + c0)[j] =
-                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         }
       }
     }
   }
-  }  // builders
   tc::fence_before_sync();
   __syncthreads();
   enc_stamp(dbg, 9);
