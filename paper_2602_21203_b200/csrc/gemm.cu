@@ -1302,7 +1302,9 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     int cs = 8;
     for (int i = 0; i < b.nprob; ++i) {
       const int n = b.p[i].N;
-      const int c = n >= 256 && n % 256 == 0 ? 4 : (n >= 128 && n % 128 == 0 ? 2 : 1);
+      // 512-wide rows (c3's critic): 2 CTAs of 256 columns (c3 1538 -> 1683 updates/s against 4 of 128:
+      // half the CTAs, each A tile loaded by 2 CTAs instead of 4)
+      const int c = n >= 512 && n % 512 == 0 ? 2 : (n >= 256 && n % 256 == 0 ? 4 : (n >= 128 && n % 128 == 0 ? 2 : 1));
       cs = c < cs ? c : cs;
     }
     // LayerNorm backward over 256-column rows: 8-CTA clusters of 32 columns (16 per warp in the
