@@ -94,7 +94,14 @@ __global__ void __launch_bounds__(256) k_conv_tiles(const float* __restrict__ w1
   }
 }
 
-__device__ unsigned long long g_enc_stamps[160][16];  // debug: per-CTA phase timestamps (SQUINT_ENC_DBG)
+__device__ unsigned long long g_enc_stamps[160][32];  // debug: per-CTA phase timestamps (SQUINT_ENC_DBG)
+__device__ __forceinline__ void enc_stamp_any(bool on, int k) {  // caller picks the thread
+  if (on && blockIdx.x < 160) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_enc_stamps[blockIdx.x][k] = t;
+  }
+}
 __device__ __forceinline__ void enc_stamp(bool on, int k) {
   if (on && threadIdx.x == 0 && blockIdx.x < 160) {
     unsigned long long t;
@@ -412,20 +419,24 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ 
 // above runs each group's phases back to back with the whole CTA; here they run in separate roles so
 // the tensor core works through one group's conv2 while the CUDA cores stage and im2col the next
 // group and run the previous group's epilogues:
-//   P  warps 0-3   images of group i -> xs (u8), conv1 im2col -> A1          (a1_full / a1_empty)
-//   E1 warps 4-7   conv1 accumulator T1 -> ReLU(acc / 255 + b1) -> y1 (smem) + y1b (global)
+//   P  warps 0-7   images of group i -> xs (u8, two buffers; group i+1's global loads in flight
+//                  during group i's im2col), conv1 im2col -> A1                (a1_full / a1_empty)
+//   E1 warps 8-11  conv1 accumulator T1 -> ReLU(acc / 255 + b1) -> y1 (smem) + y1b (global)
 //                                                       (t1_full / t1_empty, y1_full / y1_empty)
-//   E2 warps 8-11  conv2 accumulator T2 -> ReLU(acc + b2) -> h (global)      (t2_full / t2_empty)
-//   M  warp 12     conv1 MMAs (A1, W1) -> T1; conv2 as nine row-shifted MMAs per tile (y1, W2) -> T2
+//   E2 warps 12-15 conv2 accumulator T2 -> ReLU(acc + b2) -> h (global)      (t2_full / t2_empty)
+//   M  warp 16     conv1 MMAs (A1, W1) -> T1; conv2 as nine row-shifted MMAs per tile (y1, W2) -> T2
 // Every barrier completes once per group; TMEM holds T1 (3 C columns) and T2 (3 C columns).
-constexpr int kWsWarps = 13;
+constexpr int kPW = 8;                // producer warps
+constexpr int kWsWarps = kPW + 9;     // + conv1 / conv2 epilogue teams (4 + 4) + the MMA warp
 template <int C>
 struct FwdW {
   static constexpr uint32_t w = 0;
-  static constexpr uint32_t a1 = (C * 128 + ((9 * C + 63) / 64) * C * 128 + 1023) & ~1023u;  // 3 x 16 KB
-  static constexpr uint32_t y1 = a1 + 3 * 16384;
-  static constexpr uint32_t xs = y1 + ((416u * C * 2 + 1023) & ~1023u);
-  static constexpr uint32_t total = xs + kGF * 768;
+  // conv1 A: 384 rows x 32 K (27 used) bf16, 64-byte rows with the 64-byte swizzle
+  static constexpr uint32_t a1 = (C * 128 + ((9 * C + 63) / 64) * C * 128 + 1023) & ~1023u;
+  static constexpr uint32_t y1sz = (416u * C * 2 + 1023) & ~1023u;
+  static constexpr uint32_t y1 = a1 + 384 * 64;                 // 2 buffers (group parity)
+  static constexpr uint32_t xs = y1 + 2 * y1sz;                 // 2 buffers of kGF images
+  static constexpr uint32_t total = xs + 2 * kGF * 768;
   // fused squint (act, mode 1 with factor 8; C = 32 only): a 2-slot ring of rendered 3x128x128 frames
   static constexpr uint32_t fring = (total + 1023) & ~1023u;
   static constexpr uint32_t total_sq = fring + 2 * 49152;
@@ -436,10 +447,15 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
   using L = FwdW<C>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t wbar, a1_full, a1_empty, t1_full, t1_empty, y1_full, y1_empty, t2_full, t2_empty, fbar[2];
+  __shared__ uint64_t wbar, a1_full, a1_empty, t1_full, t1_empty, y1_full[2], y1_empty[2], t2_full, t2_empty, fbar[2];
   __shared__ uint32_t tmem_slot;
   __shared__ int s_koff[32];
   __shared__ float s_b1[64], s_b2[64];
+  // mode 0: this CTA's replay rows and shifts, group i image ii at [i * kGF + ii] (read once up front so
+  // a group's image loads are one memory round trip; groups beyond kMaxLoc read them from global memory)
+  constexpr int kMaxLoc = 32;
+  __shared__ int64_t s_row[kMaxLoc * kGF];
+  __shared__ uint8_t s_dx[kMaxLoc * kGF], s_dy[kMaxLoc * kGF];
   const int H = a.H;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ngroups = (a.B + kGF - 1) / kGF;
@@ -449,12 +465,14 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
   if (warp == 0) tc::tmem_alloc(&tmem_slot, 512);
   if (tid == 32) {
     tc::mbar_init(&wbar, 1);
-    tc::mbar_init(&a1_full, 4);
+    tc::mbar_init(&a1_full, kPW);
     tc::mbar_init(&a1_empty, 1);
     tc::mbar_init(&t1_full, 1);
     tc::mbar_init(&t1_empty, 4);
-    tc::mbar_init(&y1_full, 4);
-    tc::mbar_init(&y1_empty, 1);
+    tc::mbar_init(&y1_full[0], 4);
+    tc::mbar_init(&y1_full[1], 4);
+    tc::mbar_init(&y1_empty[0], 1);
+    tc::mbar_init(&y1_empty[1], 1);
     tc::mbar_init(&t2_full, 1);
     tc::mbar_init(&t2_empty, 4);
     tc::mbar_init(&fbar[0], 1);
@@ -474,6 +492,16 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
     s_b1[tid] = a.b1[tid];
     s_b2[tid] = a.b2[tid];
   }
+  if (a.mode == 0)
+    for (int e = tid; e < min(nloc, kMaxLoc) * kGF; e += kWsWarps * 32) {
+      const int i = e / kGF, ii = e - i * kGF, job = blockIdx.x + i * gridDim.x;
+      const int src = job / ngroups, b = (job - src * ngroups) * kGF + ii;
+      if (b < a.B) {
+        s_row[e] = a.idx[b];
+        s_dx[e] = a.shifts[b * 4 + 2 * src];
+        s_dy[e] = a.shifts[b * 4 + 2 * src + 1];
+      }
+    }
   if (tid == 32) {
     tc::mbar_expect_tx(&wbar, fwd_wbytes(C));
     tc::bulk_load_1d(sm + L::w, a.wtiles, fwd_wbytes(C), &wbar);
@@ -483,9 +511,13 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
   const uint32_t t_c1 = tmem, t_c2 = tmem + 3 * C;
   uint8_t* xs = sm + L::xs;
 
-  if (warp < 4) {
+  if (warp < kPW) {
     // ---- P: stage + conv1 im2col --------------------------------------------------------------------
-    const int pt = tid;  // 0..127
+    // The global loads of group i + 1's images (replay gather + shift, or 768-byte pre-squinted rows)
+    // are issued into registers before group i's im2col, so their latency hides behind it; xs alternates
+    // between two buffers.
+    const int pt = tid;  // 0 .. kPW * 32 - 1
+    constexpr int NPT = kPW * 32, NU = (kGF * 48 + NPT - 1) / NPT;
     // fused squint: frame k of this CTA (k = i * kGF + ii) streams into ring slot k % 2 by one bulk copy
     // (49,152 B, completion on fbar[k % 2]); the copy of frame k + 2 is issued once frame k is reduced
     const bool squint = a.mode == 1 && a.factor == 8;
@@ -506,120 +538,199 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
       issue_frame(0);
       issue_frame(1);
     }
-    for (int i = 0; i < nloc; ++i) {
+    uint4 rvA[NU], rvB[NU];  // image rows of two groups in flight (group parity)
+    int rdxA[NU], rdxB[NU];
+    // replay row gathers of s, a, s' (GatherJobs): each thread's items of the flattened (job, image,
+    // column) list, loaded with the group's images
+    constexpr int NG = 2;  // <= 2 * 256 items: 7 images x (12 + 6 + 12 + 12) columns per source at most
+    float gvA[NG], gvB[NG];
+    auto gj_item = [&](int src, int e, int& jb, int& ii, int& jj) -> bool {
+      for (jb = 0; jb < a.ngj[src]; ++jb) {
+        const int n = kGF * a.gj[src][jb].width;
+        if (e < n) {
+          ii = e / a.gj[src][jb].width;
+          jj = e - ii * a.gj[src][jb].width;
+          return true;
+        }
+        e -= n;
+      }
+      return false;
+    };
+    auto load_stage = [&](int i, uint4 (&rv)[NU], int (&rdx)[NU], float (&gv)[NG]) {  // group i -> registers
       const int job = blockIdx.x + i * gridDim.x;
       const int src = job / ngroups, g = job - src * ngroups, b0 = g * kGF;
-      tc::named_bar(1, 128);  // the previous group's im2col has read xs
-      if (a.mode == 0) {
-        const uint8_t* R = a.src[src];
-        for (int e = pt; e < kGF * 48; e += 128) {
-          const int ii = e / 48, rem = e - ii * 48, cc = rem >> 4, y = rem & 15;
-          const int b = b0 + ii;
-          uint4 o = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        const int e = pt + u * NPT;
+        rv[u] = make_uint4(0, 0, 0, 0);
+        rdx[u] = -1;
+        if (e < kGF * 48) {
+          const int ii = e / 48, rem = e - ii * 48, b = b0 + ii;
           if (b < a.B) {
-            const int64_t row = a.idx[b];
-            const int dx = a.shifts[b * 4 + 2 * src], dy = a.shifts[b * 4 + 2 * src + 1];
-            const int sy = min(max(y + dy - a.pad, 0), H - 1);
-            const uint4 v = *reinterpret_cast<const uint4*>(R + row * 768 + cc * 256 + sy * 16);
+            if (a.mode == 0) {
+              const int cc = rem >> 4, y = rem & 15, si = i * kGF + ii;
+              const int64_t row = i < kMaxLoc ? s_row[si] : a.idx[b];
+              const int dx = i < kMaxLoc ? s_dx[si] : a.shifts[b * 4 + 2 * src];
+              const int dy = i < kMaxLoc ? s_dy[si] : a.shifts[b * 4 + 2 * src + 1];
+              const int sy = min(max(y + dy - a.pad, 0), H - 1);
+              rv[u] = *reinterpret_cast<const uint4*>(a.src[src] + row * 768 + cc * 256 + sy * 16);
+              rdx[u] = dx;
+            } else {
+              rv[u] = __ldcs(reinterpret_cast<const uint4*>(a.src[0] + (int64_t)b * 768) + rem);
+              rdx[u] = a.pad;  // no horizontal shift
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < NG; ++u) {
+        int jb, ii, jj;
+        gv[u] = 0.f;
+        if (gj_item(src, pt + u * NPT, jb, ii, jj) && b0 + ii < a.B) {
+          const GatherJob& gj = a.gj[src][jb];
+          const int64_t row =
+              gj.use_idx ? (i < kMaxLoc && a.mode == 0 ? s_row[i * kGF + ii] : a.idx[b0 + ii]) : (int64_t)(b0 + ii);
+          gv[u] = gj.src[row * gj.width + jj];
+        }
+      }
+    };
+    auto store_stage = [&](int i, uint8_t* xb, const uint4 (&rv)[NU], const int (&rdx)[NU], const float (&gv)[NG]) {
+      const int job = blockIdx.x + i * gridDim.x;
+      const int src = job / ngroups, g = job - src * ngroups, b0 = g * kGF;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        const int e = pt + u * NPT;
+        if (e >= kGF * 48) continue;
+        const int ii = e / 48, rem = e - ii * 48, b = b0 + ii;
+        uint4 o = make_uint4(0, 0, 0, 0);
+        if (rdx[u] >= 0) {
+          if (a.mode == 0) {
+            const int dx = rdx[u];
             uint32_t wv[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               uint32_t acc = 0;
 #pragma unroll
-              for (int j = 0; j < 4; ++j) acc |= byte_of(v, min(max(4 * k + j + dx - a.pad, 0), H - 1)) << (8 * j);
+              for (int j = 0; j < 4; ++j) acc |= byte_of(rv[u], min(max(4 * k + j + dx - a.pad, 0), H - 1)) << (8 * j);
               wv[k] = acc;
             }
             o = make_uint4(wv[0], wv[1], wv[2], wv[3]);
             uint8_t* dump = src == 0 ? a.img0 : a.img1;
-            if (dump) *reinterpret_cast<uint4*>(dump + (int64_t)b * 768 + cc * 256 + y * 16) = o;
+            if (dump) *reinterpret_cast<uint4*>(dump + (int64_t)b * 768 + rem * 16) = o;
+          } else {
+            o = rv[u];
+            if (a.ring) reinterpret_cast<uint4*>(a.ring + a.slots[b] * 768)[rem] = o;
           }
-          *reinterpret_cast<uint4*>(xs + ii * 768 + cc * 256 + y * 16) = o;
         }
-      } else if (squint) {
+        reinterpret_cast<uint4*>(xb + ii * 768)[rem] = o;
+      }
+#pragma unroll
+      for (int u = 0; u < NG; ++u) {
+        int jb, ii, jj;
+        if (gj_item(src, pt + u * NPT, jb, ii, jj) && b0 + ii < a.B) {
+          const GatherJob& gj = a.gj[src][jb];
+          gj.dst[(int64_t)(b0 + ii) * gj.ld + gj.col + jj] = __float2bfloat16_rn(gv[u]);
+        }
+      }
+    };
+    // two groups ahead: group i + 2's loads are issued while group i is stored and im2col'ed
+    if (!squint && nloc > 0) load_stage(0, rvA, rdxA, gvA);
+    if (!squint && nloc > 1) load_stage(1, rvB, rdxB, gvB);
+    for (int i = 0; i < nloc; ++i) {
+      const int job = blockIdx.x + i * gridDim.x;
+      const int src = job / ngroups, g = job - src * ngroups, b0 = g * kGF;
+      uint8_t* xb = xs + (i & 1) * (kGF * 768);
+      if (squint) {
         // 8x8 block sums of each frame from shared memory, round half to even (Q1) -> xs (+ ring)
         for (int ii = 0; ii < kGF; ++ii) {
           const int k = i * kGF + ii, b = b0 + ii;
-          uint8_t* dst = xs + ii * 768;
+          uint8_t* dst = xb + ii * 768;
           if (b < a.B) {
             tc::mbar_wait(&fbar[k & 1], (k >> 1) & 1);
             const uint8_t* F = sm + L::fring + (k & 1) * 49152;
-            for (int e = pt; e < 3 * 16 * 8; e += 128) {  // (channel, output row, 16-byte column chunk)
+            for (int e = pt; e < 3 * 16 * 8; e += NPT) {  // (channel, output row, 16-byte column chunk)
               const int ck = e & 7, oy = (e >> 3) & 15, cc = e >> 7;
-              const uint8_t* src = F + (cc * 128 + oy * 8) * 128 + ck * 16;
+              const uint8_t* srcp = F + (cc * 128 + oy * 8) * 128 + ck * 16;
               uint32_t lo = 0, hi = 0;
 #pragma unroll
               for (int r = 0; r < 8; ++r) {
-                const uint4 v = *reinterpret_cast<const uint4*>(src + r * 128);
+                const uint4 v = *reinterpret_cast<const uint4*>(srcp + r * 128);
                 lo = __dp4a(v.x, 0x01010101u, __dp4a(v.y, 0x01010101u, lo));
                 hi = __dp4a(v.z, 0x01010101u, __dp4a(v.w, 0x01010101u, hi));
               }
-              const uint16_t q = (uint16_t)(rhe64(lo) | (rhe64(hi) << 8));
+              const uint16_t qv = (uint16_t)(rhe64(lo) | (rhe64(hi) << 8));
               const int off = cc * 256 + oy * 16 + 2 * ck;
-              *reinterpret_cast<uint16_t*>(dst + off) = q;
-              if (a.ring) *reinterpret_cast<uint16_t*>(a.ring + a.slots[b] * 768 + off) = q;
+              *reinterpret_cast<uint16_t*>(dst + off) = qv;
+              if (a.ring) *reinterpret_cast<uint16_t*>(a.ring + a.slots[b] * 768 + off) = qv;
             }
           } else {
-            for (int e = pt; e < 48; e += 128) reinterpret_cast<uint4*>(dst)[e] = make_uint4(0, 0, 0, 0);
+            for (int e = pt; e < 48; e += NPT) reinterpret_cast<uint4*>(dst)[e] = make_uint4(0, 0, 0, 0);
           }
-          tc::named_bar(1, 128);  // slot k % 2 read by every P thread
+          tc::named_bar(1, NPT);  // slot k % 2 read by every P thread
           issue_frame(k + 2);
         }
-      } else {  // frames already at the stored resolution (factor 1): 768-byte copies
-        const uint8_t* Fr = a.src[0];
-        for (int e = pt; e < kGF * 48; e += 128) {
-          const int ii = e / 48, rem = e - ii * 48, b = b0 + ii;
-          uint4 o = make_uint4(0, 0, 0, 0);
-          if (b < a.B) {
-            o = __ldcs(reinterpret_cast<const uint4*>(Fr + (int64_t)b * 768) + rem);
-            if (a.ring) reinterpret_cast<uint4*>(a.ring + a.slots[b] * 768)[rem] = o;
-          }
-          reinterpret_cast<uint4*>(xs + ii * 768)[rem] = o;
-        }
+      } else if (i & 1) {
+        store_stage(i, xb, rvB, rdxB, gvB);
+      } else {
+        store_stage(i, xb, rvA, rdxA, gvA);
       }
-      for (int jb = 0; jb < a.ngj[src]; ++jb) {
-        const GatherJob& gj = a.gj[src][jb];
-        for (int e = pt; e < kGF * gj.width; e += 128) {
-          const int ii = e / gj.width, j = e - ii * gj.width, b = b0 + ii;
-          if (b < a.B) {
-            const int64_t row = gj.use_idx ? a.idx[b] : (int64_t)b;
-            gj.dst[(int64_t)b * gj.ld + gj.col + j] = __float2bfloat16_rn(gj.src[row * gj.width + j]);
+      if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 24);
+      if (squint)  // (the other modes gather with their images in load_stage / store_stage)
+        for (int jb = 0; jb < a.ngj[src]; ++jb) {
+          const GatherJob& gj = a.gj[src][jb];
+          for (int e = pt; e < kGF * gj.width; e += NPT) {
+            const int ii = e / gj.width, jj = e - ii * gj.width, b = b0 + ii;
+            if (b < a.B) {
+              const int64_t row = gj.use_idx ? a.idx[b] : (int64_t)b;
+              gj.dst[(int64_t)b * gj.ld + gj.col + jj] = __float2bfloat16_rn(gj.src[row * gj.width + jj]);
+            }
           }
         }
+      if (!squint && i + 2 < nloc) {  // in flight during this and the next group's im2col
+        if (i & 1)
+          load_stage(i + 2, rvB, rdxB, gvB);
+        else
+          load_stage(i + 2, rvA, rdxA, gvA);
       }
-      tc::named_bar(1, 128);  // xs complete
+      if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 25);
+      tc::named_bar(1, NPT);  // xs[i % 2] complete
+      if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 26);
       if (i >= 1) tc::mbar_wait(&a1_empty, (i - 1) & 1);
+      if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 27);
       // conv1 im2col: row (img, oy, ox), K 0..26 = (ci, ki, kj) at byte offset koff[k] from the output
       // pixel's top-left input byte; K 27..31 zero (the MMAs read the first 64 bytes of each row)
-      for (int e = pt; e < 384 * 4; e += 128) {
+      for (int e = pt; e < 384 * 4; e += NPT) {
         const int r = e >> 2, ch = e & 3;
         float f[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) f[j] = 0.f;
         if (r < kGF * 49) {
           const int ii = r / 49, p = r - ii * 49, oy = p / 7, ox = p - oy * 7;
-          const uint8_t* px = xs + ii * 768 + 2 * oy * 16 + 2 * ox;
+          const uint8_t* px = xb + ii * 768 + 2 * oy * 16 + 2 * ox;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int k = ch * 8 + j;
             if (k < 27) f[j] = (float)px[s_koff[k]];
           }
         }
-        *reinterpret_cast<uint4*>(sm + L::a1 + (r >> 7) * 16384 + sw(r & 127, ch)) = tc::pack_bf16x8(f);
+        *reinterpret_cast<uint4*>(sm + L::a1 + y1_off<32>(r, ch)) = tc::pack_bf16x8(f);
       }
       tc::fence_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&a1_full);
       if (i == 0) enc_stamp(a.dbg, 11);
+      if ((i == 2 || i == 3) && pt == 0) enc_stamp_any(a.dbg, 16 + (i - 2) * 4 + 0);
     }
-  } else if (warp < 8) {
+  } else if (warp < kPW + 4) {
     // ---- E1: conv1 epilogue -> y1 ---------------------------------------------------------------
     const int q = warp & 3;
     const float inv255 = 1.0f / 255.0f;
     for (int i = 0; i < nloc; ++i) {
       const int job = blockIdx.x + i * gridDim.x;
       const int src = job / ngroups, g = job - src * ngroups, b0 = g * kGF;
+      uint8_t* y1b_s = sm + L::y1 + (i & 1) * L::y1sz;  // y1 buffer of this group's parity
       tc::mbar_wait(&t1_full, i & 1);
-      if (i >= 1) tc::mbar_wait(&y1_empty, (i - 1) & 1);
+      if (i >= 2) tc::mbar_wait(&y1_empty[i & 1], ((i - 2) >> 1) & 1);  // conv2 of group i - 2 read it
       tc::fence_after_sync();
 #pragma unroll 1
       for (int t = 0; t < 3; ++t) {
@@ -639,7 +750,7 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
 #pragma unroll
               for (int j = 0; j < 8; ++j) f[j] = v[j8 * 8 + j];
               const uint4 u = tc::pack_bf16x8(f);
-              *reinterpret_cast<uint4*>(sm + L::y1 + y1_off<C>(r, (c0 + j8 * 8) / 8)) = u;
+              *reinterpret_cast<uint4*>(y1b_s + y1_off<C>(r, (c0 + j8 * 8) / 8)) = u;
               if (a.y1b && src == 0 && b < a.B)
                 *reinterpret_cast<uint4*>(a.y1b + ((int64_t)b * 49 + p) * C + c0 + j8 * 8) = u;
             }
@@ -650,12 +761,12 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) {
-        tc::mbar_arrive(&y1_full);
+        tc::mbar_arrive(&y1_full[i & 1]);
         tc::mbar_arrive(&t1_empty);
       }
-      if (i == 0) enc_stamp(a.dbg && warp == 4, 12);
+      if ((i == 2 || i == 3) && warp == kPW && lane == 0) enc_stamp_any(a.dbg, 16 + (i - 2) * 4 + 1);
     }
-  } else if (warp < 12) {
+  } else if (warp < kPW + 8) {
     // ---- E2: conv2 epilogue -> h (valid 5x5 positions, HWC) ------------------------------------------
     const int q = warp & 3;
     for (int i = 0; i < nloc; ++i) {
@@ -687,15 +798,15 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&t2_empty);
-      if (i == 0) enc_stamp(a.dbg && warp == 8, 13);
+      if ((i == 2 || i == 3) && warp == kPW + 4 && lane == 0) enc_stamp_any(a.dbg, 16 + (i - 2) * 4 + 2);
     }
   } else {
     // ---- M: the MMAs (whole warp, one elected lane issues) --------------------------------------------
+    // conv1 of group i + 1 is issued ahead of conv2 of group i when its operand is already built, so the
+    // conv1 epilogue of i + 1 (into the other y1 buffer) overlaps conv2 of i on the tensor core
     const uint32_t id_c = tc::idesc_bf16(128, C);
-    const uint32_t a0 = tc::smem_u32(sm + L::a1), w0 = tc::smem_u32(sm + L::w), y0 = tc::smem_u32(sm + L::y1),
-                   w2 = w0 + C * 128;
-    if (nloc > 0) tc::mbar_wait(&wbar, 0);
-    for (int i = 0; i < nloc; ++i) {
+    const uint32_t a0 = tc::smem_u32(sm + L::a1), w0 = tc::smem_u32(sm + L::w), w2 = w0 + C * 128;
+    auto conv1 = [&](int i) {
       tc::mbar_wait(&a1_full, i & 1);
       if (i >= 1) tc::mbar_wait(&t1_empty, (i - 1) & 1);
       tc::fence_after_sync();
@@ -703,13 +814,24 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
       for (int t = 0; t < 3; ++t)
 #pragma unroll
         for (int k = 0; k < 2; ++k)
-          tc::mma_bf16_e(t_c1 + t * C, tc::sdesc_k128(a0 + t * 16384 + 32 * k), tc::sdesc_k128(w0 + 32 * k), id_c, k);
+          tc::mma_bf16_e(t_c1 + t * C, sdesc_sw(a0 + t * 128 * 64 + 32 * k, 64), tc::sdesc_k128(w0 + 32 * k), id_c, k);
       tc::mma_commit_e(&a1_empty);
       tc::mma_commit_e(&t1_full);
-      tc::mbar_wait(&y1_full, i & 1);
+    };
+    if (nloc > 0) {
+      tc::mbar_wait(&wbar, 0);
+      conv1(0);
+    }
+    for (int i = 0; i < nloc; ++i) {
+      tc::mbar_wait(&y1_full[i & 1], (i >> 1) & 1);
       if (i >= 1) tc::mbar_wait(&t2_empty, (i - 1) & 1);
       tc::fence_after_sync();
+      // (y1_full(i) implies t1_empty(i): E1 arrives both; the producers are rarely behind by more than
+      // the tensor core's conv2 time, so waiting for group i + 1's im2col here costs less than letting
+      // its conv1 queue behind conv2 of group i)
+      if (i + 1 < nloc) conv1(i + 1);
       // conv2 as nine row-shifted GEMMs over the full 7x7 grid (see k_enc_fwd_tc)
+      const uint32_t y0 = tc::smem_u32(sm + L::y1 + (i & 1) * L::y1sz);
       for (int t = 0; t < 3; ++t)
         for (int tap = 0; tap < 9; ++tap) {
           const int shift = (tap / 3) * 7 + tap % 3;
@@ -719,8 +841,9 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
             tc::mma_bf16_e(t_c2 + t * C, sdesc_sw(y0 + (t * 128 + shift) * C * 2 + 32 * k, C * 2),
                            tc::sdesc_k128(w2 + kb * C * 128 + (koff + 16 * k) * 2), id_c, (tap | k) != 0);
         }
-      tc::mma_commit_e(&y1_empty);
+      tc::mma_commit_e(&y1_empty[i & 1]);
       tc::mma_commit_e(&t2_full);
+      if ((i == 2 || i == 3) && lane == 0) enc_stamp_any(a.dbg, 16 + (i - 2) * 4 + 3);
     }
   }
   if (tid == 32 && nloc == 0) tc::mbar_wait(&wbar, 0);  // never exit with the bulk copy in flight
@@ -1157,5 +1280,5 @@ int launch_enc_bwd_tc(const EncBwdArgs& a, cudaStream_t s) {
 
 extern "C" __attribute__((visibility("default"))) int squint_debug_enc_stamps(unsigned long long* host) {
   cudaDeviceSynchronize();
-  return (int)cudaMemcpyFromSymbol(host, sq::g_enc_stamps, sizeof(unsigned long long) * 160 * 16);
+  return (int)cudaMemcpyFromSymbol(host, sq::g_enc_stamps, sizeof(unsigned long long) * 160 * 32);
 }
