@@ -32,12 +32,13 @@ namespace {
 using namespace gd;
 constexpr int kThreads = 256;
 constexpr int kMaxStages = 8;
-constexpr int kDbgSlots = 16;  // globaltimer stamps per CTA (SQUINT_GEMM_DBG)
+constexpr int kDbgSlots = 16;  // globaltimer stamps per CTA (SQUINT_GEMM_DBG); slot 15 = EPI (+64 split-K) | grid << 8
 constexpr int kABytes = 16384;  // 128 x 64 bf16
 constexpr float kLog2Pi = 1.8378770664093453f;
 constexpr float kSquashEps = 1e-6f;
 constexpr int kColaccOff = 4 * 4 * 4096;                  // after the 4 warp pairs' box rings
 constexpr int kEpiBytes = kColaccOff + 4 * 3 * 512 * 4;    // + LN-bwd column partials [4][3][512]
+constexpr int kStaticSmem = 16 * 1024;  // k_gemm's static __shared__ (ptxas: ~14.6 KB), inside the 227 KB per CTA
 
 int g_pdl = 1;
 
@@ -369,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     red[0][hh][rl] = p1;
     red[1][hh][rl] = p2;
     __syncthreads();
+    stamp(14);
     t1 = red[0][0][rl] + red[0][1][rl];
     t2 = red[1][0][rl] + red[1][1][rl];
     if (b.cs > 1) {
@@ -624,6 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
       }
     }
     float m1, m2;
+    stamp(13);
     row_total2(s1, s2, m1, m2);
     stamp(6);
     m1 /= (float)N;
@@ -737,6 +740,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   tc::fence_before_sync();
   __syncthreads();
   stamp(4);
+  if (b.dbg && tid == 0) b.dbg[blockIdx.x * kDbgSlots + 15] = (unsigned long long)EPI | ((unsigned long long)gridDim.x << 8);
   if (warp == 0) tc::tmem_dealloc(tmem, ncols);
 }
 
@@ -1179,6 +1183,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_sk(const __grid_constant__
   tc::fence_before_sync();
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // peers' copies from this CTA done
   stamp(4);
+  if (b.dbg && tid == 0) b.dbg[blockIdx.x * kDbgSlots + 15] = (unsigned long long)(EPI | 64) | ((unsigned long long)gridDim.x << 8);
   if (warp == 0) tc::tmem_dealloc(tmem, 64);
 }
 
@@ -1444,7 +1449,7 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
       ng = g > ng ? g : ng;
     }
     const size_t xb = (size_t)4 * 4 * 4096;  // 4 pairs x (up to) 4 boxes
-    if (ng <= 4 && smem + xb + 1024 <= 227 * 1024) {
+    if (ng <= 4 && smem + xb + 1024 + kStaticSmem <= 227 * 1024) {
       b.xpre_off = (int)smem;
       smem += xb;
     }
