@@ -47,6 +47,8 @@ def _compile(src, nccl_inc, verbose):
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
            "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", nccl_inc, "-c", src, "-o", obj]
+    if os.environ.get("SQUINT_NVCC_DEFS"):  # experiments: extra -D definitions (space separated)
+        cmd[1:1] = ["-D" + d for d in os.environ["SQUINT_NVCC_DEFS"].split()]
     if os.environ.get("SQUINT_PTXAS_V"):
         cmd.insert(1, "-Xptxas=-v")
     if src.endswith(".cpp"):

@@ -33,7 +33,7 @@ for i in used[-per:]:
     rel = lambda k: np.median((t[:, k] - t[:, 0]) / 1e3) if (t[:, k] > 0).all() else float("nan")
     span = (t[:, 4].max() - t0) / 1e3
     print(f"{i:3d} {nm:14s} grid {grid:4d} span {span:6.2f}  setup {rel(1):5.2f} wait {rel(2):5.2f} "
-          f"first {rel(8):5.2f} lastfull {rel(9):5.2f} mma_done {rel(3):5.2f} st5 {rel(5):5.2f} st13 {rel(13):5.2f} st14 {rel(14):5.2f} st6 {rel(6):5.2f} end {rel(4):5.2f} start_spread {(t[:,0].max()-t0)/1e3:5.2f}")
+          f"xpre {rel(10):5.2f} prod_done {rel(11):5.2f} first {rel(8):5.2f} lastfull {rel(9):5.2f} mma_done {rel(3):5.2f} st5 {rel(5):5.2f} st13 {rel(13):5.2f} st14 {rel(14):5.2f} st6 {rel(6):5.2f} end {rel(4):5.2f} start_spread {(t[:,0].max()-t0)/1e3:5.2f}")
 k = int(os.environ.get("TILES_OF", "-1"))
 if k >= 0:
     i = used[-per:][k]
