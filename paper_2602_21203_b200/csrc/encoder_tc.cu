@@ -854,6 +854,13 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
 }
 
 // ---- backward --------------------------------------------------------------------------------
+// element offset of (row r, 8-channel chunk ch) in the backward's y1 rows: the chunk index is XORed
+// with row bits so that 32 lanes reading one chunk of 32 consecutive rows (the dX epilogue's ReLU'
+// mask) hit distinct bank groups; 8 lanes reading the 8 chunks of one row (the dW2 gathers) still do
+template <int C>
+__device__ __forceinline__ int y1x(int r, int ch) {
+  return r * C + ((C == 64 ? (ch ^ (r & 7)) : (ch ^ ((r >> 1) & 3))) << 3);
+}
 template <int C>
 struct BwdL {
   static constexpr int nst = C == 32 ? 4 : 2;  // ring stages of 16 KB (one K block of an operand tile)
@@ -901,6 +908,13 @@ __global__ void __launch_bounds__(kThr + 32, 1) k_enc_bwd_tc(const __grid_consta
       tc::mbar_init(&full[i], kThr / 32);
     }
     tc::fence_mbar_init();
+  }
+  // The zero pads of the dX operand grids (rows i * 63 + Y * 9 + X outside the 5 x 5 interior, and
+  // rows 252 .. 287) are never written per group: zeroed once here
+  for (int e = tid; e < 288 * cch; e += kThr + 32) {
+    const int R = e / cch, ch = e - R * cch, rem = R % 63, Y = rem / 9, X = rem - Y * 9;
+    if (R >= kGB * 63 || Y < 2 || Y >= 7 || X < 2 || X >= 7)
+      *reinterpret_cast<uint4*>(sm + L::d2p + y1_off<C>(R, ch)) = make_uint4(0, 0, 0, 0);
   }
   // dA1 rows 196 .. 255 (the K tail of conv1 dW) and, for C = 32, the unused half of every 128-byte
   // row stay zero: written once here, never by the per-group epilogue
@@ -985,54 +999,63 @@ __global__ void __launch_bounds__(kThr + 32, 1) k_enc_bwd_tc(const __grid_consta
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&full[st]);
     };
+    // Global loads of a group (D2 dense MN-major rows r2 = img * 25 + p for dW2, D2 on the padded
+    // grids for dX, y1 rows, the u8 images) go to registers; group g + 1's are issued as soon as
+    // group g's are stored, so their latency hides behind group g's operand builds.
+    constexpr int n_d2 = 128 * 8 / kThr, n_y1 = (kGB * 49 * cch + kThr - 1) / kThr;
+    uint4 ud[n_d2], uy[n_y1], ux;
+    auto load_group = [&](int g) {
+      const int b0 = g * kGB;
+      const bool gv = g < ngroups;
+#pragma unroll
+      for (int k = 0; k < n_d2; ++k) {
+        const int e = tid + k * kThr, r2 = e >> 3, ch = e & 7, i = r2 / 25, p = r2 - i * 25, b = b0 + i;
+        ud[k] = make_uint4(0, 0, 0, 0);
+        if (gv && r2 < kGB * 25 && b < a.B && ch < cch)
+          ud[k] = *reinterpret_cast<const uint4*>(a.dA2_hwc + (int64_t)b * a.dA2_ld + p * C + ch * 8);
+      }
+#pragma unroll
+      for (int k = 0; k < n_y1; ++k) {
+        const int e = tid + k * kThr, r1 = e / cch, ch = e - r1 * cch, i = r1 / 49, p = r1 - i * 49, b = b0 + i;
+        uy[k] = make_uint4(0, 0, 0, 0);
+        if (gv && e < kGB * 49 * cch && b < a.B)
+          uy[k] = *reinterpret_cast<const uint4*>(a.y1_hwc + ((int64_t)b * 49 + p) * C + ch * 8);
+      }
+      ux = make_uint4(0, 0, 0, 0);
+      if (gv && tid < kGB * 48 && b0 + tid / 48 < a.B)  // 16-byte chunks of the images
+        ux = *reinterpret_cast<const uint4*>(a.img + (int64_t)(b0 + tid / 48) * 768 + (tid % 48) * 16);
+    };
+    // loop-invariant operand-build geometry of this thread (its 16-byte chunk ch of every 8-row
+    // item is fixed: e = tid + n * kThr with kThr % 8 == 0)
+    const int bch = tid & 7, brr = tid >> 3;  // chunk, first K row (the second is brr + 32)
+    // conv1 dW operand: element u of the thread's chunk is K row m = 8 bch + u = (ci, ki, kj) of the
+    // im2col; its byte offset in an image (>= 0), or -2 for the ones row (m = 27), -1 for zero
+    int xoff[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int m = bch * 8 + u, ci = m / 9, t = m - ci * 9, ki = t / 3, kj = t - ki * 3;
+      xoff[u] = (bch < 4 && m < 27) ? ci * 256 + ki * 16 + kj : (m == 27 ? -2 : -1);
+    }
+    if (blockIdx.x < ngroups) load_group(blockIdx.x);
     for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++gi) {
       const int b0 = g * kGB;
       const bool first = gi == 0;
-      // ---- load D2 (dense MN-major rows r2 = img * 25 + p, for dW2; and on the padded grids, for dX),
-      // y1 rows (HWC), images: every global load of the group is issued before any is stored ----------
       {
-        constexpr int n_d2 = 128 * 8 / kThr, n_dp = (288 * cch + kThr - 1) / kThr,
-                      n_y1 = (kGB * 49 * cch + kThr - 1) / kThr;
-        uint4 ud[n_d2], up[n_dp], uy[n_y1], ux;
-#pragma unroll
-        for (int k = 0; k < n_d2; ++k) {
-          const int e = tid + k * kThr, r2 = e >> 3, ch = e & 7, i = r2 / 25, p = r2 - i * 25, b = b0 + i;
-          ud[k] = make_uint4(0, 0, 0, 0);
-          if (r2 < kGB * 25 && b < a.B && ch < cch)
-            ud[k] = *reinterpret_cast<const uint4*>(a.dA2_hwc + (int64_t)b * a.dA2_ld + p * C + ch * 8);
-        }
-#pragma unroll
-        for (int k = 0; k < n_dp; ++k) {
-          const int e = tid + k * kThr, R = e / cch, ch = e - R * cch;
-          const int i = R / 63, rem = R - i * 63, Y = rem / 9, X = rem - Y * 9, b = b0 + i;
-          up[k] = make_uint4(0, 0, 0, 0);
-          if (e < 288 * cch && i < kGB && b < a.B && Y >= 2 && Y < 7 && X >= 2 && X < 7)
-            up[k] = *reinterpret_cast<const uint4*>(a.dA2_hwc + (int64_t)b * a.dA2_ld + ((Y - 2) * 5 + X - 2) * C + ch * 8);
-        }
-#pragma unroll
-        for (int k = 0; k < n_y1; ++k) {
-          const int e = tid + k * kThr, r1 = e / cch, ch = e - r1 * cch, i = r1 / 49, p = r1 - i * 49, b = b0 + i;
-          uy[k] = make_uint4(0, 0, 0, 0);
-          if (e < kGB * 49 * cch && b < a.B)
-            uy[k] = *reinterpret_cast<const uint4*>(a.y1_hwc + ((int64_t)b * 49 + p) * C + ch * 8);
-        }
-        ux = make_uint4(0, 0, 0, 0);
-        if (tid < kGB * 48 && b0 + tid / 48 < a.B)  // 16-byte chunks of the images
-          ux = *reinterpret_cast<const uint4*>(a.img + (int64_t)(b0 + tid / 48) * 768 + (tid % 48) * 16);
 #pragma unroll
         for (int k = 0; k < n_d2; ++k) {
           const int e = tid + k * kThr, r2 = e >> 3, ch = e & 7;
           *reinterpret_cast<uint4*>(sm + L::d2s + (r2 >> 6) * 8192 + sw(r2 & 63, ch)) = ud[k];
-        }
-#pragma unroll
-        for (int k = 0; k < n_dp; ++k) {
-          const int e = tid + k * kThr, R = e / cch, ch = e - R * cch;
-          if (e < 288 * cch) *reinterpret_cast<uint4*>(sm + L::d2p + y1_off<C>(R, ch)) = up[k];
+          // the same D2 value at its place (i, y + 2, x + 2) on the zero-padded grids of the dX MMAs
+          // (the pad rows were zeroed once at entry; invalid images store zeros here)
+          if (r2 < kGB * 25 && ch < cch) {
+            const int i = r2 / 25, p = r2 - i * 25, y = p / 5, x = p - y * 5;
+            *reinterpret_cast<uint4*>(sm + L::d2p + y1_off<C>(i * 63 + (y + 2) * 9 + x + 2, ch)) = ud[k];
+          }
         }
 #pragma unroll
         for (int k = 0; k < n_y1; ++k) {
           const int e = tid + k * kThr, r1 = e / cch, ch = e - r1 * cch;
-          if (e < kGB * 49 * cch) *reinterpret_cast<uint4*>(y1s + r1 * C + ch * 8) = uy[k];
+          if (e < kGB * 49 * cch) *reinterpret_cast<uint4*>(y1s + y1x<C>(r1, ch)) = uy[k];
         }
         if (tid < kGB * 48) *reinterpret_cast<uint4*>(xs + tid * 16) = ux;
       }
@@ -1042,44 +1065,55 @@ __global__ void __launch_bounds__(kThr + 32, 1) k_enc_bwd_tc(const __grid_consta
       tc::fence_before_sync();
       tc::named_bar(1, kThr);
       if (lane == 0) tc::mbar_arrive(&d2_full);
-      enc_stamp(dbg && first, 2);
+      load_group(g + gridDim.x);  // in flight during this group's builds
+      enc_stamp(dbg && gi < 2, 2 + 20 * gi);
       // ---- conv2 dW (+ db2 via the ones row), accumulated across groups: one row tile x one K block
-      //      per stage, built while the dX MMAs run ------------------------------------------------------
-      for (int mt = 0; mt < nt2; ++mt)
+      //      per stage, built while the dX MMAs run.  Item (j, h) of a stage: A row m = 128 mt + 64 j +
+      //      8 bch .. +7 (tap t, channels c0 ..), K row r2 = 64 kb + brr + 32 h (image i, output p) ->
+      //      y1 row i * 49 + (oy + ki) * 7 + ox + kj ------------------------------------------------------
+      int rbase[2][2];  // [kb][h]: y1 row of output r2 at tap (0, 0), or -1 past the group
+#pragma unroll
+      for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r2 = kb * 64 + brr + 32 * h, i = r2 / 25, p = r2 - i * 25, oy = p / 5, ox = p - oy * 5;
+          rbase[kb][h] = (r2 < kGB * 25 && b0 + i < a.B) ? i * 49 + oy * 7 + ox : -1;
+        }
+      for (int mt = 0; mt < nt2; ++mt) {
+        int toff[2], tcc[2];  // [j]: tap offset in y1 rows (-1: ones row, -2: zero), channel chunk
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const int m0 = mt * 128 + jj * 64 + bch * 8, t = m0 / C, c0 = m0 - t * C;
+          toff[jj] = t < 9 ? (t / 3) * 7 + t % 3 : (m0 == 9 * C ? -1 : -2);
+          tcc[jj] = c0 >> 3;
+        }
+#pragma unroll
         for (int kb = 0; kb < 2; ++kb, ++it) {
           int st;
           uint8_t* A = stage_acquire(st);
-          uint4 u[1024 / kThr];
+          uint4 u[4];
 #pragma unroll
-          for (int n = 0; n < 1024 / kThr; ++n) {  // (atom, K row, chunk)
-            const int e = tid + n * kThr;
-            const int j = e >> 9, rr = (e >> 3) & 63, ch = e & 7, r2 = kb * 64 + rr;
-            const int m0 = mt * 128 + j * 64 + ch * 8, t = m0 / C, c0 = m0 - t * C;
-            const int i = r2 / 25, p = r2 - i * 25;
-            const bool rv = r2 < kGB * 25 && b0 + i < a.B;
+          for (int n = 0; n < 4; ++n) {  // n = 2 j + h
+            const int jj = n >> 1, h = n & 1, rb = rbase[kb][h];
             u[n] = make_uint4(0, 0, 0, 0);
-            if (rv) {
-              if (t < 9) {
-                const int oy = p / 5, ox = p - oy * 5, ki = t / 3, kj = t - ki * 3;
-                u[n] = *reinterpret_cast<const uint4*>(y1s + (i * 49 + (oy + ki) * 7 + ox + kj) * C + c0);
-              } else if (m0 == 9 * C) {
+            if (rb >= 0) {
+              if (toff[jj] >= 0)
+                u[n] = *reinterpret_cast<const uint4*>(y1s + y1x<C>(rb + toff[jj], tcc[jj]));
+              else if (toff[jj] == -1)
                 u[n].x = 0x3F80u;  // bf16 1.0 in element 0
-              }
             }
           }
 #pragma unroll
-          for (int n = 0; n < 1024 / kThr; ++n) {
-            const int e = tid + n * kThr;
-            const int j = e >> 9, rr = (e >> 3) & 63, ch = e & 7;
-            *reinterpret_cast<uint4*>(A + j * 8192 + sw(rr, ch)) = u[n];
-          }
+          for (int n = 0; n < 4; ++n)
+            *reinterpret_cast<uint4*>(A + (n >> 1) * 8192 + sw(brr + 32 * (n & 1), bch)) = u[n];
           built(st);
         }
-      enc_stamp(dbg && first, 4);
+      }
+      enc_stamp(dbg && gi < 2, 4 + 20 * gi);
       // ---- dX epilogue: dA1 = dy1 * (y1 > 0) -> smem (MN-major rows r1); warp (q, hh) -> tile hh -----
       tc::mbar_wait(&bar_dx, gi & 1);
       tc::fence_after_sync();
-      enc_stamp(dbg && first, 5);
+      enc_stamp(dbg && gi < 2, 5 + 20 * gi);
       {
         const int o = hh * 128 + q * 32 + lane, i = o / 63, rem = o - i * 63, y = rem / 9, x = rem - y * 9;
         const bool ov = i < kGB && x < 7;
@@ -1092,7 +1126,7 @@ __global__ void __launch_bounds__(kThr + 32, 1) k_enc_bwd_tc(const __grid_consta
 #pragma unroll
             for (int j8 = 0; j8 < 4; ++j8) {
               float f[8];
-              const uint4 yv = *reinterpret_cast<const uint4*>(y1s + r1 * C + c0 + j8 * 8);
+              const uint4 yv = *reinterpret_cast<const uint4*>(y1s + y1x<C>(r1, (c0 >> 3) + j8));
               const __nv_bfloat162* yp = reinterpret_cast<const __nv_bfloat162*>(&yv);
 #pragma unroll
               for (int jj = 0; jj < 4; ++jj) {
@@ -1109,34 +1143,31 @@ __global__ void __launch_bounds__(kThr + 32, 1) k_enc_bwd_tc(const __grid_consta
       tc::fence_async_smem();
       tc::fence_before_sync();
       tc::named_bar(1, kThr);
-      enc_stamp(dbg && first, 6);
+      enc_stamp(dbg && gi < 2, 6 + 20 * gi);
       // ---- conv1 dW (+ db1), accumulated across groups: 4 steps of one K block (64 rows r1) ---------
       for (int s4 = 0; s4 < 4; ++s4, ++it) {
         int st;
         uint8_t* A = stage_acquire(st);
-        for (int e = tid; e < 2 * 64 * 8; e += kThr) {
-          const int j = e >> 9, rr = (e >> 3) & 63, ch = e & 7, r1 = s4 * 64 + rr;
+        // items (j, h): A row m = 64 j + 8 bch + u (j = 1 and m >= 28 are zero), K row r1 = 64 s4 +
+        // brr + 32 h (image i, output (y, x)) -> byte (ci, 2 y + ki, 2 x + kj) of image i
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int rr = brr + 32 * h, r1 = s4 * 64 + rr, i = r1 / 49, p = r1 - i * 49, y = p / 7, x = p - y * 7;
+          const bool rv = bch < 4 && r1 < kGB * 49 && b0 + i < a.B;
+          const uint8_t* xb = xs + i * 768 + 2 * y * 16 + 2 * x;
           float f[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) f[u] = 0.f;
-          const int i = r1 / 49, p = r1 - i * 49, y = p / 7, x = p - y * 7;
-          if (j == 0 && ch < 4 && r1 < kGB * 49 && b0 + i < a.B) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int m = ch * 8 + u, ci = m / 9, t = m - ci * 9, ki = t / 3, kj = t - ki * 3;
-              if (m < 27) f[u] = (float)xs[i * 768 + ci * 256 + (2 * y + ki) * 16 + 2 * x + kj];
-              else if (m == 27) f[u] = 1.f;
-            }
-          }
-          *reinterpret_cast<uint4*>(A + j * 8192 + sw(rr, ch)) = tc::pack_bf16x8(f);
+          for (int u = 0; u < 8; ++u) f[u] = !rv ? 0.f : (xoff[u] >= 0 ? (float)xb[xoff[u]] : (xoff[u] == -2 ? 1.f : 0.f));
+          *reinterpret_cast<uint4*>(A + sw(rr, bch)) = tc::pack_bf16x8(f);
+          *reinterpret_cast<uint4*>(A + 8192 + sw(rr, bch)) = make_uint4(0, 0, 0, 0);
         }
         built(st);
       }
-      enc_stamp(dbg && first, 7);
+      enc_stamp(dbg && gi < 2, 7 + 20 * gi);
       tc::mbar_wait(&bar_grp, gi & 1);  // every MMA of the group done: smem inputs may be reused
       tc::fence_after_sync();
       tc::named_bar(1, kThr);
-      enc_stamp(dbg && first, 8);
+      enc_stamp(dbg && gi < 2, 8 + 20 * gi);
     }
     // ---- per-CTA partials, row-major [row][o]: rows 0..9C = dW2 (t, c) (+ db2), then dW1 (ci, t) (+ db1)
     float* part = a.part + (int64_t)blockIdx.x * part_rows(C) * C;
