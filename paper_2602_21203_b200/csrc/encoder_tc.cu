@@ -518,6 +518,14 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
     // between two buffers.
     const int pt = tid;  // 0 .. kPW * 32 - 1
     constexpr int NPT = kPW * 32, NU = (kGF * 48 + NPT - 1) / NPT;
+    static_assert(NPT % 4 == 0, "im2col: fixed K chunk per thread");
+    const int kch = pt & 3;
+    int kof[8];  // conv1 im2col: K = 8 kch + j = (ci, ki, kj) -> byte offset ci*256 + ki*16 + kj, -1 past 27
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = kch * 8 + j, ci = k / 9, t = k - ci * 9, ki = t / 3, kj = t - ki * 3;
+      kof[j] = k < 27 ? ci * 256 + ki * 16 + kj : -1;
+    }
     // fused squint: frame k of this CTA (k = i * kGF + ii) streams into ring slot k % 2 by one bulk copy
     // (49,152 B, completion on fbar[k % 2]); the copy of frame k + 2 is issued once frame k is reduced
     const bool squint = a.mode == 1 && a.factor == 8;
@@ -640,6 +648,7 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
       const int job = blockIdx.x + i * gridDim.x;
       const int src = job / ngroups, g = job - src * ngroups, b0 = g * kGF;
       uint8_t* xb = xs + (i & 1) * (kGF * 768);
+      if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 16);
       if (squint) {
         // 8x8 block sums of each frame from shared memory, round half to even (Q1) -> xs (+ ring)
         for (int ii = 0; ii < kGF; ++ii) {
@@ -674,7 +683,7 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
       } else {
         store_stage(i, xb, rvA, rdxA, gvA);
       }
-      if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 24);
+      if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 17);
       if (squint)  // (the other modes gather with their images in load_stage / store_stage)
         for (int jb = 0; jb < a.ngj[src]; ++jb) {
           const GatherJob& gj = a.gj[src][jb];
@@ -692,15 +701,16 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
         else
           load_stage(i + 2, rvA, rdxA, gvA);
       }
-      if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 25);
+      if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 18);
       tc::named_bar(1, NPT);  // xs[i % 2] complete
-      if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 26);
+      if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 19);
       if (i >= 1) tc::mbar_wait(&a1_empty, (i - 1) & 1);
-      if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 27);
+      if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 20);
       // conv1 im2col: row (img, oy, ox), K 0..26 = (ci, ki, kj) at byte offset koff[k] from the output
       // pixel's top-left input byte; K 27..31 zero (the MMAs read the first 64 bytes of each row)
+      // (the thread's 8-wide K chunk ch = pt % 4 is fixed: its byte offsets live in registers)
       for (int e = pt; e < 384 * 4; e += NPT) {
-        const int r = e >> 2, ch = e & 3;
+        const int r = e >> 2;
         float f[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) f[j] = 0.f;
@@ -708,18 +718,17 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
           const int ii = r / 49, p = r - ii * 49, oy = p / 7, ox = p - oy * 7;
           const uint8_t* px = xb + ii * 768 + 2 * oy * 16 + 2 * ox;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int k = ch * 8 + j;
-            if (k < 27) f[j] = (float)px[s_koff[k]];
-          }
+          for (int j = 0; j < 8; ++j)
+            if (kof[j] >= 0) f[j] = (float)px[kof[j]];
         }
-        *reinterpret_cast<uint4*>(sm + L::a1 + y1_off<32>(r, ch)) = tc::pack_bf16x8(f);
+        *reinterpret_cast<uint4*>(sm + L::a1 + y1_off<32>(r, kch)) = tc::pack_bf16x8(f);
       }
       tc::fence_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&a1_full);
       if (i == 0) enc_stamp(a.dbg, 11);
-      if ((i == 2 || i == 3) && pt == 0) enc_stamp_any(a.dbg, 16 + (i - 2) * 4 + 0);
+      if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 21);
+      if (i == 4 && pt == 0) enc_stamp_any(a.dbg, 30);
     }
   } else if (warp < kPW + 4) {
     // ---- E1: conv1 epilogue -> y1 ---------------------------------------------------------------
@@ -732,6 +741,7 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
       tc::mbar_wait(&t1_full, i & 1);
       if (i >= 2) tc::mbar_wait(&y1_empty[i & 1], ((i - 2) >> 1) & 1);  // conv2 of group i - 2 read it
       tc::fence_after_sync();
+      if (i == 3 && warp == kPW && lane == 0) enc_stamp_any(a.dbg, 22);
 #pragma unroll 1
       for (int t = 0; t < 3; ++t) {
         const int r = t * 128 + q * 32 + lane;
@@ -764,7 +774,7 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
         tc::mbar_arrive(&y1_full[i & 1]);
         tc::mbar_arrive(&t1_empty);
       }
-      if ((i == 2 || i == 3) && warp == kPW && lane == 0) enc_stamp_any(a.dbg, 16 + (i - 2) * 4 + 1);
+      if (i == 3 && warp == kPW && lane == 0) enc_stamp_any(a.dbg, 23);
     }
   } else if (warp < kPW + 8) {
     // ---- E2: conv2 epilogue -> h (valid 5x5 positions, HWC) ------------------------------------------
@@ -775,6 +785,7 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
       bf16_t* hout = a.hb[src];
       tc::mbar_wait(&t2_full, i & 1);
       tc::fence_after_sync();
+      if (i == 3 && warp == kPW + 4 && lane == 0) enc_stamp_any(a.dbg, 24);
 #pragma unroll 1
       for (int t = 0; t < 3; ++t) {
         const int r = t * 128 + q * 32 + lane, ii = r / 49, p = r - ii * 49, oy = p / 7, ox = p - oy * 7, b = b0 + ii;
@@ -798,7 +809,7 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&t2_empty);
-      if ((i == 2 || i == 3) && warp == kPW + 4 && lane == 0) enc_stamp_any(a.dbg, 16 + (i - 2) * 4 + 2);
+      if (i == 3 && warp == kPW + 4 && lane == 0) enc_stamp_any(a.dbg, 25);
     }
   } else {
     // ---- M: the MMAs (whole warp, one elected lane issues) --------------------------------------------
@@ -824,12 +835,15 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
     }
     for (int i = 0; i < nloc; ++i) {
       tc::mbar_wait(&y1_full[i & 1], (i >> 1) & 1);
+      if (i == 3 && lane == 0) enc_stamp_any(a.dbg, 26);
       if (i >= 1) tc::mbar_wait(&t2_empty, (i - 1) & 1);
+      if (i == 3 && lane == 0) enc_stamp_any(a.dbg, 27);
       tc::fence_after_sync();
       // (y1_full(i) implies t1_empty(i): E1 arrives both; the producers are rarely behind by more than
       // the tensor core's conv2 time, so waiting for group i + 1's im2col here costs less than letting
       // its conv1 queue behind conv2 of group i)
       if (i + 1 < nloc) conv1(i + 1);
+      if (i == 3 && lane == 0) enc_stamp_any(a.dbg, 28);
       // conv2 as nine row-shifted GEMMs over the full 7x7 grid (see k_enc_fwd_tc)
       const uint32_t y0 = tc::smem_u32(sm + L::y1 + (i & 1) * L::y1sz);
       for (int t = 0; t < 3; ++t)
@@ -843,7 +857,7 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
         }
       tc::mma_commit_e(&y1_empty[i & 1]);
       tc::mma_commit_e(&t2_full);
-      if ((i == 2 || i == 3) && lane == 0) enc_stamp_any(a.dbg, 16 + (i - 2) * 4 + 3);
+      if (i == 3 && lane == 0) enc_stamp_any(a.dbg, 29);
     }
   }
   if (tid == 32 && nloc == 0) tc::mbar_wait(&wbar, 0);  // never exit with the bulk copy in flight
@@ -1039,7 +1053,6 @@ __global__ void __launch_bounds__(kThr + 32, 1) k_enc_bwd_tc(const __grid_consta
     if (blockIdx.x < ngroups) load_group(blockIdx.x);
     for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++gi) {
       const int b0 = g * kGB;
-      const bool first = gi == 0;
       {
 #pragma unroll
         for (int k = 0; k < n_d2; ++k) {
@@ -1066,7 +1079,7 @@ __global__ void __launch_bounds__(kThr + 32, 1) k_enc_bwd_tc(const __grid_consta
       tc::named_bar(1, kThr);
       if (lane == 0) tc::mbar_arrive(&d2_full);
       load_group(g + gridDim.x);  // in flight during this group's builds
-      enc_stamp(dbg && gi < 2, 2 + 20 * gi);
+      enc_stamp(dbg && gi == 0, 2);
       // ---- conv2 dW (+ db2 via the ones row), accumulated across groups: one row tile x one K block
       //      per stage, built while the dX MMAs run.  Item (j, h) of a stage: A row m = 128 mt + 64 j +
       //      8 bch .. +7 (tap t, channels c0 ..), K row r2 = 64 kb + brr + 32 h (image i, output p) ->
@@ -1109,11 +1122,11 @@ __global__ void __launch_bounds__(kThr + 32, 1) k_enc_bwd_tc(const __grid_consta
           built(st);
         }
       }
-      enc_stamp(dbg && gi < 2, 4 + 20 * gi);
+      enc_stamp(dbg && gi == 0, 4);
       // ---- dX epilogue: dA1 = dy1 * (y1 > 0) -> smem (MN-major rows r1); warp (q, hh) -> tile hh -----
       tc::mbar_wait(&bar_dx, gi & 1);
       tc::fence_after_sync();
-      enc_stamp(dbg && gi < 2, 5 + 20 * gi);
+      enc_stamp(dbg && gi == 0, 5);
       {
         const int o = hh * 128 + q * 32 + lane, i = o / 63, rem = o - i * 63, y = rem / 9, x = rem - y * 9;
         const bool ov = i < kGB && x < 7;
@@ -1143,7 +1156,7 @@ __global__ void __launch_bounds__(kThr + 32, 1) k_enc_bwd_tc(const __grid_consta
       tc::fence_async_smem();
       tc::fence_before_sync();
       tc::named_bar(1, kThr);
-      enc_stamp(dbg && gi < 2, 6 + 20 * gi);
+      enc_stamp(dbg && gi == 0, 6);
       // ---- conv1 dW (+ db1), accumulated across groups: 4 steps of one K block (64 rows r1) ---------
       for (int s4 = 0; s4 < 4; ++s4, ++it) {
         int st;
@@ -1163,11 +1176,11 @@ __global__ void __launch_bounds__(kThr + 32, 1) k_enc_bwd_tc(const __grid_consta
         }
         built(st);
       }
-      enc_stamp(dbg && gi < 2, 7 + 20 * gi);
+      enc_stamp(dbg && gi == 0, 7);
       tc::mbar_wait(&bar_grp, gi & 1);  // every MMA of the group done: smem inputs may be reused
       tc::fence_after_sync();
       tc::named_bar(1, kThr);
-      enc_stamp(dbg && gi < 2, 8 + 20 * gi);
+      enc_stamp(dbg && gi == 0, 8);
     }
     // ---- per-CTA partials, row-major [row][o]: rows 0..9C = dW2 (t, c) (+ db2), then dW1 (ci, t) (+ db1)
     float* part = a.part + (int64_t)blockIdx.x * part_rows(C) * C;
