@@ -209,22 +209,65 @@ __device__ __forceinline__ int shadow_slot(const ShadowTable& t, int i) {
   return -1;
 }
 
+// One group's shadow refresh.  Work unit = (row, 128-column segment) of an entry, one warp per
+// unit: a float4 per lane (-> 4 bf16) for plain entries; for the projection weight's (channel,
+// pixel) -> (pixel, channel) column permutation, 4 gathered elements per lane in destination order,
+// all loads issued before the stores.  (The element-wise version spent two runtime divisions per
+// element and walked the entries one after another.)
+__device__ __forceinline__ void shadow_rows(const float* __restrict__ master, const ShadowTable& t, int gw, int nw) {
+  const int lane = threadIdx.x & 31;
+  const bool m16 = (reinterpret_cast<uintptr_t>(master) & 15) == 0;
+  int ubase = 0;
+  for (int k = 0; k < t.n; ++k) {
+    const ShadowEnt& e = t.e[k];
+    const int nseg = (e.cols + 127) >> 7, units = e.rows * nseg;
+    int u0 = (gw - ubase) % nw;
+    if (u0 < 0) u0 += nw;
+    const bool vec = e.perm_c == 0 && m16 && ((e.cols | (int)e.src | e.ld | (int)e.dst) & 3) == 0;
+    for (int u = u0; u < units; u += nw) {
+      const int row = u / nseg, c0 = (u - row * nseg) << 7;
+      const float* src = master + e.src + (int64_t)row * e.cols;
+      __nv_bfloat16* dst = t.base + e.dst + (int64_t)row * e.ld;
+      if (vec) {
+        const int c = c0 + 4 * lane;
+        if (c < e.cols) {
+          const float4 v = *reinterpret_cast<const float4*>(src + c);
+          const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+          uint2 w;
+          w.x = *reinterpret_cast<const uint32_t*>(&lo);
+          w.y = *reinterpret_cast<const uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(dst + c) = w;
+        }
+      } else {
+        float v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int cc = c0 + lane + 32 * i;
+          v[i] = 0.f;
+          if (cc < e.cols) {
+            int sc = cc;
+            if (e.perm_c > 0) {
+              const int pix = cc / e.perm_c, ch = cc - pix * e.perm_c;
+              sc = ch * e.perm_p + pix;
+            }
+            v[i] = src[sc];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int cc = c0 + lane + 32 * i;
+          if (cc < e.cols) dst[cc] = __float2bfloat16_rn(v[i]);
+        }
+      }
+    }
+    ubase += units;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_shadow(const float* __restrict__ master, const __grid_constant__ ShadowTable t) {
   grid_wait();
   grid_trigger();
-  for (int k = 0; k < t.n; ++k) {
-    const ShadowEnt& e = t.e[k];
-    const int n = e.rows * e.cols;
-    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < n; l += gridDim.x * blockDim.x) {
-      const int row = l / e.cols, col = l - row * e.cols;
-      int cc = col;
-      if (e.perm_c > 0) {
-        const int ch = col / e.perm_p, pix = col - ch * e.perm_p;
-        cc = pix * e.perm_c + ch;
-      }
-      t.base[(int)e.dst + row * e.ld + cc] = __float2bfloat16_rn(master[e.src + l]);
-    }
-  }
+  shadow_rows(master, t, blockIdx.x * 8 + (threadIdx.x >> 5), gridDim.x * 8);
 }
 
 __global__ void __launch_bounds__(256) k_adam_sh(float4* __restrict__ p, const float4* __restrict__ g,
@@ -325,21 +368,7 @@ struct ShadowJobs {
 __global__ void __launch_bounds__(256) k_shadow3(const __grid_constant__ ShadowJobs j) {
   grid_wait();
   grid_trigger();
-  const ShadowTable& t = j.t[blockIdx.y];
-  const float* __restrict__ master = j.master[blockIdx.y];
-  for (int k = 0; k < t.n; ++k) {
-    const ShadowEnt& e = t.e[k];
-    const int n = e.rows * e.cols;
-    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < n; l += gridDim.x * blockDim.x) {
-      const int row = l / e.cols, col = l - row * e.cols;
-      int cc = col;
-      if (e.perm_c > 0) {
-        const int ch = col / e.perm_p, pix = col - ch * e.perm_p;
-        cc = pix * e.perm_c + ch;
-      }
-      t.base[(int)e.dst + row * e.ld + cc] = __float2bfloat16_rn(master[e.src + l]);
-    }
-  }
+  shadow_rows(j.master[blockIdx.y], j.t[blockIdx.y], blockIdx.x * 8 + (threadIdx.x >> 5), gridDim.x * 8);
 }
 
 int launch_shadow3(const float* const master[3], const ShadowTable* const t[3], cudaStream_t s) {
