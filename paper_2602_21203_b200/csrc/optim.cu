@@ -209,6 +209,33 @@ __device__ __forceinline__ int shadow_slot(const ShadowTable& t, int i) {
   return -1;
 }
 
+// The shadow slots of flat indices i .. i + 3 (i % 4 == 0) after an optimizer step: one entry
+// search per float4; the four values go out as one 8-byte store when they sit in one row of a
+// plain entry (every entry with cols % 4 == 0), else element by element.
+__device__ __forceinline__ void shadow_store4(const ShadowTable& t, int i, const float* f) {
+  for (int k = 0; k < t.n; ++k) {
+    const ShadowEnt& e = t.e[k];
+    const int l = i - (int)e.src;
+    if (l >= 0 && l < e.rows * e.cols) {
+      if (e.perm_c == 0 && ((e.cols | l | e.ld | (int)e.dst) & 3) == 0) {
+        const int row = l / e.cols, col = l - row * e.cols;
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(f[0], f[1]), hi = __floats2bfloat162_rn(f[2], f[3]);
+        uint2 w;
+        w.x = *reinterpret_cast<const uint32_t*>(&lo);
+        w.y = *reinterpret_cast<const uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(t.base + e.dst + (int64_t)row * e.ld + col) = w;
+        return;
+      }
+      break;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int sl = shadow_slot(t, i + k);
+    if (sl >= 0) t.base[sl] = __float2bfloat16_rn(f[k]);
+  }
+}
+
 // One group's shadow refresh.  Work unit = (row, 128-column segment) of an entry, one warp per
 // unit: a float4 per lane (-> 4 bf16) for plain entries; for the projection weight's (channel,
 // pixel) -> (pixel, channel) column permutation, 4 gathered elements per lane in destination order,
@@ -320,13 +347,7 @@ __global__ void __launch_bounds__(256) k_adam_sh(float4* __restrict__ p, const f
     m[i] = mm;
     v[i] = vv;
     p[i] = pp;
-    if (t.n) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int sl = shadow_slot(t, base + (int)(4 * i + k));
-        if (sl >= 0) t.base[sl] = __float2bfloat16_rn(pf[k]);
-      }
-    }
+    if (t.n) shadow_store4(t, base + (int)(4 * i), pf);
   }
   if (part) {
     ss = block_sum(ss, red);
@@ -347,14 +368,7 @@ __global__ void __launch_bounds__(256) k_polyak_sh(float4* __restrict__ t4, cons
     a.z = keep * a.z + tau * b.z;
     a.w = keep * a.w + tau * b.w;
     t4[i] = a;
-    if (t.n) {
-      const float* af = reinterpret_cast<const float*>(&a);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int sl = shadow_slot(t, (int)(4 * i + k));
-        if (sl >= 0) t.base[sl] = __float2bfloat16_rn(af[k]);
-      }
-    }
+    if (t.n) shadow_store4(t, (int)(4 * i), reinterpret_cast<const float*>(&a));
   }
 }
 
