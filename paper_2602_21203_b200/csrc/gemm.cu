@@ -38,7 +38,7 @@ constexpr float kLog2Pi = 1.8378770664093453f;
 constexpr float kSquashEps = 1e-6f;
 constexpr int kColaccOff = 4 * 4 * 4096;                  // after the 4 warp pairs' box rings
 constexpr int kEpiBytes = kColaccOff + 4 * 3 * 512 * 4;    // + LN-bwd column partials [4][3][512]
-constexpr int kStaticSmem = 16 * 1024;  // k_gemm's static __shared__ (ptxas: ~14.6 KB), inside the 227 KB per CTA
+constexpr int kStaticSmem = 17 * 1024;  // static __shared__ of k_gemm (~14.6 KB) / k_gemm_ln16 (~16.6 KB), inside the 227 KB per CTA
 
 int g_pdl = 1;
 
@@ -745,6 +745,364 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
 }
 
 // ---------------------------------------------------------------------------------------------
+// LayerNorm backward over wide whole tiles (c3: 128 x 256 tiles of 512-wide rows in 2-CTA
+// clusters): the same producer / MMA roles as k_gemm, and an epilogue run by 16 warps instead of
+// 8.  The k_gemm epilogue of such a tile was issue- and latency-bound at two warps per SM
+// sub-partition (~6.5 us per pass over the tile, ncu: 6.9-8.7 cycles per issued instruction);
+// here warp w takes TMEM lane quarter w % 4 and column quarter w / 4, in 8-column steps (TMEM
+// loads one step ahead) with 8-value shuffle column sums, so each thread holds ~40 live values.
+// Host contract (gemm_launch): ks == 1, every problem's slice bn a multiple of 64 and <= 256,
+// N % bn == 0, M % 128 == 0 (no ragged rows or columns).
+constexpr int kBlnThreads = 512;
+
+// column sums of 8 values per lane over the warp's 32 rows: lane l returns column l % 8 (fixed
+// butterfly order: bitwise reproducible)
+__device__ __forceinline__ float colsum8(float (&v)[8]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 4; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int j = 0; j < s; ++j) {
+      const float send = up ? v[j] : v[j + s];
+      const float keep = up ? v[j + s] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  float t = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 8);
+  return t + __shfl_xor_sync(0xffffffffu, t, 16);
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kBlnThreads, 1) k_gemm_ln16(const __grid_constant__ GBatch b) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], done_bar, ld_bar[8], stats_bar;
+  __shared__ uint32_t tmem_slot;
+  __shared__ float red[2][4][128];
+  __shared__ float2 cl_red[8][128];
+  __shared__ __align__(16) float s_g[512], s_beta[512];
+  __shared__ __align__(16) GProb sP;
+  constexpr bool BWD = EPI == GE_BWD_LN_RELU || EPI == GE_BWD_LN_TANH;
+  static_assert(BWD, "k_gemm_ln16: LayerNorm backward only");
+
+  const int tile = blockIdx.x;
+  int pi = 0;
+  while (pi + 1 < b.nprob && tile >= b.p[pi + 1].tile0) ++pi;
+  {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(&b.p[pi]);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(&sP);
+    for (int i = threadIdx.x; i < (int)(sizeof(GProb) / 4); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const GProb& P = sP;
+  const int lt = tile - P.tile0;
+  const int mt = lt / P.tiles_n;
+  const int m0 = mt * 128, n0 = (lt % P.tiles_n) * P.bn;
+  const int nreal = P.bn;  // host contract: whole slices
+  const uint32_t ncols = nreal <= 32 ? 32u : (nreal <= 64 ? 64u : (nreal <= 128 ? 128u : 256u));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int S = b.nstages;
+  auto stamp = [&](int k) {
+    if (b.dbg && tid == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      b.dbg[blockIdx.x * kDbgSlots + k] = t;
+    }
+  };
+  stamp(0);
+  if (warp == 0) tc::tmem_alloc(&tmem_slot, ncols);
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < S; ++i) {
+      tc::mbar_init(&full_bar[i], 1);
+      tc::mbar_init(&empty_bar[i], 1);
+    }
+    tc::mbar_init(&done_bar, 1);
+    for (int i = 0; i < 8; ++i) tc::mbar_init(&ld_bar[i], 1);
+    tc::mbar_init(&stats_bar, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 2 && lane < P.nseg) {
+    tc::tma_prefetch_desc(&b.maps[P.seg[lane].amap]);
+    tc::tma_prefetch_desc(&b.maps[P.seg[lane].bmap]);
+  }
+  if (warp == 2 && lane >= 8 && lane < 10) tc::tma_prefetch_desc(&b.maps[lane == 8 ? P.omap : P.xmap]);
+  tc::fence_before_sync();
+  if (b.cs > 1) tc::cluster_sync_init();
+  else __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = tmem_slot;
+  stamp(1);
+  int npre = 0;
+  if (b.prefetch_b && warp == 0 && lane == 0) {
+    int kb = 0;
+    for (int s = 0; s < P.nseg && kb < S; ++s) {
+      const GSeg& G = P.seg[s];
+      const TileGeo geo = tile_geo(P, nreal, G.b_mn);
+      for (int l = 0; l < G.nkb && kb < S; ++l, ++kb) {
+        uint8_t* Bs = smem + kb * b.stage_bytes + kABytes;
+        tc::mbar_expect_tx(&full_bar[kb], kABytes + geo.bbytes);
+        for (int i = 0; i < geo.nbox_b; ++i) {
+          if (!G.b_mn)
+            tc::tma_load_2d(Bs + i * geo.bnb * 128, &b.maps[G.bmap], G.b_k + 64 * l, P.b_n + n0 + geo.bnb * i, &full_bar[kb]);
+          else
+            tc::tma_load_2d(Bs + i * 8192, &b.maps[G.bmap], P.b_n + n0 + 64 * i, G.b_k + 64 * l, &full_bar[kb]);
+        }
+      }
+    }
+    npre = kb;
+  }
+  if (warp == 0) npre = __shfl_sync(0xffffffffu, npre, 0);
+  tc::pdl_wait();
+  tc::pdl_trigger();
+  stamp(2);
+  // epilogue geometry: warp (q, hq): TMEM lanes / tile rows 32 q .., column quarter hq; the pair
+  // p = hq / 2 owns the 64-column boxes g = p, p + 2 (half hh = hq % 2 of each)
+  const int q = warp & 3, hq = warp >> 2, pp = hq >> 1, hh = hq & 1, rl = q * 32 + lane;
+  const int row0 = m0 + q * 32, r = row0 + lane;
+  const int ngrp = nreal / 64;
+  const float rs_pre = BWD ? P.rstd[r] : 0.f;
+  uint8_t* xs = (b.xpre_off ? smem + b.xpre_off : smem) + (q * 2 + pp) * 2 * kSlotBytes;  // the pair's <= 2 boxes
+  if (BWD && b.xpre_off && hh == 0 && lane == 0) {
+    const int nb = (ngrp - pp + 1) / 2;
+    if (nb > 0) {
+      tc::mbar_expect_tx(&ld_bar[q * 2 + pp], nb * kSlotBytes);
+      for (int j = 0; j < nb; ++j)
+        tc::tma_load_2d(xs + j * kSlotBytes, &b.maps[P.xmap], n0 + (pp + 2 * j) * 64, row0, &ld_bar[q * 2 + pp]);
+    }
+  }
+  if (warp >= 2)
+    for (int c = tid - 64; c < nreal; c += kBlnThreads - 64) {
+      s_g[c] = P.g[n0 + c];
+      s_beta[c] = P.beta[n0 + c];
+    }
+
+  if (warp == 0) {
+    // ---------------- TMA producer (as k_gemm) ----------------
+    const int sbytes = b.stage_bytes, rank = b.mcast ? (int)(blockIdx.x % b.cs) : 0, cs = b.cs;
+    const uint16_t mask = (uint16_t)((1u << cs) - 1u);
+    int kb = 0, st = 0, ph = 0;
+    for (int s = 0; s < P.nseg; ++s) {
+      const GSeg G = P.seg[s];
+      const TileGeo geo = tile_geo(P, nreal, G.b_mn);
+      const void* am = &b.maps[G.amap];
+      const void* bm = &b.maps[G.bmap];
+      const int am0 = P.a_m + m0, bn0 = P.b_n + n0;
+      const uint32_t tx = kABytes + geo.bbytes;
+      for (int l = 0; l < G.nkb; ++l, ++kb) {
+        if (kb >= S) tc::mbar_wait(&empty_bar[st], ph ^ 1);
+        uint8_t* As = smem + st * sbytes;
+        uint8_t* Bs = As + kABytes;
+        const bool pre = kb < npre;
+        const int kc = G.a_k + 64 * l, kcb = G.b_k + 64 * l;
+        if (!pre) tc::mbar_expect_tx_e(&full_bar[st], tx);
+        if (b.mcast) {
+          if ((kb & (cs - 1)) == rank) {
+            if (!G.a_mn) {
+              tc::tma_load_2d_mc_e(As, am, kc, am0, &full_bar[st], mask);
+            } else {
+              tc::tma_load_2d_mc_e(As, am, am0, kc, &full_bar[st], mask);
+              tc::tma_load_2d_mc_e(As + 8192, am, am0 + 64, kc, &full_bar[st], mask);
+            }
+          }
+        } else if (!G.a_mn) {
+          tc::tma_load_2d_e(As, am, kc, am0, &full_bar[st]);
+        } else {
+          tc::tma_load_2d_e(As, am, am0, kc, &full_bar[st]);
+          tc::tma_load_2d_e(As + 8192, am, am0 + 64, kc, &full_bar[st]);
+        }
+        if (!pre) {
+          if (!G.b_mn)
+            for (int i = 0; i < geo.nbox_b; ++i)
+              tc::tma_load_2d_e(Bs + i * geo.bnb * 128, bm, kcb, bn0 + geo.bnb * i, &full_bar[st]);
+          else
+            for (int i = 0; i < geo.nbox_b; ++i) tc::tma_load_2d_e(Bs + i * 8192, bm, bn0 + 64 * i, kcb, &full_bar[st]);
+        }
+        if (++st == S) st = 0, ph ^= 1;
+      }
+    }
+    if (lane == 0) { if (b.dbg) { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); b.dbg[blockIdx.x * kDbgSlots + 11] = t; } }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (as k_gemm; nreal <= 256: one MMA per K step) ----------------
+    const uint32_t smem0 = tc::smem_u32(smem), sbytes = (uint32_t)b.stage_bytes;
+    int kb = 0, st = 0, ph = 0;
+    for (int s = 0; s < P.nseg; ++s) {
+      const GSeg& G = P.seg[s];
+      const uint32_t id1 = tc::idesc_bf16_major(128, nreal, G.a_mn, G.b_mn);
+      const uint32_t astep = G.a_mn ? 2048u : 32u, bstep = G.b_mn ? 2048u : 32u;
+      const uint32_t albo = G.a_mn ? 8192u : 16u, blbo = G.b_mn ? 8192u : 16u;
+      for (int l = 0; l < G.nkb; ++l, ++kb) {
+        tc::mbar_wait(&full_bar[st], ph);
+        tc::fence_after_sync();
+        const uint32_t a0 = smem0 + st * sbytes, b0 = a0 + kABytes;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc::mma_bf16_e(tmem, tc::sdesc_sw128(a0 + astep * k, albo, 1024), tc::sdesc_sw128(b0 + bstep * k, blbo, 1024), id1,
+                         (kb | k) != 0);
+        tc::mma_commit_e(&empty_bar[st]);
+        if (++st == S) st = 0, ph ^= 1;
+      }
+    }
+    tc::mma_commit_e(&done_bar);
+  }
+  __syncwarp();
+  if (tid == 0) tc::mbar_wait(&done_bar, 0);
+  __syncthreads();
+  tc::fence_after_sync();
+  stamp(3);
+
+  const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+  // row totals: the four column quarters of this CTA (smem, in order), then the cluster CTAs
+  auto row_total4 = [&](float& t1, float& t2) {
+    if (b.cs > 1 && tid == 0) tc::mbar_expect_tx(&stats_bar, b.cs * 128 * 8);
+    red[0][hq][rl] = t1;
+    red[1][hq][rl] = t2;
+    __syncthreads();
+    t1 = (red[0][0][rl] + red[0][1][rl]) + (red[0][2][rl] + red[0][3][rl]);
+    t2 = (red[1][0][rl] + red[1][1][rl]) + (red[1][2][rl] + red[1][3][rl]);
+    if (b.cs > 1) {
+      const uint32_t me = (uint32_t)(blockIdx.x % b.cs);
+      if (hq == 0)
+        for (int rk = 0; rk < b.cs; ++rk)
+          tc::st_async_v2(tc::mapa(&cl_red[me][rl], (uint32_t)rk), t1, t2, tc::mapa(&stats_bar, (uint32_t)rk));
+      tc::mbar_wait(&stats_bar, 0);
+      t1 = t2 = 0.f;
+      for (int rk = 0; rk < b.cs; ++rk) {
+        t1 += cl_red[rk][rl].x;
+        t2 += cl_red[rk][rl].y;
+      }
+    }
+  };
+  {
+    // x_hat boxes (when not prefetched: now, into the pair's slots past the freed ring start)
+    if (!b.xpre_off && hh == 0 && lane == 0) {
+      const int nb = (ngrp - pp + 1) / 2;
+      if (nb > 0) {
+        tc::mbar_expect_tx(&ld_bar[q * 2 + pp], nb * kSlotBytes);
+        for (int j = 0; j < nb; ++j)
+          tc::tma_load_2d(xs + j * kSlotBytes, &b.maps[P.xmap], n0 + (pp + 2 * j) * 64, row0, &ld_bar[q * 2 + pp]);
+      }
+    }
+    if (pp < ngrp) tc::mbar_wait(&ld_bar[q * 2 + pp], 0);
+    stamp(5);
+    float* colacc = reinterpret_cast<float*>(smem + kColaccOff);  // [4][3][512]
+    // dn = dL/d(g x_hat + beta) through the activation
+    auto dnf = [&](float v, float x, float gg, float be) {
+      const float n = fmaf(x, gg, be);
+      return (EPI == GE_BWD_LN_RELU) ? (n > 0.f ? v : 0.f) : v * sech2_fast(n);
+    };
+    float s1 = 0.f, s2 = 0.f;
+    for (int g = pp; g < ngrp; g += 2) {
+      const int c0 = g * 64 + hh * 32;
+      const uint8_t* xb = xs + (g >> 1) * kSlotBytes;
+      uint32_t cur[8], nxt[8];
+      tc::tmem_ld8_async(trow + c0, cur);
+      tc::tmem_wait8(cur);
+  #pragma unroll 1
+      for (int k = 0; k < 4; ++k) {
+        if (k < 3) tc::tmem_ld8_async(trow + c0 + 8 * (k + 1), nxt);
+        const uint4 u = *reinterpret_cast<const uint4*>(xb + gd::box_off(lane, 4 * hh + k));
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+        const float4 ga = *reinterpret_cast<const float4*>(&s_g[c0 + 8 * k]);
+        const float4 gb = *reinterpret_cast<const float4*>(&s_g[c0 + 8 * k + 4]);
+        const float4 ba = *reinterpret_cast<const float4*>(&s_beta[c0 + 8 * k]);
+        const float4 bb = *reinterpret_cast<const float4*>(&s_beta[c0 + 8 * k + 4]);
+        const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+        const float bv[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+        float pg[8], pb[8];
+  #pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float2 f = __bfloat1622float2(h2[j >> 1]);
+          const float x = (j & 1) ? f.y : f.x;
+          const float dn = dnf(__uint_as_float(cur[j]), x, gv[j], bv[j]);
+          const float dxh = dn * gv[j];
+          s1 += dxh;
+          s2 += dxh * x;
+          pg[j] = dn * x;
+          pb[j] = dn;
+        }
+        const float cg = colsum8(pg), cb = colsum8(pb);
+        if (lane < 8) {
+          colacc[(q * 3 + 1) * 512 + c0 + 8 * k + lane] = cg;
+          colacc[(q * 3 + 2) * 512 + c0 + 8 * k + lane] = cb;
+        }
+        if (k < 3) {
+          tc::tmem_wait8(nxt);
+  #pragma unroll
+          for (int j = 0; j < 8; ++j) cur[j] = nxt[j];
+        }
+      }
+    }
+    float m1 = s1, m2 = s2;
+    row_total4(m1, m2);
+    stamp(6);
+    m1 /= (float)P.N;
+    m2 /= (float)P.N;
+    const float rs = rs_pre;
+    for (int g = pp; g < ngrp; g += 2) {
+      const int c0 = g * 64 + hh * 32;
+      uint8_t* sl = xs + (g >> 1) * kSlotBytes;
+      uint32_t cur[8], nxt[8];
+      tc::tmem_ld8_async(trow + c0, cur);
+      tc::tmem_wait8(cur);
+  #pragma unroll 1
+      for (int k = 0; k < 4; ++k) {
+        if (k < 3) tc::tmem_ld8_async(trow + c0 + 8 * (k + 1), nxt);
+        uint4* xp = reinterpret_cast<uint4*>(sl + gd::box_off(lane, 4 * hh + k));
+        const uint4 u = *xp;
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+        const float4 ga = *reinterpret_cast<const float4*>(&s_g[c0 + 8 * k]);
+        const float4 gb = *reinterpret_cast<const float4*>(&s_g[c0 + 8 * k + 4]);
+        const float4 ba = *reinterpret_cast<const float4*>(&s_beta[c0 + 8 * k]);
+        const float4 bb = *reinterpret_cast<const float4*>(&s_beta[c0 + 8 * k + 4]);
+        const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+        const float bv[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+        float o[8];
+  #pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float2 f = __bfloat1622float2(h2[j >> 1]);
+          const float x = (j & 1) ? f.y : f.x;
+          const float dn = dnf(__uint_as_float(cur[j]), x, gv[j], bv[j]);
+          o[j] = rs * (dn * gv[j] - m1 - x * m2);
+        }
+        *xp = tc::pack_bf16x8(o);
+        const float cx = colsum8(o);
+        if (lane < 8) colacc[(q * 3 + 0) * 512 + c0 + 8 * k + lane] = cx;
+        if (k < 3) {
+          tc::tmem_wait8(nxt);
+  #pragma unroll
+          for (int j = 0; j < 8; ++j) cur[j] = nxt[j];
+        }
+      }
+      // the pair's box g is complete: to the TMA unit (named barrier of the pair's 64 threads)
+      tc::fence_async_smem();
+      tc::named_bar(1 + q * 2 + pp, 64);
+      if (hh == 0 && lane == 0) {
+        tc::tma_store_2d(&b.maps[P.omap], sl, n0 + g * 64, row0);
+        tc::bulk_commit();
+      }
+    }
+    __syncthreads();
+    if (P.part) {
+      for (int e = tid; e < 3 * nreal; e += kBlnThreads) {
+        const int kk = e / nreal, c = e - kk * nreal;
+        float sacc = 0.f;
+  #pragma unroll
+        for (int qq = 0; qq < 4; ++qq) sacc += colacc[(qq * 3 + kk) * 512 + c];
+        P.part[((int64_t)mt * 3 + kk) * P.N + n0 + c] = sacc;
+      }
+    }
+  }
+  stamp(7);
+  if (lane == 0) tc::bulk_wait_read<0>();
+  tc::fence_before_sync();
+  __syncthreads();
+  stamp(4);
+  if (b.dbg && tid == 0) b.dbg[blockIdx.x * kDbgSlots + 15] = (unsigned long long)(EPI | 128) | ((unsigned long long)gridDim.x << 8);
+  if (warp == 0) tc::tmem_dealloc(tmem, ncols);
+}
+
+// ---------------------------------------------------------------------------------------------
 // Split-K variant for narrow row-complete layers (N <= 64 with long K: the projection LayerNorm,
 // its backward, the tanh-Gaussian head and its backward).  With one 128-row tile per CTA those
 // launches ran on 4-16 SMs, serial over up to 13 K blocks, with a 32-element-per-thread
@@ -1214,6 +1572,14 @@ GemmKernel kernel_for(int epi) {
   return nullptr;
 }
 
+GemmKernel kernel_ln16_for(int epi) {
+  switch (epi) {
+    case GE_BWD_LN_RELU: return k_gemm_ln16<GE_BWD_LN_RELU>;
+    case GE_BWD_LN_TANH: return k_gemm_ln16<GE_BWD_LN_TANH>;
+  }
+  return nullptr;
+}
+
 bool row_complete(int e) {
   return e == GE_LN_RELU || e == GE_LN_TANH || e == GE_BWD_LN_RELU || e == GE_BWD_LN_TANH || e == GE_TG_FWD ||
          e == GE_TG_BWD;
@@ -1458,10 +1824,18 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   const int epi = b.p[0].epi;
   for (int i = 1; i < b.nprob; ++i)
     if (b.p[i].epi != epi) return -1;  // one epilogue kind per launch (template instance)
-  GemmKernel kern = b.ks > 1 ? kernel_sk_for(epi) : kernel_for(epi);
+  // LayerNorm backward over whole slices of 64..256 columns: the 16-warp epilogue kernel
+  // (measured for the forward LayerNorm too: no gain, its second pass is bound by the two TMA
+  // stores per tile -- c3 ln_relu 124 vs 118 us per update -- so k_gemm keeps it)
+  bool bln = b.ks == 1 && (epi == GE_BWD_LN_RELU || epi == GE_BWD_LN_TANH);
+  for (int i = 0; i < b.nprob && bln; ++i) {
+    const GProb& p = b.p[i];
+    bln = p.bn >= 64 && p.bn <= 256 && p.bn % 64 == 0 && p.N % p.bn == 0 && p.M % 128 == 0;
+  }
+  GemmKernel kern = b.ks > 1 ? kernel_sk_for(epi) : (bln ? kernel_ln16_for(epi) : kernel_for(epi));
   if (!kern) return -1;
-  static size_t attr_smem[32] = {0};  // opt-in limit set so far per instance
-  const int ai = epi + (b.ks > 1 ? 16 : 0);
+  static size_t attr_smem[48] = {0};  // opt-in limit set so far per instance
+  const int ai = epi + (b.ks > 1 ? 16 : 0) + (bln ? 32 : 0);
   if (smem > attr_smem[ai]) {
     cudaError_t ae = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ae != cudaSuccess) return (int)ae;
@@ -1492,7 +1866,7 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3(b.ntiles * b.ks);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(bln ? kBlnThreads : kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
@@ -1520,7 +1894,8 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     double flops = 0;
     for (int i = 0; i < b.nprob; ++i)
       for (int k = 0; k < b.p[i].nseg; ++k) flops += 2.0 * b.p[i].M * (double)(b.p[i].N - b.p[i].acc_col0) * b.p[i].seg[k].k;
-    note_launch(s, b.ks > 1 ? sk_names[epi] : names[epi], flops, 0);
+    static const char* ln16_names[6] = {"", "", "", "", "k_gemm_ln16<bwd_ln_relu>", "k_gemm_ln16<bwd_ln_tanh>"};
+    note_launch(s, b.ks > 1 ? sk_names[epi] : (bln ? ln16_names[epi] : names[epi]), flops, 0);
   }
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, b);
   static const bool dbg = getenv("SQUINT_DEBUG_SYNC") != nullptr;
