@@ -1638,9 +1638,15 @@ void GemmBuilder::seg(GProb& p, const Mat& A, int a_mn, int a_k, const Mat& Bm, 
   p.nseg++;
 }
 
+static int plan_fail(int line) {  // a planning / tensor-map failure: -1 (SQUINT_DEBUG_SYNC names the check)
+  static const bool dbg = getenv("SQUINT_DEBUG_SYNC") != nullptr;
+  if (dbg) fprintf(stderr, "[squint] gemm_launch: plan check at gemm.cu:%d failed\n", line);
+  return -1;
+}
+
 int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   GBatch& b = gb.b;
-  if (gb.err) return -1;
+  if (gb.err) return plan_fail(__LINE__);
   if (b.nprob == 0) return 0;
   // plan tiles.  LayerNorm epilogues need whole rows: with N >= 128 the row is split over a
   // cluster of cs CTAs of 64-column multiples (more SMs share the epilogue work).
@@ -1666,9 +1672,9 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
         (epi0 == GE_LN_TANH || epi0 == GE_LN_RELU || epi0 == GE_BWD_LN_TANH || epi0 == GE_BWD_LN_RELU))
       b.ks = 8;  // (one wave on the 148 SMs; c2 4845 -> 4975 updates/s)
   }
-  if (b.ks > kGemmMaxSplitK) return -1;
+  if (b.ks > kGemmMaxSplitK) return plan_fail(__LINE__);
   for (int i = 0; i < b.nprob; ++i)  // column partials: [mtiles * ks][3][N] floats must fit
-    if (b.p[i].part && (int64_t)((b.p[i].M + 127) / 128) * b.ks * 3 * b.p[i].N > b.p[i].part_cap) return -1;
+    if (b.p[i].part && (int64_t)((b.p[i].M + 127) / 128) * b.ks * 3 * b.p[i].N > b.p[i].part_cap) return plan_fail(__LINE__);
   if (ln_launch && b.ks == 1) {
     int cs = 8;
     for (int i = 0; i < b.nprob; ++i) {
@@ -1698,16 +1704,16 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   int t = 0, bmax = 0;
   for (int i = 0; i < b.nprob; ++i) {
     GProb& p = b.p[i];
-    if (p.M < 1 || p.N < 1 || p.nseg < 1) return -1;
+    if (p.M < 1 || p.N < 1 || p.nseg < 1) return plan_fail(__LINE__);
     for (int k = 0; k < p.nseg; ++k)  // TMA box starts along a contiguous dim: 16-byte aligned
       if ((p.seg[k].a_mn && (p.a_m & 7)) || (p.seg[k].b_mn && (p.b_n & 7)) || (p.seg[k].a_k & 63) ||
           (p.seg[k].b_k & 63))
-        return -1;
+        return plan_fail(__LINE__);
     const int n16 = (p.N + 15) & ~15;
     if (row_complete(p.epi)) {
-      if (n16 > 512) return -1;
+      if (n16 > 512) return plan_fail(__LINE__);
       p.bn = b.cs > 1 ? p.N / b.cs : n16;
-      if (b.ks > 1 && n16 > 64) return -1;
+      if (b.ks > 1 && n16 > 64) return plan_fail(__LINE__);
     } else if (p.epi == GE_DW) {
       p.bn = n16 >= 256 ? 64 : (n16 > 128 ? 128 : n16);
     } else {
@@ -1756,7 +1762,7 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   if (b.wide > 1) maxkb = (maxkb + b.wide - 1) / b.wide;  // stages hold b.wide K blocks
   S = S > maxkb ? maxkb : S;
   S = S < 2 ? 2 : S;
-  if ((size_t)S * b.stage_bytes > 200 * 1024) return -1;
+  if ((size_t)S * b.stage_bytes > 200 * 1024) return plan_fail(__LINE__);
   b.nstages = S;
   // A multicast across a LayerNorm cluster (its CTAs share the rows): only without ring reuse,
   // so no stage is refilled before every CTA's MMAs consumed it
@@ -1770,10 +1776,10 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     const int bn16 = (p.bn + 15) & ~15;
     for (int k = 0; k < p.nseg; ++k) {
       GSeg& g = p.seg[k];
-      if (b.nmaps + 2 > kGemmMaxMaps) return -1;
-      if (tmap_get(gb.segA[i][k], g.a_mn ? 64 * b.wide : 128, &b.maps[b.nmaps])) return -1;
+      if (b.nmaps + 2 > kGemmMaxMaps) return plan_fail(__LINE__);
+      if (tmap_get(gb.segA[i][k], g.a_mn ? 64 * b.wide : 128, &b.maps[b.nmaps])) return plan_fail(__LINE__);
       g.amap = b.nmaps++;
-      if (tmap_get(gb.segB[i][k], g.b_mn ? 64 * b.wide : (bn16 > 256 ? 256 : bn16), &b.maps[b.nmaps])) return -1;
+      if (tmap_get(gb.segB[i][k], g.b_mn ? 64 * b.wide : (bn16 > 256 ? 256 : bn16), &b.maps[b.nmaps])) return plan_fail(__LINE__);
       g.bmap = b.nmaps++;
     }
   }
@@ -1785,16 +1791,16 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     const bool bwd = p.epi == GE_BWD_LN_RELU || p.epi == GE_BWD_LN_TANH;
     if (b.ks > 1) continue;  // the split-K epilogue stores directly
     if (ln || bwd || p.epi == GE_RELU_MASK) {
-      if (b.nmaps + 3 > kGemmMaxMaps || !p.out) return -1;
-      if (tmap_get(Mat{p.out, p.M, p.N, p.ldo}, 32, &b.maps[b.nmaps])) return -1;
+      if (b.nmaps + 3 > kGemmMaxMaps || !p.out) return plan_fail(__LINE__);
+      if (tmap_get(Mat{p.out, p.M, p.N, p.ldo}, 32, &b.maps[b.nmaps])) return plan_fail(__LINE__);
       p.omap = b.nmaps++;
     }
     if ((ln && p.xh) || bwd) {
-      if (!p.xh || tmap_get(Mat{p.xh, p.M, p.N, p.ldx}, 32, &b.maps[b.nmaps])) return -1;
+      if (!p.xh || tmap_get(Mat{p.xh, p.M, p.N, p.ldx}, 32, &b.maps[b.nmaps])) return plan_fail(__LINE__);
       p.xmap = b.nmaps++;
     }
     if (p.epi == GE_RELU_MASK) {
-      if (!p.y || tmap_get(Mat{p.y, p.M, p.N, p.ldy}, 32, &b.maps[b.nmaps])) return -1;
+      if (!p.y || tmap_get(Mat{p.y, p.M, p.N, p.ldy}, 32, &b.maps[b.nmaps])) return plan_fail(__LINE__);
       p.ymap = b.nmaps++;
     }
   }
@@ -1823,7 +1829,7 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   smem += 1024;
   const int epi = b.p[0].epi;
   for (int i = 1; i < b.nprob; ++i)
-    if (b.p[i].epi != epi) return -1;  // one epilogue kind per launch (template instance)
+    if (b.p[i].epi != epi) return plan_fail(__LINE__);  // one epilogue kind per launch (template instance)
   // LayerNorm backward over whole slices of 64..256 columns: the 16-warp epilogue kernel
   // (measured for the forward LayerNorm too: no gain, its second pass is bound by the two TMA
   // stores per tile -- c3 ln_relu 124 vs 118 us per update -- so k_gemm keeps it)
@@ -1833,7 +1839,7 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
     bln = p.bn >= 64 && p.bn <= 256 && p.bn % 64 == 0 && p.N % p.bn == 0 && p.M % 128 == 0;
   }
   GemmKernel kern = b.ks > 1 ? kernel_sk_for(epi) : (bln ? kernel_ln16_for(epi) : kernel_for(epi));
-  if (!kern) return -1;
+  if (!kern) return plan_fail(__LINE__);
   static size_t attr_smem[48] = {0};  // opt-in limit set so far per instance
   const int ai = epi + (b.ks > 1 ? 16 : 0) + (bln ? 32 : 0);
   if (smem > attr_smem[ai]) {
@@ -1901,8 +1907,14 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   static const bool dbg = getenv("SQUINT_DEBUG_SYNC") != nullptr;
   if (dbg) {
     cudaError_t se = cudaStreamSynchronize(s);
-    fprintf(stderr, "[squint] k_gemm nprob=%d tiles=%d ks=%d stages=%d stage_bytes=%d -> %s\n", b.nprob, b.ntiles, b.ks, S,
-            b.stage_bytes, cudaGetErrorString(se));
+    fprintf(stderr, "[squint] k_gemm epi=%d nprob=%d tiles=%d ks=%d cs=%d wide=%d stages=%d stage_bytes=%d -> %s\n", epi, b.nprob,
+            b.ntiles, b.ks, b.cs, b.wide, S, b.stage_bytes, cudaGetErrorString(se));
+    for (int i = 0; i < b.nprob; ++i) {
+      int K = 0;
+      for (int k = 0; k < b.p[i].nseg; ++k) K += b.p[i].seg[k].k;
+      fprintf(stderr, "[squint]   problem %d: M %d N %d K %d bn %d tiles %d\n", i, b.p[i].M, b.p[i].N, K, b.p[i].bn,
+              b.p[i].tiles_n * ((b.p[i].M + 127) / 128));
+    }
     for (int i = 0; i < b.nprob; ++i) {
       const GProb& p = b.p[i];
       fprintf(stderr, "   p%d epi=%d M=%d N=%d bn=%d nseg=%d", i, p.epi, p.M, p.N, p.bn, p.nseg);

@@ -87,7 +87,7 @@ struct GProb {
   int omap, xmap, ymap;      // epilogue tensor maps (set by gemm_launch): out, xh, y (64 x 32 boxes)
 };
 
-constexpr int kGemmMaxProb = 8;
+constexpr int kGemmMaxProb = 16;  // (a K-split weight-gradient launch: up to 4 copies of 4 problems)
 // largest split-K cluster gemm_launch plans (k_gemm_sk): LayerNorm column partials of a split-K
 // launch take kGemmMaxSplitK * mtiles * 3 * N floats
 constexpr int kGemmMaxSplitK = 8;

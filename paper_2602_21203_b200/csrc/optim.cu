@@ -385,6 +385,27 @@ __global__ void __launch_bounds__(256) k_shadow3(const __grid_constant__ ShadowJ
   shadow_rows(j.master[blockIdx.y], j.t[blockIdx.y], blockIdx.x * 8 + (threadIdx.x >> 5), gridDim.x * 8);
 }
 
+__global__ void __launch_bounds__(256) k_split_sum(const __grid_constant__ SplitSumJobs j) {
+  grid_wait();
+  grid_trigger();
+  const int job = blockIdx.y;
+  const int n = j.n[job];
+  const float* src = j.src[job];
+  float* dst = j.dst[job];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    float acc = src[i];
+    for (int r = 1; r < j.nsplit; ++r) acc += src[(int64_t)r * n + i];
+    dst[i] = acc;
+  }
+}
+
+int launch_split_sum(const SplitSumJobs& j, cudaStream_t s) {
+  if (j.njobs <= 0) return 0;
+  note_launch(s, "k_split_sum", 0, 0);
+  launch_pdl(k_split_sum, dim3(148, j.njobs), dim3(256), 0, s, j);
+  return (int)cudaGetLastError();
+}
+
 int launch_shadow3(const float* const master[3], const ShadowTable* const t[3], cudaStream_t s) {
   ShadowJobs j;
   memset(&j, 0, sizeof(j));

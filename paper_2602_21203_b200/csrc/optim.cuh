@@ -79,6 +79,17 @@ int launch_stage_pinned(void* dst, const void* src, size_t bytes, cudaStream_t s
 int launch_polyak_shadow(float* target, const float* online, int64_t n, float tau, const ShadowTable* t,
                          cudaStream_t s);
 
+// dst_j[i] = sum_{r < nsplit} src_j[r n_j + i] in r order (the K-split partials of weight-gradient
+// launches; fixed order: bitwise reproducible)
+constexpr int kMaxSplitJobs = 16;
+struct SplitSumJobs {
+  int njobs, nsplit;
+  float* dst[kMaxSplitJobs];
+  const float* src[kMaxSplitJobs];
+  int n[kMaxSplitJobs];
+};
+int launch_split_sum(const SplitSumJobs& j, cudaStream_t s);
+
 struct MetricsArgs {
   int B;
   float inv_btotal;

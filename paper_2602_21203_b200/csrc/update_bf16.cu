@@ -68,6 +68,7 @@ struct BfLay {
   FB part_q2[2], part_q1[2], part_pq, part_a2, part_a1, part_pp;  // LayerNorm column partials
   size_t grad_critic, grad_actor, adam_part, scal, lpi_sums;
   size_t y1b, img0, img1, dA1enc, enc_part, wtiles;
+  FB dwsplit;  // fp32 partials of K-split weight-gradient launches (dw_launch)
   // bf16 shadows: critic, target, actor, and a second critic set -- update j reads the critic set of
   // parity j (theta) and its Adam writes the other one (theta+), so a kernel still reading theta on the
   // forked branch (the dh GEMM) never races the main stream's Adam (with_parity swaps sh[0] / sh[3])
@@ -76,6 +77,7 @@ struct BfLay {
 };
 
 const char* kHeads[2] = {"critic.q1", "critic.q2"};
+constexpr int kDwMaxSplit = 4;
 
 ShadowPlan shadow_plan(WsPlan& P, const squint_dims& d, const Layout& L, int grp) {
   ShadowPlan s;
@@ -211,6 +213,13 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
   w.dA1enc = 0;
   w.enc_part = fl(enc_bwd_tc_partial_floats(C, B));
   w.wtiles = P.take(conv_tiles_bytes(C));
+  {
+    // K-split weight gradients (dw_launch): up to kDwMaxSplit partial copies of the largest launch
+    const size_t crit = 2 * ((size_t)N * Hc + (size_t)Hc * Hc + (size_t)Hc * nq + N + 2 * Hc) + (size_t)Lt * F + Lt;
+    const size_t act = (size_t)2 * A * Ha + (size_t)Ha * Ha + (size_t)Ha * npi + (size_t)Lt * F + 2 * A + 2 * Ha + Lt;
+    const size_t n = (size_t)kDwMaxSplit * (crit > act ? crit : act);
+    w.dwsplit = FB{P.take(n * f), (int64_t)n};
+  }
   w.sh[0] = shadow_plan(P, d, L, SQUINT_GROUP_CRITIC);
   w.sh[1] = shadow_plan(P, d, L, SQUINT_GROUP_TARGET);
   w.sh[2] = shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
@@ -347,6 +356,77 @@ GProb& dw(GemmBuilder& gb, const Mat& D, const Mat& X, const LinG& G, int nin) {
   p.dbeta = G.beta;
   return p;
 }
+// Launches a weight-gradient batch (every problem from dw(): one MN-major segment over the K = B
+// batch rows).  At large batches with few output tiles (c3's actor: ~40 tiles of K = 4096 on 148
+// SMs, ~36 us of per-CTA latency-bound streaming) the problems are split over K into kspl copies
+// that write fp32 partials (and the ones-column bias partials) into `scratch`; k_split_sum adds
+// them in copy order (deterministic).  The LayerNorm-affine / bias partials of part_in are
+// K-independent and stay with copy 0.
+int dw_launch(GemmBuilder& gb, float* scratch, int64_t cap, cudaStream_t s) {
+  const GBatch& b = gb.b;
+  int tiles = 0, K = -1;
+  bool ok = !gb.err;
+  for (int i = 0; i < b.nprob && ok; ++i) {
+    const GProb& p = b.p[i];
+    const int n16 = (p.N + 15) & ~15, bn = n16 >= 256 ? 64 : (n16 > 128 ? 128 : n16);
+    tiles += ((p.N + bn - 1) / bn) * ((p.M + 127) / 128);
+    ok = p.nseg == 1 && p.epi == GE_DW && p.a_m == 0 && p.b_n == 0 && p.ldf == p.N && (K < 0 || K == p.seg[0].k);
+    K = p.seg[0].k;
+  }
+  int kspl = 1;
+  while (ok && K >= 2048 && kspl < kDwMaxSplit && tiles * kspl * 2 <= 148 && K % (kspl * 2 * 256) == 0 &&
+         b.nprob * kspl * 2 <= kGemmMaxProb)
+    kspl *= 2;
+  int64_t need = 0;
+  for (int i = 0; i < b.nprob; ++i) need += (int64_t)kspl * b.p[i].M * ((int64_t)b.p[i].N + (b.p[i].bias_ones ? 1 : 0));
+  if (kspl == 1 || need > cap) return gemm_launch(gb, s);
+  GemmBuilder g2(b.prefetch_b);
+  SplitSumJobs jobs;
+  memset(&jobs, 0, sizeof(jobs));
+  jobs.nsplit = kspl;
+  float* sp = scratch;
+  const int kc = K / kspl;
+  for (int i = 0; i < b.nprob; ++i) {
+    const GProb o = b.p[i];
+    const Mat A = gb.segA[i][0], Bm = gb.segB[i][0];
+    float* wpart = sp;
+    sp += (int64_t)kspl * o.M * o.N;
+    float* dbpart = nullptr;
+    if (o.bias_ones) {
+      dbpart = sp;
+      sp += (int64_t)kspl * o.M;
+    }
+    for (int r = 0; r < kspl; ++r) {
+      GProb& p = g2.add(o.M, o.N, GE_DW);
+      g2.seg(p, A, 1, o.seg[0].a_k + r * kc, Bm, 1, o.seg[0].b_k + r * kc, kc);
+      p.outf = wpart + (int64_t)r * o.M * o.N;
+      p.ldf = o.N;
+      p.bias_ones = o.bias_ones;
+      if (o.bias_ones) {
+        p.db = dbpart + (int64_t)r * o.M;
+      } else if (r == 0) {
+        p.db = o.db;
+        p.dg = o.dg;
+        p.dbeta = o.dbeta;
+        p.part_in = o.part_in;
+        p.part_tiles = o.part_tiles;
+      }
+    }
+    if (jobs.njobs + 2 > kMaxSplitJobs) return -1;
+    jobs.dst[jobs.njobs] = o.outf;
+    jobs.src[jobs.njobs] = wpart;
+    jobs.n[jobs.njobs++] = o.M * o.N;
+    if (o.bias_ones && o.db) {
+      jobs.dst[jobs.njobs] = o.db;
+      jobs.src[jobs.njobs] = dbpart;
+      jobs.n[jobs.njobs++] = o.M;
+    }
+  }
+  const int e = gemm_launch(g2, s);
+  if (e) return e;
+  return launch_split_sum(jobs, s);
+}
+
 void bwd_ln(GProb& p, const Lin& W, bf16* xh, int ldx, float* rstd, bf16* out, int ldo, float* part, int64_t part_cap) {
   p.g = W.g;
   p.beta = W.beta;
@@ -873,7 +953,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     GProb& pp = dw(gb, c.mat(w.dAp), c.mat(w.Xh), ling(L, gc, gC, "critic.proj", "critic.proj.ln"), F);
     pp.part_in = c.F(w.part_pq);
     pp.part_tiles = mt * ks_pq;
-    BF_CK(gemm_launch(gb, s));
+    BF_CK(dw_launch(gb, c.F(w.dwsplit), w.dwsplit.n, s));
   }
   if (comm) {
     BF_CK(launch_row_sums(c.F(w.logp_cur), c.F(w.row_loss), B, extras, s));
@@ -1058,7 +1138,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     GProb& pp = dw(gb, c.mat(w.adAp), c.mat(w.Xh), ling(L, ga, gA, "actor.proj", "actor.proj.ln"), F);
     pp.part_in = c.F(w.part_pp);
     pp.part_tiles = mt * ks_pp;
-    BF_CK(gemm_launch(gb, s));
+    BF_CK(dw_launch(gb, c.F(w.dwsplit), w.dwsplit.n, s));
   }
   float* lpis = c.F(w.lpi_sums);
   PhaseScope ps15(15, rep, s);
