@@ -518,14 +518,7 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
     // between two buffers.
     const int pt = tid;  // 0 .. kPW * 32 - 1
     constexpr int NPT = kPW * 32, NU = (kGF * 48 + NPT - 1) / NPT;
-    static_assert(NPT % 4 == 0, "im2col: fixed K chunk per thread");
-    const int kch = pt & 3;
-    int kof[8];  // conv1 im2col: K = 8 kch + j = (ci, ki, kj) -> byte offset ci*256 + ki*16 + kj, -1 past 27
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int k = kch * 8 + j, ci = k / 9, t = k - ci * 9, ki = t / 3, kj = t - ki * 3;
-      kof[j] = k < 27 ? ci * 256 + ki * 16 + kj : -1;
-    }
+
     // fused squint: frame k of this CTA (k = i * kGF + ii) streams into ring slot k % 2 by one bulk copy
     // (49,152 B, completion on fbar[k % 2]); the copy of frame k + 2 is issued once frame k is reduced
     const bool squint = a.mode == 1 && a.factor == 8;
@@ -708,9 +701,8 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
       if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 20);
       // conv1 im2col: row (img, oy, ox), K 0..26 = (ci, ki, kj) at byte offset koff[k] from the output
       // pixel's top-left input byte; K 27..31 zero (the MMAs read the first 64 bytes of each row)
-      // (the thread's 8-wide K chunk ch = pt % 4 is fixed: its byte offsets live in registers)
       for (int e = pt; e < 384 * 4; e += NPT) {
-        const int r = e >> 2;
+        const int r = e >> 2, ch = e & 3;
         float f[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) f[j] = 0.f;
@@ -718,10 +710,12 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
           const int ii = r / 49, p = r - ii * 49, oy = p / 7, ox = p - oy * 7;
           const uint8_t* px = xb + ii * 768 + 2 * oy * 16 + 2 * ox;
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (kof[j] >= 0) f[j] = (float)px[kof[j]];
+          for (int j = 0; j < 8; ++j) {
+            const int k = ch * 8 + j;
+            if (k < 27) f[j] = (float)px[s_koff[k]];
+          }
         }
-        *reinterpret_cast<uint4*>(sm + L::a1 + y1_off<32>(r, kch)) = tc::pack_bf16x8(f);
+        *reinterpret_cast<uint4*>(sm + L::a1 + y1_off<32>(r, ch)) = tc::pack_bf16x8(f);
       }
       tc::fence_async_smem();
       __syncwarp();
