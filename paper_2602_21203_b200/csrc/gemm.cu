@@ -1665,6 +1665,11 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
       ok = ((b.p[i].N + 15) & ~15) <= 64;
     }
     if (ok) b.ks = minkb >= 4 ? 4 : (minkb >= 2 ? 2 : 1);
+    // no more split CTAs than one wave: at c3 (B = 4096: 32 row tiles per problem) the 4-way
+    // split ran 512 CTAs in 3.5 waves
+    int mtiles = 0;
+    for (int i = 0; i < b.nprob; ++i) mtiles += (b.p[i].M + 127) / 128;
+    while (b.ks > 1 && mtiles * b.ks > 148) b.ks >>= 1;
     // LayerNorm split-K over 8 CTAs (16 rows each) when every CTA still gets >= 1 K block
     int tiles8 = 0;
     for (int i = 0; i < b.nprob; ++i) tiles8 += 8 * ((b.p[i].M + 127) / 128);
