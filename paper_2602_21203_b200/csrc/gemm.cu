@@ -1723,6 +1723,9 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
       p.bn = n16 >= 256 ? 64 : (n16 > 128 ? 128 : n16);
     } else {
       p.bn = n16 > 128 ? 128 : n16;
+      // the masked dh of the encoder at c3 (4096 x 1600, K = 50): 416 tiles of 128 columns ran in
+      // 2.8 waves; 256-column tiles halve the waves
+      if (p.epi == GE_RELU_MASK && n16 >= 1024 && ((p.M + 127) / 128) * ((p.N + 127) / 128) > 148) p.bn = 256;
     }
     p.tiles_n = (p.N + p.bn - 1) / p.bn;
     p.tile0 = t;
