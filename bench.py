@@ -6,7 +6,11 @@ One step = one Algorithm-1 iteration at BASELINE configs[2]:
   squint_act   on the 1024 squinted o_t (encoder + actor + sample, o_t written into the 1M
                replay ring's obs rows: a16 + a1),
   squint_update with UTD 4 at batch 512 (a2-a15), 101 atoms on [-20, 20].
-(--act-full: the act squints a second 128x128 batch itself, the insert writes next_obs only.)
+The insert and the act run on side streams beside the updates: the act reads a snapshot of the
+weights taken before the step's first optimizer step (squint_act_ex; the updates wait for that copy
+only) and the updates sample ring rows outside the step's own slots (the newest transitions become
+sampleable one step later).  (--act-full: the act squints a second 128x128 batch itself, the insert
+writes next_obs only.)
 
 value = optimizer updates/s of the GLOBAL batch (UTD * K / time).  With N > 1 ranks (torchrun)
 the global batch is split: --config c2 (default) keeps the metric's "batch 512" and gives each rank
@@ -225,7 +229,12 @@ def run_gpu(args):
     T = K + W
     gi = torch.Generator(device=dev)
     gi.manual_seed(2 + 1000 * rank)
-    idx_all = torch.randint(0, cap, (T, UTD, B), generator=gi, device=dev, dtype=torch.int64)
+    # step k's updates sample the ring outside the block its own act / insert write (slots of step
+    # k = [k n_env, (k + 1) n_env) mod cap): the newest transitions become sampleable one step later,
+    # so the act (policy before the step's updates, weights snapshotted by squint_act_ex) and the
+    # insert run beside the updates (R-step)
+    idx_all = torch.randint(0, cap - n_env, (T, UTD, B), generator=gi, device=dev, dtype=torch.int64)
+    idx_all = (idx_all + ((torch.arange(T, device=dev) + 1) * n_env).view(T, 1, 1)) % cap
     sh_all = torch.randint(0, 2 * d["pad"] + 1, (T, UTD, B, 4), generator=gi, device=dev, dtype=torch.uint8)
     eps_all = torch.randn((T, UTD, 2, B, A), generator=gi, device=dev)
     aeps_all = torch.randn((T, n_env, A), generator=gi, device=dev)
@@ -268,11 +277,17 @@ def run_gpu(args):
     P.squint_insert_ex(pools[NPOOL - 1], 8, stage_slots, stage[0], hwc=hwc, jitter=jit)
 
     side = torch.cuda.Stream(device=dev)
-    ins_fork, ins_done = torch.cuda.Event(), torch.cuda.Event()
+    side_act = torch.cuda.Stream(device=dev)
+    ins_fork, ins_done, act_done = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
+    weights_read = torch.cuda.Event()
+    weights_read.record()  # (created lazily by torch: materialise it before any capture)
 
-    def step(j, stream=None):
-        # act (o_t) and the insert of o_{t+1} are independent: the insert (HBM-bound) runs on a
-        # side stream beside the act's MLP; the updates wait for both (they may sample the new rows)
+    def step(j, stream=None, serial=False):
+        # The insert of o_{t+1} (HBM-bound) and the act on o_t run on side streams beside the
+        # updates: the updates sample rows outside this step's slots (idx_all), and the act reads a
+        # snapshot of the weights taken before the first optimizer step (squint_act_ex: the updates
+        # wait only for that copy).  Both join at the end of the step.  serial=True (the launch
+        # timeline) runs the act on the caller's stream before the updates.
         nx, par = pools[j % NPOOL], j % 2
         cur = stream if stream is not None else torch.cuda.current_stream()
         ins_fork.record(cur)
@@ -284,10 +299,20 @@ def run_gpu(args):
                 insert_new(nx, slots_s, stage[1 - par], stream=side)
             ins_done.record(side)
         fr = act_pool[j % NPOOL] if args.act_full else stage[par]
-        P.squint_act(L.dims, L.hp, L.actor, L.critic, fr, prop_s, aeps_s, act_out, logp_out, act_ws,
-                     ring=obs_ring, slots=slots_s, stream=stream)
-        cur.wait_event(ins_done)
+        if serial:
+            P.squint_act(L.dims, L.hp, L.actor, L.critic, fr, prop_s, aeps_s, act_out, logp_out, act_ws,
+                         ring=obs_ring, slots=slots_s, stream=stream)
+        else:
+            side_act.wait_event(ins_fork)
+            with torch.cuda.stream(side_act):
+                P.squint_act(L.dims, L.hp, L.actor, L.critic, fr, prop_s, aeps_s, act_out, logp_out, act_ws,
+                             ring=obs_ring, slots=slots_s, stream=side_act, weights_read=weights_read)
+                act_done.record(side_act)
+            cur.wait_event(weights_read)
         L.update(replay, idx_s, sh_s, eps_s, metrics, stream=stream)
+        cur.wait_event(ins_done)
+        if not serial:
+            cur.wait_event(act_done)
 
     def load_inputs(k):
         idx_s.copy_(idx_all[k], non_blocking=True)
@@ -363,7 +388,7 @@ def run_gpu(args):
     # are pessimistic; shares are taken against their own sum.
     kern, event_overhead_us = {}, None
     if use_graph and not args.no_timeline:
-        kern, event_overhead_us = timeline(S, torch, dev, lambda st: step(0, stream=st), reps=10,
+        kern, event_overhead_us = timeline(S, torch, dev, lambda st: step(0, stream=st, serial=True), reps=10,
                                            load=lambda r: load_inputs(W + (r % K)))
 
     # e2e: the environment loop through the public API from pinned host buffers.  Step t acts on
@@ -426,13 +451,20 @@ def run_gpu(args):
                     nxt[sl].copy_(h_fr[k % NPOOL][sl], non_blocking=True)
                     copied[c].record(cps[c])
             fr = dbuf[(k + 1) % 2] if args.act_full else stage[k % 2]
-            P.squint_act(L.dims, L.hp, L.actor, L.critic, fr, prop, aeps, act_out, logp_out, act_ws,
-                         ring=obs_ring, slots=slots)
-            if args.act_full:
-                freed[(k + 1) % 2].record(main)
-            for dst, src in zip(h_out[:2], (act_out, logp_out)):
-                dst.copy_(src, non_blocking=True)
+            # the act (and the read-back of its actions) beside the updates, as in the device step
+            side_act.wait_event(staged[k % 2])
+            side_act.wait_stream(main)
+            with torch.cuda.stream(side_act):
+                P.squint_act(L.dims, L.hp, L.actor, L.critic, fr, prop, aeps, act_out, logp_out, act_ws,
+                             ring=obs_ring, slots=slots, stream=side_act, weights_read=weights_read)
+                if args.act_full:
+                    freed[(k + 1) % 2].record(side_act)
+                for dst, src in zip(h_out[:2], (act_out, logp_out)):
+                    dst.copy_(src, non_blocking=True)
+                act_done.record(side_act)
+            main.wait_event(weights_read)
             L.update(replay, idx, sh, eps, metrics)
+            main.wait_event(act_done)
             main.wait_event(copied[0])
             main.wait_event(copied[1])
             if args.act_full:

@@ -218,6 +218,18 @@ SQUINT_API squint_status squint_act(const squint_dims* dims, const squint_hparam
                          int frame_w, const float* proprio, const float* eps, float* action_out,
                          float* logp_out, uint8_t* ring, const int64_t* slots, int64_t ring_capacity,
                          void* workspace, squint_stream_t stream);
+/* squint_act with weights_read (a cudaEvent_t, may be NULL = squint_act): the act first copies the
+ * weights it reads (the whole ACTOR buffer and the CRITIC encoder head) into the tail of its
+ * workspace (squint_act_workspace_bytes includes the room), records weights_read on `stream`, and
+ * computes from the copies.  A caller that runs the act beside optimizer steps (Algorithm 1 L4-5
+ * acting with the pre-update policy while L8-24 update) waits on weights_read before its first
+ * step writes ACTOR or CRITIC.  Results are bitwise those of squint_act. */
+typedef void* squint_event_t;
+SQUINT_API squint_status squint_act_ex(const squint_dims* dims, const squint_hparams* hp, const float* actor_params,
+                                       const float* critic_params, const uint8_t* frames, int64_t n, int frame_h,
+                                       int frame_w, const float* proprio, const float* eps, float* action_out,
+                                       float* logp_out, uint8_t* ring, const int64_t* slots, int64_t ring_capacity,
+                                       void* workspace, squint_stream_t stream, squint_event_t weights_read);
 
 /* ---- a2-a15: `utd` sequential SAC updates (Algorithm 1 L8-24; Q17-Q30) -------------
  * idx [utd, B] int64 in [0, replay->size) (device, unchecked);

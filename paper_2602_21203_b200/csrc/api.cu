@@ -762,15 +762,26 @@ squint_status squint_workspace_region(const squint_dims* dims, int region, size_
   return SQUINT_OK;
 }
 
+// squint_act_ex's weight snapshot (the ACTOR group and the CRITIC encoder head), placed past the
+// act's own workspace
+static size_t act_snapshot_floats(const squint_dims& d) {
+  const Layout L = make_layout(d);
+  return (size_t)((L.gsize[SQUINT_GROUP_ACTOR] + 3) & ~int64_t(3)) + (size_t)((L.enc_end + 3) & ~int64_t(3));
+}
+static size_t act_core_bytes(const squint_dims& d, int64_t n);
+
 squint_status squint_act_workspace_bytes(const squint_dims* dims, int64_t n, size_t* bytes) {
   if (!dims || !bytes) return fail(SQUINT_EINVAL, "NULL argument");
   std::string e;
   if (!check_dims(*dims, &e)) return fail(SQUINT_EINVAL, e);
   if (n < 0) return fail(SQUINT_EINVAL, "n must be >= 0");
-  if (dims->precision == SQUINT_BF16) {
-    *bytes = bf16_act_workspace_bytes(*dims, n);
-    return SQUINT_OK;
-  }
+  *bytes = ((act_core_bytes(*dims, n) + 255) & ~size_t(255)) + act_snapshot_floats(*dims) * sizeof(float);
+  return SQUINT_OK;
+}
+
+static size_t act_core_bytes(const squint_dims& dd, int64_t n) {
+  const squint_dims* dims = &dd;
+  if (dims->precision == SQUINT_BF16) return bf16_act_workspace_bytes(*dims, n);
   const size_t f = sizeof(float), F = flat_dim(*dims);
   WsPlan P;
   P.take(n * F * f);                           // h
@@ -778,8 +789,7 @@ squint_status squint_act_workspace_bytes(const squint_dims* dims, int64_t n, siz
   P.take(n * dims->actor_hidden * f);          // h1
   P.take(n * dims->actor_hidden * f);          // h2
   P.take(n * 2 * dims->action_dim * f);        // out
-  *bytes = P.top + 256;
-  return SQUINT_OK;
+  return P.top + 256;
 }
 
 squint_status squint_insert2(const uint8_t* frames, int64_t n, int c, int h, int w, int factor, const int64_t* slots,
@@ -865,6 +875,15 @@ squint_status squint_act(const squint_dims* dims, const squint_hparams* hp, cons
                          const float* critic_params, const uint8_t* frames, int64_t n, int frame_h, int frame_w,
                          const float* proprio, const float* eps, float* action_out, float* logp_out, uint8_t* ring,
                          const int64_t* slots, int64_t ring_capacity, void* workspace, squint_stream_t stream) {
+  return squint_act_ex(dims, hp, actor_params, critic_params, frames, n, frame_h, frame_w, proprio, eps, action_out,
+                       logp_out, ring, slots, ring_capacity, workspace, stream, nullptr);
+}
+
+squint_status squint_act_ex(const squint_dims* dims, const squint_hparams* hp, const float* actor_params,
+                            const float* critic_params, const uint8_t* frames, int64_t n, int frame_h, int frame_w,
+                            const float* proprio, const float* eps, float* action_out, float* logp_out, uint8_t* ring,
+                            const int64_t* slots, int64_t ring_capacity, void* workspace, squint_stream_t stream,
+                            squint_event_t weights_read) {
   if (!dims || !hp) return fail(SQUINT_EINVAL, "NULL dims/hparams");
   std::string e;
   if (!check_dims(*dims, &e)) return fail(SQUINT_EINVAL, e);
@@ -887,6 +906,21 @@ squint_status squint_act(const squint_dims* dims, const squint_hparams* hp, cons
     return fail(SQUINT_EINVAL, "frames must be 16-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
   const squint_dims& d = *dims;
+  if (weights_read) {
+    // snapshot the weights the act reads (ACTOR, CRITIC encoder head) into the workspace tail, then
+    // signal: from here on the act reads only the copies, so the caller may start optimizer steps
+    const Layout Ls = make_layout(d);
+    float* snap = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) +
+                                           ((act_core_bytes(d, n) + 255) & ~size_t(255)));
+    float* snap_c = snap + ((Ls.gsize[SQUINT_GROUP_ACTOR] + 3) & ~int64_t(3));
+    if (cudaMemcpyAsync(snap, actor_params, Ls.gsize[SQUINT_GROUP_ACTOR] * sizeof(float), cudaMemcpyDeviceToDevice, s) !=
+            cudaSuccess ||
+        cudaMemcpyAsync(snap_c, critic_params, Ls.enc_end * sizeof(float), cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+        cudaEventRecord((cudaEvent_t)weights_read, s) != cudaSuccess)
+      return fail(SQUINT_ECUDA, "squint_act_ex: weight snapshot");
+    actor_params = snap;
+    critic_params = snap_c;
+  }
   if (d.precision == SQUINT_BF16)
     return bf16_act(d, *hp, actor_params, critic_params, frames, n, f, proprio, eps, action_out, logp_out, ring, slots,
                     workspace, s);

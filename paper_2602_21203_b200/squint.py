@@ -83,6 +83,8 @@ def _load():
         "squint_insert_ex": (st, [vp, i64, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp]),
         "squint_act": (st, [C.POINTER(Dims), C.POINTER(HParams), vp, vp, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp,
                             i64, vp, vp]),
+        "squint_act_ex": (st, [C.POINTER(Dims), C.POINTER(HParams), vp, vp, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp,
+                            i64, vp, vp, vp]),
         "squint_update": (st, [C.POINTER(Dims), C.POINTER(HParams), C.POINTER(Replay), vp, vp, vp, i32,
                                C.POINTER(State), vp, vp, sz, vp, vp]),
         "squint_soft_update": (st, [vp, vp, i64, f32, vp]),
@@ -106,7 +108,7 @@ def _load():
 LIB = _load()
 EXPORTED = ["squint_last_error", "squint_version", "squint_param_layout", "squint_workspace_bytes",
             "squint_workspace_region", "squint_act_workspace_bytes", "squint_comm_unique_id", "squint_comm_init",
-            "squint_comm_destroy", "squint_insert", "squint_insert2", "squint_insert_ex", "squint_act", "squint_update", "squint_soft_update", "squint_stage_pinned",
+            "squint_comm_destroy", "squint_insert", "squint_insert2", "squint_insert_ex", "squint_act", "squint_act_ex", "squint_update", "squint_soft_update", "squint_stage_pinned",
             "squint_launch_count", "squint_set_phase_events", "squint_phase_name", "squint_selftest_gemm",
             "squint_set_launch_events", "squint_record_launch_event", "squint_launch_info",
             "squint_set_option"]
@@ -321,11 +323,19 @@ def selftest_gemm(A: torch.Tensor, a_cols: int, a_mn: int, B: torch.Tensor, b_co
 
 def squint_act(dims: Dims, hp: HParams, actor: torch.Tensor, critic: torch.Tensor, frames: torch.Tensor,
                proprio: torch.Tensor, eps, action_out: torch.Tensor, logp_out, workspace: torch.Tensor,
-               ring=None, slots=None, stream=None):
+               ring=None, slots=None, stream=None, weights_read=None):
+    """weights_read: optional torch.cuda.Event recorded once the act has copied the weights it reads
+    (squint_act_ex): optimizer steps may start after it."""
     n, _, fh, fw = frames.shape
-    _check(LIB.squint_act(C.byref(dims), C.byref(hp), _ptr(actor), _ptr(critic), _ptr(frames), n, fh, fw,
-                          _ptr(proprio), _ptr(eps), _ptr(action_out), _ptr(logp_out), _ptr(ring), _ptr(slots),
-                          0 if ring is None else ring.shape[0], _ptr(workspace), _stream(stream)))
+    args = (C.byref(dims), C.byref(hp), _ptr(actor), _ptr(critic), _ptr(frames), n, fh, fw,
+            _ptr(proprio), _ptr(eps), _ptr(action_out), _ptr(logp_out), _ptr(ring), _ptr(slots),
+            0 if ring is None else ring.shape[0], _ptr(workspace), _stream(stream))
+    if weights_read is None:
+        _check(LIB.squint_act(*args))
+    else:
+        if not weights_read.cuda_event:
+            raise ValueError("weights_read: record the torch.cuda.Event once before use (it is created lazily)")
+        _check(LIB.squint_act_ex(*args, C.c_void_p(weights_read.cuda_event)))
 
 
 def squint_update(dims: Dims, hp: HParams, replay: Replay, idx, shifts, eps, state: State, metrics,

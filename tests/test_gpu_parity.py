@@ -596,3 +596,35 @@ def test_gemm_engine(a_mn, b_mn, M, N, K):
     P.squint.selftest_gemm(A, ac, a_mn, B, bc, b_mn, M, N, K, out)
     torch.cuda.synchronize()
     compare("gemm", out.cpu().numpy(), ref.numpy(), 1e-5)
+
+
+def test_act_ex_weight_snapshot_bitwise():
+    """squint_act_ex (weights copied into the workspace tail, an event recorded after the copy) gives
+    bitwise the results of squint_act; overwriting the master weights after the event does not
+    change the act that is still running from the copies (the act-beside-the-updates step)."""
+    pr = Problem("c2", seed=9, capacity=2048)
+    L = pr.gpu_setup(precision=P.BF16)
+    n = 1024
+    fr = torch.as_tensor(SI.make_frames(n, 16, seed=3)).to(DEV)
+    prop = torch.as_tensor(SI.make_proprio(n, 12, seed=3)).to(DEV)
+    eps = torch.as_tensor(np.random.default_rng(3).standard_normal((n, 6)).astype(np.float32)).to(DEV)
+    dims = P.make_dims(pr.dims, P.BF16)
+    hp = P.make_hparams(pr.hp)
+    ws = torch.zeros(P.act_workspace_bytes(dims, n), dtype=torch.uint8, device=DEV)
+    a0, l0 = torch.zeros((n, 6), device=DEV), torch.zeros(n, device=DEV)
+    P.squint_act(dims, hp, L.actor, L.critic, fr, prop, eps, a0, l0, ws)
+    ev = torch.cuda.Event()
+    ev.record()
+    a1, l1 = torch.zeros((n, 6), device=DEV), torch.zeros(n, device=DEV)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    actor0, critic0 = L.actor.clone(), L.critic.clone()
+    with torch.cuda.stream(side):
+        P.squint_act(dims, hp, L.actor, L.critic, fr, prop, eps, a1, l1, ws, stream=side, weights_read=ev)
+    torch.cuda.current_stream().wait_event(ev)
+    L.actor.mul_(-3.0)  # an "optimizer step" right after the snapshot
+    L.critic.mul_(-3.0)
+    torch.cuda.synchronize()
+    assert torch.equal(a0, a1) and torch.equal(l0, l1)
+    L.actor.copy_(actor0)
+    L.critic.copy_(critic0)
