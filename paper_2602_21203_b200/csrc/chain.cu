@@ -163,7 +163,12 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
   // then stores it to global memory and / or bulk-copies it to the 4 CTAs' next-layer A.
   // peers_only: the box already sits in this CTA's A (forward layers write their slice in
   // place), so only the other kCS - 1 CTAs receive copies
-  auto box_out = [&](uint8_t* slot, int omap, int col, bool bcast, bool peers_only = false) {
+  // emap >= 0: the exchange goes through L2 instead -- the box is stored to emap's global copy
+  // (omap's store when emap == omap), the pair leader waits for the store to complete, then one
+  // TMA load multicasts it into the peers' A slot (completion on their anext, as the DSMEM copies).
+  // DSMEM bulk copies cost the sender's shared-memory port (~20 B/clk: ~2 us per 256-wide layer
+  // for 3 x 16 KB); the TMA path moves the same bytes at L2 rates.
+  auto box_out = [&](uint8_t* slot, int omap, int col, bool bcast, bool peers_only = false, int emap = -1) {
     tc::fence_async_smem();
     tc::named_bar(1 + q, 64);
     if (hh == 0 && lane == 0) {
@@ -171,11 +176,20 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
         tc::tma_store_2d(&b.maps[omap], slot, col, row0);
         tc::bulk_commit();
       }
-      if (bcast)
+      if (bcast && emap >= 0) {
+        if (emap != omap) {
+          tc::tma_store_2d(&b.maps[emap], slot, col, row0);
+          tc::bulk_commit();
+        }
+        tc::bulk_wait_all();  // the box is in global memory
+        const uint16_t mask = (uint16_t)(((1u << kCS) - 1u) & ~(1u << rank));
+        tc::tma_load_2d_mc(A + rank * 16384 + q * 4096, &b.maps[emap], col, row0, &anext, mask);
+      } else if (bcast) {
         for (int rk = 0; rk < kCS; ++rk)
           if (!peers_only || rk != rank)
             tc::bulk_s2cluster(tc::mapa(A + rank * 16384 + q * 4096, (uint32_t)rk), slot, 4096,
                                tc::mapa(&anext, (uint32_t)rk));
+      }
     }
   };
 
@@ -264,7 +278,7 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
       tc::named_bar(1 + q, 64);
       box_put(sy, hh, v);
       if (L.xmap >= 0) box_put(sx, hh, a);
-      box_out(sy, L.omap, n0, bcast, true);
+      box_out(sy, L.omap, n0, bcast, true, L.emap);
       if (L.xmap >= 0) box_out(sx, L.xmap, n0, false);
     } else if (epi == GE_BWD_LN_RELU || epi == GE_BWD_LN_TANH) {
       // pass 1: dn through the activation, row sums of dxh = dn g and dxh x_hat, column partials of
@@ -310,7 +324,7 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
       box_put(sy, hh, v);
       const float cx = colsum32(a);
       colacc[(q * 3 + 0) * 64 + hh * 32 + lane] = cx;
-      box_out(sy, L.omap, n0, bcast, true);
+      box_out(sy, L.omap, n0, bcast, true, L.emap);
       __syncthreads();
       if (L.part)
         for (int e = tid; e < 3 * 64; e += kThr) {
@@ -444,7 +458,7 @@ CLayer& ChainBuilder::layer(CProb& p, int epi, const Mat& W, int b_mn, int N, in
   L.b_mn = b_mn;
   L.ln_eps = 1e-5f;
   L.slice = (epi == GE_BIAS_F32) ? 32 : (epi == GE_TG_FWD ? 16 : 64);
-  L.omap = L.xmap = -1;
+  L.omap = L.xmap = L.emap = -1;
   wmat[pi][l] = W;
   omat[pi][l] = O;
   xmat[pi][l] = X;
@@ -455,6 +469,7 @@ int chain_launch(ChainBuilder& cb, cudaStream_t s) {
   CBatch& b = cb.b;
   if (cb.err || b.nprob == 0) return cb.err ? -1 : 0;
   int nm = 0, ncl = 0;
+  size_t xused = 0;
   double flops = 0;
   for (int i = 0; i < b.nprob; ++i) {
     CProb& p = b.p[i];
@@ -482,6 +497,17 @@ int chain_launch(ChainBuilder& cb, cudaStream_t s) {
         L.xmap = nm++;
       } else if (L.epi == GE_BWD_LN_RELU || L.epi == GE_BWD_LN_TANH) {
         return -1;
+      }
+      // next-layer exchange through L2 (omap, else a scratch copy while the scratch lasts)
+      if (ln && l + 1 < p.nlayers) {
+        const size_t bytes = (size_t)p.M * 256 * 2;
+        if (L.omap >= 0) {
+          L.emap = L.omap;
+        } else if (cb.xscr && xused + bytes <= cb.xcap && nm + 1 <= kChainMaxMaps) {
+          if (tmap_get(Mat{cb.xscr + xused, p.M, 256, 256}, 32, &b.maps[nm])) return -1;
+          L.emap = nm++;
+          xused += bytes;
+        }
       }
       flops += 2.0 * p.M * (double)L.N * L.K;
     }

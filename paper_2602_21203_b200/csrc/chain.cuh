@@ -33,6 +33,8 @@ struct CLayer {
   const float* g;
   const float* beta;
   int omap, xmap;  // bf16 output / x_hat tensor maps (64 x 32 boxes), -1: none
+  int emap;        // LayerNorm layers feeding a next layer: the global copy of the output the
+                   // cluster CTAs exchange through (omap, or a workspace scratch); -1: DSMEM copies
   float* rstd;     // fwd LN: written; bwd LN: read
   float* part;     // bwd LN: column partials [mtile][3][N] (may be NULL)
   float* outf;     // GE_BIAS_F32 output (fp32, ld = ldf)
@@ -72,6 +74,10 @@ struct ChainBuilder {
   Mat amat[kChainMaxProb];
   Mat wmat[kChainMaxProb][kChainMaxLayers], omat[kChainMaxProb][kChainMaxLayers], xmat[kChainMaxProb][kChainMaxLayers];
   int err = 0;
+  // global scratch for the next-layer exchange of layers without a stored output (chain_launch
+  // maps M x 256 bf16 per such layer while it lasts; the rest exchange through DSMEM)
+  char* xscr = nullptr;
+  size_t xcap = 0;
   explicit ChainBuilder(int prefetch_b = 1) {
     b.nprob = 0;
     b.nclusters = 0;

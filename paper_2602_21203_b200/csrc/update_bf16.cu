@@ -69,6 +69,7 @@ struct BfLay {
   size_t grad_critic, grad_actor, adam_part, scal, lpi_sums;
   size_t y1b, img0, img1, dA1enc, enc_part, wtiles;
   FB dwsplit;  // fp32 partials of K-split weight-gradient launches (dw_launch)
+  size_t xchg, xchg_bytes;  // chain next-layer exchange scratch (ChainBuilder::xscr)
   // bf16 shadows: critic, target, actor, and a second critic set -- update j reads the critic set of
   // parity j (theta) and its Adam writes the other one (theta+), so a kernel still reading theta on the
   // forked branch (the dh GEMM) never races the main stream's Adam (with_parity swaps sh[0] / sh[3])
@@ -220,6 +221,9 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
     const size_t n = (size_t)kDwMaxSplit * (crit > act ? crit : act);
     w.dwsplit = FB{P.take(n * f), (int64_t)n};
   }
+  // fused-chain exchange scratch: up to 4 problems x 2 hidden layers of B x 256 bf16
+  w.xchg_bytes = (chain_supported(Hc) && chain_supported(Ha)) ? (size_t)4 * 2 * B * 256 * 2 : 0;
+  w.xchg = P.take(w.xchg_bytes);
   w.sh[0] = shadow_plan(P, d, L, SQUINT_GROUP_CRITIC);
   w.sh[1] = shadow_plan(P, d, L, SQUINT_GROUP_TARGET);
   w.sh[2] = shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
@@ -671,6 +675,8 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   if (c.chain) {
     PhaseScope ps(5, rep, s);
     ChainBuilder cb(1);
+    cb.xscr = c.ws + w.xchg;
+    cb.xcap = w.xchg_bytes;
     CProb& pn = cb.add(B, c.mat(w.Xan));
     ch_fwd(cb, pn, GE_LN_RELU, am.l1, Ha, npi, none_mat(), none_mat(), nullptr, le);
     ch_fwd(cb, pn, GE_LN_RELU, am.l2, Ha, Ha, none_mat(), none_mat(), nullptr, le);
@@ -737,6 +743,8 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   if (c.chain) {
     PhaseScope ps(6, rep, s);
     ChainBuilder cb(1);
+    cb.xscr = c.ws + w.xchg;
+    cb.xcap = w.xchg_bytes;
     for (int i = 0; i < 2; ++i) {
       CProb& p = cb.add(B, c.mat(w.Xt));
       ch_fwd(cb, p, GE_LN_RELU, tq[i].l1, Hc, nq, none_mat(), none_mat(), nullptr, le);
@@ -1010,6 +1018,8 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     }
     if (c.chain) {
       ChainBuilder cb(1);
+      cb.xscr = c.ws + w.xchg;
+      cb.xcap = w.xchg_bytes;
       for (int i = 0; i < 2; ++i) {
         CProb& p = cb.add(B, c.mat(w.Xq1));
         ch_fwd(cb, p, GE_LN_RELU, cq1[i].l1, Hc, nq, none_mat(), c.mat(w.q1XH1[i]), c.F(w.q1R1[i]), le);
@@ -1270,6 +1280,7 @@ size_t bf16_act_workspace_bytes(const squint_dims& d, int64_t n) {
   P.take((size_t)n * ldp(Ha) * 2);
   shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
   P.take(conv_tiles_bytes(d.conv_ch));
+  P.take((size_t)n * 256 * 2 * 2);  // chain exchange scratch (2 hidden layers)
   return P.top + 256;
 }
 
@@ -1289,6 +1300,8 @@ squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const flo
   BM H2{P.take((size_t)n * ldp(Ha) * 2), M, Ha, ldp(Ha)};
   ShadowPlan sp = shadow_plan(P, d, L, SQUINT_GROUP_ACTOR);
   uint8_t* wtiles = reinterpret_cast<uint8_t*>(ws + P.take(conv_tiles_bytes(d.conv_ch)));
+  const size_t xchg_bytes = (size_t)n * 256 * 2 * 2;
+  char* xchg = ws + P.take(xchg_bytes);
   Ctx c{d, L, ws, s, false, nullptr};
   const int gC = SQUINT_GROUP_CRITIC, gA = SQUINT_GROUP_ACTOR;
   std::optional<PhaseScope> ps;
@@ -1333,6 +1346,8 @@ squint_status bf16_act(const squint_dims& d, const squint_hparams& hp, const flo
   if (chain_supported(Ha)) {
     // the whole actor MLP + tanh-Gaussian head in one fused chain launch
     ChainBuilder cb(1);
+    cb.xscr = xchg;
+    cb.xcap = xchg_bytes;
     CProb& pa = cb.add(M, c.mat(Xa));
     ch_fwd(cb, pa, GE_LN_RELU, am.l1, Ha, npi, none_mat(), none_mat(), nullptr, hp.ln_eps);
     ch_fwd(cb, pa, GE_LN_RELU, am.l2, Ha, Ha, none_mat(), none_mat(), nullptr, hp.ln_eps);
