@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
   __shared__ uint32_t tmem_slot;
   __shared__ float red[2][2][128];
   __shared__ float2 cl_red[kCS][128];  // per-row (sum, sum of squares) partials pushed by each CTA
-  __shared__ __align__(16) float s_bias[64], s_g[64], s_beta[64];
+  __shared__ __align__(16) float s_par[kChainMaxLayers][3][64];  // every layer's bias, g, beta slice
 
   const int rank = blockIdx.x % kCS, cl = blockIdx.x / kCS;
   int pi = 0;
@@ -97,9 +97,36 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
   // a CTA computes layer l unless l is the tanh-Gaussian head (rank 0 only); inactive CTAs load
   // nothing for that layer
   auto active_l = [&](int l) { return P.L[l].epi != GE_TG_FWD || rank == 0; };
-  if (tid == 0 && b.prefetch_b) {  // weights: never written by the immediately preceding kernel
-    issue_b(b, P.L[0], rank * P.L[0].slice, sm + kBreg, &bfull[0]);
-    if (nl > 1 && active_l(1)) issue_b(b, P.L[1], rank * P.L[1].slice, sm + kBreg + 32768, &bfull[1]);
+  // every layer's bias / LayerNorm affine slice into shared memory up front (one load per thread,
+  // all in flight together) instead of a dependent global load at the top of each layer
+  // (warps 1-7, all loads issued before the first store: warp 0 issues the TMA loads meanwhile)
+  auto stage_par = [&]() {
+    if (warp == 0) return;
+    constexpr int kPer = (kChainMaxLayers * 3 * 64 + kThr - 33) / (kThr - 32);
+    float val[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int e = tid - 32 + i * (kThr - 32), l = e / 192, kind = (e / 64) % 3, c = e % 64;
+      val[i] = 0.f;
+      if (l < nl) {
+        const CLayer& L = P.L[l];
+        const int gc = rank * L.slice + c;
+        const float* src = kind == 0 ? L.bias : (kind == 1 ? L.g : L.beta);
+        if (c < L.slice && gc < L.N && src) val[i] = src[gc];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int e = tid - 32 + i * (kThr - 32);
+      if (e < nl * 192) (&s_par[0][0][0])[e] = val[i];
+    }
+  };
+  if (b.prefetch_b) {  // weights: never written by the immediately preceding kernel
+    if (tid == 0) {
+      issue_b(b, P.L[0], rank * P.L[0].slice, sm + kBreg, &bfull[0]);
+      if (nl > 1 && active_l(1)) issue_b(b, P.L[1], rank * P.L[1].slice, sm + kBreg + 32768, &bfull[1]);
+    }
+    stage_par();
   }
   tc::pdl_wait();
   tc::pdl_trigger();
@@ -118,6 +145,7 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
   if (warp < 4)
     for (int l = 0; l < nl; ++l)
       if (bwd_l(l)) s_rs[l][rl] = rv ? P.L[l].rstd[r] : 0.f;
+  if (!b.prefetch_b) stage_par();
   if (tid == 0) {
     if (!b.prefetch_b) {
       issue_b(b, P.L[0], rank * P.L[0].slice, sm + kBreg, &bfull[0]);
@@ -201,32 +229,31 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
     const int nreal = min(L.slice, L.N - n0);
     const bool bcast = l + 1 < nl;
     uint8_t* pslots = pslots_base + (l & 1) * 8192;
-    if (tid < L.slice) {
-      const int gc = n0 + tid;
-      const bool ok = gc < L.N;
-      s_bias[tid] = (ok && L.bias) ? L.bias[gc] : 0.f;
-      s_g[tid] = (ok && L.g) ? L.g[gc] : 0.f;
-      s_beta[tid] = (ok && L.beta) ? L.beta[gc] : 0.f;
-    }
+    const float* s_bias = s_par[l][0];
+    const float* s_g = s_par[l][1];
+    const float* s_beta = s_par[l][2];
     // ---- MMA: A (smem) x this CTA's weight slice -> TMEM ----------------------------------------
     // every CTA waits for its broadcast input even when it does not use it: no DSMEM copy may
     // still be landing in this CTA's shared memory when it exits
-    if (tid == 0 && l >= 1) tc::mbar_wait(&anext, (l - 1) & 1);
-    if (tid == 0 && active && nreal > 0) {
+    // issued by all of warp 0 (one elected lane) with the descriptors built once and stepped by
+    // constant offsets: a single-thread issue loop re-deriving each descriptor cost ~1 us per layer
+    if (warp == 0 && l >= 1) tc::mbar_wait(&anext, (l - 1) & 1);
+    if (warp == 0 && active && nreal > 0) {
       if (l == 0) tc::mbar_wait(&aload, 0);
       tc::mbar_wait(&bfull[l & 1], (l >> 1) & 1);
       tc::fence_after_sync();
-      const uint32_t a0 = tc::smem_u32(A), b0 = tc::smem_u32(sm + kBreg + (l & 1) * 32768);
-      const uint32_t id = tc::idesc_bf16_major(128, L.slice, 0, L.b_mn);
-      for (int kb = 0; kb < L.nkb; ++kb)
+      const int bmn = L.b_mn, nkb = L.nkb, slice = L.slice;
+      const uint32_t id = tc::idesc_bf16_major(128, slice, 0, bmn);
+      const uint64_t ad0 = tc::sdesc_sw128(tc::smem_u32(A), 16, 1024);
+      const uint32_t b0 = tc::smem_u32(sm + kBreg + (l & 1) * 32768);
+      const uint64_t bd0 = bmn ? tc::sdesc_sw128(b0, 8192, 1024) : tc::sdesc_sw128(b0, 16, 1024);
+      const uint32_t bkb = bmn ? 512u : (uint32_t)slice * 8u, bk = bmn ? 128u : 2u;  // 16-byte units
+      for (int kb = 0; kb < nkb; ++kb)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint64_t ad = tc::sdesc_sw128(a0 + kb * 16384 + 32 * k, 16, 1024);
-          const uint64_t bd = L.b_mn ? tc::sdesc_sw128(b0 + kb * 8192 + 2048 * k, 8192, 1024)
-                                     : tc::sdesc_sw128(b0 + kb * L.slice * 128 + 32 * k, 16, 1024);
-          tc::mma_bf16(tmem, ad, bd, id, (kb | k) != 0);
-        }
-      tc::mma_commit(&done);
+        for (int k = 0; k < 4; ++k)
+          tc::mma_bf16_e(tmem, ad0 + (uint64_t)(kb * 1024 + 2 * k), bd0 + (uint64_t)(kb * bkb + k * bk), id,
+                         (kb | k) != 0);
+      tc::mma_commit_e(&done);
     }
     stamp(3 + 4 * l);
     // forward LayerNorm layers write their own slice in place: kCS - 1 incoming slices
@@ -236,7 +263,7 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
       tc::mbar_wait(&done, l & 1);
       tc::fence_after_sync();
     }
-    __syncthreads();  // s_bias / s_g / s_beta staged; layer l's MMAs done
+    __syncthreads();  // layer l's MMAs done
     // last layer: every copy into this CTA has landed; arrive now, wait at exit (all copies out of
     // this CTA have then landed too)
     if (l == nl - 1) tc::cluster_arrive_relaxed();
