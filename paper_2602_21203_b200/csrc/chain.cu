@@ -288,14 +288,11 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
       const float mean = t1 / (float)L.N;
       const float rs = rsqrtf(fmaxf(t2 / (float)L.N - mean * mean, 0.f) + L.ln_eps);
       if (rv && hh == 0 && rank == 0 && L.rstd) L.rstd[r] = rs;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int cc = hh * 32 + j;
-        const float x = bf16_round((v[j] + s_bias[cc] - mean) * rs);
-        const float n = fmaf(x, s_g[cc], s_beta[cc]);
-        a[j] = x;
-        v[j] = (epi == GE_LN_RELU) ? fmaxf(n, 0.f) : tanh_fast(n);
-      }
+      uint32_t yp[16], xp[16];
+      if (epi == GE_LN_RELU)
+        ln_fwd32<true>(v, s_bias + hh * 32, s_g + hh * 32, s_beta + hh * 32, mean, rs, yp, xp);
+      else
+        ln_fwd32<false>(v, s_bias + hh * 32, s_g + hh * 32, s_beta + hh * 32, mean, rs, yp, xp);
       // y straight into this CTA's slice (K block `rank`) of the next layer's A: this layer's MMA
       // is done, and the stats exchange above proved every peer finished reading the previous
       // broadcast of that slice
@@ -303,8 +300,8 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
       uint8_t* sx = pslots + 4096;
       if (l >= 1 && hh == 0 && lane == 0) tc::bulk_wait_read<0>();  // the pair's stores of layer l-1
       tc::named_bar(1 + q, 64);
-      box_put(sy, hh, v);
-      if (L.xmap >= 0) box_put(sx, hh, a);
+      box_put_pk(sy, hh, yp);
+      if (L.xmap >= 0) box_put_pk(sx, hh, xp);
       box_out(sy, L.omap, n0, bcast, true, L.emap);
       if (L.xmap >= 0) box_out(sx, L.xmap, n0, false);
     } else if (epi == GE_BWD_LN_RELU || epi == GE_BWD_LN_TANH) {

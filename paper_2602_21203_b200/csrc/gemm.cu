@@ -484,19 +484,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
       const int ch = 2 * g + hh;
       if (ch < nch) {
         tc::tmem_ld32(trow + ch * 32, v);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int cc = ch * 32 + j;
-          const float x = bf16_round((v[j] + s_bias[cc] - mean) * rs);
-          const float n = fmaf(x, s_g[cc], s_beta[cc]);
-          a[j] = x;
-          v[j] = (EPI == GE_LN_RELU) ? fmaxf(n, 0.f) : tanh_fast(n);
-        }
+        uint32_t yp[16], xp[16];
+        ln_fwd32<EPI == GE_LN_RELU>(v, s_bias + ch * 32, s_g + ch * 32, s_beta + ch * 32, mean, rs, yp, xp);
         // TMA stores are masked at 16-byte granularity: an output block whose last column is
         // not 8-aligned (the projection's z inside [z | s | a]) is stored directly instead.
-        if (tma_out) box_put(sy, hh, v);
-        else if (rv) row_st_bf16(P.out + (int64_t)r * P.ldo + n0 + ch * 32, min(32, nreal - ch * 32), v);
-        if (P.xh) box_put(sx, hh, a);
+        if (tma_out) {
+          box_put_pk(sy, hh, yp);
+        } else if (rv) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[2 * j] = bf2_lo(yp[j]), v[2 * j + 1] = bf2_hi(yp[j]);
+          row_st_bf16(P.out + (int64_t)r * P.ldo + n0 + ch * 32, min(32, nreal - ch * 32), v);
+        }
+        if (P.xh) box_put_pk(sx, hh, xp);
       }
       if (tma_out) pair_store(sy, &b.maps[P.omap], n0 + g * 64, row0, q, hh);
       if (P.xh) pair_store(sx, &b.maps[P.xmap], n0 + g * 64, row0, q, hh);

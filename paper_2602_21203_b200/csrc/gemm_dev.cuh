@@ -125,6 +125,34 @@ __device__ __forceinline__ void box_put(uint8_t* slot, int c, const float (&v)[3
     *reinterpret_cast<uint4*>(slot + box_off(lane, 4 * c + j)) = tc::pack_bf16x8(f);
   }
 }
+// box_put of 32 values already packed as bf16 pairs (w[j] = columns 2j, 2j + 1 of 32c ..)
+__device__ __forceinline__ void box_put_pk(uint8_t* slot, int c, const uint32_t (&w)[16]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    *reinterpret_cast<uint4*>(slot + box_off(lane, 4 * c + j)) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+}
+// two floats -> a bf16 pair (round to nearest even; one paired conversion instead of two scalar
+// ones) and the pair's values back as floats (exact)
+__device__ __forceinline__ uint32_t bf2_rn(float lo, float hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ float bf2_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf2_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+// LayerNorm forward of 32 accumulator columns of this lane's row (DESIGN R-bf16: x_hat rounded
+// to bf16 before the affine): xp = bf16 x_hat = (v + bias - mean) rs, yp = bf16 act(x_hat g + beta)
+template <bool RELU>
+__device__ __forceinline__ void ln_fwd32(const float (&v)[32], const float* sb, const float* sg, const float* sbe,
+                                         float mean, float rs, uint32_t (&yp)[16], uint32_t (&xp)[16]) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const uint32_t w = bf2_rn((v[2 * j] + sb[2 * j] - mean) * rs, (v[2 * j + 1] + sb[2 * j + 1] - mean) * rs);
+    xp[j] = w;
+    const float n0 = fmaf(bf2_lo(w), sg[2 * j], sbe[2 * j]), n1 = fmaf(bf2_hi(w), sg[2 * j + 1], sbe[2 * j + 1]);
+    yp[j] = RELU ? bf2_rn(fmaxf(n0, 0.f), fmaxf(n1, 0.f)) : bf2_rn(tanh_fast(n0), tanh_fast(n1));
+  }
+}
 __device__ __forceinline__ void box_get(const uint8_t* slot, int c, float (&v)[32]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
