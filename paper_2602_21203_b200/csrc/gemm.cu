@@ -173,16 +173,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     npre = kb;
   }
   if (warp == 0) npre = __shfl_sync(0xffffffffu, npre, 0);  // the producer loop runs warp-wide
-  tc::pdl_wait();
-  tc::pdl_trigger();
+  // The producer (warp 0) waits for the preceding kernel right before its first load, with its
+  // loop invariants computed; everything else below (x_hat / 1/sigma prefetches, epilogue
+  // parameters) is issued by the other warps, off the path to the first operand load.
+  if (warp != 0) {
+    tc::pdl_wait();
+    tc::pdl_trigger();
+  }
   stamp(2);
-  // LayerNorm backward: the pair's x_hat boxes (TMA) and the row's 1/sigma, fetched while the
-  // main loop runs (b.xpre_off: their shared-memory home past the operand ring)
+  // LayerNorm backward: the pair's x_hat boxes (TMA, by warps 4-7) and the row's 1/sigma, fetched
+  // while the main loop runs (b.xpre_off: their shared-memory home past the operand ring)
   float rs_pre = 0.f;
+  const int q0 = warp & 3, r0 = m0 + q0 * 32 + lane;
   if constexpr (EPI == GE_BWD_LN_RELU || EPI == GE_BWD_LN_TANH) {
-    const int q0 = warp & 3, r0 = m0 + q0 * 32 + lane;
-    if (r0 < P.M) rs_pre = P.rstd[r0];
-    if (b.xpre_off && warp < 4 && lane == 0) {
+    if (warp >= 2 && r0 < P.M) rs_pre = P.rstd[r0];  // warps 0 / 1: after their role loops
+    if (b.xpre_off && warp >= 4 && lane == 0) {
       const int ng = (nreal + 63) / 64;
       uint8_t* xs = smem + b.xpre_off + q0 * 4 * kSlotBytes;
       tc::mbar_expect_tx(&ld_bar[q0], ng * kSlotBytes);
@@ -218,6 +223,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     const int am0 = P.a_m + m0, bn0 = P.b_n + n0, nsb = (G.nkb + KW - 1) / KW;
     const uint32_t tx = (uint32_t)((2 + geo.nbox_b) * KW * 8192);
     int st = 0, ph = 0;
+    tc::pdl_wait();
+    tc::pdl_trigger();
     for (int sb = 0; sb < nsb; ++sb) {
       if (sb >= S) tc::mbar_wait(&empty_bar[st], ph ^ 1);
       uint8_t* As = smem + st * sbytes;
@@ -270,6 +277,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
       const void* bm = &b.maps[G.bmap];
       const int am0 = P.a_m + m0, bn0 = P.b_n + n0;
       const uint32_t tx = kABytes + geo.bbytes;
+      if (s == 0) {
+        tc::pdl_wait();
+        tc::pdl_trigger();
+      }
       for (int l = 0; l < G.nkb; ++l, ++kb) {
         if (kb >= S) tc::mbar_wait(&empty_bar[st], ph ^ 1);
         uint8_t* As = smem + st * sbytes;
@@ -338,6 +349,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
     tc::mma_commit_e(&done_bar);
   }
   __syncwarp();
+  if constexpr (EPI == GE_BWD_LN_RELU || EPI == GE_BWD_LN_TANH)
+    if (warp < 2 && r0 < P.M) rs_pre = P.rstd[r0];
   // one poller: 256 threads spinning in try_wait compete with the TMA's complete_tx traffic on
   // the shared-memory barrier unit; the rest wait in bar.sync
   if (tid == 0) tc::mbar_wait(&done_bar, 0);
