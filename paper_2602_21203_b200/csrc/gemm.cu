@@ -865,17 +865,19 @@ __global__ void __launch_bounds__(kBlnThreads, 1) k_gemm_ln16(const __grid_const
     npre = kb;
   }
   if (warp == 0) npre = __shfl_sync(0xffffffffu, npre, 0);
-  tc::pdl_wait();
-  tc::pdl_trigger();
+  if (warp != 0) {  // the producer waits right before its first load (see k_gemm)
+    tc::pdl_wait();
+    tc::pdl_trigger();
+  }
   stamp(2);
   // epilogue geometry: warp (q, hq): TMEM lanes / tile rows 32 q .., column quarter hq; the pair
   // p = hq / 2 owns the 64-column boxes g = p, p + 2 (half hh = hq % 2 of each)
   const int q = warp & 3, hq = warp >> 2, pp = hq >> 1, hh = hq & 1, rl = q * 32 + lane;
   const int row0 = m0 + q * 32, r = row0 + lane;
   const int ngrp = nreal / 64;
-  const float rs_pre = BWD ? P.rstd[r] : 0.f;
+  float rs_pre = (BWD && warp >= 2) ? P.rstd[r] : 0.f;  // warps 0 / 1: after their role loops
   uint8_t* xs = (b.xpre_off ? smem + b.xpre_off : smem) + (q * 2 + pp) * 2 * kSlotBytes;  // the pair's <= 2 boxes
-  if (BWD && b.xpre_off && hh == 0 && lane == 0) {
+  if (BWD && b.xpre_off && hh == 1 && lane == 0) {  // (the pair's second warp: warp 0 is the producer)
     const int nb = (ngrp - pp + 1) / 2;
     if (nb > 0) {
       tc::mbar_expect_tx(&ld_bar[q * 2 + pp], nb * kSlotBytes);
@@ -901,6 +903,10 @@ __global__ void __launch_bounds__(kBlnThreads, 1) k_gemm_ln16(const __grid_const
       const void* bm = &b.maps[G.bmap];
       const int am0 = P.a_m + m0, bn0 = P.b_n + n0;
       const uint32_t tx = kABytes + geo.bbytes;
+      if (s == 0) {
+        tc::pdl_wait();
+        tc::pdl_trigger();
+      }
       for (int l = 0; l < G.nkb; ++l, ++kb) {
         if (kb >= S) tc::mbar_wait(&empty_bar[st], ph ^ 1);
         uint8_t* As = smem + st * sbytes;
@@ -958,6 +964,7 @@ __global__ void __launch_bounds__(kBlnThreads, 1) k_gemm_ln16(const __grid_const
     tc::mma_commit_e(&done_bar);
   }
   __syncwarp();
+  if (BWD && warp < 2) rs_pre = P.rstd[r];
   if (tid == 0) tc::mbar_wait(&done_bar, 0);
   __syncthreads();
   tc::fence_after_sync();
@@ -1210,16 +1217,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_sk(const __grid_constant__
     }
   }
   if (warp == 0) npre = __shfl_sync(0xffffffffu, npre, 0);  // the producer loop runs warp-wide
-  tc::pdl_wait();
-  tc::pdl_trigger();
+  if (warp != 0) {  // the producer waits right before its first load (see k_gemm)
+    tc::pdl_wait();
+    tc::pdl_trigger();
+  }
   stamp(2);
-  // per-row epilogue inputs, loaded while the main loop runs: thread (row tid / 8 + 32 it,
-  // column group tid % 8); R / 32 <= 2 rows per thread
+  // per-row epilogue inputs, loaded while the main loop runs (warps 0 / 1: after their role
+  // loops): thread (row tid / 8 + 32 it, column group tid % 8); R / 32 <= 2 rows per thread
   const int cg = tid & 7, c0 = cg * 8;
   const int nit = (R + 31) / 32;  // R = 16 (ks = 8): threads of rows tid / 8 >= R idle
   uint4 xpre[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
   float rspre[2] = {0.f, 0.f};
   float tg_pre[2][2][3];  // tanh-Gaussian: [it][d = cg, cg + 8][mu | l | eps]
+  float dlp = 0.f;
+  auto load_pre = [&]() {
   for (int it = 0; it < nit; ++it) {
     const int r = m0 + (int)kr * R + (tid >> 3) + 32 * it;
     if (r >= P.M || (tid >> 3) + 32 * it >= R) continue;
@@ -1242,8 +1253,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_sk(const __grid_constant__
       }
     }
   }
-  float dlp = 0.f;
   if constexpr (EPI == GE_TG_BWD) dlp = P.dlogp_scale[0];
+  };
+  if (warp >= 2) load_pre();
   if (warp >= 2) {
     for (int c = tid - 64; c < nt; c += kThreads - 64) {
       const bool ok = c < P.N;
@@ -1257,6 +1269,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_sk(const __grid_constant__
     tc::mbar_expect_tx_e(&recv_bar, kSkRecvBytes);
     const int sbytes = b.stage_bytes;
     int st = 0, ph = 0;
+    tc::pdl_wait();
+    tc::pdl_trigger();
     for (int kb = kb0; kb < kb1; ++kb) {
       const int i = kb - kb0;
       int l;
@@ -1307,6 +1321,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_sk(const __grid_constant__
     tc::mma_commit_e(&done_bar);
   }
   __syncwarp();
+  if (warp < 2) load_pre();
   if (tid == 0) tc::mbar_wait(&done_bar, 0);
   __syncthreads();
   tc::fence_after_sync();
