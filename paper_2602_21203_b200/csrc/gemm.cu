@@ -378,7 +378,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   // rank order (every CTA gets the same bits; no remote access after the barrier).
   // (st.async into every cluster CTA's cl_red[rank], completion counted on its stats_bar; the
   // receiver sums the cs entries in rank order: every CTA gets the same bits, no cluster barrier)
-  auto row_total2 = [&](float p1, float p2, float& t1, float& t2) {
+  // (split in two so that independent work can run while the partials travel: row_push, then
+  // row_pull for the totals)
+  auto row_push = [&](float p1, float p2, float& t1, float& t2) {
     if (b.cs > 1 && tid == 0) tc::mbar_expect_tx(&stats_bar, b.cs * 128 * 8);
     red[0][hh][rl] = p1;
     red[1][hh][rl] = p2;
@@ -391,6 +393,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
       if (hh == 0)
         for (int rk = 0; rk < b.cs; ++rk)
           tc::st_async_v2(tc::mapa(&cl_red[me][rl], (uint32_t)rk), t1, t2, tc::mapa(&stats_bar, (uint32_t)rk));
+    }
+  };
+  auto row_pull = [&](float& t1, float& t2) {
+    if (b.cs > 1) {
       tc::mbar_wait(&stats_bar, 0);
       t1 = t2 = 0.f;
       for (int rk = 0; rk < b.cs; ++rk) {
@@ -398,6 +404,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
         t2 += cl_red[rk][rl].y;
       }
     }
+  };
+  auto row_total2 = [&](float p1, float p2, float& t1, float& t2) {
+    row_push(p1, p2, t1, t2);
+    row_pull(t1, t2);
   };
 
   if constexpr (EPI == GE_BIAS_F32 || EPI == GE_DW) {
@@ -555,13 +565,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
         dn[j] = d;
         xh[j] = x;
       }
+      float m1, m2;
+      row_push(s1, s2, m1, m2);
+      // the column partials while the row partials travel through the cluster
       const float cg = gd::colsum16(pg), cb = gd::colsum16(pb);
       if (lane < 16) {
         colacc[(q * 3 + 1) * 512 + c0 + lane] = cg;
         colacc[(q * 3 + 2) * 512 + c0 + lane] = cb;
       }
-      float m1, m2;
-      row_total2(s1, s2, m1, m2);
+      row_pull(m1, m2);
       stamp(6);
       m1 /= (float)N;
       m2 /= (float)N;
