@@ -74,21 +74,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   __shared__ float red[2][2][128];
   __shared__ float2 cl_red[8][128];  // per-row (sum, sum of squares) of each cluster CTA, pushed by the CTAs
   __shared__ __align__(16) float s_bias[512], s_g[512], s_beta[512];  // per-column epilogue params
-  // This CTA's problem descriptor, copied once into shared memory: indexed reads of the large
-  // __grid_constant__ batch go through the constant cache and miss there (hundreds of cycles
-  // each, measured ~0.35 us per producer-loop iteration)
-  __shared__ __align__(16) GProb sP;
+  // (the problem descriptor is read from the parameter block: a shared-memory copy of it, once
+  // needed by a producer loop that re-read it per iteration, measured 2 % slower at c2 since the
+  // loop invariants are hoisted)
 
   const int tile = blockIdx.x;
   int pi = 0;
   while (pi + 1 < b.nprob && tile >= b.p[pi + 1].tile0) ++pi;
-  {
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(&b.p[pi]);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(&sP);
-    for (int i = threadIdx.x; i < (int)(sizeof(GProb) / 4); i += blockDim.x) dst[i] = src[i];
-  }
-  __syncthreads();
-  const GProb& P = sP;
+  const GProb& P = b.p[pi];
   const int lt = tile - P.tile0;
   const int mt = lt / P.tiles_n;
   const int m0 = mt * 128, n0 = (lt % P.tiles_n) * P.bn;
