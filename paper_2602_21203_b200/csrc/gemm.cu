@@ -799,20 +799,13 @@ __global__ void __launch_bounds__(kBlnThreads, 1) k_gemm_ln16(const __grid_const
   __shared__ float red[2][4][128];
   __shared__ float2 cl_red[8][128];
   __shared__ __align__(16) float s_g[512], s_beta[512];
-  __shared__ __align__(16) GProb sP;
   constexpr bool BWD = EPI == GE_BWD_LN_RELU || EPI == GE_BWD_LN_TANH;
   static_assert(BWD, "k_gemm_ln16: LayerNorm backward only");
 
   const int tile = blockIdx.x;
   int pi = 0;
   while (pi + 1 < b.nprob && tile >= b.p[pi + 1].tile0) ++pi;
-  {
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(&b.p[pi]);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(&sP);
-    for (int i = threadIdx.x; i < (int)(sizeof(GProb) / 4); i += blockDim.x) dst[i] = src[i];
-  }
-  __syncthreads();
-  const GProb& P = sP;
+  const GProb& P = b.p[pi];
   const int lt = tile - P.tile0;
   const int mt = lt / P.tiles_n;
   const int m0 = mt * 128, n0 = (lt % P.tiles_n) * P.bn;
