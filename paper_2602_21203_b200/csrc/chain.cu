@@ -128,8 +128,21 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
     }
     stage_par();
   }
+  // the first layer's input right after the wait (by thread 0: expect_tx set and the A map and
+  // K-block count read before the wait), weights first when they could not be prefetched
+  const int nkb0 = P.L[0].nkb;
+  const void* amap = &b.maps[P.amap];
+  if (tid == 0) tc::mbar_expect_tx(&aload, (uint32_t)nkb0 * 16384u);
   tc::pdl_wait();
   tc::pdl_trigger();
+  if (tid == 0) {
+    if (!b.prefetch_b) {
+      issue_b(b, P.L[0], rank * P.L[0].slice, sm + kBreg, &bfull[0]);
+      if (nl > 1 && active_l(1)) issue_b(b, P.L[1], rank * P.L[1].slice, sm + kBreg + 32768, &bfull[1]);
+    }
+    for (int kb = 0; kb < nkb0; ++kb) tc::tma_load_2d(A + kb * 16384, amap, 64 * kb, m0, &aload);
+    stamp(2);
+  }
   // backward LayerNorm layers: x_hat boxes of the first two layers (TMA, one barrier per layer
   // parity and warp pair) and every layer's 1/sigma, fetched while the first A / MMA proceed
   auto bwd_l = [&](int l) { return P.L[l].epi == GE_BWD_LN_RELU || P.L[l].epi == GE_BWD_LN_TANH; };
@@ -146,15 +159,6 @@ __global__ void __launch_bounds__(kThr, 1) k_chain(const __grid_constant__ CBatc
     for (int l = 0; l < nl; ++l)
       if (bwd_l(l)) s_rs[l][rl] = rv ? P.L[l].rstd[r] : 0.f;
   if (!b.prefetch_b) stage_par();
-  if (tid == 0) {
-    if (!b.prefetch_b) {
-      issue_b(b, P.L[0], rank * P.L[0].slice, sm + kBreg, &bfull[0]);
-      if (nl > 1 && active_l(1)) issue_b(b, P.L[1], rank * P.L[1].slice, sm + kBreg + 32768, &bfull[1]);
-    }
-    stamp(2);
-    tc::mbar_expect_tx(&aload, (uint32_t)P.L[0].nkb * 16384u);
-    for (int kb = 0; kb < P.L[0].nkb; ++kb) tc::tma_load_2d(A + kb * 16384, &b.maps[P.amap], 64 * kb, m0, &aload);
-  }
   // the pair's boxes alternate between two sets by layer parity: a box bulk-copied to the peers in
   // layer l is rewritten only in layer l + 2, after layer l + 1's cluster barrier proved every
   // peer received it
