@@ -13,6 +13,18 @@ muts = {
  "pre_step_theta": ('    Lpi, gpi, qmean = actor_loss_and_grads(d, hp, st["critic"],', '    Lpi, gpi, qmean = actor_loss_and_grads(d, hp, _pre_critic,'),
  "shift_swap": ('O = shift_images(R["obs"][idx], shift[:, 0], shift[:, 1], p)', 'O = shift_images(R["obs"][idx], shift[:, 1], shift[:, 0], p)'),
  "shift_obs_next": ('O = shift_images(R["obs"][idx], shift[:, 0], shift[:, 1], p)', 'O = shift_images(R["obs"][idx], shift[:, 2], shift[:, 3], p)'),
+ "ln_eps_outside": ('    rstd = 1.0 / np.sqrt(var + eps)', '    rstd = 1.0 / (np.sqrt(var) + eps)'),
+ "ln_bwd_drop_term": ('dx = rstd * (dxh - dxh.mean(axis=-1, keepdims=True) - xh * (dxh * xh).mean(axis=-1, keepdims=True))',
+                      'dx = rstd * (dxh - dxh.mean(axis=-1, keepdims=True))'),
+ "adam_bias_t": ('    mhat = m / (1.0 - b1 ** t)', '    mhat = m / (1.0 - b1 ** (t + 1))'),
+ "polyak_swap": ('    return (1.0 - tau) * target + tau * online', '    return tau * target + (1.0 - tau) * online'),
+ "squash_sign": ('- 0.5 * LOG_2PI - np.log(1.0 - a * a + SQUASH_EPS)).sum(axis=1)', '- 0.5 * LOG_2PI + np.log(1.0 - a * a + SQUASH_EPS)).sum(axis=1)'),
+ "proj_weights_swap": ('                m[b, lo] += p[b, j] * (hi - bj)\n                m[b, hi] += p[b, j] * (bj - lo)',
+                       '                m[b, lo] += p[b, j] * (bj - lo)\n                m[b, hi] += p[b, j] * (hi - bj)'),
+ "proj_gamma_missing": ('            g = r[b] + not_done[b] * gamma * (z[j] - shift[b])', '            g = r[b] + not_done[b] * (z[j] - shift[b])'),
+ "proj_shift_sign": ('            g = r[b] + not_done[b] * gamma * (z[j] - shift[b])', '            g = r[b] + not_done[b] * gamma * (z[j] + shift[b])'),
+ "rhe_floor": ('    return np.rint(s / float(factor * factor)).astype(np.uint8)', '    return np.floor(s / float(factor * factor)).astype(np.uint8)'),
+ "tg_bwd_tanh_deriv": ('    dl = dlog_std * 0.5 * (hi - lo) * (1.0 - tl * tl)', '    dl = dlog_std * 0.5 * (hi - lo)'),
 }
 src = open(os.path.join(ROOT, "oracle", "squint_oracle.py")).read()
 for name, (a, b) in muts.items():
