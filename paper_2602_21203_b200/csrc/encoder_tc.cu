@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(kThr, 1) k_enc_fwd_tc(const __grid_constant__ 
 //   E2 warps 12-15 conv2 accumulator T2 -> ReLU(acc + b2) -> h (global)      (t2_full / t2_empty)
 //   M  warp 16     conv1 MMAs (A1, W1) -> T1; conv2 as nine row-shifted MMAs per tile (y1, W2) -> T2
 // Every barrier completes once per group; TMEM holds T1 (3 C columns) and T2 (3 C columns).
-constexpr int kPW = 8;                // producer warps
+constexpr int kPW = 12;               // producer warps
 constexpr int kWsWarps = kPW + 9;     // + conv1 / conv2 epilogue teams (4 + 4) + the MMA warp
 template <int C>
 struct FwdW {
