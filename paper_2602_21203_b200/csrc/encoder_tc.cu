@@ -701,21 +701,34 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1) k_enc_fwd_ws(const __grid_co
       if (i == 3 && pt == 0) enc_stamp_any(a.dbg, 20);
       // conv1 im2col: row (img, oy, ox), K 0..26 = (ci, ki, kj) at byte offset koff[k] from the output
       // pixel's top-left input byte; K 27..31 zero (the MMAs read the first 64 bytes of each row)
-      for (int e = pt; e < 384 * 4; e += NPT) {
-        const int r = e >> 2, ch = e & 3;
-        float f[8];
+      // one thread per output row: the 3 x 3 x 3 window as 18 aligned 16-bit loads (columns 2 ox ..
+      // 2 ox + 3 of each input row), was 27 byte gathers through an offset table per row
+      for (int r = pt; r < 384; r += NPT) {
+        float f[32];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) f[j] = 0.f;
+        for (int j = 0; j < 32; ++j) f[j] = 0.f;
         if (r < kGF * 49) {
           const int ii = r / 49, p = r - ii * 49, oy = p / 7, ox = p - oy * 7;
           const uint8_t* px = xb + ii * 768 + 2 * oy * 16 + 2 * ox;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int k = ch * 8 + j;
-            if (k < 27) f[j] = (float)px[s_koff[k]];
-          }
+          for (int ci = 0; ci < 3; ++ci)
+#pragma unroll
+            for (int ki = 0; ki < 3; ++ki) {
+              const uint16_t* rp = reinterpret_cast<const uint16_t*>(px + ci * 256 + ki * 16);
+              const uint32_t w0 = rp[0], w1 = rp[1];
+              const int k = ci * 9 + ki * 3;
+              f[k] = (float)(w0 & 0xffu);
+              f[k + 1] = (float)(w0 >> 8);
+              f[k + 2] = (float)(w1 & 0xffu);
+            }
         }
-        *reinterpret_cast<uint4*>(sm + L::a1 + y1_off<32>(r, ch)) = tc::pack_bf16x8(f);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          float g[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) g[j] = f[ch * 8 + j];
+          *reinterpret_cast<uint4*>(sm + L::a1 + y1_off<32>(r, ch)) = tc::pack_bf16x8(g);
+        }
       }
       tc::fence_async_smem();
       __syncwarp();
