@@ -188,6 +188,8 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # NCCL's own log (stderr) names the ranks, the transport and whether NVLS is used
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         dist.init_process_group("nccl", device_id=dev)
     precision = {"fp32": P.FP32, "bf16": P.BF16}[args.precision]
     d, hp, vlabel = variant(args)
