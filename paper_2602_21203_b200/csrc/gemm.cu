@@ -72,7 +72,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GB
   __shared__ uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], done_bar, ld_bar[8], stats_bar;
   __shared__ uint32_t tmem_slot;
   __shared__ float red[2][2][128];
-  __shared__ float2 cl_red[8][128];  // per-row (sum, sum of squares) of each cluster CTA, pushed by the CTAs
+  // per-row (sum, sum of squares) of each cluster CTA, pushed by the CTAs (8-CTA clusters only for the
+  // LayerNorm backward; 4 rows of partials keep the forward LayerNorm CTA small enough for two per SM)
+  __shared__ float2 cl_red[(EPI == GE_BWD_LN_RELU || EPI == GE_BWD_LN_TANH) ? 8 : 4][128];
   __shared__ __align__(16) float s_bias[512], s_g[512], s_beta[512];  // per-column epilogue params
   // (the problem descriptor is read from the parameter block: a shared-memory copy of it, once
   // needed by a producer loop that re-read it per iteration, measured 2 % slower at c2 since the
@@ -1795,6 +1797,14 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   if (b.wide > 1) maxkb = (maxkb + b.wide - 1) / b.wide;  // stages hold b.wide K blocks
   S = S > maxkb ? maxkb : S;
   S = S < 2 ? 2 : S;
+  // forward LayerNorm launches of more than one wave (c3: 256 CTAs of 128 x 256 tiles): two stages
+  // (96 KB) so that two CTAs fit on an SM (TMEM 2 x 256 columns) and one CTA's epilogue overlaps the
+  // other's main loop, where the second wave used to start only after the first had finished
+  if ((b.p[0].epi == GE_LN_RELU || b.p[0].epi == GE_LN_TANH) && b.ks == 1 && t > 148) {
+    bool fit = true;
+    for (int i = 0; i < b.nprob; ++i) fit = fit && b.p[i].bn <= 256;
+    if (fit && 2 * b.stage_bytes <= 96 * 1024) S = 2;
+  }
   if ((size_t)S * b.stage_bytes > 200 * 1024) return plan_fail(__LINE__);
   b.nstages = S;
   // A multicast across a LayerNorm cluster (its CTAs share the rows): only without ring reuse,
@@ -1877,6 +1887,9 @@ int gemm_launch(GemmBuilder& gb, cudaStream_t s) {
   const int ai = epi + (b.ks > 1 ? 16 : 0) + (bln ? 32 : 0);
   if (smem > attr_smem[ai]) {
     cudaError_t ae = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the largest shared-memory carveout, so that two ~110 KB CTAs (two-stage LayerNorm launches)
+    // can share an SM
+    if (ae == cudaSuccess) ae = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (ae != cudaSuccess) return (int)ae;
     attr_smem[ai] = smem;
   }
