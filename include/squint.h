@@ -156,6 +156,24 @@ SQUINT_API squint_status squint_act_workspace_bytes(const squint_dims* dims, int
 SQUINT_API squint_status squint_comm_unique_id(void* id_out);
 SQUINT_API squint_status squint_comm_init(void** comm, const void* id /* host, 128 B */, int rank, int nranks);
 SQUINT_API squint_status squint_comm_destroy(void* comm);
+/* Gradient exchange of the SQUINT_BF16 update (the per-update gradient
+ * steps of Algorithm 1, with the critic, alpha and actor ordering of Q19):
+ *   mode 0 (default): ncclAllReduce(sum) of each flat gradient group + its row-sum tail, then
+ *          Adam replicated on every rank;
+ *   mode 1: peer memory over NVLink.  Every rank's gradient, parameter and partial-sum buffers are
+ *          mapped into each process (cudaIpcMemHandle records exchanged with ncclAllGather on
+ *          first use of a buffer -- so that first call must not be inside a stream capture);
+ *          per group one kernel sums this rank's 1/G slice of the gradients from all peers in rank
+ *          order, steps Adam on it (m, v: the slice only is touched) and stores the stepped
+ *          fp32 slice into every rank's parameters; a one-block cross-rank barrier (system-scope
+ *          release/acquire counters, own epoch in device memory, graph-replay safe) follows,
+ *          then each rank refreshes its bf16 shadows.  The row-sum tails (alpha step, metrics)
+ *          are summed in the barrier before the critic step.  G <= 8.
+ *          The fp32 update (SQUINT_FP32) keeps mode 0.
+ * Call on every rank with the same mode before the next squint_update.  The state's parameter
+ * tensors (critic, actor) and the workspace must be device allocations (cudaMalloc-backed).
+ * Errors: EINVAL (NULL comm, mode not 0/1), EUNSUPPORTED (G > 8, allocation failure). */
+SQUINT_API squint_status squint_comm_set_mode(void* comm, int mode);
 
 /* ---- a1: resolution squint + insert (Q1, Q4) ------------
  * frames u8 [n, c, h, w]; ring u8 [capacity, c, h/factor, w/factor];

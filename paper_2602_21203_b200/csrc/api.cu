@@ -1110,6 +1110,12 @@ squint_status squint_comm_init(void** comm, const void* id, int rank, int nranks
   *comm = c;
   return SQUINT_OK;
 }
+squint_status squint_comm_set_mode(void* comm, int mode) {
+  if (!comm) return fail(SQUINT_EINVAL, "NULL comm");
+  if (mode != 0 && mode != 1) return fail(SQUINT_EINVAL, "mode must be 0 or 1");
+  if (comm_set_mode(reinterpret_cast<Comm*>(comm), mode) != 0) return fail(SQUINT_EUNSUPPORTED, comm_error());
+  return SQUINT_OK;
+}
 squint_status squint_comm_destroy(void* comm) {
   if (comm) comm_destroy(reinterpret_cast<Comm*>(comm));
   return SQUINT_OK;

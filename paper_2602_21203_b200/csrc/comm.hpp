@@ -13,5 +13,15 @@ int comm_init(Comm** c, const void* id128, int rank, int nranks);
 void comm_destroy(Comm* c);
 int comm_nranks(const Comm* c);
 int comm_allreduce_sum(Comm* c, float* buf, int64_t n, cudaStream_t s);
+// f1: peer-memory all-reduce fused with a sharded Adam.  mode 1 maps every
+// rank's gradient / parameter buffers into each process (CUDA IPC over NVLink) so one kernel
+// per group sums the rank's 1/G slice of the gradients from all peers, steps Adam on it and
+// stores the stepped slice into every peer's parameters.
+constexpr int kMaxRanks = 8;
+int comm_rank(const Comm* c);
+int comm_mode(const Comm* c);
+int comm_set_mode(Comm* c, int mode);
+int comm_peer_ptrs(Comm* c, const void* local, void** out /* [nranks] */);
+unsigned* comm_flags(Comm* c);  // [kMaxRanks] arrivals per source rank, [kMaxRanks] = own epoch
 const char* comm_error();
 }  // namespace sq

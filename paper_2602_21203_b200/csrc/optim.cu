@@ -511,4 +511,123 @@ int launch_lpi_sums(const float* row_lpi, const float* row_q, int B, float* out2
   return (int)cudaGetLastError();
 }
 
+// ---- f1: peer-memory gradient all-reduce fused with a sharded Adam ----
+// Cross-rank barrier: thread 0 adds 1 to its slot of every peer's arrival counters (release, system
+// scope, over NVLink), then waits until every peer's arrival count in its own counters reaches its
+// epoch + 1 (acquire).  One block; the next kernel on the stream starts after it completes.
+namespace {
+__device__ __forceinline__ void red_release_sys(unsigned* p, unsigned v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(64) k_dp_sync(const __grid_constant__ DpSync a) {
+  grid_wait();
+  grid_trigger();
+  if (threadIdx.x == 0) {
+    const unsigned e = a.own[kDpMaxRanks] + 1;
+    __threadfence_system();  // this rank's earlier writes (its gradients, its peer stores) first
+    for (int q = 0; q < a.G; ++q) red_release_sys(a.flag[q] + a.rank, 1u);
+    for (int q = 0; q < a.G; ++q)
+      while (ld_acquire_sys(a.own + q) < e) {
+      }
+    a.own[kDpMaxRanks] = e;
+  }
+  __syncthreads();
+  // the reduced row-sum tail (alpha step, metrics), summed in rank order
+  for (int t = threadIdx.x; t < a.ntail; t += blockDim.x) {
+    float acc = __ldcg(a.tail[0] + t);
+    for (int q = 1; q < a.G; ++q) acc += __ldcg(a.tail[q] + t);
+    a.tail_out[t] = acc;
+  }
+}
+
+// This rank's slice [lo4, hi4) (float4 units) of one parameter group: g = sum over ranks (rank
+// order, read from the peers' gradient buffers over NVLink), Adam (the arithmetic of k_adam_sh),
+// the stepped parameters stored into every rank's copy, sum(g^2) per block into every rank's
+// partial buffer at [rank * gridDim.x + block].  m and v: this rank's slice only is ever touched.
+__global__ void __launch_bounds__(256) k_dp_adam(const __grid_constant__ DpAdam d, float4* __restrict__ m,
+                                                 float4* __restrict__ v, float lr, float b1, float b2, float eps,
+                                                 const float* __restrict__ c1p, const float* __restrict__ c2p,
+                                                 const __grid_constant__ ShadowTable t, int grad_perm) {
+  grid_wait();
+  grid_trigger();
+  __shared__ float red[32];
+  const float c1 = c1p[0], c2 = c2p[0];
+  int pe = -1;
+  int64_t plo = 0, phi = 0;
+  if (grad_perm)
+    for (int k = 0; k < t.n; ++k)
+      if (t.e[k].perm_c > 0) {
+        pe = k;
+        plo = t.e[k].src;
+        phi = plo + (int64_t)t.e[k].rows * t.e[k].cols;
+      }
+  float ss = 0.f;
+  for (int64_t i = d.lo4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.hi4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 gg;
+    float* gf = reinterpret_cast<float*>(&gg);
+    if (pe >= 0 && 4 * i >= plo && 4 * i < phi) {
+      const ShadowEnt& e = t.e[pe];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int l = (int)(4 * i + k - plo), row = l / e.cols, col = l - row * e.cols;
+        const int ch = col / e.perm_p, pix = col - ch * e.perm_p;
+        const int64_t j = plo + (int64_t)row * e.cols + pix * e.perm_c + ch;
+        float acc = __ldcg(d.g[0] + j);
+        for (int q = 1; q < d.G; ++q) acc += __ldcg(d.g[q] + j);
+        gf[k] = acc;
+      }
+    } else {
+      gg = __ldcg(reinterpret_cast<const float4*>(d.g[0]) + i);
+      for (int q = 1; q < d.G; ++q) {
+        const float4 o = __ldcg(reinterpret_cast<const float4*>(d.g[q]) + i);
+        gg.x += o.x;
+        gg.y += o.y;
+        gg.z += o.z;
+        gg.w += o.w;
+      }
+    }
+    float4 mm = m[i], vv = v[i], pp = reinterpret_cast<const float4*>(d.p[d.rank])[i];
+    float* mf = reinterpret_cast<float*>(&mm);
+    float* vf = reinterpret_cast<float*>(&vv);
+    float* pf = reinterpret_cast<float*>(&pp);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      ss = fmaf(gf[k], gf[k], ss);
+      mf[k] = b1 * mf[k] + (1.f - b1) * gf[k];
+      vf[k] = b2 * vf[k] + (1.f - b2) * gf[k] * gf[k];
+      pf[k] = pf[k] - lr * (mf[k] * c1) / (sqrtf(vf[k] * c2) + eps);
+    }
+    m[i] = mm;
+    v[i] = vv;
+    for (int q = 0; q < d.G; ++q) reinterpret_cast<float4*>(d.p[q])[i] = pp;
+  }
+  ss = block_sum(ss, red);
+  if (threadIdx.x == 0 && d.part[0])
+    for (int q = 0; q < d.G; ++q) d.part[q][d.rank * gridDim.x + blockIdx.x] = ss;
+}
+}  // namespace
+
+int launch_dp_sync(const DpSync& a, cudaStream_t s) {
+  note_launch(s, "k_dp_sync", 0, 0);
+  launch_pdl(k_dp_sync, dim3(1), dim3(64), 0, s, a);
+  return (int)cudaGetLastError();
+}
+
+int launch_dp_adam(const DpAdam& d, float* m, float* v, float lr, float b1, float b2, float eps, const float* c1,
+                   const float* c2, const ShadowTable* t, int grad_perm, cudaStream_t s) {
+  ShadowTable none;
+  memset(&none, 0, sizeof(none));
+  note_launch(s, "k_dp_adam", 0, (16.0 + 8.0 * d.G) * 4.0 * (double)(d.hi4 - d.lo4));
+  launch_pdl(k_dp_adam, dim3(kAdamBlocks), dim3(256), 0, s, d, reinterpret_cast<float4*>(m),
+             reinterpret_cast<float4*>(v), lr, b1, b2, eps, c1, c2, t ? *t : none, grad_perm);
+  return (int)cudaGetLastError();
+}
+
 }  // namespace sq

@@ -106,4 +106,30 @@ struct MetricsArgs {
 int launch_metrics(const MetricsArgs& a, cudaStream_t s);
 int launch_lpi_sums(const float* row_lpi, const float* row_q, int B, float* out2, cudaStream_t s);
 
+// ---- f1: peer-memory all-reduce fused with a sharded Adam (data-parallel bf16 update) ----------
+// Pointers are every rank's copy of a buffer as mapped in this process (CUDA IPC; own rank = local).
+constexpr int kDpMaxRanks = 8;
+struct DpSync {
+  unsigned* flag[kDpMaxRanks];  // rank q's arrival counters [kDpMaxRanks] (+ its epoch)
+  unsigned* own;                // this rank's counters; own[kDpMaxRanks] = its epoch
+  int G, rank;
+  const float* tail[kDpMaxRanks];  // every rank's row-sum tail (ntail floats), or unused
+  float* tail_out;                 // [ntail] local: sum over ranks
+  int ntail;
+};
+// cross-rank barrier (all ranks' earlier stream work done and visible), then the tail sum
+int launch_dp_sync(const DpSync& a, cudaStream_t s);
+struct DpAdam {
+  const float* g[kDpMaxRanks];  // every rank's flat gradient of the group
+  float* p[kDpMaxRanks];        // every rank's fp32 parameters of the group
+  float* part[kDpMaxRanks];     // every rank's sum(g^2) partials [G * kAdamBlocks]
+  int G, rank;
+  int64_t lo4, hi4;             // this rank's slice, float4 units
+};
+// Adam (as launch_adam_shadow without the shadow) on this rank's slice of the all-reduced gradient;
+// t: the group's shadow table, read only for the grad_perm gather.  Needs a launch_dp_sync after it
+// before any rank reads its parameters.
+int launch_dp_adam(const DpAdam& d, float* m, float* v, float lr, float b1, float b2, float eps, const float* c1,
+                   const float* c2, const ShadowTable* t, int grad_perm, cudaStream_t s);
+
 }  // namespace sq

@@ -66,7 +66,7 @@ struct BfLay {
   size_t R1ac, R2ac, Rpq, Rpp, Rpq1, qR1[2], qR2[2], q1R1[2], q1R2[2];
   size_t tlogits, logits, logits1, m, tgo_ac, a_cur, logp_cur, logp_next, row_loss, row_q, row_lpi;
   FB part_q2[2], part_q1[2], part_pq, part_a2, part_a1, part_pp;  // LayerNorm column partials
-  size_t grad_critic, grad_actor, adam_part, scal, lpi_sums;
+  size_t grad_critic, grad_actor, adam_part, scal, lpi_sums, dp_tail;
   size_t y1b, img0, img1, dA1enc, enc_part, wtiles;
   FB dwsplit;  // fp32 partials of K-split weight-gradient launches (dw_launch)
   size_t xchg, xchg_bytes;  // chain next-layer exchange scratch (ChainBuilder::xscr)
@@ -205,7 +205,10 @@ BfLay plan_bf(const squint_dims& d, const Layout& L) {
   w.part_pp = fb(mt * 3 * Lt);
   w.grad_critic = fl(L.gsize[SQUINT_GROUP_CRITIC] + kExtra);
   w.grad_actor = fl(L.gsize[SQUINT_GROUP_ACTOR] + kExtra);
-  w.adam_part = fl(kAdamBlocks + kEncAdamBlocks);
+  // [G * kAdamBlocks] with the peer-memory data-parallel Adam (f1)
+  w.adam_part = fl(kDpMaxRanks * kAdamBlocks > kAdamBlocks + kEncAdamBlocks ? kDpMaxRanks * kAdamBlocks
+                                                                            : kAdamBlocks + kEncAdamBlocks);
+  w.dp_tail = fl(2 * kExtra);
   w.scal = fl(kScal);
   w.lpi_sums = fl(2);
   w.y1b = P.take((size_t)B * P1 * C * 2);
@@ -577,6 +580,56 @@ squint_status early_fwd(const Ctx& c, const BfLay& w_in, const squint_hparams& h
   return SQUINT_OK;
 }
 
+// ---- f1: peer-memory all-reduce fused with a sharded Adam (comm mode 1) --------------------------
+// Cross-rank barrier; with ntail > 0 also the sum over ranks of every rank's `tail` into `out`.
+squint_status dp_barrier(Comm* cm, const float* tail, float* out, int ntail, cudaStream_t s) {
+  static_assert(kDpMaxRanks == kMaxRanks, "rank bound");
+  DpSync a;
+  memset(&a, 0, sizeof(a));
+  a.G = comm_nranks(cm);
+  a.rank = comm_rank(cm);
+  void* f[kMaxRanks];
+  if (comm_peer_ptrs(cm, comm_flags(cm), f) != 0) return set_error(SQUINT_ENCCL, comm_error());
+  for (int q = 0; q < a.G; ++q) a.flag[q] = static_cast<unsigned*>(f[q]);
+  a.own = comm_flags(cm);
+  if (ntail > 0) {
+    if (comm_peer_ptrs(cm, tail, f) != 0) return set_error(SQUINT_ENCCL, comm_error());
+    for (int q = 0; q < a.G; ++q) a.tail[q] = static_cast<const float*>(f[q]);
+    a.tail_out = out;
+    a.ntail = ntail;
+  }
+  BF_CK(launch_dp_sync(a, s));
+  return SQUINT_OK;
+}
+
+// One group's optimizer step in peer mode: this rank's 1/G slice of sum_ranks(g) through Adam,
+// stored into every rank's parameters; barrier; this rank's bf16 shadow of the whole group.
+squint_status dp_adam(Comm* cm, const float* g, float* p, float* m, float* v, int64_t n, float lr,
+                      const squint_hparams& hp, const float* c1, const float* c2, float* part, const ShadowTable* t,
+                      int grad_perm, cudaStream_t s) {
+  DpAdam d;
+  memset(&d, 0, sizeof(d));
+  d.G = comm_nranks(cm);
+  d.rank = comm_rank(cm);
+  void* f[kMaxRanks];
+  if (comm_peer_ptrs(cm, g, f) != 0) return set_error(SQUINT_ENCCL, comm_error());
+  for (int q = 0; q < d.G; ++q) d.g[q] = static_cast<const float*>(f[q]);
+  if (comm_peer_ptrs(cm, p, f) != 0) return set_error(SQUINT_ENCCL, comm_error());
+  for (int q = 0; q < d.G; ++q) d.p[q] = static_cast<float*>(f[q]);
+  if (part) {
+    if (comm_peer_ptrs(cm, part, f) != 0) return set_error(SQUINT_ENCCL, comm_error());
+    for (int q = 0; q < d.G; ++q) d.part[q] = static_cast<float*>(f[q]);
+  }
+  const int64_t n4 = n / 4;
+  d.lo4 = n4 * d.rank / d.G;
+  d.hi4 = n4 * (d.rank + 1) / d.G;
+  BF_CK(launch_dp_adam(d, m, v, lr, hp.beta1, hp.beta2, hp.adam_eps, c1, c2, t, grad_perm, s));
+  squint_status r = dp_barrier(cm, nullptr, nullptr, 0, s);
+  if (r != SQUINT_OK) return r;
+  if (t && t->n) BF_CK(launch_shadow(p, *t, s));
+  return SQUINT_OK;
+}
+
 // pipe: the early forward of this update already ran (early_fwd); next: the following update's
 // inputs (its early forward is issued on this update's branch), NULL for the last update
 squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& hp, const squint_replay& R,
@@ -611,6 +664,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   // conv weight tiles: with the auxiliary branch they were written at the end of the previous
   // update's branch (or by the call prologue)
   const bool branch = comm == nullptr && c.aux != nullptr;
+  const bool dp_peer = comm && comm_mode(comm) == 1;
   if (!branch) BF_CK(launch_conv_tiles(crit + L.off(gC, "enc.conv1.w"), crit + L.off(gC, "enc.conv2.w"), C, wtiles, s));
   if (pipe) {
     // encoder, critic/target projections and online heads came from early_fwd (on the previous
@@ -965,7 +1019,14 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   }
   if (comm) {
     BF_CK(launch_row_sums(c.F(w.logp_cur), c.F(w.row_loss), B, extras, s));
-    if (comm_allreduce_sum(comm, gc, L.gsize[gC] + kExtra, s) != 0) return set_error(SQUINT_ENCCL, comm_error());
+    if (dp_peer) {
+      // the gradients stay where they are: every rank's Adam slice reads them from the peers
+      squint_status r = dp_barrier(comm, extras, c.F(w.dp_tail), kExtra, s);
+      if (r != SQUINT_OK) return r;
+      extras = c.F(w.dp_tail);
+    } else if (comm_allreduce_sum(comm, gc, L.gsize[gC] + kExtra, s) != 0) {
+      return set_error(SQUINT_ENCCL, comm_error());
+    }
   }
   // the critic Adam writes theta+ into the other critic shadow set (read by the actor pass below and by
   // the next update); theta's set stays intact for the branch
@@ -999,6 +1060,10 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
         squint_status r = early_fwd(c, w_in, hp, R, *next, st, par ^ 1, es, 74, c.aux->enc, c.aux->chn);
         if (r != SQUINT_OK) return r;
       }
+    } else if (dp_peer) {
+      squint_status r = dp_adam(comm, gc, st.critic, st.m_critic, st.v_critic, L.gsize[gC], hp.lr_critic, hp,
+                                scal + S_C1_CRITIC, scal + S_C2_CRITIC, c.F(w.adam_part), &shC, 1, s);
+      if (r != SQUINT_OK) return r;
     } else {
       BF_CK(launch_adam_shadow(st.critic, gc, st.m_critic, st.v_critic, L.gsize[gC], hp.lr_critic, hp.beta1,
                                hp.beta2, hp.adam_eps, scal + S_C1_CRITIC, scal + S_C2_CRITIC, c.F(w.adam_part), &shC,
@@ -1155,11 +1220,23 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   if (comm) {
     float* ax = ga + L.gsize[gA];
     BF_CK(launch_lpi_sums(c.F(w.row_lpi), c.F(w.row_q), B, ax, s));
-    if (comm_allreduce_sum(comm, ga, L.gsize[gA] + kExtra, s) != 0) return set_error(SQUINT_ENCCL, comm_error());
-    lpis = ax;
+    if (dp_peer) {
+      squint_status r = dp_barrier(comm, ax, c.F(w.dp_tail) + kExtra, kExtra, s);
+      if (r != SQUINT_OK) return r;
+      lpis = c.F(w.dp_tail) + kExtra;
+    } else {
+      if (comm_allreduce_sum(comm, ga, L.gsize[gA] + kExtra, s) != 0) return set_error(SQUINT_ENCCL, comm_error());
+      lpis = ax;
+    }
   }
-  BF_CK(launch_adam_shadow(st.actor, ga, st.m_actor, st.v_actor, L.gsize[gA], hp.lr_actor, hp.beta1, hp.beta2,
-                           hp.adam_eps, scal + S_C1_ACTOR, scal + S_C2_ACTOR, nullptr, &shA, s, 0, kAdamBlocks, 1));
+  if (dp_peer) {
+    squint_status r = dp_adam(comm, ga, st.actor, st.m_actor, st.v_actor, L.gsize[gA], hp.lr_actor, hp,
+                              scal + S_C1_ACTOR, scal + S_C2_ACTOR, nullptr, &shA, 1, s);
+    if (r != SQUINT_OK) return r;
+  } else {
+    BF_CK(launch_adam_shadow(st.actor, ga, st.m_actor, st.v_actor, L.gsize[gA], hp.lr_actor, hp.beta1, hp.beta2,
+                             hp.adam_eps, scal + S_C1_ACTOR, scal + S_C2_ACTOR, nullptr, &shA, s, 0, kAdamBlocks, 1));
+  }
   // a14: Polyak over every critic tensor except the encoder (+ target shadow)
   if (!branch) BF_CK(launch_polyak_shadow(st.critic_target, st.critic + L.enc_end, L.gsize[gT], hp.tau, &shT, s));
   {
@@ -1169,7 +1246,7 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     if (branch) BF_CK(cudaStreamWaitEvent(es, c.aux->qdone, 0));
     MetricsArgs m;
     memset(&m, 0, sizeof(m));
-    m.npart = branch ? kAdamBlocks + kEncAdamBlocks : kAdamBlocks;
+    m.npart = branch ? kAdamBlocks + kEncAdamBlocks : dp_peer ? comm_nranks(comm) * kAdamBlocks : kAdamBlocks;
     m.B = B;
     m.inv_btotal = inv_btotal;
     m.row_lpi = c.F(w.row_lpi);

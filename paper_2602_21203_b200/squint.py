@@ -78,6 +78,7 @@ def _load():
         "squint_comm_unique_id": (st, [vp]),
         "squint_comm_init": (st, [C.POINTER(vp), vp, i32, i32]),
         "squint_comm_destroy": (st, [vp]),
+        "squint_comm_set_mode": (st, [vp, i32]),
         "squint_insert": (st, [vp, i64, i32, i32, i32, i32, vp, vp, i64, vp]),
         "squint_insert2": (st, [vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, i64, vp]),
         "squint_insert_ex": (st, [vp, i64, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp]),
@@ -108,7 +109,7 @@ def _load():
 LIB = _load()
 EXPORTED = ["squint_last_error", "squint_version", "squint_param_layout", "squint_workspace_bytes",
             "squint_workspace_region", "squint_act_workspace_bytes", "squint_comm_unique_id", "squint_comm_init",
-            "squint_comm_destroy", "squint_insert", "squint_insert2", "squint_insert_ex", "squint_act", "squint_act_ex", "squint_update", "squint_soft_update", "squint_stage_pinned",
+            "squint_comm_destroy", "squint_comm_set_mode", "squint_insert", "squint_insert2", "squint_insert_ex", "squint_act", "squint_act_ex", "squint_update", "squint_soft_update", "squint_stage_pinned",
             "squint_launch_count", "squint_set_phase_events", "squint_phase_name", "squint_selftest_gemm",
             "squint_set_launch_events", "squint_record_launch_event", "squint_launch_info",
             "squint_set_option"]
@@ -357,6 +358,11 @@ def comm_init(uid: bytes, rank: int, nranks: int):
     buf = C.create_string_buffer(uid, 128)
     _check(LIB.squint_comm_init(C.byref(h), buf, rank, nranks))
     return h
+
+
+def comm_set_mode(h, mode: int):
+    """0: ncclAllReduce + replicated Adam; 1: peer-memory all-reduce fused with a sharded Adam (f1)."""
+    _check(LIB.squint_comm_set_mode(h, int(mode)))
 
 
 def comm_destroy(h):

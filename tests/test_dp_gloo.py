@@ -42,14 +42,46 @@ def _adam_group(params, grads, m, v, t, lr, hp):
         params[k], m[k], v[k] = O.adam_step(params[k], grads[k], m[k], v[k], t, lr, hp.beta1, hp.beta2, hp.adam_eps)
 
 
+def _shard(n, rank, world):
+    """libsquint's slice of a flat group for comm mode 1 (update_bf16.cu dp_adam): float4 units,
+    [n4 * rank / G, n4 * (rank + 1) / G), the group size a multiple of 4 there; here the flat
+    oracle group may have a ragged tail, which the last rank owns."""
+    n4 = n // 4
+    lo, hi = 4 * (n4 * rank // world), 4 * (n4 * (rank + 1) // world)
+    return lo, (n if rank == world - 1 else hi)
+
+
+def _sharded_adam_group(params, grads_local, m, v, t, lr, hp):
+    """f1 (comm mode 1): this rank's slice of the SUM of every rank's gradient through Adam, the
+    stepped slice written into every rank's parameters (here: a SUM all-reduce of a buffer that
+    holds only this rank's slice, so each element comes from exactly one owner); m and v are
+    touched on the slice only."""
+    keys = sorted(params)
+    world, rank = dist.get_world_size(), dist.get_rank()
+    g = _allreduce(_flat(grads_local, keys))  # the peers' gradients, summed for the slice
+    p, mf, vf = _flat(params, keys), _flat(m, keys), _flat(v, keys)
+    lo, hi = _shard(p.size, rank, world)
+    out = np.zeros_like(p)
+    out[lo:hi], mf[lo:hi], vf[lo:hi] = O.adam_step(p[lo:hi], g[lo:hi], mf[lo:hi], vf[lo:hi], t, lr, hp.beta1,
+                                                   hp.beta2, hp.adam_eps)
+    p = _allreduce(out)
+    for k, val in _unflat(p, params, keys).items():
+        params[k] = val
+    for k, val in _unflat(mf, m, keys).items():
+        m[k] = val
+    for k, val in _unflat(vf, v, keys).items():
+        v[k] = val
+
+
 def _allreduce(v):
     t = torch.from_numpy(np.ascontiguousarray(v))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return t.numpy()
 
 
-def dp_update_one(d, hp, R, idx, shift, eps, st, b_global):
-    """One update of this rank's shard (rows idx) with libsquint's DP exchange."""
+def dp_update_one(d, hp, R, idx, shift, eps, st, b_global, sharded=False):
+    """One update of this rank's shard (rows idx) with libsquint's DP exchange (sharded: comm
+    mode 1, the row-sum tails summed in the barrier, Adam on this rank's slice)."""
     p = d.pad
     Ob = O.shift_images(R["obs"][idx], shift[:, 0], shift[:, 1], p)
     On = O.shift_images(R["next_obs"][idx], shift[:, 2], shift[:, 3], p)
@@ -66,11 +98,16 @@ def dp_update_one(d, hp, R, idx, shift, eps, st, b_global):
     # pre-step phi on sg(h): the current-state sample does not depend on the critic step (Q18)
     at, logp, caches = O.actor_forward(d, hp, st["actor"], h, s, eps[1])
     ck = sorted(gc)
-    buf = _allreduce(np.concatenate([_flat(gc, ck), [logp.sum(), LQ]]))
-    gc = _unflat(buf, gc, ck)
-    sum_logp = buf[-2]
-    st["step"][0] += 1
-    _adam_group(st["critic"], gc, st["m"]["critic"], st["v"]["critic"], st["step"][0], hp.lr_critic, hp)
+    if sharded:
+        sum_logp = _allreduce(np.array([logp.sum(), LQ]))[0]
+        st["step"][0] += 1
+        _sharded_adam_group(st["critic"], gc, st["m"]["critic"], st["v"]["critic"], st["step"][0], hp.lr_critic, hp)
+    else:
+        buf = _allreduce(np.concatenate([_flat(gc, ck), [logp.sum(), LQ]]))
+        gc = _unflat(buf, gc, ck)
+        sum_logp = buf[-2]
+        st["step"][0] += 1
+        _adam_group(st["critic"], gc, st["m"]["critic"], st["v"]["critic"], st["step"][0], hp.lr_critic, hp)
     La, ga = O.alpha_loss_and_grad(hp, st["log_alpha"], sum_logp / b_global)
     st["step"][2] += 1
     la, ma, va = O.adam_step(np.array([st["log_alpha"]]), np.array([ga]), np.array([st["m"]["alpha"]]),
@@ -80,10 +117,13 @@ def dp_update_one(d, hp, R, idx, shift, eps, st, b_global):
     alpha1 = math.exp(st["log_alpha"])
     Lpi, gpi, qmean = O.actor_loss_and_grads(d, hp, st["critic"], st["actor"], h, s, at, logp, caches, alpha1, scale)
     ak = sorted(gpi)
-    buf = _allreduce(np.concatenate([_flat(gpi, ak), [Lpi, qmean.sum()]]))
-    gpi = _unflat(buf, gpi, ak)
     st["step"][1] += 1
-    _adam_group(st["actor"], gpi, st["m"]["actor"], st["v"]["actor"], st["step"][1], hp.lr_actor, hp)
+    if sharded:
+        _sharded_adam_group(st["actor"], gpi, st["m"]["actor"], st["v"]["actor"], st["step"][1], hp.lr_actor, hp)
+    else:
+        buf = _allreduce(np.concatenate([_flat(gpi, ak), [Lpi, qmean.sum()]]))
+        gpi = _unflat(buf, gpi, ak)
+        _adam_group(st["actor"], gpi, st["m"]["actor"], st["v"]["actor"], st["step"][1], hp.lr_actor, hp)
     for k in st["target"]:
         st["target"][k] = O.polyak(st["target"][k], st["critic"][k], hp.tau)
     return st
@@ -125,13 +165,23 @@ def _state_vec(st):
     return np.concatenate(parts)
 
 
-def _worker(rank, port, b_local, utd, out_dir, kind=0, mode=0):
+def _worker(rank, port, b_local, utd, out_dir, kind=0, mode=0, sharded=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     d, h, dims, R, st, idx, sh, eps = _problem(b_local, utd, kind, mode)
     for j in range(utd):
-        st = dp_update_one(d, h, R, idx[rank][j], sh[rank][j], eps[rank][j], st, b_local * WORLD)
+        st = dp_update_one(d, h, R, idx[rank][j], sh[rank][j], eps[rank][j], st, b_local * WORLD, sharded)
+    if sharded:
+        # m, v: every rank holds only its own slice; assemble the owners' slices
+        for g in ("critic", "actor"):
+            keys = sorted(st["m"][g])
+            for mv in ("m", "v"):
+                f = _flat(st[mv][g], keys)
+                lo, hi = _shard(f.size, rank, WORLD)
+                own = np.zeros_like(f)
+                own[lo:hi] = f[lo:hi]
+                st[mv][g] = _unflat(_allreduce(own), st[mv][g], keys)
     np.save(os.path.join(out_dir, f"state{rank}.npy"), _state_vec(st))
     dist.barrier()
     dist.destroy_process_group()
@@ -162,3 +212,33 @@ def test_dp_gloo_world2_matches_global_batch(tmp_path, b_local, utd, kind, mode)
     r = _state_vec(ref)
     err = np.abs(s0 - r).max() / np.abs(r).max()
     assert err < 1e-10, err
+
+
+@pytest.mark.parametrize("b_local,utd", [(3, 1), (4, 2)])
+def test_dp_gloo_world2_sharded_adam_matches_global_batch(tmp_path, b_local, utd):
+    """f1 (comm mode 1): all-reduce fused with a sharded Adam -- each rank steps only its slice of
+    the summed gradient and writes it to every rank -- leaves the ranks' parameters bit-identical
+    and equal (with the owners' m, v slices) to the single-process update on the global batch."""
+    mp.spawn(_worker, args=(_free_port(), b_local, utd, str(tmp_path), 0, 0, True), nprocs=WORLD, join=True)
+    s0 = np.load(tmp_path / "state0.npy")
+    s1 = np.load(tmp_path / "state1.npy")
+    assert np.array_equal(s0, s1), "sharded data-parallel replicas diverged"
+    d, h, dims, R, st, idx, sh, eps = _problem(b_local, utd)
+    dg = O.Dims(**dict(dims, batch=b_local * WORLD))
+    ref, _ = O.update(dg, h, R, np.concatenate(idx, axis=1), np.concatenate(sh, axis=1),
+                      np.concatenate(eps, axis=2), copy.deepcopy(st))
+    r = _state_vec(ref)
+    err = np.abs(s0 - r).max() / np.abs(r).max()
+    assert err < 1e-10, err
+
+
+def test_shard_ranges_tile_the_group():
+    """The slices of comm mode 1 are disjoint, float4-aligned and cover the group for G = 1..8."""
+    for n in (4, 8, 12, 4 * 37, 4 * 1000 + 4, 4 * 148 * 3):
+        for world in range(1, 9):
+            covered = np.zeros(n, np.int64)
+            for rank in range(world):
+                lo, hi = _shard(n, rank, world)
+                assert lo % 4 == 0 and hi % 4 == 0 and lo <= hi
+                covered[lo:hi] += 1
+            assert (covered == 1).all(), (n, world)

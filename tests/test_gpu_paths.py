@@ -64,6 +64,46 @@ def test_update_one_rank_comm(comm1, cfg, prec, over):
             compare(f"comm vs local {grp} {n}", a[n], b[n], 1e-4)
 
 
+@pytest.fixture(scope="module")
+def comm1_peer():
+    h = P.squint.comm_init(P.squint.comm_unique_id(), 0, 1)
+    P.squint.comm_set_mode(h, 1)
+    yield h
+    P.squint.comm_destroy(h)
+
+
+@pytest.mark.parametrize("cfg,over,oracle", [
+    ("c2", dict(utd=2, capacity=4096), True),
+    ("c3", dict(utd=1, capacity=4096, batch=512), True),
+    ("c2", dict(utd=3, capacity=4096, batch=37), False),
+])
+def test_update_one_rank_peer_mode(comm1, comm1_peer, cfg, over, oracle):
+    """f1 (comm mode 1: peer-memory all-reduce fused with a sharded Adam) at G = 1: the slice is the
+    whole group, the barrier passes on the rank's own counters, the tails are copied.  Bit for bit
+    against mode 0 (ncclAllReduce + replicated Adam) on the same inputs -- same gradient sums, same
+    Adam arithmetic, same per-block sum(g^2) partials -- over several updates (the barrier epochs
+    advance in device memory), and against the oracle at the bf16 bars (the a15 cases of
+    test_update_one_rank_comm)."""
+    over = dict(over)
+    utd = over.pop("utd")
+    pr = Problem(cfg, utd=utd, seed=21, **over)
+    L = pr.gpu_setup(precision=P.BF16)
+    L.comm = comm1_peer
+    met = pr.gpu_update(L)
+    L0 = pr.gpu_setup(precision=P.BF16)
+    L0.comm = comm1
+    met0 = pr.gpu_update(L0)
+    assert np.array_equal(np.asarray(met), np.asarray(met0)), "metrics differ between comm modes"
+    for grp in ("critic", "actor", "target"):
+        a, b = group_values(L, grp), group_values(L0, grp)
+        for n in a:
+            assert np.array_equal(a[n], b[n]), f"mode 1 vs mode 0: {grp} {n}"
+    if oracle:
+        trace = []
+        st_ref, met_ref = pr.oracle_update(trace)
+        _check_update_bf16(pr, L, met, st_ref, met_ref, trace)
+
+
 # ---- a3-a4: gather + random shift, bit-exact ----------------------------------------------------
 @pytest.mark.parametrize("cfg,utd,batch", [("c2", 2, 512), ("c2", 1, 37), ("c3", 1, 4096)])
 def test_gather_shift_bit_exact_bf16(cfg, utd, batch):
