@@ -213,6 +213,10 @@ def run_gpu(args):
         t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
         dist.broadcast(t, 0)
         L.comm = S.comm_init(bytes(t.cpu().tolist()), rank, world)
+        if args.comm_mode == 1 and precision == P.BF16:
+            # f1: peer-memory all-reduce fused with a sharded Adam (the warm step before the graph
+            # capture maps the peers' buffers)
+            S.comm_set_mode(L.comm, 1)
 
     # replay ring (replica per rank, data seed 0): device-side seeded fill, same distributions as c0
     g = torch.Generator(device=dev)
@@ -545,6 +549,8 @@ def run_gpu(args):
                                    + (" (act squints its own frames)" if args.act_full else "") + vlabel,
                        "global_batch": gbatch, "batch_per_rank": B, "utd": UTD,
                        "n_env": N_ENV, "parallelism": f"dp{world}", "capacity": cap,
+                       "grad_exchange": ("peer-sharded-adam" if args.comm_mode == 1 and args.precision == "bf16"
+                                         else "nccl-allreduce") if world > 1 else "none",
                        "l2": f"ring {cap * 1662 / 1e9:.2f} GB + rotating frame pools (4 x {n_env * 49152 / 1e6:.0f} MB) > L2",
                        "graph": use_graph},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
@@ -756,6 +762,8 @@ def main():
     ap.add_argument("--target", default="avg", choices=["avg", "cdq"])
     ap.add_argument("--insert", default="chw", choices=["chw", "hwc", "jitter", "hwc-jitter"])
     ap.add_argument("--config", default=CFG, choices=["c2", "c3"])  # c3: the DP shapes on one GPU (B 4096)
+    # N > 1: 0 = ncclAllReduce + replicated Adam, 1 = peer-memory all-reduce fused with a sharded Adam (f1)
+    ap.add_argument("--comm-mode", type=int, default=0, choices=[0, 1])
     ap.add_argument("--capacity", type=int, default=0)  # replay rows (0: configs' 1M; f3: 100K axis)
     args = ap.parse_args()
     if args.act_full and args.insert != "chw":
