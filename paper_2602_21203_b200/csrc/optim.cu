@@ -12,16 +12,39 @@ namespace sq {
 
 namespace {
 
+// Per-thread partial sums of two row vectors over i = tid, tid + blockDim, ... in that order; the
+// loads of four strides are issued before their adds (the loop was one dependent L2 round trip per
+// stride: ~10 us for B = 4096 on one block).
+__device__ __forceinline__ void row_sums2(const float* __restrict__ ra, const float* __restrict__ rb, int B, float& a,
+                                          float& b) {
+  const int st = blockDim.x;
+  int i = threadIdx.x;
+  for (; i + 3 * st < B; i += 4 * st) {
+    float va[4], vb[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      va[k] = ra[i + k * st];
+      vb[k] = rb[i + k * st];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a += va[k];
+      b += vb[k];
+    }
+  }
+  for (; i < B; i += st) {
+    a += ra[i];
+    b += rb[i];
+  }
+}
+
 __global__ void __launch_bounds__(256) k_row_sums(const float* __restrict__ logp, const float* __restrict__ row_loss,
                                                   int B, float* __restrict__ extras) {
   grid_wait();
   grid_trigger();
   __shared__ float red[32];
   float a = 0.f, b = 0.f;
-  for (int i = threadIdx.x; i < B; i += blockDim.x) {
-    a += logp[i];
-    b += row_loss[i];
-  }
+  row_sums2(logp, row_loss, B, a, b);
   a = block_sum(a, red);
   b = block_sum(b, red);
   if (threadIdx.x == 0) {
@@ -145,10 +168,7 @@ __global__ void __launch_bounds__(256) k_lpi_sums(const float* __restrict__ row_
   grid_trigger();
   __shared__ float red[32];
   float a = 0.f, b = 0.f;
-  for (int i = threadIdx.x; i < B; i += blockDim.x) {
-    a += row_lpi[i];
-    b += row_q[i];
-  }
+  row_sums2(row_lpi, row_q, B, a, b);
   a = block_sum(a, red);
   b = block_sum(b, red);
   if (threadIdx.x == 0) {
@@ -212,7 +232,8 @@ __device__ __forceinline__ int shadow_slot(const ShadowTable& t, int i) {
 // The shadow slots of flat indices i .. i + 3 (i % 4 == 0) after an optimizer step: one entry
 // search per float4; the four values go out as one 8-byte store when they sit in one row of a
 // plain entry (every entry with cols % 4 == 0), else element by element.
-__device__ __forceinline__ void shadow_store4(const ShadowTable& t, int i, const float* f) {
+// (base: this table's shadow buffer, or another rank's copy of it -- same layout)
+__device__ __forceinline__ void shadow_store4(const ShadowTable& t, __nv_bfloat16* base, int i, const float* f) {
   for (int k = 0; k < t.n; ++k) {
     const ShadowEnt& e = t.e[k];
     const int l = i - (int)e.src;
@@ -223,7 +244,7 @@ __device__ __forceinline__ void shadow_store4(const ShadowTable& t, int i, const
         uint2 w;
         w.x = *reinterpret_cast<const uint32_t*>(&lo);
         w.y = *reinterpret_cast<const uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(t.base + e.dst + (int64_t)row * e.ld + col) = w;
+        *reinterpret_cast<uint2*>(base + e.dst + (int64_t)row * e.ld + col) = w;
         return;
       }
       break;
@@ -232,8 +253,11 @@ __device__ __forceinline__ void shadow_store4(const ShadowTable& t, int i, const
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int sl = shadow_slot(t, i + k);
-    if (sl >= 0) t.base[sl] = __float2bfloat16_rn(f[k]);
+    if (sl >= 0) base[sl] = __float2bfloat16_rn(f[k]);
   }
+}
+__device__ __forceinline__ void shadow_store4(const ShadowTable& t, int i, const float* f) {
+  shadow_store4(t, t.base, i, f);
 }
 
 // One group's shadow refresh.  Work unit = (row, 128-column segment) of an entry, one warp per
@@ -516,25 +540,41 @@ int launch_lpi_sums(const float* row_lpi, const float* row_q, int B, float* out2
 // scope, over NVLink), then waits until every peer's arrival count in its own counters reaches its
 // epoch + 1 (acquire).  One block; the next kernel on the stream starts after it completes.
 namespace {
-__device__ __forceinline__ void red_release_sys(unsigned* p, unsigned v) {
-  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void red_relaxed_sys(unsigned* p, unsigned v) {
+  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
   unsigned v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
-__global__ void __launch_bounds__(64) k_dp_sync(const __grid_constant__ DpSync a) {
+__global__ void __launch_bounds__(256) k_dp_sync(const __grid_constant__ DpSync a) {
   grid_wait();
   grid_trigger();
+  __shared__ float red[32];
+  if (a.ra) {
+    // this rank's row sums into its own tail (k_row_sums / k_lpi_sums, same block and order)
+    float x = 0.f, y = 0.f;
+    row_sums2(a.ra, a.rb, a.B, x, y);
+    x = block_sum(x, red);
+    y = block_sum(y, red);
+    if (threadIdx.x == 0) {
+      a.tail_mine[0] = x;
+      a.tail_mine[1] = y;
+    }
+  }
   if (threadIdx.x == 0) {
     const unsigned e = a.own[kDpMaxRanks] + 1;
-    __threadfence_system();  // this rank's earlier writes (its gradients, its peer stores) first
-    for (int q = 0; q < a.G; ++q) red_release_sys(a.flag[q] + a.rank, 1u);
+    // one release fence orders everything this rank wrote before (its gradients and tail, its
+    // stores into the peers) ahead of the arrival counts; one acquire fence after the spin
+    fence_acq_rel_sys();
+    for (int q = 0; q < a.G; ++q) red_relaxed_sys(a.flag[q] + a.rank, 1u);
     for (int q = 0; q < a.G; ++q)
-      while (ld_acquire_sys(a.own + q) < e) {
+      while (ld_relaxed_sys(a.own + q) < e) {
       }
+    fence_acq_rel_sys();
     a.own[kDpMaxRanks] = e;
   }
   __syncthreads();
@@ -548,7 +588,8 @@ __global__ void __launch_bounds__(64) k_dp_sync(const __grid_constant__ DpSync a
 
 // This rank's slice [lo4, hi4) (float4 units) of one parameter group: g = sum over ranks (rank
 // order, read from the peers' gradient buffers over NVLink), Adam (the arithmetic of k_adam_sh),
-// the stepped parameters stored into every rank's copy, sum(g^2) per block into every rank's
+// the stepped parameters (and their bf16 shadow entries) stored into every rank's copy, sum(g^2)
+// per block into every rank's
 // partial buffer at [rank * gridDim.x + block].  m and v: this rank's slice only is ever touched.
 __global__ void __launch_bounds__(256) k_dp_adam(const __grid_constant__ DpAdam d, float4* __restrict__ m,
                                                  float4* __restrict__ v, float lr, float b1, float b2, float eps,
@@ -607,6 +648,8 @@ __global__ void __launch_bounds__(256) k_dp_adam(const __grid_constant__ DpAdam 
     m[i] = mm;
     v[i] = vv;
     for (int q = 0; q < d.G; ++q) reinterpret_cast<float4*>(d.p[q])[i] = pp;
+    if (t.n)
+      for (int q = 0; q < d.G; ++q) shadow_store4(t, d.sh[q], (int)(4 * i), pf);
   }
   ss = block_sum(ss, red);
   if (threadIdx.x == 0 && d.part[0])
@@ -616,7 +659,7 @@ __global__ void __launch_bounds__(256) k_dp_adam(const __grid_constant__ DpAdam 
 
 int launch_dp_sync(const DpSync& a, cudaStream_t s) {
   note_launch(s, "k_dp_sync", 0, 0);
-  launch_pdl(k_dp_sync, dim3(1), dim3(64), 0, s, a);
+  launch_pdl(k_dp_sync, dim3(1), dim3(256), 0, s, a);
   return (int)cudaGetLastError();
 }
 
@@ -624,7 +667,7 @@ int launch_dp_adam(const DpAdam& d, float* m, float* v, float lr, float b1, floa
                    const float* c2, const ShadowTable* t, int grad_perm, cudaStream_t s) {
   ShadowTable none;
   memset(&none, 0, sizeof(none));
-  note_launch(s, "k_dp_adam", 0, (16.0 + 8.0 * d.G) * 4.0 * (double)(d.hi4 - d.lo4));
+  note_launch(s, "k_dp_adam", 0, (16.0 + 10.0 * d.G) * 4.0 * (double)(d.hi4 - d.lo4));
   launch_pdl(k_dp_adam, dim3(kAdamBlocks), dim3(256), 0, s, d, reinterpret_cast<float4*>(m),
              reinterpret_cast<float4*>(v), lr, b1, b2, eps, c1, c2, t ? *t : none, grad_perm);
   return (int)cudaGetLastError();

@@ -116,19 +116,27 @@ struct DpSync {
   const float* tail[kDpMaxRanks];  // every rank's row-sum tail (ntail floats), or unused
   float* tail_out;                 // [ntail] local: sum over ranks
   int ntail;
+  // optional (ra != NULL): first this rank's row sums, tail_mine[0] = sum ra[0..B), [1] = sum rb
+  const float* ra;
+  const float* rb;
+  int B;
+  float* tail_mine;
 };
-// cross-rank barrier (all ranks' earlier stream work done and visible), then the tail sum
+// [row sums into this rank's tail,] cross-rank barrier (all ranks' earlier stream work done and
+// visible), then the tail sum
 int launch_dp_sync(const DpSync& a, cudaStream_t s);
 struct DpAdam {
   const float* g[kDpMaxRanks];  // every rank's flat gradient of the group
   float* p[kDpMaxRanks];        // every rank's fp32 parameters of the group
   float* part[kDpMaxRanks];     // every rank's sum(g^2) partials [G * kAdamBlocks]
+  __nv_bfloat16* sh[kDpMaxRanks];  // every rank's copy of the group's shadow buffer (t->base)
   int G, rank;
   int64_t lo4, hi4;             // this rank's slice, float4 units
 };
 // Adam (as launch_adam_shadow without the shadow) on this rank's slice of the all-reduced gradient;
-// t: the group's shadow table, read only for the grad_perm gather.  Needs a launch_dp_sync after it
-// before any rank reads its parameters.
+// t: the group's shadow table (grad_perm gather; the stepped weights' bf16 entries are stored into
+// every rank's shadow buffer sh[q]).  Needs a launch_dp_sync after it before any rank reads its
+// parameters or shadows.
 int launch_dp_adam(const DpAdam& d, float* m, float* v, float lr, float b1, float b2, float eps, const float* c1,
                    const float* c2, const ShadowTable* t, int grad_perm, cudaStream_t s);
 

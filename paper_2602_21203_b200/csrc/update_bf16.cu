@@ -581,8 +581,10 @@ squint_status early_fwd(const Ctx& c, const BfLay& w_in, const squint_hparams& h
 }
 
 // ---- f1: peer-memory all-reduce fused with a sharded Adam (comm mode 1) --------------------------
-// Cross-rank barrier; with ntail > 0 also the sum over ranks of every rank's `tail` into `out`.
-squint_status dp_barrier(Comm* cm, const float* tail, float* out, int ntail, cudaStream_t s) {
+// Cross-rank barrier; with ntail > 0 also the sum over ranks of every rank's `tail` into `out`, and
+// with ra != NULL first this rank's row sums (as k_row_sums / k_lpi_sums) into tail[0..1].
+squint_status dp_barrier(Comm* cm, const float* tail, float* out, int ntail, cudaStream_t s,
+                         const float* ra = nullptr, const float* rb = nullptr, int B = 0) {
   static_assert(kDpMaxRanks == kMaxRanks, "rank bound");
   DpSync a;
   memset(&a, 0, sizeof(a));
@@ -597,13 +599,19 @@ squint_status dp_barrier(Comm* cm, const float* tail, float* out, int ntail, cud
     for (int q = 0; q < a.G; ++q) a.tail[q] = static_cast<const float*>(f[q]);
     a.tail_out = out;
     a.ntail = ntail;
+    if (ra) {
+      a.ra = ra;
+      a.rb = rb;
+      a.B = B;
+      a.tail_mine = const_cast<float*>(tail);
+    }
   }
   BF_CK(launch_dp_sync(a, s));
   return SQUINT_OK;
 }
 
 // One group's optimizer step in peer mode: this rank's 1/G slice of sum_ranks(g) through Adam,
-// stored into every rank's parameters; barrier; this rank's bf16 shadow of the whole group.
+// stored (fp32 and its bf16 shadow entries) into every rank's copies; barrier.
 squint_status dp_adam(Comm* cm, const float* g, float* p, float* m, float* v, int64_t n, float lr,
                       const squint_hparams& hp, const float* c1, const float* c2, float* part, const ShadowTable* t,
                       int grad_perm, cudaStream_t s) {
@@ -620,14 +628,15 @@ squint_status dp_adam(Comm* cm, const float* g, float* p, float* m, float* v, in
     if (comm_peer_ptrs(cm, part, f) != 0) return set_error(SQUINT_ENCCL, comm_error());
     for (int q = 0; q < d.G; ++q) d.part[q] = static_cast<float*>(f[q]);
   }
+  if (t && t->n) {
+    if (comm_peer_ptrs(cm, t->base, f) != 0) return set_error(SQUINT_ENCCL, comm_error());
+    for (int q = 0; q < d.G; ++q) d.sh[q] = static_cast<__nv_bfloat16*>(f[q]);
+  }
   const int64_t n4 = n / 4;
   d.lo4 = n4 * d.rank / d.G;
   d.hi4 = n4 * (d.rank + 1) / d.G;
   BF_CK(launch_dp_adam(d, m, v, lr, hp.beta1, hp.beta2, hp.adam_eps, c1, c2, t, grad_perm, s));
-  squint_status r = dp_barrier(cm, nullptr, nullptr, 0, s);
-  if (r != SQUINT_OK) return r;
-  if (t && t->n) BF_CK(launch_shadow(p, *t, s));
-  return SQUINT_OK;
+  return dp_barrier(cm, nullptr, nullptr, 0, s);
 }
 
 // pipe: the early forward of this update already ran (early_fwd); next: the following update's
@@ -1018,14 +1027,14 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
     BF_CK(dw_launch(gb, c.F(w.dwsplit), w.dwsplit.n, s));
   }
   if (comm) {
-    BF_CK(launch_row_sums(c.F(w.logp_cur), c.F(w.row_loss), B, extras, s));
     if (dp_peer) {
       // the gradients stay where they are: every rank's Adam slice reads them from the peers
-      squint_status r = dp_barrier(comm, extras, c.F(w.dp_tail), kExtra, s);
+      squint_status r = dp_barrier(comm, extras, c.F(w.dp_tail), kExtra, s, c.F(w.logp_cur), c.F(w.row_loss), B);
       if (r != SQUINT_OK) return r;
       extras = c.F(w.dp_tail);
-    } else if (comm_allreduce_sum(comm, gc, L.gsize[gC] + kExtra, s) != 0) {
-      return set_error(SQUINT_ENCCL, comm_error());
+    } else {
+      BF_CK(launch_row_sums(c.F(w.logp_cur), c.F(w.row_loss), B, extras, s));
+      if (comm_allreduce_sum(comm, gc, L.gsize[gC] + kExtra, s) != 0) return set_error(SQUINT_ENCCL, comm_error());
     }
   }
   // the critic Adam writes theta+ into the other critic shadow set (read by the actor pass below and by
@@ -1219,12 +1228,12 @@ squint_status update_one(const Ctx& c, const BfLay& w_in, const squint_hparams& 
   PhaseScope ps15(15, rep, s);
   if (comm) {
     float* ax = ga + L.gsize[gA];
-    BF_CK(launch_lpi_sums(c.F(w.row_lpi), c.F(w.row_q), B, ax, s));
     if (dp_peer) {
-      squint_status r = dp_barrier(comm, ax, c.F(w.dp_tail) + kExtra, kExtra, s);
+      squint_status r = dp_barrier(comm, ax, c.F(w.dp_tail) + kExtra, kExtra, s, c.F(w.row_lpi), c.F(w.row_q), B);
       if (r != SQUINT_OK) return r;
       lpis = c.F(w.dp_tail) + kExtra;
     } else {
+      BF_CK(launch_lpi_sums(c.F(w.row_lpi), c.F(w.row_q), B, ax, s));
       if (comm_allreduce_sum(comm, ga, L.gsize[gA] + kExtra, s) != 0) return set_error(SQUINT_ENCCL, comm_error());
       lpis = ax;
     }
